@@ -1,0 +1,131 @@
+/* rm.h -- C ABI of the B200-native multigrid relaxation sweep of arXiv 2211.14284
+ * ("Optimal-complexity and robust multigrid relaxation for the de Rham Riesz maps").
+ *
+ * The operation (§3-§4):
+ *   problems  beta u - div(alpha grad u) = f            (k = 0, H(grad))   eq:hgrad
+ *             beta u + curl(alpha curl u) = f           (k = 1, H(curl))   eq:hcurl
+ *             beta u - grad(alpha div u) = f            (k = 2, H(div))    eq:hdiv
+ *   weak form a^k(v,u) = (v, beta u) + (d^k v, alpha d^k u)   eq:common_weak_formulation
+ *   spaces    Q_p / NCE_p / NCF_p with the FDM basis on a logically structured hex mesh;
+ *             DoFs are reference values.
+ *   sweep     r = f - A u  (true A, sum-factorised, eq:sum-factorization P:690-692)
+ *             u_out = u_in + omega * sum_i R_i^T A_i^{-1} R_i r          eq:asm-afw
+ *             [+ omega * D (sum_j R_j^T B_j^{-1} R_j) D^T r  for the PH decomposition, eq:asm-hiptmair]
+ *             with star patches and exact Cholesky or, on non-Cartesian
+ *             cells, the auxiliary operator (eq:sum-factorization_approx P:732-739) with ICC on the
+ *             static-condensation pattern.  No p=1 coarse term (reading G10).
+ *
+ * VECTOR LAYOUT (reading G16): component-major; each component a C-order
+ * [Z][Y][X] array (X fastest).  Per direction d a component uses a P family (n_d p + 1 entries,
+ * shared at multiples of p) or a DP family (n_d p entries):
+ *   Q_p (P,P,P);  NCE_p x:(DP,P,P) y:(P,DP,P) z:(P,P,DP);  NCF_p x:(P,DP,DP) y:(DP,P,DP) z:(DP,DP,P).
+ * A DoF is CONSTRAINED iff one of its P-family indices lies on a Gamma_D plane.
+ * Inputs may hold anything in constrained entries (they are read as zero); outputs hold zero
+ * in constrained entries, except rm_relax, which leaves u_out = u_in there.
+ *
+ * MEMORY: every vector argument of rm_apply / rm_residual / rm_relax / rm_precondition / rm_pcg
+ * is an fp64 CUDA DEVICE pointer of n_local = rm_layout().n_local elements, owned by the caller
+ * (e.g. a torch tensor).  The context owns every device buffer it allocates; rm_destroy frees
+ * them.  Host-side arguments (coordinates, coefficients, masks, the *_host calls) are plain host
+ * pointers, copied during the call.  Work is enqueued on options.stream (cudaStream_t; NULL =
+ * the legacy default stream); rm_apply, rm_residual, rm_relax and rm_precondition are
+ * asynchronous; rm_pcg, rm_relax_host and the query calls synchronise.
+ *
+ * ERRORS: every call returns an rm_status; no C++ exception crosses the ABI.  rm_last_error()
+ * returns a thread-local message for the last failing call.  RM_NOT_CONVERGED from rm_pcg is a
+ * report (iters == maxit), not an error.  A handle must not be used from two host threads at once.
+ */
+#ifndef RM_H_
+#define RM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rm_ctx rm_ctx;
+
+typedef enum { RM_HGRAD = 0, RM_HCURL = 1, RM_HDIV = 2 } rm_space;   /* form degree k */
+
+typedef enum {
+  RM_OK = 0,
+  RM_NOT_CONVERGED = 1,
+  RM_EINVAL = -1,     /* bad sizes, p < 1 or p > 15, bad mask, unsupported combination */
+  RM_ENOMEM = -2,     /* host or device allocation failed */
+  RM_ENUMERIC = -3,   /* non-positive pivot in a patch factorization (message names the patch) */
+  RM_ECUDA = -4,      /* CUDA runtime error (message carries cudaGetErrorString) */
+  RM_ENCCL = -5       /* NCCL error (multi-GPU) */
+} rm_status;
+
+enum { RM_PAFW = 0, RM_PH = 1 };                       /* decomposition: vertex stars | k-stars + potential */
+enum { RM_CHOL = 0, RM_ICC_SC = 1 };                   /* patch factorization */
+enum { RM_ALL_ENTITIES = 0, RM_INTERIOR_ONLY = 1 };    /* patch_entities (interior-only = test mode) */
+
+/* Gamma_D bitmask: bit0 x=0, bit1 x=1, bit2 y=0, bit3 y=1, bit4 z=0, bit5 z=1 */
+typedef struct {
+  int32_t nx, ny, nz;        /* global cells per direction                                        */
+  const double *coords;      /* host, (nz+1)(ny+1)(nx+1)*3, C-order [z][y][x][xyz];                */
+                             /* NULL = uniform grid of the unit cube. Axis-aligned grids use the    */
+                             /* Cartesian Kronecker path; any other grid is treated as trilinear.  */
+  int32_t z_begin, z_end;    /* cell layers owned by this rank; [0, nz) on one GPU                 */
+} rm_mesh;
+
+typedef struct {
+  int32_t decomposition;     /* RM_PAFW | RM_PH (k = 0: identical)                                 */
+  int32_t factorization;     /* RM_CHOL | RM_ICC_SC                                                 */
+  int32_t patch_entities;    /* RM_ALL_ENTITIES | RM_INTERIOR_ONLY                                  */
+  double potential_shift;    /* eps_s for k = 2 PH (reading G8), default 1e-6                        */
+  int32_t coarse;            /* must be 0 (p = 1 coarse level not built, reading G10)              */
+  void *stream;              /* cudaStream_t                                                        */
+  const void *nccl_id;       /* 128-byte ncclUniqueId or NULL (single GPU)                          */
+  int32_t rank, nranks, device;
+} rm_options;
+
+typedef struct {
+  int64_t n_local;           /* DoFs in the local vectors (constrained included)                   */
+  int64_t n_free;            /* unconstrained DoFs (global)                                         */
+  int64_t n_patches, n_patches_potential;
+  int64_t n_factor_blocks;   /* distinct patch factors (identical patches share one)               */
+  int64_t factor_bytes;      /* bytes of patch-factor values read by one sweep (primary+potential) */
+  int64_t sweep_bytes;       /* algorithmic bytes of one sweep: factor values (per patch) + f,u,u_out */
+  int32_t n_colors, n_classes;
+  double icc_sigma_max;      /* largest ICC restart shift used (reading G7), 0 if none             */
+  double setup_seconds;
+} rm_info;
+
+void rm_default_options(rm_options *opt);
+
+/* Builds the 1D FDM tables, the structured layout, all patch factors and uploads them.
+ * alpha, beta: host arrays, n == 1 (constant) or one value per cell, C-order [z][y][x]. */
+rm_status rm_setup(rm_ctx **ctx, const rm_mesh *mesh, int32_t p, rm_space space,
+                   const double *alpha, int64_t n_alpha, const double *beta, int64_t n_beta,
+                   uint32_t gamma_d, const rm_options *opt);
+
+/* shape[m][0..2] = (Z, Y, X) extents of component m (zeros for absent components). */
+rm_status rm_layout(const rm_ctx *ctx, int64_t *n_local, int64_t *n_free, int32_t shape[3][3]);
+rm_status rm_info_get(const rm_ctx *ctx, rm_info *info);
+/* host mask[n_local]: 1 = constrained DoF. */
+rm_status rm_constrained_mask(const rm_ctx *ctx, uint8_t *mask);
+
+rm_status rm_apply(rm_ctx *ctx, const double *u, double *v);                 /* v = A u              */
+rm_status rm_residual(rm_ctx *ctx, const double *f, const double *u, double *r);   /* r = f - A u  */
+/* u_out = u_in + omega * P^{-1}(f - A u_in); u_out may alias u_in. */
+rm_status rm_relax(rm_ctx *ctx, const double *f, const double *u_in, double *u_out, double omega);
+/* z = P^{-1} r  (the additive Schwarz preconditioner = one sweep from zero with omega = 1). */
+rm_status rm_precondition(rm_ctx *ctx, const double *r, double *z);
+/* Same as rm_relax with HOST buffers: copies f, u_in to the device, sweeps, copies u_out back,
+ * synchronises. */
+rm_status rm_relax_host(rm_ctx *ctx, const double *f, const double *u_in, double *u_out, double omega);
+/* PCG on the true A with the sweep preconditioner from u = 0; stops at the first k with
+ * sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0). u: device, overwritten. */
+rm_status rm_pcg(rm_ctx *ctx, const double *f, double *u, double rtol, int32_t maxit,
+                 int32_t *iters, double *rel_natural_residual);
+
+void rm_destroy(rm_ctx *ctx);
+const char *rm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RM_H_ */

@@ -42,6 +42,7 @@ class Problem:
     factorization: str = "chol"      # "chol" | "icc_sc"
     interior_only: bool = False
     matfree: bool = False            # apply A cell by cell (large p) instead of via CSR
+    potential_shift: float = EPS_S   # eps_s of reading G8 (k = 2 PH)
     space: Space = field(init=False)
     constrained: np.ndarray = field(init=False)
     free: np.ndarray = field(init=False)
@@ -118,7 +119,7 @@ class Problem:
         B = D.T @ Af @ D
         if self.k == 2:
             M = assemble(pspace, self.X, np.zeros_like(self.alpha), self.beta)
-            B = B + EPS_S * M
+            B = B + self.potential_shift * M
         B = (Pf @ B @ Pf).tocsr()
         pats = all_patches(pspace, kp, pcon, self.interior_only)
         sol = []

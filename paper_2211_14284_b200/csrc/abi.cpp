@@ -1,0 +1,564 @@
+// C ABI (include/rm.h): context, setup (host factorization + upload), sweep orchestration.
+#include "../../include/rm.h"
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "basis.hpp"
+#include "kernels.cuh"
+#include "model.hpp"
+#include "patches.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RmError : std::runtime_error {
+  rm_status st;
+  RmError(rm_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw RmError(RM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevFamily {
+  std::vector<void*> allocs;
+  rm::DClass* d_classes = nullptr;
+  int* d_pclass = nullptr;
+  long long* d_pbase = nullptr;
+  long long* d_pvals = nullptr;
+  double* d_vals = nullptr;
+  std::vector<int> color_start;
+  size_t smem = 0;
+  int maxT = 1;
+  int64_t npatch = 0, nfactors = 0, nclasses = 0;
+  int64_t sweep_value_bytes = 0;   // sum over patches of value-block bytes
+  double sigma_max = 0.0;
+  bool present = false;
+
+  template <class T>
+  T* upload(const std::vector<T>& h) {
+    if (h.empty()) return nullptr;
+    void* d = nullptr;
+    if (cudaMalloc(&d, h.size() * sizeof(T)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed");
+    allocs.push_back(d);
+    CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return static_cast<T*>(d);
+  }
+  void release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+  }
+};
+
+rm::DSliced to_dev(DevFamily& F, const rm::Sliced& s) {
+  rm::DSliced d{};
+  d.r0 = s.r0; d.nrows = s.nrows; d.nslices = (int)s.slice_w.size();
+  d.sw = F.upload(s.slice_w);
+  d.soff = F.upload(s.slice_off);
+  d.cols = F.upload(s.cols);
+  d.vofs = s.vofs;
+  return d;
+}
+
+void upload_family(DevFamily& F, const rm::PatchFamily& P) {
+  const int NW = 8;
+  std::vector<rm::DClass> hc(P.classes.size());
+  size_t smem = 0;
+  int maxT = 1;
+  for (size_t c = 0; c < P.classes.size(); ++c) {
+    const rm::ClassProgram& C = P.classes[c];
+    rm::DClass& d = hc[c];
+    std::memset(&d, 0, sizeof d);
+    d.n = C.n; d.nlev = (int)C.lev.size(); d.m = C.m; d.final_kind = C.final_kind;
+    if (d.nlev > RM_MAXLEV) throw RmError(RM_EINVAL, "too many elimination levels");
+    d.offs = F.upload(C.offs);
+    std::vector<unsigned char> comp(C.comp.begin(), C.comp.end());
+    d.comp = F.upload(comp);
+    size_t auxn = 0;
+    for (int l = 0; l < d.nlev; ++l) {
+      d.lev[l].e0 = C.lev[l].e0; d.lev[l].e1 = C.lev[l].e1;
+      d.lev[l].blk.nblk = C.lev[l].blk.nblk;
+      d.lev[l].blk.bs = C.lev[l].blk.bs;
+      d.lev[l].blk.mem = F.upload(C.lev[l].blk.mem);
+      d.lev[l].blk.vofs = C.lev[l].blk.vofs;
+      d.lev[l].w = to_dev(F, C.lev[l].w);
+      d.lev[l].wt = to_dev(F, C.lev[l].wt);
+      auxn = std::max(auxn, (size_t)(C.lev[l].e1 - C.lev[l].e0));
+    }
+    d.vofs_final = C.vofs_final;
+    if (C.final_kind == rm::FINAL_DENSE_INV) {
+      auxn = std::max(auxn, (size_t)C.m * (NW + 1));
+      maxT = std::max(maxT, (C.m + 31) / 32);
+    } else {
+      d.icc_nlev = (int)C.icc_level_ptr.size() - 1;
+      d.icct_nlev = (int)C.icct_level_ptr.size() - 1;
+      d.icc_nnz = C.icc_rowptr.empty() ? 0 : C.icc_rowptr.back();
+      d.icc_rowptr = F.upload(C.icc_rowptr); d.icc_col = F.upload(C.icc_col);
+      d.icc_lptr = F.upload(C.icc_level_ptr); d.icc_lrows = F.upload(C.icc_level_rows);
+      d.icct_rowptr = F.upload(C.icct_rowptr); d.icct_col = F.upload(C.icct_col);
+      d.icct_lptr = F.upload(C.icct_level_ptr); d.icct_lrows = F.upload(C.icct_level_rows);
+    }
+    smem = std::max(smem, (C.n + auxn) * sizeof(double));
+  }
+  if (smem > 227 * 1024)
+    throw RmError(RM_EINVAL, "patch too large for the shared-memory patch kernel (" + std::to_string(smem) + " bytes)");
+  if (maxT > 32) throw RmError(RM_EINVAL, "final Schur block larger than 1024");
+  F.smem = smem; F.maxT = maxT;
+  F.d_classes = F.upload(hc);
+  // patches sorted by colour
+  const size_t np = P.pclass.size();
+  std::vector<size_t> order(np);
+  F.color_start.assign(P.ncolors + 1, 0);
+  for (size_t t = 0; t < np; ++t) F.color_start[P.pcolor[t] + 1]++;
+  for (int c = 0; c < P.ncolors; ++c) F.color_start[c + 1] += F.color_start[c];
+  std::vector<int> fill(F.color_start.begin(), F.color_start.end() - 1);
+  for (size_t t = 0; t < np; ++t) order[fill[P.pcolor[t]]++] = t;
+  std::vector<int> pc(np);
+  std::vector<long long> pb(3 * np), pv(np);
+  int64_t bytes = 0;
+  for (size_t i = 0; i < np; ++i) {
+    size_t t = order[i];
+    pc[i] = P.pclass[t];
+    for (int m = 0; m < 3; ++m) pb[3 * i + m] = P.pbase[3 * t + m];
+    pv[i] = P.pvals[t];
+    bytes += P.classes[P.pclass[t]].nvals * 8;
+  }
+  F.d_pclass = F.upload(pc);
+  F.d_pbase = F.upload(pb);
+  F.d_pvals = F.upload(pv);
+  F.d_vals = F.upload(P.values);
+  F.npatch = (int64_t)np;
+  F.nfactors = P.nfactors;
+  F.nclasses = (int64_t)P.classes.size();
+  F.sweep_value_bytes = bytes;
+  F.sigma_max = P.sigma_max;
+  F.present = true;
+}
+
+}  // namespace
+
+struct rm_ctx {
+  int k = 0, p = 1, n[3] = {1, 1, 1};
+  uint32_t gamma = 0;
+  int decomposition = RM_PAFW;
+  bool cartesian = true;
+  rm::Space sp, spot;
+  int64_t ndof = 0, npot = 0, nfree = 0;
+  cudaStream_t st = nullptr;
+  int device = 0;
+  rm::OpParams op{};
+  std::vector<void*> allocs;
+  double *d_alpha = nullptr, *d_beta = nullptr, *d_hpow = nullptr;
+  int coef_const = 0;
+  DevFamily prim, pot;
+  std::vector<double> Dh;   // p x (p+1)
+  double *d_r = nullptr, *d_t = nullptr, *d_s = nullptr;
+  double *d_z = nullptr, *d_pp = nullptr, *d_q = nullptr, *d_pr = nullptr;
+  double *d_sc = nullptr, *d_part = nullptr;
+  double *d_hf = nullptr, *d_hu = nullptr;
+  std::vector<uint8_t> mask;
+  double setup_seconds = 0.0;
+
+  double* dalloc(size_t n) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed");
+    allocs.push_back(d);
+    return static_cast<double*>(d);
+  }
+  ~rm_ctx() {
+    for (void* p : allocs) cudaFree(p);
+    prim.release();
+    pot.release();
+  }
+};
+
+namespace {
+
+rm::OpParams make_op(const rm::Space& sp, uint32_t gamma) {
+  rm::CellOperator co = rm::build_cell_operator(sp.k, sp.p);
+  rm::OpParams op;
+  std::memset(&op, 0, sizeof op);
+  op.k = sp.k; op.p = sp.p; op.ncomp = sp.ncomp;
+  for (int d = 0; d < 3; ++d) op.n[d] = sp.n[d];
+  for (int m = 0; m < 3; ++m)
+    for (int d = 0; d < 3; ++d) {
+      op.fam[m][d] = sp.fam[m][d];
+      op.len[m][d] = m < sp.ncomp ? sp.len(m, d) : 0;
+    }
+  for (int m = 0; m <= 3; ++m) op.off[m] = sp.offset(std::min(m, sp.ncomp));
+  op.gamma_d = gamma;
+  if ((int)co.terms.size() > RM_MAXTERMS || (int)co.mats.size() > RM_MAXMATS)
+    throw RmError(RM_EINVAL, "operator term table overflow");
+  op.nterms = (int)co.terms.size();
+  op.nmats = (int)co.mats.size();
+  for (int t = 0; t < op.nterms; ++t) {
+    const rm::Term& T = co.terms[t];
+    op.terms[t].mout = T.mout; op.terms[t].min = T.min; op.terms[t].coef = T.coef; op.terms[t].c = T.c;
+    for (int d = 0; d < 3; ++d) { op.terms[t].hexp[d] = T.hexp[d]; op.terms[t].mat[d] = T.mat[d]; }
+  }
+  for (int m = 0; m < op.nmats; ++m) {
+    const rm::Mat1& M = co.mats[m];
+    if (M.rows > RM_MAXP1) throw RmError(RM_EINVAL, "p too large");
+    int nz = 0;
+    for (int i = 0; i < M.rows; ++i) {
+      op.rowptr[m][i] = (short)nz;
+      for (int j = 0; j < M.cols; ++j)
+        if (M(i, j) != 0.0) {
+          if (nz >= RM_MAXMATNZ) throw RmError(RM_EINVAL, "1D matrix too dense");
+          op.col[m][nz] = (unsigned char)j; op.val[m][nz] = M(i, j); ++nz;
+        }
+    }
+    op.rowptr[m][M.rows] = (short)nz;
+  }
+  return op;
+}
+
+void check_cuda_status() { CK(cudaGetLastError()); }
+
+rm_status fail(const RmError& e) { g_err = e.what(); return e.st; }
+
+}  // namespace
+
+extern "C" {
+
+void rm_default_options(rm_options* o) {
+  std::memset(o, 0, sizeof *o);
+  o->decomposition = RM_PAFW;
+  o->factorization = RM_CHOL;
+  o->patch_entities = RM_ALL_ENTITIES;
+  o->potential_shift = 1e-6;
+  o->nranks = 1;
+}
+
+const char* rm_last_error(void) { return g_err.c_str(); }
+
+rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space, const double* alpha,
+                   int64_t n_alpha, const double* beta, int64_t n_beta, uint32_t gamma_d, const rm_options* opt) {
+  auto t0 = std::chrono::steady_clock::now();
+  try {
+    if (!out || !mesh || !alpha || !beta) throw RmError(RM_EINVAL, "null argument");
+    *out = nullptr;
+    rm_options o;
+    if (opt) o = *opt; else rm_default_options(&o);
+    if (p < 1 || p > 15) throw RmError(RM_EINVAL, "p must be in 1..15");
+    if (space < 0 || space > 2) throw RmError(RM_EINVAL, "space must be 0, 1 or 2");
+    if (mesh->nx < 1 || mesh->ny < 1 || mesh->nz < 1) throw RmError(RM_EINVAL, "mesh sizes must be >= 1");
+    if (gamma_d > 0x3F) throw RmError(RM_EINVAL, "gamma_d has bits above bit 5");
+    if (o.coarse != 0) throw RmError(RM_EINVAL, "coarse level not supported (reading G10)");
+    if (o.nranks > 1) throw RmError(RM_EINVAL, "multi-rank slabs not supported in this build");
+    if (o.decomposition != RM_PAFW && o.decomposition != RM_PH) throw RmError(RM_EINVAL, "bad decomposition");
+    if (o.factorization != RM_CHOL && o.factorization != RM_ICC_SC) throw RmError(RM_EINVAL, "bad factorization");
+    const int64_t ncell = (int64_t)mesh->nx * mesh->ny * mesh->nz;
+    if (!(n_alpha == 1 || n_alpha == ncell) || !(n_beta == 1 || n_beta == ncell))
+      throw RmError(RM_EINVAL, "alpha/beta must have 1 or ncells entries");
+    for (int64_t i = 0; i < n_alpha; ++i) if (!(alpha[i] > 0)) throw RmError(RM_EINVAL, "alpha must be > 0");
+    for (int64_t i = 0; i < n_beta; ++i) if (!(beta[i] >= 0)) throw RmError(RM_EINVAL, "beta must be >= 0");
+    CK(cudaSetDevice(o.device));
+    std::unique_ptr<rm_ctx> c(new rm_ctx);
+    c->k = space; c->p = p; c->n[0] = mesh->nx; c->n[1] = mesh->ny; c->n[2] = mesh->nz;
+    c->gamma = gamma_d; c->decomposition = (space == 0) ? RM_PAFW : o.decomposition;
+    c->st = static_cast<cudaStream_t>(o.stream);
+    c->device = o.device;
+    c->sp.init(space, p, mesh->nx, mesh->ny, mesh->nz);
+    c->ndof = c->sp.ndof();
+    // geometry: detect an axis-aligned grid
+    std::vector<double> h[3];
+    bool cart = true;
+    for (int d = 0; d < 3; ++d) h[d].assign(c->n[d], 1.0 / c->n[d]);
+    if (mesh->coords) {
+      const double* X = mesh->coords;
+      auto at = [&](int z, int y, int x, int i) { return X[(((int64_t)z * (c->n[1] + 1) + y) * (c->n[0] + 1) + x) * 3 + i]; };
+      for (int z = 0; z <= c->n[2] && cart; ++z)
+        for (int y = 0; y <= c->n[1] && cart; ++y)
+          for (int x = 0; x <= c->n[0] && cart; ++x) {
+            if (at(z, y, x, 0) != at(0, 0, x, 0) || at(z, y, x, 1) != at(0, y, 0, 1) || at(z, y, x, 2) != at(z, 0, 0, 2)) cart = false;
+          }
+      if (cart) {
+        for (int x = 0; x < c->n[0]; ++x) h[0][x] = at(0, 0, x + 1, 0) - at(0, 0, x, 0);
+        for (int y = 0; y < c->n[1]; ++y) h[1][y] = at(0, y + 1, 0, 1) - at(0, y, 0, 1);
+        for (int z = 0; z < c->n[2]; ++z) h[2][z] = at(z + 1, 0, 0, 2) - at(z, 0, 0, 2);
+        for (int d = 0; d < 3; ++d)
+          for (double v : h[d]) if (!(v > 0)) throw RmError(RM_EINVAL, "non-positive cell size");
+      }
+    }
+    c->cartesian = cart;
+    if (!cart) throw RmError(RM_EINVAL, "trilinear (non-axis-aligned) meshes: apply kernel not available in this build");
+    // ---- device operator
+    c->op = make_op(c->sp, gamma_d);
+    c->coef_const = (n_alpha == 1 && n_beta == 1);
+    {
+      std::vector<double> hp;
+      for (int d = 0; d < 3; ++d)
+        for (int e = -3; e <= 3; ++e)
+          for (int i = 0; i < c->n[d]; ++i) hp.push_back(std::pow(h[d][i], e));
+      c->d_hpow = c->dalloc(hp.size());
+      CK(cudaMemcpy(c->d_hpow, hp.data(), hp.size() * 8, cudaMemcpyHostToDevice));
+      std::vector<double> a(alpha, alpha + n_alpha), b(beta, beta + n_beta);
+      if (!c->coef_const) {   // expand to per-cell
+        if (n_alpha == 1) a.assign(ncell, alpha[0]);
+        if (n_beta == 1) b.assign(ncell, beta[0]);
+      }
+      c->d_alpha = c->dalloc(a.size()); c->d_beta = c->dalloc(b.size());
+      CK(cudaMemcpy(c->d_alpha, a.data(), a.size() * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(c->d_beta, b.data(), b.size() * 8, cudaMemcpyHostToDevice));
+    }
+    // constrained mask / free count
+    c->mask.assign(c->ndof, 0);
+    {
+      int64_t nf = 0;
+      for (int m = 0; m < c->sp.ncomp; ++m)
+        for (int64_t z = 0; z < c->sp.len(m, 2); ++z)
+          for (int64_t y = 0; y < c->sp.len(m, 1); ++y)
+            for (int64_t x = 0; x < c->sp.len(m, 0); ++x) {
+              bool con = c->sp.constrained(m, x, y, z, gamma_d);
+              c->mask[c->sp.gidx(m, z, y, x)] = con;
+              nf += !con;
+            }
+      c->nfree = nf;
+    }
+    // ---- patch families
+    rm::SetupInput in{};
+    in.k = space; in.p = p; in.n[0] = mesh->nx; in.n[1] = mesh->ny; in.n[2] = mesh->nz;
+    in.gamma_d = gamma_d; in.coords = mesh->coords; in.alpha = alpha; in.beta = beta;
+    in.n_alpha = n_alpha; in.n_beta = n_beta;
+    in.dim = (c->decomposition == RM_PAFW) ? 0 : space;
+    in.factorization = o.factorization;
+    in.interior_only = o.patch_entities == RM_INTERIOR_ONLY;
+    in.cartesian = cart;
+    in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    {
+      auto fam = rm::build_patch_family(in);
+      upload_family(c->prim, *fam);
+    }
+    if (c->decomposition == RM_PH && space >= 1) {
+      // potential problem B = D^T A D (+ eps_s beta M^{k-1} for k = 2): the V^{k-1} operator with
+      // (alpha', beta') = (beta, 0) for k = 1 and (beta, eps_s beta) for k = 2 (reading G8)
+      std::vector<double> ap(beta, beta + n_beta), bp(n_beta);
+      for (int64_t i = 0; i < n_beta; ++i) bp[i] = (space == 2) ? o.potential_shift * beta[i] : 0.0;
+      for (double v : ap) if (!(v > 0)) throw RmError(RM_EINVAL, "PH potential needs beta > 0");
+      rm::SetupInput ip = in;
+      ip.k = space - 1; ip.alpha = ap.data(); ip.beta = bp.data(); ip.n_alpha = n_beta; ip.n_beta = n_beta;
+      ip.dim = space - 1;
+      ip.factorization = RM_CHOL;
+      auto fam = rm::build_patch_family(ip);
+      upload_family(c->pot, *fam);
+      c->spot.init(space - 1, p, mesh->nx, mesh->ny, mesh->nz);
+      c->npot = c->spot.ndof();
+      const rm::Basis1D& b = rm::basis(p);
+      c->Dh.assign(p * (p + 1), 0.0);
+      for (int i = 0; i < p; ++i)
+        for (int j = 0; j <= p; ++j)
+          if (j == 0 || j == p || j == i) c->Dh[i * (p + 1) + j] = b.D[i * (p + 1) + j];
+      c->d_t = c->dalloc(c->npot); c->d_s = c->dalloc(c->npot);
+    }
+    c->d_r = c->dalloc(c->ndof);
+    c->d_sc = c->dalloc(8);
+    c->d_part = c->dalloc(1024);
+    CK(cudaDeviceSynchronize());
+    c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c.release();
+    return RM_OK;
+  } catch (const RmError& e) {
+    return fail(e);
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return RM_ENOMEM;
+  } catch (const std::exception& e) {
+    std::string m = e.what();
+    g_err = m;
+    if (m.find("pivot") != std::string::npos || m.find("breakdown") != std::string::npos) return RM_ENUMERIC;
+    return RM_EINVAL;
+  }
+}
+
+rm_status rm_layout(const rm_ctx* c, int64_t* n_local, int64_t* n_free, int32_t shape[3][3]) {
+  if (!c) { g_err = "null context"; return RM_EINVAL; }
+  if (n_local) *n_local = c->ndof;
+  if (n_free) *n_free = c->nfree;
+  if (shape)
+    for (int m = 0; m < 3; ++m)
+      for (int d = 0; d < 3; ++d) shape[m][d] = (m < c->sp.ncomp) ? (int32_t)c->sp.len(m, 2 - d) : 0;
+  return RM_OK;
+}
+
+rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
+  if (!c || !info) { g_err = "null argument"; return RM_EINVAL; }
+  std::memset(info, 0, sizeof *info);
+  info->n_local = c->ndof;
+  info->n_free = c->nfree;
+  info->n_patches = c->prim.npatch;
+  info->n_patches_potential = c->pot.npatch;
+  info->n_factor_blocks = c->prim.nfactors + c->pot.nfactors;
+  info->factor_bytes = c->prim.sweep_value_bytes + c->pot.sweep_value_bytes;
+  info->sweep_bytes = info->factor_bytes + 3 * 8 * c->ndof;
+  info->n_colors = (int32_t)c->prim.color_start.size() - 1;
+  info->n_classes = (int32_t)(c->prim.nclasses + c->pot.nclasses);
+  info->icc_sigma_max = c->prim.sigma_max;
+  info->setup_seconds = c->setup_seconds;
+  return RM_OK;
+}
+
+rm_status rm_constrained_mask(const rm_ctx* c, uint8_t* mask) {
+  if (!c || !mask) { g_err = "null argument"; return RM_EINVAL; }
+  std::memcpy(mask, c->mask.data(), c->mask.size());
+  return RM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
+  CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st));
+}
+
+void run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
+  for (size_t col = 0; col + 1 < F.color_start.size(); ++col) {
+    const int a = F.color_start[col], b = F.color_start[col + 1];
+    if (b <= a) continue;
+    CK(rm::launch_patch_solve(F.d_classes, F.d_pclass + a, F.d_pbase + 3LL * a, F.d_pvals + a, F.d_vals, r, u, omega,
+                              b - a, F.maxT, F.smem, c->st));
+  }
+}
+
+// u += omega * P^{-1} r  (r zero on constrained DoFs)
+void add_precond(rm_ctx* c, const double* r, double* u, double omega) {
+  run_family(c, c->prim, r, u, omega);
+  if (c->pot.present) {
+    CK(rm::launch_hiptmair_DT(c->k, c->p, c->n, c->gamma, c->Dh.data(), r, c->d_t, c->st));
+    CK(cudaMemsetAsync(c->d_s, 0, c->npot * sizeof(double), c->st));
+    run_family(c, c->pot, c->d_t, c->d_s, 1.0);
+    CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, u, omega, c->st));
+  }
+}
+
+template <class F>
+rm_status guarded(rm_ctx* c, F&& f) {
+  if (!c) { g_err = "null context"; return RM_EINVAL; }
+  try {
+    CK(cudaSetDevice(c->device));
+    f();
+    return RM_OK;
+  } catch (const RmError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return RM_EINVAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+rm_status rm_apply(rm_ctx* c, const double* u, double* v) {
+  return guarded(c, [&] {
+    if (!u || !v) throw RmError(RM_EINVAL, "null vector");
+    do_apply(c, u, nullptr, v);
+  });
+}
+
+rm_status rm_residual(rm_ctx* c, const double* f, const double* u, double* r) {
+  return guarded(c, [&] {
+    if (!f || !u || !r) throw RmError(RM_EINVAL, "null vector");
+    do_apply(c, u, f, r);
+  });
+}
+
+rm_status rm_relax(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
+  return guarded(c, [&] {
+    if (!f || !u_in || !u_out) throw RmError(RM_EINVAL, "null vector");
+    do_apply(c, u_in, f, c->d_r);
+    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    add_precond(c, c->d_r, u_out, omega);
+  });
+}
+
+rm_status rm_precondition(rm_ctx* c, const double* r, double* z) {
+  return guarded(c, [&] {
+    if (!r || !z) throw RmError(RM_EINVAL, "null vector");
+    // r with constrained entries read as zero: r_masked = r - 0*A0 ... use the residual kernel with u = 0
+    CK(cudaMemsetAsync(z, 0, c->ndof * sizeof(double), c->st));
+    do_apply(c, z, r, c->d_r);   // d_r = r - A*0 = r, constrained entries zeroed
+    add_precond(c, c->d_r, z, 1.0);
+  });
+}
+
+rm_status rm_relax_host(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
+  return guarded(c, [&] {
+    if (!f || !u_in || !u_out) throw RmError(RM_EINVAL, "null vector");
+    if (!c->d_hf) { c->d_hf = c->dalloc(c->ndof); c->d_hu = c->dalloc(c->ndof); }
+    const size_t B = c->ndof * sizeof(double);
+    CK(cudaMemcpyAsync(c->d_hf, f, B, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->d_hu, u_in, B, cudaMemcpyHostToDevice, c->st));
+    do_apply(c, c->d_hu, c->d_hf, c->d_r);
+    add_precond(c, c->d_r, c->d_hu, omega);
+    CK(cudaMemcpyAsync(u_out, c->d_hu, B, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  });
+}
+
+rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t maxit, int32_t* iters, double* rel) {
+  rm_status conv = RM_OK;
+  rm_status s = guarded(c, [&] {
+    if (!f || !u) throw RmError(RM_EINVAL, "null vector");
+    if (!c->d_z) { c->d_z = c->dalloc(c->ndof); c->d_pp = c->dalloc(c->ndof); c->d_q = c->dalloc(c->ndof); c->d_pr = c->dalloc(c->ndof); }
+    const size_t B = c->ndof * sizeof(double);
+    double* r = c->d_pr;
+    double* rz = c->d_sc + 0;
+    double* pq = c->d_sc + 1;
+    double* rzn = c->d_sc + 2;
+    CK(cudaMemsetAsync(u, 0, B, c->st));
+    do_apply(c, u, f, r);                         // r = f (masked)
+    CK(cudaMemsetAsync(c->d_z, 0, B, c->st));
+    add_precond(c, r, c->d_z, 1.0);
+    CK(rm::launch_dot(c->ndof, r, c->d_z, c->d_part, rz, c->st));
+    double rz0 = 0.0;
+    CK(cudaMemcpyAsync(&rz0, rz, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    int it = 0;
+    double relv = 0.0;
+    if (rz0 != 0.0) {
+      relv = 1.0;
+      CK(cudaMemcpyAsync(c->d_pp, c->d_z, B, cudaMemcpyDeviceToDevice, c->st));
+      bool done = false;
+      for (it = 1; it <= maxit; ++it) {
+        do_apply(c, c->d_pp, nullptr, c->d_q);
+        CK(rm::launch_dot(c->ndof, c->d_pp, c->d_q, c->d_part, pq, c->st));
+        CK(rm::launch_pcg_update(c->ndof, rz, pq, c->d_pp, c->d_q, u, r, c->st));
+        CK(cudaMemsetAsync(c->d_z, 0, B, c->st));
+        add_precond(c, r, c->d_z, 1.0);
+        CK(rm::launch_dot(c->ndof, r, c->d_z, c->d_part, rzn, c->st));
+        double h = 0.0;
+        CK(cudaMemcpyAsync(&h, rzn, 8, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        relv = std::sqrt(std::max(h, 0.0) / rz0);
+        if (relv <= rtol) { done = true; break; }
+        CK(rm::launch_pcg_pupdate(c->ndof, rzn, rz, c->d_z, c->d_pp, c->st));
+        CK(cudaMemcpyAsync(rz, rzn, 8, cudaMemcpyDeviceToDevice, c->st));
+      }
+      if (!done) { it = maxit; conv = RM_NOT_CONVERGED; }
+    }
+    CK(cudaStreamSynchronize(c->st));
+    if (iters) *iters = it;
+    if (rel) *rel = relv;
+  });
+  return s != RM_OK ? s : conv;
+}
+
+void rm_destroy(rm_ctx* c) { delete c; }
+
+}  // extern "C"

@@ -1,0 +1,847 @@
+#include "patches.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <tuple>
+#include <unordered_map>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace rm {
+
+namespace {
+
+struct DirSpec { int kind; int v; };   // kind 0 = node (vertex-type direction), 1 = cell
+struct Entity { DirSpec s[3]; };
+
+// per-direction window of a family (oracle reading G5 is the same rule)
+void window(const DirSpec& s, int fam, int p, int ncell, int& lo, int& hi) {
+  if (fam == FAM_P) {
+    if (s.kind == 0) { lo = s.v * p - (p - 1); hi = s.v * p + (p - 1); }
+    else { lo = s.v * p + 1; hi = s.v * p + p - 1; }
+    lo = std::max(lo, 0); hi = std::min(hi, ncell * p);
+  } else {
+    if (s.kind == 0) { lo = s.v * p - p; hi = s.v * p + p - 1; }
+    else { lo = s.v * p; hi = s.v * p + p - 1; }
+    lo = std::max(lo, 0); hi = std::min(hi, ncell * p - 1);
+  }
+}
+
+std::vector<Entity> entities(const Space& sp, int dim, bool interior_only) {
+  std::vector<Entity> out;
+  auto push = [&](Entity e) {
+    if (interior_only)
+      for (int d = 0; d < 3; ++d)
+        if (e.s[d].kind == 0 && (e.s[d].v == 0 || e.s[d].v == sp.n[d])) return;
+    out.push_back(e);
+  };
+  if (dim == 0) {
+    for (int z = 0; z <= sp.n[2]; ++z)
+      for (int y = 0; y <= sp.n[1]; ++y)
+        for (int x = 0; x <= sp.n[0]; ++x) push(Entity{{{0, x}, {0, y}, {0, z}}});
+  } else if (dim == 1 || dim == 2) {
+    for (int e = 0; e < 3; ++e) {
+      int lim[3];
+      for (int d = 0; d < 3; ++d) {
+        bool cellkind = (dim == 1) ? (d == e) : (d != e);
+        lim[d] = cellkind ? sp.n[d] : sp.n[d] + 1;
+      }
+      for (int z = 0; z < lim[2]; ++z)
+        for (int y = 0; y < lim[1]; ++y)
+          for (int x = 0; x < lim[0]; ++x) {
+            int idx[3] = {x, y, z};
+            Entity en;
+            for (int d = 0; d < 3; ++d) {
+              bool cellkind = (dim == 1) ? (d == e) : (d != e);
+              en.s[d] = {cellkind ? 1 : 0, idx[d]};
+            }
+            push(en);
+          }
+    }
+  } else {
+    throw std::runtime_error("entities: dim");
+  }
+  return out;
+}
+
+typedef std::array<int, 9> ClassKey;   // per direction: kind, low clip, high clip
+ClassKey class_key(const Space& sp, const Entity& e) {
+  ClassKey k;
+  for (int d = 0; d < 3; ++d) {
+    k[3 * d] = e.s[d].kind;
+    k[3 * d + 1] = (e.s[d].kind == 0 && e.s[d].v == 0);
+    k[3 * d + 2] = (e.s[d].kind == 0 && e.s[d].v == sp.n[d]);
+  }
+  return k;
+}
+
+int color_of(const Entity& e, int dim) {
+  if (dim == 0) return (e.s[0].v & 1) | ((e.s[1].v & 1) << 1) | ((e.s[2].v & 1) << 2);
+  int dir = 0;
+  for (int d = 0; d < 3; ++d)
+    if ((dim == 1 && e.s[d].kind == 1) || (dim == 2 && e.s[d].kind == 0)) dir = d;
+  int bits = 0, nb = 0;
+  for (int d = 0; d < 3; ++d)
+    if (e.s[d].kind == 0) bits |= (e.s[d].v & 1) << (nb++);
+  return dir * (1 << nb) + bits;
+}
+
+int64_t anchor_coord(const DirSpec& s, int p) { return (int64_t)s.v * p; }
+
+struct NatDof { int comp, ix, iy, iz, group; int64_t g; };
+
+// small dense SPD inverse (n <= 3) via Gauss-Jordan on the SPD block
+bool small_inverse(int n, const double* a, double* inv) {
+  double m[3][6];
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 2 * n; ++j) m[i][j] = (j < n) ? a[i * n + j] : (j - n == i ? 1.0 : 0.0);
+  for (int c = 0; c < n; ++c) {
+    if (!(m[c][c] > 0)) return false;
+    double piv = m[c][c];
+    for (int j = 0; j < 2 * n; ++j) m[c][j] /= piv;
+    for (int r = 0; r < n; ++r)
+      if (r != c) {
+        double f = m[r][c];
+        for (int j = 0; j < 2 * n; ++j) m[r][j] -= f * m[c][j];
+      }
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) inv[i * n + j] = m[i][j + n];
+  return true;
+}
+
+void build_sliced(Sliced& s, int r0, const std::vector<std::vector<int>>& rowcols) {
+  s.r0 = r0; s.nrows = (int)rowcols.size();
+  s.rowcols = rowcols;
+  int nsl = (s.nrows + 31) / 32;
+  s.slice_w.assign(nsl, 0); s.slice_off.assign(nsl, 0);
+  int64_t off = 0;
+  for (int sl = 0; sl < nsl; ++sl) {
+    int w = 0;
+    for (int l = 0; l < 32; ++l) {
+      int r = sl * 32 + l;
+      if (r < s.nrows) w = std::max(w, (int)rowcols[r].size());
+    }
+    s.slice_w[sl] = w; s.slice_off[sl] = (int)off;
+    off += (int64_t)w * 32;
+  }
+  s.nelem = off;
+  s.cols.assign(off, 0);
+  for (int sl = 0; sl < nsl; ++sl)
+    for (int l = 0; l < 32; ++l) {
+      int r = sl * 32 + l;
+      if (r >= s.nrows) continue;
+      for (size_t kk = 0; kk < rowcols[r].size(); ++kk) s.cols[s.slice_off[sl] + kk * 32 + l] = (uint16_t)rowcols[r][kk];
+    }
+}
+
+void build_blocks(Blocks& B, const std::vector<std::vector<int>>& blocks) {
+  B.nblk = (int)blocks.size();
+  B.bs = 1;
+  for (auto& b : blocks) B.bs = std::max(B.bs, (int)b.size());
+  B.mem.assign((size_t)B.bs * B.nblk, 0xFFFF);
+  for (int i = 0; i < B.nblk; ++i)
+    for (size_t j = 0; j < blocks[i].size(); ++j) B.mem[j * B.nblk + i] = (uint16_t)blocks[i][j];
+}
+
+}  // namespace
+
+// ===================================================================================== builder
+struct Builder {
+  const SetupInput& in;
+  Space sp;
+  PatchFamily* fam;
+  CellOperator op;
+  std::vector<int> cell_rows, cell_cols;   // structural pattern of the cell matrix
+  int nloc = 0;
+  std::vector<int> loc_comp, loc_a[3];     // local dof -> comp, local index per direction
+
+  explicit Builder(const SetupInput& in_, PatchFamily* f) : in(in_), fam(f) {
+    sp.init(in.k, in.p, in.n[0], in.n[1], in.n[2]);
+    nloc = sp.nloc();
+    for (int m = 0; m < sp.ncomp; ++m)
+      for (int c = 0; c < sp.lsize(m, 2); ++c)
+        for (int b = 0; b < sp.lsize(m, 1); ++b)
+          for (int a = 0; a < sp.lsize(m, 0); ++a) {
+            loc_comp.push_back(m); loc_a[0].push_back(a); loc_a[1].push_back(b); loc_a[2].push_back(c);
+          }
+    if (in.cartesian) {
+      op = build_cell_operator(in.k, in.p);
+      CellEntries e = cartesian_cell_entries(op, sp, 1.0, 1.0, 1.0);
+      cell_rows = e.row; cell_cols = e.col;
+    } else {
+      if (in.k != 0) throw std::runtime_error("trilinear cells are supported for H(grad) only");
+      double Xc[8][3];
+      for (int a = 0; a < 8; ++a) { Xc[a][0] = a & 1; Xc[a][1] = (a >> 1) & 1; Xc[a][2] = (a >> 2) & 1; }
+      CellEntries e;
+      aux_cell_entries(in.p, Xc, 1.0, 1.0, e);
+      cell_rows = e.row; cell_cols = e.col;
+    }
+  }
+
+  double coef(const double* arr, int64_t n_arr, int cx, int cy, int cz) const {
+    if (n_arr == 1) return arr[0];
+    return arr[((int64_t)cz * sp.n[1] + cy) * sp.n[0] + cx];
+  }
+
+  // ---------------------------------------------------------------- class program (symbolic)
+  void build_class(const Entity& e, ClassProgram& C) {
+    const int p = sp.p;
+    std::vector<NatDof> dofs;
+    for (int m = 0; m < sp.ncomp; ++m) {
+      int lo[3], hi[3];
+      for (int d = 0; d < 3; ++d) window(e.s[d], sp.fam[m][d], p, sp.n[d], lo[d], hi[d]);
+      for (int iz = lo[2]; iz <= hi[2]; ++iz)
+        for (int iy = lo[1]; iy <= hi[1]; ++iy)
+          for (int ix = lo[0]; ix <= hi[0]; ++ix) {
+            if (sp.constrained(m, ix, iy, iz, in.gamma_d)) continue;
+            int grp = 0;
+            const int idx[3] = {ix, iy, iz};
+            for (int d = 0; d < 3; ++d) if (sp.fam[m][d] == FAM_P && idx[d] % p == 0) ++grp;
+            dofs.push_back({m, ix, iy, iz, grp, sp.gidx(m, iz, iy, ix)});
+          }
+    }
+    // natural (pinned) order: group, comp, z, y, x (reading G6)
+    std::sort(dofs.begin(), dofs.end(), [](const NatDof& a, const NatDof& b) {
+      return std::tie(a.group, a.comp, a.iz, a.iy, a.ix) < std::tie(b.group, b.comp, b.iz, b.iy, b.ix);
+    });
+    const int n = (int)dofs.size();
+    std::unordered_map<int64_t, int> nat_of;
+    for (int i = 0; i < n; ++i) nat_of[dofs[i].g] = i;
+    // star cells
+    std::vector<int> cr[3];
+    for (int d = 0; d < 3; ++d) {
+      const DirSpec& s = e.s[d];
+      if (s.kind == 1) cr[d] = {s.v};
+      else { if (s.v - 1 >= 0) cr[d].push_back(s.v - 1); if (s.v < sp.n[d]) cr[d].push_back(s.v); }
+    }
+    std::vector<std::vector<int>> slot_nat;
+    for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0]) {
+      std::vector<int> mp(nloc, -1);
+      for (int l = 0; l < nloc; ++l) {
+        int m = loc_comp[l];
+        int64_t g = sp.gidx(m, (int64_t)cz * p + loc_a[2][l], (int64_t)cy * p + loc_a[1][l], (int64_t)cx * p + loc_a[0][l]);
+        auto it = nat_of.find(g);
+        if (it != nat_of.end()) mp[l] = it->second;
+      }
+      slot_nat.push_back(mp);
+      C.slot_dc[0].push_back(cx - (int)(anchor_coord(e.s[0], 1)));
+      C.slot_dc[1].push_back(cy - (int)(anchor_coord(e.s[1], 1)));
+      C.slot_dc[2].push_back(cz - (int)(anchor_coord(e.s[2], 1)));
+    }
+    // structural pattern (natural indices)
+    std::vector<std::vector<int>> adj(n);
+    for (auto& mp : slot_nat)
+      for (size_t t = 0; t < cell_rows.size(); ++t) {
+        int i = mp[cell_rows[t]], j = mp[cell_cols[t]];
+        if (i >= 0 && j >= 0) adj[i].push_back(j);
+      }
+    for (auto& a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
+
+    // ---- symbolic elimination
+    std::vector<int> E0;
+    for (int i = 0; i < n; ++i) if (dofs[i].group == 0) E0.push_back(i);
+    std::vector<char> isE0(n, 0);
+    for (int i : E0) isE0[i] = 1;
+    // blocks of E0 = connected components inside E0
+    std::vector<int> blk(n, -1);
+    std::vector<std::vector<int>> blocks0;
+    for (int i : E0) {
+      if (blk[i] >= 0) continue;
+      std::vector<int> st{i}, comp;
+      blk[i] = (int)blocks0.size();
+      while (!st.empty()) {
+        int u = st.back(); st.pop_back(); comp.push_back(u);
+        for (int v : adj[u]) if (isE0[v] && blk[v] < 0) { blk[v] = blk[i]; st.push_back(v); }
+      }
+      if (comp.size() > 3) throw std::runtime_error("interior block larger than 3x3: operator not in FDM-sparse form");
+      std::sort(comp.begin(), comp.end());
+      blocks0.push_back(comp);
+    }
+    std::vector<int> G;   // interface natural indices
+    for (int i = 0; i < n; ++i) if (!isE0[i]) G.push_back(i);
+    const int nG = (int)G.size();
+    std::vector<int> gpos(n, -1);
+    for (int t = 0; t < nG; ++t) gpos[G[t]] = t;
+    std::vector<char> Sb((size_t)nG * nG, 0);   // Schur pattern over interface
+    for (int t = 0; t < nG; ++t)
+      for (int j : adj[G[t]]) if (gpos[j] >= 0) Sb[(size_t)t * nG + gpos[j]] = 1;
+    for (auto& b : blocks0) {
+      std::vector<int> nb;
+      for (int u : b) for (int v : adj[u]) if (gpos[v] >= 0) nb.push_back(gpos[v]);
+      std::sort(nb.begin(), nb.end()); nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+      for (int a : nb) for (int c : nb) Sb[(size_t)a * nG + c] = 1;
+    }
+    // exact: greedy independent-set levels on the Schur pattern; icc: none
+    std::vector<std::vector<int>> Elev;   // interface local indices per level (after level 0)
+    std::vector<char> alive(nG, 1);
+    int nalive = nG;
+    if (in.factorization == 0) {
+      while (nalive > 48) {
+        std::vector<int> R, deg(nG, 0);
+        for (int t = 0; t < nG; ++t) if (alive[t]) R.push_back(t);
+        for (int t : R) {
+          int d = 0;
+          for (int u : R) if (u != t && Sb[(size_t)t * nG + u]) ++d;
+          deg[t] = d;
+        }
+        std::vector<int> ord = R;
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+        std::vector<char> blocked(nG, 0);
+        std::vector<int> pick;
+        for (int t : ord) {
+          if (blocked[t]) continue;
+          pick.push_back(t); blocked[t] = 1;
+          for (int u : R) if (Sb[(size_t)t * nG + u]) blocked[u] = 1;
+        }
+        int64_t m = (int64_t)R.size(), nE = (int64_t)pick.size(), nnzW = 0;
+        for (int t : pick) nnzW += deg[t];
+        int64_t oldc = m * (m + 1) / 2;
+        int64_t newc = nE + 2 * nnzW + (m - nE) * (m - nE + 1) / 2;
+        if (newc > (oldc * 97) / 100) break;
+        std::sort(pick.begin(), pick.end());
+        for (int t : pick) { alive[t] = 0; --nalive; }
+        for (int t : pick) {
+          std::vector<int> nb;
+          for (int u : R) if (alive[u] && Sb[(size_t)t * nG + u]) nb.push_back(u);
+          for (int a : nb) for (int c : nb) Sb[(size_t)a * nG + c] = 1;
+        }
+        Elev.push_back(pick);
+      }
+    }
+    // ---- positions: E0 | E1 | ... | final (natural order inside each set)
+    std::vector<int> order;
+    for (int i : E0) order.push_back(i);
+    for (auto& L : Elev) for (int t : L) order.push_back(G[t]);
+    std::vector<int> finalset;
+    for (int t = 0; t < nG; ++t) if (alive[t]) finalset.push_back(t);
+    for (int t : finalset) order.push_back(G[t]);
+    std::vector<int> pos(n);
+    for (int q = 0; q < n; ++q) pos[order[q]] = q;
+    C.n = n;
+    C.offs.resize(n); C.group.resize(n);
+    std::vector<int> comp_of_pos(n);
+    for (int q = 0; q < n; ++q) {
+      const NatDof& d = dofs[order[q]];
+      C.group[q] = d.group;
+      comp_of_pos[q] = d.comp;
+      int64_t base = sp.gidx(d.comp, anchor_coord(e.s[2], p), anchor_coord(e.s[1], p), anchor_coord(e.s[0], p));
+      int64_t rel = d.g - base;
+      if (rel > INT32_MAX || rel < INT32_MIN) throw std::runtime_error("patch offset overflow");
+      C.offs[q] = (int)rel;
+    }
+    C.comp = comp_of_pos;
+    C.slot_map.clear();
+    for (auto& mp : slot_nat) {
+      std::vector<int> m2(nloc, -1);
+      for (int l = 0; l < nloc; ++l) if (mp[l] >= 0) m2[l] = pos[mp[l]];
+      C.slot_map.push_back(m2);
+    }
+    // pattern CSR over positions
+    C.prow.assign(n + 1, 0); C.pcol.clear();
+    {
+      std::vector<std::vector<int>> pa(n);
+      for (int i = 0; i < n; ++i) for (int j : adj[i]) pa[pos[i]].push_back(pos[j]);
+      for (int q = 0; q < n; ++q) {
+        std::sort(pa[q].begin(), pa[q].end());
+        C.prow[q + 1] = C.prow[q] + (int)pa[q].size();
+        C.pcol.insert(C.pcol.end(), pa[q].begin(), pa[q].end());
+      }
+    }
+    // ---- levels
+    C.lev.clear();
+    int64_t vofs = 0;
+    auto place = [&](Sliced& s) { s.vofs = vofs; vofs += s.nelem; };
+    auto placeb = [&](Blocks& b) { b.vofs = vofs; vofs += b.nval(); };
+    {   // level 0
+      Level L;
+      L.e0 = 0; L.e1 = (int)E0.size();
+      std::vector<std::vector<int>> wrows(n - L.e1), wtrows(L.e1);
+      for (auto& b : blocks0) {
+        std::vector<int> bp;
+        for (int u : b) bp.push_back(pos[u]);
+        L.blocks.push_back(bp);
+        std::vector<int> nb;
+        for (int u : b) for (int v : adj[u]) if (!isE0[v]) nb.push_back(pos[v]);
+        std::sort(nb.begin(), nb.end()); nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+        for (int q : bp) wtrows[q] = nb;
+        for (int r : nb) for (int q : bp) wrows[r - L.e1].push_back(q);
+      }
+      for (auto& w : wrows) std::sort(w.begin(), w.end());
+      build_blocks(L.blk, L.blocks); placeb(L.blk);
+      build_sliced(L.w, L.e1, wrows); place(L.w);
+      build_sliced(L.wt, L.e0, wtrows); place(L.wt);
+      C.lev.push_back(std::move(L));
+    }
+    {   // levels >= 1 (recompute the evolving Schur pattern to get W patterns)
+      std::vector<char> Sb2((size_t)nG * nG, 0);
+      for (int t = 0; t < nG; ++t)
+        for (int j : adj[G[t]]) if (gpos[j] >= 0) Sb2[(size_t)t * nG + gpos[j]] = 1;
+      for (auto& b : blocks0) {
+        std::vector<int> nb;
+        for (int u : b) for (int v : adj[u]) if (gpos[v] >= 0) nb.push_back(gpos[v]);
+        std::sort(nb.begin(), nb.end()); nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+        for (int a : nb) for (int c : nb) Sb2[(size_t)a * nG + c] = 1;
+      }
+      std::vector<char> al(nG, 1);
+      int start = (int)E0.size();
+      for (auto& Lset : Elev) {
+        Level L;
+        L.e0 = start; L.e1 = start + (int)Lset.size();
+        std::vector<std::vector<int>> wrows(n - L.e1), wtrows(Lset.size());
+        for (size_t a = 0; a < Lset.size(); ++a) {
+          int t = Lset[a];
+          int q = pos[G[t]];
+          L.blocks.push_back({q});
+          std::vector<int> nb;
+          for (int u = 0; u < nG; ++u)
+            if (u != t && al[u] && Sb2[(size_t)t * nG + u]) {
+              bool inE = std::binary_search(Lset.begin(), Lset.end(), u);
+              if (!inE) nb.push_back(pos[G[u]]);
+            }
+          std::sort(nb.begin(), nb.end());
+          wtrows[a] = nb;
+          for (int r : nb) wrows[r - L.e1].push_back(q);
+        }
+        for (auto& w : wrows) std::sort(w.begin(), w.end());
+        for (int t : Lset) al[t] = 0;
+        for (int t : Lset) {
+          std::vector<int> nb;
+          for (int u = 0; u < nG; ++u) if (al[u] && Sb2[(size_t)t * nG + u]) nb.push_back(u);
+          for (int a : nb) for (int c : nb) Sb2[(size_t)a * nG + c] = 1;
+        }
+        build_blocks(L.blk, L.blocks); placeb(L.blk);
+        build_sliced(L.w, L.e1, wrows); place(L.w);
+        build_sliced(L.wt, L.e0, wtrows); place(L.wt);
+        C.lev.push_back(std::move(L));
+        start = C.lev.back().e1;
+      }
+      // final block
+      C.m = n - start;
+      C.vofs_final = vofs;
+      if (in.factorization == 0) {
+        C.final_kind = FINAL_DENSE_INV;
+        vofs += (int64_t)C.m * (C.m + 1) / 2;
+      } else {
+        C.final_kind = FINAL_ICC;
+        // ICC(0) on the Schur pattern of the final block (positions start..n-1, pinned order)
+        const int m = C.m;
+        std::vector<std::vector<int>> rows(m);
+        for (int a = 0; a < m; ++a) {
+          int ta = finalset[a];
+          for (int b = 0; b <= a; ++b) if (Sb2[(size_t)ta * nG + finalset[b]]) rows[a].push_back(b);
+        }
+        C.icc_rowptr.assign(m + 1, 0); C.icc_col.clear();
+        for (int a = 0; a < m; ++a) {
+          C.icc_rowptr[a + 1] = C.icc_rowptr[a] + (int)rows[a].size();
+          C.icc_col.insert(C.icc_col.end(), rows[a].begin(), rows[a].end());
+        }
+        const int nnz = C.icc_rowptr[m];
+        // forward levels
+        std::vector<int> lv(m, 0);
+        int maxl = 0;
+        for (int a = 0; a < m; ++a) {
+          int l = 0;
+          for (int t = C.icc_rowptr[a]; t < C.icc_rowptr[a + 1]; ++t) { int b = C.icc_col[t]; if (b != a) l = std::max(l, lv[b] + 1); }
+          lv[a] = l; maxl = std::max(maxl, l);
+        }
+        C.icc_level_ptr.assign(maxl + 2, 0); C.icc_level_rows.clear();
+        for (int l = 0; l <= maxl; ++l) {
+          for (int a = 0; a < m; ++a) if (lv[a] == l) C.icc_level_rows.push_back(a);
+          C.icc_level_ptr[l + 1] = (int)C.icc_level_rows.size();
+        }
+        // transpose (rows of L^T), diag last -> first
+        std::vector<std::vector<std::pair<int, int>>> trows(m);
+        for (int a = 0; a < m; ++a)
+          for (int t = C.icc_rowptr[a]; t < C.icc_rowptr[a + 1]; ++t) trows[C.icc_col[t]].push_back({a, t});
+        C.icct_rowptr.assign(m + 1, 0); C.icct_col.clear(); C.icct_src.clear();
+        for (int b = 0; b < m; ++b) {
+          std::sort(trows[b].begin(), trows[b].end());
+          C.icct_rowptr[b + 1] = C.icct_rowptr[b] + (int)trows[b].size();
+          for (auto& pr : trows[b]) { C.icct_col.push_back(pr.first); C.icct_src.push_back(pr.second); }
+        }
+        std::vector<int> lt(m, 0);
+        int maxt = 0;
+        for (int b = m - 1; b >= 0; --b) {
+          int l = 0;
+          for (int t = C.icct_rowptr[b]; t < C.icct_rowptr[b + 1]; ++t) { int a = C.icct_col[t]; if (a != b) l = std::max(l, lt[a] + 1); }
+          lt[b] = l; maxt = std::max(maxt, l);
+        }
+        C.icct_level_ptr.assign(maxt + 2, 0); C.icct_level_rows.clear();
+        for (int l = 0; l <= maxt; ++l) {
+          for (int b = 0; b < m; ++b) if (lt[b] == l) C.icct_level_rows.push_back(b);
+          C.icct_level_ptr[l + 1] = (int)C.icct_level_rows.size();
+        }
+        vofs += 2 * (int64_t)nnz;   // L values (row order) then L^T values (transpose order)
+      }
+    }
+    C.nvals = vofs;
+  }
+
+  // ---------------------------------------------------------------- numeric factorization
+  // Returns false on a non-positive pivot (message in err).
+  bool factor_patch(const ClassProgram& C, const Entity& e, double* out, double shift, std::string& err) {
+    const int n = C.n;
+    const int p = sp.p;
+    std::vector<double> P(C.pcol.size(), 0.0);
+    // assemble from the star cells
+    std::vector<int> cr[3];
+    for (int d = 0; d < 3; ++d) {
+      const DirSpec& s = e.s[d];
+      if (s.kind == 1) cr[d] = {s.v};
+      else { if (s.v - 1 >= 0) cr[d].push_back(s.v - 1); if (s.v < sp.n[d]) cr[d].push_back(s.v); }
+    }
+    int slot = 0;
+    CellEntries ce;
+    for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0]) {
+      const std::vector<int>& mp = C.slot_map[slot++];
+      const double a = coef(in.alpha, in.n_alpha, cx, cy, cz), b = coef(in.beta, in.n_beta, cx, cy, cz);
+      const CellEntries* E;
+      if (in.cartesian) {
+        E = &cart_entries(in.hx[cx], in.hy[cy], in.hz[cz]);
+      } else {
+        double Xc[8][3];
+        for (int az = 0; az < 2; ++az)
+          for (int ay = 0; ay < 2; ++ay)
+            for (int ax = 0; ax < 2; ++ax) {
+              int64_t vi = (((int64_t)(cz + az) * (sp.n[1] + 1) + (cy + ay)) * (sp.n[0] + 1) + (cx + ax)) * 3;
+              for (int i = 0; i < 3; ++i) Xc[az * 4 + ay * 2 + ax][i] = in.coords[vi + i];
+            }
+        aux_cell_entries(p, Xc, a, b, ce);
+        E = &ce;
+      }
+      const bool cart = in.cartesian;
+      for (size_t t = 0; t < E->row.size(); ++t) {
+        int i = mp[E->row[t]], j = mp[E->col[t]];
+        if (i < 0 || j < 0) continue;
+        const int* b0 = &C.pcol[C.prow[i]];
+        const int* b1 = &C.pcol[C.prow[i + 1]];
+        const int* it = std::lower_bound(b0, b1, j);
+        double v = cart ? (a * E->kval[t] + b * E->mval[t]) : E->kval[t];
+        P[it - C.pcol.data()] += v;
+      }
+    }
+    if (shift != 0.0)
+      for (int i = 0; i < n; ++i) {
+        const int* b0 = &C.pcol[C.prow[i]];
+        const int* it = std::lower_bound(b0, &C.pcol[C.prow[i + 1]], i);
+        P[it - C.pcol.data()] *= (1.0 + shift);
+      }
+    auto Pij = [&](int i, int j) -> double {
+      const int* b0 = &C.pcol[C.prow[i]];
+      const int* b1 = &C.pcol[C.prow[i + 1]];
+      const int* it = std::lower_bound(b0, b1, j);
+      return (it != b1 && *it == j) ? P[it - C.pcol.data()] : 0.0;
+    };
+    const Level& L0 = C.lev[0];
+    const int nI = L0.e1, nG = n - nI;
+    // dense Schur complement over positions nI..n-1
+    std::vector<double> S((size_t)nG * nG, 0.0);
+    for (int r = nI; r < n; ++r)
+      for (int t = C.prow[r]; t < C.prow[r + 1]; ++t) {
+        int c = C.pcol[t];
+        if (c >= nI) S[(size_t)(r - nI) * nG + (c - nI)] = P[t];
+      }
+    // level 0: block inverses, W = P_RE Dinv, S -= W P_ER
+    auto put_sliced = [&](const Sliced& s, auto&& val) {
+      double* o = out + s.vofs;
+      const int nsl = (int)s.slice_w.size();
+      for (int sl = 0; sl < nsl; ++sl)
+        for (int l = 0; l < 32; ++l) {
+          int r = sl * 32 + l;
+          if (r >= s.nrows) continue;
+          const auto& rc = s.rowcols[r];
+          for (size_t kk = 0; kk < rc.size(); ++kk) o[s.slice_off[sl] + kk * 32 + l] = val(s.r0 + r, rc[kk]);
+        }
+    };
+    auto put_blocks = [&](const Blocks& B, const std::vector<std::vector<double>>& Lb) {
+      // Lb[i]: row-major lower factor of block i (bs_i x bs_i); stored slot-major, diag inverted
+      double* o = out + B.vofs;
+      for (int i = 0; i < B.nblk; ++i) {
+        const int bs = (int)std::lround(std::sqrt((double)Lb[i].size()));
+        int slot = 0;
+        for (int r = 0; r < B.bs; ++r)
+          for (int c = 0; c <= r; ++c, ++slot) {
+            double v = 0.0;
+            if (r < bs && c <= r) v = Lb[i][r * bs + c];
+            if (r == c) v = (r < bs) ? 1.0 / v : 0.0;
+            o[(size_t)slot * B.nblk + i] = v;
+          }
+      }
+    };
+    {
+      // level 0: Cholesky of each interior block, M = P_RE L^{-T}, S -= M M^T
+      const int nb0 = (int)L0.blocks.size();
+      std::vector<std::vector<double>> Lb(nb0);
+      std::vector<int> bid(n, -1), bidx(n, 0);
+      for (int bi = 0; bi < nb0; ++bi) {
+        const auto& b = L0.blocks[bi];
+        const int bs = (int)b.size();
+        std::vector<double> Lm(bs * bs, 0.0);
+        for (int j = 0; j < bs; ++j) {
+          double d = Pij(b[j], b[j]);
+          for (int k = 0; k < j; ++k) d -= Lm[j * bs + k] * Lm[j * bs + k];
+          if (!(d > 0)) { err = "non-positive pivot in an interior block"; return false; }
+          Lm[j * bs + j] = std::sqrt(d);
+          for (int i = j + 1; i < bs; ++i) {
+            double t = Pij(b[i], b[j]);
+            for (int k = 0; k < j; ++k) t -= Lm[i * bs + k] * Lm[j * bs + k];
+            Lm[i * bs + j] = t / Lm[j * bs + j];
+          }
+        }
+        for (int i = 0; i < bs; ++i) { bid[b[i]] = bi; bidx[b[i]] = i; }
+        Lb[bi] = Lm;
+      }
+      put_blocks(L0.blk, Lb);
+      // M rows per block: for r in nb(block): M[r][b] = solve L_b m = P[b][r]  (m = L^{-1} P_br)
+      std::vector<std::map<int, double>> Mrow(nG);   // interface row -> (E position -> value)
+      for (int bi = 0; bi < nb0; ++bi) {
+        const auto& b = L0.blocks[bi];
+        const int bs = (int)b.size();
+        std::vector<int> nb;
+        for (int q : b)
+          for (int t = C.prow[q]; t < C.prow[q + 1]; ++t) if (C.pcol[t] >= nI) nb.push_back(C.pcol[t]);
+        std::sort(nb.begin(), nb.end()); nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+        const std::vector<double>& Lm = Lb[bi];
+        std::vector<double> Mv(nb.size() * bs);
+        for (size_t i = 0; i < nb.size(); ++i) {
+          double y[3];
+          for (int j = 0; j < bs; ++j) {
+            double t = Pij(nb[i], b[j]);
+            for (int k = 0; k < j; ++k) t -= Lm[j * bs + k] * y[k];
+            y[j] = t / Lm[j * bs + j];
+            Mv[i * bs + j] = y[j];
+            Mrow[nb[i] - nI][b[j]] = y[j];
+          }
+        }
+        for (size_t i = 0; i < nb.size(); ++i)
+          for (size_t c = 0; c < nb.size(); ++c) {
+            double s = 0;
+            for (int j = 0; j < bs; ++j) s += Mv[i * bs + j] * Mv[c * bs + j];
+            S[(size_t)(nb[i] - nI) * nG + (nb[c] - nI)] -= s;
+          }
+      }
+      auto mval = [&](int r, int q) {
+        const auto& mr = Mrow[r - nI];
+        auto it = mr.find(q);
+        return it == mr.end() ? 0.0 : it->second;
+      };
+      put_sliced(L0.w, mval);
+      put_sliced(L0.wt, [&](int q, int r) { return mval(r, q); });
+    }
+    // levels >= 1 on the dense Schur complement, 1x1 pivots: L = sqrt(S_qq), M = S_Rq / L
+    for (size_t l = 1; l < C.lev.size(); ++l) {
+      const Level& L = C.lev[l];
+      auto Sv = [&](int r, int c) -> double& { return S[(size_t)(r - nI) * nG + (c - nI)]; };
+      std::vector<std::vector<double>> Lb;
+      for (int q = L.e0; q < L.e1; ++q) {
+        if (!(Sv(q, q) > 0)) { err = "non-positive pivot in an interface level"; return false; }
+        Lb.push_back({std::sqrt(Sv(q, q))});
+      }
+      put_blocks(L.blk, Lb);
+      put_sliced(L.w, [&](int r, int q) { return Sv(r, q) / std::sqrt(Sv(q, q)); });
+      put_sliced(L.wt, [&](int q, int r) { return Sv(r, q) / std::sqrt(Sv(q, q)); });
+      for (int q = L.e0; q < L.e1; ++q) {
+        const auto& nb = L.wt.rowcols[q - L.e0];
+        double d = Sv(q, q);
+        std::vector<double> w(nb.size()), sq(nb.size());
+        for (size_t i = 0; i < nb.size(); ++i) { w[i] = Sv(nb[i], q) / d; sq[i] = Sv(q, nb[i]); }
+        for (size_t i = 0; i < nb.size(); ++i)
+          for (size_t c = 0; c < nb.size(); ++c) Sv(nb[i], nb[c]) -= w[i] * sq[c];
+      }
+    }
+    // final block
+    const int m = C.m, f0 = n - m;
+    std::vector<double> F((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) F[(size_t)i * m + j] = S[(size_t)(f0 + i - nI) * nG + (f0 + j - nI)];
+    if (C.final_kind == FINAL_DENSE_INV) {
+      // Cholesky F = L L^T (lower, in place), Linv, then inverse lower = (Linv^T Linv) lower part
+      for (int j = 0; j < m; ++j) {
+        double d = F[(size_t)j * m + j];
+        for (int k = 0; k < j; ++k) d -= F[(size_t)j * m + k] * F[(size_t)j * m + k];
+        if (!(d > 0)) { err = "non-positive pivot in the final interface block"; return false; }
+        d = std::sqrt(d);
+        F[(size_t)j * m + j] = d;
+        for (int i = j + 1; i < m; ++i) {
+          double s = F[(size_t)i * m + j];
+          const double* fi = &F[(size_t)i * m];
+          const double* fj = &F[(size_t)j * m];
+          for (int k = 0; k < j; ++k) s -= fi[k] * fj[k];
+          F[(size_t)i * m + j] = s / d;
+        }
+      }
+      // Linv lower (row-major): solve L X = I column by column
+      std::vector<double> Li((size_t)m * m, 0.0);
+      for (int c = 0; c < m; ++c) {
+        Li[(size_t)c * m + c] = 1.0 / F[(size_t)c * m + c];
+        for (int i = c + 1; i < m; ++i) {
+          double s = 0;
+          const double* fi = &F[(size_t)i * m];
+          for (int k = c; k < i; ++k) s += fi[k] * Li[(size_t)k * m + c];
+          Li[(size_t)i * m + c] = -s / F[(size_t)i * m + i];
+        }
+      }
+      // inverse(i,j) = sum_{k >= max(i,j)} Li(k,i) Li(k,j); packed lower rows
+      double* o = out + C.vofs_final;
+      // transpose Li for contiguous access: LiT[i][k] = Li[k][i]
+      std::vector<double> LiT((size_t)m * m);
+      for (int i = 0; i < m; ++i) for (int k = 0; k < m; ++k) LiT[(size_t)i * m + k] = Li[(size_t)k * m + i];
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j <= i; ++j) {
+          const double* a = &LiT[(size_t)i * m];
+          const double* b = &LiT[(size_t)j * m];
+          double s = 0;
+          for (int k = i; k < m; ++k) s += a[k] * b[k];
+          o[(size_t)i * (i + 1) / 2 + j] = s;
+        }
+    } else {
+      // ICC(0) on the final pattern, up-looking rows (same definition as oracle/patches.py)
+      const int nnz = C.icc_rowptr[m];
+      std::vector<double> Lv(nnz, 0.0);
+      for (int a = 0; a < m; ++a) {
+        for (int t = C.icc_rowptr[a]; t < C.icc_rowptr[a + 1]; ++t) {
+          int b = C.icc_col[t];
+          double s = F[(size_t)a * m + b];
+          // sum_{k<b} L_ak L_bk over the two sparse rows
+          int ia = C.icc_rowptr[a], ib = C.icc_rowptr[b];
+          const int ea = t, eb = C.icc_rowptr[b + 1] - 1;   // exclude column b itself in both rows
+          while (ia < ea && ib < eb) {
+            int ca = C.icc_col[ia], cb = C.icc_col[ib];
+            if (ca == cb) { s -= Lv[ia] * Lv[ib]; ++ia; ++ib; }
+            else if (ca < cb) ++ia; else ++ib;
+          }
+          if (b == a) {
+            if (!(s > 0)) { err = "icc breakdown"; return false; }
+            Lv[t] = std::sqrt(s);
+          } else {
+            Lv[t] = s / Lv[C.icc_rowptr[b + 1] - 1];
+          }
+        }
+      }
+      double* o = out + C.vofs_final;
+      for (int t = 0; t < nnz; ++t) o[t] = Lv[t];
+      for (int a = 0; a < m; ++a) { int t = C.icc_rowptr[a + 1] - 1; o[t] = 1.0 / Lv[t]; }
+      for (int t = 0; t < nnz; ++t) {
+        int src = C.icct_src[t];
+        o[nnz + t] = o[src];
+      }
+    }
+    return true;
+  }
+
+  std::map<std::tuple<double, double, double>, CellEntries> cart_cache;
+  std::mutex cart_mu;
+  const CellEntries& cart_entries(double hx, double hy, double hz) {
+    std::lock_guard<std::mutex> lk(cart_mu);
+    auto key = std::make_tuple(hx, hy, hz);
+    auto it = cart_cache.find(key);
+    if (it == cart_cache.end()) it = cart_cache.emplace(key, cartesian_cell_entries(op, sp, hx, hy, hz)).first;
+    return it->second;
+  }
+};
+
+std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
+  auto fam = std::make_unique<PatchFamily>();
+  Builder B(in, fam.get());
+  fam->sp = B.sp; fam->dim = in.dim; fam->gamma_d = in.gamma_d; fam->factorization = in.factorization;
+  std::vector<Entity> ents = entities(B.sp, in.dim, in.interior_only != 0);
+  std::map<ClassKey, int> cls_of;
+  std::vector<int> ecls(ents.size());
+  std::vector<Entity> rep;
+  for (size_t i = 0; i < ents.size(); ++i) {
+    ClassKey k = class_key(B.sp, ents[i]);
+    auto it = cls_of.find(k);
+    if (it == cls_of.end()) { it = cls_of.emplace(k, (int)rep.size()).first; rep.push_back(ents[i]); }
+    ecls[i] = it->second;
+  }
+  fam->classes.resize(rep.size());
+  for (size_t c = 0; c < rep.size(); ++c) B.build_class(rep[c], fam->classes[c]);
+  // drop empty patches
+  std::vector<size_t> keep;
+  for (size_t i = 0; i < ents.size(); ++i) if (fam->classes[ecls[i]].n > 0) keep.push_back(i);
+  const size_t np = keep.size();
+  fam->pclass.resize(np); fam->pbase.resize(np * 3); fam->pvals.resize(np); fam->pcolor.resize(np);
+  fam->ncolors = (in.dim == 0) ? 8 : (in.dim == 1 ? 12 : 6);
+  // dedup key: class + per-slot coefficients (+ cell sizes); trilinear cells are never shared
+  std::map<std::vector<double>, int64_t> dedup;
+  std::vector<int64_t> fid(np);
+  std::vector<int64_t> foff;
+  std::vector<size_t> frep;
+  int64_t total = 0;
+  for (size_t t = 0; t < np; ++t) {
+    const Entity& e = ents[keep[t]];
+    const int c = ecls[keep[t]];
+    fam->pclass[t] = c;
+    fam->pcolor[t] = color_of(e, in.dim);
+    for (int m = 0; m < 3; ++m)
+      fam->pbase[t * 3 + m] = (m < B.sp.ncomp)
+          ? B.sp.gidx(m, anchor_coord(e.s[2], B.sp.p), anchor_coord(e.s[1], B.sp.p), anchor_coord(e.s[0], B.sp.p)) : 0;
+    std::vector<double> key{(double)c};
+    if (in.cartesian) {
+      std::vector<int> cr[3];
+      for (int d = 0; d < 3; ++d) {
+        const DirSpec& s = e.s[d];
+        if (s.kind == 1) cr[d] = {s.v};
+        else { if (s.v - 1 >= 0) cr[d].push_back(s.v - 1); if (s.v < B.sp.n[d]) cr[d].push_back(s.v); }
+      }
+      for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0]) {
+        key.push_back(B.coef(in.alpha, in.n_alpha, cx, cy, cz));
+        key.push_back(B.coef(in.beta, in.n_beta, cx, cy, cz));
+        key.push_back(in.hx[cx]); key.push_back(in.hy[cy]); key.push_back(in.hz[cz]);
+      }
+    } else {
+      key.push_back(-1.0 - (double)t);
+    }
+    auto it = dedup.find(key);
+    if (it == dedup.end()) {
+      it = dedup.emplace(key, (int64_t)foff.size()).first;
+      foff.push_back(total);
+      frep.push_back(t);
+      total += fam->classes[c].nvals;
+    }
+    fid[t] = it->second;
+    fam->pvals[t] = foff[fid[t]];
+  }
+  fam->nfactors = (int64_t)foff.size();
+  fam->values.assign(total, 0.0);
+  std::string first_err;
+  std::mutex emu;
+  double smax = 0.0;
+  const int64_t nf = (int64_t)foff.size();
+#pragma omp parallel for schedule(dynamic, 4) reduction(max : smax)
+  for (int64_t f = 0; f < nf; ++f) {
+    size_t t = frep[f];
+    const Entity& e = ents[keep[t]];
+    const ClassProgram& C = fam->classes[fam->pclass[t]];
+    std::string err;
+    bool ok = B.factor_patch(C, e, fam->values.data() + foff[f], 0.0, err);
+    if (!ok && in.factorization == 1) {   // reading G7: P + sigma diag(P), sigma = 1e-10 doubling
+      for (double shift = 1e-10; shift <= 1e-2 && !ok; shift *= 2.0) {
+        ok = B.factor_patch(C, e, fam->values.data() + foff[f], shift, err);
+        if (ok) smax = std::max(smax, shift);
+      }
+    }
+    if (!ok) {
+      std::lock_guard<std::mutex> lk(emu);
+      if (first_err.empty()) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "patch %zu (entity %d,%d,%d): %s", t, e.s[0].v, e.s[1].v, e.s[2].v, err.c_str());
+        first_err = buf;
+      }
+    }
+  }
+  fam->sigma_max = smax;
+  if (!first_err.empty()) throw std::runtime_error(first_err);
+  return fam;
+}
+
+}  // namespace rm
