@@ -1,0 +1,272 @@
+#!/usr/bin/env python
+"""Benchmark: DoFs/s per relaxation sweep (fp64) on B200 -- BASELINE.json metric.
+
+One "step" = one rm_relax sweep (residual r = f - A u, all star-patch solves, scatter-add,
+u_out = u_in + omega c) over the whole mesh of the workload (default: BASELINE.json configs[1],
+H(grad) Q_7 on 32^3 cells, log10(alpha) ~ U[-2,2] per cell, Dirichlet x=0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Timing: W untimed sweeps, then K sweeps between barrier + cuda.synchronize, CUDA events on the
+library stream, max over ranks.  The patch factors (tens of GB for cfg2) exceed the 126 MB L2,
+so no L2 flush is needed ("l2": "inputs larger than L2").  value = free DoFs (all ranks) / s.
+Multi-GPU (torchrun): each rank runs an independent replica of the workload ("replicas";
+the slab-partitioned halo path is not built yet), so scaling is weak.
+
+Extra keys: roofline (dominant kernel = batched patch solve; algorithmic bytes = patch-factor
+values + r gather + u_out read-modify-write, per launch), e2e (rm_relax_host with pinned host
+buffers, copies inside the timed region), cpu_baseline (the oracle, on a bounded sample),
+clocks (nvidia-smi during the timed region), gpu_launches (our kernels in the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import rm_inputs as ri  # noqa: E402
+
+# bounded oracle samples (same p, space, coefficient law, BCs; smaller mesh) -- DESIGN.md
+ORACLE_SAMPLE = {1: (4, 4, 4), 2: (3, 3, 3), 3: (2, 2, 2), 4: (2, 2, 2), 5: (2, 2, 2)}
+SPACE_NAME = {0: "H(grad) Q", 1: "H(curl) NCE", 2: "H(div) NCF"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.strip().split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1])); mx.append(float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(nm)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sweep_rate(w, cfg):
+    """The oracle as it stands, one sweep on a bounded sample mesh: free DoFs / s."""
+    from oracle.solver import Problem
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    nx, ny, nz = ORACLE_SAMPLE[cfg]
+    ws = w.with_mesh(nx, ny, nz)
+    pb = Problem(ws.space, ws.p, nx, ny, nz, ri.vertex_coords(ws), ri.cell_alpha(ws), ri.cell_beta(ws), ws.gamma_d,
+                 decomposition=ws.decomposition, factorization=ws.factorization, matfree=(ws.perturb > 0))
+    f = ri.uniform_vector(ws.cfg, 0, pb.space.ndof); f[pb.constrained] = 0
+    u = ri.uniform_vector(ws.cfg, 3, pb.space.ndof); u[pb.constrained] = 0
+    t0 = time.perf_counter()
+    pb.patch_solvers()
+    if ws.decomposition == "ph":
+        pb.potential()
+    _ = pb.A if not pb.matfree else None
+    setup = time.perf_counter() - t0
+    times = []
+    for _ in range(3):
+        t = time.perf_counter()
+        pb.relax(f, u)
+        times.append(time.perf_counter() - t)
+    sec = float(np.median(times))
+    nfree = int(pb.free.sum())
+    return nfree / sec, {"cores": cores, "sample": f"{nx}x{ny}x{nz} cells, p={ws.p}, {nfree} free DoFs, median of 3 "
+                                                    f"sweeps (oracle setup {setup:.1f} s untimed)", "sec_per_sweep": sec}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--mesh", type=int, default=0, help="override cells per direction (testing only)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    w = ri.CONFIGS[args.config]
+    if args.mesh:
+        w = w.with_mesh(args.mesh)
+    metric = "DoFs/s per relaxation sweep (fp64)"
+    workload = (f"cfg{args.config}: {SPACE_NAME[w.space]}_{w.p} on {w.nx}x{w.ny}x{w.nz} hexes, "
+                f"{'perturbed trilinear' if w.perturb else 'axis-aligned'}, {w.decomposition.upper()} stars, "
+                f"{'exact Cholesky' if w.factorization == 'chol' else 'ICC-SC'}")
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        rate, cb = oracle_sweep_rate(w, args.config)
+        line = {"impl": "reference", "metric": metric, "value": rate, "unit": "DoFs/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["sec_per_sweep"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload + " (oracle on a bounded sample)", "sample": cb["sample"]},
+                "cpu_baseline": {"value": rate, "unit": "DoFs/s", "cores": cb["cores"], "kind": "oracle",
+                                 "sample": cb["sample"]},
+                "e2e": {"value": rate, "unit": "DoFs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2211_14284_b200 as rmb
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+
+    t0 = time.perf_counter()
+    coords = None if w.perturb == 0 else ri.vertex_coords(w)
+    ctx = rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(), w.gamma_d,
+                       coords=coords, decomposition=rmb.RM_PH if w.decomposition == "ph" else rmb.RM_PAFW,
+                       factorization=rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL,
+                       stream=stream.cuda_stream, device=torch.cuda.current_device())
+    setup_s = time.perf_counter() - t0
+    info = ctx.info()
+    n = ctx.n_local
+    mask = ctx.constrained_mask()
+    f = ri.uniform_vector(w.cfg, 0, n); f[mask] = 0
+    u = ri.uniform_vector(w.cfg, 3, n); u[mask] = 0
+    ft = torch.tensor(f, device=dev)
+    ut = torch.tensor(u, device=dev)
+    uo = torch.empty_like(ut)
+
+    for _ in range(args.warmup):
+        rmb.rm_relax(ctx, ft, ut, uo, 1.0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = Clocks(torch.cuda.current_device())
+    time.sleep(0.3)
+    rmb.rm_timing_enable(ctx, True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rmb.rm_relax(ctx, ft, ut, uo, 1.0)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    phase_ms, launches = rmb.rm_timing_read(ctx)
+    rmb.rm_timing_enable(ctx, False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nfree_all = info["n_free"] * world
+    value = nfree_all / (ms * 1e-3)
+
+    # roofline of the dominant kernel (patch solve, phase 1)
+    hbm, peak_kind = peaks()
+    ph1_ms_sweep = phase_ms[1] / args.steps
+    ph1_launch_sweep = launches[1] / args.steps
+    prim_bytes = info["factor_bytes"] + 3 * 8 * n   # factor values + r gather + u_out RMW
+    achieved = prim_bytes / (ph1_ms_sweep * 1e-3) / 1e9 if ph1_ms_sweep > 0 else 0.0
+    roof = {"kernel": "patch_solve_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+            "bytes_per_launch": prim_bytes / max(ph1_launch_sweep, 1),
+            "launch_ms_avg": ph1_ms_sweep / max(ph1_launch_sweep, 1),
+            "share_of_step": ph1_ms_sweep / ms if ms > 0 else None,
+            "phase_ms_per_step": [x / args.steps for x in phase_ms]}
+
+    e2e = None
+    if not args.no_e2e:
+        fh = torch.tensor(f).pin_memory()
+        uh = torch.tensor(u).pin_memory()
+        oh = torch.empty(n, dtype=torch.float64).pin_memory()
+        rmb.rm_relax_host(ctx, fh, uh, oh, 1.0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            rmb.rm_relax_host(ctx, fh, uh, oh, 1.0)
+        dt = (time.perf_counter() - t) / args.steps
+        if world > 1:
+            tt = torch.tensor([dt], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": nfree_all / dt, "unit": "DoFs/s", "h2d_bytes_per_step": 2 * 8 * n,
+               "d2h_bytes_per_step": 8 * n, "ms_per_step": dt * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cb = oracle_sweep_rate(w, args.config)
+        cpu = {"value": rate, "unit": "DoFs/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"]}
+
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (rm_inputs seeded recipe)",
+                "config": {"workload": workload, "free_dofs_per_gpu": info["n_free"], "dofs_per_gpu": n,
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "l2": "inputs larger than L2 (patch factors %.1f GB)" % (info["factor_bytes"] / 1e9),
+                           "setup_s": setup_s, "patches": info["n_patches"] + info["n_patches_potential"],
+                           "factor_blocks": info["n_factor_blocks"]},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "gpu_launches": int(sum(launches[:3]))}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

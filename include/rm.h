@@ -75,7 +75,7 @@ typedef struct {
   int32_t decomposition;     /* RM_PAFW | RM_PH (k = 0: identical)                                 */
   int32_t factorization;     /* RM_CHOL | RM_ICC_SC                                                 */
   int32_t patch_entities;    /* RM_ALL_ENTITIES | RM_INTERIOR_ONLY                                  */
-  double potential_shift;    /* eps_s for k = 2 PH (reading G8), default 1e-6                        */
+  double potential_shift;    /* eps_s for k = 2 PH (reading G8), default 1e-3                        */
   int32_t coarse;            /* must be 0 (p = 1 coarse level not built, reading G10)              */
   void *stream;              /* cudaStream_t                                                        */
   const void *nccl_id;       /* 128-byte ncclUniqueId or NULL (single GPU)                          */
@@ -121,6 +121,14 @@ rm_status rm_relax_host(rm_ctx *ctx, const double *f, const double *u_in, double
  * sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0). u: device, overwritten. */
 rm_status rm_pcg(rm_ctx *ctx, const double *f, double *u, double rtol, int32_t maxit,
                  int32_t *iters, double *rel_natural_residual);
+
+/* Phase timing (instrumentation used by bench.py).  While enabled, rm_relax / rm_precondition /
+ * rm_pcg record CUDA events on their stream around each phase: [0] residual (apply kernel),
+ * [1] primary patch solves (one launch per colour), [2] potential stage (D^T, patch solves, D),
+ * [3] everything else (copies, PCG vector kernels).  rm_timing_read synchronises and returns the
+ * accumulated milliseconds and kernel launches per phase since the last enable/read. */
+rm_status rm_timing_enable(rm_ctx *ctx, int32_t on);
+rm_status rm_timing_read(rm_ctx *ctx, double ms[4], int64_t launches[4]);
 
 void rm_destroy(rm_ctx *ctx);
 const char *rm_last_error(void);

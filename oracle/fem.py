@@ -407,17 +407,61 @@ def apply_matfree(space: Space, X, alpha, beta, u):
     return v
 
 
+def dof_coords(space: Space, g):
+    """(component, ix, iy, iz) of a global DoF index."""
+    off = space.offsets()
+    m = int(np.searchsorted(off, g, side="right") - 1)
+    Lz, Ly, Lx = space.comp_shape(m)
+    r = g - off[m]
+    return m, r % Lx, (r // Lx) % Ly, r // (Lx * Ly)
+
+
+def cells_containing(space: Space, g):
+    """Cells whose closure carries the basis function of DoF g (structured layout rule)."""
+    m, ix, iy, iz = dof_coords(space, g)
+    n = (space.nx, space.ny, space.nz)
+    per = []
+    for d, i in enumerate((ix, iy, iz)):
+        if space.fams[m][d] == D_FAM or i % space.p:
+            per.append([i // space.p])
+        else:
+            per.append([c for c in (i // space.p - 1, i // space.p) if 0 <= c < n[d]])
+    return [(cx, cy, cz) for cz in per[2] for cy in per[1] for cx in per[0]]
+
+
+def _cell_matrix(space, X, alpha, beta, cx, cy, cz):
+    Xc = cell_vertices(X, cx, cy, cz)
+    if is_axis_aligned(Xc):
+        h = Xc[1, 1, 1] - Xc[0, 0, 0]
+        M, K = _cartesian_parts(space.k, space.p, float(h[0]), float(h[1]), float(h[2]))
+        return beta[cz, cy, cx] * M + alpha[cz, cy, cx] * K
+    return element_matrix(space.k, space.p, Xc, alpha[cz, cy, cx], beta[cz, cy, cx])
+
+
+def local_matrix(space: Space, X, alpha, beta, g):
+    """A[g][:, g] assembled only from the cells carrying those DoFs (no global matrix)."""
+    g = np.asarray(g)
+    pos = {int(v): i for i, v in enumerate(g)}
+    cells = set()
+    for v in g:
+        cells.update(cells_containing(space, int(v)))
+    A = np.zeros((len(g), len(g)))
+    for (cx, cy, cz) in sorted(cells):
+        cd = space.cell_dofs(cx, cy, cz)
+        loc = np.array([pos.get(int(v), -1) for v in cd])
+        sel = np.flatnonzero(loc >= 0)
+        AK = _cell_matrix(space, X, alpha, beta, cx, cy, cz)
+        A[np.ix_(loc[sel], loc[sel])] += AK[np.ix_(sel, sel)]
+    return A
+
+
 def cell_rows_apply(space: Space, X, alpha, beta, u, rows):
     """(A u)[rows] computed only from the cells that contain those DoFs (sampled parity)."""
     rows = np.asarray(rows)
     out = np.zeros(len(rows))
     cells = set()
-    for cz in range(space.nz):
-        for cy in range(space.ny):
-            for cx in range(space.nx):
-                g = space.cell_dofs(cx, cy, cz)
-                if np.isin(rows, g).any():
-                    cells.add((cx, cy, cz))
+    for r in rows:
+        cells.update(cells_containing(space, int(r)))
     for (cx, cy, cz) in sorted(cells):
         g = space.cell_dofs(cx, cy, cz)
         Xc = cell_vertices(X, cx, cy, cz)

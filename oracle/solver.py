@@ -24,7 +24,7 @@ import scipy.sparse as sp
 from .fem import Space, assemble, assemble_aux, apply_matfree, global_derivative
 from .patches import DenseCholeskyPatch, ICCSCPatch, all_patches
 
-EPS_S = 1e-6   # reading G8
+EPS_S = 1e-3   # reading G8: eps_s = 1e-3 of the potential-space mass
 
 
 @dataclass
@@ -170,3 +170,42 @@ class Problem:
             pdir = z + (rz_new / rz) * pdir
             rz = rz_new
         return x, maxit, rel
+
+
+def sampled_relax(space: Space, X, alpha, beta, gamma_d, f, u, rows, omega=1.0):
+    """u_out[rows] of one PAFW exact-Cholesky sweep (k = 0), computed only from the star
+    patches that contain those rows, each assembled from its own cells (no global matrix):
+    for every patch i containing row g:  u_out[g] += omega * (A_i^{-1} R_i (f - A u))[g].
+    Used for full-size sampled parity (the same definitions as Problem.relax)."""
+    from .fem import cell_rows_apply, dof_coords, local_matrix
+    from .patches import patch_dofs
+    constrained = space.constrained_mask(gamma_d)
+    u = np.where(constrained, 0.0, u)
+    f = np.where(constrained, 0.0, f)
+    n = (space.nx, space.ny, space.nz)
+    out = u[np.asarray(rows)].copy()
+    cache = {}
+    for t, g in enumerate(rows):
+        if constrained[g]:
+            continue
+        _, ix, iy, iz = dof_coords(space, int(g))
+        cand = [[v for v in (i // space.p - 1, i // space.p, i // space.p + 1) if 0 <= v <= n[d]]
+                for d, i in enumerate((ix, iy, iz))]
+        for vz in cand[2]:
+            for vy in cand[1]:
+                for vx in cand[0]:
+                    ent = (("node", vx), ("node", vy), ("node", vz))
+                    if ent not in cache:
+                        gp, _ = patch_dofs(space, ent, constrained)
+                        cache[ent] = gp
+                    gp = cache[ent]
+                    where = np.flatnonzero(gp == g)
+                    if not len(where):
+                        continue
+                    key = ("x",) + ent
+                    if key not in cache:
+                        r = f[gp] - cell_rows_apply(space, X, alpha, beta, u, gp)
+                        Ai = local_matrix(space, X, alpha, beta, gp)
+                        cache[key] = DenseCholeskyPatch(Ai).solve(r)
+                    out[t] += omega * cache[key][where[0]]
+    return out

@@ -73,11 +73,13 @@ def _load():
     lib.rm_precondition.argtypes = [P, P, P]
     lib.rm_relax_host.argtypes = [P, P, P, P, D]
     lib.rm_pcg.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]
+    lib.rm_timing_enable.argtypes = [P, I32]
+    lib.rm_timing_read.argtypes = [P, ctypes.POINTER(D * 4), ctypes.POINTER(I64 * 4)]
     lib.rm_destroy.argtypes = [P]
     lib.rm_destroy.restype = None
     lib.rm_last_error.restype = ctypes.c_char_p
     for f in ("rm_setup", "rm_layout", "rm_info_get", "rm_constrained_mask", "rm_apply", "rm_residual",
-              "rm_relax", "rm_precondition", "rm_relax_host", "rm_pcg"):
+              "rm_relax", "rm_precondition", "rm_relax_host", "rm_pcg", "rm_timing_enable", "rm_timing_read"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -138,12 +140,14 @@ class RmContext:
 def _stream_ptr(stream):
     if stream is None:
         import torch
+        if not torch.cuda.is_available():
+            return 0      # rm_setup will report the missing device as RM_ECUDA
         return torch.cuda.current_stream().cuda_stream
     return int(stream)
 
 
 def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposition=RM_PAFW,
-             factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-6, stream=None,
+             factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-3, stream=None,
              device=0) -> RmContext:
     alpha = np.ascontiguousarray(np.atleast_1d(np.asarray(alpha, dtype=np.float64)).ravel())
     beta = np.ascontiguousarray(np.atleast_1d(np.asarray(beta, dtype=np.float64)).ravel())
@@ -207,6 +211,18 @@ def rm_pcg(ctx: RmContext, f, u, rtol=1e-8, maxit=500):
     st = _check(_lib.rm_pcg(ctx.h, ctx._vec(f, "f"), ctx._vec(u, "u"), float(rtol), int(maxit),
                             ctypes.byref(it), ctypes.byref(rel)))
     return it.value, rel.value, st == RM_OK
+
+
+def rm_timing_enable(ctx: RmContext, on=True):
+    _check(_lib.rm_timing_enable(ctx.h, 1 if on else 0))
+
+
+def rm_timing_read(ctx: RmContext):
+    """-> (ms[4], launches[4]) accumulated per phase: residual, primary patches, potential, other."""
+    ms = (ctypes.c_double * 4)()
+    nl = (ctypes.c_int64 * 4)()
+    _check(_lib.rm_timing_read(ctx.h, ctypes.byref(ms), ctypes.byref(nl)))
+    return list(ms), list(nl)
 
 
 def exported_symbols():

@@ -74,7 +74,7 @@ rm::DSliced to_dev(DevFamily& F, const rm::Sliced& s) {
 }
 
 void upload_family(DevFamily& F, const rm::PatchFamily& P) {
-  const int NW = 8;
+  const int NW = rm::RM_PATCH_CONSUMER_WARPS;
   std::vector<rm::DClass> hc(P.classes.size());
   size_t smem = 0;
   int maxT = 1;
@@ -100,7 +100,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     }
     d.vofs_final = C.vofs_final;
     if (C.final_kind == rm::FINAL_DENSE_INV) {
-      auxn = std::max(auxn, (size_t)C.m * (NW + 1));
+      auxn = std::max(auxn, (size_t)((C.m + 31) / 32) * 32 * (NW + 1));
       maxT = std::max(maxT, (C.m + 31) / 32);
     } else {
       d.icc_nlev = (int)C.icc_level_ptr.size() - 1;
@@ -111,7 +111,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
       d.icct_rowptr = F.upload(C.icct_rowptr); d.icct_col = F.upload(C.icct_col);
       d.icct_lptr = F.upload(C.icct_level_ptr); d.icct_lrows = F.upload(C.icct_level_rows);
     }
-    smem = std::max(smem, (C.n + auxn) * sizeof(double));
+    smem = std::max(smem, rm::patch_solve_smem_bytes(C.n, (int)auxn));
   }
   if (smem > 227 * 1024)
     throw RmError(RM_EINVAL, "patch too large for the shared-memory patch kernel (" + std::to_string(smem) + " bytes)");
@@ -171,6 +171,11 @@ struct rm_ctx {
   double *d_hf = nullptr, *d_hu = nullptr;
   std::vector<uint8_t> mask;
   double setup_seconds = 0.0;
+  // phase timing (rm_timing_enable / rm_timing_read)
+  bool timing = false;
+  struct Ev { int phase; cudaEvent_t a, b; };
+  std::vector<Ev> events;
+  int64_t launches[4] = {0, 0, 0, 0};
 
   double* dalloc(size_t n) {
     void* d = nullptr;
@@ -179,6 +184,7 @@ struct rm_ctx {
     return static_cast<double*>(d);
   }
   ~rm_ctx() {
+    for (auto& e : events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : allocs) cudaFree(p);
     prim.release();
     pot.release();
@@ -223,6 +229,16 @@ rm::OpParams make_op(const rm::Space& sp, uint32_t gamma) {
     }
     op.rowptr[m][M.rows] = (short)nz;
   }
+  if (sp.k == 0) {   // x-stiffness term: X = A-hat, Y = Z = B-hat
+    for (int t = 0; t < op.nterms; ++t) {
+      const rm::Term& T = co.terms[t];
+      if (T.coef == 0 && T.mat[0] != T.mat[1]) {
+        const rm::Mat1 &A = co.mats[T.mat[0]], &B = co.mats[T.mat[1]];
+        for (size_t i = 0; i < A.v.size(); ++i) { op.Ah[i] = A.v[i]; op.Bh[i] = B.v[i]; }
+        break;
+      }
+    }
+  }
   return op;
 }
 
@@ -239,7 +255,7 @@ void rm_default_options(rm_options* o) {
   o->decomposition = RM_PAFW;
   o->factorization = RM_CHOL;
   o->patch_entities = RM_ALL_ENTITIES;
-  o->potential_shift = 1e-6;
+  o->potential_shift = 1e-3;   // reading G8: roundoff of the sweep grows like eps/eps_s
   o->nranks = 1;
 }
 
@@ -421,26 +437,54 @@ rm_status rm_constrained_mask(const rm_ctx* c, uint8_t* mask) {
 
 namespace {
 
+// records CUDA events around a phase when timing is enabled
+struct Phase {
+  rm_ctx* c;
+  int ph;
+  cudaEvent_t a = nullptr;
+  Phase(rm_ctx* c_, int ph_) : c(c_), ph(ph_) {
+    if (!c->timing) return;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventRecord(a, c->st));
+  }
+  ~Phase() {
+    if (!a) return;
+    cudaEvent_t b;
+    if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, c->st) == cudaSuccess) c->events.push_back({ph, a, b});
+    else cudaEventDestroy(a);
+  }
+};
+
 void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
-  CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st));
+  Phase ph(c, 0);
+  int nl = 0;
+  CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl));
+  c->launches[0] += nl;
 }
 
-void run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
+int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
+  int nl = 0;
   for (size_t col = 0; col + 1 < F.color_start.size(); ++col) {
     const int a = F.color_start[col], b = F.color_start[col + 1];
     if (b <= a) continue;
     CK(rm::launch_patch_solve(F.d_classes, F.d_pclass + a, F.d_pbase + 3LL * a, F.d_pvals + a, F.d_vals, r, u, omega,
-                              b - a, F.maxT, F.smem, c->st));
+                              b - a, F.smem, c->st));
+    ++nl;
   }
+  return nl;
 }
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)
 void add_precond(rm_ctx* c, const double* r, double* u, double omega) {
-  run_family(c, c->prim, r, u, omega);
+  {
+    Phase ph(c, 1);
+    c->launches[1] += run_family(c, c->prim, r, u, omega);
+  }
   if (c->pot.present) {
+    Phase ph(c, 2);
     CK(rm::launch_hiptmair_DT(c->k, c->p, c->n, c->gamma, c->Dh.data(), r, c->d_t, c->st));
     CK(cudaMemsetAsync(c->d_s, 0, c->npot * sizeof(double), c->st));
-    run_family(c, c->pot, c->d_t, c->d_s, 1.0);
+    c->launches[2] += 2 + run_family(c, c->pot, c->d_t, c->d_s, 1.0);
     CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, u, omega, c->st));
   }
 }
@@ -557,6 +601,35 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
     if (rel) *rel = relv;
   });
   return s != RM_OK ? s : conv;
+}
+
+rm_status rm_timing_enable(rm_ctx* c, int32_t on) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->st));
+    for (auto& e : c->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+    c->events.clear();
+    for (auto& l : c->launches) l = 0;
+    c->timing = on != 0;
+  });
+}
+
+rm_status rm_timing_read(rm_ctx* c, double ms[4], int64_t launches[4]) {
+  return guarded(c, [&] {
+    CK(cudaStreamSynchronize(c->st));
+    double acc[4] = {0, 0, 0, 0};
+    for (auto& e : c->events) {
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, e.a, e.b));
+      acc[e.phase] += t;
+      cudaEventDestroy(e.a); cudaEventDestroy(e.b);
+    }
+    c->events.clear();
+    for (int i = 0; i < 4; ++i) {
+      if (ms) ms[i] = acc[i];
+      if (launches) launches[i] = c->launches[i];
+      c->launches[i] = 0;
+    }
+  });
 }
 
 void rm_destroy(rm_ctx* c) { delete c; }

@@ -21,6 +21,9 @@ struct OpParams {
   long long off[4];               // component offsets
   unsigned gamma_d;
   OpTerm terms[RM_MAXTERMS];
+  // k = 0: the two 1D matrices of the H(grad) operator, B-hat and A-hat = D-hat^T D-hat,
+  // (p+1)^2 row-major with structural zeros exact (used by the specialised apply_q kernel)
+  double Bh[RM_MAXP1 * RM_MAXP1], Ah[RM_MAXP1 * RM_MAXP1];
   short rowptr[RM_MAXMATS][RM_MAXP1 + 1];
   unsigned char col[RM_MAXMATS][RM_MAXMATNZ];
   double val[RM_MAXMATS][RM_MAXMATNZ];
@@ -50,10 +53,13 @@ struct DClass {
 // launchers (kernels.cu)
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
-                                   long long ndof, cudaStream_t st);
+                                   long long ndof, cudaStream_t st, int* nlaunch);
 cudaError_t launch_patch_solve(const DClass* classes, const int* pclass, const long long* pbase,
                                const long long* pvals, const double* vals, const double* r, double* u,
-                               double omega, int npatch, int maxT, size_t smem_bytes, cudaStream_t st);
+                               double omega, int npatch, size_t smem_bytes, cudaStream_t st);
+// dynamic shared memory of the patch kernel for a class with n DoFs and max_aux scratch doubles
+size_t patch_solve_smem_bytes(int n, int max_aux);
+constexpr int RM_PATCH_CONSUMER_WARPS = 8;
 cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -247,6 +249,14 @@ struct Builder {
     for (auto& a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
 
     // ---- symbolic elimination
+    // face orientation of group-1 DoFs (direction of the P index on a cell boundary), 3 otherwise
+    std::vector<int> orient(n, 3);
+    for (int i = 0; i < n; ++i) {
+      if (dofs[i].group != 1) continue;
+      const int idx[3] = {dofs[i].ix, dofs[i].iy, dofs[i].iz};
+      for (int d = 0; d < 3; ++d)
+        if (sp.fam[dofs[i].comp][d] == FAM_P && idx[d] % p == 0) orient[i] = d;
+    }
     std::vector<int> E0;
     for (int i = 0; i < n; ++i) if (dofs[i].group == 0) E0.push_back(i);
     std::vector<char> isE0(n, 0);
@@ -285,7 +295,7 @@ struct Builder {
     std::vector<char> alive(nG, 1);
     int nalive = nG;
     if (in.factorization == 0) {
-      while (nalive > 48) {
+      while (nalive > 16 && (int)Elev.size() < 5) {   // <= 6 levels incl. level 0 (kernel limit 8)
         std::vector<int> R, deg(nG, 0);
         for (int t = 0; t < nG; ++t) if (alive[t]) R.push_back(t);
         for (int t : R) {
@@ -293,19 +303,40 @@ struct Builder {
           for (int u : R) if (u != t && Sb[(size_t)t * nG + u]) ++d;
           deg[t] = d;
         }
-        std::vector<int> ord = R;
-        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return deg[a] < deg[b]; });
-        std::vector<char> blocked(nG, 0);
+        // candidate independent sets: greedy by degree, and greedy preferring each face
+        // orientation first (faces normal to one direction do not couple after the interior
+        // elimination on Cartesian stars); keep the cheapest
+        std::vector<int> ord;
         std::vector<int> pick;
-        for (int t : ord) {
-          if (blocked[t]) continue;
-          pick.push_back(t); blocked[t] = 1;
-          for (int u : R) if (Sb[(size_t)t * nG + u]) blocked[u] = 1;
+        int64_t best = -1;
+        const int64_t m = (int64_t)R.size();
+        for (int pref = -1; pref < 3; ++pref) {
+          ord = R;
+          std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+            int oa = (pref >= 0 && orient[G[a]] == pref) ? 0 : 1, ob = (pref >= 0 && orient[G[b]] == pref) ? 0 : 1;
+            if (oa != ob) return oa < ob;
+            return deg[a] < deg[b];
+          });
+          std::vector<char> blocked(nG, 0);
+          std::vector<int> cand;
+          for (int t : ord) {
+            if (blocked[t]) continue;
+            cand.push_back(t); blocked[t] = 1;
+            for (int u : R) if (Sb[(size_t)t * nG + u]) blocked[u] = 1;
+          }
+          int64_t nE = (int64_t)cand.size(), nnzW = 0;
+          for (int t : cand) nnzW += deg[t];
+          int64_t c = nE + 2 * nnzW + (m - nE) * (m - nE + 1) / 2;
+          if (best < 0 || c < best) { best = c; pick = cand; }
         }
-        int64_t m = (int64_t)R.size(), nE = (int64_t)pick.size(), nnzW = 0;
+        int64_t nE = (int64_t)pick.size(), nnzW = 0;
         for (int t : pick) nnzW += deg[t];
         int64_t oldc = m * (m + 1) / 2;
         int64_t newc = nE + 2 * nnzW + (m - nE) * (m - nE + 1) / 2;
+        if (getenv("RM_DEBUG_LEVELS"))
+          fprintf(stderr, "[levels] n=%d nG=%d m=%lld pick=%lld nnzW=%lld mindeg=%d maxdeg=%d old=%lld new=%lld\n", n, nG,
+                  (long long)m, (long long)nE, (long long)nnzW, deg[ord.front()], deg[ord.back()], (long long)oldc,
+                  (long long)newc);
         if (newc > (oldc * 97) / 100) break;
         std::sort(pick.begin(), pick.end());
         for (int t : pick) { alive[t] = 0; --nalive; }
@@ -426,10 +457,12 @@ struct Builder {
       }
       // final block
       C.m = n - start;
+      vofs = (vofs + 1) & ~int64_t(1);   // 16-byte alignment of the tile stream (TMA bulk copies)
       C.vofs_final = vofs;
       if (in.factorization == 0) {
         C.final_kind = FINAL_DENSE_INV;
-        vofs += (int64_t)C.m * (C.m + 1) / 2;
+        const int64_t T = (C.m + 31) / 32;
+        vofs += T * (T + 1) / 2 * 1024;
       } else {
         C.final_kind = FINAL_ICC;
         // ICC(0) on the Schur pattern of the final block (positions start..n-1, pinned order)
@@ -483,7 +516,7 @@ struct Builder {
         vofs += 2 * (int64_t)nnz;   // L values (row order) then L^T values (transpose order)
       }
     }
-    C.nvals = vofs;
+    C.nvals = (vofs + 1) & ~int64_t(1);   // keep every patch value block 16-byte aligned
   }
 
   // ---------------------------------------------------------------- numeric factorization
@@ -690,10 +723,9 @@ struct Builder {
           Li[(size_t)i * m + c] = -s / F[(size_t)i * m + i];
         }
       }
-      // inverse(i,j) = sum_{k >= max(i,j)} Li(k,i) Li(k,j); packed lower rows
-      double* o = out + C.vofs_final;
+      // inverse(i,j) = sum_{k >= max(i,j)} Li(k,i) Li(k,j)
       // transpose Li for contiguous access: LiT[i][k] = Li[k][i]
-      std::vector<double> LiT((size_t)m * m);
+      std::vector<double> LiT((size_t)m * m), Sinv((size_t)m * m);
       for (int i = 0; i < m; ++i) for (int k = 0; k < m; ++k) LiT[(size_t)i * m + k] = Li[(size_t)k * m + i];
       for (int i = 0; i < m; ++i)
         for (int j = 0; j <= i; ++j) {
@@ -701,7 +733,21 @@ struct Builder {
           const double* b = &LiT[(size_t)j * m];
           double s = 0;
           for (int k = i; k < m; ++k) s += a[k] * b[k];
-          o[(size_t)i * (i + 1) / 2 + j] = s;
+          Sinv[(size_t)i * m + j] = Sinv[(size_t)j * m + i] = s;
+        }
+      // 32x32 tiles of the lower block triangle, row-major over (I, J <= I), diagonal tiles full;
+      // inside a tile element (r, c) sits at r*32 + ((c + r) & 31) (bank-conflict-free rows and
+      // columns in shared memory after a TMA bulk copy)
+      double* o = out + C.vofs_final;
+      const int T = (m + 31) / 32;
+      for (int I = 0; I < T; ++I)
+        for (int J = 0; J <= I; ++J) {
+          double* tb = o + (size_t)(I * (I + 1) / 2 + J) * 1024;
+          for (int r = 0; r < 32; ++r)
+            for (int c = 0; c < 32; ++c) {
+              const int i = 32 * I + r, j = 32 * J + c;
+              tb[r * 32 + ((c + r) & 31)] = (i < m && j < m) ? Sinv[(size_t)i * m + j] : 0.0;
+            }
         }
     } else {
       // ICC(0) on the final pattern, up-looking rows (same definition as oracle/patches.py)

@@ -55,13 +55,18 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
       }
       const int m = C.m, f0 = n - m;
       if (C.final_kind == FINAL_DENSE_INV) {
-        std::vector<double> x(m, 0.0);
-        const double* S = V + C.vofs_final;
-        for (int i = 0; i < m; ++i)
-          for (int j = 0; j <= i; ++j) {
-            double s = S[(size_t)i * (i + 1) / 2 + j];
-            x[i] += s * v[f0 + j];
-            if (j < i) x[j] += s * v[f0 + i];
+        const int T = (m + 31) / 32;
+        std::vector<double> x(32 * T, 0.0), g(32 * T, 0.0);
+        for (int i = 0; i < m; ++i) g[i] = v[f0 + i];
+        for (int I = 0; I < T; ++I)
+          for (int J = 0; J <= I; ++J) {
+            const double* tb = V + C.vofs_final + (size_t)(I * (I + 1) / 2 + J) * 1024;
+            for (int r = 0; r < 32; ++r)
+              for (int c = 0; c < 32; ++c) {
+                const double s = tb[r * 32 + ((c + r) & 31)];
+                x[32 * I + r] += s * g[32 * J + c];
+                if (I != J) x[32 * J + c] += s * g[32 * I + r];
+              }
           }
         for (int i = 0; i < m; ++i) v[f0 + i] = x[i];
       } else {
