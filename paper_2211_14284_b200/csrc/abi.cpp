@@ -11,6 +11,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "basis.hpp"
@@ -35,14 +36,8 @@ struct RmError : std::runtime_error {
 
 struct DevFamily {
   std::vector<void*> allocs;
-  rm::DClass* d_classes = nullptr;
-  int* d_pclass = nullptr;
-  long long* d_pbase = nullptr;
-  long long* d_pvals = nullptr;
-  double* d_vals = nullptr;
+  rm::PatchLaunch launch{};
   std::vector<int> color_start;
-  size_t smem = 0;
-  int maxT = 1;
   int64_t npatch = 0, nfactors = 0, nclasses = 0;
   int64_t sweep_value_bytes = 0;   // sum over patches of value-block bytes
   double sigma_max = 0.0;
@@ -63,61 +58,59 @@ struct DevFamily {
   }
 };
 
-rm::DSliced to_dev(DevFamily& F, const rm::Sliced& s) {
-  rm::DSliced d{};
-  d.r0 = s.r0; d.nrows = s.nrows; d.nslices = (int)s.slice_w.size();
-  d.sw = F.upload(s.slice_w);
-  d.soff = F.upload(s.slice_off);
-  d.cols = F.upload(s.cols);
-  d.vofs = s.vofs;
-  return d;
-}
-
 void upload_family(DevFamily& F, const rm::PatchFamily& P) {
-  const int NW = rm::RM_PATCH_CONSUMER_WARPS;
+  const int NW = rm::RM_PATCH_TILE_WARPS;
   std::vector<rm::DClass> hc(P.classes.size());
-  size_t smem = 0;
-  int maxT = 1;
+  int n_max = 0, piv_max = 0, mem_max = 0, aux_max = 0, unit_max = 0;
   for (size_t c = 0; c < P.classes.size(); ++c) {
     const rm::ClassProgram& C = P.classes[c];
     rm::DClass& d = hc[c];
     std::memset(&d, 0, sizeof d);
     d.n = C.n; d.nlev = (int)C.lev.size(); d.m = C.m; d.final_kind = C.final_kind;
     if (d.nlev > RM_MAXLEV) throw RmError(RM_EINVAL, "too many elimination levels");
-    d.offs = F.upload(C.offs);
-    std::vector<unsigned char> comp(C.comp.begin(), C.comp.end());
-    d.comp = F.upload(comp);
-    size_t auxn = 0;
+    int auxn = 0;
     for (int l = 0; l < d.nlev; ++l) {
-      d.lev[l].e0 = C.lev[l].e0; d.lev[l].e1 = C.lev[l].e1;
-      d.lev[l].blk.nblk = C.lev[l].blk.nblk;
-      d.lev[l].blk.bs = C.lev[l].blk.bs;
-      d.lev[l].blk.mem = F.upload(C.lev[l].blk.mem);
-      d.lev[l].blk.vofs = C.lev[l].blk.vofs;
-      d.lev[l].w = to_dev(F, C.lev[l].w);
-      d.lev[l].wt = to_dev(F, C.lev[l].wt);
-      auxn = std::max(auxn, (size_t)(C.lev[l].e1 - C.lev[l].e0));
+      const rm::Level& L = C.lev[l];
+      rm::DLevel& dl = d.lev[l];
+      dl.e0 = L.e0; dl.e1 = L.e1;
+      dl.blk.nblk = L.blk.nblk;
+      dl.blk.bs = L.blk.bs;
+      dl.w.r0 = L.w.r0; dl.w.nrows = L.w.nrows;
+      dl.wt.r0 = L.wt.r0; dl.wt.nrows = L.wt.nrows;
+      dl.piv_b = C.piv_b[l]; dl.w_b = C.w_b[l]; dl.w_e = C.w_e[l]; dl.wt_b = C.wt_b[l]; dl.wt_e = C.wt_e[l];
+      dl.piv_per = C.piv_per[l]; dl.piv_ofs = C.piv_ofs[l]; dl.mem_ofs = C.mem_ofs[l];
     }
-    d.vofs_final = C.vofs_final;
+    std::vector<rm::DUnit> us(C.units.size());
+    for (size_t i = 0; i < us.size(); ++i) {
+      const rm::Unit& u = C.units[i];
+      const bool tile = (int)i >= C.tu0 && (int)i < C.tu1;
+      if (u.np > 0x7FFF || u.mbytes > 0xFFFF) throw RmError(RM_EINVAL, "transfer unit too large");
+      us[i] = rm::DUnit{u.mofs, (int)((uint32_t)u.mbytes | ((uint32_t)u.np << 16) | (tile ? 0x80000000u : 0u)), u.sofs, u.nd};
+      unit_max = std::max(unit_max, u.mbytes + 8 * u.nd);
+    }
+    d.codes = F.upload(C.codes);
+    d.units = F.upload(us);
+    d.meta = F.upload(C.meta);
+    d.nunits = (int)us.size();
+    d.ngs = C.ngs;
+    d.tile_p0 = C.tile_p0; d.tile_p1 = C.tile_p1;
     if (C.final_kind == rm::FINAL_DENSE_INV) {
-      auxn = std::max(auxn, (size_t)((C.m + 31) / 32) * 32 * (NW + 1));
-      maxT = std::max(maxT, (C.m + 31) / 32);
+      if ((C.m + 31) / 32 > 32) throw RmError(RM_EINVAL, "final Schur block larger than 1024");
+      auxn = std::max(auxn, ((C.m + 31) / 32) * 32 * (NW + 1));   // g + per-tile-warp partials
     } else {
-      d.icc_nlev = (int)C.icc_level_ptr.size() - 1;
-      d.icct_nlev = (int)C.icct_level_ptr.size() - 1;
-      d.icc_nnz = C.icc_rowptr.empty() ? 0 : C.icc_rowptr.back();
-      d.icc_rowptr = F.upload(C.icc_rowptr); d.icc_col = F.upload(C.icc_col);
-      d.icc_lptr = F.upload(C.icc_level_ptr); d.icc_lrows = F.upload(C.icc_level_rows);
-      d.icct_rowptr = F.upload(C.icct_rowptr); d.icct_col = F.upload(C.icct_col);
-      d.icct_lptr = F.upload(C.icct_level_ptr); d.icct_lrows = F.upload(C.icct_level_rows);
+      d.iccf_nlev = (int)C.iccf_lpiece.size() - 1;
+      d.iccb_nlev = (int)C.iccb_lpiece.size() - 1;
+      d.iccf_lp = F.upload(C.iccf_lpiece);
+      d.iccb_lp = F.upload(C.iccb_lpiece);
     }
-    smem = std::max(smem, rm::patch_solve_smem_bytes(C.n, (int)auxn));
+    n_max = std::max(n_max, C.n);
+    piv_max = std::max(piv_max, C.piv_total);
+    mem_max = std::max(mem_max, C.mem_total);
+    aux_max = std::max(aux_max, (auxn + 1) & ~1);
   }
-  if (smem > 227 * 1024)
-    throw RmError(RM_EINVAL, "patch too large for the shared-memory patch kernel (" + std::to_string(smem) + " bytes)");
-  if (maxT > 32) throw RmError(RM_EINVAL, "final Schur block larger than 1024");
-  F.smem = smem; F.maxT = maxT;
-  F.d_classes = F.upload(hc);
+  if (P.ncolors > rm::RM_MAXCOLORS) throw RmError(RM_EINVAL, "too many colours");
+  rm::PatchLaunch& Lh = F.launch;
+  Lh.classes = F.upload(hc);
   // patches sorted by colour
   const size_t np = P.pclass.size();
   std::vector<size_t> order(np);
@@ -136,10 +129,59 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     pv[i] = P.pvals[t];
     bytes += P.classes[P.pclass[t]].nvals * 8;
   }
-  F.d_pclass = F.upload(pc);
-  F.d_pbase = F.upload(pb);
-  F.d_pvals = F.upload(pv);
-  F.d_vals = F.upload(P.values);
+  Lh.pclass = F.upload(pc);
+  Lh.pbase = F.upload(pb);
+  Lh.npatch = (int)np;
+  Lh.cs.ncolors = P.ncolors;
+  for (int c = 0; c <= P.ncolors; ++c) Lh.cs.start[c] = F.color_start[c];
+  Lh.done = F.upload(std::vector<unsigned>(1, 0u));
+  Lh.n_max = n_max; Lh.piv_max = piv_max; Lh.mem_max = mem_max; Lh.aux_max = aux_max;
+  Lh.unit_bytes_max = unit_max;
+  if (np > 0) {
+    cudaError_t e = rm::plan_patch_solve(Lh);
+    if (e != cudaSuccess)
+      throw RmError(RM_EINVAL, "patch too large for the shared-memory patch kernel (fixed " +
+                                   std::to_string(Lh.smem_fixed) + " bytes): " + cudaGetErrorString(e));
+  }
+  // HBM layout of the value blocks: CTA b of the persistent grid takes patches b, b + grid, ...
+  // (colour-sorted); distinct blocks are placed in that consumption order so that every CTA
+  // streams one contiguous region (scattered blocks cost ~35% of the stream rate: TLB reach).
+  {
+    const int G = std::max(1, Lh.grid);
+    std::unordered_map<long long, long long> remap;
+    remap.reserve(2 * P.nfactors + 16);
+    std::vector<long long> pvn(np);
+    void* dv = nullptr;
+    if (!P.values.empty()) {
+      if (cudaMalloc(&dv, P.values.size() * sizeof(double)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed (patch factors)");
+      F.allocs.push_back(dv);
+    }
+    double* dvals = static_cast<double*>(dv);
+    std::vector<double> stage;
+    const size_t chunk = (size_t)32 << 20;   // doubles per staging flush (256 MB)
+    long long cur = 0, flushed = 0;
+    auto flush = [&]() {
+      if (stage.empty()) return;
+      CK(cudaMemcpy(dvals + flushed, stage.data(), stage.size() * sizeof(double), cudaMemcpyHostToDevice));
+      flushed += (long long)stage.size();
+      stage.clear();
+    };
+    for (int b = 0; b < G; ++b)
+      for (size_t q = (size_t)b; q < np; q += (size_t)G) {
+        auto it = remap.find(pv[q]);
+        if (it == remap.end()) {
+          const long long nv = P.classes[pc[q]].nvals;
+          it = remap.emplace(pv[q], cur).first;
+          stage.insert(stage.end(), P.values.begin() + pv[q], P.values.begin() + pv[q] + nv);
+          cur += nv;
+          if (stage.size() >= chunk) flush();
+        }
+        pvn[q] = it->second;
+      }
+    flush();
+    Lh.pvals = F.upload(pvn);
+    Lh.vals = dvals;
+  }
   F.npatch = (int64_t)np;
   F.nfactors = P.nfactors;
   F.nclasses = (int64_t)P.classes.size();
@@ -463,15 +505,9 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
 }
 
 int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
-  int nl = 0;
-  for (size_t col = 0; col + 1 < F.color_start.size(); ++col) {
-    const int a = F.color_start[col], b = F.color_start[col + 1];
-    if (b <= a) continue;
-    CK(rm::launch_patch_solve(F.d_classes, F.d_pclass + a, F.d_pbase + 3LL * a, F.d_pvals + a, F.d_vals, r, u, omega,
-                              b - a, F.smem, c->st));
-    ++nl;
-  }
-  return nl;
+  if (F.npatch == 0) return 0;
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st));
+  return 1;
 }
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)

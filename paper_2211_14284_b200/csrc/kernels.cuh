@@ -30,36 +30,59 @@ struct OpParams {
 };
 
 // ---------------------------------------------------------------- patch programs
-struct DSliced {
-  int r0, nrows, nslices, pad;
-  const int* sw;
-  const int* soff;
-  const uint16_t* cols;
-  long long vofs;
+// (host counterparts and the stream layout: patches.hpp)
+// producer's view of a transfer unit: meta bytes [mofs, mofs + (mb_np & 0xFFFF)) of the class
+// meta stream, values [sofs, sofs + nd) of the patch value block, np = (mb_np >> 16) & 0x7FFF
+// pieces, channel = bit 31 (1 = dense-tile channel)
+struct DUnit { int mofs, mb_np, sofs, nd; };
+struct DSliced { int r0, nrows; };
+struct DBlocks { int nblk, bs; };
+struct DLevel {
+  int e0, e1;
+  DBlocks blk;
+  DSliced w, wt;
+  int piv_b, w_b, w_e, wt_b, wt_e, piv_per, piv_ofs, mem_ofs;
 };
-struct DBlocks { int nblk, bs; const uint16_t* mem; long long vofs; };
-struct DLevel { int e0, e1; DBlocks blk; DSliced w, wt; };
+// Per class: the elimination program's shape (levels, piece ranges); every per-DoF / per-entry
+// index travels in the pieces' metadata blocks (class meta stream), not here.
 struct DClass {
   int n, nlev, m, final_kind;
-  const int* offs;
-  const unsigned char* comp;
   DLevel lev[RM_MAXLEV];
-  long long vofs_final;
-  int icc_nlev, icct_nlev, icc_nnz, pad;
-  const int *icc_rowptr, *icc_col, *icc_lptr, *icc_lrows;
-  const int *icct_rowptr, *icct_col, *icct_lptr, *icct_lrows;
+  const DUnit* units;
+  const unsigned char* meta;     // class meta stream (L2-resident)
+  const int* codes;              // per position: (offs << 2) | comp, gather / scatter
+  int nunits, ngs, tile_p0, tile_p1, iccf_nlev, iccb_nlev;
+  const int *iccf_lp, *iccb_lp;  // per ICC level: first piece (size nlev + 1)
 };
+constexpr int RM_MAXCOLORS = 12;
+struct ColorStarts { int ncolors; int start[RM_MAXCOLORS + 1]; };
 
 // launchers (kernels.cu)
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch);
-cudaError_t launch_patch_solve(const DClass* classes, const int* pclass, const long long* pbase,
-                               const long long* pvals, const double* vals, const double* r, double* u,
-                               double omega, int npatch, size_t smem_bytes, cudaStream_t st);
-// dynamic shared memory of the patch kernel for a class with n DoFs and max_aux scratch doubles
-size_t patch_solve_smem_bytes(int n, int max_aux);
+// Persistent streaming patch solve over one family: patches sorted by colour, CTA b takes
+// patches b, b + grid, ...; scatters wait for the previous colours through *done (zeroed here).
+struct PatchLaunch {
+  const DClass* classes;
+  const int* pclass;
+  const long long* pbase;
+  const long long* pvals;
+  const double* vals;
+  int npatch;
+  ColorStarts cs;
+  unsigned* done;        // scattered patches (zeroed per launch)
+  int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
+  size_t smem_fixed;     // barriers + v + pivots + aux (bytes)
+  int ring_bytes;
+  int grid;
+  int unit_bytes_max;    // largest transfer unit (meta + values)
+};
+cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st);
+// shared-memory plan: fixed part for the largest class, then the ring; returns the grid size
+cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;
+constexpr int RM_PATCH_TILE_WARPS = 4;   // consumer warps sharing the dense tiles
 cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,

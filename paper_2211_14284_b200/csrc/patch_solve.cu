@@ -1,25 +1,57 @@
-// Batched star-patch solve: one CTA per patch of one colour.
+// Batched star-patch solve as ONE persistent streaming kernel
+// per patch family and sweep.
 //
-//   gather   v = R_i r                                   (P:949-959; structured offsets per class)
-//   forward  per elimination level: y_E = L_E^{-1} v_E (pivot blocks <= 3x3),  v_R -= M y_E
-//   final    x_F = S_F^{-1} v_F, S_F^{-1} stored as 32x32 tiles of the lower block triangle and
-//            streamed HBM -> shared memory by a producer warp with TMA bulk copies
-//            (cp.async.bulk + mbarrier ring); consumer warps do the symmetric tile GEMV
-//            (row sums and transposed column sums, bank-conflict-free by the stored swizzle)
-//            -- or, for ICC-SC, level-scheduled sparse triangular solves
-//   backward per level in reverse: x_E = L_E^{-T}(y_E - M^T x_R)
-//   scatter  u += omega R_i^T x                          (patches of a colour are disjoint)
-// The elimination is the Cholesky factorization of the patch matrix with the eliminated sets
-// first (exact for the Cholesky family), so x = A_i^{-1} R_i r up to rounding.
+// Per patch i:
+//   gather   v = R_i r                                   (structured offsets per class)
+//   forward  per elimination level: y^_E = P_EE^{-1} v_E (pivot blocks <= 3x3, Cholesky form),
+//            v_R -= P_RE y^_E
+//   final    x_F = S_F^{-1} v_F  (S_F^{-1} as 32x32 tiles of the lower block triangle, symmetric
+//            tile GEMV) -- or, for ICC-SC, level-scheduled triangular solves
+//   backward per level in reverse: x_E = y^_E - (P_EE^{-1} P_ER) x_R
+//   scatter  u += omega R_i^T x
+// This is block Gaussian elimination of the patch matrix with the eliminated sets first (exact
+// for the Cholesky family), so x = A_i^{-1} R_i r up to rounding.
+//
+// B200 structure.  Every factor value is read exactly once per sweep, so the kernel is an HBM
+// stream.  Each patch value block is laid out in consumption order (patches.hpp); consecutive
+// pieces form transfer units of <= 32 KB.  One producer warp per CTA streams the units of ALL
+// the CTA's patches HBM -> shared memory with cp.async.bulk (TMA bulk copies, SASS UBLKCP) into a
+// variable-size ring; it only waits for ring space, so the HBM stream stays busy across patches.
+// Two channels share the ring: the main channel (consumed by all 8 consumer warps) and the tile
+// channel (the dense-tile units, consumed by the 4 tile warps only).  While the tile warps
+// stream the tiles of patch i, the other 4 warps scatter patch i-1 and gather patch i+1 (second
+// v buffer), so the latency-bound global gathers/scatters and the colour wait leave the
+// critical path.
+//
+// Colours.  Patches of one colour are disjoint, so their scatters commute; patches are sorted
+// by colour and a colour-c patch is scattered only after every patch of colours < c has been
+// scattered (a device counter, acquire/release).  Each u entry therefore receives its updates in
+// colour order: the sweep is bitwise deterministic, with one launch instead of one per colour.
+// All CTAs are co-resident (grid = occupancy x SMs) and take patches in increasing order (CTA b:
+// b, b + grid, ...), scattering each before the next-but-one; the wait cannot deadlock (the
+// pending scatter of lowest colour never waits; induction on the colour).  The value blocks are
+// laid out in HBM in that per-CTA order (abi.cpp), so every CTA streams one contiguous region.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace rm {
 
 namespace {
 
-constexpr int NC = 8;        // consumer warps
-constexpr int NS = 4;        // TMA ring stages (8 KB each)
-constexpr int NTHR = (NC + 1) * 32;
+constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // consumer warps
+constexpr int NT = NC * 32;
+constexpr int NTHR = NT + 32;                  // + producer warp
+constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps (the others do the side work)
+constexpr int NSW = NC - NTW;                  // side-work warps
+constexpr int NDESC = 16;                      // in-flight transfer units per channel
+constexpr int GB = 8;                          // gather/scatter loads in flight per thread
+// shared-memory header: per channel full/empty mbarriers and slot tables (offset, pieces, meta)
+constexpr int HDR_BYTES = 2 * (2 * NDESC * 8 + 3 * NDESC * 4);   // 896
+constexpr int BAR_BYTES = (HDR_BYTES + 127) & ~127;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
@@ -45,260 +77,546 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
-// barrier among the consumer warps only (the producer warp never joins)
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory"); }
+// named barriers: 1 = all consumer warps, 2 = tile warps, 3 = side-work warps
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+__device__ __forceinline__ void tsync() { asm volatile("bar.sync 2, %0;" ::"n"(NTW * 32) : "memory"); }
+__device__ __forceinline__ void ssync() { asm volatile("bar.sync 3, %0;" ::"n"(NSW * 32) : "memory"); }
 
-__device__ __forceinline__ double warp_sum(double x) {
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// shared-memory view of one channel
+struct ChanSm {
+  uint64_t* full;
+  uint64_t* empty;
+  int* ofs;
+  int* np;
+  int* mb;
+};
+__device__ __forceinline__ ChanSm chan_sm(unsigned char* smraw, int ch) {
+  unsigned char* b = smraw + ch * (HDR_BYTES / 2);
+  ChanSm c;
+  c.full = reinterpret_cast<uint64_t*>(b);
+  c.empty = c.full + NDESC;
+  c.ofs = reinterpret_cast<int*>(c.empty + NDESC);
+  c.np = c.ofs + NDESC;
+  c.mb = c.np + NDESC;
+  return c;
+}
+
+// Ring placement (producer only): units at increasing virtual byte offsets, never straddling
+// the end of the ring.
+__device__ __forceinline__ uint32_t ring_place(uint32_t& H, uint32_t nbytes, uint32_t cap) {
+  const uint32_t off = H % cap;
+  if (off + nbytes > cap) H += cap - off;
+  const uint32_t vs = H;
+  H += nbytes;
+  return vs;
+}
+
+struct Piece_ { const unsigned char* pb; const double* val; };
+
+// Consumer side of one channel: unit j sits in slot j % NDESC; inside a unit the pieces are
+// walked with a meta cursor and a value cursor (header word 3 = meta bytes | values << 16).
+struct Consumer {
+  ChanSm c;
+  const unsigned char* ring;
+  int j, left;
+  const unsigned char* mcur;
+  const unsigned char* vcur;
+  __device__ __forceinline__ Piece_ acquire() {
+    if (left == 0) {
+      const int d = j % NDESC;
+      mbar_wait(&c.full[d], (uint32_t)(j / NDESC) & 1u);
+      mcur = ring + c.ofs[d];
+      vcur = mcur + c.mb[d];
+      left = c.np[d];
+    }
+    return Piece_{mcur, reinterpret_cast<const double*>(vcur)};
+  }
+  // done with the current piece; the unit is released after its last piece
+  __device__ __forceinline__ void release(int lane) {
+    const uint32_t w3 = reinterpret_cast<const uint32_t*>(mcur)[3];
+    mcur += w3 & 0xFFFFu;
+    vcur += (size_t)(w3 >> 16) * 8u;
+    if (--left == 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[j % NDESC]);
+      ++j;
+    }
+  }
+};
+
+struct Hdr { int a0, a1, e0, mbytes; };
+__device__ __forceinline__ Hdr hdr(const unsigned char* pb) {
+  const int4 h = *reinterpret_cast<const int4*>(pb);
+  return Hdr{h.x, h.y, h.z, h.w & 0xFFFF};
+}
+
+// one sliced-ELL piece: slice s is owned by warp s % NC (so split slices stay in one warp);
+// meta = per slice (start/32 | count << 16), then uint16 columns of the piece's elements
+template <class Emit>
+__device__ __forceinline__ void sliced_piece(Piece_ pc, const double* v, int nrows, int warp, int lane, Emit&& emit) {
+  const Hdr h = hdr(pc.pb);
+  const int nsl = h.a1 - h.a0;
+  const uint32_t* si = reinterpret_cast<const uint32_t*>(pc.pb + 16);
+  const uint16_t* cols = reinterpret_cast<const uint16_t*>(si + nsl);
+  const double* val = pc.val;
+  for (int ls = (warp - h.a0 % NC + NC) % NC; ls < nsl; ls += NC) {
+    const uint32_t info = si[ls];
+    const int st = 32 * (int)(info & 0xFFFFu) + lane, cnt = (int)(info >> 16);
+    double acc = 0.0;
+    int kk = 0;
+    for (; kk + 4 <= cnt; kk += 4) {
+      const int e = st + kk * 32;
+      acc += val[e] * v[cols[e]] + val[e + 32] * v[cols[e + 32]] + val[e + 64] * v[cols[e + 64]] +
+             val[e + 96] * v[cols[e + 96]];
+    }
+    for (; kk < cnt; ++kk) {
+      const int e = st + kk * 32;
+      acc += val[e] * v[cols[e]];
+    }
+    const int row = (h.a0 + ls) * 32 + lane;
+    if (row < nrows) emit(row, acc);
+  }
+}
+
+// One 32x32 tile of the final block's inverse (lane-block layout, patches.hpp):
+//   x_I += S g_J (row sums) and x_J += S^T g_I (column sums); for a diagonal tile (I == J) the
+//   stored L' (strictly lower + half diagonal) gives S g = L' g + L'^T g with the same two sums.
+// Lane (a, b) = (lane >> 2, lane & 3) accumulates 4 row partials and 8 column partials; two
+// shuffle reduce-scatters leave row 4a + b and column 8b + a in lane (a, b).
+__device__ __forceinline__ void tile_gemv(const double* __restrict__ tile, const double* __restrict__ g,
+                                          double* __restrict__ part, int I, int J, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int a = lane >> 2, b = lane & 3;
+  const bool diag = (I == J);
+  const bool active = !diag || b <= (a >> 1);
+  const int slot = diag ? a + (a >> 1) * ((a - 1) >> 1) + b : lane;
+  const int stride = diag ? 20 : 32;
+  double ra0 = 0.0, ra1 = 0.0, ra2 = 0.0, ra3 = 0.0;
+  double ca[8];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
+  for (int q = 0; q < 8; ++q) ca[q] = 0.0;
+  if (active) {
+    const double2* T = reinterpret_cast<const double2*>(tile) + slot;
+    const double2* gJ2 = reinterpret_cast<const double2*>(g + 32 * J + 8 * b);
+    const double* gI = g + 32 * I + 4 * a;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {   // row 4a + i: four steps (8 columns), loads issued together
+      double2 t[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) t[q] = T[(4 * i + q) * stride];
+      const double gi = gI[i];
+      double& ra = (i == 0) ? ra0 : (i == 1) ? ra1 : (i == 2) ? ra2 : ra3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 gj = gJ2[q];   // broadcast within the 8 lanes of equal b
+        ra = fma(t[q].x, gj.x, ra);
+        ra = fma(t[q].y, gj.y, ra);
+        ca[2 * q] = fma(t[q].x, gi, ca[2 * q]);
+        ca[2 * q + 1] = fma(t[q].y, gi, ca[2 * q + 1]);
+      }
+    }
+  }
+  // rows: reduce-scatter 4 values over the 4 lanes b = 0..3 (lane bits 0, 1)
+  double rowsum;
+  {
+    const bool hi = (b & 2) != 0;
+    double k0 = hi ? ra2 : ra0, k1 = hi ? ra3 : ra1;
+    const double s0 = hi ? ra0 : ra2, s1 = hi ? ra1 : ra3;
+    k0 += __shfl_xor_sync(FULL, s0, 2);
+    k1 += __shfl_xor_sync(FULL, s1, 2);
+    const bool h1 = (b & 1) != 0;
+    rowsum = (h1 ? k1 : k0) + __shfl_xor_sync(FULL, h1 ? k0 : k1, 1);
+  }
+  // columns: reduce-scatter 8 values over the 8 lanes a = 0..7 (lane bits 2, 3, 4)
+  double colsum;
+  {
+    const bool h4 = (a & 4) != 0;
+    double k4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double keep = h4 ? ca[4 + q] : ca[q], send = h4 ? ca[q] : ca[4 + q];
+      k4[q] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+    const bool h2 = (a & 2) != 0;
+    double k2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double keep = h2 ? k4[2 + q] : k4[q], send = h2 ? k4[q] : k4[2 + q];
+      k2[q] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    const bool h1 = (a & 1) != 0;
+    colsum = (h1 ? k2[1] : k2[0]) + __shfl_xor_sync(FULL, h1 ? k2[0] : k2[1], 4);
+  }
+  part[32 * I + 4 * a + b] += rowsum;
+  part[32 * J + 8 * b + a] += colsum;
+}
+
+// global index of gather code c for a patch with component bases b0, b1, b2
+__device__ __forceinline__ long long gidx(int c, long long b0, long long b1, long long b2) {
+  const int m = c & 3;
+  return (m == 0 ? b0 : (m == 1 ? b1 : b2)) + (c >> 2);
+}
+
+__device__ __forceinline__ int color_of(int q, const ColorStarts& cs) {
+  int col = 0;
+  while (col + 1 < cs.ncolors && cs.start[col + 1] <= q) ++col;
+  return col;
+}
+
+struct Shared {
+  const DClass* classes;
+  const int* pclass;
+  const long long* pbase;
+  const double* r;
+  double* u;
+  double omega;
+  unsigned* done;
+};
+
+// v = R_q r  (threads t = 0..nth-1 of a group, GB loads in flight per thread)
+__device__ __forceinline__ void gather_patch(const Shared& S, int q, double* v, int t, int nth) {
+  const DClass& C = S.classes[S.pclass[q]];
+  const int n = C.n;
+  const int* codes = C.codes;
+  const long long b0 = S.pbase[3 * q], b1 = S.pbase[3 * q + 1], b2 = S.pbase[3 * q + 2];
+  for (int k0 = t; k0 < n; k0 += GB * nth) {
+    double x[GB];
+#pragma unroll
+    for (int k = 0; k < GB; ++k) {
+      const int kk = k0 + k * nth;
+      if (kk < n) x[k] = __ldg(S.r + gidx(__ldg(codes + kk), b0, b1, b2));
+    }
+#pragma unroll
+    for (int k = 0; k < GB; ++k) {
+      const int kk = k0 + k * nth;
+      if (kk < n) v[kk] = x[k];
+    }
+  }
+}
+
+// u += omega R_q^T v after the colours below q's are complete; `sync` is the group's barrier
+template <class Sync>
+__device__ __forceinline__ void scatter_patch(const Shared& S, const ColorStarts& cs, int q, const double* v, int t,
+                                              int nth, Sync&& sync) {
+  const DClass& C = S.classes[S.pclass[q]];
+  const int n = C.n;
+  const int* codes = C.codes;
+  const long long b0 = S.pbase[3 * q], b1 = S.pbase[3 * q + 1], b2 = S.pbase[3 * q + 2];
+  const int col = color_of(q, cs);
+  if (t == 0 && col > 0) {
+    const unsigned need = (unsigned)cs.start[col];
+    while (ld_acquire(S.done) < need) __nanosleep(64);
+  }
+  sync();
+  for (int k0 = t; k0 < n; k0 += GB * nth) {
+    double x[GB];
+#pragma unroll
+    for (int k = 0; k < GB; ++k) {
+      const int kk = k0 + k * nth;
+      if (kk < n) x[k] = __ldcg(S.u + gidx(__ldg(codes + kk), b0, b1, b2));
+    }
+#pragma unroll
+    for (int k = 0; k < GB; ++k) {
+      const int kk = k0 + k * nth;
+      if (kk < n) __stcg(S.u + gidx(__ldg(codes + kk), b0, b1, b2), x[k] + S.omega * v[kk]);
+    }
+  }
+  sync();
+  if (t == 0) {
+    __threadfence();
+    atomicAdd(S.done, 1u);
+  }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(NTHR) patch_solve_kernel(const DClass* __restrict__ classes,
-                                                           const int* __restrict__ pclass,
-                                                           const long long* __restrict__ pbase,
-                                                           const long long* __restrict__ pvals,
-                                                           const double* __restrict__ vals,
-                                                           const double* __restrict__ r, double* __restrict__ u,
-                                                           double omega) {
+__global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __restrict__ classes,
+                                                               const int* __restrict__ pclass,
+                                                               const long long* __restrict__ pbase,
+                                                               const long long* __restrict__ pvals,
+                                                               const double* __restrict__ vals,
+                                                               const double* __restrict__ r, double* __restrict__ u,
+                                                               double omega, int npatch, ColorStarts cs,
+                                                               unsigned* __restrict__ done, uint32_t cap, int n_max) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
-  uint64_t* empty = full + NS;
-  double* ring = reinterpret_cast<double*>(smraw + 128);
+  unsigned char* ring = smraw + BAR_BYTES;
+  double* vbuf0 = reinterpret_cast<double*>(ring + cap);
+  double* vbuf1 = vbuf0 + ((n_max + 1) & ~1);
+  double* aux = vbuf1 + ((n_max + 1) & ~1);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int pi = blockIdx.x;
-  const DClass& C = classes[pclass[pi]];
-  const int n = C.n;
-  const double* V = vals + pvals[pi];
-  const int m = C.m, f0 = n - m;
-  const int T = (m + 31) >> 5;
-  const int ntiles = (C.final_kind == 0) ? T * (T + 1) / 2 : 0;
+  const int G = gridDim.x;
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NC); }
+    for (int ch = 0; ch < 2; ++ch) {
+      ChanSm c = chan_sm(smraw, ch);
+      for (int s = 0; s < NDESC; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], ch == 0 ? NC : NTW); }
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // ------------------------------------------------------------------ producer warp
+  // ================================================================== producer warp
   if (warp == NC) {
-    if (lane == 0) {
-      const double* tiles = V + C.vofs_final;
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % NS;
-        if (t >= NS) mbar_wait(&empty[s], ((t / NS) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], 8192u);
-        bulk_g2s(ring + s * 1024, tiles + (size_t)t * 1024, 8192u, &full[s]);
+    ChanSm cm[2] = {chan_sm(smraw, 0), chan_sm(smraw, 1)};
+    uint32_t H = 0;
+    int jc[2] = {0, 0}, relc[2] = {0, 0};
+    // in-flight units in allocation order (channel, per-channel sequence, virtual start)
+    int fch[2 * NDESC], fseq[2 * NDESC];
+    uint32_t fvs[2 * NDESC];
+    int fh = 0, ft = 0;
+    for (int q = blockIdx.x; q < npatch; q += G) {   // static schedule; value blocks laid out per CTA
+      const DClass& C = classes[pclass[q]];
+      const double* V = vals + pvals[q];
+      const DUnit* U = C.units;
+      const unsigned char* M = C.meta;
+      const int nu = C.nunits;
+      for (int i0 = 0; i0 < nu; i0 += 32) {
+        int4 d = make_int4(0, 0, 0, 0);
+        if (i0 + lane < nu) d = *reinterpret_cast<const int4*>(U + i0 + lane);
+        const int kn = min(32, nu - i0);
+        for (int k = 0; k < kn; ++k) {
+          const int mofs = __shfl_sync(0xffffffffu, d.x, k), mbnp = __shfl_sync(0xffffffffu, d.y, k);
+          const int sofs = __shfl_sync(0xffffffffu, d.z, k), nd = __shfl_sync(0xffffffffu, d.w, k);
+          if (lane == 0) {
+            const int ch = (int)(((uint32_t)mbnp >> 31) & 1u);
+            const uint32_t mb = (uint32_t)mbnp & 0xFFFFu;
+            const uint32_t vb = (uint32_t)nd * 8u, tot = mb + vb;
+            const uint32_t vs = ring_place(H, tot, cap);
+            // room: this channel's slot must be free and [vs, H) must not overlap unreleased units
+            while (ft > fh && (jc[ch] - relc[ch] >= NDESC || H - fvs[fh % (2 * NDESC)] > cap)) {
+              const int oc = fch[fh % (2 * NDESC)], os = fseq[fh % (2 * NDESC)];
+              mbar_wait(&cm[oc].empty[os % NDESC], (uint32_t)(os / NDESC) & 1u);
+              ++relc[oc];
+              ++fh;
+            }
+            const int sl = jc[ch] % NDESC;
+            ChanSm& c = cm[ch];
+            c.ofs[sl] = (int)(vs % cap);
+            c.np[sl] = (int)(((uint32_t)mbnp >> 16) & 0x7FFFu);
+            c.mb[sl] = (int)mb;
+            mbar_arrive_expect_tx(&c.full[sl], tot);
+            bulk_g2s(ring + vs % cap, M + mofs, mb, &c.full[sl]);
+            if (vb) bulk_g2s(ring + vs % cap + mb, V + sofs, vb, &c.full[sl]);
+            fch[ft % (2 * NDESC)] = ch;
+            fseq[ft % (2 * NDESC)] = jc[ch];
+            fvs[ft % (2 * NDESC)] = vs;
+            ++ft;
+            ++jc[ch];
+          }
+          __syncwarp();
+        }
       }
     }
     return;
   }
-  // ------------------------------------------------------------------ consumers
-  constexpr int NT = NC * 32;
-  double* v = ring + NS * 1024;
-  double* aux = v + ((n + 1) & ~1);
-  const long long b0 = pbase[3 * pi], b1 = pbase[3 * pi + 1], b2 = pbase[3 * pi + 2];
-  const int* offs = C.offs;
-  const unsigned char* comp = C.comp;
-  for (int t = tid; t < n; t += NT) {
-    const int c = comp[t];
-    const long long base = c == 0 ? b0 : (c == 1 ? b1 : b2);
-    v[t] = r[base + offs[t]];
-  }
+  // ================================================================== consumer warps
+  const Shared S{classes, pclass, pbase, r, u, omega, done};
+  Consumer cn{chan_sm(smraw, 0), ring, 0, 0, nullptr, nullptr};   // main channel
+  Consumer ct{chan_sm(smraw, 1), ring, 0, 0, nullptr, nullptr};   // tile channel (tile warps)
+  double* v = vbuf0;
+  double* vo = vbuf1;
+  if ((int)blockIdx.x < npatch) gather_patch(S, blockIdx.x, v, tid, NT);
   csync();
-  // ---- forward eliminations
-  const int nlev = C.nlev;
-  for (int l = 0; l < nlev; ++l) {
-    {
-      const DBlocks& Bk = C.lev[l].blk;
-      const double* Bv = V + Bk.vofs;
-      const int nb = Bk.nblk;
-      for (int i = tid; i < nb; i += NT) {
-        const int m0 = __ldg(Bk.mem + i);
-        const double y0 = v[m0] * __ldcs(Bv + i);
-        v[m0] = y0;
-        if (Bk.bs > 1) {
-          const int m1 = __ldg(Bk.mem + nb + i);
+  int qlast = -1;
+  for (int q = blockIdx.x; q < npatch; q += G) {
+    const DClass& C = classes[pclass[q]];
+    const int n = C.n;
+    const int qprev = q - G, qnext = q + G;
+    // ---- forward eliminations
+    const int nlev = C.nlev;
+    for (int l = 0; l < nlev; ++l) {
+      const DLevel& L = C.lev[l];
+      const int bs = L.blk.bs;
+      // y^_E = L^{-T} L^{-1} v_E in place (pivot blocks <= 3x3, diagonal stored inverted)
+      for (int pi = L.piv_b; pi < L.w_b; ++pi) {
+        const Piece_ pc = cn.acquire();
+        const Hdr h = hdr(pc.pb);
+        const uint16_t* mem = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+        const double* pv = pc.val;
+        const int cnt = h.a1 - h.a0;
+        for (int li = tid; li < cnt; li += NT) {
+          const int m0 = mem[li];
+          if (bs == 1) {
+            const double d = pv[li];
+            v[m0] *= d * d;
+            continue;
+          }
+          const int m1 = mem[cnt + li];
+          const int m2 = (bs > 2) ? mem[2 * cnt + li] : 0xFFFF;
+          const double l00 = pv[li], l10 = pv[cnt + li], l11 = pv[2 * cnt + li];
+          double y0 = v[m0] * l00, y1 = 0.0, y2 = 0.0;
+          if (m1 != 0xFFFF) y1 = (v[m1] - l10 * y0) * l11;
+          if (m2 != 0xFFFF) {
+            const double l20 = pv[3 * cnt + li], l21 = pv[4 * cnt + li], l22 = pv[5 * cnt + li];
+            y2 = (v[m2] - l20 * y0 - l21 * y1) * l22;
+            y2 *= l22;
+            v[m2] = y2;
+            if (m1 != 0xFFFF) y1 -= l21 * y2;
+            y0 -= l20 * y2;
+          }
           if (m1 != 0xFFFF) {
-            const double y1 = (v[m1] - __ldcs(Bv + nb + i) * y0) * __ldcs(Bv + 2 * nb + i);
+            y1 *= l11;
             v[m1] = y1;
-            if (Bk.bs > 2) {
-              const int m2 = __ldg(Bk.mem + 2 * nb + i);
-              if (m2 != 0xFFFF)
-                v[m2] = (v[m2] - __ldcs(Bv + 3 * nb + i) * y0 - __ldcs(Bv + 4 * nb + i) * y1) * __ldcs(Bv + 5 * nb + i);
+            y0 -= l10 * y1;
+          }
+          v[m0] = y0 * l00;
+        }
+        cn.release(lane);
+      }
+      csync();
+      const int r0 = L.w.r0;
+      for (int pi = L.w_b; pi < L.w_e; ++pi) {
+        const Piece_ pc = cn.acquire();
+        sliced_piece(pc, v, L.w.nrows, warp, lane, [&](int row, double acc) { v[r0 + row] -= acc; });
+        cn.release(lane);
+      }
+      csync();
+    }
+    // ---- final Schur block, with the side work (scatter of q - G, gather of q + G) overlapped
+    const int m = C.m, f0 = n - m;
+    if (C.final_kind == 0 && m > 0) {
+      const int T = (m + 31) >> 5, mpad = 32 * T;
+      double* g = aux;             // padded copy of v_F
+      double* parts = aux + mpad;  // per-tile-warp partial results
+      if (warp < NTW) {
+        const int tt = tid;        // 0 .. 32*NTW-1
+        for (int jj = tt; jj < mpad; jj += 32 * NTW) g[jj] = (jj < m) ? v[f0 + jj] : 0.0;
+        for (int jj = lane; jj < mpad; jj += 32) parts[warp * mpad + jj] = 0.0;
+        tsync();
+        // whole tiles per warp (tile t of the patch -> warp t % NTW), lane-block layout
+        // (patches.hpp): 16 conflict-free LDS.128 and 64 independent DFMA per lane and tile
+        double* mypart = parts + warp * mpad;
+        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
+          const Piece_ pc = ct.acquire();
+          if (((pi - C.tile_p0) % NTW) == warp) {
+            const Hdr h = hdr(pc.pb);
+            tile_gemv(pc.val, g, mypart, h.a0, h.a1, lane);
+          }
+          ct.release(lane);
+        }
+        tsync();
+        for (int jj = tt; jj < m; jj += 32 * NTW) {
+          double x = 0.0;
+#pragma unroll
+          for (int w = 0; w < NTW; ++w) x += parts[w * mpad + jj];
+          v[f0 + jj] = x;
+        }
+      } else {
+        const int ts = tid - 32 * NTW;
+        if (qprev >= 0) scatter_patch(S, cs, qprev, vo, ts, 32 * NSW, [] { ssync(); });
+        if (qnext < npatch) gather_patch(S, qnext, vo, ts, 32 * NSW);
+      }
+      csync();
+    } else {
+      if (C.final_kind != 0) {
+        // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
+        // then backward rows of L^T by levels (diag first); rows of one level are independent.
+        // meta = uint16 rows, uint16 value starts (cnt + 1), uint16 columns
+        double* y = v + f0;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int nl = pass == 0 ? C.iccf_nlev : C.iccb_nlev;
+          const int* lp = pass == 0 ? C.iccf_lp : C.iccb_lp;
+          for (int l = 0; l < nl; ++l) {
+            const int pe = lp[l + 1];
+            for (int pi = lp[l]; pi < pe; ++pi) {
+              const Piece_ pc = cn.acquire();
+              const Hdr h = hdr(pc.pb);
+              const int cnt = h.a1 - h.a0;
+              const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+              const uint16_t* st = rows + cnt;
+              const uint16_t* cols = st + cnt + 1;
+              const double* val = pc.val;
+              for (int k = tid; k < cnt; k += NT) {
+                const int a = rows[k], t0 = st[k], t1 = st[k + 1];
+                double s = y[a];
+                if (pass == 0) {
+                  for (int t = t0; t < t1 - 1; ++t) s -= val[t] * y[cols[t]];
+                  y[a] = s * val[t1 - 1];
+                } else {
+                  for (int t = t0 + 1; t < t1; ++t) s -= val[t] * y[cols[t]];
+                  y[a] = s * val[t0];
+                }
+              }
+              cn.release(lane);
             }
+            csync();
           }
         }
       }
+      if (qprev >= 0) scatter_patch(S, cs, qprev, vo, tid, NT, [] { csync(); });
+      if (qnext < npatch) gather_patch(S, qnext, vo, tid, NT);
       csync();
     }
-    const DSliced& W = C.lev[l].w;
-    const double* Wv = V + W.vofs;
-    for (int s = warp; s < W.nslices; s += NC) {
-      const int row = s * 32 + lane;
-      const int w = __ldg(W.sw + s), o = __ldg(W.soff + s);
-      double acc = 0.0;
-      int kk = 0;
-      for (; kk + 4 <= w; kk += 4) {
-        const int e = o + kk * 32 + lane;
-        const double a0 = __ldcs(Wv + e), a1 = __ldcs(Wv + e + 32), a2 = __ldcs(Wv + e + 64), a3 = __ldcs(Wv + e + 96);
-        const int c0 = __ldg(W.cols + e), c1 = __ldg(W.cols + e + 32), c2 = __ldg(W.cols + e + 64), c3 = __ldg(W.cols + e + 96);
-        acc += a0 * v[c0] + a1 * v[c1] + a2 * v[c2] + a3 * v[c3];
+    // ---- backward substitution: x_E = y^_E - W^ x_R  (W^ = P_EE^{-1} P_ER, in place)
+    for (int l = nlev - 1; l >= 0; --l) {
+      const DLevel& L = C.lev[l];
+      const int e0 = L.e0;
+      for (int pi = L.wt_b; pi < L.wt_e; ++pi) {
+        const Piece_ pc = cn.acquire();
+        sliced_piece(pc, v, L.wt.nrows, warp, lane, [&](int row, double acc) { v[e0 + row] -= acc; });
+        cn.release(lane);
       }
-      for (; kk < w; ++kk) {
-        const int e = o + kk * 32 + lane;
-        acc += __ldcs(Wv + e) * v[__ldg(W.cols + e)];
-      }
-      if (row < W.nrows) v[W.r0 + row] -= acc;
+      csync();
     }
-    csync();
+    double* tmp = v;
+    v = vo;
+    vo = tmp;
+    qlast = q;
   }
-  // ---- final Schur block
-  if (C.final_kind == 0) {
-    if (m > 0) {
-      const int mpad = 32 * T;
-      double* g = aux;            // padded copy of v_F
-      double* parts = aux + mpad; // per-warp partial results
-      for (int j = tid; j < mpad; j += NT) g[j] = (j < m) ? v[f0 + j] : 0.0;
-      for (int j = lane; j < mpad; j += 32) parts[warp * mpad + j] = 0.0;
-      csync();
-      // every consumer warp takes part in every tile (tiles are consumed in order, so each
-      // mbarrier phase is awaited only after the previous phase of that stage completed):
-      // warp w covers tile columns 4w..4w+3 for the row sums and tile rows 4w..4w+3 for the
-      // transposed column sums; lane = row (resp. column); partial sums stay per warp.
-      double* mypart = parts + warp * mpad;
-      int I = 0, J = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int s = t % NS;
-        mbar_wait(&full[s], (t / NS) & 1);
-        const double* tile = ring + s * 1024;
-        const double* gJ = g + 32 * J + 4 * warp;
-        const double* gI = g + 32 * I + 4 * warp;
-        double racc = 0.0, cacc = 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int c = 4 * warp + q;
-          racc += tile[lane * 32 + ((c + lane) & 31)] * gJ[q];
-          cacc += tile[c * 32 + ((lane + c) & 31)] * gI[q];
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        mypart[32 * I + lane] += racc;
-        if (I != J) mypart[32 * J + lane] += cacc;
-        if (++J > I) { ++I; J = 0; }
-      }
-      csync();
-      for (int j = tid; j < m; j += NT) {
-        double x = 0.0;
-#pragma unroll
-        for (int w = 0; w < NC; ++w) x += parts[w * mpad + j];
-        v[f0 + j] = x;
-      }
-      csync();
-    }
-  } else {
-    // ICC(0): forward rows of L by levels, backward rows of L^T by levels; diagonal stored inverted
-    const double* Lv = V + C.vofs_final;
-    const double* LTv = Lv + C.icc_nnz;
-    double* y = v + f0;
-    for (int l = 0; l < C.icc_nlev; ++l) {
-      const int a0 = C.icc_lptr[l], a1 = C.icc_lptr[l + 1];
-      for (int q = a0 + tid; q < a1; q += NT) {
-        const int a = C.icc_lrows[q];
-        const int t0 = C.icc_rowptr[a], t1 = C.icc_rowptr[a + 1] - 1;
-        double s = y[a];
-        for (int t = t0; t < t1; ++t) s -= Lv[t] * y[C.icc_col[t]];
-        y[a] = s * Lv[t1];
-      }
-      csync();
-    }
-    for (int l = 0; l < C.icct_nlev; ++l) {
-      const int a0 = C.icct_lptr[l], a1 = C.icct_lptr[l + 1];
-      for (int q = a0 + tid; q < a1; q += NT) {
-        const int b = C.icct_lrows[q];
-        const int t0 = C.icct_rowptr[b], t1 = C.icct_rowptr[b + 1];
-        double s = y[b];
-        for (int t = t0 + 1; t < t1; ++t) s -= LTv[t] * y[C.icct_col[t]];
-        y[b] = s * LTv[t0];
-      }
-      csync();
-    }
-  }
-  // ---- backward substitution: x_E = L^{-T} (y_E - M^T x_R)
-  for (int l = nlev - 1; l >= 0; --l) {
-    const DLevel& L = C.lev[l];
-    const DSliced& WT = L.wt;
-    const double* Tv = V + WT.vofs;
-    for (int s = warp; s < WT.nslices; s += NC) {
-      const int row = s * 32 + lane;
-      double acc = (row < WT.nrows) ? v[L.e0 + row] : 0.0;
-      const int w = __ldg(WT.sw + s), o = __ldg(WT.soff + s);
-      int kk = 0;
-      for (; kk + 4 <= w; kk += 4) {
-        const int e = o + kk * 32 + lane;
-        const double a0 = __ldcs(Tv + e), a1 = __ldcs(Tv + e + 32), a2 = __ldcs(Tv + e + 64), a3 = __ldcs(Tv + e + 96);
-        const int c0 = __ldg(WT.cols + e), c1 = __ldg(WT.cols + e + 32), c2 = __ldg(WT.cols + e + 64), c3 = __ldg(WT.cols + e + 96);
-        acc -= a0 * v[c0] + a1 * v[c1] + a2 * v[c2] + a3 * v[c3];
-      }
-      for (; kk < w; ++kk) {
-        const int e = o + kk * 32 + lane;
-        acc -= __ldcs(Tv + e) * v[__ldg(WT.cols + e)];
-      }
-      if (row < WT.nrows) aux[row] = acc;
-    }
-    csync();
-    {
-      const DBlocks& Bk = L.blk;
-      const double* Bv = V + Bk.vofs;
-      const int nb = Bk.nblk;
-      for (int i = tid; i < nb; i += NT) {
-        const int m0 = __ldg(Bk.mem + i);
-        if (Bk.bs == 1) {
-          v[m0] = aux[m0 - L.e0] * __ldcs(Bv + i);
-          continue;
-        }
-        const int m1 = __ldg(Bk.mem + nb + i);
-        const int m2 = (Bk.bs > 2) ? __ldg(Bk.mem + 2 * nb + i) : 0xFFFF;
-        double x2 = 0.0, x1 = 0.0;
-        if (m2 != 0xFFFF) { x2 = aux[m2 - L.e0] * __ldcs(Bv + 5 * nb + i); v[m2] = x2; }
-        if (m1 != 0xFFFF) {
-          x1 = aux[m1 - L.e0];
-          if (m2 != 0xFFFF) x1 -= __ldcs(Bv + 4 * nb + i) * x2;
-          x1 *= __ldcs(Bv + 2 * nb + i);
-          v[m1] = x1;
-        }
-        double x0 = aux[m0 - L.e0];
-        if (m1 != 0xFFFF) x0 -= __ldcs(Bv + nb + i) * x1;
-        if (m2 != 0xFFFF) x0 -= __ldcs(Bv + 3 * nb + i) * x2;
-        v[m0] = x0 * __ldcs(Bv + i);
-      }
-    }
-    csync();
-  }
-  // ---- scatter-add omega * R_i^T x
-  for (int t = tid; t < n; t += NT) {
-    const int c = comp[t];
-    const long long base = c == 0 ? b0 : (c == 1 ? b1 : b2);
-    double* up = u + base + offs[t];
-    *up += omega * v[t];
-  }
+  // ---- drain: scatter the last patch
+  if (qlast >= 0) scatter_patch(S, cs, qlast, vo, tid, NT, [] { csync(); });
 }
 
-size_t patch_solve_smem_bytes(int n, int max_aux) {
-  return 128 + (size_t)NS * 8192 + (size_t)(((n + 1) & ~1) + max_aux) * sizeof(double);
+cudaError_t plan_patch_solve(PatchLaunch& L) {
+  L.smem_fixed = BAR_BYTES + (size_t)(2 * ((L.n_max + 1) & ~1) + L.aux_max) * sizeof(double);
+  int dev = 0, nsm = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
+    return e;
+  // two CTAs per SM when the fixed part leaves >= 64 KB of ring each, else one CTA with the rest
+  // (env RM_CTAS_PER_SM / RM_RING_KB override for experiments); the ring must hold 2 units
+  const size_t per_sm = 228 * 1024;
+  int want = 2;
+  if (const char* s = getenv("RM_CTAS_PER_SM")) want = atoi(s);
+  size_t ring = 0;
+  for (; want >= 1; --want) {
+    const size_t avail = std::min<size_t>(per_sm / want - 1024, optin);
+    if (avail >= L.smem_fixed + 64 * 1024) { ring = avail - L.smem_fixed; break; }
+  }
+  if (want < 1) {
+    if ((size_t)optin < L.smem_fixed + 2 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
+    ring = optin - L.smem_fixed;
+    want = 1;
+  }
+  if (const char* s = getenv("RM_RING_KB")) ring = std::min<size_t>(ring, (size_t)atoi(s) * 1024);
+  ring &= ~(size_t)127;
+  if (ring < (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
+  L.ring_bytes = (int)ring;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, patch_stream_kernel, NTHR, L.smem_fixed + ring)) != cudaSuccess)
+    return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  L.grid = std::max(1, std::min(L.npatch, occ * nsm));
+  if (getenv("RM_VERBOSE"))
+    fprintf(stderr, "[rm] patch plan: npatch=%d n_max=%d aux_max=%d fixed=%zu ring=%d occ=%d grid=%d\n", L.npatch,
+            L.n_max, L.aux_max, L.smem_fixed, L.ring_bytes, occ, L.grid);
+  return cudaSuccess;
 }
 
-cudaError_t launch_patch_solve(const DClass* classes, const int* pclass, const long long* pbase,
-                               const long long* pvals, const double* vals, const double* r, double* u,
-                               double omega, int npatch, size_t smem, cudaStream_t st) {
-  if (npatch <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(patch_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  patch_solve_kernel<<<npatch, NTHR, smem, st>>>(classes, pclass, pbase, pvals, vals, r, u, omega);
+cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st) {
+  if (L.npatch <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes, st>>>(
+      L.classes, L.pclass, L.pbase, L.pvals, L.vals, r, u, omega, L.npatch, L.cs, L.done, (uint32_t)L.ring_bytes,
+      L.n_max);
   return cudaGetLastError();
 }
 

@@ -154,6 +154,271 @@ void build_blocks(Blocks& B, const std::vector<std::vector<int>>& blocks) {
     for (size_t j = 0; j < blocks[i].size(); ++j) B.mem[j * B.nblk + i] = (uint16_t)blocks[i][j];
 }
 
+// ---------------------------------------------------------------- stream layout (patches.hpp)
+void add_piece(ClassProgram& C, int64_t& s, Piece p) {
+  if (p.nd <= 0 && p.kind != PK_GATHER && p.kind != PK_SCATTER) return;
+  p.nd = (p.nd + 1) & ~1;
+  if (p.nd > kPieceMax) throw std::runtime_error("stream piece larger than kPieceMax");
+  p.sofs = (int)s;
+  s += p.nd;
+  C.pieces.push_back(p);
+}
+
+void sliced_pieces(ClassProgram& C, int64_t& s, int kind, int lev, const Sliced& S) {
+  const int ns = (int)S.slice_w.size();
+  int sl = 0;
+  while (sl < ns) {
+    const int sz = 32 * S.slice_w[sl];
+    if (sz > kPieceMax) {   // one wide slice: split its columns
+      const int per = kPieceMax / 32;
+      for (int k0 = 0; k0 < S.slice_w[sl]; k0 += per) {
+        const int nk = std::min(per, S.slice_w[sl] - k0);
+        add_piece(C, s, Piece{kind, lev, sl, sl + 1, S.slice_off[sl] + 32 * k0, 0, 32 * nk, (int)S.vofs + S.slice_off[sl] + 32 * k0});
+      }
+      ++sl;
+      continue;
+    }
+    const int a0 = sl;
+    int tot = 0;
+    while (sl < ns && tot + 32 * S.slice_w[sl] <= kPieceMax) tot += 32 * S.slice_w[sl++];
+    add_piece(C, s, Piece{kind, lev, a0, sl, S.slice_off[a0], 0, tot, (int)S.vofs + S.slice_off[a0]});
+  }
+}
+
+// class meta stream: one 16-byte-aligned block per piece, header {a0, a1, e0, mbytes}
+void build_meta(ClassProgram& C) {
+  std::vector<uint8_t>& M = C.meta;
+  M.clear();
+  auto put = [&](const void* p, size_t nb) { const uint8_t* b = (const uint8_t*)p; M.insert(M.end(), b, b + nb); };
+  auto put16 = [&](int x) { uint16_t h = (uint16_t)x; if (x < 0 || x > 0xFFFF) throw std::runtime_error("meta u16 overflow"); put(&h, 2); };
+  auto align16 = [&]() { while (M.size() & 15) M.push_back(0); };
+  for (size_t i = 0; i < C.pieces.size(); ++i) {
+    Piece& p = C.pieces[i];
+    if (p.kind == PK_SCATTER) {   // reuses the GATHER block of the same positions
+      const Piece& g = C.pieces[i - (C.pieces.size() - C.ngs)];
+      p.mofs = g.mofs; p.mbytes = g.mbytes;
+      continue;
+    }
+    const size_t at = M.size();
+    int32_t hdr[4] = {p.a0, p.a1, p.e0, 0};
+    put(hdr, 16);
+    switch (p.kind) {
+      case PK_GATHER:
+        for (int t = p.a0; t < p.a1; ++t) {
+          const int64_t code = ((int64_t)C.offs[t] << 2) | C.comp[t];
+          if (code > INT32_MAX || code < INT32_MIN) throw std::runtime_error("gather code overflow");
+          int32_t c32 = (int32_t)code;
+          put(&c32, 4);
+        }
+        break;
+      case PK_PIV: {
+        const Blocks& B = C.lev[p.lev].blk;
+        for (int sl = 0; sl < B.bs; ++sl)
+          for (int b = p.a0; b < p.a1; ++b) put16(B.mem[(size_t)sl * B.nblk + b]);
+        break;
+      }
+      case PK_W:
+      case PK_WT: {
+        const Sliced& S = (p.kind == PK_W) ? C.lev[p.lev].w : C.lev[p.lev].wt;
+        for (int sl = p.a0; sl < p.a1; ++sl) {
+          const int o = S.slice_off[sl];
+          const int k0 = std::max(0, (p.e0 - o) / 32), k1 = std::min(S.slice_w[sl], (p.e0 + p.nd - o) / 32);
+          const int start = o + 32 * k0 - p.e0;
+          const uint32_t info = (uint32_t)(start / 32) | ((uint32_t)std::max(0, k1 - k0) << 16);
+          put(&info, 4);
+        }
+        for (int e = p.e0; e < p.e0 + p.nd; ++e) put(&S.cols[e], 2);
+        break;
+      }
+      case PK_TILE:
+        break;
+      case PK_ICCF:
+      case PK_ICCB: {
+        const bool f = p.kind == PK_ICCF;
+        const std::vector<int>& row = f ? C.iccf_row : C.iccb_row;
+        const std::vector<int>& rp = f ? C.iccf_rp : C.iccb_rp;
+        const std::vector<int>& col = f ? C.iccf_col : C.iccb_col;
+        for (int q = p.a0; q < p.a1; ++q) put16(row[q]);
+        for (int q = p.a0; q <= p.a1; ++q) put16(rp[q] - p.e0);
+        for (int t = rp[p.a0]; t < rp[p.a1]; ++t) put16(col[t]);
+        break;
+      }
+    }
+    align16();
+    p.mofs = (int)at;
+    p.mbytes = (int)(M.size() - at);
+    if (p.mbytes > 0xFFFF || p.nd > 0xFFFF) throw std::runtime_error("piece too large for its header");
+    const uint32_t w3 = (uint32_t)p.mbytes | ((uint32_t)p.nd << 16);
+    std::memcpy(&M[at + 12], &w3, 4);
+  }
+  // transfer units: consecutive pieces whose metas and values are both contiguous
+  static const int unit_vals = getenv("RM_UNIT_VALS") ? atoi(getenv("RM_UNIT_VALS")) : kUnitVals;
+  C.units.clear();
+  const int ns = (int)C.pieces.size() - C.ngs;   // first SCATTER piece
+  for (int i = 0; i < (int)C.pieces.size();) {
+    Unit u{i, 0, C.pieces[i].mofs, 0, C.pieces[i].sofs, 0};
+    while (i < (int)C.pieces.size()) {
+      const Piece& p = C.pieces[i];
+      const bool boundary = u.np > 0 && (i == C.ngs || i == ns || i == C.tile_p0 || i == C.tile_p1);
+      if (u.np > 0 && (boundary || u.nd + p.nd > unit_vals || u.mbytes + p.mbytes > kUnitMeta)) break;
+      if (p.mofs != u.mofs + u.mbytes || p.sofs != u.sofs + u.nd) {
+        if (u.np > 0) break;
+      }
+      u.np++; u.mbytes += p.mbytes; u.nd += p.nd;
+      ++i;
+    }
+    C.units.push_back(u);
+  }
+  C.tu0 = C.tu1 = 0;
+  for (size_t k = 0; k < C.units.size(); ++k) {
+    const bool tile = C.units[k].p0 >= C.tile_p0 && C.units[k].p0 < C.tile_p1 && C.final_kind == FINAL_DENSE_INV;
+    if (tile && C.tu1 == 0) C.tu0 = (int)k;
+    if (tile) C.tu1 = (int)k + 1;
+  }
+}
+
+void build_stream(ClassProgram& C) {
+  C.pieces.clear();
+  const int L = (int)C.lev.size();
+  C.ngs = 0;   // gather/scatter codes travel in C.codes (read from L2 by the side-work warps)
+  C.codes.resize(C.n);
+  for (int t = 0; t < C.n; ++t) {
+    const int64_t code = ((int64_t)C.offs[t] << 2) | C.comp[t];
+    if (code > INT32_MAX || code < INT32_MIN) throw std::runtime_error("gather code overflow");
+    C.codes[t] = (int32_t)code;
+  }
+  C.piv_b.assign(L, 0); C.w_b.assign(L, 0); C.w_e.assign(L, 0); C.wt_b.assign(L, 0); C.wt_e.assign(L, 0);
+  C.piv_per.assign(L, 1); C.piv_ofs.assign(L, 0); C.mem_ofs.assign(L, 0);
+  int64_t s = 0;
+  int pivofs = 0, memofs = 0;
+  for (int l = 0; l < L; ++l) {
+    const Blocks& B = C.lev[l].blk;
+    const int ns = B.bs * (B.bs + 1) / 2;
+    const int per = std::max(1, (kPieceMax / ns) & ~1);
+    C.piv_per[l] = per;
+    C.piv_ofs[l] = pivofs;
+    C.mem_ofs[l] = memofs;
+    pivofs += ns * B.nblk;
+    memofs += B.bs * B.nblk;
+    C.piv_b[l] = (int)C.pieces.size();
+    for (int a0 = 0; a0 < B.nblk; a0 += per) {
+      const int a1 = std::min(B.nblk, a0 + per);
+      add_piece(C, s, Piece{PK_PIV, l, a0, a1, 0, 0, ns * (a1 - a0), (int)B.vofs});
+    }
+    C.w_b[l] = (int)C.pieces.size();
+    sliced_pieces(C, s, PK_W, l, C.lev[l].w);
+    C.w_e[l] = (int)C.pieces.size();
+  }
+  C.piv_total = (pivofs + 1) & ~1;
+  C.mem_total = (memofs + 7) & ~7;
+  C.tile_p0 = (int)C.pieces.size();
+  const int m = C.m;
+  if (C.final_kind == FINAL_DENSE_INV) {
+    const int T = (m + 31) / 32;
+    for (int I = 0; I < T; ++I)
+      for (int J = 0; J <= I; ++J)
+        add_piece(C, s, Piece{PK_TILE, 0, I, J, 0, 0, I == J ? kTileDiag : 1024,
+                              (int)C.vofs_final + (I * (I + 1) / 2 + J) * 1024});
+  } else {
+    // level-ordered CSR copies (forward rows of L diag last, backward rows of L^T diag first)
+    const int nnz = C.icc_rowptr.empty() ? 0 : C.icc_rowptr[m];
+    C.iccf_row.clear(); C.iccf_rp.assign(1, 0); C.iccf_col.clear(); C.iccf_src.clear(); C.iccf_lpiece.clear();
+    const int nlf = (int)C.icc_level_ptr.size() - 1;
+    for (int l = 0; l < nlf; ++l) {
+      C.iccf_lpiece.push_back((int)C.pieces.size());
+      int q = C.icc_level_ptr[l];
+      const int qe = C.icc_level_ptr[l + 1];
+      while (q < qe) {
+        const int q0 = q;
+        const int v0 = C.iccf_rp[q];
+        while (q < qe) {
+          const int a = C.icc_level_rows[q];
+          const int len = C.icc_rowptr[a + 1] - C.icc_rowptr[a];
+          if (len > kPieceMax) throw std::runtime_error("ICC row longer than kPieceMax");
+          if (C.iccf_rp[q] + len - v0 > kPieceMax) break;
+          C.iccf_row.push_back(a);
+          for (int t = C.icc_rowptr[a]; t < C.icc_rowptr[a + 1]; ++t) { C.iccf_col.push_back(C.icc_col[t]); C.iccf_src.push_back(t); }
+          C.iccf_rp.push_back(C.iccf_rp.back() + len);
+          ++q;
+        }
+        // values are addressed by their level-ordered index t, at o[t - v0] inside the piece
+        add_piece(C, s, Piece{PK_ICCF, l, q0, q, v0, 0, C.iccf_rp[q] - v0, -1});
+      }
+    }
+    C.iccf_lpiece.push_back((int)C.pieces.size());
+    C.iccb_row.clear(); C.iccb_rp.assign(1, 0); C.iccb_col.clear(); C.iccb_src.clear(); C.iccb_lpiece.clear();
+    const int nlb = (int)C.icct_level_ptr.size() - 1;
+    for (int l = 0; l < nlb; ++l) {
+      C.iccb_lpiece.push_back((int)C.pieces.size());
+      int q = C.icct_level_ptr[l];
+      const int qe = C.icct_level_ptr[l + 1];
+      while (q < qe) {
+        const int q0 = q;
+        const int v0 = C.iccb_rp[q];
+        while (q < qe) {
+          const int b = C.icct_level_rows[q];
+          const int len = C.icct_rowptr[b + 1] - C.icct_rowptr[b];
+          if (len > kPieceMax) throw std::runtime_error("ICC row longer than kPieceMax");
+          if (C.iccb_rp[q] + len - v0 > kPieceMax) break;
+          C.iccb_row.push_back(b);
+          for (int t = C.icct_rowptr[b]; t < C.icct_rowptr[b + 1]; ++t) {
+            C.iccb_col.push_back(C.icct_col[t]);
+            C.iccb_src.push_back(nnz + t);
+          }
+          C.iccb_rp.push_back(C.iccb_rp.back() + len);
+          ++q;
+        }
+        add_piece(C, s, Piece{PK_ICCB, l, q0, q, v0, 0, C.iccb_rp[q] - v0, -1});
+      }
+    }
+    C.iccb_lpiece.push_back((int)C.pieces.size());
+  }
+  C.tile_p1 = (int)C.pieces.size();
+  for (int l = L - 1; l >= 0; --l) {
+    C.wt_b[l] = (int)C.pieces.size();
+    sliced_pieces(C, s, PK_WT, l, C.lev[l].wt);
+    C.wt_e[l] = (int)C.pieces.size();
+  }
+  C.nvals = s;
+  build_meta(C);
+}
+
+// canonical (factorization-order) block -> stream block
+void pack_stream(const ClassProgram& C, const double* canon, double* out) {
+  for (const Piece& p : C.pieces) {
+    double* o = out + p.sofs;
+    std::fill(o, o + p.nd, 0.0);
+    switch (p.kind) {
+      case PK_PIV: {
+        const Blocks& B = C.lev[p.lev].blk;
+        const int ns = B.bs * (B.bs + 1) / 2, cnt = p.a1 - p.a0;
+        for (int slot = 0; slot < ns; ++slot)
+          for (int i = p.a0; i < p.a1; ++i) o[slot * cnt + (i - p.a0)] = canon[p.cofs + (size_t)slot * B.nblk + i];
+        break;
+      }
+      case PK_W:
+      case PK_WT:
+        std::copy(canon + p.cofs, canon + p.cofs + p.nd, o);
+        break;
+      case PK_TILE:   // canonical tiles hold element (r, c) at r*32 + ((c + r) & 31)
+        for (int r = 0; r < 32; ++r)
+          for (int c = 0; c < 32; ++c) {
+            const double x = canon[p.cofs + r * 32 + ((c + r) & 31)];
+            if (p.a0 != p.a1) o[tile_pos_full(r, c)] = x;
+            else if (c < r) o[tile_pos_diag(r, c)] = x;
+            else if (c == r) o[tile_pos_diag(r, c)] = 0.5 * x;
+          }
+        break;
+      case PK_ICCF:
+        for (int t = C.iccf_rp[p.a0]; t < C.iccf_rp[p.a1]; ++t) o[t - p.e0] = canon[C.vofs_final + C.iccf_src[t]];
+        break;
+      case PK_ICCB:
+        for (int t = C.iccb_rp[p.a0]; t < C.iccb_rp[p.a1]; ++t) o[t - p.e0] = canon[C.vofs_final + C.iccb_src[t]];
+        break;
+    }
+  }
+}
+
 }  // namespace
 
 // ===================================================================================== builder
@@ -516,7 +781,8 @@ struct Builder {
         vofs += 2 * (int64_t)nnz;   // L values (row order) then L^T values (transpose order)
       }
     }
-    C.nvals = (vofs + 1) & ~int64_t(1);   // keep every patch value block 16-byte aligned
+    C.nvals_canon = (vofs + 1) & ~int64_t(1);
+    build_stream(C);
   }
 
   // ---------------------------------------------------------------- numeric factorization
@@ -635,7 +901,7 @@ struct Builder {
       }
       put_blocks(L0.blk, Lb);
       // M rows per block: for r in nb(block): M[r][b] = solve L_b m = P[b][r]  (m = L^{-1} P_br)
-      std::vector<std::map<int, double>> Mrow(nG);   // interface row -> (E position -> value)
+      std::vector<std::map<int, double>> What(nG);   // interface row -> (E position -> (P_EE^{-1} P_ER)^T)
       for (int bi = 0; bi < nb0; ++bi) {
         const auto& b = L0.blocks[bi];
         const int bs = (int)b.size();
@@ -652,7 +918,6 @@ struct Builder {
             for (int k = 0; k < j; ++k) t -= Lm[j * bs + k] * y[k];
             y[j] = t / Lm[j * bs + j];
             Mv[i * bs + j] = y[j];
-            Mrow[nb[i] - nI][b[j]] = y[j];
           }
         }
         for (size_t i = 0; i < nb.size(); ++i)
@@ -661,14 +926,25 @@ struct Builder {
             for (int j = 0; j < bs; ++j) s += Mv[i * bs + j] * Mv[c * bs + j];
             S[(size_t)(nb[i] - nI) * nG + (nb[c] - nI)] -= s;
           }
+        // backward coupling W^ = P_EE^{-1} P_ER: z = L^{-T} y for every neighbour column
+        for (size_t i = 0; i < nb.size(); ++i) {
+          double z[3];
+          for (int j = bs - 1; j >= 0; --j) {
+            double t = Mv[i * bs + j];
+            for (int k = j + 1; k < bs; ++k) t -= Lm[k * bs + j] * z[k];
+            z[j] = t / Lm[j * bs + j];
+            What[nb[i] - nI][b[j]] = z[j];
+          }
+        }
       }
-      auto mval = [&](int r, int q) {
-        const auto& mr = Mrow[r - nI];
+      // forward: v_R -= P_RE y^_E with y^_E = P_EE^{-1} v_E (computed in place by the pivot step);
+      // backward: x_E = y^_E - (P_EE^{-1} P_ER) x_R
+      put_sliced(L0.w, [&](int r, int q) { return Pij(r, q); });
+      put_sliced(L0.wt, [&](int q, int r) {
+        const auto& mr = What[r - nI];
         auto it = mr.find(q);
         return it == mr.end() ? 0.0 : it->second;
-      };
-      put_sliced(L0.w, mval);
-      put_sliced(L0.wt, [&](int q, int r) { return mval(r, q); });
+      });
     }
     // levels >= 1 on the dense Schur complement, 1x1 pivots: L = sqrt(S_qq), M = S_Rq / L
     for (size_t l = 1; l < C.lev.size(); ++l) {
@@ -680,8 +956,8 @@ struct Builder {
         Lb.push_back({std::sqrt(Sv(q, q))});
       }
       put_blocks(L.blk, Lb);
-      put_sliced(L.w, [&](int r, int q) { return Sv(r, q) / std::sqrt(Sv(q, q)); });
-      put_sliced(L.wt, [&](int q, int r) { return Sv(r, q) / std::sqrt(Sv(q, q)); });
+      put_sliced(L.w, [&](int r, int q) { return Sv(r, q); });
+      put_sliced(L.wt, [&](int q, int r) { return Sv(q, r) / Sv(q, q); });
       for (int q = L.e0; q < L.e1; ++q) {
         const auto& nb = L.wt.rowcols[q - L.e0];
         double d = Sv(q, q);
@@ -869,13 +1145,16 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     const Entity& e = ents[keep[t]];
     const ClassProgram& C = fam->classes[fam->pclass[t]];
     std::string err;
-    bool ok = B.factor_patch(C, e, fam->values.data() + foff[f], 0.0, err);
+    std::vector<double> canon(C.nvals_canon, 0.0);
+    bool ok = B.factor_patch(C, e, canon.data(), 0.0, err);
     if (!ok && in.factorization == 1) {   // reading G7: P + sigma diag(P), sigma = 1e-10 doubling
       for (double shift = 1e-10; shift <= 1e-2 && !ok; shift *= 2.0) {
-        ok = B.factor_patch(C, e, fam->values.data() + foff[f], shift, err);
+        std::fill(canon.begin(), canon.end(), 0.0);
+        ok = B.factor_patch(C, e, canon.data(), shift, err);
         if (ok) smax = std::max(smax, shift);
       }
     }
+    if (ok) pack_stream(C, canon.data(), fam->values.data() + foff[f]);
     if (!ok) {
       std::lock_guard<std::mutex> lk(emu);
       if (first_err.empty()) {

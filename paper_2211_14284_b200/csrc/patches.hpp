@@ -37,10 +37,11 @@ struct Blocks {             // pivot blocks of one level, thread-per-block layou
   int64_t nval() const { return (int64_t)nblk * bs * (bs + 1) / 2; }
 };
 
-// One elimination level in Cholesky form: with the pivot blocks P_EE = L L^T,
-//   forward  y_E = L^{-1} v_E,  v_R -= M y_E           (M = P_RE L^{-T}, sliced by R rows: w)
-//   backward x_E = L^{-T} (y_E - M^T x_R)              (M^T sliced by E rows: wt)
-// i.e. exactly the Cholesky factorization of the patch matrix with E eliminated first.
+// One elimination level.  With the pivot blocks P_EE = L L^T (stored: L with inverted diagonal),
+//   forward  y^_E = L^{-T} L^{-1} v_E = P_EE^{-1} v_E  (in place),   v_R -= P_RE y^_E     (w)
+//   backward x_E  = y^_E - W^ x_R,   W^ = P_EE^{-1} P_ER  (prescaled on the host)        (wt)
+// i.e. block Gaussian elimination of the patch matrix with E eliminated first; the backward pass
+// needs no pivots.
 struct Level {
   int e0 = 0, e1 = 0;                    // E = positions [e0, e1), R = [e1, n)
   std::vector<std::vector<int>> blocks;  // pivot blocks (positions), sizes 1..3
@@ -49,6 +50,53 @@ struct Level {
 };
 
 enum FinalKind { FINAL_DENSE_INV = 0, FINAL_ICC = 1 };
+
+// Stream layout.  A patch is processed as a sequence of PIECES, each streamed HBM/L2 -> shared
+// memory by one producer warp with bulk copies (TMA) while the consumer warps work on earlier
+// pieces.  A piece = a metadata block (from the class's L2-resident meta stream: a 16-byte
+// header {a0, a1, e0, mbytes} then indices) followed by its factor values (from the patch's
+// value block, <= kPieceMax doubles, 16-byte aligned), so the consumers never chase a global
+// pointer.  Order of the pieces (= order of the values in the patch value block):
+//   forward:  for l = 0..L-1: PIV(l) pieces (block members + pivots), W(l) pieces
+//   final:    TILE pieces (row-major over I, J <= I; diagonal tiles packed lower, 528 doubles)
+//             or ICC forward-row pieces then ICC backward-row pieces (split at level boundaries)
+//   backward: for l = L-1..0: WT(l) pieces  (pivots and members reused from a shared copy)
+// (gather / scatter use the class's codes (offs << 2 | comp) from global memory; the dense-tile
+// units form their own channel, consumed by the tile warps only)
+enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_GATHER = 6, PK_SCATTER = 7 };
+constexpr int kPieceMax = 2048;      // doubles (16 KB) of values per piece
+constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
+// Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
+// owns rows 4a..4a+3 and columns 8b..8b+7; step k (0..15) holds its elements (row 4a + k/4,
+// columns 8b + 2(k%4) + {0,1}); the stream stores step k of all lanes contiguously
+// (16 bytes per lane: one conflict-free LDS.128).  Diagonal tiles keep only the 20 sub-blocks
+// (b <= a/2) that touch the lower triangle, with the strictly upper part zero and the diagonal
+// halved, so that the tile equals L' + L'^T and one row-sum + column-sum pass applies it.
+constexpr int kTileDiag = 640;       // 16 steps x 20 lanes x 2
+inline int tile_pos_full(int r, int c) {
+  const int l = (r >> 2) * 4 + (c >> 3), k = (r & 3) * 4 + ((c & 7) >> 1);
+  return (k * 32 + l) * 2 + (c & 1);
+}
+inline int tile_diag_slot(int a, int b) { return a + (a >> 1) * ((a - 1) >> 1) + b; }   // b <= a/2
+inline int tile_pos_diag(int r, int c) {   // c <= r
+  const int a = r >> 2, b = c >> 3, k = (r & 3) * 4 + ((c & 7) >> 1);
+  return (k * 20 + tile_diag_slot(a, b)) * 2 + (c & 1);
+}
+struct Piece {
+  int kind, lev;
+  int a0, a1;     // PIV: blocks; W/WT: slices; TILE: I, J; ICC: level-ordered rows; GATHER: positions
+  int e0;         // W/WT: first element of the sliced array; ICC: first value
+  int sofs;       // stream offset (doubles) inside the patch value block
+  int nd;         // doubles (even)
+  int cofs;       // source offset inside the canonical block (host packing only)
+  int mofs = 0, mbytes = 0;   // metadata block inside the class meta stream (bytes, 16-aligned)
+};
+
+// Transfer unit: consecutive pieces moved by one mbarrier round trip (<= kUnitVals doubles of
+// values and <= kUnitMeta bytes of metadata; the ring holds [metas][values] of the unit).
+constexpr int kUnitVals = 4096;
+constexpr int kUnitMeta = 16384;
+struct Unit { int p0, np, mofs, mbytes, sofs, nd; };
 
 struct ClassProgram {
   int n = 0;
@@ -66,7 +114,23 @@ struct ClassProgram {
   std::vector<int> icc_level_ptr, icc_level_rows;    // forward level schedule
   std::vector<int> icct_rowptr, icct_col, icct_src;  // backward: rows of L^T (src = index into L values)
   std::vector<int> icct_level_ptr, icct_level_rows;
-  int64_t nvals = 0;                     // doubles per patch value block
+  // ICC in level order (stream layout): q = level-ordered row index; rp over values in stream order
+  std::vector<int> iccf_row, iccf_rp, iccf_col, iccf_src, iccf_lpiece;   // forward (diag last)
+  std::vector<int> iccb_row, iccb_rp, iccb_col, iccb_src, iccb_lpiece;   // backward (diag first)
+  int64_t nvals_canon = 0;               // doubles per canonical (factorization-order) block
+  int64_t nvals = 0;                     // doubles per patch value block (stream layout)
+  // stream pieces and the piece ranges of each section
+  std::vector<Piece> pieces;
+  std::vector<int> piv_b, w_b, w_e, wt_b, wt_e;   // per level: piece ranges (PIV(l) = [piv_b, w_b))
+  int tile_p0 = 0, tile_p1 = 0;
+  std::vector<int> piv_per, piv_ofs, mem_ofs;   // per level: blocks per PIV piece, shared-memory offsets
+  int piv_total = 0;                     // doubles of the shared-memory pivot copy
+  int mem_total = 0;                     // uint16 of the shared-memory block-member copy
+  int ngs = 0;                           // GATHER pieces (= SCATTER pieces)
+  std::vector<uint8_t> meta;             // class meta stream (pieces' metadata blocks)
+  std::vector<Unit> units;
+  int tu0 = 0, tu1 = 0;                  // units of the dense-tile phase (tile channel)
+  std::vector<int32_t> codes;            // per position: (offs << 2) | comp (gather / scatter)
   // structural pattern of the patch matrix (CSR over positions)
   std::vector<int> prow, pcol;
 };

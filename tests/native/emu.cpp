@@ -6,6 +6,7 @@
 // schedules, ICC, packing) against the oracle without a GPU.
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -16,6 +17,45 @@
 
 using namespace rm;
 
+// Re-enacts patch_stream_kernel on the STREAM layout (patches.hpp): every index comes from the
+// pieces' metadata blocks (class meta stream) and every value from the pieces of the patch value
+// block, in piece order, exactly as the kernel's shared-memory ring presents them.
+struct PieceView {
+  const uint8_t* pb;      // metadata block
+  const double* val;      // values
+  int a0, a1, e0, mbytes, nd;
+};
+// Builds every piece's view the way the kernel sees it: per transfer unit, one buffer holding
+// [metas of the unit's pieces][values of the unit's pieces]; inside it the consumer walks the
+// pieces with a meta cursor and a value cursor advanced by the header's (mbytes, nd).
+static std::vector<PieceView> unit_views(const ClassProgram& C, const double* V, std::vector<std::vector<uint8_t>>& bufs) {
+  std::vector<PieceView> out(C.pieces.size());
+  bufs.assign(C.units.size(), {});
+  for (size_t k = 0; k < C.units.size(); ++k) {
+    const Unit& u = C.units[k];
+    std::vector<uint8_t>& b = bufs[k];
+    b.resize((size_t)u.mbytes + (size_t)u.nd * 8 + 16);
+    std::memcpy(b.data(), C.meta.data() + u.mofs, u.mbytes);
+    std::memcpy(b.data() + u.mbytes, V + u.sofs, (size_t)u.nd * 8);
+    const uint8_t* mcur = b.data();
+    const uint8_t* vcur = b.data() + u.mbytes;
+    for (int i = u.p0; i < u.p0 + u.np; ++i) {
+      PieceView w;
+      int32_t h[4];
+      std::memcpy(h, mcur, 16);
+      w.pb = mcur; w.a0 = h[0]; w.a1 = h[1]; w.e0 = h[2];
+      w.mbytes = (int)((uint32_t)h[3] & 0xFFFFu); w.nd = (int)((uint32_t)h[3] >> 16);
+      if (w.mbytes != C.pieces[i].mbytes || w.nd != C.pieces[i].nd) throw std::runtime_error("meta header mismatch");
+      w.val = reinterpret_cast<const double*>(vcur);
+      out[i] = w;
+      mcur += w.mbytes;
+      vcur += (size_t)w.nd * 8;
+    }
+  }
+  return out;
+}
+template <class T> static T rd(const uint8_t* b, size_t i) { T x; std::memcpy(&x, b + i * sizeof(T), sizeof(T)); return x; }
+
 static void emulate_family(const PatchFamily& F, const double* r, double* z) {
   const size_t np = F.pclass.size();
   for (int color = 0; color < F.ncolors; ++color)
@@ -23,94 +63,110 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
       if (F.pcolor[t] != color) continue;
       const ClassProgram& C = F.classes[F.pclass[t]];
       const double* V = F.values.data() + F.pvals[t];
+      std::vector<std::vector<uint8_t>> bufs;
+      const std::vector<PieceView> views = unit_views(C, V, bufs);
+      auto view = [&](const ClassProgram&, const double*, int i) { return views[i]; };
+      const int64_t base[3] = {F.pbase[3 * t], F.pbase[3 * t + 1], F.pbase[3 * t + 2]};
       const int n = C.n;
+      const int L = (int)C.lev.size();
       std::vector<double> v(n);
-      for (int q = 0; q < n; ++q) v[q] = r[F.pbase[3 * t + C.comp[q]] + C.offs[q]];
-      auto sliced = [&](const Sliced& S, int row, const double* x) {
-        double acc = 0;
-        int sl = row / 32, l = row % 32;
-        for (int kk = 0; kk < S.slice_w[sl]; ++kk) {
-          int e = S.slice_off[sl] + kk * 32 + l;
-          acc += V[S.vofs + e] * x[S.cols[e]];
-        }
-        return acc;
-      };
-      auto bval = [&](const Blocks& B, int slot, int i) { return V[B.vofs + (size_t)slot * B.nblk + i]; };
-      for (const Level& L : C.lev) {
-        const Blocks& B = L.blk;
-        for (int i = 0; i < B.nblk; ++i) {   // y = L^{-1} v on the block
-          int mm[3];
-          for (int j = 0; j < 3; ++j) mm[j] = (j < B.bs) ? B.mem[(size_t)j * B.nblk + i] : 0xFFFF;
-          double y[3];
-          int slot = 0;
-          for (int r = 0; r < B.bs; ++r) {
-            double s = (mm[r] != 0xFFFF) ? v[mm[r]] : 0.0;
-            for (int c = 0; c < r; ++c) s -= bval(B, slot + c, i) * y[c];
-            y[r] = s * bval(B, slot + r, i);
-            slot += r + 1;
-            if (mm[r] != 0xFFFF) v[mm[r]] = y[r];
+      auto code_ix = [&](int32_t code) { return base[code & 3] + (code >> 2); };
+      for (int t2 = 0; t2 < n; ++t2) v[t2] = r[code_ix(C.codes[t2])];
+      // sliced piece: per slice (start/32, count) then cols, rows = s*32 + lane
+      auto sliced_piece = [&](const PieceView& w, int nrows, auto&& emit) {
+        const int nsl = w.a1 - w.a0;
+        const uint8_t* cols = w.pb + 16 + 4 * nsl;
+        for (int ls = 0; ls < nsl; ++ls) {
+          const uint32_t info = rd<uint32_t>(w.pb + 16, ls);
+          const int st = 32 * (int)(info & 0xFFFF), cnt = (int)(info >> 16);
+          for (int lane = 0; lane < 32; ++lane) {
+            const int row = (w.a0 + ls) * 32 + lane;
+            double acc = 0;
+            for (int kk = 0; kk < cnt; ++kk) {
+              const int e = st + kk * 32 + lane;
+              acc += w.val[e] * v[rd<uint16_t>(cols, e)];
+            }
+            if (row < nrows) emit(row, acc);
           }
         }
-        for (int row = 0; row < L.w.nrows; ++row) v[L.w.r0 + row] -= sliced(L.w, row, v.data());
+      };
+      for (int l = 0; l < L; ++l) {
+        const Level& Lv = C.lev[l];
+        const int bs = Lv.blk.bs;
+        for (int pi = C.piv_b[l]; pi < C.w_b[l]; ++pi) {
+          PieceView w = view(C, V, pi);
+          const int cnt = w.a1 - w.a0;
+          auto pc = [&](int slot, int li) { return w.val[slot * cnt + li]; };
+          for (int li = 0; li < cnt; ++li) {
+            int mm[3];
+            for (int j = 0; j < 3; ++j) mm[j] = (j < bs) ? rd<uint16_t>(w.pb + 16, (size_t)j * cnt + li) : 0xFFFF;
+            double y[3] = {0, 0, 0};
+            for (int rr = 0; rr < bs; ++rr) {   // y = L^{-1} v
+              if (mm[rr] == 0xFFFF) continue;
+              double s = v[mm[rr]];
+              for (int c = 0; c < rr; ++c) s -= pc(rr * (rr + 1) / 2 + c, li) * y[c];
+              y[rr] = s * pc(rr * (rr + 1) / 2 + rr, li);
+            }
+            for (int rr = bs - 1; rr >= 0; --rr) {   // y^ = L^{-T} y
+              if (mm[rr] == 0xFFFF) continue;
+              double s = y[rr];
+              for (int c = rr + 1; c < bs; ++c)
+                if (mm[c] != 0xFFFF) s -= pc(c * (c + 1) / 2 + rr, li) * y[c];
+              y[rr] = s * pc(rr * (rr + 1) / 2 + rr, li);
+              v[mm[rr]] = y[rr];
+            }
+          }
+        }
+        for (int pi = C.w_b[l]; pi < C.w_e[l]; ++pi)
+          sliced_piece(view(C, V, pi), Lv.w.nrows, [&](int row, double acc) { v[Lv.w.r0 + row] -= acc; });
       }
       const int m = C.m, f0 = n - m;
       if (C.final_kind == FINAL_DENSE_INV) {
         const int T = (m + 31) / 32;
         std::vector<double> x(32 * T, 0.0), g(32 * T, 0.0);
         for (int i = 0; i < m; ++i) g[i] = v[f0 + i];
-        for (int I = 0; I < T; ++I)
-          for (int J = 0; J <= I; ++J) {
-            const double* tb = V + C.vofs_final + (size_t)(I * (I + 1) / 2 + J) * 1024;
-            for (int r = 0; r < 32; ++r)
-              for (int c = 0; c < 32; ++c) {
-                const double s = tb[r * 32 + ((c + r) & 31)];
-                x[32 * I + r] += s * g[32 * J + c];
-                if (I != J) x[32 * J + c] += s * g[32 * I + r];
-              }
-          }
+        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
+          PieceView w = view(C, V, pi);
+          const int I = w.a0, J = w.a1;
+          const double* tb = w.val;
+          for (int rr = 0; rr < 32; ++rr)   // tile = S (off-diagonal) or L' with S = L' + L'^T (diagonal)
+            for (int c = 0; c < 32; ++c) {
+              if (I == J && c > rr) continue;
+              const double s = (I == J) ? tb[tile_pos_diag(rr, c)] : tb[tile_pos_full(rr, c)];
+              x[32 * I + rr] += s * g[32 * J + c];
+              x[32 * J + c] += s * g[32 * I + rr];
+            }
+        }
         for (int i = 0; i < m; ++i) v[f0 + i] = x[i];
       } else {
-        const double* Lv = V + C.vofs_final;
-        const int nnz = C.icc_rowptr[m];
-        const double* LTv = Lv + nnz;
         double* y = v.data() + f0;
-        for (size_t l = 0; l + 1 < C.icc_level_ptr.size(); ++l)
-          for (int q = C.icc_level_ptr[l]; q < C.icc_level_ptr[l + 1]; ++q) {
-            int a = C.icc_level_rows[q];
-            int t0 = C.icc_rowptr[a], t1 = C.icc_rowptr[a + 1] - 1;
+        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
+          PieceView w = view(C, V, pi);
+          const int cnt = w.a1 - w.a0;
+          const uint8_t* rows = w.pb + 16;
+          const uint8_t* st = rows + 2 * cnt;
+          const uint8_t* cols = st + 2 * (cnt + 1);
+          for (int k = 0; k < cnt; ++k) {
+            const int a = rd<uint16_t>(rows, k), t0 = rd<uint16_t>(st, k), t1 = rd<uint16_t>(st, k + 1);
             double s = y[a];
-            for (int tt = t0; tt < t1; ++tt) s -= Lv[tt] * y[C.icc_col[tt]];
-            y[a] = s * Lv[t1];
-          }
-        for (size_t l = 0; l + 1 < C.icct_level_ptr.size(); ++l)
-          for (int q = C.icct_level_ptr[l]; q < C.icct_level_ptr[l + 1]; ++q) {
-            int b = C.icct_level_rows[q];
-            int t0 = C.icct_rowptr[b], t1 = C.icct_rowptr[b + 1];
-            double s = y[b];
-            for (int tt = t0 + 1; tt < t1; ++tt) s -= LTv[tt] * y[C.icct_col[tt]];
-            y[b] = s * LTv[t0];
-          }
-      }
-      for (int l = (int)C.lev.size() - 1; l >= 0; --l) {
-        const Level& L = C.lev[l];
-        std::vector<double> a(L.e1 - L.e0);
-        for (int row = 0; row < L.wt.nrows; ++row) a[row] = v[L.e0 + row] - sliced(L.wt, row, v.data());
-        const Blocks& B = L.blk;
-        for (int i = 0; i < B.nblk; ++i) {   // x = L^{-T} a on the block
-          int mm[3];
-          for (int j = 0; j < 3; ++j) mm[j] = (j < B.bs) ? B.mem[(size_t)j * B.nblk + i] : 0xFFFF;
-          double x[3] = {0, 0, 0};
-          for (int r = B.bs - 1; r >= 0; --r) {
-            if (mm[r] == 0xFFFF) continue;
-            double s = a[mm[r] - L.e0];
-            for (int c = r + 1; c < B.bs; ++c)
-              if (mm[c] != 0xFFFF) s -= bval(B, c * (c + 1) / 2 + r, i) * x[c];
-            x[r] = s * bval(B, r * (r + 1) / 2 + r, i);
-            v[mm[r]] = x[r];
+            if (C.pieces[pi].kind == PK_ICCF) {
+              for (int tt = t0; tt < t1 - 1; ++tt) s -= w.val[tt] * y[rd<uint16_t>(cols, tt)];
+              y[a] = s * w.val[t1 - 1];
+            } else {
+              for (int tt = t0 + 1; tt < t1; ++tt) s -= w.val[tt] * y[rd<uint16_t>(cols, tt)];
+              y[a] = s * w.val[t0];
+            }
           }
         }
       }
-      for (int q = 0; q < n; ++q) z[F.pbase[3 * t + C.comp[q]] + C.offs[q]] += v[q];
+      for (int l = L - 1; l >= 0; --l) {   // x_E = y^_E - W^ x_R, in place
+        const Level& Lv = C.lev[l];
+        std::vector<double> upd(Lv.wt.nrows, 0.0);
+        for (int pi = C.wt_b[l]; pi < C.wt_e[l]; ++pi)
+          sliced_piece(view(C, V, pi), Lv.wt.nrows, [&](int row, double acc) { upd[row] += acc; });
+        for (int row = 0; row < Lv.wt.nrows; ++row) v[Lv.e0 + row] -= upd[row];
+      }
+      for (int t2 = 0; t2 < n; ++t2) z[code_ix(C.codes[t2])] += v[t2];
     }
 }
 
