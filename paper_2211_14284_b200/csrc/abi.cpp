@@ -55,6 +55,8 @@ struct DevFamily {
   void release() {
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
+    if (launch.tm_dev) cudaFree(launch.tm_dev);
+    launch.tm_dev = nullptr;
   }
 };
 
@@ -88,7 +90,6 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
       us[i] = rm::DUnit{u.mofs, (int)((uint32_t)u.mbytes | ((uint32_t)u.np << 16) | (tile ? 0x80000000u : 0u)), u.sofs, u.nd};
       unit_max = std::max(unit_max, u.mbytes + 8 * u.nd);
     }
-    d.codes = F.upload(C.codes);
     d.units = F.upload(us);
     d.meta = F.upload(C.meta);
     d.nunits = (int)us.size();
@@ -96,7 +97,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     d.tile_p0 = C.tile_p0; d.tile_p1 = C.tile_p1;
     if (C.final_kind == rm::FINAL_DENSE_INV) {
       if ((C.m + 31) / 32 > 32) throw RmError(RM_EINVAL, "final Schur block larger than 1024");
-      auxn = std::max(auxn, ((C.m + 31) / 32) * 32 * (NW + 1));   // g + per-tile-warp partials
+      // g + per-tile-warp partials + final-block box list (uint16)
+      auxn = std::max(auxn, ((C.m + 31) / 32) * 32 * (NW + 1) + ((C.m + 31) / 32) * 8 + 2);
     } else {
       d.iccf_nlev = (int)C.iccf_lpiece.size() - 1;
       d.iccb_nlev = (int)C.iccb_lpiece.size() - 1;
@@ -119,18 +121,46 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
   for (int c = 0; c < P.ncolors; ++c) F.color_start[c + 1] += F.color_start[c];
   std::vector<int> fill(F.color_start.begin(), F.color_start.end() - 1);
   for (size_t t = 0; t < np; ++t) order[fill[P.pcolor[t]]++] = t;
-  std::vector<int> pc(np);
-  std::vector<long long> pb(3 * np), pv(np);
+  std::vector<int> pc(np), po(9 * np);
+  std::vector<long long> pv(np);
   int64_t bytes = 0;
   for (size_t i = 0; i < np; ++i) {
     size_t t = order[i];
     pc[i] = P.pclass[t];
-    for (int m = 0; m < 3; ++m) pb[3 * i + m] = P.pbase[3 * t + m];
+    for (int k = 0; k < 9; ++k) po[9 * i + k] = P.porig[9 * t + k];
     pv[i] = P.pvals[t];
     bytes += P.classes[P.pclass[t]].nvals * 8;
   }
   Lh.pclass = F.upload(pc);
-  Lh.pbase = F.upload(pb);
+  Lh.porig = F.upload(po);
+  // window boxes and the padded component layout of r / c (TMA row strides: multiples of 16 B)
+  Lh.ncomp = P.sp.ncomp;
+  for (int m = 0; m < 3; ++m) {
+    for (int d = 0; d < 3; ++d) Lh.box[m][d] = P.box[m][d];
+    Lh.boff[m] = P.boff[m];
+  }
+  Lh.boff[3] = P.boff[3];
+  Lh.box_total = P.box_total;
+  {
+    rm::PadLayout& pl = Lh.pad;
+    std::memset(&pl, 0, sizeof pl);
+    pl.ncomp = P.sp.ncomp;
+    long long o = 0, po2 = 0;
+    for (int m = 0; m < pl.ncomp; ++m) {
+      for (int d = 0; d < 3; ++d) pl.len[m][d] = P.sp.len(m, d);
+      pl.lxp[m] = pl.len[m][0] + (pl.len[m][0] & 1);
+      pl.off[m] = o; pl.poff[m] = po2;
+      o += pl.len[m][0] * pl.len[m][1] * pl.len[m][2];
+      po2 += pl.lxp[m] * pl.len[m][1] * pl.len[m][2];
+    }
+    for (int m = pl.ncomp; m <= 3; ++m) { pl.off[m] = o; pl.poff[m] = po2; }
+    Lh.npad = po2;
+    void *a = nullptr, *b = nullptr;
+    if (cudaMalloc(&a, po2 * sizeof(double)) != cudaSuccess || cudaMalloc(&b, po2 * sizeof(double)) != cudaSuccess)
+      throw RmError(RM_ENOMEM, "cudaMalloc failed (padded r / c)");
+    F.allocs.push_back(a); F.allocs.push_back(b);
+    Lh.rpad = static_cast<double*>(a); Lh.cpad = static_cast<double*>(b);
+  }
   Lh.npatch = (int)np;
   Lh.cs.ncolors = P.ncolors;
   for (int c = 0; c <= P.ncolors; ++c) Lh.cs.start[c] = F.color_start[c];

@@ -1,6 +1,7 @@
 // Device-side data structures shared by the kernels and the host launcher (abi.cpp).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace rm {
@@ -50,7 +51,6 @@ struct DClass {
   DLevel lev[RM_MAXLEV];
   const DUnit* units;
   const unsigned char* meta;     // class meta stream (L2-resident)
-  const int* codes;              // per position: (offs << 2) | comp, gather / scatter
   int nunits, ngs, tile_p0, tile_p1, iccf_nlev, iccb_nlev;
   const int *iccf_lp, *iccb_lp;  // per ICC level: first piece (size nlev + 1)
 };
@@ -61,28 +61,49 @@ struct ColorStarts { int ncolors; int start[RM_MAXCOLORS + 1]; };
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch);
+// Padded component layout of the patch kernel's input r and correction c: x rows padded to an
+// even length so that TMA tensor maps (row strides multiple of 16 bytes) can address them.
+struct PadLayout {
+  int ncomp;
+  long long len[3][3];      // [comp][dir] unpadded extents (x, y, z)
+  long long off[4];         // unpadded component offsets
+  long long poff[4];        // padded component offsets
+  long long lxp[3];         // padded x extents
+};
+struct TMaps { CUtensorMap r[3], c[3]; };   // 3D maps of the padded r / c components
+
 // Persistent streaming patch solve over one family: patches sorted by colour, CTA b takes
-// patches b, b + grid, ...; scatters wait for the previous colours through *done (zeroed here).
+// patches b, b + grid, ...; every patch works on its window box (gathered from rpad and
+// reduce-added into cpad with TMA tensor copies); reduce-adds follow the colour order through
+// *done (zeroed per launch).
 struct PatchLaunch {
   const DClass* classes;
   const int* pclass;
-  const long long* pbase;
   const long long* pvals;
+  const int* porig;      // per patch [comp][dir] box origins
   const double* vals;
   int npatch;
   ColorStarts cs;
-  unsigned* done;        // scattered patches (zeroed per launch)
+  unsigned* done;
+  int ncomp, box[3][3], boff[4], box_total;
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
-  size_t smem_fixed;     // barriers + v + pivots + aux (bytes)
+  size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)
   int ring_bytes;
   int grid;
   int unit_bytes_max;    // largest transfer unit (meta + values)
+  PadLayout pad;
+  long long npad;
+  double *rpad, *cpad;
+  TMaps tm;
+  TMaps* tm_dev;         // device copy of tm (owned by the launch plan)
+  unsigned long long* prof;   // RM_PROFILE=1 instrumentation counters (else null)
 };
+// u += omega * (patch corrections of one family applied to r); r, u in the vector layout
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st);
-// shared-memory plan: fixed part for the largest class, then the ring; returns the grid size
+// shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;
-constexpr int RM_PATCH_TILE_WARPS = 4;   // consumer warps sharing the dense tiles
+constexpr int RM_PATCH_TILE_WARPS = 8;   // consumer warps sharing the dense tiles
 cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,

@@ -14,23 +14,25 @@
 //
 // B200 structure.  Every factor value is read exactly once per sweep, so the kernel is an HBM
 // stream.  Each patch value block is laid out in consumption order (patches.hpp); consecutive
-// pieces form transfer units of <= 32 KB.  One producer warp per CTA streams the units of ALL
-// the CTA's patches HBM -> shared memory with cp.async.bulk (TMA bulk copies, SASS UBLKCP) into a
-// variable-size ring; it only waits for ring space, so the HBM stream stays busy across patches.
-// Two channels share the ring: the main channel (consumed by all 8 consumer warps) and the tile
-// channel (the dense-tile units, consumed by the 4 tile warps only).  While the tile warps
-// stream the tiles of patch i, the other 4 warps scatter patch i-1 and gather patch i+1 (second
-// v buffer), so the latency-bound global gathers/scatters and the colour wait leave the
-// critical path.
+// pieces form transfer units of <= 32 KB.  Warp roles per CTA (persistent, 2 CTAs per SM):
+//   producer  streams the units of ALL the CTA's patches HBM -> shared memory with cp.async.bulk
+//             (TMA bulk copies, SASS UBLKCP) into a variable-size ring, and loads each patch's
+//             window box of r with a TMA tensor copy (UTMALDG) into one of two box buffers;
+//   8 compute warps  run the elimination on the box (every metadata index is a box index);
+//             the dense-tile units travel in their own channel, consumed by 4 of them;
+//   store     reduce-adds the finished box into the correction c with a TMA tensor reduction
+//             (UTMAREDG .add, fp64, atomic per element) once the colour order allows.
+// There is no latency-bound global gather or scatter loop left on the compute warps.
 //
-// Colours.  Patches of one colour are disjoint, so their scatters commute; patches are sorted
-// by colour and a colour-c patch is scattered only after every patch of colours < c has been
-// scattered (a device counter, acquire/release).  Each u entry therefore receives its updates in
-// colour order: the sweep is bitwise deterministic, with one launch instead of one per colour.
-// All CTAs are co-resident (grid = occupancy x SMs) and take patches in increasing order (CTA b:
-// b, b + grid, ...), scattering each before the next-but-one; the wait cannot deadlock (the
-// pending scatter of lowest colour never waits; induction on the colour).  The value blocks are
-// laid out in HBM in that per-CTA order (abi.cpp), so every CTA streams one contiguous region.
+// Colours.  Patches of one colour are disjoint, so their corrections commute; patches are
+// sorted by colour and a colour-c box is reduce-added only after every box of colours < c has
+// landed (a device counter, acquire/release).  Each c entry therefore receives its updates in
+// colour order (boxes also add exact zeros outside their patch, which commute): the sweep is
+// bitwise deterministic, with one launch instead of one per colour.  All CTAs are co-resident
+// (grid = occupancy x SMs) and take patches in increasing order (CTA b: b, b + grid, ...); the
+// wait cannot deadlock (the pending reduction of lowest colour never waits; induction on the
+// colour).  The value blocks are laid out in HBM in that per-CTA order (abi.cpp), so every CTA
+// streams one contiguous region.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -44,14 +46,16 @@ namespace {
 
 constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // consumer warps
 constexpr int NT = NC * 32;
-constexpr int NTHR = NT + 32;                  // + producer warp
-constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps (the others do the side work)
-constexpr int NSW = NC - NTW;                  // side-work warps
+constexpr int NTHR = NT + 64;                  // + producer warp + store warp
+constexpr int WPROD = NC, WSTORE = NC + 1;
+constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps
 constexpr int NDESC = 16;                      // in-flight transfer units per channel
-constexpr int GB = 8;                          // gather/scatter loads in flight per thread
-// shared-memory header: per channel full/empty mbarriers and slot tables (offset, pieces, meta)
+// shared-memory header: per channel full/empty mbarriers and slot tables (offset, pieces, meta),
+// then the box-buffer barriers vfull[2] (TMA box landed), vdone[2] (compute warps done),
+// vempty[2] (store warp's reduction has read the box)
 constexpr int HDR_BYTES = 2 * (2 * NDESC * 8 + 3 * NDESC * 4);   // 896
-constexpr int BAR_BYTES = (HDR_BYTES + 127) & ~127;
+constexpr int VBAR_OFS = HDR_BYTES;
+constexpr int BAR_BYTES = (HDR_BYTES + 6 * 8 + 127) & ~127;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
@@ -77,10 +81,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
-// named barriers: 1 = all consumer warps, 2 = tile warps, 3 = side-work warps
+// named barriers: 1 = all compute warps, 2 = tile warps
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 __device__ __forceinline__ void tsync() { asm volatile("bar.sync 2, %0;" ::"n"(NTW * 32) : "memory"); }
-__device__ __forceinline__ void ssync() { asm volatile("bar.sync 3, %0;" ::"n"(NSW * 32) : "memory"); }
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src))
+               : "memory");
+}
+
+// one lane of a converged warp (PTX elect.sync)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -157,13 +180,14 @@ __device__ __forceinline__ Hdr hdr(const unsigned char* pb) {
 }
 
 // one sliced-ELL piece: slice s is owned by warp s % NC (so split slices stay in one warp);
-// meta = per slice (start/32 | count << 16), then uint16 columns of the piece's elements
+// meta = per slice (start/32 | count << 16), per slice 32 row boxes, column boxes (uint16)
 template <class Emit>
 __device__ __forceinline__ void sliced_piece(Piece_ pc, const double* v, int nrows, int warp, int lane, Emit&& emit) {
   const Hdr h = hdr(pc.pb);
   const int nsl = h.a1 - h.a0;
   const uint32_t* si = reinterpret_cast<const uint32_t*>(pc.pb + 16);
-  const uint16_t* cols = reinterpret_cast<const uint16_t*>(si + nsl);
+  const uint16_t* rows = reinterpret_cast<const uint16_t*>(si + nsl);
+  const uint16_t* cols = rows + 32 * nsl;
   const double* val = pc.val;
   for (int ls = (warp - h.a0 % NC + NC) % NC; ls < nsl; ls += NC) {
     const uint32_t info = si[ls];
@@ -179,8 +203,7 @@ __device__ __forceinline__ void sliced_piece(Piece_ pc, const double* v, int nro
       const int e = st + kk * 32;
       acc += val[e] * v[cols[e]];
     }
-    const int row = (h.a0 + ls) * 32 + lane;
-    if (row < nrows) emit(row, acc);
+    if ((h.a0 + ls) * 32 + lane < nrows) emit(rows[ls * 32 + lane], acc);
   }
 }
 
@@ -257,98 +280,34 @@ __device__ __forceinline__ void tile_gemv(const double* __restrict__ tile, const
   part[32 * J + 8 * b + a] += colsum;
 }
 
-// global index of gather code c for a patch with component bases b0, b1, b2
-__device__ __forceinline__ long long gidx(int c, long long b0, long long b1, long long b2) {
-  const int m = c & 3;
-  return (m == 0 ? b0 : (m == 1 ? b1 : b2)) + (c >> 2);
-}
-
 __device__ __forceinline__ int color_of(int q, const ColorStarts& cs) {
   int col = 0;
   while (col + 1 < cs.ncolors && cs.start[col + 1] <= q) ++col;
   return col;
 }
 
-struct Shared {
-  const DClass* classes;
-  const int* pclass;
-  const long long* pbase;
-  const double* r;
-  double* u;
-  double omega;
-  unsigned* done;
-};
-
-// v = R_q r  (threads t = 0..nth-1 of a group, GB loads in flight per thread)
-__device__ __forceinline__ void gather_patch(const Shared& S, int q, double* v, int t, int nth) {
-  const DClass& C = S.classes[S.pclass[q]];
-  const int n = C.n;
-  const int* codes = C.codes;
-  const long long b0 = S.pbase[3 * q], b1 = S.pbase[3 * q + 1], b2 = S.pbase[3 * q + 2];
-  for (int k0 = t; k0 < n; k0 += GB * nth) {
-    double x[GB];
-#pragma unroll
-    for (int k = 0; k < GB; ++k) {
-      const int kk = k0 + k * nth;
-      if (kk < n) x[k] = __ldg(S.r + gidx(__ldg(codes + kk), b0, b1, b2));
-    }
-#pragma unroll
-    for (int k = 0; k < GB; ++k) {
-      const int kk = k0 + k * nth;
-      if (kk < n) v[kk] = x[k];
-    }
-  }
-}
-
-// u += omega R_q^T v after the colours below q's are complete; `sync` is the group's barrier
-template <class Sync>
-__device__ __forceinline__ void scatter_patch(const Shared& S, const ColorStarts& cs, int q, const double* v, int t,
-                                              int nth, Sync&& sync) {
-  const DClass& C = S.classes[S.pclass[q]];
-  const int n = C.n;
-  const int* codes = C.codes;
-  const long long b0 = S.pbase[3 * q], b1 = S.pbase[3 * q + 1], b2 = S.pbase[3 * q + 2];
-  const int col = color_of(q, cs);
-  if (t == 0 && col > 0) {
-    const unsigned need = (unsigned)cs.start[col];
-    while (ld_acquire(S.done) < need) __nanosleep(64);
-  }
-  sync();
-  for (int k0 = t; k0 < n; k0 += GB * nth) {
-    double x[GB];
-#pragma unroll
-    for (int k = 0; k < GB; ++k) {
-      const int kk = k0 + k * nth;
-      if (kk < n) x[k] = __ldcg(S.u + gidx(__ldg(codes + kk), b0, b1, b2));
-    }
-#pragma unroll
-    for (int k = 0; k < GB; ++k) {
-      const int kk = k0 + k * nth;
-      if (kk < n) __stcg(S.u + gidx(__ldg(codes + kk), b0, b1, b2), x[k] + S.omega * v[kk]);
-    }
-  }
-  sync();
-  if (t == 0) {
-    __threadfence();
-    atomicAdd(S.done, 1u);
-  }
-}
-
 }  // namespace
 
-__global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __restrict__ classes,
+struct BoxGeom { int ncomp, box[3][3], boff[3], bytes; };
+
+__global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __restrict__ tmg,
+                                                               const DClass* __restrict__ classes,
                                                                const int* __restrict__ pclass,
-                                                               const long long* __restrict__ pbase,
                                                                const long long* __restrict__ pvals,
-                                                               const double* __restrict__ vals,
-                                                               const double* __restrict__ r, double* __restrict__ u,
-                                                               double omega, int npatch, ColorStarts cs,
-                                                               unsigned* __restrict__ done, uint32_t cap, int n_max) {
+                                                               const int* __restrict__ porig,
+                                                               const double* __restrict__ vals, int npatch,
+                                                               ColorStarts cs, BoxGeom bg,
+                                                               unsigned* __restrict__ done, uint32_t cap,
+                                                               int box_total, int dbg,
+                                                               unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* ring = smraw + BAR_BYTES;
+  uint64_t* vfull = reinterpret_cast<uint64_t*>(smraw + VBAR_OFS);
+  uint64_t* vdone = vfull + 2;
+  uint64_t* vempty = vfull + 4;
+  const int boxd = (box_total + 15) & ~15;   // doubles per box buffer (128-byte multiple)
   double* vbuf0 = reinterpret_cast<double*>(ring + cap);
-  double* vbuf1 = vbuf0 + ((n_max + 1) & ~1);
-  double* aux = vbuf1 + ((n_max + 1) & ~1);
+  double* aux = vbuf0 + 2 * boxd;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   if (tid == 0) {
@@ -356,11 +315,12 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
       ChanSm c = chan_sm(smraw, ch);
       for (int s = 0; s < NDESC; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], ch == 0 ? NC : NTW); }
     }
+    for (int b = 0; b < 2; ++b) { mbar_init(&vfull[b], 1); mbar_init(&vdone[b], NC); mbar_init(&vempty[b], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   // ================================================================== producer warp
-  if (warp == NC) {
+  if (warp == WPROD) {
     ChanSm cm[2] = {chan_sm(smraw, 0), chan_sm(smraw, 1)};
     uint32_t H = 0;
     int jc[2] = {0, 0}, relc[2] = {0, 0};
@@ -368,12 +328,40 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
     int fch[2 * NDESC], fseq[2 * NDESC];
     uint32_t fvs[2 * NDESC];
     int fh = 0, ft = 0;
-    for (int q = blockIdx.x; q < npatch; q += G) {   // static schedule; value blocks laid out per CTA
+    int i = 0;
+    unsigned long long pt_vempty = 0, pt_room = 0, pt0 = prof ? clock64() : 0;
+    for (int q = blockIdx.x; q < npatch; q += G, ++i) {   // static schedule; value blocks laid out per CTA
       const DClass& C = classes[pclass[q]];
       const double* V = vals + pvals[q];
       const DUnit* U = C.units;
       const unsigned char* M = C.meta;
       const int nu = C.nunits;
+      {   // window box of r -> box buffer i & 1 (after the store warp released it); the whole
+          // warp is converged and the operands are warp-uniform, one elected lane issues
+        const int b = i & 1;
+        const unsigned long long tw0 = prof ? clock64() : 0;
+        if (i >= 2) mbar_wait(&vempty[b], (uint32_t)((i >> 1) - 1) & 1u);
+        if (prof) pt_vempty += clock64() - tw0;
+        double* vb = vbuf0 + b * boxd;
+        int o[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) o[k] = (dbg & 8) ? 0 : __ldg(porig + 9 * q + k);
+        if (dbg & 16) vb = reinterpret_cast<double*>(ring);
+        if ((dbg & 4) && blockIdx.x < 3 && i < 2 && lane == 0)
+          printf("[dbg] cta %d q %d origin %d %d %d smem %u\n", blockIdx.x, q, o[0], o[1], o[2], smem_u32(vb));
+        __syncwarp();
+        if (elect_one()) {
+          if (dbg & 1) {
+            mbar_arrive(&vfull[b]);
+          } else {
+            mbar_arrive_expect_tx(&vfull[b], (uint32_t)bg.bytes);
+            tma_load_3d(vb + bg.boff[0], &tmg->r[0], o[0], o[1], o[2], &vfull[b]);
+            if (bg.ncomp > 1) tma_load_3d(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
+            if (bg.ncomp > 2) tma_load_3d(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
+          }
+        }
+        __syncwarp();
+      }
       for (int i0 = 0; i0 < nu; i0 += 32) {
         int4 d = make_int4(0, 0, 0, 0);
         if (i0 + lane < nu) d = *reinterpret_cast<const int4*>(U + i0 + lane);
@@ -387,12 +375,14 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
             const uint32_t vb = (uint32_t)nd * 8u, tot = mb + vb;
             const uint32_t vs = ring_place(H, tot, cap);
             // room: this channel's slot must be free and [vs, H) must not overlap unreleased units
+            const unsigned long long tr0 = prof ? clock64() : 0;
             while (ft > fh && (jc[ch] - relc[ch] >= NDESC || H - fvs[fh % (2 * NDESC)] > cap)) {
               const int oc = fch[fh % (2 * NDESC)], os = fseq[fh % (2 * NDESC)];
               mbar_wait(&cm[oc].empty[os % NDESC], (uint32_t)(os / NDESC) & 1u);
               ++relc[oc];
               ++fh;
             }
+            if (prof) pt_room += clock64() - tr0;
             const int sl = jc[ch] % NDESC;
             ChanSm& c = cm[ch];
             c.ofs[sl] = (int)(vs % cap);
@@ -411,21 +401,68 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
         }
       }
     }
+    if (prof && lane == 0) {
+      unsigned long long* o = prof + 24 * blockIdx.x;
+      o[0] = clock64() - pt0; o[1] = pt_vempty; o[2] = pt_room;
+    }
     return;
   }
-  // ================================================================== consumer warps
-  const Shared S{classes, pclass, pbase, r, u, omega, done};
+  // ================================================================== store warp
+  if (warp == WSTORE) {   // whole warp converged; one elected lane issues and waits on the TMA
+    int i = 0;
+    unsigned long long st_done = 0, st_col = 0, st_red = 0, st0 = prof ? clock64() : 0;
+    for (int q = blockIdx.x; q < npatch; q += G, ++i) {
+      const int b = i & 1;
+      unsigned long long ta = prof ? clock64() : 0;
+      mbar_wait(&vdone[b], (uint32_t)(i >> 1) & 1u);
+      if (prof) { const unsigned long long tb = clock64(); st_done += tb - ta; ta = tb; }
+      const int col = color_of(q, cs);
+      if (col > 0) {
+        const unsigned need = (unsigned)cs.start[col];
+        while (ld_acquire(done) < need) __nanosleep(64);
+      }
+      if (prof) { const unsigned long long tb = clock64(); st_col += tb - ta; ta = tb; }
+      int o[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) o[k] = __ldg(porig + 9 * q + k);
+      const double* vb = vbuf0 + b * boxd;
+      __syncwarp();
+      if (elect_one()) {
+        if (!(dbg & 2)) {
+          tma_reduce_add_3d(&tmg->c[0], o[0], o[1], o[2], vb + bg.boff[0]);
+          if (bg.ncomp > 1) tma_reduce_add_3d(&tmg->c[1], o[3], o[4], o[5], vb + bg.boff[1]);
+          if (bg.ncomp > 2) tma_reduce_add_3d(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&vempty[b]);   // the producer may reload this box buffer
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        atomicAdd(done, 1u);
+      }
+      __syncwarp();
+      if (prof) st_red += clock64() - ta;
+    }
+    if (prof && lane == 0) {
+      unsigned long long* o = prof + 24 * blockIdx.x;
+      o[3] = clock64() - st0; o[4] = st_done; o[5] = st_col; o[6] = st_red;
+    }
+    return;
+  }
+  // ================================================================== compute warps
   Consumer cn{chan_sm(smraw, 0), ring, 0, 0, nullptr, nullptr};   // main channel
   Consumer ct{chan_sm(smraw, 1), ring, 0, 0, nullptr, nullptr};   // tile channel (tile warps)
-  double* v = vbuf0;
-  double* vo = vbuf1;
-  if ((int)blockIdx.x < npatch) gather_patch(S, blockIdx.x, v, tid, NT);
-  csync();
-  int qlast = -1;
-  for (int q = blockIdx.x; q < npatch; q += G) {
+  const bool pf = prof != nullptr && (tid == 0 || tid == 32 * (NC - 1));
+  unsigned long long ct_box = 0, ct_fwd = 0, ct_fin = 0, ct_bwd = 0, ct0 = pf ? clock64() : 0, tm0 = 0;
+  int i = 0;
+  for (int q = blockIdx.x; q < npatch; q += G, ++i) {
     const DClass& C = classes[pclass[q]];
-    const int n = C.n;
-    const int qprev = q - G, qnext = q + G;
+    const int b = i & 1;
+    double* v = vbuf0 + b * boxd;
+    if (pf) tm0 = clock64();
+    mbar_wait(&vfull[b], (uint32_t)(i >> 1) & 1u);   // the window box of r has landed
+    if (pf) { const unsigned long long t = clock64(); ct_box += t - tm0; tm0 = t; }
     // ---- forward eliminations
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
@@ -468,31 +505,41 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
         cn.release(lane);
       }
       csync();
-      const int r0 = L.w.r0;
       for (int pi = L.w_b; pi < L.w_e; ++pi) {
         const Piece_ pc = cn.acquire();
-        sliced_piece(pc, v, L.w.nrows, warp, lane, [&](int row, double acc) { v[r0 + row] -= acc; });
+        sliced_piece(pc, v, L.w.nrows, warp, lane, [&](int rb, double acc) { v[rb] -= acc; });
         cn.release(lane);
       }
       csync();
     }
-    // ---- final Schur block, with the side work (scatter of q - G, gather of q + G) overlapped
-    const int m = C.m, f0 = n - m;
-    if (C.final_kind == 0 && m > 0) {
-      const int T = (m + 31) >> 5, mpad = 32 * T;
-      double* g = aux;             // padded copy of v_F
-      double* parts = aux + mpad;  // per-tile-warp partial results
-      if (warp < NTW) {
-        const int tt = tid;        // 0 .. 32*NTW-1
-        for (int jj = tt; jj < mpad; jj += 32 * NTW) g[jj] = (jj < m) ? v[f0 + jj] : 0.0;
-        for (int jj = lane; jj < mpad; jj += 32) parts[warp * mpad + jj] = 0.0;
+    if (pf) { const unsigned long long t = clock64(); ct_fwd += t - tm0; tm0 = t; }
+    // ---- final Schur block
+    const int m = C.m;
+    if (C.final_kind == 0) {
+      if (m > 0 && warp < NTW) {
+        const int T = (m + 31) >> 5, mpad = 32 * T;
+        double* g = aux;                                              // padded copy of v_F
+        double* parts = aux + mpad;                                   // per-tile-warp partials
+        uint16_t* fb = reinterpret_cast<uint16_t*>(parts + NTW * mpad);   // final-block boxes
+        const int tt = tid;   // 0 .. 32*NTW-1
+        {
+          const Piece_ pc = ct.acquire();   // FINAL piece: boxes of the final block
+          const uint16_t* fbs = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+          for (int jj = tt; jj < mpad; jj += 32 * NTW) {
+            const int bx = (jj < m) ? fbs[jj] : 0;
+            fb[jj] = (uint16_t)bx;
+            g[jj] = (jj < m) ? v[bx] : 0.0;
+          }
+          for (int jj = lane; jj < mpad; jj += 32) parts[warp * mpad + jj] = 0.0;
+          ct.release(lane);
+        }
         tsync();
         // whole tiles per warp (tile t of the patch -> warp t % NTW), lane-block layout
         // (patches.hpp): 16 conflict-free LDS.128 and 64 independent DFMA per lane and tile
         double* mypart = parts + warp * mpad;
-        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
+        for (int pi = C.tile_p0 + 1; pi < C.tile_p1; ++pi) {
           const Piece_ pc = ct.acquire();
-          if (((pi - C.tile_p0) % NTW) == warp) {
+          if (((pi - C.tile_p0 - 1) % NTW) == warp) {
             const Hdr h = hdr(pc.pb);
             tile_gemv(pc.val, g, mypart, h.a0, h.a1, lane);
           }
@@ -503,76 +550,129 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const DClass* __r
           double x = 0.0;
 #pragma unroll
           for (int w = 0; w < NTW; ++w) x += parts[w * mpad + jj];
-          v[f0 + jj] = x;
+          v[fb[jj]] = x;
         }
-      } else {
-        const int ts = tid - 32 * NTW;
-        if (qprev >= 0) scatter_patch(S, cs, qprev, vo, ts, 32 * NSW, [] { ssync(); });
-        if (qnext < npatch) gather_patch(S, qnext, vo, ts, 32 * NSW);
       }
       csync();
     } else {
-      if (C.final_kind != 0) {
-        // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
-        // then backward rows of L^T by levels (diag first); rows of one level are independent.
-        // meta = uint16 rows, uint16 value starts (cnt + 1), uint16 columns
-        double* y = v + f0;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int nl = pass == 0 ? C.iccf_nlev : C.iccb_nlev;
-          const int* lp = pass == 0 ? C.iccf_lp : C.iccb_lp;
-          for (int l = 0; l < nl; ++l) {
-            const int pe = lp[l + 1];
-            for (int pi = lp[l]; pi < pe; ++pi) {
-              const Piece_ pc = cn.acquire();
-              const Hdr h = hdr(pc.pb);
-              const int cnt = h.a1 - h.a0;
-              const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
-              const uint16_t* st = rows + cnt;
-              const uint16_t* cols = st + cnt + 1;
-              const double* val = pc.val;
-              for (int k = tid; k < cnt; k += NT) {
-                const int a = rows[k], t0 = st[k], t1 = st[k + 1];
-                double s = y[a];
-                if (pass == 0) {
-                  for (int t = t0; t < t1 - 1; ++t) s -= val[t] * y[cols[t]];
-                  y[a] = s * val[t1 - 1];
-                } else {
-                  for (int t = t0 + 1; t < t1; ++t) s -= val[t] * y[cols[t]];
-                  y[a] = s * val[t0];
-                }
+      // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
+      // then backward rows of L^T by levels (diag first); rows of one level are independent.
+      // meta = uint16 row boxes, uint16 value starts (cnt + 1), uint16 column boxes
+      for (int pass = 0; pass < 2; ++pass) {
+        const int nl = pass == 0 ? C.iccf_nlev : C.iccb_nlev;
+        const int* lp = pass == 0 ? C.iccf_lp : C.iccb_lp;
+        for (int l = 0; l < nl; ++l) {
+          const int pe = lp[l + 1];
+          for (int pi = lp[l]; pi < pe; ++pi) {
+            const Piece_ pc = cn.acquire();
+            const Hdr h = hdr(pc.pb);
+            const int cnt = h.a1 - h.a0;
+            const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+            const uint16_t* st = rows + cnt;
+            const uint16_t* cols = st + cnt + 1;
+            const double* val = pc.val;
+            for (int k = tid; k < cnt; k += NT) {
+              const int a = rows[k], t0 = st[k], t1 = st[k + 1];
+              double s = v[a];
+              if (pass == 0) {
+                for (int t = t0; t < t1 - 1; ++t) s -= val[t] * v[cols[t]];
+                v[a] = s * val[t1 - 1];
+              } else {
+                for (int t = t0 + 1; t < t1; ++t) s -= val[t] * v[cols[t]];
+                v[a] = s * val[t0];
               }
-              cn.release(lane);
             }
-            csync();
+            cn.release(lane);
           }
+          csync();
         }
       }
-      if (qprev >= 0) scatter_patch(S, cs, qprev, vo, tid, NT, [] { csync(); });
-      if (qnext < npatch) gather_patch(S, qnext, vo, tid, NT);
-      csync();
     }
+    if (pf) { const unsigned long long t = clock64(); ct_fin += t - tm0; tm0 = t; }
     // ---- backward substitution: x_E = y^_E - W^ x_R  (W^ = P_EE^{-1} P_ER, in place)
     for (int l = nlev - 1; l >= 0; --l) {
       const DLevel& L = C.lev[l];
-      const int e0 = L.e0;
       for (int pi = L.wt_b; pi < L.wt_e; ++pi) {
         const Piece_ pc = cn.acquire();
-        sliced_piece(pc, v, L.wt.nrows, warp, lane, [&](int row, double acc) { v[e0 + row] -= acc; });
+        sliced_piece(pc, v, L.wt.nrows, warp, lane, [&](int rb, double acc) { v[rb] -= acc; });
         cn.release(lane);
       }
       csync();
     }
-    double* tmp = v;
-    v = vo;
-    vo = tmp;
-    qlast = q;
+    // ---- zero the box entries outside the patch, hand the box to the store warp
+    {
+      const Piece_ pc = cn.acquire();   // ZERO piece
+      const Hdr h = hdr(pc.pb);
+      const uint16_t* zl = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+      for (int k = tid; k < h.a1 - h.a0; k += NT) v[zl[k]] = 0.0;
+      cn.release(lane);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&vdone[b]);
+    if (pf) { const unsigned long long t = clock64(); ct_bwd += t - tm0; }
   }
-  // ---- drain: scatter the last patch
-  if (qlast >= 0) scatter_patch(S, cs, qlast, vo, tid, NT, [] { csync(); });
+  if (pf) {
+    unsigned long long* o = prof + 24 * blockIdx.x + (tid == 0 ? 7 : 12);
+    o[0] = clock64() - ct0; o[1] = ct_box; o[2] = ct_fwd; o[3] = ct_fin; o[4] = ct_bwd;
+  }
 }
 
+namespace {
+
+__global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ r, double* __restrict__ rp,
+                           long long npad) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= npad) return;
+  int m = 0;
+  while (m + 1 < P.ncomp && g >= P.poff[m + 1]) ++m;
+  const long long rr = g - P.poff[m];
+  const long long x = rr % P.lxp[m], yz = rr / P.lxp[m];
+  rp[g] = (x < P.len[m][0]) ? r[P.off[m] + yz * P.len[m][0] + x] : 0.0;
+}
+
+__global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* __restrict__ u,
+                                  double omega, long long n) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  int m = 0;
+  while (m + 1 < P.ncomp && g >= P.off[m + 1]) ++m;
+  const long long rr = g - P.off[m];
+  const long long x = rr % P.len[m][0], yz = rr / P.len[m][0];
+  u[g] += omega * cp[P.poff[m] + yz * P.lxp[m] + x];
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t encode_maps(PatchLaunch& L) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult qr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || !enc) return cudaErrorNotSupported;
+  }
+  for (int m = 0; m < L.pad.ncomp; ++m) {
+    cuuint64_t dims[3] = {(cuuint64_t)L.pad.lxp[m], (cuuint64_t)L.pad.len[m][1], (cuuint64_t)L.pad.len[m][2]};
+    cuuint64_t strides[2] = {(cuuint64_t)L.pad.lxp[m] * 8, (cuuint64_t)L.pad.lxp[m] * L.pad.len[m][1] * 8};
+    cuuint32_t box[3] = {(cuuint32_t)L.box[m][0], (cuuint32_t)L.box[m][1], (cuuint32_t)L.box[m][2]}, es[3] = {1, 1, 1};
+    for (int w = 0; w < 2; ++w) {
+      double* base = (w == 0 ? L.rpad : L.cpad) + L.pad.poff[m];
+      CUresult r = enc(w == 0 ? &L.tm.r[m] : &L.tm.c[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
 cudaError_t plan_patch_solve(PatchLaunch& L) {
-  L.smem_fixed = BAR_BYTES + (size_t)(2 * ((L.n_max + 1) & ~1) + L.aux_max) * sizeof(double);
+  const size_t boxd = (size_t)((L.box_total + 15) & ~15);
+  L.smem_fixed = BAR_BYTES + (2 * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -580,7 +680,7 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
     return e;
-  // two CTAs per SM when the fixed part leaves >= 64 KB of ring each, else one CTA with the rest
+  // two CTAs per SM when the fixed part leaves >= 48 KB of ring each, else one CTA with the rest
   // (env RM_CTAS_PER_SM / RM_RING_KB override for experiments); the ring must hold 2 units
   const size_t per_sm = 228 * 1024;
   int want = 2;
@@ -588,7 +688,7 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   size_t ring = 0;
   for (; want >= 1; --want) {
     const size_t avail = std::min<size_t>(per_sm / want - 1024, optin);
-    if (avail >= L.smem_fixed + 64 * 1024) { ring = avail - L.smem_fixed; break; }
+    if (avail >= L.smem_fixed + std::max<size_t>(48 * 1024, 2 * (size_t)L.unit_bytes_max)) { ring = avail - L.smem_fixed; break; }
   }
   if (want < 1) {
     if ((size_t)optin < L.smem_fixed + 2 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
@@ -604,19 +704,58 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
     return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   L.grid = std::max(1, std::min(L.npatch, occ * nsm));
+  if ((e = encode_maps(L)) != cudaSuccess) return e;
+  if (getenv("RM_PROFILE") && !L.prof && (e = cudaMalloc(&L.prof, (size_t)24 * 8 * L.grid)) != cudaSuccess) return e;
+  // descriptors live in global memory (64-byte aligned allocation), read by the TMA unit
+  if (!L.tm_dev && (e = cudaMalloc(&L.tm_dev, sizeof(TMaps))) != cudaSuccess) return e;
+  if ((e = cudaMemcpy(L.tm_dev, &L.tm, sizeof(TMaps), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+  if (getenv("RM_VERBOSE")) {
+    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(&L.tm.r[0]);
+    fprintf(stderr, "[rm] tmap r0:");
+    for (int k = 0; k < 16; ++k) fprintf(stderr, " %llx", w[k]);
+    fprintf(stderr, "\n[rm] rpad %p dims %lld %lld %lld box %d %d %d\n", (void*)L.rpad, L.pad.lxp[0], L.pad.len[0][1],
+            L.pad.len[0][2], L.box[0][0], L.box[0][1], L.box[0][2]);
+  }
   if (getenv("RM_VERBOSE"))
-    fprintf(stderr, "[rm] patch plan: npatch=%d n_max=%d aux_max=%d fixed=%zu ring=%d occ=%d grid=%d\n", L.npatch,
-            L.n_max, L.aux_max, L.smem_fixed, L.ring_bytes, occ, L.grid);
+    fprintf(stderr, "[rm] patch plan: npatch=%d box=%d aux_max=%d fixed=%zu ring=%d occ=%d grid=%d\n", L.npatch,
+            L.box_total, L.aux_max, L.smem_fixed, L.ring_bytes, occ, L.grid);
   return cudaSuccess;
 }
 
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st) {
   if (L.npatch <= 0) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st);
-  if (e != cudaSuccess) return e;
+  const long long n = L.pad.off[L.pad.ncomp];
+  cudaError_t e;
+  pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  BoxGeom bg;
+  bg.ncomp = L.ncomp;
+  bg.bytes = 0;
+  for (int m = 0; m < 3; ++m) {
+    for (int d = 0; d < 3; ++d) bg.box[m][d] = L.box[m][d];
+    bg.boff[m] = L.boff[m];
+    if (m < L.ncomp) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
+  }
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes, st>>>(
-      L.classes, L.pclass, L.pbase, L.pvals, L.vals, r, u, omega, L.npatch, L.cs, L.done, (uint32_t)L.ring_bytes,
-      L.n_max);
+      L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes, L.box_total,
+      getenv("RM_DEBUG_TMA") ? atoi(getenv("RM_DEBUG_TMA")) : 0, L.prof);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    std::vector<unsigned long long> h((size_t)24 * L.grid);
+    if ((e = cudaMemcpy(h.data(), L.prof, h.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;
+    double a[24] = {0};
+    for (int b = 0; b < L.grid; ++b)
+      for (int k = 0; k < 24; ++k) a[k] += (double)h[24 * b + k] / L.grid / 1e3;
+    fprintf(stderr,
+            "[rm prof kcyc] producer total %.0f vempty-wait %.0f room-wait %.0f | store total %.0f wait-done %.0f colour %.0f "
+            "reduce %.0f | tile-warp total %.0f box %.0f fwd %.0f final %.0f bwd %.0f | side-warp total %.0f box %.0f fwd "
+            "%.0f final %.0f bwd %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15], a[16]);
+  }
+  unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
   return cudaGetLastError();
 }
 

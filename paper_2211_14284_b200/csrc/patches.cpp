@@ -156,7 +156,7 @@ void build_blocks(Blocks& B, const std::vector<std::vector<int>>& blocks) {
 
 // ---------------------------------------------------------------- stream layout (patches.hpp)
 void add_piece(ClassProgram& C, int64_t& s, Piece p) {
-  if (p.nd <= 0 && p.kind != PK_GATHER && p.kind != PK_SCATTER) return;
+  if (p.nd <= 0 && p.kind != PK_FINAL && p.kind != PK_ZERO) return;
   p.nd = (p.nd + 1) & ~1;
   if (p.nd > kPieceMax) throw std::runtime_error("stream piece larger than kPieceMax");
   p.sofs = (int)s;
@@ -185,40 +185,33 @@ void sliced_pieces(ClassProgram& C, int64_t& s, int kind, int lev, const Sliced&
   }
 }
 
-// class meta stream: one 16-byte-aligned block per piece, header {a0, a1, e0, mbytes}
+// class meta stream: one 16-byte-aligned block per piece, header {a0, a1, e0, mbytes | nd << 16};
+// every DoF reference is a BOX index (C.bidx): the patch's working vector is its window box
 void build_meta(ClassProgram& C) {
   std::vector<uint8_t>& M = C.meta;
   M.clear();
   auto put = [&](const void* p, size_t nb) { const uint8_t* b = (const uint8_t*)p; M.insert(M.end(), b, b + nb); };
   auto put16 = [&](int x) { uint16_t h = (uint16_t)x; if (x < 0 || x > 0xFFFF) throw std::runtime_error("meta u16 overflow"); put(&h, 2); };
   auto align16 = [&]() { while (M.size() & 15) M.push_back(0); };
+  const int f0 = C.n - C.m;
   for (size_t i = 0; i < C.pieces.size(); ++i) {
     Piece& p = C.pieces[i];
-    if (p.kind == PK_SCATTER) {   // reuses the GATHER block of the same positions
-      const Piece& g = C.pieces[i - (C.pieces.size() - C.ngs)];
-      p.mofs = g.mofs; p.mbytes = g.mbytes;
-      continue;
-    }
+    if (p.kind == PK_ZERO) p.a1 = (int)C.zlist.size();
     const size_t at = M.size();
     int32_t hdr[4] = {p.a0, p.a1, p.e0, 0};
     put(hdr, 16);
     switch (p.kind) {
-      case PK_GATHER:
-        for (int t = p.a0; t < p.a1; ++t) {
-          const int64_t code = ((int64_t)C.offs[t] << 2) | C.comp[t];
-          if (code > INT32_MAX || code < INT32_MIN) throw std::runtime_error("gather code overflow");
-          int32_t c32 = (int32_t)code;
-          put(&c32, 4);
-        }
-        break;
-      case PK_PIV: {
+      case PK_PIV: {   // uint16 block members [slot][block]
         const Blocks& B = C.lev[p.lev].blk;
         for (int sl = 0; sl < B.bs; ++sl)
-          for (int b = p.a0; b < p.a1; ++b) put16(B.mem[(size_t)sl * B.nblk + b]);
+          for (int b = p.a0; b < p.a1; ++b) {
+            const int mpos = B.mem[(size_t)sl * B.nblk + b];
+            put16(mpos == 0xFFFF ? 0xFFFF : C.bidx[mpos]);
+          }
         break;
       }
       case PK_W:
-      case PK_WT: {
+      case PK_WT: {   // per slice (start/32 | count << 16); per slice 32 row boxes; column boxes
         const Sliced& S = (p.kind == PK_W) ? C.lev[p.lev].w : C.lev[p.lev].wt;
         for (int sl = p.a0; sl < p.a1; ++sl) {
           const int o = S.slice_off[sl];
@@ -227,22 +220,35 @@ void build_meta(ClassProgram& C) {
           const uint32_t info = (uint32_t)(start / 32) | ((uint32_t)std::max(0, k1 - k0) << 16);
           put(&info, 4);
         }
-        for (int e = p.e0; e < p.e0 + p.nd; ++e) put(&S.cols[e], 2);
+        for (int sl = p.a0; sl < p.a1; ++sl)
+          for (int l = 0; l < 32; ++l) {
+            const int row = sl * 32 + l;
+            put16(row < S.nrows ? C.bidx[S.r0 + row] : 0);
+          }
+        for (int e = p.e0; e < p.e0 + p.nd; ++e) put16(C.bidx[S.cols[e]]);
         break;
       }
       case PK_TILE:
         break;
+      case PK_FINAL:   // uint16 boxes of the final block's positions
+        for (int j = 0; j < C.m; ++j) put16(C.bidx[f0 + j]);
+        break;
+      case PK_ZERO:    // uint16 boxes that are not DoFs of the patch (zeroed before the reduce-add)
+        for (int z : C.zlist) put16(z);
+        break;
       case PK_ICCF:
-      case PK_ICCB: {
+      case PK_ICCB: {  // uint16 row boxes, uint16 value starts (cnt + 1), uint16 column boxes
         const bool f = p.kind == PK_ICCF;
         const std::vector<int>& row = f ? C.iccf_row : C.iccb_row;
         const std::vector<int>& rp = f ? C.iccf_rp : C.iccb_rp;
         const std::vector<int>& col = f ? C.iccf_col : C.iccb_col;
-        for (int q = p.a0; q < p.a1; ++q) put16(row[q]);
+        for (int q = p.a0; q < p.a1; ++q) put16(C.bidx[f0 + row[q]]);
         for (int q = p.a0; q <= p.a1; ++q) put16(rp[q] - p.e0);
-        for (int t = rp[p.a0]; t < rp[p.a1]; ++t) put16(col[t]);
+        for (int t = rp[p.a0]; t < rp[p.a1]; ++t) put16(C.bidx[f0 + col[t]]);
         break;
       }
+      default:
+        throw std::runtime_error("build_meta: piece kind");
     }
     align16();
     p.mofs = (int)at;
@@ -251,19 +257,16 @@ void build_meta(ClassProgram& C) {
     const uint32_t w3 = (uint32_t)p.mbytes | ((uint32_t)p.nd << 16);
     std::memcpy(&M[at + 12], &w3, 4);
   }
-  // transfer units: consecutive pieces whose metas and values are both contiguous
+  // transfer units: consecutive pieces (metas and values both contiguous), split at the
+  // dense-tile section (its own channel)
   static const int unit_vals = getenv("RM_UNIT_VALS") ? atoi(getenv("RM_UNIT_VALS")) : kUnitVals;
   C.units.clear();
-  const int ns = (int)C.pieces.size() - C.ngs;   // first SCATTER piece
   for (int i = 0; i < (int)C.pieces.size();) {
     Unit u{i, 0, C.pieces[i].mofs, 0, C.pieces[i].sofs, 0};
     while (i < (int)C.pieces.size()) {
       const Piece& p = C.pieces[i];
-      const bool boundary = u.np > 0 && (i == C.ngs || i == ns || i == C.tile_p0 || i == C.tile_p1);
+      const bool boundary = u.np > 0 && (i == C.tile_p0 || i == C.tile_p1);
       if (u.np > 0 && (boundary || u.nd + p.nd > unit_vals || u.mbytes + p.mbytes > kUnitMeta)) break;
-      if (p.mofs != u.mofs + u.mbytes || p.sofs != u.sofs + u.nd) {
-        if (u.np > 0) break;
-      }
       u.np++; u.mbytes += p.mbytes; u.nd += p.nd;
       ++i;
     }
@@ -271,7 +274,7 @@ void build_meta(ClassProgram& C) {
   }
   C.tu0 = C.tu1 = 0;
   for (size_t k = 0; k < C.units.size(); ++k) {
-    const bool tile = C.units[k].p0 >= C.tile_p0 && C.units[k].p0 < C.tile_p1 && C.final_kind == FINAL_DENSE_INV;
+    const bool tile = C.final_kind == FINAL_DENSE_INV && C.m > 0 && C.units[k].p0 >= C.tile_p0 && C.units[k].p0 < C.tile_p1;
     if (tile && C.tu1 == 0) C.tu0 = (int)k;
     if (tile) C.tu1 = (int)k + 1;
   }
@@ -280,13 +283,7 @@ void build_meta(ClassProgram& C) {
 void build_stream(ClassProgram& C) {
   C.pieces.clear();
   const int L = (int)C.lev.size();
-  C.ngs = 0;   // gather/scatter codes travel in C.codes (read from L2 by the side-work warps)
-  C.codes.resize(C.n);
-  for (int t = 0; t < C.n; ++t) {
-    const int64_t code = ((int64_t)C.offs[t] << 2) | C.comp[t];
-    if (code > INT32_MAX || code < INT32_MIN) throw std::runtime_error("gather code overflow");
-    C.codes[t] = (int32_t)code;
-  }
+  C.ngs = 0;
   C.piv_b.assign(L, 0); C.w_b.assign(L, 0); C.w_e.assign(L, 0); C.wt_b.assign(L, 0); C.wt_e.assign(L, 0);
   C.piv_per.assign(L, 1); C.piv_ofs.assign(L, 0); C.mem_ofs.assign(L, 0);
   int64_t s = 0;
@@ -315,6 +312,7 @@ void build_stream(ClassProgram& C) {
   const int m = C.m;
   if (C.final_kind == FINAL_DENSE_INV) {
     const int T = (m + 31) / 32;
+    if (m > 0) add_piece(C, s, Piece{PK_FINAL, 0, 0, m, 0, 0, 0, -1});
     for (int I = 0; I < T; ++I)
       for (int J = 0; J <= I; ++J)
         add_piece(C, s, Piece{PK_TILE, 0, I, J, 0, 0, I == J ? kTileDiag : 1024,
@@ -379,8 +377,8 @@ void build_stream(ClassProgram& C) {
     sliced_pieces(C, s, PK_WT, l, C.lev[l].wt);
     C.wt_e[l] = (int)C.pieces.size();
   }
+  add_piece(C, s, Piece{PK_ZERO, 0, 0, 0, 0, 0, 0, -1});   // a1 = zero-list length, set by build_meta
   C.nvals = s;
-  build_meta(C);
 }
 
 // canonical (factorization-order) block -> stream block
@@ -414,6 +412,8 @@ void pack_stream(const ClassProgram& C, const double* canon, double* out) {
         break;
       case PK_ICCB:
         for (int t = C.iccb_rp[p.a0]; t < C.iccb_rp[p.a1]; ++t) o[t - p.e0] = canon[C.vofs_final + C.iccb_src[t]];
+        break;
+      default:   // metadata-only pieces (FINAL, ZERO)
         break;
     }
   }
@@ -463,9 +463,15 @@ struct Builder {
   void build_class(const Entity& e, ClassProgram& C) {
     const int p = sp.p;
     std::vector<NatDof> dofs;
+    int wlo_abs[3][3] = {{0}};
     for (int m = 0; m < sp.ncomp; ++m) {
       int lo[3], hi[3];
-      for (int d = 0; d < 3; ++d) window(e.s[d], sp.fam[m][d], p, sp.n[d], lo[d], hi[d]);
+      for (int d = 0; d < 3; ++d) {
+        window(e.s[d], sp.fam[m][d], p, sp.n[d], lo[d], hi[d]);
+        wlo_abs[m][d] = lo[d];
+        C.wlo[m][d] = lo[d] - (int)anchor_coord(e.s[d], p);   // window origin relative to the anchor
+        C.wext[m][d] = hi[d] - lo[d] + 1;
+      }
       for (int iz = lo[2]; iz <= hi[2]; ++iz)
         for (int iy = lo[1]; iy <= hi[1]; ++iy)
           for (int ix = lo[0]; ix <= hi[0]; ++ix) {
@@ -635,6 +641,13 @@ struct Builder {
       C.offs[q] = (int)rel;
     }
     C.comp = comp_of_pos;
+    C.pcoord.resize(3 * (size_t)n);
+    for (int q = 0; q < n; ++q) {
+      const NatDof& d = dofs[order[q]];
+      C.pcoord[3 * q + 0] = d.ix - wlo_abs[d.comp][0];
+      C.pcoord[3 * q + 1] = d.iy - wlo_abs[d.comp][1];
+      C.pcoord[3 * q + 2] = d.iz - wlo_abs[d.comp][2];
+    }
     C.slot_map.clear();
     for (auto& mp : slot_nat) {
       std::vector<int> m2(nloc, -1);
@@ -782,7 +795,6 @@ struct Builder {
       }
     }
     C.nvals_canon = (vofs + 1) & ~int64_t(1);
-    build_stream(C);
   }
 
   // ---------------------------------------------------------------- numeric factorization
@@ -1087,14 +1099,40 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   }
   fam->classes.resize(rep.size());
   for (size_t c = 0; c < rep.size(); ++c) B.build_class(rep[c], fam->classes[c]);
+  // window boxes (the patches' working vectors): per component the largest window of any class
+  // plus one (box origins are rounded down to even x: a TMA box row must start 16-byte aligned),
+  // x extent rounded up to even (TMA rows are multiples of 16 bytes); components at 128-byte
+  // aligned offsets
+  const Space& spf = B.sp;
+  {
+    for (int m = 0; m < 3; ++m)
+      for (int d = 0; d < 3; ++d) fam->box[m][d] = 0;
+    for (auto& C : fam->classes)
+      if (C.n > 0)
+        for (int m = 0; m < spf.ncomp; ++m)
+          for (int d = 0; d < 3; ++d) fam->box[m][d] = std::max(fam->box[m][d], C.wext[m][d] + (d == 0 ? 1 : 0));
+    int off = 0;
+    for (int m = 0; m < spf.ncomp; ++m) {
+      fam->box[m][0] = (fam->box[m][0] + 1) & ~1;
+      fam->boff[m] = off;
+      off += (fam->box[m][0] * fam->box[m][1] * fam->box[m][2] + 15) & ~15;
+    }
+    for (int m = spf.ncomp; m <= 3; ++m) fam->boff[m] = off;
+    fam->box_total = off;
+    if (off > 0xFFFF) throw std::runtime_error("patch window box larger than 65535 entries");
+    for (auto& C : fam->classes) build_stream(C);   // piece layout (metadata after the box indices)
+  }
   // drop empty patches
   std::vector<size_t> keep;
   for (size_t i = 0; i < ents.size(); ++i) if (fam->classes[ecls[i]].n > 0) keep.push_back(i);
   const size_t np = keep.size();
   fam->pclass.resize(np); fam->pbase.resize(np * 3); fam->pvals.resize(np); fam->pcolor.resize(np);
+  fam->porig.resize(np * 9);
   fam->ncolors = (in.dim == 0) ? 8 : (in.dim == 1 ? 12 : 6);
-  // dedup key: class + per-slot coefficients (+ cell sizes); trilinear cells are never shared
+  // dedup key: class + per-slot coefficients (+ cell sizes); trilinear cells are never shared;
+  // x-parity twins of a class share value blocks (same program, different box indices)
   std::map<std::vector<double>, int64_t> dedup;
+  std::map<std::pair<int, int>, int> twins;
   std::vector<int64_t> fid(np);
   std::vector<int64_t> foff;
   std::vector<size_t> frep;
@@ -1102,8 +1140,28 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   for (size_t t = 0; t < np; ++t) {
     const Entity& e = ents[keep[t]];
     const int c = ecls[keep[t]];
-    fam->pclass[t] = c;
     fam->pcolor[t] = color_of(e, in.dim);
+    int xmask = 0;
+    for (int m = 0; m < 3; ++m)
+      for (int d = 0; d < 3; ++d) {
+        int o = (m < B.sp.ncomp) ? (int)anchor_coord(e.s[d], B.sp.p) + fam->classes[c].wlo[m][d] : 0;
+        if (d == 0 && (o & 1)) { --o; xmask |= 1 << m; }   // even x origin: the class twin shifts by one
+        fam->porig[t * 9 + m * 3 + d] = o;
+      }
+    {
+      auto tw = twins.find({c, xmask});
+      if (tw == twins.end()) {
+        int idx = c;
+        if (xmask != 0) {
+          idx = (int)fam->classes.size();
+          ClassProgram twin = fam->classes[c];
+          for (int m = 0; m < 3; ++m) twin.xshift[m] = (xmask >> m) & 1;
+          fam->classes.push_back(std::move(twin));
+        }
+        tw = twins.emplace(std::make_pair(c, xmask), idx).first;
+      }
+      fam->pclass[t] = tw->second;
+    }
     for (int m = 0; m < 3; ++m)
       fam->pbase[t * 3 + m] = (m < B.sp.ncomp)
           ? B.sp.gidx(m, anchor_coord(e.s[2], B.sp.p), anchor_coord(e.s[1], B.sp.p), anchor_coord(e.s[0], B.sp.p)) : 0;
@@ -1132,6 +1190,23 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     }
     fid[t] = it->second;
     fam->pvals[t] = foff[fid[t]];
+  }
+  // box indices of every class (and twin), the zero lists, and the class meta streams
+  for (auto& C : fam->classes) {
+    C.bidx.resize(C.n);
+    std::vector<char> used(fam->box_total, 0);
+    for (int t2 = 0; t2 < C.n; ++t2) {
+      const int m = C.comp[t2];
+      const int b = fam->boff[m] + (C.pcoord[3 * t2 + 2] * fam->box[m][1] + C.pcoord[3 * t2 + 1]) * fam->box[m][0] +
+                    C.pcoord[3 * t2 + 0] + C.xshift[m];
+      C.bidx[t2] = b;
+      used[b] = 1;
+    }
+    C.zlist.clear();
+    for (int m = 0; m < spf.ncomp; ++m)
+      for (int b = fam->boff[m]; b < fam->boff[m] + fam->box[m][0] * fam->box[m][1] * fam->box[m][2]; ++b)
+        if (!used[b]) C.zlist.push_back(b);
+    build_meta(C);
   }
   fam->nfactors = (int64_t)foff.size();
   fam->values.assign(total, 0.0);

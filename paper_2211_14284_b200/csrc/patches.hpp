@@ -63,7 +63,7 @@ enum FinalKind { FINAL_DENSE_INV = 0, FINAL_ICC = 1 };
 //   backward: for l = L-1..0: WT(l) pieces  (pivots and members reused from a shared copy)
 // (gather / scatter use the class's codes (offs << 2 | comp) from global memory; the dense-tile
 // units form their own channel, consumed by the tile warps only)
-enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_GATHER = 6, PK_SCATTER = 7 };
+enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_FINAL = 6, PK_ZERO = 7 };
 constexpr int kPieceMax = 2048;      // doubles (16 KB) of values per piece
 constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
 // Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
@@ -130,7 +130,11 @@ struct ClassProgram {
   std::vector<uint8_t> meta;             // class meta stream (pieces' metadata blocks)
   std::vector<Unit> units;
   int tu0 = 0, tu1 = 0;                  // units of the dense-tile phase (tile channel)
-  std::vector<int32_t> codes;            // per position: (offs << 2) | comp (gather / scatter)
+  // window box: per component the window origin relative to the anchor and its extent; per
+  // position its coordinates inside the window, its box index, and the box entries to zero
+  int wlo[3][3] = {{0}}, wext[3][3] = {{0}};
+  int xshift[3] = {0, 0, 0};             // x-parity twin: box x index shifted by one (odd origins)
+  std::vector<int> pcoord, bidx, zlist;
   // structural pattern of the patch matrix (CSR over positions)
   std::vector<int> prow, pcol;
 };
@@ -148,6 +152,10 @@ struct PatchFamily {
   std::vector<int> pcolor;
   int ncolors = 0;
   std::vector<double> values;     // all value blocks
+  std::vector<int> porig;         // per patch [comp][dir]: window box origin (global index)
+  int box[3][3] = {{0}};          // per component box extents (x even)
+  int boff[4] = {0, 0, 0, 0};     // component offsets inside the box vector
+  int box_total = 0;
   double sigma_max = 0.0;         // largest ICC restart shift used (reading G7)
   int64_t nfactors = 0;           // distinct value blocks
   std::string err;

@@ -58,6 +58,7 @@ template <class T> static T rd(const uint8_t* b, size_t i) { T x; std::memcpy(&x
 
 static void emulate_family(const PatchFamily& F, const double* r, double* z) {
   const size_t np = F.pclass.size();
+  const Space& sp = F.sp;
   for (int color = 0; color < F.ncolors; ++color)
     for (size_t t = 0; t < np; ++t) {
       if (F.pcolor[t] != color) continue;
@@ -65,28 +66,38 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
       const double* V = F.values.data() + F.pvals[t];
       std::vector<std::vector<uint8_t>> bufs;
       const std::vector<PieceView> views = unit_views(C, V, bufs);
-      auto view = [&](const ClassProgram&, const double*, int i) { return views[i]; };
-      const int64_t base[3] = {F.pbase[3 * t], F.pbase[3 * t + 1], F.pbase[3 * t + 2]};
-      const int n = C.n;
+      auto view = [&](int i) { return views[i]; };
       const int L = (int)C.lev.size();
-      std::vector<double> v(n);
-      auto code_ix = [&](int32_t code) { return base[code & 3] + (code >> 2); };
-      for (int t2 = 0; t2 < n; ++t2) v[t2] = r[code_ix(C.codes[t2])];
-      // sliced piece: per slice (start/32, count) then cols, rows = s*32 + lane
-      auto sliced_piece = [&](const PieceView& w, int nrows, auto&& emit) {
+      // ---- gather: TMA box load of every component window (out of bounds -> 0)
+      std::vector<double> v(F.box_total, 0.0);
+      auto box_walk = [&](auto&& fn) {
+        for (int m = 0; m < sp.ncomp; ++m) {
+          const int* o = &F.porig[t * 9 + m * 3];
+          for (int bz = 0; bz < F.box[m][2]; ++bz)
+            for (int by = 0; by < F.box[m][1]; ++by)
+              for (int bx = 0; bx < F.box[m][0]; ++bx) {
+                const int64_t gx = o[0] + bx, gy = o[1] + by, gz = o[2] + bz;
+                const int b = F.boff[m] + (bz * F.box[m][1] + by) * F.box[m][0] + bx;
+                if (gx < sp.len(m, 0) && gy < sp.len(m, 1) && gz < sp.len(m, 2)) fn(b, sp.gidx(m, gz, gy, gx));
+              }
+        }
+      };
+      box_walk([&](int b, int64_t g) { v[b] = r[g]; });
+      // sliced piece: per slice (start/32, count); per slice 32 row boxes; column boxes
+      auto sliced_piece = [&](const PieceView& w, auto&& emit) {
         const int nsl = w.a1 - w.a0;
-        const uint8_t* cols = w.pb + 16 + 4 * nsl;
+        const uint8_t* rows = w.pb + 16 + 4 * nsl;
+        const uint8_t* cols = rows + 64 * nsl;
         for (int ls = 0; ls < nsl; ++ls) {
           const uint32_t info = rd<uint32_t>(w.pb + 16, ls);
           const int st = 32 * (int)(info & 0xFFFF), cnt = (int)(info >> 16);
           for (int lane = 0; lane < 32; ++lane) {
-            const int row = (w.a0 + ls) * 32 + lane;
             double acc = 0;
             for (int kk = 0; kk < cnt; ++kk) {
               const int e = st + kk * 32 + lane;
               acc += w.val[e] * v[rd<uint16_t>(cols, e)];
             }
-            if (row < nrows) emit(row, acc);
+            emit(ls, lane, rd<uint16_t>(rows, ls * 32 + lane), acc);
           }
         }
       };
@@ -94,7 +105,7 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
         const Level& Lv = C.lev[l];
         const int bs = Lv.blk.bs;
         for (int pi = C.piv_b[l]; pi < C.w_b[l]; ++pi) {
-          PieceView w = view(C, V, pi);
+          PieceView w = view(pi);
           const int cnt = w.a1 - w.a0;
           auto pc = [&](int slot, int li) { return w.val[slot * cnt + li]; };
           for (int li = 0; li < cnt; ++li) {
@@ -117,56 +128,71 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
             }
           }
         }
-        for (int pi = C.w_b[l]; pi < C.w_e[l]; ++pi)
-          sliced_piece(view(C, V, pi), Lv.w.nrows, [&](int row, double acc) { v[Lv.w.r0 + row] -= acc; });
-      }
-      const int m = C.m, f0 = n - m;
-      if (C.final_kind == FINAL_DENSE_INV) {
-        const int T = (m + 31) / 32;
-        std::vector<double> x(32 * T, 0.0), g(32 * T, 0.0);
-        for (int i = 0; i < m; ++i) g[i] = v[f0 + i];
-        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
-          PieceView w = view(C, V, pi);
-          const int I = w.a0, J = w.a1;
-          const double* tb = w.val;
-          for (int rr = 0; rr < 32; ++rr)   // tile = S (off-diagonal) or L' with S = L' + L'^T (diagonal)
-            for (int c = 0; c < 32; ++c) {
-              if (I == J && c > rr) continue;
-              const double s = (I == J) ? tb[tile_pos_diag(rr, c)] : tb[tile_pos_full(rr, c)];
-              x[32 * I + rr] += s * g[32 * J + c];
-              x[32 * J + c] += s * g[32 * I + rr];
-            }
+        for (int pi = C.w_b[l]; pi < C.w_e[l]; ++pi) {
+          PieceView w = view(pi);
+          sliced_piece(w, [&](int ls, int lane, int rb, double acc) {
+            if ((w.a0 + ls) * 32 + lane < Lv.w.nrows) v[rb] -= acc;
+          });
         }
-        for (int i = 0; i < m; ++i) v[f0 + i] = x[i];
+      }
+      const int m = C.m;
+      if (C.final_kind == FINAL_DENSE_INV) {
+        if (m > 0) {
+          const int T = (m + 31) / 32;
+          PieceView fw = view(C.tile_p0);
+          std::vector<int> fb(m);
+          for (int j = 0; j < m; ++j) fb[j] = rd<uint16_t>(fw.pb + 16, j);
+          std::vector<double> x(32 * T, 0.0), g(32 * T, 0.0);
+          for (int i = 0; i < m; ++i) g[i] = v[fb[i]];
+          for (int pi = C.tile_p0 + 1; pi < C.tile_p1; ++pi) {
+            PieceView w = view(pi);
+            const int I = w.a0, J = w.a1;
+            const double* tb = w.val;
+            for (int rr = 0; rr < 32; ++rr)   // tile = S (off-diagonal) or L' with S = L' + L'^T (diagonal)
+              for (int c = 0; c < 32; ++c) {
+                if (I == J && c > rr) continue;
+                const double s = (I == J) ? tb[tile_pos_diag(rr, c)] : tb[tile_pos_full(rr, c)];
+                x[32 * I + rr] += s * g[32 * J + c];
+                x[32 * J + c] += s * g[32 * I + rr];
+              }
+          }
+          for (int i = 0; i < m; ++i) v[fb[i]] = x[i];
+        }
       } else {
-        double* y = v.data() + f0;
         for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
-          PieceView w = view(C, V, pi);
+          PieceView w = view(pi);
           const int cnt = w.a1 - w.a0;
           const uint8_t* rows = w.pb + 16;
           const uint8_t* st = rows + 2 * cnt;
           const uint8_t* cols = st + 2 * (cnt + 1);
           for (int k = 0; k < cnt; ++k) {
             const int a = rd<uint16_t>(rows, k), t0 = rd<uint16_t>(st, k), t1 = rd<uint16_t>(st, k + 1);
-            double s = y[a];
+            double s = v[a];
             if (C.pieces[pi].kind == PK_ICCF) {
-              for (int tt = t0; tt < t1 - 1; ++tt) s -= w.val[tt] * y[rd<uint16_t>(cols, tt)];
-              y[a] = s * w.val[t1 - 1];
+              for (int tt = t0; tt < t1 - 1; ++tt) s -= w.val[tt] * v[rd<uint16_t>(cols, tt)];
+              v[a] = s * w.val[t1 - 1];
             } else {
-              for (int tt = t0 + 1; tt < t1; ++tt) s -= w.val[tt] * y[rd<uint16_t>(cols, tt)];
-              y[a] = s * w.val[t0];
+              for (int tt = t0 + 1; tt < t1; ++tt) s -= w.val[tt] * v[rd<uint16_t>(cols, tt)];
+              v[a] = s * w.val[t0];
             }
           }
         }
       }
       for (int l = L - 1; l >= 0; --l) {   // x_E = y^_E - W^ x_R, in place
         const Level& Lv = C.lev[l];
-        std::vector<double> upd(Lv.wt.nrows, 0.0);
-        for (int pi = C.wt_b[l]; pi < C.wt_e[l]; ++pi)
-          sliced_piece(view(C, V, pi), Lv.wt.nrows, [&](int row, double acc) { upd[row] += acc; });
-        for (int row = 0; row < Lv.wt.nrows; ++row) v[Lv.e0 + row] -= upd[row];
+        std::vector<std::pair<int, double>> upd;
+        for (int pi = C.wt_b[l]; pi < C.wt_e[l]; ++pi) {
+          PieceView w = view(pi);
+          sliced_piece(w, [&](int ls, int lane, int rb, double acc) {
+            if ((w.a0 + ls) * 32 + lane < Lv.wt.nrows) upd.push_back({rb, acc});
+          });
+        }
+        for (auto& pr : upd) v[pr.first] -= pr.second;
       }
-      for (int t2 = 0; t2 < n; ++t2) z[code_ix(C.codes[t2])] += v[t2];
+      // ---- scatter: zero the non-patch box entries, TMA reduce-add of the boxes
+      PieceView zw = view((int)C.pieces.size() - 1);
+      for (int k = 0; k < zw.a1 - zw.a0; ++k) v[rd<uint16_t>(zw.pb + 16, k)] = 0.0;
+      box_walk([&](int b, int64_t g) { z[g] += v[b]; });
     }
 }
 
