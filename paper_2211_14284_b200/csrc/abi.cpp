@@ -95,6 +95,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     d.nunits = (int)us.size();
     d.ngs = C.ngs;
     d.tile_p0 = C.tile_p0; d.tile_p1 = C.tile_p1;
+    d.uf0 = C.uf0; d.uf1 = C.uf1;
+    d.fin_tiles = (C.final_kind == rm::FINAL_DENSE_INV && C.m > 0) ? 1 : 0;
     if (C.final_kind == rm::FINAL_DENSE_INV) {
       if ((C.m + 31) / 32 > 32) throw RmError(RM_EINVAL, "final Schur block larger than 1024");
       // g + per-tile-warp partials + final-block box list (uint16)
@@ -211,6 +213,45 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     flush();
     Lh.pvals = F.upload(pvn);
     Lh.vals = dvals;
+    // per-CTA producer issue lists in consumption order (patch_solve.cu): sparse channel
+    // fwd(0), then per i: fwd(i+1), final(i) unless dense tiles, bwd(i); tile channel tiles(i)
+    std::vector<unsigned char*> dmeta(P.classes.size());
+    for (size_t c = 0; c < P.classes.size(); ++c) dmeta[c] = const_cast<unsigned char*>(hc[c].meta);
+    std::vector<rm::XferEntry> xl;
+    std::vector<long long> xb;
+    xl.reserve(np * 32);
+    auto push = [&](size_t q, int u0, int u1) {
+      const rm::ClassProgram& C = P.classes[pc[q]];
+      for (int u = u0; u < u1; ++u) {
+        const rm::Unit& U = C.units[u];
+        rm::XferEntry e{};
+        e.meta = dmeta[pc[q]] + U.mofs;
+        e.vals = dvals + pvn[q] + U.sofs;
+        e.mb_np = (unsigned)U.mbytes | ((unsigned)U.np << 16);
+        e.vb = (unsigned)U.nd * 8u;
+        xl.push_back(e);
+      }
+    };
+    auto fin_tiles = [&](size_t q) { const rm::ClassProgram& C = P.classes[pc[q]]; return C.final_kind == rm::FINAL_DENSE_INV && C.m > 0; };
+    for (int b = 0; b < G; ++b) {
+      std::vector<size_t> qs;
+      for (size_t q = (size_t)b; q < np; q += (size_t)G) qs.push_back(q);
+      const int n = (int)qs.size();
+      xb.push_back((long long)xl.size());
+      if (n > 0) push(qs[0], 0, P.classes[pc[qs[0]]].uf0);
+      for (int i = 0; i < n; ++i) {
+        if (i + 1 < n) push(qs[i + 1], 0, P.classes[pc[qs[i + 1]]].uf0);
+        const rm::ClassProgram& C = P.classes[pc[qs[i]]];
+        if (!fin_tiles(qs[i])) push(qs[i], C.uf0, C.uf1);
+        push(qs[i], C.uf1, (int)C.units.size());
+      }
+      xb.push_back((long long)xl.size());
+      for (int i = 0; i < n; ++i)
+        if (fin_tiles(qs[i])) push(qs[i], P.classes[pc[qs[i]]].uf0, P.classes[pc[qs[i]]].uf1);
+    }
+    xb.push_back((long long)xl.size());
+    Lh.xfer = F.upload(xl);
+    Lh.xbeg = F.upload(xb);
   }
   F.npatch = (int64_t)np;
   F.nfactors = P.nfactors;

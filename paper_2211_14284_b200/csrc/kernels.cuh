@@ -52,6 +52,7 @@ struct DClass {
   const DUnit* units;
   const unsigned char* meta;     // class meta stream (L2-resident)
   int nunits, ngs, tile_p0, tile_p1, iccf_nlev, iccb_nlev;
+  int uf0, uf1, fin_tiles, pad2;  // final segment units [uf0, uf1); fin_tiles: on the tile channel
   const int *iccf_lp, *iccb_lp;  // per ICC level: first piece (size nlev + 1)
 };
 constexpr int RM_MAXCOLORS = 12;
@@ -72,6 +73,17 @@ struct PadLayout {
 };
 struct TMaps { CUtensorMap r[3], c[3]; };   // 3D maps of the padded r / c components
 
+// One transfer of the producer's per-CTA issue lists (host-built, in consumption order): copy
+// mb metadata bytes from `meta` and vb value bytes from `vals` into the channel's ring as one
+// unit of np pieces.
+struct XferEntry {
+  const unsigned char* meta;
+  const double* vals;
+  unsigned mb_np;   // meta bytes | pieces << 16
+  unsigned vb;      // value bytes
+  unsigned long long pad;
+};
+
 // Persistent streaming patch solve over one family: patches sorted by colour, CTA b takes
 // patches b, b + grid, ...; every patch works on its window box (gathered from rpad and
 // reduce-added into cpad with TMA tensor copies); reduce-adds follow the colour order through
@@ -88,7 +100,8 @@ struct PatchLaunch {
   int ncomp, box[3][3], boff[4], box_total;
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)
-  int ring_bytes;
+  int ring_bytes;        // sparse-channel ring
+  int ring_b_bytes;      // tile-channel ring
   int grid;
   int unit_bytes_max;    // largest transfer unit (meta + values)
   PadLayout pad;
@@ -96,6 +109,9 @@ struct PatchLaunch {
   double *rpad, *cpad;
   TMaps tm;
   TMaps* tm_dev;         // device copy of tm (owned by the launch plan)
+  const XferEntry* xfer;         // per-CTA issue lists (sparse channel, then tile channel)
+  const long long* xbeg;         // [2 * grid + 2]: CTA b's sparse list = [xbeg[2b], xbeg[2b+1]),
+                                 //                tile list = [xbeg[2b+1], xbeg[2b+2])
   unsigned long long* prof;   // RM_PROFILE=1 instrumentation counters (else null)
 };
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
@@ -103,7 +119,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;
-constexpr int RM_PATCH_TILE_WARPS = 8;   // consumer warps sharing the dense tiles
+constexpr int RM_PATCH_TILE_WARPS = 4;   // consumer warps sharing the dense tiles
 cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,

@@ -14,15 +14,18 @@
 //
 // B200 structure.  Every factor value is read exactly once per sweep, so the kernel is an HBM
 // stream.  Each patch value block is laid out in consumption order (patches.hpp); consecutive
-// pieces form transfer units of <= 32 KB.  Warp roles per CTA (persistent, 2 CTAs per SM):
-//   producer  streams the units of ALL the CTA's patches HBM -> shared memory with cp.async.bulk
-//             (TMA bulk copies, SASS UBLKCP) into a variable-size ring, and loads each patch's
-//             window box of r with a TMA tensor copy (UTMALDG) into one of two box buffers;
-//   8 compute warps  run the elimination on the box (every metadata index is a box index);
-//             the dense-tile units travel in their own channel, consumed by 4 of them;
+// pieces form transfer units (16 KB sparse, 32 KB dense-tile).  One persistent CTA per SM,
+// warp-specialised and software-pipelined across the CTA's patches i = 0, 1, ...:
+//   producer  streams the units HBM -> shared memory with cp.async.bulk (TMA, UBLKCP) into two
+//             rings (sparse channel, tile channel) and loads each patch's window box of r with a
+//             TMA tensor copy (UTMALDG) into one of three box buffers;
+//   8 sparse warps   forward(i+1), then [final(i) if not dense], backward(i) -- the sparse
+//             eliminations of two patches around the dense phase of one;
+//   4 tile warps     the dense final-block GEMV of patch i (lane-block tiles, LDS.128 + DFMA);
 //   store     reduce-adds the finished box into the correction c with a TMA tensor reduction
 //             (UTMAREDG .add, fp64, atomic per element) once the colour order allows.
-// There is no latency-bound global gather or scatter loop left on the compute warps.
+// The tile stream (~78% of the bytes) therefore runs while the latency-bound sparse phases of
+// the neighbouring patches execute, and no global gather/scatter loop is left on compute warps.
 //
 // Colours.  Patches of one colour are disjoint, so their corrections commute; patches are
 // sorted by colour and a colour-c box is reduce-added only after every box of colours < c has
@@ -44,18 +47,19 @@ namespace rm {
 
 namespace {
 
-constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // consumer warps
+constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // sparse warps
 constexpr int NT = NC * 32;
-constexpr int NTHR = NT + 64;                  // + producer warp + store warp
-constexpr int WPROD = NC, WSTORE = NC + 1;
 constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps
+constexpr int WT0 = NC, WPROD_A = NC + NTW, WPROD_B = NC + NTW + 1, WSTORE = NC + NTW + 2;
+constexpr int NTHR = 32 * (NC + NTW + 3);
 constexpr int NDESC = 16;                      // in-flight transfer units per channel
+constexpr int NBOX = 3;                        // window-box buffers (patches i-1, i, i+1)
 // shared-memory header: per channel full/empty mbarriers and slot tables (offset, pieces, meta),
-// then the box-buffer barriers vfull[2] (TMA box landed), vdone[2] (compute warps done),
-// vempty[2] (store warp's reduction has read the box)
-constexpr int HDR_BYTES = 2 * (2 * NDESC * 8 + 3 * NDESC * 4);   // 896
-constexpr int VBAR_OFS = HDR_BYTES;
-constexpr int BAR_BYTES = (HDR_BYTES + 6 * 8 + 127) & ~127;
+// then the box barriers vfull (TMA box landed), gready (forward done), xready (tiles done),
+// vdone (backward done), vempty (reduction has read the box), NBOX each
+constexpr int CH_BYTES = 2 * NDESC * 8 + 3 * NDESC * 4;   // 448
+constexpr int VBAR_OFS = 2 * CH_BYTES;
+constexpr int BAR_BYTES = (VBAR_OFS + 5 * NBOX * 8 + 127) & ~127;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
@@ -81,8 +85,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
-// named barriers: 1 = all compute warps, 2 = tile warps
+// named barriers: 1 = sparse warps, 2 = tile warps
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void tsync() { asm volatile("bar.sync 2, %0;" ::"n"(NTW * 32) : "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
@@ -120,7 +133,7 @@ struct ChanSm {
   int* mb;
 };
 __device__ __forceinline__ ChanSm chan_sm(unsigned char* smraw, int ch) {
-  unsigned char* b = smraw + ch * (HDR_BYTES / 2);
+  unsigned char* b = smraw + ch * CH_BYTES;
   ChanSm c;
   c.full = reinterpret_cast<uint64_t*>(b);
   c.empty = c.full + NDESC;
@@ -290,180 +303,243 @@ __device__ __forceinline__ int color_of(int q, const ColorStarts& cs) {
 
 struct BoxGeom { int ncomp, box[3][3], boff[3], bytes; };
 
-__global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __restrict__ tmg,
+namespace {
+
+// producer-side state of one channel ring (unused by the blocking per-channel producers)
+struct ProdChan {
+  ChanSm c;
+  unsigned char* ring;
+  uint32_t cap, H;
+  int j, rel;
+  uint32_t vs_of[NDESC];
+  // try to place a unit of `tot` bytes; releases finished units without blocking
+  __device__ __forceinline__ bool room(uint32_t tot, uint32_t& vs) {
+    const uint32_t off = H % cap;
+    const uint32_t start = (off + tot > cap) ? H + (cap - off) : H;
+    const uint32_t end = start + tot;
+    while (rel < j && (j - rel >= NDESC || end - vs_of[rel % NDESC] > cap)) {
+      if (!mbar_test(&c.empty[rel % NDESC], (uint32_t)(rel / NDESC) & 1u)) return false;
+      ++rel;
+    }
+    vs = start;
+    H = end;
+    return true;
+  }
+  __device__ __forceinline__ void issue(uint32_t vs, const unsigned char* meta, uint32_t mb, const double* vals,
+                                        uint32_t vb, int np) {
+    const int sl = j % NDESC;
+    c.ofs[sl] = (int)(vs % cap);
+    c.np[sl] = np;
+    c.mb[sl] = (int)mb;
+    vs_of[sl] = vs;
+    mbar_arrive_expect_tx(&c.full[sl], mb + vb);
+    bulk_g2s(ring + vs % cap, meta, mb, &c.full[sl]);
+    if (vb) bulk_g2s(ring + vs % cap + mb, vals, vb, &c.full[sl]);
+    ++j;
+  }
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __restrict__ tmg,
                                                                const DClass* __restrict__ classes,
                                                                const int* __restrict__ pclass,
                                                                const long long* __restrict__ pvals,
                                                                const int* __restrict__ porig,
                                                                const double* __restrict__ vals, int npatch,
                                                                ColorStarts cs, BoxGeom bg,
-                                                               unsigned* __restrict__ done, uint32_t cap,
-                                                               int box_total, int dbg,
+                                                               unsigned* __restrict__ done, uint32_t capA,
+                                                               uint32_t capB, int box_total,
+                                                               const XferEntry* __restrict__ xfer,
+                                                               const long long* __restrict__ xbeg,
                                                                unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  unsigned char* ring = smraw + BAR_BYTES;
+  unsigned char* ringA = smraw + BAR_BYTES;
+  unsigned char* ringB = ringA + capA;
   uint64_t* vfull = reinterpret_cast<uint64_t*>(smraw + VBAR_OFS);
-  uint64_t* vdone = vfull + 2;
-  uint64_t* vempty = vfull + 4;
+  uint64_t* gready = vfull + NBOX;
+  uint64_t* xready = gready + NBOX;
+  uint64_t* vdone = xready + NBOX;
+  uint64_t* vempty = vdone + NBOX;
   const int boxd = (box_total + 15) & ~15;   // doubles per box buffer (128-byte multiple)
-  double* vbuf0 = reinterpret_cast<double*>(ring + cap);
-  double* aux = vbuf0 + 2 * boxd;
+  double* box0 = reinterpret_cast<double*>(ringB + capB);
+  double* aux = box0 + NBOX * boxd;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
+  const int n = ((int)blockIdx.x < npatch) ? (npatch - (int)blockIdx.x + G - 1) / G : 0;   // patches of this CTA
   if (tid == 0) {
     for (int ch = 0; ch < 2; ++ch) {
       ChanSm c = chan_sm(smraw, ch);
       for (int s = 0; s < NDESC; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], ch == 0 ? NC : NTW); }
     }
-    for (int b = 0; b < 2; ++b) { mbar_init(&vfull[b], 1); mbar_init(&vdone[b], NC); mbar_init(&vempty[b], 1); }
+    for (int b = 0; b < NBOX; ++b) {
+      mbar_init(&vfull[b], 1); mbar_init(&gready[b], NC); mbar_init(&xready[b], NTW);
+      mbar_init(&vdone[b], NC); mbar_init(&vempty[b], 1);   // vempty unused (the store warp reloads)
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // ================================================================== producer warp
-  if (warp == WPROD) {
-    ChanSm cm[2] = {chan_sm(smraw, 0), chan_sm(smraw, 1)};
+  // ================================================================== producer warps
+  if (warp == WPROD_A || warp == WPROD_B) {
+    // one producer per channel: a plain blocking loop over the CTA's host-built issue list
+    // (abi.cpp: consumption order, absolute source pointers), the next entry prefetched
+    if (lane != 0) return;
+    const int ch = warp == WPROD_A ? 0 : 1;
+    const ChanSm c = chan_sm(smraw, ch);
+    unsigned char* ring = ch == 0 ? ringA : ringB;
+    const uint32_t cap = ch == 0 ? capA : capB;
+    const long long e0 = xbeg[2 * blockIdx.x + ch], e1 = xbeg[2 * blockIdx.x + ch + 1];
     uint32_t H = 0;
-    int jc[2] = {0, 0}, relc[2] = {0, 0};
-    // in-flight units in allocation order (channel, per-channel sequence, virtual start)
-    int fch[2 * NDESC], fseq[2 * NDESC];
-    uint32_t fvs[2 * NDESC];
-    int fh = 0, ft = 0;
-    int i = 0;
-    unsigned long long pt_vempty = 0, pt_room = 0, pt0 = prof ? clock64() : 0;
-    for (int q = blockIdx.x; q < npatch; q += G, ++i) {   // static schedule; value blocks laid out per CTA
-      const DClass& C = classes[pclass[q]];
-      const double* V = vals + pvals[q];
-      const DUnit* U = C.units;
-      const unsigned char* M = C.meta;
-      const int nu = C.nunits;
-      {   // window box of r -> box buffer i & 1 (after the store warp released it); the whole
-          // warp is converged and the operands are warp-uniform, one elected lane issues
-        const int b = i & 1;
-        const unsigned long long tw0 = prof ? clock64() : 0;
-        if (i >= 2) mbar_wait(&vempty[b], (uint32_t)((i >> 1) - 1) & 1u);
-        if (prof) pt_vempty += clock64() - tw0;
-        double* vb = vbuf0 + b * boxd;
-        int o[9];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) o[k] = (dbg & 8) ? 0 : __ldg(porig + 9 * q + k);
-        if (dbg & 16) vb = reinterpret_cast<double*>(ring);
-        if ((dbg & 4) && blockIdx.x < 3 && i < 2 && lane == 0)
-          printf("[dbg] cta %d q %d origin %d %d %d smem %u\n", blockIdx.x, q, o[0], o[1], o[2], smem_u32(vb));
-        __syncwarp();
-        if (elect_one()) {
-          if (dbg & 1) {
-            mbar_arrive(&vfull[b]);
-          } else {
-            mbar_arrive_expect_tx(&vfull[b], (uint32_t)bg.bytes);
-            tma_load_3d(vb + bg.boff[0], &tmg->r[0], o[0], o[1], o[2], &vfull[b]);
-            if (bg.ncomp > 1) tma_load_3d(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
-            if (bg.ncomp > 2) tma_load_3d(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
-          }
-        }
-        __syncwarp();
+    int j = 0, rel = 0;
+    uint32_t vs_of[NDESC];
+    int4 nlo = make_int4(0, 0, 0, 0), nhi = nlo;
+    if (e0 < e1) { const int4* pe = reinterpret_cast<const int4*>(xfer + e0); nlo = pe[0]; nhi = pe[1]; }
+    unsigned long long t_wait = 0, t0 = prof ? clock64() : 0;
+    for (long long e = e0; e < e1; ++e) {
+      const int4 lo = nlo, hi = nhi;
+      if (e + 1 < e1) { const int4* pe = reinterpret_cast<const int4*>(xfer + e + 1); nlo = pe[0]; nhi = pe[1]; }
+      const uint32_t mb = (uint32_t)hi.x & 0xFFFFu, vb = (uint32_t)hi.y, tot = mb + vb;
+      const uint32_t vs = ring_place(H, tot, cap);
+      const unsigned long long ta = prof ? clock64() : 0;
+      while (rel < j && (j - rel >= NDESC || H - vs_of[rel % NDESC] > cap)) {   // room: oldest released
+        mbar_wait(&c.empty[rel % NDESC], (uint32_t)(rel / NDESC) & 1u);
+        ++rel;
       }
-      for (int i0 = 0; i0 < nu; i0 += 32) {
-        int4 d = make_int4(0, 0, 0, 0);
-        if (i0 + lane < nu) d = *reinterpret_cast<const int4*>(U + i0 + lane);
-        const int kn = min(32, nu - i0);
-        for (int k = 0; k < kn; ++k) {
-          const int mofs = __shfl_sync(0xffffffffu, d.x, k), mbnp = __shfl_sync(0xffffffffu, d.y, k);
-          const int sofs = __shfl_sync(0xffffffffu, d.z, k), nd = __shfl_sync(0xffffffffu, d.w, k);
-          if (lane == 0) {
-            const int ch = (int)(((uint32_t)mbnp >> 31) & 1u);
-            const uint32_t mb = (uint32_t)mbnp & 0xFFFFu;
-            const uint32_t vb = (uint32_t)nd * 8u, tot = mb + vb;
-            const uint32_t vs = ring_place(H, tot, cap);
-            // room: this channel's slot must be free and [vs, H) must not overlap unreleased units
-            const unsigned long long tr0 = prof ? clock64() : 0;
-            while (ft > fh && (jc[ch] - relc[ch] >= NDESC || H - fvs[fh % (2 * NDESC)] > cap)) {
-              const int oc = fch[fh % (2 * NDESC)], os = fseq[fh % (2 * NDESC)];
-              mbar_wait(&cm[oc].empty[os % NDESC], (uint32_t)(os / NDESC) & 1u);
-              ++relc[oc];
-              ++fh;
-            }
-            if (prof) pt_room += clock64() - tr0;
-            const int sl = jc[ch] % NDESC;
-            ChanSm& c = cm[ch];
-            c.ofs[sl] = (int)(vs % cap);
-            c.np[sl] = (int)(((uint32_t)mbnp >> 16) & 0x7FFFu);
-            c.mb[sl] = (int)mb;
-            mbar_arrive_expect_tx(&c.full[sl], tot);
-            bulk_g2s(ring + vs % cap, M + mofs, mb, &c.full[sl]);
-            if (vb) bulk_g2s(ring + vs % cap + mb, V + sofs, vb, &c.full[sl]);
-            fch[ft % (2 * NDESC)] = ch;
-            fseq[ft % (2 * NDESC)] = jc[ch];
-            fvs[ft % (2 * NDESC)] = vs;
-            ++ft;
-            ++jc[ch];
-          }
-          __syncwarp();
-        }
-      }
+      if (prof) t_wait += clock64() - ta;
+      const int sl = j % NDESC;
+      c.ofs[sl] = (int)(vs % cap);
+      c.np[sl] = (int)(((uint32_t)hi.x >> 16) & 0x7FFFu);
+      c.mb[sl] = (int)mb;
+      vs_of[sl] = vs;
+      const unsigned char* meta = reinterpret_cast<const unsigned char*>(((unsigned long long)(unsigned)lo.y << 32) | (unsigned)lo.x);
+      const double* src = reinterpret_cast<const double*>(((unsigned long long)(unsigned)lo.w << 32) | (unsigned)lo.z);
+      mbar_arrive_expect_tx(&c.full[sl], tot);
+      bulk_g2s(ring + vs % cap, meta, mb, &c.full[sl]);
+      if (vb) bulk_g2s(ring + vs % cap + mb, src, vb, &c.full[sl]);
+      ++j;
     }
-    if (prof && lane == 0) {
-      unsigned long long* o = prof + 24 * blockIdx.x;
-      o[0] = clock64() - pt0; o[1] = pt_vempty; o[2] = pt_room;
-    }
+    if (prof) { unsigned long long* o = prof + 24 * blockIdx.x + 12 + 2 * ch; o[0] = clock64() - t0; o[1] = t_wait; }
     return;
   }
   // ================================================================== store warp
-  if (warp == WSTORE) {   // whole warp converged; one elected lane issues and waits on the TMA
-    int i = 0;
-    unsigned long long st_done = 0, st_col = 0, st_red = 0, st0 = prof ? clock64() : 0;
-    for (int q = blockIdx.x; q < npatch; q += G, ++i) {
-      const int b = i & 1;
+  if (warp == WSTORE) {   // one lane: window-box loads (TMA tensor) and reductions (TMA reduce-add)
+    if (lane != 0) return;
+    auto load_box = [&](int i) {   // box of patch i into buffer i % NBOX
+      const int b = i % NBOX;
+      const int q = (int)blockIdx.x + i * G;
+      const int* o = porig + 9 * q;
+      double* vb = box0 + b * boxd;
+      mbar_arrive_expect_tx(&vfull[b], (uint32_t)bg.bytes);
+      tma_load_3d(vb + bg.boff[0], &tmg->r[0], o[0], o[1], o[2], &vfull[b]);
+      if (bg.ncomp > 1) tma_load_3d(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
+      if (bg.ncomp > 2) tma_load_3d(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
+    };
+    for (int i = 0; i < n && i < NBOX; ++i) load_box(i);
+    unsigned long long st_done = 0, st_col = 0, st0 = prof ? clock64() : 0;
+    for (int i = 0; i < n; ++i) {
+      const int q = (int)blockIdx.x + i * G;
+      const int b = i % NBOX;
       unsigned long long ta = prof ? clock64() : 0;
-      mbar_wait(&vdone[b], (uint32_t)(i >> 1) & 1u);
+      mbar_wait(&vdone[b], (uint32_t)(i / NBOX) & 1u);
       if (prof) { const unsigned long long tb = clock64(); st_done += tb - ta; ta = tb; }
       const int col = color_of(q, cs);
       if (col > 0) {
         const unsigned need = (unsigned)cs.start[col];
         while (ld_acquire(done) < need) __nanosleep(64);
       }
-      if (prof) { const unsigned long long tb = clock64(); st_col += tb - ta; ta = tb; }
-      int o[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) o[k] = __ldg(porig + 9 * q + k);
-      const double* vb = vbuf0 + b * boxd;
-      __syncwarp();
-      if (elect_one()) {
-        if (!(dbg & 2)) {
-          tma_reduce_add_3d(&tmg->c[0], o[0], o[1], o[2], vb + bg.boff[0]);
-          if (bg.ncomp > 1) tma_reduce_add_3d(&tmg->c[1], o[3], o[4], o[5], vb + bg.boff[1]);
-          if (bg.ncomp > 2) tma_reduce_add_3d(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(&vempty[b]);   // the producer may reload this box buffer
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        atomicAdd(done, 1u);
-      }
-      __syncwarp();
-      if (prof) st_red += clock64() - ta;
+      if (prof) st_col += clock64() - ta;
+      const int* o = porig + 9 * q;
+      const double* vb = box0 + b * boxd;
+      tma_reduce_add_3d(&tmg->c[0], o[0], o[1], o[2], vb + bg.boff[0]);
+      if (bg.ncomp > 1) tma_reduce_add_3d(&tmg->c[1], o[3], o[4], o[5], vb + bg.boff[1]);
+      if (bg.ncomp > 2) tma_reduce_add_3d(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (i + NBOX < n) load_box(i + NBOX);   // the buffer has been read: reload it
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(done, 1u);
     }
-    if (prof && lane == 0) {
+    if (prof) {
       unsigned long long* o = prof + 24 * blockIdx.x;
-      o[3] = clock64() - st0; o[4] = st_done; o[5] = st_col; o[6] = st_red;
+      o[2] = clock64() - st0; o[3] = st_done; o[4] = st_col;
     }
     return;
   }
-  // ================================================================== compute warps
-  Consumer cn{chan_sm(smraw, 0), ring, 0, 0, nullptr, nullptr};   // main channel
-  Consumer ct{chan_sm(smraw, 1), ring, 0, 0, nullptr, nullptr};   // tile channel (tile warps)
-  const bool pf = prof != nullptr && (tid == 0 || tid == 32 * (NC - 1));
-  unsigned long long ct_box = 0, ct_fwd = 0, ct_fin = 0, ct_bwd = 0, ct0 = pf ? clock64() : 0, tm0 = 0;
-  int i = 0;
-  for (int q = blockIdx.x; q < npatch; q += G, ++i) {
+  // ================================================================== tile warps
+  if (warp >= WT0) {
+    const int tw = warp - WT0;
+    Consumer ct{chan_sm(smraw, 1), ringB, 0, 0, nullptr, nullptr};
+    unsigned long long tt_wait = 0, tt0 = prof ? clock64() : 0;
+    for (int i = 0; i < n; ++i) {
+      const int q = (int)blockIdx.x + i * G;
+      const DClass& C = classes[pclass[q]];
+      const int b = i % NBOX;
+      double* v = box0 + b * boxd;
+      unsigned long long ta = (prof && tw == 0 && lane == 0) ? clock64() : 0;
+      mbar_wait(&gready[b], (uint32_t)(i / NBOX) & 1u);   // forward(i) done
+      if (prof && tw == 0 && lane == 0) tt_wait += clock64() - ta;
+      if (C.fin_tiles) {
+        const int m = C.m;
+        const int T = (m + 31) >> 5, mpad = 32 * T;
+        double* g = aux;                                                // padded copy of v_F
+        double* parts = aux + mpad;                                     // per-tile-warp partials
+        uint16_t* fb = reinterpret_cast<uint16_t*>(parts + NTW * mpad);   // final-block boxes
+        const int tt = tid - 32 * WT0;   // 0 .. 32*NTW-1
+        {
+          const Piece_ pc = ct.acquire();   // FINAL piece: boxes of the final block
+          const uint16_t* fbs = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+          for (int jj = tt; jj < mpad; jj += 32 * NTW) {
+            const int bx = (jj < m) ? fbs[jj] : 0;
+            fb[jj] = (uint16_t)bx;
+            g[jj] = (jj < m) ? v[bx] : 0.0;
+          }
+          for (int jj = lane; jj < mpad; jj += 32) parts[tw * mpad + jj] = 0.0;
+          ct.release(lane);
+        }
+        tsync();
+        // whole tiles per warp (tile t of the patch -> tile warp t % NTW), lane-block layout
+        // (patches.hpp): 16 conflict-free LDS.128 and 64 independent DFMA per lane and tile
+        double* mypart = parts + tw * mpad;
+        for (int pi = C.tile_p0 + 1; pi < C.tile_p1; ++pi) {
+          const Piece_ pc = ct.acquire();
+          if (((pi - C.tile_p0 - 1) % NTW) == tw) {
+            const Hdr h = hdr(pc.pb);
+            tile_gemv(pc.val, g, mypart, h.a0, h.a1, lane);
+          }
+          ct.release(lane);
+        }
+        tsync();
+        for (int jj = tt; jj < m; jj += 32 * NTW) {
+          double x = 0.0;
+#pragma unroll
+          for (int w = 0; w < NTW; ++w) x += parts[w * mpad + jj];
+          v[fb[jj]] = x;
+        }
+        tsync();   // aux is reused by the next patch
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xready[b]);
+    }
+    if (prof && tw == 0 && lane == 0) {
+      unsigned long long* o = prof + 24 * blockIdx.x;
+      o[5] = clock64() - tt0; o[6] = tt_wait;
+    }
+    return;
+  }
+  // ================================================================== sparse warps
+  Consumer cn{chan_sm(smraw, 0), ringA, 0, 0, nullptr, nullptr};
+  unsigned long long sp_box = 0, sp_x = 0, sp_fwd = 0, sp_bwd = 0, sp0 = prof ? clock64() : 0;
+  const bool pf = prof != nullptr && tid == 0;
+  auto forward = [&](int i) {
+    const int q = (int)blockIdx.x + i * G;
     const DClass& C = classes[pclass[q]];
-    const int b = i & 1;
-    double* v = vbuf0 + b * boxd;
-    if (pf) tm0 = clock64();
-    mbar_wait(&vfull[b], (uint32_t)(i >> 1) & 1u);   // the window box of r has landed
-    if (pf) { const unsigned long long t = clock64(); ct_box += t - tm0; tm0 = t; }
-    // ---- forward eliminations
+    const int b = i % NBOX;
+    double* v = box0 + b * boxd;
+    unsigned long long ta = pf ? clock64() : 0;
+    mbar_wait(&vfull[b], (uint32_t)(i / NBOX) & 1u);   // the window box of r has landed
+    if (pf) { const unsigned long long tb = clock64(); sp_box += tb - ta; ta = tb; }
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
       const DLevel& L = C.lev[l];
@@ -512,49 +588,19 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __re
       }
       csync();
     }
-    if (pf) { const unsigned long long t = clock64(); ct_fwd += t - tm0; tm0 = t; }
-    // ---- final Schur block
-    const int m = C.m;
-    if (C.final_kind == 0) {
-      if (m > 0 && warp < NTW) {
-        const int T = (m + 31) >> 5, mpad = 32 * T;
-        double* g = aux;                                              // padded copy of v_F
-        double* parts = aux + mpad;                                   // per-tile-warp partials
-        uint16_t* fb = reinterpret_cast<uint16_t*>(parts + NTW * mpad);   // final-block boxes
-        const int tt = tid;   // 0 .. 32*NTW-1
-        {
-          const Piece_ pc = ct.acquire();   // FINAL piece: boxes of the final block
-          const uint16_t* fbs = reinterpret_cast<const uint16_t*>(pc.pb + 16);
-          for (int jj = tt; jj < mpad; jj += 32 * NTW) {
-            const int bx = (jj < m) ? fbs[jj] : 0;
-            fb[jj] = (uint16_t)bx;
-            g[jj] = (jj < m) ? v[bx] : 0.0;
-          }
-          for (int jj = lane; jj < mpad; jj += 32) parts[warp * mpad + jj] = 0.0;
-          ct.release(lane);
-        }
-        tsync();
-        // whole tiles per warp (tile t of the patch -> warp t % NTW), lane-block layout
-        // (patches.hpp): 16 conflict-free LDS.128 and 64 independent DFMA per lane and tile
-        double* mypart = parts + warp * mpad;
-        for (int pi = C.tile_p0 + 1; pi < C.tile_p1; ++pi) {
-          const Piece_ pc = ct.acquire();
-          if (((pi - C.tile_p0 - 1) % NTW) == warp) {
-            const Hdr h = hdr(pc.pb);
-            tile_gemv(pc.val, g, mypart, h.a0, h.a1, lane);
-          }
-          ct.release(lane);
-        }
-        tsync();
-        for (int jj = tt; jj < m; jj += 32 * NTW) {
-          double x = 0.0;
-#pragma unroll
-          for (int w = 0; w < NTW; ++w) x += parts[w * mpad + jj];
-          v[fb[jj]] = x;
-        }
-      }
-      csync();
-    } else {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&gready[b]);   // the tile warps may read v_F
+    if (pf) sp_fwd += clock64() - ta;
+  };
+  auto backward = [&](int i) {
+    const int q = (int)blockIdx.x + i * G;
+    const DClass& C = classes[pclass[q]];
+    const int b = i % NBOX;
+    double* v = box0 + b * boxd;
+    unsigned long long ta = pf ? clock64() : 0;
+    mbar_wait(&xready[b], (uint32_t)(i / NBOX) & 1u);   // tiles(i) done (or skipped)
+    if (pf) { const unsigned long long tb = clock64(); sp_x += tb - ta; ta = tb; }
+    if (C.final_kind != 0) {
       // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
       // then backward rows of L^T by levels (diag first); rows of one level are independent.
       // meta = uint16 row boxes, uint16 value starts (cnt + 1), uint16 column boxes
@@ -588,9 +634,8 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __re
         }
       }
     }
-    if (pf) { const unsigned long long t = clock64(); ct_fin += t - tm0; tm0 = t; }
-    // ---- backward substitution: x_E = y^_E - W^ x_R  (W^ = P_EE^{-1} P_ER, in place)
-    for (int l = nlev - 1; l >= 0; --l) {
+    // x_E = y^_E - W^ x_R  (W^ = P_EE^{-1} P_ER, in place)
+    for (int l = C.nlev - 1; l >= 0; --l) {
       const DLevel& L = C.lev[l];
       for (int pi = L.wt_b; pi < L.wt_e; ++pi) {
         const Piece_ pc = cn.acquire();
@@ -599,8 +644,7 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __re
       }
       csync();
     }
-    // ---- zero the box entries outside the patch, hand the box to the store warp
-    {
+    {   // zero the box entries outside the patch, hand the box to the store warp
       const Piece_ pc = cn.acquire();   // ZERO piece
       const Hdr h = hdr(pc.pb);
       const uint16_t* zl = reinterpret_cast<const uint16_t*>(pc.pb + 16);
@@ -610,11 +654,16 @@ __global__ void __launch_bounds__(NTHR, 2) patch_stream_kernel(const TMaps* __re
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
     __syncwarp();
     if (lane == 0) mbar_arrive(&vdone[b]);
-    if (pf) { const unsigned long long t = clock64(); ct_bwd += t - tm0; }
+    if (pf) sp_bwd += clock64() - ta;
+  };
+  if (n > 0) forward(0);
+  for (int i = 0; i < n; ++i) {
+    if (i + 1 < n) forward(i + 1);
+    backward(i);
   }
   if (pf) {
-    unsigned long long* o = prof + 24 * blockIdx.x + (tid == 0 ? 7 : 12);
-    o[0] = clock64() - ct0; o[1] = ct_box; o[2] = ct_fwd; o[3] = ct_fin; o[4] = ct_bwd;
+    unsigned long long* o = prof + 24 * blockIdx.x;
+    o[7] = clock64() - sp0; o[8] = sp_box; o[9] = sp_x; o[10] = sp_fwd; o[11] = sp_bwd;
   }
 }
 
@@ -672,7 +721,7 @@ cudaError_t encode_maps(PatchLaunch& L) {
 
 cudaError_t plan_patch_solve(PatchLaunch& L) {
   const size_t boxd = (size_t)((L.box_total + 15) & ~15);
-  L.smem_fixed = BAR_BYTES + (2 * boxd + (size_t)L.aux_max) * sizeof(double);
+  L.smem_fixed = BAR_BYTES + (NBOX * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -680,27 +729,20 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
     return e;
-  // two CTAs per SM when the fixed part leaves >= 48 KB of ring each, else one CTA with the rest
-  // (env RM_CTAS_PER_SM / RM_RING_KB override for experiments); the ring must hold 2 units
-  const size_t per_sm = 228 * 1024;
-  int want = 2;
-  if (const char* s = getenv("RM_CTAS_PER_SM")) want = atoi(s);
-  size_t ring = 0;
-  for (; want >= 1; --want) {
-    const size_t avail = std::min<size_t>(per_sm / want - 1024, optin);
-    if (avail >= L.smem_fixed + std::max<size_t>(48 * 1024, 2 * (size_t)L.unit_bytes_max)) { ring = avail - L.smem_fixed; break; }
-  }
-  if (want < 1) {
-    if ((size_t)optin < L.smem_fixed + 2 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
-    ring = optin - L.smem_fixed;
-    want = 1;
-  }
-  if (const char* s = getenv("RM_RING_KB")) ring = std::min<size_t>(ring, (size_t)atoi(s) * 1024);
-  ring &= ~(size_t)127;
-  if (ring < (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
-  L.ring_bytes = (int)ring;
+  // one CTA per SM; the rings share what the boxes leave: 1/3 sparse channel, 2/3 tile channel
+  // (env RM_RING_A_KB overrides the sparse share)
+  if ((size_t)optin < L.smem_fixed + 4 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
+  const size_t rings = (optin - L.smem_fixed) & ~(size_t)127;
+  size_t capA = (rings / 3) & ~(size_t)127;
+  if (const char* s = getenv("RM_RING_A_KB")) capA = std::min<size_t>(rings / 2, (size_t)atoi(s) * 1024) & ~(size_t)127;
+  capA = std::max(capA, (size_t)((L.unit_bytes_max + 127) & ~127) * 2);
+  const size_t capB = (rings - capA) & ~(size_t)127;
+  if (capB < 2 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
+  L.ring_bytes = (int)capA;
+  L.ring_b_bytes = (int)capB;
   int occ = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, patch_stream_kernel, NTHR, L.smem_fixed + ring)) != cudaSuccess)
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, patch_stream_kernel, NTHR, L.smem_fixed + capA + capB)) !=
+      cudaSuccess)
     return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   L.grid = std::max(1, std::min(L.npatch, occ * nsm));
@@ -709,16 +751,9 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   // descriptors live in global memory (64-byte aligned allocation), read by the TMA unit
   if (!L.tm_dev && (e = cudaMalloc(&L.tm_dev, sizeof(TMaps))) != cudaSuccess) return e;
   if ((e = cudaMemcpy(L.tm_dev, &L.tm, sizeof(TMaps), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-  if (getenv("RM_VERBOSE")) {
-    const unsigned long long* w = reinterpret_cast<const unsigned long long*>(&L.tm.r[0]);
-    fprintf(stderr, "[rm] tmap r0:");
-    for (int k = 0; k < 16; ++k) fprintf(stderr, " %llx", w[k]);
-    fprintf(stderr, "\n[rm] rpad %p dims %lld %lld %lld box %d %d %d\n", (void*)L.rpad, L.pad.lxp[0], L.pad.len[0][1],
-            L.pad.len[0][2], L.box[0][0], L.box[0][1], L.box[0][2]);
-  }
   if (getenv("RM_VERBOSE"))
-    fprintf(stderr, "[rm] patch plan: npatch=%d box=%d aux_max=%d fixed=%zu ring=%d occ=%d grid=%d\n", L.npatch,
-            L.box_total, L.aux_max, L.smem_fixed, L.ring_bytes, occ, L.grid);
+    fprintf(stderr, "[rm] patch plan: npatch=%d box=%d aux_max=%d fixed=%zu ringA=%zu ringB=%zu occ=%d grid=%d\n",
+            L.npatch, L.box_total, L.aux_max, L.smem_fixed, capA, capB, occ, L.grid);
   return cudaSuccess;
 }
 
@@ -738,9 +773,9 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     bg.boff[m] = L.boff[m];
     if (m < L.ncomp) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
   }
-  patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes, st>>>(
-      L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes, L.box_total,
-      getenv("RM_DEBUG_TMA") ? atoi(getenv("RM_DEBUG_TMA")) : 0, L.prof);
+  patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
+      L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
+      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.prof);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -750,10 +785,10 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     for (int b = 0; b < L.grid; ++b)
       for (int k = 0; k < 24; ++k) a[k] += (double)h[24 * b + k] / L.grid / 1e3;
     fprintf(stderr,
-            "[rm prof kcyc] producer total %.0f vempty-wait %.0f room-wait %.0f | store total %.0f wait-done %.0f colour %.0f "
-            "reduce %.0f | tile-warp total %.0f box %.0f fwd %.0f final %.0f bwd %.0f | side-warp total %.0f box %.0f fwd "
-            "%.0f final %.0f bwd %.0f\n",
-            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15], a[16]);
+            "[rm prof kcyc] producer total %.0f idle %.0f | store total %.0f wait-done %.0f colour %.0f | tiles total %.0f "
+            "wait-fwd %.0f | sparse total %.0f box-wait %.0f x-wait %.0f fwd %.0f bwd %.0f | prodA total %.0f room-wait %.0f "
+            "| prodB total %.0f room-wait %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15]);
   }
   unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
   return cudaGetLastError();

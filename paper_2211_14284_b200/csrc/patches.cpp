@@ -260,24 +260,29 @@ void build_meta(ClassProgram& C) {
   // transfer units: consecutive pieces (metas and values both contiguous), split at the
   // dense-tile section (its own channel)
   static const int unit_vals = getenv("RM_UNIT_VALS") ? atoi(getenv("RM_UNIT_VALS")) : kUnitVals;
+  static const int unit_vals_tile = getenv("RM_UNIT_VALS_TILE") ? atoi(getenv("RM_UNIT_VALS_TILE")) : kUnitValsTile;
   C.units.clear();
   for (int i = 0; i < (int)C.pieces.size();) {
     Unit u{i, 0, C.pieces[i].mofs, 0, C.pieces[i].sofs, 0};
+    const bool tile_sec = C.final_kind == FINAL_DENSE_INV && i >= C.tile_p0 && i < C.tile_p1;
+    const int cap_vals = tile_sec ? unit_vals_tile : unit_vals;
     while (i < (int)C.pieces.size()) {
       const Piece& p = C.pieces[i];
       const bool boundary = u.np > 0 && (i == C.tile_p0 || i == C.tile_p1);
-      if (u.np > 0 && (boundary || u.nd + p.nd > unit_vals || u.mbytes + p.mbytes > kUnitMeta)) break;
+      if (u.np > 0 && (boundary || u.nd + p.nd > cap_vals || u.mbytes + p.mbytes > kUnitMeta)) break;
       u.np++; u.mbytes += p.mbytes; u.nd += p.nd;
       ++i;
     }
     C.units.push_back(u);
   }
-  C.tu0 = C.tu1 = 0;
-  for (size_t k = 0; k < C.units.size(); ++k) {
-    const bool tile = C.final_kind == FINAL_DENSE_INV && C.m > 0 && C.units[k].p0 >= C.tile_p0 && C.units[k].p0 < C.tile_p1;
-    if (tile && C.tu1 == 0) C.tu0 = (int)k;
-    if (tile) C.tu1 = (int)k + 1;
+  // unit ranges of the three segments: forward [0, uf0), final [uf0, uf1), backward [uf1, end)
+  C.uf0 = C.uf1 = (int)C.units.size();
+  for (int k = (int)C.units.size() - 1; k >= 0; --k) {
+    if (C.units[k].p0 >= C.tile_p0) C.uf0 = k;
+    if (C.units[k].p0 >= C.tile_p1) C.uf1 = k;
   }
+  C.tu0 = C.tu1 = 0;
+  if (C.final_kind == FINAL_DENSE_INV && C.m > 0) { C.tu0 = C.uf0; C.tu1 = C.uf1; }
 }
 
 void build_stream(ClassProgram& C) {

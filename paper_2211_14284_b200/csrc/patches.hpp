@@ -94,7 +94,8 @@ struct Piece {
 
 // Transfer unit: consecutive pieces moved by one mbarrier round trip (<= kUnitVals doubles of
 // values and <= kUnitMeta bytes of metadata; the ring holds [metas][values] of the unit).
-constexpr int kUnitVals = 4096;
+constexpr int kUnitVals = 2048;       // sparse-channel units (16 KB of values)
+constexpr int kUnitValsTile = 4096;   // tile-channel units (32 KB)
 constexpr int kUnitMeta = 16384;
 struct Unit { int p0, np, mofs, mbytes, sofs, nd; };
 
@@ -130,6 +131,7 @@ struct ClassProgram {
   std::vector<uint8_t> meta;             // class meta stream (pieces' metadata blocks)
   std::vector<Unit> units;
   int tu0 = 0, tu1 = 0;                  // units of the dense-tile phase (tile channel)
+  int uf0 = 0, uf1 = 0;                  // final segment units [uf0, uf1) (tiles or ICC)
   // window box: per component the window origin relative to the anchor and its extent; per
   // position its coordinates inside the window, its box index, and the box entries to zero
   int wlo[3][3] = {{0}}, wext[3][3] = {{0}};
