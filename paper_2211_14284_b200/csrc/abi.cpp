@@ -63,7 +63,7 @@ struct DevFamily {
 void upload_family(DevFamily& F, const rm::PatchFamily& P) {
   const int NW = rm::RM_PATCH_TILE_WARPS;
   std::vector<rm::DClass> hc(P.classes.size());
-  int n_max = 0, piv_max = 0, mem_max = 0, aux_max = 0, unit_max = 0;
+  int n_max = 0, piv_max = 0, mem_max = 0, aux_max = 0, unit_max = 0, unit_max_a = 0, unit_max_b = 0;
   for (size_t c = 0; c < P.classes.size(); ++c) {
     const rm::ClassProgram& C = P.classes[c];
     rm::DClass& d = hc[c];
@@ -89,6 +89,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
       if (u.np > 0x7FFF || u.mbytes > 0xFFFF) throw RmError(RM_EINVAL, "transfer unit too large");
       us[i] = rm::DUnit{u.mofs, (int)((uint32_t)u.mbytes | ((uint32_t)u.np << 16) | (tile ? 0x80000000u : 0u)), u.sofs, u.nd};
       unit_max = std::max(unit_max, u.mbytes + 8 * u.nd);
+      if (tile) unit_max_b = std::max(unit_max_b, u.mbytes + 8 * u.nd);
+      else unit_max_a = std::max(unit_max_a, u.mbytes + 8 * u.nd);
     }
     d.units = F.upload(us);
     d.meta = F.upload(C.meta);
@@ -169,6 +171,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
   Lh.done = F.upload(std::vector<unsigned>(1, 0u));
   Lh.n_max = n_max; Lh.piv_max = piv_max; Lh.mem_max = mem_max; Lh.aux_max = aux_max;
   Lh.unit_bytes_max = unit_max;
+  Lh.unit_bytes_max_a = unit_max_a;
+  Lh.unit_bytes_max_b = unit_max_b;
   if (np > 0) {
     cudaError_t e = rm::plan_patch_solve(Lh);
     if (e != cudaSuccess)
@@ -578,7 +582,7 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
 int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
   if (F.npatch == 0) return 0;
   CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st));
-  return 1;
+  return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)

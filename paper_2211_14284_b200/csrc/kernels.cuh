@@ -102,8 +102,10 @@ struct PatchLaunch {
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)
   int ring_bytes;        // sparse-channel ring
   int ring_b_bytes;      // tile-channel ring
+  int nbox;              // window-box buffers (2 or 3)
   int grid;
   int unit_bytes_max;    // largest transfer unit (meta + values)
+  int unit_bytes_max_a, unit_bytes_max_b;   // per channel (sparse, tile)
   PadLayout pad;
   long long npad;
   double *rpad, *cpad;

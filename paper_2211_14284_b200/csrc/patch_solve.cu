@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
                                                                unsigned* __restrict__ done, uint32_t capA,
                                                                uint32_t capB, int box_total,
                                                                const XferEntry* __restrict__ xfer,
-                                                               const long long* __restrict__ xbeg,
+                                                               const long long* __restrict__ xbeg, int nbox,
                                                                unsigned long long* __restrict__ prof) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* ringA = smraw + BAR_BYTES;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   uint64_t* vempty = vdone + NBOX;
   const int boxd = (box_total + 15) & ~15;   // doubles per box buffer (128-byte multiple)
   double* box0 = reinterpret_cast<double*>(ringB + capB);
-  double* aux = box0 + NBOX * boxd;
+  double* aux = box0 + nbox * boxd;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
   const int n = ((int)blockIdx.x < npatch) ? (npatch - (int)blockIdx.x + G - 1) / G : 0;   // patches of this CTA
@@ -424,8 +424,8 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   // ================================================================== store warp
   if (warp == WSTORE) {   // one lane: window-box loads (TMA tensor) and reductions (TMA reduce-add)
     if (lane != 0) return;
-    auto load_box = [&](int i) {   // box of patch i into buffer i % NBOX
-      const int b = i % NBOX;
+    auto load_box = [&](int i) {   // box of patch i into buffer i % nbox
+      const int b = i % nbox;
       const int q = (int)blockIdx.x + i * G;
       const int* o = porig + 9 * q;
       double* vb = box0 + b * boxd;
@@ -434,13 +434,13 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       if (bg.ncomp > 1) tma_load_3d(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
       if (bg.ncomp > 2) tma_load_3d(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
     };
-    for (int i = 0; i < n && i < NBOX; ++i) load_box(i);
+    for (int i = 0; i < n && i < nbox; ++i) load_box(i);
     unsigned long long st_done = 0, st_col = 0, st0 = prof ? clock64() : 0;
     for (int i = 0; i < n; ++i) {
       const int q = (int)blockIdx.x + i * G;
-      const int b = i % NBOX;
+      const int b = i % nbox;
       unsigned long long ta = prof ? clock64() : 0;
-      mbar_wait(&vdone[b], (uint32_t)(i / NBOX) & 1u);
+      mbar_wait(&vdone[b], (uint32_t)(i / nbox) & 1u);
       if (prof) { const unsigned long long tb = clock64(); st_done += tb - ta; ta = tb; }
       const int col = color_of(q, cs);
       if (col > 0) {
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       if (bg.ncomp > 2) tma_reduce_add_3d(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      if (i + NBOX < n) load_box(i + NBOX);   // the buffer has been read: reload it
+      if (i + nbox < n) load_box(i + nbox);   // the buffer has been read: reload it
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence();
@@ -475,10 +475,10 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     for (int i = 0; i < n; ++i) {
       const int q = (int)blockIdx.x + i * G;
       const DClass& C = classes[pclass[q]];
-      const int b = i % NBOX;
+      const int b = i % nbox;
       double* v = box0 + b * boxd;
       unsigned long long ta = (prof && tw == 0 && lane == 0) ? clock64() : 0;
-      mbar_wait(&gready[b], (uint32_t)(i / NBOX) & 1u);   // forward(i) done
+      mbar_wait(&gready[b], (uint32_t)(i / nbox) & 1u);   // forward(i) done
       if (prof && tw == 0 && lane == 0) tt_wait += clock64() - ta;
       if (C.fin_tiles) {
         const int m = C.m;
@@ -535,10 +535,10 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   auto forward = [&](int i) {
     const int q = (int)blockIdx.x + i * G;
     const DClass& C = classes[pclass[q]];
-    const int b = i % NBOX;
+    const int b = i % nbox;
     double* v = box0 + b * boxd;
     unsigned long long ta = pf ? clock64() : 0;
-    mbar_wait(&vfull[b], (uint32_t)(i / NBOX) & 1u);   // the window box of r has landed
+    mbar_wait(&vfull[b], (uint32_t)(i / nbox) & 1u);   // the window box of r has landed
     if (pf) { const unsigned long long tb = clock64(); sp_box += tb - ta; ta = tb; }
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
@@ -595,10 +595,10 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   auto backward = [&](int i) {
     const int q = (int)blockIdx.x + i * G;
     const DClass& C = classes[pclass[q]];
-    const int b = i % NBOX;
+    const int b = i % nbox;
     double* v = box0 + b * boxd;
     unsigned long long ta = pf ? clock64() : 0;
-    mbar_wait(&xready[b], (uint32_t)(i / NBOX) & 1u);   // tiles(i) done (or skipped)
+    mbar_wait(&xready[b], (uint32_t)(i / nbox) & 1u);   // tiles(i) done (or skipped)
     if (pf) { const unsigned long long tb = clock64(); sp_x += tb - ta; ta = tb; }
     if (C.final_kind != 0) {
       // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
@@ -721,7 +721,9 @@ cudaError_t encode_maps(PatchLaunch& L) {
 
 cudaError_t plan_patch_solve(PatchLaunch& L) {
   const size_t boxd = (size_t)((L.box_total + 15) & ~15);
-  L.smem_fixed = BAR_BYTES + (NBOX * boxd + (size_t)L.aux_max) * sizeof(double);
+  // three box buffers (patches i-1, i, i+1 in flight) when they fit, else two
+  L.nbox = NBOX;
+  L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -729,15 +731,21 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(patch_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin)) != cudaSuccess)
     return e;
-  // one CTA per SM; the rings share what the boxes leave: 1/3 sparse channel, 2/3 tile channel
-  // (env RM_RING_A_KB overrides the sparse share)
-  if ((size_t)optin < L.smem_fixed + 4 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
+  // one CTA per SM; the rings share what the boxes leave: about 1/3 sparse channel, 2/3 tile
+  // channel, each holding at least two of its largest units (env RM_RING_A_KB overrides)
+  const size_t ua = (size_t)((L.unit_bytes_max_a + 127) & ~127), ub = (size_t)((L.unit_bytes_max_b + 127) & ~127);
+  if ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub) {
+    L.nbox = 2;
+    L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
+  }
+  if ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub) return cudaErrorInvalidValue;
   const size_t rings = (optin - L.smem_fixed) & ~(size_t)127;
   size_t capA = (rings / 3) & ~(size_t)127;
-  if (const char* s = getenv("RM_RING_A_KB")) capA = std::min<size_t>(rings / 2, (size_t)atoi(s) * 1024) & ~(size_t)127;
-  capA = std::max(capA, (size_t)((L.unit_bytes_max + 127) & ~127) * 2);
+  if (const char* s = getenv("RM_RING_A_KB")) capA = ((size_t)atoi(s) * 1024) & ~(size_t)127;
+  capA = std::min(std::max(capA, 2 * ua), rings - 2 * ub);
+  if (ub == 0) capA = rings - 128;   // no dense tiles in this family: the sparse channel takes the rings
+  capA = std::max(capA, (size_t)128);
   const size_t capB = (rings - capA) & ~(size_t)127;
-  if (capB < 2 * (size_t)L.unit_bytes_max) return cudaErrorInvalidValue;
   L.ring_bytes = (int)capA;
   L.ring_b_bytes = (int)capB;
   int occ = 0;
@@ -752,8 +760,8 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if (!L.tm_dev && (e = cudaMalloc(&L.tm_dev, sizeof(TMaps))) != cudaSuccess) return e;
   if ((e = cudaMemcpy(L.tm_dev, &L.tm, sizeof(TMaps), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
   if (getenv("RM_VERBOSE"))
-    fprintf(stderr, "[rm] patch plan: npatch=%d box=%d aux_max=%d fixed=%zu ringA=%zu ringB=%zu occ=%d grid=%d\n",
-            L.npatch, L.box_total, L.aux_max, L.smem_fixed, capA, capB, occ, L.grid);
+    fprintf(stderr, "[rm] patch plan: npatch=%d box=%d x%d aux_max=%d fixed=%zu ringA=%zu ringB=%zu occ=%d grid=%d\n",
+            L.npatch, L.box_total, L.nbox, L.aux_max, L.smem_fixed, capA, capB, occ, L.grid);
   return cudaSuccess;
 }
 
@@ -775,7 +783,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   }
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
       L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
-      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.prof);
+      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
