@@ -49,6 +49,23 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one patch-kernel launch (= one sweep's patch
+    phase) from the committed ncu --set full summary of the same workload, or None."""
+    path = os.path.join(ROOT, "profiles", f"r01_ncu_patch_solve_cfg{cfg}.txt")
+    try:
+        vals = {}
+        for line in open(path):
+            parts = line.rstrip("\n").split("\t")
+            if len(parts) >= 3 and parts[0].startswith("dram__"):
+                vals[parts[0]] = (float(parts[1]), parts[2])
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
+        return rd[0] * scale[rd[1]] + wr[0] * scale[wr[1]]
+    except Exception:
+        return None
+
+
 class Clocks:
     """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
 
@@ -220,8 +237,8 @@ def main():
     ph1_launch_sweep = launches[1] / args.steps
     prim_bytes = info["factor_bytes"] + 3 * 8 * n   # factor values + r gather + u_out RMW
     achieved = prim_bytes / (ph1_ms_sweep * 1e-3) / 1e9 if ph1_ms_sweep > 0 else 0.0
-    roof = {"kernel": "patch_solve_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+    roof = {"kernel": "patch_stream_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
             "bytes_per_launch": prim_bytes / max(ph1_launch_sweep, 1),
             "launch_ms_avg": ph1_ms_sweep / max(ph1_launch_sweep, 1),
             "share_of_step": ph1_ms_sweep / ms if ms > 0 else None,

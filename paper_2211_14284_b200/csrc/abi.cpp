@@ -279,6 +279,8 @@ struct rm_ctx {
   rm::OpParams op{};
   std::vector<void*> allocs;
   double *d_alpha = nullptr, *d_beta = nullptr, *d_hpow = nullptr;
+  double *d_X = nullptr, *d_tabs = nullptr;   // trilinear cells: vertices, 1D tables
+  rm::TriParams tri{};
   int coef_const = 0;
   DevFamily prim, pot;
   std::vector<double> Dh;   // p x (p+1)
@@ -428,7 +430,30 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       }
     }
     c->cartesian = cart;
-    if (!cart) throw RmError(RM_EINVAL, "trilinear (non-axis-aligned) meshes: apply kernel not available in this build");
+    if (!cart) {
+      // trilinear cells (H(grad) only): vertex array and the 1D tables at the n_q GLL points
+      if (space != 0) throw RmError(RM_EINVAL, "trilinear (non-axis-aligned) meshes are supported for H(grad) only");
+      const int nq = (3 * (p + 1) + 1) / 2;   // reading G1
+      if (nq > 24) throw RmError(RM_EINVAL, "trilinear apply: p too large");
+      const rm::Basis1D& b1 = rm::basis(p);
+      std::vector<double> xq, wq, sv, dsv;
+      rm::gll_rule(nq, xq, wq);
+      b1.tab_s(xq, sv, dsv);
+      std::vector<double> tabs;
+      tabs.insert(tabs.end(), sv.begin(), sv.end());
+      tabs.insert(tabs.end(), dsv.begin(), dsv.end());
+      tabs.insert(tabs.end(), xq.begin(), xq.end());
+      tabs.insert(tabs.end(), wq.begin(), wq.end());
+      c->d_tabs = c->dalloc(tabs.size());
+      CK(cudaMemcpy(c->d_tabs, tabs.data(), tabs.size() * 8, cudaMemcpyHostToDevice));
+      const size_t nv = (size_t)(c->n[0] + 1) * (c->n[1] + 1) * (c->n[2] + 1) * 3;
+      c->d_X = c->dalloc(nv);
+      CK(cudaMemcpy(c->d_X, mesh->coords, nv * 8, cudaMemcpyHostToDevice));
+      c->tri.p = p; c->tri.nq = nq;
+      for (int d = 0; d < 3; ++d) c->tri.n[d] = c->n[d];
+      c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
+      c->tri.gamma_d = gamma_d;
+    }
     // ---- device operator
     c->op = make_op(c->sp, gamma_d);
     c->coef_const = (n_alpha == 1 && n_beta == 1);
@@ -575,7 +600,14 @@ struct Phase {
 void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
   Phase ph(c, 0);
   int nl = 0;
-  CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl));
+  if (c->cartesian) {
+    CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl));
+  } else {
+    CK(rm::launch_apply_init(c->op, f, out, c->ndof, c->st));
+    nl = 1;
+    CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, out,
+                                  f ? -1.0 : 1.0, c->st, &nl));
+  }
   c->launches[0] += nl;
 }
 

@@ -296,6 +296,11 @@ static cudaError_t launch_q(const OpParams& op, const double* alpha, const doubl
   return cudaGetLastError();
 }
 
+cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, long long ndof, cudaStream_t st) {
+  apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch) {

@@ -58,6 +58,19 @@ struct DClass {
 constexpr int RM_MAXCOLORS = 12;
 struct ColorStarts { int ncolors; int start[RM_MAXCOLORS + 1]; };
 
+// trilinear H(grad) apply (apply_tri.cu): 1D tables (S, D at the n_q GLL points, nodes, weights)
+// in a device buffer [S (nq x (p+1)) | D (nq x (p+1)) | x (nq) | w (nq)]
+struct TriParams {
+  int p, nq, n[3];
+  long long Lx, Ly, Lz;
+  unsigned gamma_d;
+};
+cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, const double* X, const double* alpha,
+                                   const double* beta, int coef_const, const double* u, double* out, double sign,
+                                   cudaStream_t st, int* nlaunch);
+// out = f (or 0) with constrained entries zeroed (apply.cu)
+cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, long long ndof, cudaStream_t st);
+
 // launchers (kernels.cu)
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,

@@ -53,6 +53,10 @@ CASES = [
     ("cfg3-2^3-p6", ri.CONFIGS[3].with_mesh(2), 1e-11),
     ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), 1e-10),
     ("cfg4-3^3-p4", ri.CONFIGS[4].with_mesh(3).with_p(4), 1e-10),
+    # trilinear cells (perturbed vertices): true operator by quadrature, auxiliary-operator
+    # patches with ICC on the static-condensation pattern (cfg5 shapes at reduced size)
+    ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3), 1e-11),
+    ("cfg5-2^3-p7", ri.CONFIGS[5].with_mesh(2).with_p(7), 1e-11),
 ]
 
 
@@ -85,7 +89,8 @@ def test_apply_and_sweep_parity(dev, name, w, tol):
 
 @pytest.mark.parametrize("name,w", [("cfg1", ri.CONFIGS[1]), ("cfg2-2^3-p3", ri.CONFIGS[2].with_mesh(2).with_p(3)),
                                     ("cfg3-2^3-p3", ri.CONFIGS[3].with_mesh(2).with_p(3)),
-                                    ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3))])
+                                    ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3)),
+                                    ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3))])
 def test_pcg_iterations(dev, name, w):
     import paper_2211_14284_b200 as rmb
     ctx, pb = setup_pair(w)
@@ -148,3 +153,22 @@ def test_cfg2_full_size_sampled(dev):
     so = sampled_relax(sp, X, al, be, w.gamma_d, f, u, rows[:4])
     got = out.cpu().numpy()[rows[:4]]
     assert np.abs(got - so).max() < 1e-11 * np.abs(so).max()
+
+
+@pytest.mark.parametrize("nx,p", [(2, 15), (3, 5)])
+def test_trilinear_apply_full_degree(dev, nx, p):
+    """cfg5's degree p = 15 (n_q = 24 GLL points per direction) on perturbed trilinear cells:
+    the matrix-free apply against the oracle's quadrature apply (element by element)."""
+    import paper_2211_14284_b200 as rmb
+    from oracle.fem import Space, apply_matfree
+    w = ri.CONFIGS[5].with_mesh(nx).with_p(p)
+    ctx = rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(), w.gamma_d,
+                       coords=ri.vertex_coords(w), factorization=rmb.RM_ICC_SC)
+    f, u = vecs(w, ctx)
+    m = ctx.constrained_mask()
+    v = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
+    rmb.rm_apply(ctx, torch.tensor(u, device=dev), v)
+    sp_ = Space(0, w.p, w.nx, w.ny, w.nz)
+    ref = apply_matfree(sp_, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), np.where(m, 0.0, u))
+    ref[m] = 0.0
+    assert rel(v.cpu().numpy(), ref) < 1e-11
