@@ -68,7 +68,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     const rm::ClassProgram& C = P.classes[c];
     rm::DClass& d = hc[c];
     std::memset(&d, 0, sizeof d);
-    d.n = C.n; d.nlev = (int)C.lev.size(); d.m = C.m; d.final_kind = C.final_kind;
+    d.n = C.n; d.nlev = C.sc ? 0 : (int)C.lev.size(); d.m = C.m; d.final_kind = C.final_kind;
     if (d.nlev > RM_MAXLEV) throw RmError(RM_EINVAL, "too many elimination levels");
     int auxn = 0;
     for (int l = 0; l < d.nlev; ++l) {
@@ -145,6 +145,15 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
   }
   Lh.boff[3] = P.boff[3];
   Lh.box_total = P.box_total;
+  Lh.nsub = P.nsub;
+  for (int sb = 0; sb < 3; ++sb) Lh.sub_comp[sb] = P.sub_comp[sb];
+  if (!P.sc_nk.empty()) {
+    Lh.sc_dinv = F.upload(P.sc_dinv);
+    Lh.sc_c = F.upload(P.sc_c);
+    Lh.sc_nk = F.upload(P.sc_nk);
+    Lh.sc_p = P.sp.p;
+    for (int d = 0; d < 3; ++d) Lh.sc_n[d] = P.sp.n[d];
+  }
   {
     rm::PadLayout& pl = Lh.pad;
     std::memset(&pl, 0, sizeof pl);
@@ -204,6 +213,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     };
     for (int b = 0; b < G; ++b)
       for (size_t q = (size_t)b; q < np; q += (size_t)G) {
+        // an empty block (fully condensed patch) shares its offset with the next block: never a key
+        if (P.classes[pc[q]].nvals == 0) { pvn[q] = 0; continue; }
         auto it = remap.find(pv[q]);
         if (it == remap.end()) {
           const long long nv = P.classes[pc[q]].nvals;

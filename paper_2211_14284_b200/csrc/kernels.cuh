@@ -84,7 +84,7 @@ struct PadLayout {
   long long poff[4];        // padded component offsets
   long long lxp[3];         // padded x extents
 };
-struct TMaps { CUtensorMap r[3], c[3]; };   // 3D maps of the padded r / c components
+struct TMaps { CUtensorMap r[3], c[3]; };   // 3D maps of the padded r / c, one per window sub-box
 
 // One transfer of the producer's per-CTA issue lists (host-built, in consumption order): copy
 // mb metadata bytes from `meta` and vb value bytes from `vals` into the channel's ring as one
@@ -111,6 +111,13 @@ struct PatchLaunch {
   ColorStarts cs;
   unsigned* done;
   int ncomp, box[3][3], boff[4], box_total;
+  int nsub, sub_comp[3];  // window sub-boxes (components, or anchor planes for static condensation)
+  // static condensation of the cell interiors (ICC-SC, k = 0): per cell inverse interior
+  // diagonal [ncell][(p-1)^3], face couplings [ncell][6][(p-1)^3], patches per cell
+  const double* sc_dinv;
+  const double* sc_c;
+  const int* sc_nk;
+  int sc_p, sc_n[3];
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)
   int ring_bytes;        // sparse-channel ring

@@ -301,7 +301,7 @@ __device__ __forceinline__ int color_of(int q, const ColorStarts& cs) {
 
 }  // namespace
 
-struct BoxGeom { int ncomp, box[3][3], boff[3], bytes; };
+struct BoxGeom { int ncomp, box[3][3], boff[3], bytes; };   // ncomp = number of window sub-boxes
 
 namespace {
 
@@ -352,7 +352,8 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
                                                                uint32_t capB, int box_total,
                                                                const XferEntry* __restrict__ xfer,
                                                                const long long* __restrict__ xbeg, int nbox,
-                                                               unsigned long long* __restrict__ prof) {
+                                                               unsigned long long* __restrict__ prof, int dbg_q,
+                                                               double* __restrict__ dbg_out) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* ringA = smraw + BAR_BYTES;
   unsigned char* ringB = ringA + capA;
@@ -540,6 +541,13 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     unsigned long long ta = pf ? clock64() : 0;
     mbar_wait(&vfull[b], (uint32_t)(i / nbox) & 1u);   // the window box of r has landed
     if (pf) { const unsigned long long tb = clock64(); sp_box += tb - ta; ta = tb; }
+    if (dbg_out && dbg_q == 2) {   // debug dump of every loaded box (experiments only)
+      csync();
+      double* d = dbg_out + (size_t)q * (box_total + 9);
+      for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
+      if (tid < 9) d[tid] = (double)porig[9 * q + tid];
+      csync();
+    }
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
       const DLevel& L = C.lev[l];
@@ -617,6 +625,16 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
             const uint16_t* st = rows + cnt;
             const uint16_t* cols = st + cnt + 1;
             const double* val = pc.val;
+            if (dbg_out && dbg_q == 3 && tid == 0) {   // debug: ICC piece record (experiments only)
+              double* d = dbg_out + (size_t)q * (box_total + 9);
+              const int j = (int)d[9];
+              if (j < 14) {
+                double* e = d + 10 + 8 * j;
+                e[0] = pass; e[1] = l; e[2] = cnt; e[3] = rows[0]; e[4] = st[1]; e[5] = cols[0]; e[6] = val[0]; e[7] = v[rows[0]];
+              }
+              d[9] = j + 1;
+              for (int k = 0; k < 9; ++k) d[k] = (double)porig[9 * q + k];
+            }
             for (int k = tid; k < cnt; k += NT) {
               const int a = rows[k], t0 = st[k], t1 = st[k + 1];
               double s = v[a];
@@ -650,6 +668,13 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       const uint16_t* zl = reinterpret_cast<const uint16_t*>(pc.pb + 16);
       for (int k = tid; k < h.a1 - h.a0; k += NT) v[zl[k]] = 0.0;
       cn.release(lane);
+    }
+    if (dbg_out && dbg_q == 1) {   // debug dump of every finished box (experiments only, RM_DEBUG_Q)
+      csync();
+      double* d = dbg_out + (size_t)q * (box_total + 9);
+      for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
+      if (tid < 9) d[tid] = (double)porig[9 * q + tid];
+      csync();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
     __syncwarp();
@@ -691,6 +716,91 @@ __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const dou
   u[g] += omega * cp[P.poff[m] + yz * P.lxp[m] + x];
 }
 
+// ---- static condensation of the cell interiors (ICC-SC families, k = 0), on the padded layout
+// pre:  rp[f] -= sum over the 2 cells K at face DoF f, sum_i c_K(f, I) dinv_K(I) rp[I]   (one thread per face DoF)
+// post: cp[I] = n_K dinv_K(I) rp[I] - dinv_K(I) sum_faces c_K(f, I) cp[f]               (one thread per interior DoF)
+struct ScGeom { int p, n[3]; long long lxp, ly; };
+
+__device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long long y, long long z) {
+  return (z * G.ly + y) * G.lxp + x;
+}
+
+__global__ void sc_pre_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
+                              const double* __restrict__ cc, double* __restrict__ rp, long long nface) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nface) return;
+  const int p = G.p, pm = p - 1, ni = pm * pm * pm;
+  // face DoF t: direction dir, plane index P in 0..n_dir, the two other cells and in-face indices
+  const long long per_dir_x = (long long)(G.n[0] + 1) * G.n[1] * G.n[2] * pm * pm;
+  const long long per_dir_y = (long long)(G.n[1] + 1) * G.n[0] * G.n[2] * pm * pm;
+  int dir;
+  long long r = t;
+  if (r < per_dir_x) dir = 0;
+  else if ((r -= per_dir_x) < per_dir_y) dir = 1;
+  else { r -= per_dir_y; dir = 2; }
+  const int d1 = dir == 0 ? 1 : 0, d2 = dir == 2 ? 1 : 2;   // in-face directions (ascending)
+  const int j = (int)(r % pm) + 1;  r /= pm;                 // along d1
+  const int k = (int)(r % pm) + 1;  r /= pm;                 // along d2
+  const int c1 = (int)(r % G.n[d1]); r /= G.n[d1];
+  const int c2 = (int)(r % G.n[d2]); r /= G.n[d2];
+  const int P = (int)r;                                       // plane 0..n_dir
+  long long g[3];
+  g[dir] = (long long)P * p; g[d1] = (long long)c1 * p + j; g[d2] = (long long)c2 * p + k;
+  double e = 0.0;
+  for (int side = 0; side < 2; ++side) {   // cell below (face +) and above (face -) the plane
+    const int cd = side == 0 ? P - 1 : P;
+    if (cd < 0 || cd >= G.n[dir]) continue;
+    int cell[3];
+    cell[dir] = cd; cell[d1] = c1; cell[d2] = c2;
+    const long long K = ((long long)cell[2] * G.n[1] + cell[1]) * G.n[0] + cell[0];
+    const int face = 2 * dir + (side == 0 ? 1 : 0);
+    for (int i = 1; i < p; ++i) {
+      int loc[3];
+      loc[dir] = i; loc[d1] = j; loc[d2] = k;
+      const int I = ((loc[2] - 1) * pm + (loc[1] - 1)) * pm + (loc[0] - 1);
+      const double y = rp[sc_idx(G, (long long)cell[0] * p + loc[0], (long long)cell[1] * p + loc[1], (long long)cell[2] * p + loc[2])] *
+                       dinv[K * ni + I];
+      e = fma(cc[(K * 6 + face) * ni + I], y, e);
+    }
+  }
+  rp[sc_idx(G, g[0], g[1], g[2])] -= e;
+}
+
+__global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
+                               const double* __restrict__ cc, const int* __restrict__ nk,
+                               const double* __restrict__ rp, double* __restrict__ cp, long long nint) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nint) return;
+  const int p = G.p, pm = p - 1, ni = pm * pm * pm;
+  const long long K = t / ni;
+  const int I = (int)(t % ni);
+  const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / (pm * pm) + 1;
+  const int cx = (int)(K % G.n[0]), cy = (int)((K / G.n[0]) % G.n[1]), cz = (int)(K / ((long long)G.n[0] * G.n[1]));
+  const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
+  const double dv = dinv[K * ni + I];
+  double s = cc[(K * 6 + 0) * ni + I] * cp[sc_idx(G, x, y + j, z + k)];
+  s = fma(cc[(K * 6 + 1) * ni + I], cp[sc_idx(G, x + p, y + j, z + k)], s);
+  s = fma(cc[(K * 6 + 2) * ni + I], cp[sc_idx(G, x + i, y, z + k)], s);
+  s = fma(cc[(K * 6 + 3) * ni + I], cp[sc_idx(G, x + i, y + p, z + k)], s);
+  s = fma(cc[(K * 6 + 4) * ni + I], cp[sc_idx(G, x + i, y + j, z)], s);
+  s = fma(cc[(K * 6 + 5) * ni + I], cp[sc_idx(G, x + i, y + j, z + p)], s);
+  const long long gi = sc_idx(G, x + i, y + j, z + k);
+  cp[gi] = dv * (nk[K] * rp[gi] - s);
+}
+
+double* dbg_buf(int n) {   // experiments: box dump buffer (RM_DEBUG_Q)
+  static double* b = nullptr;
+  if (!getenv("RM_DEBUG_Q")) return nullptr;
+  if (!b) { cudaMalloc(&b, (size_t)(1 << 22) * 8); cudaMemset(b, 0, (size_t)(1 << 22) * 8); }
+  (void)n;
+  return b;
+}
+extern "C" __attribute__((visibility("default"))) int rm_debug_box(double* host, int n) {
+  double* b = dbg_buf(n);
+  if (!b) return -1;
+  return cudaMemcpy(host, b, (size_t)n * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                                   const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -702,13 +812,14 @@ cudaError_t encode_maps(PatchLaunch& L) {
     cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &qr);
     if (e != cudaSuccess || !enc) return cudaErrorNotSupported;
   }
-  for (int m = 0; m < L.pad.ncomp; ++m) {
+  for (int sb = 0; sb < L.nsub; ++sb) {
+    const int m = L.sub_comp[sb];
     cuuint64_t dims[3] = {(cuuint64_t)L.pad.lxp[m], (cuuint64_t)L.pad.len[m][1], (cuuint64_t)L.pad.len[m][2]};
     cuuint64_t strides[2] = {(cuuint64_t)L.pad.lxp[m] * 8, (cuuint64_t)L.pad.lxp[m] * L.pad.len[m][1] * 8};
-    cuuint32_t box[3] = {(cuuint32_t)L.box[m][0], (cuuint32_t)L.box[m][1], (cuuint32_t)L.box[m][2]}, es[3] = {1, 1, 1};
+    cuuint32_t box[3] = {(cuuint32_t)L.box[sb][0], (cuuint32_t)L.box[sb][1], (cuuint32_t)L.box[sb][2]}, es[3] = {1, 1, 1};
     for (int w = 0; w < 2; ++w) {
       double* base = (w == 0 ? L.rpad : L.cpad) + L.pad.poff[m];
-      CUresult r = enc(w == 0 ? &L.tm.r[m] : &L.tm.c[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
+      CUresult r = enc(w == 0 ? &L.tm.r[sb] : &L.tm.c[sb], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
@@ -754,6 +865,8 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
     return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   L.grid = std::max(1, std::min(L.npatch, occ * nsm));
+  if (const char* g = getenv("RM_GRID")) L.grid = std::max(1, std::min(L.grid, atoi(g)));   // experiments
+  if (getenv("RM_NBOX2")) L.nbox = 2;
   if ((e = encode_maps(L)) != cudaSuccess) return e;
   if (getenv("RM_PROFILE") && !L.prof && (e = cudaMalloc(&L.prof, (size_t)24 * 8 * L.grid)) != cudaSuccess) return e;
   // descriptors live in global memory (64-byte aligned allocation), read by the TMA unit
@@ -771,19 +884,40 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   cudaError_t e;
   pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  ScGeom sg{};
+  long long nface = 0, nint = 0;
+  if (L.sc_dinv) {
+    sg.p = L.sc_p;
+    for (int d = 0; d < 3; ++d) sg.n[d] = L.sc_n[d];
+    sg.lxp = L.pad.lxp[0];
+    sg.ly = L.pad.len[0][1];
+    const long long pm = L.sc_p - 1;
+    nface = ((long long)(sg.n[0] + 1) * sg.n[1] * sg.n[2] + (long long)(sg.n[1] + 1) * sg.n[0] * sg.n[2] +
+             (long long)(sg.n[2] + 1) * sg.n[0] * sg.n[1]) * pm * pm;
+    nint = (long long)sg.n[0] * sg.n[1] * sg.n[2] * pm * pm * pm;
+    if (nface > 0) {
+      sc_pre_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.rpad, nface);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+  }
+  if (getenv("RM_DEBUG_SC_PRE")) {   // debug: u += omega * r_sc (the pre step only)
+    unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.rpad, u, omega, n);
+    return cudaGetLastError();
+  }
   if ((e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
   BoxGeom bg;
-  bg.ncomp = L.ncomp;
+  bg.ncomp = L.nsub;
   bg.bytes = 0;
   for (int m = 0; m < 3; ++m) {
     for (int d = 0; d < 3; ++d) bg.box[m][d] = L.box[m][d];
     bg.boff[m] = L.boff[m];
-    if (m < L.ncomp) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
+    if (m < L.nsub) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
   }
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
       L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
-      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof);
+      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof,
+      getenv("RM_DEBUG_Q") ? atoi(getenv("RM_DEBUG_Q")) : -1, dbg_buf(L.box_total));
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -797,6 +931,10 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
             "wait-fwd %.0f | sparse total %.0f box-wait %.0f x-wait %.0f fwd %.0f bwd %.0f | prodA total %.0f room-wait %.0f "
             "| prodB total %.0f room-wait %.0f\n",
             a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15]);
+  }
+  if (L.sc_dinv && nint > 0 && !getenv("RM_DEBUG_SC_NOPOST")) {
+    sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
   return cudaGetLastError();

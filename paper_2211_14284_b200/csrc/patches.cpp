@@ -297,6 +297,10 @@ void build_stream(ClassProgram& C) {
     const Blocks& B = C.lev[l].blk;
     const int ns = B.bs * (B.bs + 1) / 2;
     const int per = std::max(1, (kPieceMax / ns) & ~1);
+    if (C.sc) {   // cell interiors are condensed per cell, outside the patch kernel
+      C.piv_per[l] = per; C.piv_b[l] = C.w_b[l] = C.w_e[l] = (int)C.pieces.size();
+      continue;
+    }
     C.piv_per[l] = per;
     C.piv_ofs[l] = pivofs;
     C.mem_ofs[l] = memofs;
@@ -379,7 +383,7 @@ void build_stream(ClassProgram& C) {
   C.tile_p1 = (int)C.pieces.size();
   for (int l = L - 1; l >= 0; --l) {
     C.wt_b[l] = (int)C.pieces.size();
-    sliced_pieces(C, s, PK_WT, l, C.lev[l].wt);
+    if (!C.sc) sliced_pieces(C, s, PK_WT, l, C.lev[l].wt);
     C.wt_e[l] = (int)C.pieces.size();
   }
   add_piece(C, s, Piece{PK_ZERO, 0, 0, 0, 0, 0, 0, -1});   // a1 = zero-list length, set by build_meta
@@ -467,6 +471,8 @@ struct Builder {
   // ---------------------------------------------------------------- class program (symbolic)
   void build_class(const Entity& e, ClassProgram& C) {
     const int p = sp.p;
+    static const bool sc_off = getenv("RM_NO_SC") != nullptr;   // experiments: ICC-SC inside the patch kernel
+    const bool sc = in.factorization == 1 && in.k == 0 && !sc_off;   // ICC-SC: condense cell interiors per cell
     std::vector<NatDof> dofs;
     int wlo_abs[3][3] = {{0}};
     for (int m = 0; m < sp.ncomp; ++m) {
@@ -646,12 +652,33 @@ struct Builder {
       C.offs[q] = (int)rel;
     }
     C.comp = comp_of_pos;
-    C.pcoord.resize(3 * (size_t)n);
+    // window sub-boxes: one per component, or -- static condensation of the cell interiors (sc,
+    // ICC-SC families) -- the three anchor planes that carry the patch's interface DoFs
+    const int an[3] = {(int)anchor_coord(e.s[0], p), (int)anchor_coord(e.s[1], p), (int)anchor_coord(e.s[2], p)};
+    C.sc = sc;
+    if (!sc) {
+      for (int m = 0; m < sp.ncomp; ++m)
+        for (int d = 0; d < 3; ++d) { C.sub_org[m][d] = C.wlo[m][d]; C.sub_ext[m][d] = C.wext[m][d]; }
+    } else {
+      for (int sb = 0; sb < 3; ++sb)
+        for (int d = 0; d < 3; ++d) {
+          C.sub_org[sb][d] = (d == sb) ? 0 : C.wlo[0][d];
+          C.sub_ext[sb][d] = (d == sb) ? 1 : C.wext[0][d];
+        }
+    }
+    C.psub.assign(n, -1);
+    C.pcoord.assign(3 * (size_t)n, 0);
     for (int q = 0; q < n; ++q) {
       const NatDof& d = dofs[order[q]];
-      C.pcoord[3 * q + 0] = d.ix - wlo_abs[d.comp][0];
-      C.pcoord[3 * q + 1] = d.iy - wlo_abs[d.comp][1];
-      C.pcoord[3 * q + 2] = d.iz - wlo_abs[d.comp][2];
+      const int rel[3] = {d.ix - an[0], d.iy - an[1], d.iz - an[2]};
+      int sb = d.comp;
+      if (sc) {
+        if (d.group == 0) continue;              // cell interiors: condensed per cell (sc kernels)
+        sb = (rel[0] == 0) ? 0 : (rel[1] == 0 ? 1 : 2);
+        if (rel[sb] != 0) throw std::runtime_error("static condensation: interface DoF off the anchor planes");
+      }
+      C.psub[q] = sb;
+      for (int k2 = 0; k2 < 3; ++k2) C.pcoord[3 * q + k2] = rel[k2] - C.sub_org[sb][k2];
     }
     C.slot_map.clear();
     for (auto& mp : slot_nat) {
@@ -1104,25 +1131,28 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   }
   fam->classes.resize(rep.size());
   for (size_t c = 0; c < rep.size(); ++c) B.build_class(rep[c], fam->classes[c]);
-  // window boxes (the patches' working vectors): per component the largest window of any class
-  // plus one (box origins are rounded down to even x: a TMA box row must start 16-byte aligned),
-  // x extent rounded up to even (TMA rows are multiples of 16 bytes); components at 128-byte
-  // aligned offsets
+  // window boxes (the patches' working vectors): per sub-box (component, or anchor plane for
+  // static condensation) the largest extent of any class plus one in x (box origins are rounded
+  // down to even x: a TMA box row must start 16-byte aligned), x extent rounded up to even (TMA
+  // rows are multiples of 16 bytes); sub-boxes at 128-byte aligned offsets
   const Space& spf = B.sp;
+  const bool fam_sc = !fam->classes.empty() && fam->classes[0].sc;
+  fam->nsub = fam_sc ? 3 : spf.ncomp;
+  for (int sb = 0; sb < 3; ++sb) fam->sub_comp[sb] = fam_sc ? 0 : sb;
   {
     for (int m = 0; m < 3; ++m)
       for (int d = 0; d < 3; ++d) fam->box[m][d] = 0;
     for (auto& C : fam->classes)
       if (C.n > 0)
-        for (int m = 0; m < spf.ncomp; ++m)
-          for (int d = 0; d < 3; ++d) fam->box[m][d] = std::max(fam->box[m][d], C.wext[m][d] + (d == 0 ? 1 : 0));
+        for (int m = 0; m < fam->nsub; ++m)
+          for (int d = 0; d < 3; ++d) fam->box[m][d] = std::max(fam->box[m][d], C.sub_ext[m][d] + (d == 0 ? 1 : 0));
     int off = 0;
-    for (int m = 0; m < spf.ncomp; ++m) {
+    for (int m = 0; m < fam->nsub; ++m) {
       fam->box[m][0] = (fam->box[m][0] + 1) & ~1;
       fam->boff[m] = off;
       off += (fam->box[m][0] * fam->box[m][1] * fam->box[m][2] + 15) & ~15;
     }
-    for (int m = spf.ncomp; m <= 3; ++m) fam->boff[m] = off;
+    for (int m = fam->nsub; m <= 3; ++m) fam->boff[m] = off;
     fam->box_total = off;
     if (off > 0xFFFF) throw std::runtime_error("patch window box larger than 65535 entries");
     for (auto& C : fam->classes) build_stream(C);   // piece layout (metadata after the box indices)
@@ -1149,7 +1179,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     int xmask = 0;
     for (int m = 0; m < 3; ++m)
       for (int d = 0; d < 3; ++d) {
-        int o = (m < B.sp.ncomp) ? (int)anchor_coord(e.s[d], B.sp.p) + fam->classes[c].wlo[m][d] : 0;
+        int o = (m < fam->nsub) ? (int)anchor_coord(e.s[d], B.sp.p) + fam->classes[c].sub_org[m][d] : 0;
         if (d == 0 && (o & 1)) { --o; xmask |= 1 << m; }   // even x origin: the class twin shifts by one
         fam->porig[t * 9 + m * 3 + d] = o;
       }
@@ -1198,17 +1228,18 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   }
   // box indices of every class (and twin), the zero lists, and the class meta streams
   for (auto& C : fam->classes) {
-    C.bidx.resize(C.n);
+    C.bidx.assign(C.n, -1);
     std::vector<char> used(fam->box_total, 0);
     for (int t2 = 0; t2 < C.n; ++t2) {
-      const int m = C.comp[t2];
+      const int m = C.psub[t2];
+      if (m < 0) continue;   // condensed cell interior (sc)
       const int b = fam->boff[m] + (C.pcoord[3 * t2 + 2] * fam->box[m][1] + C.pcoord[3 * t2 + 1]) * fam->box[m][0] +
                     C.pcoord[3 * t2 + 0] + C.xshift[m];
       C.bidx[t2] = b;
       used[b] = 1;
     }
     C.zlist.clear();
-    for (int m = 0; m < spf.ncomp; ++m)
+    for (int m = 0; m < fam->nsub; ++m)
       for (int b = fam->boff[m]; b < fam->boff[m] + fam->box[m][0] * fam->box[m][1] * fam->box[m][2]; ++b)
         if (!used[b]) C.zlist.push_back(b);
     build_meta(C);
@@ -1245,6 +1276,78 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     }
   }
   fam->sigma_max = smax;
+  if (fam_sc) {
+    // per-cell static-condensation data from the same cell entries the patch matrices use
+    const Space& sp = B.sp;
+    const int p = sp.p, P1 = p + 1, pm = p - 1, ni = pm * pm * pm;
+    const int64_t ncell = (int64_t)sp.n[0] * sp.n[1] * sp.n[2];
+    fam->sc_dinv.assign((size_t)ncell * ni, 0.0);
+    fam->sc_c.assign((size_t)ncell * 6 * ni, 0.0);
+    fam->sc_nk.assign(ncell, 0);
+    std::string sc_err;
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t K = 0; K < ncell; ++K) {
+      const int cx = (int)(K % sp.n[0]), cy = (int)((K / sp.n[0]) % sp.n[1]), cz = (int)(K / ((int64_t)sp.n[0] * sp.n[1]));
+      const double a = B.coef(in.alpha, in.n_alpha, cx, cy, cz), b = B.coef(in.beta, in.n_beta, cx, cy, cz);
+      CellEntries ce;
+      const CellEntries* E;
+      if (in.cartesian) {
+        E = &B.cart_entries(in.hx[cx], in.hy[cy], in.hz[cz]);
+      } else {
+        double Xc[8][3];
+        for (int az = 0; az < 2; ++az)
+          for (int ay = 0; ay < 2; ++ay)
+            for (int ax = 0; ax < 2; ++ax) {
+              const int64_t vi = (((int64_t)(cz + az) * (sp.n[1] + 1) + (cy + ay)) * (sp.n[0] + 1) + (cx + ax)) * 3;
+              for (int i = 0; i < 3; ++i) Xc[az * 4 + ay * 2 + ax][i] = in.coords[vi + i];
+            }
+        aux_cell_entries(p, Xc, a, b, ce);
+        E = &ce;
+      }
+      std::vector<int> nc(ni, 0);
+      for (size_t t = 0; t < E->row.size(); ++t) {
+        const int r = E->row[t], c = E->col[t];
+        const int ra = r % P1, rb = (r / P1) % P1, rc = r / (P1 * P1);
+        if (ra == 0 || ra == p || rb == 0 || rb == p || rc == 0 || rc == p) continue;   // row not interior
+        const int I = ((rc - 1) * pm + (rb - 1)) * pm + (ra - 1);
+        const double v = in.cartesian ? a * E->kval[t] + b * E->mval[t] : E->kval[t];
+        const int ca = c % P1, cb = (c / P1) % P1, cc = c / (P1 * P1);
+        int face = -1;
+        if (c == r) { fam->sc_dinv[(size_t)K * ni + I] += v; continue; }
+        if (cb == rb && cc == rc && (ca == 0 || ca == p)) face = ca == 0 ? 0 : 1;
+        else if (ca == ra && cc == rc && (cb == 0 || cb == p)) face = cb == 0 ? 2 : 3;
+        else if (ca == ra && cb == rb && (cc == 0 || cc == p)) face = cc == 0 ? 4 : 5;
+        if (face < 0) {
+          if (v != 0.0) {
+#pragma omp critical
+            sc_err = "static condensation: interior DoF coupled outside its 6 face lines";
+          }
+          continue;
+        }
+        fam->sc_c[((size_t)K * 6 + face) * ni + I] += v;
+        ++nc[I];
+      }
+      for (int I = 0; I < ni; ++I) {
+        double& d = fam->sc_dinv[(size_t)K * ni + I];
+        if (!(d > 0)) {
+#pragma omp critical
+          sc_err = "static condensation: non-positive interior diagonal";
+        }
+        d = 1.0 / d;
+      }
+    }
+    if (!sc_err.empty()) throw std::runtime_error(sc_err);
+    for (size_t t = 0; t < np; ++t) {   // patches containing each cell (its interiors in the window)
+      const Entity& e = ents[keep[t]];
+      std::vector<int> cr[3];
+      for (int d = 0; d < 3; ++d) {
+        const DirSpec& ds = e.s[d];
+        if (ds.kind == 1) cr[d] = {ds.v};
+        else { if (ds.v - 1 >= 0) cr[d].push_back(ds.v - 1); if (ds.v < sp.n[d]) cr[d].push_back(ds.v); }
+      }
+      for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0]) ++fam->sc_nk[((int64_t)cz * sp.n[1] + cy) * sp.n[0] + cx];
+    }
+  }
   if (!first_err.empty()) throw std::runtime_error(first_err);
   return fam;
 }

@@ -136,6 +136,9 @@ struct ClassProgram {
   // position its coordinates inside the window, its box index, and the box entries to zero
   int wlo[3][3] = {{0}}, wext[3][3] = {{0}};
   int xshift[3] = {0, 0, 0};             // x-parity twin: box x index shifted by one (odd origins)
+  bool sc = false;                       // cell interiors condensed per cell (ICC-SC families)
+  int sub_org[3][3] = {{0}}, sub_ext[3][3] = {{0}};   // sub-boxes: origin rel. anchor, extent
+  std::vector<int> psub;                 // per position: sub-box (-1: condensed interior)
   std::vector<int> pcoord, bidx, zlist;
   // structural pattern of the patch matrix (CSR over positions)
   std::vector<int> prow, pcol;
@@ -155,8 +158,15 @@ struct PatchFamily {
   int ncolors = 0;
   std::vector<double> values;     // all value blocks
   std::vector<int> porig;         // per patch [comp][dir]: window box origin (global index)
-  int box[3][3] = {{0}};          // per component box extents (x even)
-  int boff[4] = {0, 0, 0, 0};     // component offsets inside the box vector
+  int nsub = 0;                   // sub-boxes: components, or the 3 anchor planes (sc)
+  int sub_comp[3] = {0, 0, 0};    // component of each sub-box
+  int box[3][3] = {{0}};          // per sub-box extents (x even)
+  int boff[4] = {0, 0, 0, 0};     // sub-box offsets inside the box vector
+  // static condensation of the cell interiors (sc): per cell, interior DoFs (i,j,k) in 1..p-1
+  // (x fastest): inverse diagonal, couplings to the 6 face DoFs [x-, x+, y-, y+, z-, z+], and the
+  // number of patches containing the cell
+  std::vector<double> sc_dinv, sc_c;
+  std::vector<int> sc_nk;
   int box_total = 0;
   double sigma_max = 0.0;         // largest ICC restart shift used (reading G7)
   int64_t nfactors = 0;           // distinct value blocks

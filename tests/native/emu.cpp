@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -56,9 +57,36 @@ static std::vector<PieceView> unit_views(const ClassProgram& C, const double* V,
 }
 template <class T> static T rd(const uint8_t* b, size_t i) { T x; std::memcpy(&x, b + i * sizeof(T), sizeof(T)); return x; }
 
-static void emulate_family(const PatchFamily& F, const double* r, double* z) {
+static void emulate_family(const PatchFamily& F, const double* r_in, double* z_out) {
   const size_t np = F.pclass.size();
   const Space& sp = F.sp;
+  // static condensation (sc): r_sc = r - sum_K R_K^T P_GI P_II^{-1} r_I on face DoFs; the patches
+  // solve on the interface only; post: c_I = n_K P_II^{-1} r_I - P_II^{-1} P_IG c_G per cell
+  const bool sc = !F.sc_nk.empty();
+  const int p = sp.p, pm = p - 1, ni = pm * pm * pm;
+  auto cell_dof = [&](int cx, int cy, int cz, int a, int b, int c) {
+    return sp.gidx(0, (int64_t)cz * p + c, (int64_t)cy * p + b, (int64_t)cx * p + a);
+  };
+  auto face_dof = [&](int cx, int cy, int cz, int face, int i, int j, int k) {
+    const int a = face == 0 ? 0 : face == 1 ? p : i, b = face == 2 ? 0 : face == 3 ? p : j, c = face == 4 ? 0 : face == 5 ? p : k;
+    return cell_dof(cx, cy, cz, a, b, c);
+  };
+  std::vector<double> rsc(r_in, r_in + sp.ndof()), cacc(sp.ndof(), 0.0);
+  if (sc)
+    for (int cz = 0; cz < sp.n[2]; ++cz)
+      for (int cy = 0; cy < sp.n[1]; ++cy)
+        for (int cx = 0; cx < sp.n[0]; ++cx) {
+          const int64_t K = ((int64_t)cz * sp.n[1] + cy) * sp.n[0] + cx;
+          for (int k = 1; k < p; ++k)
+            for (int j = 1; j < p; ++j)
+              for (int i = 1; i < p; ++i) {
+                const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
+                const double y = r_in[cell_dof(cx, cy, cz, i, j, k)] * F.sc_dinv[(size_t)K * ni + I];
+                for (int f = 0; f < 6; ++f) rsc[face_dof(cx, cy, cz, f, i, j, k)] -= F.sc_c[((size_t)K * 6 + f) * ni + I] * y;
+              }
+        }
+  const double* r = rsc.data();
+  double* z = cacc.data();
   for (int color = 0; color < F.ncolors; ++color)
     for (size_t t = 0; t < np; ++t) {
       if (F.pcolor[t] != color) continue;
@@ -71,13 +99,14 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
       // ---- gather: TMA box load of every component window (out of bounds -> 0)
       std::vector<double> v(F.box_total, 0.0);
       auto box_walk = [&](auto&& fn) {
-        for (int m = 0; m < sp.ncomp; ++m) {
-          const int* o = &F.porig[t * 9 + m * 3];
-          for (int bz = 0; bz < F.box[m][2]; ++bz)
-            for (int by = 0; by < F.box[m][1]; ++by)
-              for (int bx = 0; bx < F.box[m][0]; ++bx) {
+        for (int sb = 0; sb < F.nsub; ++sb) {
+          const int m = F.sub_comp[sb];
+          const int* o = &F.porig[t * 9 + sb * 3];
+          for (int bz = 0; bz < F.box[sb][2]; ++bz)
+            for (int by = 0; by < F.box[sb][1]; ++by)
+              for (int bx = 0; bx < F.box[sb][0]; ++bx) {
                 const int64_t gx = o[0] + bx, gy = o[1] + by, gz = o[2] + bz;
-                const int b = F.boff[m] + (bz * F.box[m][1] + by) * F.box[m][0] + bx;
+                const int b = F.boff[sb] + (bz * F.box[sb][1] + by) * F.box[sb][0] + bx;
                 if (gx < sp.len(m, 0) && gy < sp.len(m, 1) && gz < sp.len(m, 2)) fn(b, sp.gidx(m, gz, gy, gx));
               }
         }
@@ -192,8 +221,31 @@ static void emulate_family(const PatchFamily& F, const double* r, double* z) {
       // ---- scatter: zero the non-patch box entries, TMA reduce-add of the boxes
       PieceView zw = view((int)C.pieces.size() - 1);
       for (int k = 0; k < zw.a1 - zw.a0; ++k) v[rd<uint16_t>(zw.pb + 16, k)] = 0.0;
+      if (getenv("RM_DEBUG_EMU_PATCH")) {   // experiments: append every finished box (porig + box) to a file
+        FILE* fo = fopen(getenv("RM_DEBUG_EMU_PATCH"), "a");
+        for (int k2 = 0; k2 < 9; ++k2) fprintf(fo, "%d ", F.porig[t * 9 + k2]);
+        for (int b2 = 0; b2 < F.box_total; ++b2) fprintf(fo, "%.17g ", v[b2]);
+        fprintf(fo, "\n");
+        fclose(fo);
+      }
       box_walk([&](int b, int64_t g) { z[g] += v[b]; });
     }
+  if (sc && !getenv("RM_DEBUG_SC_NOPOST"))
+    for (int cz = 0; cz < sp.n[2]; ++cz)
+      for (int cy = 0; cy < sp.n[1]; ++cy)
+        for (int cx = 0; cx < sp.n[0]; ++cx) {
+          const int64_t K = ((int64_t)cz * sp.n[1] + cy) * sp.n[0] + cx;
+          for (int k = 1; k < p; ++k)
+            for (int j = 1; j < p; ++j)
+              for (int i = 1; i < p; ++i) {
+                const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
+                const double dinv = F.sc_dinv[(size_t)K * ni + I];
+                double s = 0.0;
+                for (int f = 0; f < 6; ++f) s += F.sc_c[((size_t)K * 6 + f) * ni + I] * cacc[face_dof(cx, cy, cz, f, i, j, k)];
+                cacc[cell_dof(cx, cy, cz, i, j, k)] = F.sc_nk[K] * r_in[cell_dof(cx, cy, cz, i, j, k)] * dinv - dinv * s;
+              }
+        }
+  for (int64_t g = 0; g < sp.ndof(); ++g) z_out[g] += cacc[g];
 }
 
 extern "C" {
@@ -227,6 +279,39 @@ int emu_precondition(int k, int p, int nx, int ny, int nz, unsigned gamma, const
     snprintf(err, errlen, "%s", e.what());
     return 1;
   }
+}
+
+// r_sc = r - sum_K R_K^T P_GI P_II^{-1} r_I of an ICC-SC family (static condensation, pre step)
+int emu_sc_pre(int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na, const double* beta,
+               long long nb, const double* coords, const double* r, double* rsc) {
+  std::vector<double> h[3];
+  const int n[3] = {nx, ny, nz};
+  for (int d = 0; d < 3; ++d) h[d].assign(n[d], 1.0 / n[d]);
+  SetupInput in{};
+  in.k = 0; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
+  in.coords = coords; in.alpha = alpha; in.beta = beta; in.n_alpha = na; in.n_beta = nb;
+  in.dim = 0; in.factorization = 1; in.interior_only = 0;
+  in.cartesian = (coords == nullptr);
+  in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+  auto F = build_patch_family(in);
+  const Space& sp = F->sp;
+  const int pm = p - 1, ni = pm * pm * pm;
+  for (int64_t g = 0; g < sp.ndof(); ++g) rsc[g] = r[g];
+  auto cd = [&](int cx, int cy, int cz, int a, int b, int c) { return sp.gidx(0, (int64_t)cz * p + c, (int64_t)cy * p + b, (int64_t)cx * p + a); };
+  for (int cz = 0; cz < nz; ++cz)
+    for (int cy = 0; cy < ny; ++cy)
+      for (int cx = 0; cx < nx; ++cx) {
+        const int64_t K = ((int64_t)cz * ny + cy) * nx + cx;
+        for (int k = 1; k < p; ++k)
+          for (int j = 1; j < p; ++j)
+            for (int i = 1; i < p; ++i) {
+              const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
+              const double y = r[cd(cx, cy, cz, i, j, k)] * F->sc_dinv[(size_t)K * ni + I];
+              const int fa[6][3] = {{0, j, k}, {p, j, k}, {i, 0, k}, {i, p, k}, {i, j, 0}, {i, j, p}};
+              for (int f = 0; f < 6; ++f) rsc[cd(cx, cy, cz, fa[f][0], fa[f][1], fa[f][2])] -= F->sc_c[((size_t)K * 6 + f) * ni + I] * y;
+            }
+      }
+  return 0;
 }
 
 // Global Cartesian operator from the product's Kronecker term list (host assembly, COO out).
