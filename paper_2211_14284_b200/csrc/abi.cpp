@@ -291,6 +291,7 @@ struct rm_ctx {
   std::vector<void*> allocs;
   double *d_alpha = nullptr, *d_beta = nullptr, *d_hpow = nullptr;
   double *d_X = nullptr, *d_tabs = nullptr;   // trilinear cells: vertices, 1D tables
+  double* d_cellbuf = nullptr;                 // trilinear apply: per-cell local results
   rm::TriParams tri{};
   int coef_const = 0;
   DevFamily prim, pot;
@@ -464,6 +465,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       for (int d = 0; d < 3; ++d) c->tri.n[d] = c->n[d];
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
+      c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
     }
     // ---- device operator
     c->op = make_op(c->sp, gamma_d);
@@ -614,10 +616,8 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
   if (c->cartesian) {
     CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl));
   } else {
-    CK(rm::launch_apply_init(c->op, f, out, c->ndof, c->st));
-    nl = 1;
-    CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, out,
-                                  f ? -1.0 : 1.0, c->st, &nl));
+    CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, f, out,
+                                  f ? -1.0 : 1.0, c->d_cellbuf, c->st, &nl));
   }
   c->launches[0] += nl;
 }

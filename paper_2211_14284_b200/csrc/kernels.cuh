@@ -66,8 +66,10 @@ struct TriParams {
   unsigned gamma_d;
 };
 cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, const double* X, const double* alpha,
-                                   const double* beta, int coef_const, const double* u, double* out, double sign,
-                                   cudaStream_t st, int* nlaunch);
+                                   const double* beta, int coef_const, const double* u, const double* f, double* out,
+                                   double sign, double* cellbuf, cudaStream_t st, int* nlaunch);
+// doubles of the per-cell result buffer the trilinear apply needs (apply_tri.cu)
+size_t tri_cellbuf_doubles(const TriParams& tp);
 // out = f (or 0) with constrained entries zeroed (apply.cu)
 cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, long long ndof, cudaStream_t st);
 
