@@ -19,32 +19,43 @@
 // (padded rows contribute exact zeros).  Each CTA writes its cell's local result to a cell
 // buffer; tri_gather_kernel then sums, per DoF and in a fixed order, the <= 8 cell
 // contributions: no colouring, one launch over all cells, bitwise deterministic.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace rm {
 
 namespace {
 
-constexpr int TRI_THREADS = 256;
+constexpr int TRI_THREADS = 384;   // 12 warps = 4 planes x 3 yq tiles per batch
+constexpr int TRI_WARPS = TRI_THREADS / 32;
 constexpr int K1 = 16;    // coefficients per direction (padded)
 constexpr int NQP = 24;   // quadrature points per direction (padded)
 constexpr int ZB = 4;     // z planes per batch
-// shared memory (doubles)
-constexpr int XS_AZ = 20, SZ_AZ = K1 * XS_AZ;      // Az/Bz plane, [x][y] (y contiguous)
-constexpr int XS_Q = 17, SZ_Q = K1 * XS_Q;         // Q1/Q2 plane, [x][y]
-constexpr int XS_AS = 20, SZ_AS = NQP * XS_AS;     // AS/AD/BS plane, [yq][x]
-constexpr int XS_TH = 28, SZ_TH = NQP * XS_TH;     // T/HX/HY/HZ plane, [yq][xq]
-constexpr int XS_P = 28, SZ_P = K1 * XS_P;         // P1/P2/P3 plane, [x][yq]
+// shared memory (doubles); strides / XOR swizzles chosen for conflict-free fragment access
+// (layouts found by an exhaustive search over strides and XOR swizzles: the fragment loads AND
+// the fragment stores of every buffer below are bank-conflict free)
+constexpr int XS_AS = 16, SZ_ASF = 8 * XS_AS;   // warp rows AS/AD/BS [f][r][x ^ h_as(r)]
+constexpr int XS_TH = 24, SZ_THF = 8 * XS_TH;   // warp rows T/HX/HY/HZ [f][r][xq ^ h_th(r)]
+constexpr int WR_SIZE = 4 * SZ_THF;             // per-warp region (T/H rows; AS rows alias it)
+constexpr int XS_P = 32, SZ_P = K1 * XS_P;      // P1/P2/P3 plane [x][yq ^ h_p(x)]
+constexpr int XS_Q = 18, SZ_Q = K1 * XS_Q; // Q1/Q2 plane [x][y] (fragment stores: stride = 2 mod 16)
 constexpr int O_SG = 0, O_DG = O_SG + NQP * K1, O_XQ = O_DG + NQP * K1, O_WQ = O_XQ + NQP, O_GC = O_WQ + NQP,
-              O_U = O_GC + 24, O_OUT = O_U + K1 * K1 * K1, O_R1 = O_OUT + K1 * K1 * K1;
-constexpr int R1_SIZE = ZB * 4 * SZ_TH;   // T/H (largest); Az/Bz at [0, 2560), Q at [2560, 4736)
-constexpr int O_Q = ZB * 2 * SZ_AZ;
-constexpr int O_R2 = O_R1 + R1_SIZE;
-constexpr int R2_SIZE = ZB * 3 * SZ_AS;   // AS (largest); P aliases it
-constexpr size_t TRI_SMEM = sizeof(double) * (O_R2 + R2_SIZE);
-static_assert(O_Q + ZB * 2 * SZ_Q <= R1_SIZE, "R1 layout");
-static_assert(ZB * 3 * SZ_P <= R2_SIZE, "R2 layout");
-static_assert(TRI_SMEM <= 227 * 1024, "shared memory");
+              O_FA = O_GC + 24, O_FT = O_FA + 2 * 3 * 4 * 32, O_U = O_FT + 2 * 6 * 2 * 32, O_OUT = O_U + 4096,
+              O_AZ = O_OUT + 4096, O_WR = O_AZ + ZB * 2 * 256, O_P = O_WR + TRI_WARPS * WR_SIZE,
+              O_VX = O_P + ZB * 3 * SZ_P, O_END = O_VX + 28;
+constexpr size_t TRI_SMEM = sizeof(double) * O_END;
+static_assert(ZB * 2 * SZ_Q <= TRI_WARPS * WR_SIZE, "Q aliases the warp regions");
+static_assert(TRI_SMEM <= 232448, "shared memory");
+static_assert(ZB == 4 && TRI_WARPS == 12, "job tables below assume 4 planes and 12 warps");
+
+// [x][y] planes of 16 x 16 with the y index XOR-swizzled: lanes along y (z stages) and the
+// B-fragment pattern (x = 8n + l/4, y = 4k + l%4) are both conflict-free
+__device__ __forceinline__ int sw16(int x, int y) { return x * 16 + (y ^ (4 * (x & 3))); }
+__device__ __forceinline__ int swu(int x, int y) { return x * 16 + (y ^ x); }   // U / OUT planes
+__device__ __forceinline__ int h_as(int r) { return 8 * (r & 1) + 4 * ((r >> 1) & 1); }
+__device__ __forceinline__ int h_th(int r) { return 4 * ((r >> 1) & 1); }
+__device__ __forceinline__ int h_p(int x) { return (5 * x) & 28; }
 
 __device__ __forceinline__ bool tri_cons(long long idx, long long last, unsigned gamma_d, int d) {
   if (idx == 0 && (gamma_d & (1u << (2 * d)))) return true;
@@ -52,16 +63,20 @@ __device__ __forceinline__ bool tri_cons(long long idx, long long last, unsigned
   return false;
 }
 
+// 8-byte global -> shared async copy, zero-filled when !valid (Dirichlet entries, padding)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // D(8x8) += A(8x4, row) B(4x8, col); lane l: a = A[l/4][l%4], b = B[l%4][l/4],
 // c0/c1 = C[l/4][2(l%4) + 0/1]
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));
-}
-__device__ __forceinline__ double pick2(const double a0, const double a1, int i) { return i ? a1 : a0; }
-__device__ __forceinline__ double pick3(const double a0, const double a1, const double a2, int i) {
-  return i == 0 ? a0 : (i == 1 ? a1 : a2);
 }
 
 }  // namespace
@@ -82,10 +97,14 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
   double* XQ = sm + O_XQ;
   double* WQ = sm + O_WQ;
   double* GC = sm + O_GC;   // trilinear coefficients [monomial][coord]
-  double* U = sm + O_U;     // [z][y][x]
-  double* OUT = sm + O_OUT; // [z][y][x], the cell's result (each thread owns its (y, x) line)
-  double* R1 = sm + O_R1;
-  double* R2 = sm + O_R2;
+  double* FA = sm + O_FA;   // fragments T[8m + l/4][4k + l%4], [S/D][m][k][lane]
+  double* FT = sm + O_FT;   // fragments T[4k + l%4][8n + l/4], [S/D][k][n][lane]
+  double* U = sm + O_U;     // [z] swu(x, y)
+  double* OUT = sm + O_OUT; // [z] swu(x, y): the cell's result
+  double* AZ = sm + O_AZ;   // [plane][Az/Bz] sw16(x, y)
+  double* WRg = sm + O_WR + w * WR_SIZE;   // this warp's rows
+  double* PP = sm + O_P;    // [plane][P1/P2/P3] [x][yq]
+  double* QQ = sm + O_WR;   // [plane][Q1/Q2] [x][y] (aliases the warp regions)
   for (int i = t; i < NQP * K1; i += TRI_THREADS) {
     const int q = i / K1, j = i % K1;
     const bool in = q < NQ && j < P1;
@@ -96,65 +115,55 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
     XQ[t] = t < NQ ? tabs[2 * NQ * P1 + t] : 0.0;
     WQ[t] = t < NQ ? tabs[2 * NQ * P1 + NQ + t] : 0.0;
   }
-  const long long cell = blockIdx.x;
-  const int cx = (int)(cell % tp.n[0]), cy = (int)((cell / tp.n[0]) % tp.n[1]), cz = (int)(cell / ((long long)tp.n[0] * tp.n[1]));
-  if (t < 24) {
-    // x(xi, eta, zeta) = sum_a X_a prod_d (1 + s_ad xi_d) / 2 = sum_m GC[m] mono_m,
-    // monomials m: 1, xi, eta, zeta, xi eta, xi zeta, eta zeta, xi eta zeta
-    const int m = t / 3, i = t % 3;
-    const int ex = (m == 1 || m == 4 || m == 5 || m == 7), ey = (m == 2 || m == 4 || m == 6 || m == 7),
-              ez = (m == 3 || m == 5 || m == 6 || m == 7);
-    double s = 0.0;
-    for (int a = 0; a < 8; ++a) {
-      const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2;
-      const double xa = X[(((long long)(cz + az) * (tp.n[1] + 1) + (cy + ay)) * (tp.n[0] + 1) + (cx + ax)) * 3 + i];
-      const double sg = ((ex && !ax) ? -1.0 : 1.0) * ((ey && !ay) ? -1.0 : 1.0) * ((ez && !az) ? -1.0 : 1.0);
-      s += sg * xa;
-    }
-    GC[m * 3 + i] = 0.125 * s;
-  }
-  const double al = coef_const ? alpha[0] : alpha[cell];
-  const double be = coef_const ? beta[0] : beta[cell];
+  double* VX = sm + O_VX;   // prefetched vertices [a][i] (24), alpha, beta of the next cell
+  const long long ncell = (long long)tp.n[0] * tp.n[1] * tp.n[2];
   const long long lastx = (long long)tp.n[0] * p, lasty = (long long)tp.n[1] * p, lastz = (long long)tp.n[2] * p;
-  // coefficients of the cell (constrained entries read as zero), [z][y][x]
-  for (int i = t; i < K1 * K1 * K1; i += TRI_THREADS) {
-    const int z = i >> 8, y = (i >> 4) & 15, x = i & 15;
-    double v = 0.0;
-    if (x < P1 && y < P1 && z < P1) {
+  // async prefetch of a cell's coefficients (constrained entries zero-filled) into U[z] swu(x, y),
+  // its 8 vertices and its coefficients into VX
+  auto prefetch = [&](long long c) {
+    const int cx = (int)(c % tp.n[0]), cy = (int)((c / tp.n[0]) % tp.n[1]), cz = (int)(c / ((long long)tp.n[0] * tp.n[1]));
+    for (int i = t; i < K1 * K1 * K1; i += TRI_THREADS) {
+      const int z = i >> 8, y = (i >> 4) & 15, x = i & 15;
       const long long gx = (long long)cx * p + x, gy = (long long)cy * p + y, gz = (long long)cz * p + z;
-      if (!tri_cons(gx, lastx, tp.gamma_d, 0) && !tri_cons(gy, lasty, tp.gamma_d, 1) && !tri_cons(gz, lastz, tp.gamma_d, 2))
-        v = __ldg(u + (gz * tp.Ly + gy) * tp.Lx + gx);
+      const bool ok = x < P1 && y < P1 && z < P1 && !tri_cons(gx, lastx, tp.gamma_d, 0) &&
+                      !tri_cons(gy, lasty, tp.gamma_d, 1) && !tri_cons(gz, lastz, tp.gamma_d, 2);
+      cp_async8(U + z * 256 + swu(x, y), ok ? u + (gz * tp.Ly + gy) * tp.Lx + gx : u, ok);
     }
-    U[i] = v;
-    OUT[i] = 0.0;
-  }
+    if (t < 24) {
+      const int a = t / 3, i = t % 3, ax = a & 1, ay = (a >> 1) & 1, az = a >> 2;
+      cp_async8(VX + t, X + (((long long)(cz + az) * (tp.n[1] + 1) + (cy + ay)) * (tp.n[0] + 1) + (cx + ax)) * 3 + i, true);
+    } else if (t == 24) {
+      cp_async8(VX + 24, coef_const ? alpha : alpha + c, true);
+    } else if (t == 25) {
+      cp_async8(VX + 25, coef_const ? beta : beta + c, true);
+    }
+    cp_async_commit();
+  };
+  for (int i = t; i < 4096; i += TRI_THREADS) OUT[i] = 0.0;
+  if ((long long)blockIdx.x < ncell) prefetch(blockIdx.x);
   __syncthreads();
-  // table fragments: fa[m][k] = T[8m + l/4][4k + l%4] (A pattern), ft[k][n] = T[4k + l%4][8n + l/4]
-  double faS[3][4], faD[3][4], ftS[6][2], ftD[6][2];
-#pragma unroll
-  for (int m = 0; m < 3; ++m)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      faS[m][k] = SG[(8 * m + l4) * K1 + 4 * k + lm];
-      faD[m][k] = DG[(8 * m + l4) * K1 + 4 * k + lm];
-    }
-#pragma unroll
-  for (int k = 0; k < 6; ++k)
-#pragma unroll
-    for (int n = 0; n < 2; ++n) {
-      ftS[k][n] = SG[(4 * k + lm) * K1 + 8 * n + l4];
-      ftD[k][n] = DG[(4 * k + lm) * K1 + 8 * n + l4];
-    }
-  const int lx = t & 15, ly = t >> 4;   // per-thread line (y, x)
+  for (int i = t; i < 2 * 3 * 4 * 32; i += TRI_THREADS) {
+    const int f = i / 384, m = (i / 128) % 3, k = (i / 32) & 3, l = i & 31;
+    FA[i] = (f ? DG : SG)[(8 * m + (l >> 2)) * K1 + 4 * k + (l & 3)];
+  }
+  for (int i = t; i < 2 * 6 * 2 * 32; i += TRI_THREADS) {
+    const int f = i / 384, k = (i / 64) % 6, n = (i / 32) & 1, l = i & 31;
+    FT[i] = (f ? DG : SG)[(4 * k + (l & 3)) * K1 + 8 * n + (l >> 2)];
+  }
+  auto fa = [&](int f, int m, int k) { return FA[((f * 3 + m) * 4 + k) * 32 + lane]; };
+  auto ft = [&](int f, int k, int n) { return FT[((f * 6 + k) * 2 + n) * 32 + lane]; };
+  const int ly = t & 15, lx = t >> 4;   // per-thread line (x, y), y fastest (threads < 256)
+  const bool zline = t < K1 * K1;
   const int nb = (NQ + ZB - 1) / ZB;
 
-  auto forward_z = [&](int b) {   // Az/Bz of the batch's planes, stored [x][y]
+  auto forward_z = [&](int b) {   // Az/Bz of the batch's planes
+    if (!zline) return;
     double a[ZB], c[ZB];
 #pragma unroll
     for (int pl = 0; pl < ZB; ++pl) a[pl] = c[pl] = 0.0;
 #pragma unroll
     for (int z = 0; z < K1; ++z) {
-      const double uz = U[z * 256 + t];
+      const double uz = U[z * 256 + swu(lx, ly)];
 #pragma unroll
       for (int pl = 0; pl < ZB; ++pl) {
         const int zq = b * ZB + pl;
@@ -164,74 +173,99 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
     }
 #pragma unroll
     for (int pl = 0; pl < ZB; ++pl) {
-      R1[(pl * 2 + 0) * SZ_AZ + lx * XS_AZ + ly] = a[pl];
-      R1[(pl * 2 + 1) * SZ_AZ + lx * XS_AZ + ly] = c[pl];
+      AZ[(pl * 2 + 0) * 256 + sw16(lx, ly)] = a[pl];
+      AZ[(pl * 2 + 1) * 256 + sw16(lx, ly)] = c[pl];
     }
   };
   auto backward_z = [&](int b) {
+    if (!zline) return;
     double q1[ZB], q2[ZB];
 #pragma unroll
     for (int pl = 0; pl < ZB; ++pl) {
-      q1[pl] = R1[O_Q + (pl * 2 + 0) * SZ_Q + lx * XS_Q + ly];
-      q2[pl] = R1[O_Q + (pl * 2 + 1) * SZ_Q + lx * XS_Q + ly];
+      q1[pl] = QQ[(pl * 2 + 0) * SZ_Q + lx * XS_Q + ly];
+      q2[pl] = QQ[(pl * 2 + 1) * SZ_Q + lx * XS_Q + ly];
     }
 #pragma unroll 4
     for (int z = 0; z < K1; ++z) {
-      double o = OUT[z * 256 + t];
+      double o = OUT[z * 256 + swu(lx, ly)];
 #pragma unroll
       for (int pl = 0; pl < ZB; ++pl) {
         const int zq = b * ZB + pl;
         o = fma(SG[zq * K1 + z], q1[pl], fma(DG[zq * K1 + z], q2[pl], o));
       }
-      OUT[z * 256 + t] = o;
+      OUT[z * 256 + swu(lx, ly)] = o;
     }
   };
 
+  const int wpl = w / 3, wmt = w % 3;   // this warp's (plane, yq tile)
+  for (long long cell = blockIdx.x; cell < ncell; cell += gridDim.x) {
+  cp_async_wait_all();
+  __syncthreads();   // U, VX of this cell landed; OUT zeroed
+  if (t < 24) {
+    // x(xi, eta, zeta) = sum_a X_a prod_d (1 + s_ad xi_d) / 2 = sum_m GC[m] mono_m,
+    // monomials m: 1, xi, eta, zeta, xi eta, xi zeta, eta zeta, xi eta zeta
+    const int m = t / 3, i = t % 3;
+    const int ex = (m == 1 || m == 4 || m == 5 || m == 7), ey = (m == 2 || m == 4 || m == 6 || m == 7),
+              ez = (m == 3 || m == 5 || m == 6 || m == 7);
+    double s = 0.0;
+    for (int a = 0; a < 8; ++a) {
+      const int ax = a & 1, ay = (a >> 1) & 1, az = a >> 2;
+      const double sg = ((ex && !ax) ? -1.0 : 1.0) * ((ey && !ay) ? -1.0 : 1.0) * ((ez && !az) ? -1.0 : 1.0);
+      s += sg * VX[a * 3 + i];
+    }
+    GC[m * 3 + i] = 0.125 * s;
+  }
   forward_z(0);
-  __syncthreads();
+  __syncthreads();   // also publishes GC
+  const double al = VX[24], be = VX[25];
+  const long long next = cell + gridDim.x;
   for (int b = 0; b < nb; ++b) {
-    // ---- forward y: warp w -> plane w/2, x tile w%2; all three yq tiles, fields AS, AD, BS
-    {
-      const int pl = w >> 1, nt = w & 1;
-      double cS[3][2] = {}, cD[3][2] = {}, cB[3][2] = {};
-      const double* az = R1 + (pl * 2 + 0) * SZ_AZ + (8 * nt + l4) * XS_AZ + lm;
-      const double* bz = R1 + (pl * 2 + 1) * SZ_AZ + (8 * nt + l4) * XS_AZ + lm;
+    const int zq = b * ZB + wpl;
+    if (b == nb - 1 && next < ncell) prefetch(next);   // U's last reader was forward_z(nb - 1)
+    // ===== per-warp chain on rows yq in tile wmt of plane wpl (only __syncwarp inside)
+    {   // forward y: AS/AD/BS rows [r][x] (x tiles 0, 1), 24 DMMA
+      double cS[2][2] = {}, cD[2][2] = {}, cB[2][2] = {};
+      const double* az = AZ + (wpl * 2 + 0) * 256;
+      const double* bz = AZ + (wpl * 2 + 1) * 256;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const double ba = az[4 * k], bb = bz[4 * k];
+        const double aS = fa(0, wmt, k), aD = fa(1, wmt, k);
 #pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          dmma(cS[m], faS[m][k], ba);
-          dmma(cD[m], faD[m][k], ba);
-          dmma(cB[m], faS[m][k], bb);
+        for (int nt = 0; nt < 2; ++nt) {
+          const int o = sw16(8 * nt + l4, 4 * k + lm);
+          const double ba = az[o], bb = bz[o];
+          dmma(cS[nt], aS, ba);
+          dmma(cD[nt], aD, ba);
+          dmma(cB[nt], aS, bb);
         }
       }
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int o = (8 * m + l4) * XS_AS + 8 * nt + 2 * lm;
-        *reinterpret_cast<double2*>(R2 + (pl * 3 + 0) * SZ_AS + o) = make_double2(cS[m][0], cS[m][1]);
-        *reinterpret_cast<double2*>(R2 + (pl * 3 + 1) * SZ_AS + o) = make_double2(cD[m][0], cD[m][1]);
-        *reinterpret_cast<double2*>(R2 + (pl * 3 + 2) * SZ_AS + o) = make_double2(cB[m][0], cB[m][1]);
+      for (int nt = 0; nt < 2; ++nt) {
+        const int o = l4 * XS_AS + ((8 * nt + 2 * lm) ^ h_as(l4));
+        *reinterpret_cast<double2*>(WRg + 0 * SZ_ASF + o) = make_double2(cS[nt][0], cS[nt][1]);
+        *reinterpret_cast<double2*>(WRg + 1 * SZ_ASF + o) = make_double2(cD[nt][0], cD[nt][1]);
+        *reinterpret_cast<double2*>(WRg + 2 * SZ_ASF + o) = make_double2(cB[nt][0], cB[nt][1]);
       }
     }
-    __syncthreads();
-    // ---- forward x + pointwise: 36 (plane, yq tile, xq tile) jobs over 8 warps
-    for (int j = w; j < ZB * 9; j += 8) {
-      const int pl = j / 9, mt = (j % 9) / 3, nt = j % 3;
-      const int zq = b * ZB + pl;
-      double cu[2] = {}, c0[2] = {}, c1[2] = {}, c2[2] = {};
-      const double* as = R2 + (pl * 3 + 0) * SZ_AS + (8 * mt + l4) * XS_AS + lm;
+    __syncwarp();
+    // forward x: u_q and hat-gradient at the 8 x 24 points of the rows, 48 DMMA
+    double cu[3][2] = {}, c0[3][2] = {}, c1[3][2] = {}, c2[3][2] = {};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double aS = as[4 * k], aD = as[SZ_AS + 4 * k], aB = as[2 * SZ_AS + 4 * k];
-        const double bS = pick3(faS[0][k], faS[1][k], faS[2][k], nt), bD = pick3(faD[0][k], faD[1][k], faD[2][k], nt);
-        dmma(cu, aS, bS);
-        dmma(c0, aS, bD);
-        dmma(c1, aD, bS);
-        dmma(c2, aB, bS);
+    for (int k = 0; k < 4; ++k) {
+      const double* as = WRg + l4 * XS_AS + ((4 * k + lm) ^ h_as(l4));
+      const double aS = as[0], aD = as[SZ_ASF], aB = as[2 * SZ_ASF];
+#pragma unroll
+      for (int nt = 0; nt < 3; ++nt) {
+        const double bS = fa(0, nt, k), bD = fa(1, nt, k);
+        dmma(cu[nt], aS, bS);
+        dmma(c0[nt], aS, bD);
+        dmma(c1[nt], aD, bS);
+        dmma(c2[nt], aB, bS);
       }
-      // pointwise at (zq, yq, xq + i), i = 0, 1
-      const int yq = 8 * mt + l4, xq0 = 8 * nt + 2 * lm;
+    }
+    __syncwarp();   // AS rows consumed: the region now takes T/H rows
+    {   // pointwise at (zq, yq, xq)
+      const int yq = 8 * wmt + l4;
       const double ze = XQ[zq], et = XQ[yq];
       const double wzy = WQ[zq] * WQ[yq];
       double Jx[3], Jya[3], Jyb[3], Jza[3], Jzb[3];
@@ -245,101 +279,136 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
         Jza[i] = fma(g6, et, g3);                             // d/dzeta = Jza + Jzb xi
         Jzb[i] = fma(g7, et, g5);
       }
-      double tv[2], hx[2], hy[2], hz[2];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int xq = xq0 + e;
-        const double xi = XQ[xq];
-        double J[3][3];
+      for (int nt = 0; nt < 3; ++nt) {
+        double tv[2], hx[2], hy[2], hz[2];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          J[i][0] = Jx[i];
-          J[i][1] = fma(Jyb[i], xi, Jya[i]);
-          J[i][2] = fma(Jzb[i], xi, Jza[i]);
+        for (int e = 0; e < 2; ++e) {
+          const int xq = 8 * nt + 2 * lm + e;
+          const double xi = XQ[xq];
+          double J[3][3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            J[i][0] = Jx[i];
+            J[i][1] = fma(Jyb[i], xi, Jya[i]);
+            J[i][2] = fma(Jzb[i], xi, Jza[i]);
+          }
+          // adj(J): J^{-1} = adj / det
+          const double a00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], a01 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                       a02 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+          const double a10 = J[1][2] * J[2][0] - J[1][0] * J[2][2], a11 = J[0][0] * J[2][2] - J[0][2] * J[2][0],
+                       a12 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+          const double a20 = J[1][0] * J[2][1] - J[1][1] * J[2][0], a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                       a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+          const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
+          const double wgt = wzy * WQ[xq];
+          const double ad = fabs(det);
+          const double kk = al * wgt * __drcp_rn(ad);
+          const double g0 = c0[nt][e], g1 = c1[nt][e], g2 = c2[nt][e];
+          // h = k adj adj^T g: v = adj^T g, h = k adj v
+          const double v0 = a00 * g0 + a10 * g1 + a20 * g2, v1 = a01 * g0 + a11 * g1 + a21 * g2,
+                       v2 = a02 * g0 + a12 * g1 + a22 * g2;
+          hx[e] = kk * (a00 * v0 + a01 * v1 + a02 * v2);
+          hy[e] = kk * (a10 * v0 + a11 * v1 + a12 * v2);
+          hz[e] = kk * (a20 * v0 + a21 * v1 + a22 * v2);
+          tv[e] = be * wgt * ad * cu[nt][e];
         }
-        // adj(J): J^{-1} = adj / det
-        const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], c01 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
-                     c02 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
-        const double c10 = J[1][2] * J[2][0] - J[1][0] * J[2][2], c11 = J[0][0] * J[2][2] - J[0][2] * J[2][0],
-                     c12 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
-        const double c20 = J[1][0] * J[2][1] - J[1][1] * J[2][0], c21 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
-                     c22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
-        const double det = J[0][0] * c00 + J[0][1] * c10 + J[0][2] * c20;
-        const double wgt = wzy * WQ[xq];
-        const double ad = fabs(det);
-        const double k = al * wgt * __drcp_rn(ad);
-        const double g0 = c0[e], g1 = c1[e], g2 = c2[e];
-        // h = k adj adj^T g: v = adj^T g (columns of adj dotted with g), h = k adj v
-        const double v0 = c00 * g0 + c10 * g1 + c20 * g2, v1 = c01 * g0 + c11 * g1 + c21 * g2,
-                     v2 = c02 * g0 + c12 * g1 + c22 * g2;
-        hx[e] = k * (c00 * v0 + c01 * v1 + c02 * v2);
-        hy[e] = k * (c10 * v0 + c11 * v1 + c12 * v2);
-        hz[e] = k * (c20 * v0 + c21 * v1 + c22 * v2);
-        tv[e] = be * wgt * ad * cu[e];
+        const int o = l4 * XS_TH + ((8 * nt + 2 * lm) ^ h_th(l4));
+        *reinterpret_cast<double2*>(WRg + 0 * SZ_THF + o) = make_double2(tv[0], tv[1]);
+        *reinterpret_cast<double2*>(WRg + 1 * SZ_THF + o) = make_double2(hx[0], hx[1]);
+        *reinterpret_cast<double2*>(WRg + 2 * SZ_THF + o) = make_double2(hy[0], hy[1]);
+        *reinterpret_cast<double2*>(WRg + 3 * SZ_THF + o) = make_double2(hz[0], hz[1]);
       }
-      const int o = yq * XS_TH + xq0;
-      *reinterpret_cast<double2*>(R1 + (pl * 4 + 0) * SZ_TH + o) = make_double2(tv[0], tv[1]);
-      *reinterpret_cast<double2*>(R1 + (pl * 4 + 1) * SZ_TH + o) = make_double2(hx[0], hx[1]);
-      *reinterpret_cast<double2*>(R1 + (pl * 4 + 2) * SZ_TH + o) = make_double2(hy[0], hy[1]);
-      *reinterpret_cast<double2*>(R1 + (pl * 4 + 3) * SZ_TH + o) = make_double2(hz[0], hz[1]);
     }
-    __syncthreads();
-    // ---- backward x: 24 (plane, yq tile, x tile) jobs; P stored [x][yq]
-#pragma unroll 1
-    for (int j = w; j < ZB * 6; j += 8) {
-      const int pl = j / 6, mt = (j % 6) >> 1, nt = j & 1;
-      double p1[2] = {}, p2[2] = {}, p3[2] = {};
-      const double* th = R1 + (pl * 4) * SZ_TH + (8 * mt + l4) * XS_TH + lm;
+    __syncwarp();
+    {   // backward x: P rows (x tiles 0, 1), 48 DMMA; P stored [x][yq] for the block-wide y stage
+      double pa[2][2] = {}, pb[2][2] = {}, p2[2][2] = {}, p3[2][2] = {};
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
-        const double aT = th[4 * k], aX = th[SZ_TH + 4 * k], aY = th[2 * SZ_TH + 4 * k], aZ = th[3 * SZ_TH + 4 * k];
-        const double bS = pick2(ftS[k][0], ftS[k][1], nt), bD = pick2(ftD[k][0], ftD[k][1], nt);
-        dmma(p1, aT, bS);
-        dmma(p1, aX, bD);
-        dmma(p2, aY, bS);
-        dmma(p3, aZ, bS);
+        const double* a = WRg + l4 * XS_TH + ((4 * k + lm) ^ h_th(l4));
+        const double aT = a[0], aX = a[SZ_THF], aY = a[2 * SZ_THF], aZ = a[3 * SZ_THF];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const double bS = ft(0, k, nt), bD = ft(1, k, nt);
+          dmma(pa[nt], aT, bS);
+          dmma(pb[nt], aX, bD);
+          dmma(p2[nt], aY, bS);
+          dmma(p3[nt], aZ, bS);
+        }
       }
-      const int yq = 8 * mt + l4, x0 = 8 * nt + 2 * lm;
-      double* P = R2 + (pl * 3) * SZ_P + yq;
-      P[x0 * XS_P] = p1[0];
-      P[(x0 + 1) * XS_P] = p1[1];
-      P[SZ_P + x0 * XS_P] = p2[0];
-      P[SZ_P + (x0 + 1) * XS_P] = p2[1];
-      P[2 * SZ_P + x0 * XS_P] = p3[0];
-      P[2 * SZ_P + (x0 + 1) * XS_P] = p3[1];
+      const int yq = 8 * wmt + l4;
+      double* P = PP + (wpl * 3) * SZ_P;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int x = 8 * nt + 2 * lm + e;
+          const int o = x * XS_P + (yq ^ h_p(x));
+          P[o] = pa[nt][e] + pb[nt][e];
+          P[SZ_P + o] = p2[nt][e];
+          P[2 * SZ_P + o] = p3[nt][e];
+        }
     }
     __syncthreads();
-    // ---- backward y: 16 (plane, y tile, x tile) jobs; Q stored [x][y]
-#pragma unroll 1
-    for (int j = w; j < ZB * 4; j += 8) {
-      const int pl = j >> 2, mt = (j >> 1) & 1, nt = j & 1;
-      double q1[2] = {}, q2[2] = {};
-      const double* P = R2 + (pl * 3) * SZ_P + (8 * nt + l4) * XS_P + lm;
+    // ===== backward y: warps 0-7 two Q1 jobs (2 terms), warps 8-11 four Q2 jobs; Q stored [x][y]
+    if (w < 8) {
+      double qa[2][2] = {}, qb[2][2] = {};
+      const int mt = (w >> 1) & 1;   // shared by both jobs
 #pragma unroll
       for (int k = 0; k < 6; ++k) {
-        const double b1 = P[4 * k], b2 = P[SZ_P + 4 * k], b3 = P[2 * SZ_P + 4 * k];
-        const double aS = pick2(ftS[k][0], ftS[k][1], mt), aD = pick2(ftD[k][0], ftD[k][1], mt);
-        dmma(q1, aS, b1);
-        dmma(q1, aD, b2);
-        dmma(q2, aS, b3);
+        const double aS = ft(0, k, mt), aD = ft(1, k, mt);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int j = w + 8 * i, pl = j >> 2, nt = j & 1;
+          const int x = 8 * nt + l4;
+          const double* P = PP + (pl * 3) * SZ_P + x * XS_P + ((4 * k + lm) ^ h_p(x));
+          dmma(qa[i], aS, P[0]);
+          dmma(qb[i], aD, P[SZ_P]);
+        }
       }
-      const int y = 8 * mt + l4, x0 = 8 * nt + 2 * lm;
-      double* Q = R1 + O_Q + (pl * 2) * SZ_Q + y;
-      Q[x0 * XS_Q] = q1[0];
-      Q[(x0 + 1) * XS_Q] = q1[1];
-      Q[SZ_Q + x0 * XS_Q] = q2[0];
-      Q[SZ_Q + (x0 + 1) * XS_Q] = q2[1];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int j = w + 8 * i, pl = j >> 2, nt = j & 1;
+        const int y = 8 * mt + l4, x0 = 8 * nt + 2 * lm;
+        double* Q = QQ + (pl * 2) * SZ_Q + y;
+        Q[x0 * XS_Q] = qa[i][0] + qb[i][0];
+        Q[(x0 + 1) * XS_Q] = qa[i][1] + qb[i][1];
+      }
+    } else {
+      double qc[4][2] = {};
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = (w - 8) + 4 * i, pl = j >> 2, mt = (j >> 1) & 1, nt = j & 1;
+          const int x = 8 * nt + l4;
+          dmma(qc[i], ft(0, k, mt), PP[(pl * 3 + 2) * SZ_P + x * XS_P + ((4 * k + lm) ^ h_p(x))]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = (w - 8) + 4 * i, pl = j >> 2, mt = (j >> 1) & 1, nt = j & 1;
+        const int y = 8 * mt + l4, x0 = 8 * nt + 2 * lm;
+        double* Q = QQ + (pl * 2 + 1) * SZ_Q + y;
+        Q[x0 * XS_Q] = qc[i][0];
+        Q[(x0 + 1) * XS_Q] = qc[i][1];
+      }
     }
     __syncthreads();
-    // ---- backward z of this batch, forward z of the next (disjoint parts of R1)
+    // ===== backward z of this batch, forward z of the next
     backward_z(b);
     if (b + 1 < nb) forward_z(b + 1);
     __syncthreads();
   }
-  // local result of the cell, [z][y][x] with stride P1
-  if (lx < P1 && ly < P1) {
-    double* o = cellbuf + cell * P1 * P1 * P1 + ly * P1 + lx;
-    for (int z = 0; z < P1; ++z) o[z * P1 * P1] = OUT[z * 256 + t];
+  // local result of the cell -> cellbuf [z][y][x] (stride P1), x fastest for coalescing; OUT
+  // zeroed for the next cell by the thread that read it (padding entries stay zero)
+  const int n3 = P1 * P1 * P1;
+  double* o = cellbuf + cell * n3;
+  for (int i = t; i < n3; i += TRI_THREADS) {
+    const int z = i / (P1 * P1), y = (i / P1) % P1, x = i % P1;
+    o[i] = OUT[z * 256 + swu(x, y)];
+    OUT[z * 256 + swu(x, y)] = 0.0;
+  }
   }
 }
 
@@ -392,7 +461,15 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
   const long long ncell = (long long)tp.n[0] * tp.n[1] * tp.n[2];
   const long long nd = tp.Lx * tp.Ly * tp.Lz;
   if (ncell <= 0) return cudaSuccess;
-  apply_tri_kernel<<<(unsigned)ncell, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, cellbuf);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const unsigned grid = (unsigned)std::min<long long>(ncell, nsm);   // persistent: one CTA per SM
+  apply_tri_kernel<<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, cellbuf);
   tri_gather_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(tp, cellbuf, f, out, sign);
   if (nlaunch) *nlaunch += 2;
   return cudaGetLastError();
