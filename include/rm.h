@@ -123,12 +123,16 @@ rm_status rm_pcg(rm_ctx *ctx, const double *f, double *u, double rtol, int32_t m
                  int32_t *iters, double *rel_natural_residual);
 
 /* Phase timing (instrumentation used by bench.py).  While enabled, rm_relax / rm_precondition /
- * rm_pcg record CUDA events on their stream around each phase: [0] residual (apply kernel),
- * [1] primary patch solves (one launch per colour), [2] potential stage (D^T, patch solves, D),
- * [3] everything else (copies, PCG vector kernels).  rm_timing_read synchronises and returns the
- * accumulated milliseconds and kernel launches per phase since the last enable/read. */
+ * rm_pcg record CUDA events on their stream around each phase: [0] residual (apply kernels incl.
+ * init / gather), [1] primary patch stage (pad, condensation, patch kernel, combine), [2] potential
+ * stage (D^T, patch stage, D), [3] everything else (copies, PCG vector kernels); and around single
+ * kernels (subsets of the phases above): [4] the persistent patch kernel launches (primary and
+ * potential families), [5] the apply kernel launches (without init / gather).  rm_timing_read
+ * synchronises and returns the accumulated milliseconds and launches per entry since the last
+ * enable/read.  Arrays have RM_NPHASE entries. */
+#define RM_NPHASE 8
 rm_status rm_timing_enable(rm_ctx *ctx, int32_t on);
-rm_status rm_timing_read(rm_ctx *ctx, double ms[4], int64_t launches[4]);
+rm_status rm_timing_read(rm_ctx *ctx, double ms[RM_NPHASE], int64_t launches[RM_NPHASE]);
 
 void rm_destroy(rm_ctx *ctx);
 const char *rm_last_error(void);

@@ -25,6 +25,7 @@ RM_PAFW, RM_PH = 0, 1
 RM_CHOL, RM_ICC_SC = 0, 1
 RM_ALL_ENTITIES, RM_INTERIOR_ONLY = 0, 1
 RM_OK, RM_NOT_CONVERGED = 0, 1
+RM_NPHASE = 8   # entries of rm_timing_read (include/rm.h)
 STATUS = {0: "RM_OK", 1: "RM_NOT_CONVERGED", -1: "RM_EINVAL", -2: "RM_ENOMEM", -3: "RM_ENUMERIC",
           -4: "RM_ECUDA", -5: "RM_ENCCL"}
 
@@ -74,7 +75,7 @@ def _load():
     lib.rm_relax_host.argtypes = [P, P, P, P, D]
     lib.rm_pcg.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]
     lib.rm_timing_enable.argtypes = [P, I32]
-    lib.rm_timing_read.argtypes = [P, ctypes.POINTER(D * 4), ctypes.POINTER(I64 * 4)]
+    lib.rm_timing_read.argtypes = [P, ctypes.POINTER(D * RM_NPHASE), ctypes.POINTER(I64 * RM_NPHASE)]
     lib.rm_destroy.argtypes = [P]
     lib.rm_destroy.restype = None
     lib.rm_last_error.restype = ctypes.c_char_p
@@ -218,9 +219,10 @@ def rm_timing_enable(ctx: RmContext, on=True):
 
 
 def rm_timing_read(ctx: RmContext):
-    """-> (ms[4], launches[4]) accumulated per phase: residual, primary patches, potential, other."""
-    ms = (ctypes.c_double * 4)()
-    nl = (ctypes.c_int64 * 4)()
+    """-> (ms[RM_NPHASE], launches[RM_NPHASE]) accumulated per entry (include/rm.h): residual,
+    primary patch stage, potential stage, other, patch kernel alone, apply kernel alone."""
+    ms = (ctypes.c_double * RM_NPHASE)()
+    nl = (ctypes.c_int64 * RM_NPHASE)()
     _check(_lib.rm_timing_read(ctx.h, ctypes.byref(ms), ctypes.byref(nl)))
     return list(ms), list(nl)
 

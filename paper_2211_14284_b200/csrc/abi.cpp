@@ -151,6 +151,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     Lh.sc_dinv = F.upload(P.sc_dinv);
     Lh.sc_c = F.upload(P.sc_c);
     Lh.sc_nk = F.upload(P.sc_nk);
+    Lh.sc_fb = F.upload(std::vector<double>(P.sc_nk.size() * 6 * (size_t)(P.sp.p - 1) * (P.sp.p - 1), 0.0));
     Lh.sc_p = P.sp.p;
     for (int d = 0; d < 3; ++d) Lh.sc_n[d] = P.sp.n[d];
   }
@@ -306,7 +307,7 @@ struct rm_ctx {
   bool timing = false;
   struct Ev { int phase; cudaEvent_t a, b; };
   std::vector<Ev> events;
-  int64_t launches[4] = {0, 0, 0, 0};
+  int64_t launches[RM_NPHASE] = {};
 
   double* dalloc(size_t n) {
     void* d = nullptr;
@@ -592,6 +593,31 @@ rm_status rm_constrained_mask(const rm_ctx* c, uint8_t* mask) {
 
 namespace {
 
+// records CUDA events around one kernel launch (phases 4, 5) when timing is enabled
+struct KPhase {
+  rm_ctx* c;
+  int ph;
+  cudaEvent_t a = nullptr;
+  static void begin(void* p) {
+    auto* k = static_cast<KPhase*>(p);
+    if (!k->c->timing) return;
+    if (cudaEventCreate(&k->a) != cudaSuccess || cudaEventRecord(k->a, k->c->st) != cudaSuccess) k->a = nullptr;
+  }
+  static void end(void* p) {
+    auto* k = static_cast<KPhase*>(p);
+    if (!k->a) return;
+    cudaEvent_t b;
+    if (cudaEventCreate(&b) == cudaSuccess && cudaEventRecord(b, k->c->st) == cudaSuccess) {
+      k->c->events.push_back({k->ph, k->a, b});
+      k->c->launches[k->ph] += 1;
+    } else {
+      cudaEventDestroy(k->a);
+    }
+    k->a = nullptr;
+  }
+  rm::KTimer timer() { return rm::KTimer{&KPhase::begin, &KPhase::end, this}; }
+};
+
 // records CUDA events around a phase when timing is enabled
 struct Phase {
   rm_ctx* c;
@@ -613,18 +639,23 @@ struct Phase {
 void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
   Phase ph(c, 0);
   int nl = 0;
+  KPhase kp{c, 5};
+  const rm::KTimer kt = kp.timer();
   if (c->cartesian) {
-    CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl));
+    CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl,
+                                  &kt));
   } else {
     CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, f, out,
-                                  f ? -1.0 : 1.0, c->d_cellbuf, c->st, &nl));
+                                  f ? -1.0 : 1.0, c->d_cellbuf, c->st, &nl, &kt));
   }
   c->launches[0] += nl;
 }
 
 int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
   if (F.npatch == 0) return 0;
-  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st));
+  KPhase kp{c, 4};
+  const rm::KTimer kt = kp.timer();
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt));
   return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
@@ -767,10 +798,10 @@ rm_status rm_timing_enable(rm_ctx* c, int32_t on) {
   });
 }
 
-rm_status rm_timing_read(rm_ctx* c, double ms[4], int64_t launches[4]) {
+rm_status rm_timing_read(rm_ctx* c, double ms[RM_NPHASE], int64_t launches[RM_NPHASE]) {
   return guarded(c, [&] {
     CK(cudaStreamSynchronize(c->st));
-    double acc[4] = {0, 0, 0, 0};
+    double acc[RM_NPHASE] = {};
     for (auto& e : c->events) {
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, e.a, e.b));
@@ -778,7 +809,7 @@ rm_status rm_timing_read(rm_ctx* c, double ms[4], int64_t launches[4]) {
       cudaEventDestroy(e.a); cudaEventDestroy(e.b);
     }
     c->events.clear();
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < RM_NPHASE; ++i) {
       if (ms) ms[i] = acc[i];
       if (launches) launches[i] = c->launches[i];
       c->launches[i] = 0;

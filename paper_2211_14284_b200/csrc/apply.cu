@@ -303,9 +303,14 @@ cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, 
 
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
-                                   long long ndof, cudaStream_t st, int* nlaunch) {
+                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt) {
   apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
   int nl = 1;
+  if (kt) kt->begin(kt->arg);
+  struct End {
+    const KTimer* kt;
+    ~End() { if (kt) kt->end(kt->arg); }
+  } end_{kt};
   if (op.k == 0) {
     const double sgn = f ? -1.0 : 1.0;
     cudaError_t e;

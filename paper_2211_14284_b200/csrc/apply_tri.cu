@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
                                                                     const double* __restrict__ alpha,
                                                                     const double* __restrict__ beta, int coef_const,
                                                                     const double* __restrict__ u,
+                                                                    const double* __restrict__ f,
+                                                                    double* __restrict__ out, double sign,
                                                                     double* __restrict__ cellbuf) {
   extern __shared__ __align__(16) double sm[];
   const int P1 = tp.p + 1, NQ = tp.nq, p = tp.p;
@@ -400,57 +402,85 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
     if (b + 1 < nb) forward_z(b + 1);
     __syncthreads();
   }
-  // local result of the cell -> cellbuf [z][y][x] (stride P1), x fastest for coalescing; OUT
-  // zeroed for the next cell by the thread that read it (padding entries stay zero)
-  const int n3 = P1 * P1 * P1;
-  double* o = cellbuf + cell * n3;
-  for (int i = t; i < n3; i += TRI_THREADS) {
-    const int z = i / (P1 * P1), y = (i / P1) % P1, x = i % P1;
-    o[i] = OUT[z * 256 + swu(x, y)];
-    OUT[z * 256 + swu(x, y)] = 0.0;
+  // local result of the cell: interior DoFs (owned by this cell alone) straight to out =
+  // sign * A_K u (stores only; the gather adds f); skeleton entries (a local index 0 or p) ->
+  // cellbuf [z][y][x].  OUT is zeroed for the next cell by the thread that read it.
+  {
+    const int cx = (int)(cell % tp.n[0]), cy = (int)((cell / tp.n[0]) % tp.n[1]),
+              cz = (int)(cell / ((long long)tp.n[0] * tp.n[1]));
+    const int n3 = P1 * P1 * P1;
+    double* ob = cellbuf + cell * n3;
+    for (int i = t; i < n3; i += TRI_THREADS) {
+      const int z = i / (P1 * P1), y = (i / P1) % P1, x = i % P1;
+      const double v = OUT[z * 256 + swu(x, y)];
+      OUT[z * 256 + swu(x, y)] = 0.0;
+      if (x == 0 || x == p || y == 0 || y == p || z == 0 || z == p) {
+        ob[i] = v;
+      } else {
+        const long long g = (((long long)cz * p + z) * tp.Ly + (long long)cy * p + y) * tp.Lx + (long long)cx * p + x;
+        out[g] = sign * v;
+      }
+    }
   }
   }
 }
 
-// out[g] = f[g] (or 0) + sign * sum over the cells containing g of their local result;
-// constrained entries 0.  Fixed summation order (cells ascending in z, y, x): deterministic.
+// out[g] = f[g] (or 0) + (cell interior DoF: the value the apply kernel stored | skeleton DoF,
+// on a cell face, edge or vertex: sign * the sum over the cells containing g of their local
+// result, cells ascending in z, y, x: deterministic); constrained entries 0.  One warp per grid
+// row (gy, gz), grid-stride over rows; 32-bit index math.
 __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                   const double* __restrict__ f, double* __restrict__ out, double sign) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nd = tp.Lx * tp.Ly * tp.Lz;
-  if (g >= nd) return;
-  const int p = tp.p, P1 = p + 1;
-  const long long gx = g % tp.Lx, gy = (g / tp.Lx) % tp.Ly, gz = g / (tp.Lx * tp.Ly);
-  const long long lastx = (long long)tp.n[0] * p, lasty = (long long)tp.n[1] * p, lastz = (long long)tp.n[2] * p;
-  if (tri_cons(gx, lastx, tp.gamma_d, 0) || tri_cons(gy, lasty, tp.gamma_d, 1) || tri_cons(gz, lastz, tp.gamma_d, 2)) {
-    out[g] = 0.0;
-    return;
+  const int Lx = (int)tp.Lx, Ly = (int)tp.Ly, Lz = (int)tp.Lz;
+  const int p = tp.p, P1 = p + 1, n3 = P1 * P1 * P1;
+  const int lane = threadIdx.x & 31;
+  const int nrow = Ly * Lz;
+  const int wstride = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrow; row += wstride) {
+    const int gy = row % Ly, gz = row / Ly;
+    const bool rcons = tri_cons(gy, tp.n[1] * p, tp.gamma_d, 1) || tri_cons(gz, tp.n[2] * p, tp.gamma_d, 2);
+    const bool rskel = (gy % p == 0) || (gz % p == 0);
+    // cells and local indices along y and z of this row
+    int cyv[2], ayv[2], ny = 0, czv[2], azv[2], nz = 0;
+    {
+      int cc = gy / p; if (cc >= tp.n[1]) cc = tp.n[1] - 1;
+      const int aa = gy - cc * p;
+      if (aa == 0 && cc > 0) { cyv[ny] = cc - 1; ayv[ny] = p; ++ny; }
+      cyv[ny] = cc; ayv[ny] = aa; ++ny;
+    }
+    {
+      int cc = gz / p; if (cc >= tp.n[2]) cc = tp.n[2] - 1;
+      const int aa = gz - cc * p;
+      if (aa == 0 && cc > 0) { czv[nz] = cc - 1; azv[nz] = p; ++nz; }
+      czv[nz] = cc; azv[nz] = aa; ++nz;
+    }
+    const long long rbase = (long long)row * Lx;
+    for (int gx = lane; gx < Lx; gx += 32) {
+      const long long g = rbase + gx;
+      if (rcons || tri_cons(gx, tp.n[0] * p, tp.gamma_d, 0)) { out[g] = 0.0; continue; }
+      const double fv = f ? f[g] : 0.0;
+      if (!rskel && gx % p != 0) { out[g] = fv + out[g]; continue; }   // cell interior
+      int cxv[2], axv[2], nx = 0;
+      int cc = gx / p; if (cc >= tp.n[0]) cc = tp.n[0] - 1;
+      const int aa = gx - cc * p;
+      if (aa == 0 && cc > 0) { cxv[nx] = cc - 1; axv[nx] = p; ++nx; }
+      cxv[nx] = cc; axv[nx] = aa; ++nx;
+      double s = 0.0;
+      for (int kz = 0; kz < nz; ++kz)
+        for (int ky = 0; ky < ny; ++ky)
+          for (int kx = 0; kx < nx; ++kx) {
+            const int cell = (czv[kz] * tp.n[1] + cyv[ky]) * tp.n[0] + cxv[kx];
+            s += cellbuf[(size_t)cell * n3 + (azv[kz] * P1 + ayv[ky]) * P1 + axv[kx]];
+          }
+      out[g] = fv + sign * s;
+    }
   }
-  int c[3][2], a[3][2], nc[3];
-  const long long gg[3] = {gx, gy, gz};
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int i = (int)gg[d];
-    int cc = i / p;
-    if (cc >= tp.n[d]) cc = tp.n[d] - 1;
-    const int aa = i - cc * p;
-    nc[d] = 0;
-    if (aa == 0 && cc > 0) { c[d][nc[d]] = cc - 1; a[d][nc[d]] = p; ++nc[d]; }
-    c[d][nc[d]] = cc; a[d][nc[d]] = aa; ++nc[d];
-  }
-  double s = 0.0;
-  for (int kz = 0; kz < nc[2]; ++kz)
-    for (int ky = 0; ky < nc[1]; ++ky)
-      for (int kx = 0; kx < nc[0]; ++kx) {
-        const long long cell = ((long long)c[2][kz] * tp.n[1] + c[1][ky]) * tp.n[0] + c[0][kx];
-        s += cellbuf[cell * P1 * P1 * P1 + (a[2][kz] * P1 + a[1][ky]) * P1 + a[0][kx]];
-      }
-  out[g] = (f ? f[g] : 0.0) + sign * s;
+  (void)Lz;
 }
 
 cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, const double* X, const double* alpha,
                                    const double* beta, int coef_const, const double* u, const double* f, double* out,
-                                   double sign, double* cellbuf, cudaStream_t st, int* nlaunch) {
+                                   double sign, double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(apply_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
@@ -469,8 +499,11 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
     if (nsm <= 0) nsm = 148;
   }
   const unsigned grid = (unsigned)std::min<long long>(ncell, nsm);   // persistent: one CTA per SM
-  apply_tri_kernel<<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, cellbuf);
-  tri_gather_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(tp, cellbuf, f, out, sign);
+  if (kt) kt->begin(kt->arg);
+  apply_tri_kernel<<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, f, out, sign, cellbuf);
+  if (kt) kt->end(kt->arg);
+  tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
+  (void)nd;
   if (nlaunch) *nlaunch += 2;
   return cudaGetLastError();
 }

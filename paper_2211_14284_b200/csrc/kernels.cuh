@@ -65,9 +65,18 @@ struct TriParams {
   long long Lx, Ly, Lz;
   unsigned gamma_d;
 };
+// optional hooks around a launcher's main kernel (the ABI records CUDA events there for the
+// per-kernel timing phases of rm_timing_read)
+struct KTimer {
+  void (*begin)(void*);
+  void (*end)(void*);
+  void* arg;
+};
+
 cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, const double* X, const double* alpha,
                                    const double* beta, int coef_const, const double* u, const double* f, double* out,
-                                   double sign, double* cellbuf, cudaStream_t st, int* nlaunch);
+                                   double sign, double* cellbuf, cudaStream_t st, int* nlaunch,
+                                   const KTimer* kt = nullptr);
 // doubles of the per-cell result buffer the trilinear apply needs (apply_tri.cu)
 size_t tri_cellbuf_doubles(const TriParams& tp);
 // out = f (or 0) with constrained entries zeroed (apply.cu)
@@ -76,7 +85,7 @@ cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, 
 // launchers (kernels.cu)
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
-                                   long long ndof, cudaStream_t st, int* nlaunch);
+                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt = nullptr);
 // Padded component layout of the patch kernel's input r and correction c: x rows padded to an
 // even length so that TMA tensor maps (row strides multiple of 16 bytes) can address them.
 struct PadLayout {
@@ -119,6 +128,7 @@ struct PatchLaunch {
   const double* sc_dinv;
   const double* sc_c;
   const int* sc_nk;
+  double* sc_fb;         // per-cell face line sums of the pre step [ncell][6][(p-1)^2]
   int sc_p, sc_n[3];
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)
@@ -139,7 +149,8 @@ struct PatchLaunch {
   unsigned long long* prof;   // RM_PROFILE=1 instrumentation counters (else null)
 };
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
-cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st);
+cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
+                               const KTimer* kt = nullptr);
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;

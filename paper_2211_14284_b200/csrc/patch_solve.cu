@@ -725,43 +725,67 @@ __device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long l
   return (z * G.ly + y) * G.lxp + x;
 }
 
-__global__ void sc_pre_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
-                              const double* __restrict__ cc, double* __restrict__ rp, long long nface) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+// ICC-SC pre step, part 1 (one CTA per cell K): y_I = P_II^{-1} r_I, then per face f of K the
+// line sums e_f(j, k) = sum_i (P_GI)_{f, I(i, j, k)} y_I into the per-cell face buffer fb.
+// Every global array is read contiguously (couplings per (K, f) are stored I-contiguous).
+__global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
+                               const double* __restrict__ cc, const double* __restrict__ rp,
+                               double* __restrict__ fb) {
+  extern __shared__ double scs[];
+  const int p = G.p, pm = p - 1, ni = pm * pm * pm, nf = pm * pm;
+  double* y = scs;          // [k][j][i]
+  const int K = blockIdx.x;
+  const int cx = K % G.n[0], cy = (K / G.n[0]) % G.n[1], cz = K / (G.n[0] * G.n[1]);
+  const double* dk = dinv + (size_t)K * ni;
+  for (int I = threadIdx.x; I < ni; I += blockDim.x) {
+    const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / nf + 1;
+    y[I] = dk[I] * rp[sc_idx(G, (long long)cx * p + i, (long long)cy * p + j, (long long)cz * p + k)];
+  }
+  __syncthreads();
+  // one thread per (face, line): the line through face position (a, b) along the face normal
+  for (int q = threadIdx.x; q < 6 * nf; q += blockDim.x) {
+    const int f = q / nf, pos = q - f * nf, dir = f >> 1;
+    const int a = pos % pm, b = pos / pm;
+    const double* cf = cc + ((size_t)K * 6 + f) * ni;
+    const int I0 = dir == 0 ? (b * pm + a) * pm : (dir == 1 ? b * pm * pm + a : b * pm + a);
+    const int st = dir == 0 ? 1 : (dir == 1 ? pm : nf);
+    double e = 0.0;
+    for (int l = 0; l < pm; ++l) e = fma(cf[I0 + l * st], y[I0 + l * st], e);
+    fb[((size_t)K * 6 + f) * nf + pos] = e;
+  }
+}
+
+// ICC-SC pre step, part 2 (one thread per face-interior DoF): r_G -= the line sums of the
+// (<= 2) cells sharing the face, lower cell first (fixed order: deterministic)
+__global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ fb,
+                               double* __restrict__ rp, int nface) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nface) return;
-  const int p = G.p, pm = p - 1, ni = pm * pm * pm;
-  // face DoF t: direction dir, plane index P in 0..n_dir, the two other cells and in-face indices
-  const long long per_dir_x = (long long)(G.n[0] + 1) * G.n[1] * G.n[2] * pm * pm;
-  const long long per_dir_y = (long long)(G.n[1] + 1) * G.n[0] * G.n[2] * pm * pm;
-  int dir;
-  long long r = t;
-  if (r < per_dir_x) dir = 0;
-  else if ((r -= per_dir_x) < per_dir_y) dir = 1;
-  else { r -= per_dir_y; dir = 2; }
+  const int p = G.p, pm = p - 1, nf = pm * pm;
+  const int per_x = (G.n[0] + 1) * G.n[1] * G.n[2] * nf, per_y = (G.n[1] + 1) * G.n[0] * G.n[2] * nf;
+  int dir, r = t;
+  if (r < per_x) dir = 0;
+  else if ((r -= per_x) < per_y) dir = 1;
+  else { r -= per_y; dir = 2; }
   const int d1 = dir == 0 ? 1 : 0, d2 = dir == 2 ? 1 : 2;   // in-face directions (ascending)
-  const int j = (int)(r % pm) + 1;  r /= pm;                 // along d1
-  const int k = (int)(r % pm) + 1;  r /= pm;                 // along d2
-  const int c1 = (int)(r % G.n[d1]); r /= G.n[d1];
-  const int c2 = (int)(r % G.n[d2]); r /= G.n[d2];
-  const int P = (int)r;                                       // plane 0..n_dir
-  long long g[3];
-  g[dir] = (long long)P * p; g[d1] = (long long)c1 * p + j; g[d2] = (long long)c2 * p + k;
+  const int a = r % pm;  r /= pm;                           // along d1 (0-based)
+  const int b = r % pm;  r /= pm;                           // along d2
+  const int c1 = r % G.n[d1]; r /= G.n[d1];
+  const int c2 = r % G.n[d2]; r /= G.n[d2];
+  const int P = r;                                          // plane 0..n_dir
+  int cell[3], g[3];
+  cell[d1] = c1; cell[d2] = c2;
+  g[dir] = P * p; g[d1] = c1 * p + a + 1; g[d2] = c2 * p + b + 1;
   double e = 0.0;
-  for (int side = 0; side < 2; ++side) {   // cell below (face +) and above (face -) the plane
-    const int cd = side == 0 ? P - 1 : P;
-    if (cd < 0 || cd >= G.n[dir]) continue;
-    int cell[3];
-    cell[dir] = cd; cell[d1] = c1; cell[d2] = c2;
-    const long long K = ((long long)cell[2] * G.n[1] + cell[1]) * G.n[0] + cell[0];
-    const int face = 2 * dir + (side == 0 ? 1 : 0);
-    for (int i = 1; i < p; ++i) {
-      int loc[3];
-      loc[dir] = i; loc[d1] = j; loc[d2] = k;
-      const int I = ((loc[2] - 1) * pm + (loc[1] - 1)) * pm + (loc[0] - 1);
-      const double y = rp[sc_idx(G, (long long)cell[0] * p + loc[0], (long long)cell[1] * p + loc[1], (long long)cell[2] * p + loc[2])] *
-                       dinv[K * ni + I];
-      e = fma(cc[(K * 6 + face) * ni + I], y, e);
-    }
+  if (P > 0) {          // cell below: its + face
+    cell[dir] = P - 1;
+    const int K = (cell[2] * G.n[1] + cell[1]) * G.n[0] + cell[0];
+    e += fb[((size_t)K * 6 + 2 * dir + 1) * nf + b * pm + a];
+  }
+  if (P < G.n[dir]) {   // cell above: its - face
+    cell[dir] = P;
+    const int K = (cell[2] * G.n[1] + cell[1]) * G.n[0] + cell[0];
+    e += fb[((size_t)K * 6 + 2 * dir) * nf + b * pm + a];
   }
   rp[sc_idx(G, g[0], g[1], g[2])] -= e;
 }
@@ -878,7 +902,8 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   return cudaSuccess;
 }
 
-cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st) {
+cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
+                               const KTimer* kt) {
   if (L.npatch <= 0) return cudaSuccess;
   const long long n = L.pad.off[L.pad.ncomp];
   cudaError_t e;
@@ -896,7 +921,17 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
              (long long)(sg.n[2] + 1) * sg.n[0] * sg.n[1]) * pm * pm;
     nint = (long long)sg.n[0] * sg.n[1] * sg.n[2] * pm * pm * pm;
     if (nface > 0) {
-      sc_pre_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.rpad, nface);
+      const int ncell = sg.n[0] * sg.n[1] * sg.n[2];
+      const size_t smem = sizeof(double) * (size_t)(pm * pm * pm);
+      static size_t smem_set = 0;
+      if (smem > 48 * 1024 && smem > smem_set) {
+        if ((e = cudaFuncSetAttribute(sc_cell_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+          return e;
+        smem_set = smem;
+      }
+      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.rpad, L.sc_fb);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      sc_face_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_fb, L.rpad, (int)nface);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
   }
@@ -914,10 +949,12 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     bg.boff[m] = L.boff[m];
     if (m < L.nsub) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
   }
+  if (kt) kt->begin(kt->arg);
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
       L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
       (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof,
       getenv("RM_DEBUG_Q") ? atoi(getenv("RM_DEBUG_Q")) : -1, dbg_buf(L.box_total));
+  if (kt) kt->end(kt->arg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
