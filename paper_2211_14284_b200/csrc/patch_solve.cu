@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   // ================================================================== sparse warps
   Consumer cn{chan_sm(smraw, 0), ringA, 0, 0, nullptr, nullptr};
   unsigned long long sp_box = 0, sp_x = 0, sp_fwd = 0, sp_bwd = 0, sp0 = prof ? clock64() : 0;
+  unsigned long long sp_icc_acq = 0, sp_icc_sync = 0;
   const bool pf = prof != nullptr && tid == 0;
   auto forward = [&](int i) {
     const int q = (int)blockIdx.x + i * G;
@@ -618,37 +619,41 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
         for (int l = 0; l < nl; ++l) {
           const int pe = lp[l + 1];
           for (int pi = lp[l]; pi < pe; ++pi) {
+            const unsigned long long tq0 = pf ? clock64() : 0;
             const Piece_ pc = cn.acquire();
+            if (pf) sp_icc_acq += clock64() - tq0;
+            // lane-interleaved piece (patches.cpp): <= 32 rows, one per lane; the level's pieces
+            // are dealt round-robin to the sparse warps (every warp walks the ring cursor)
             const Hdr h = hdr(pc.pb);
-            const int cnt = h.a1 - h.a0;
-            const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
-            const uint16_t* st = rows + cnt;
-            const uint16_t* cols = st + cnt + 1;
-            const double* val = pc.val;
-            if (dbg_out && dbg_q == 3 && tid == 0) {   // debug: ICC piece record (experiments only)
-              double* d = dbg_out + (size_t)q * (box_total + 9);
-              const int j = (int)d[9];
-              if (j < 14) {
-                double* e = d + 10 + 8 * j;
-                e[0] = pass; e[1] = l; e[2] = cnt; e[3] = rows[0]; e[4] = st[1]; e[5] = cols[0]; e[6] = val[0]; e[7] = v[rows[0]];
+            const int cnt = h.a1 - h.a0, Lm = h.e0;
+            if ((pi - lp[l]) % NC == warp && lane < cnt) {
+              const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
+              const uint16_t* cols = rows + 32 + lane;
+              const double* off = pc.val + 32 + lane;
+              const int a = rows[lane];
+              double s0 = v[a], s1 = 0.0;
+              int j = 0;
+              for (; j + 3 < Lm; j += 4) {   // step j of this row: conflict-free value / column loads
+                const int c0 = cols[32 * j], c1 = cols[32 * j + 32], c2 = cols[32 * j + 64], c3 = cols[32 * j + 96];
+                const double w0 = off[32 * j], w1 = off[32 * j + 32], w2 = off[32 * j + 64], w3 = off[32 * j + 96];
+                const double x0 = v[c0], x1 = v[c1], x2 = v[c2], x3 = v[c3];
+                s0 = fma(-w0, x0, s0);
+                s1 = fma(-w1, x1, s1);
+                s0 = fma(-w2, x2, s0);
+                s1 = fma(-w3, x3, s1);
               }
-              d[9] = j + 1;
-              for (int k = 0; k < 9; ++k) d[k] = (double)porig[9 * q + k];
-            }
-            for (int k = tid; k < cnt; k += NT) {
-              const int a = rows[k], t0 = st[k], t1 = st[k + 1];
-              double s = v[a];
-              if (pass == 0) {
-                for (int t = t0; t < t1 - 1; ++t) s -= val[t] * v[cols[t]];
-                v[a] = s * val[t1 - 1];
-              } else {
-                for (int t = t0 + 1; t < t1; ++t) s -= val[t] * v[cols[t]];
-                v[a] = s * val[t0];
+              for (; j < Lm; ++j) {
+                const double x = v[cols[32 * j]];
+                if (j & 1) s1 = fma(-off[32 * j], x, s1);
+                else s0 = fma(-off[32 * j], x, s0);
               }
+              v[a] = (s0 + s1) * pc.val[lane];
             }
             cn.release(lane);
           }
+          const unsigned long long tq1 = pf ? clock64() : 0;
           csync();
+          if (pf) sp_icc_sync += clock64() - tq1;
         }
       }
     }
@@ -689,6 +694,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   if (pf) {
     unsigned long long* o = prof + 24 * blockIdx.x;
     o[7] = clock64() - sp0; o[8] = sp_box; o[9] = sp_x; o[10] = sp_fwd; o[11] = sp_bwd;
+    o[16] = sp_icc_acq; o[17] = sp_icc_sync;
   }
 }
 
@@ -966,8 +972,8 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     fprintf(stderr,
             "[rm prof kcyc] producer total %.0f idle %.0f | store total %.0f wait-done %.0f colour %.0f | tiles total %.0f "
             "wait-fwd %.0f | sparse total %.0f box-wait %.0f x-wait %.0f fwd %.0f bwd %.0f | prodA total %.0f room-wait %.0f "
-            "| prodB total %.0f room-wait %.0f\n",
-            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15]);
+            "| prodB total %.0f room-wait %.0f | icc acquire-wait %.0f level-sync %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15], a[16], a[17]);
   }
   if (L.sc_dinv && nint > 0 && !getenv("RM_DEBUG_SC_NOPOST")) {
     sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);

@@ -158,7 +158,10 @@ void build_blocks(Blocks& B, const std::vector<std::vector<int>>& blocks) {
 void add_piece(ClassProgram& C, int64_t& s, Piece p) {
   if (p.nd <= 0 && p.kind != PK_FINAL && p.kind != PK_ZERO) return;
   p.nd = (p.nd + 1) & ~1;
-  if (p.nd > kPieceMax) throw std::runtime_error("stream piece larger than kPieceMax");
+  // lane-interleaved ICC pieces are padded to 32 x (longest row): up to 4 x kPieceMax (the
+  // header fields are 16-bit; units and rings are sized from the actual units)
+  if (p.nd > ((p.kind == PK_ICCF || p.kind == PK_ICCB) ? 4 * kPieceMax : kPieceMax))
+    throw std::runtime_error("stream piece larger than kPieceMax");
   p.sofs = (int)s;
   s += p.nd;
   C.pieces.push_back(p);
@@ -237,14 +240,12 @@ void build_meta(ClassProgram& C) {
         for (int z : C.zlist) put16(z);
         break;
       case PK_ICCF:
-      case PK_ICCB: {  // uint16 row boxes, uint16 value starts (cnt + 1), uint16 column boxes
+      case PK_ICCB: {  // 32 uint16 row boxes, then the interleaved column boxes (pads: box 0)
         const bool f = p.kind == PK_ICCF;
         const std::vector<int>& row = f ? C.iccf_row : C.iccb_row;
-        const std::vector<int>& rp = f ? C.iccf_rp : C.iccb_rp;
         const std::vector<int>& col = f ? C.iccf_col : C.iccb_col;
-        for (int q = p.a0; q < p.a1; ++q) put16(C.bidx[f0 + row[q]]);
-        for (int q = p.a0; q <= p.a1; ++q) put16(rp[q] - p.e0);
-        for (int t = rp[p.a0]; t < rp[p.a1]; ++t) put16(C.bidx[f0 + col[t]]);
+        for (int k = 0; k < 32; ++k) put16(k < p.a1 - p.a0 ? C.bidx[f0 + row[p.a0 + k]] : 0);
+        for (int k = 32; k < p.nd; ++k) put16(col[p.cofs + k] < 0 ? 0 : C.bidx[f0 + col[p.cofs + k]]);
         break;
       }
       default:
@@ -327,58 +328,54 @@ void build_stream(ClassProgram& C) {
         add_piece(C, s, Piece{PK_TILE, 0, I, J, 0, 0, I == J ? kTileDiag : 1024,
                               (int)C.vofs_final + (I * (I + 1) / 2 + J) * 1024});
   } else {
-    // level-ordered CSR copies (forward rows of L diag last, backward rows of L^T diag first)
+    // ICC pieces, LANE-INTERLEAVED: the rows of a level, sorted by length (longest first), in
+    // chunks of <= 32 (one row per lane of the warp that takes the piece); values = the 32
+    // inverted diagonals, then step j of every row at [32 + 32 j + lane] (zero padded to the
+    // chunk's longest row); meta = 32 row boxes, then the column boxes in the same interleaved
+    // order.  Forward: rows of L (diagonal last in the CSR); backward: rows of L^T (first).
     const int nnz = C.icc_rowptr.empty() ? 0 : C.icc_rowptr[m];
-    C.iccf_row.clear(); C.iccf_rp.assign(1, 0); C.iccf_col.clear(); C.iccf_src.clear(); C.iccf_lpiece.clear();
-    const int nlf = (int)C.icc_level_ptr.size() - 1;
-    for (int l = 0; l < nlf; ++l) {
-      C.iccf_lpiece.push_back((int)C.pieces.size());
-      int q = C.icc_level_ptr[l];
-      const int qe = C.icc_level_ptr[l + 1];
-      while (q < qe) {
-        const int q0 = q;
-        const int v0 = C.iccf_rp[q];
-        while (q < qe) {
-          const int a = C.icc_level_rows[q];
-          const int len = C.icc_rowptr[a + 1] - C.icc_rowptr[a];
-          if (len > kPieceMax) throw std::runtime_error("ICC row longer than kPieceMax");
-          if (C.iccf_rp[q] + len - v0 > kPieceMax) break;
-          C.iccf_row.push_back(a);
-          for (int t = C.icc_rowptr[a]; t < C.icc_rowptr[a + 1]; ++t) { C.iccf_col.push_back(C.icc_col[t]); C.iccf_src.push_back(t); }
-          C.iccf_rp.push_back(C.iccf_rp.back() + len);
-          ++q;
-        }
-        // values are addressed by their level-ordered index t, at o[t - v0] inside the piece
-        add_piece(C, s, Piece{PK_ICCF, l, q0, q, v0, 0, C.iccf_rp[q] - v0, -1});
-      }
-    }
-    C.iccf_lpiece.push_back((int)C.pieces.size());
-    C.iccb_row.clear(); C.iccb_rp.assign(1, 0); C.iccb_col.clear(); C.iccb_src.clear(); C.iccb_lpiece.clear();
-    const int nlb = (int)C.icct_level_ptr.size() - 1;
-    for (int l = 0; l < nlb; ++l) {
-      C.iccb_lpiece.push_back((int)C.pieces.size());
-      int q = C.icct_level_ptr[l];
-      const int qe = C.icct_level_ptr[l + 1];
-      while (q < qe) {
-        const int q0 = q;
-        const int v0 = C.iccb_rp[q];
-        while (q < qe) {
-          const int b = C.icct_level_rows[q];
-          const int len = C.icct_rowptr[b + 1] - C.icct_rowptr[b];
-          if (len > kPieceMax) throw std::runtime_error("ICC row longer than kPieceMax");
-          if (C.iccb_rp[q] + len - v0 > kPieceMax) break;
-          C.iccb_row.push_back(b);
-          for (int t = C.icct_rowptr[b]; t < C.icct_rowptr[b + 1]; ++t) {
-            C.iccb_col.push_back(C.icct_col[t]);
-            C.iccb_src.push_back(nnz + t);
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<int>& rowv = pass == 0 ? C.iccf_row : C.iccb_row;
+      std::vector<int>& slot = pass == 0 ? C.iccf_src : C.iccb_src;   // per piece value slot -> canonical (-1: 0)
+      std::vector<int>& colv = pass == 0 ? C.iccf_col : C.iccb_col;   // per piece value slot -> column (-1: pad)
+      std::vector<int>& lpiece = pass == 0 ? C.iccf_lpiece : C.iccb_lpiece;
+      const std::vector<int>& lptr = pass == 0 ? C.icc_level_ptr : C.icct_level_ptr;
+      const std::vector<int>& lrows = pass == 0 ? C.icc_level_rows : C.icct_level_rows;
+      const std::vector<int>& rp = pass == 0 ? C.icc_rowptr : C.icct_rowptr;
+      const std::vector<int>& cl = pass == 0 ? C.icc_col : C.icct_col;
+      rowv.clear(); slot.clear(); colv.clear(); lpiece.clear();
+      C.iccf_rp.clear(); C.iccb_rp.clear();
+      const int nl = (int)lptr.size() - 1;
+      for (int l = 0; l < nl; ++l) {
+        lpiece.push_back((int)C.pieces.size());
+        std::vector<int> lr(lrows.begin() + lptr[l], lrows.begin() + lptr[l + 1]);
+        std::stable_sort(lr.begin(), lr.end(), [&](int x, int y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
+        for (size_t c0 = 0; c0 < lr.size(); c0 += kIccRows) {
+          const int cnt = (int)std::min<size_t>(kIccRows, lr.size() - c0);
+          int Lmax = 0;
+          for (int k = 0; k < cnt; ++k) Lmax = std::max(Lmax, rp[lr[c0 + k] + 1] - rp[lr[c0 + k]] - 1);
+          const int nd = 32 + 32 * Lmax;
+          if (nd > 4 * kPieceMax) throw std::runtime_error("ICC row too long for a piece");
+          const int a0 = (int)rowv.size(), sofs = (int)slot.size();
+          slot.resize(sofs + nd, -1);
+          colv.resize(sofs + nd, -1);
+          for (int k = 0; k < cnt; ++k) {
+            const int a = lr[c0 + k];
+            rowv.push_back(a);
+            const int d = pass == 0 ? rp[a + 1] - 1 : rp[a];         // diagonal entry (stored inverted)
+            const int o0 = pass == 0 ? rp[a] : rp[a] + 1;            // off-diagonal entries, CSR order
+            slot[sofs + k] = (pass == 0 ? 0 : nnz) + d;   // canonical: L values, then L^T values (CSR of L^T)
+            for (int j = 0; o0 + j < (pass == 0 ? rp[a + 1] - 1 : rp[a + 1]); ++j) {
+              const int t = o0 + j;
+              slot[sofs + 32 + 32 * j + k] = (pass == 0 ? 0 : nnz) + t;
+              colv[sofs + 32 + 32 * j + k] = cl[t];
+            }
           }
-          C.iccb_rp.push_back(C.iccb_rp.back() + len);
-          ++q;
+          add_piece(C, s, Piece{pass == 0 ? PK_ICCF : PK_ICCB, l, a0, a0 + cnt, Lmax, 0, nd, sofs});
         }
-        add_piece(C, s, Piece{PK_ICCB, l, q0, q, v0, 0, C.iccb_rp[q] - v0, -1});
       }
+      lpiece.push_back((int)C.pieces.size());
     }
-    C.iccb_lpiece.push_back((int)C.pieces.size());
   }
   C.tile_p1 = (int)C.pieces.size();
   for (int l = L - 1; l >= 0; --l) {
@@ -417,11 +414,14 @@ void pack_stream(const ClassProgram& C, const double* canon, double* out) {
           }
         break;
       case PK_ICCF:
-        for (int t = C.iccf_rp[p.a0]; t < C.iccf_rp[p.a1]; ++t) o[t - p.e0] = canon[C.vofs_final + C.iccf_src[t]];
+      case PK_ICCB: {   // lane-interleaved slots (p.cofs = first slot of the piece)
+        const std::vector<int>& slot = p.kind == PK_ICCF ? C.iccf_src : C.iccb_src;
+        for (int k = 0; k < p.nd; ++k) {
+          const int src = slot[p.cofs + k];
+          o[k] = src < 0 ? 0.0 : canon[C.vofs_final + src];
+        }
         break;
-      case PK_ICCB:
-        for (int t = C.iccb_rp[p.a0]; t < C.iccb_rp[p.a1]; ++t) o[t - p.e0] = canon[C.vofs_final + C.iccb_src[t]];
-        break;
+      }
       default:   // metadata-only pieces (FINAL, ZERO)
         break;
     }

@@ -65,6 +65,7 @@ enum FinalKind { FINAL_DENSE_INV = 0, FINAL_ICC = 1 };
 // units form their own channel, consumed by the tile warps only)
 enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_FINAL = 6, PK_ZERO = 7 };
 constexpr int kPieceMax = 2048;      // doubles (16 KB) of values per piece
+constexpr int kIccRows = 32;      // rows per ICC piece: one row per lane of the warp that takes it
 constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
 // Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
 // owns rows 4a..4a+3 and columns 8b..8b+7; step k (0..15) holds its elements (row 4a + k/4,
@@ -85,7 +86,7 @@ inline int tile_pos_diag(int r, int c) {   // c <= r
 struct Piece {
   int kind, lev;
   int a0, a1;     // PIV: blocks; W/WT: slices; TILE: I, J; ICC: level-ordered rows; GATHER: positions
-  int e0;         // W/WT: first element of the sliced array; ICC: first value
+  int e0;         // W/WT: first element of the sliced array; ICC: longest off-diagonal row (L)
   int sofs;       // stream offset (doubles) inside the patch value block
   int nd;         // doubles (even)
   int cofs;       // source offset inside the canonical block (host packing only)

@@ -188,22 +188,20 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
           for (int i = 0; i < m; ++i) v[fb[i]] = x[i];
         }
       } else {
-        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {
+        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {   // lane-interleaved ICC pieces
           PieceView w = view(pi);
-          const int cnt = w.a1 - w.a0;
+          const int cnt = w.a1 - w.a0, Lm = C.pieces[pi].e0;
           const uint8_t* rows = w.pb + 16;
-          const uint8_t* st = rows + 2 * cnt;
-          const uint8_t* cols = st + 2 * (cnt + 1);
-          for (int k = 0; k < cnt; ++k) {
-            const int a = rd<uint16_t>(rows, k), t0 = rd<uint16_t>(st, k), t1 = rd<uint16_t>(st, k + 1);
-            double s = v[a];
-            if (C.pieces[pi].kind == PK_ICCF) {
-              for (int tt = t0; tt < t1 - 1; ++tt) s -= w.val[tt] * v[rd<uint16_t>(cols, tt)];
-              v[a] = s * w.val[t1 - 1];
-            } else {
-              for (int tt = t0 + 1; tt < t1; ++tt) s -= w.val[tt] * v[rd<uint16_t>(cols, tt)];
-              v[a] = s * w.val[t0];
+          const uint8_t* cols = rows + 64;
+          for (int k = 0; k < cnt; ++k) {   // same arithmetic order as the kernel
+            const int a = rd<uint16_t>(rows, k);
+            double s0 = v[a], s1 = 0.0;
+            for (int j = 0; j < Lm; ++j) {
+              const double x = v[rd<uint16_t>(cols, 32 * j + k)], wv = w.val[32 + 32 * j + k];
+              if (j & 1) s1 = std::fma(-wv, x, s1);
+              else s0 = std::fma(-wv, x, s0);
             }
+            v[a] = (s0 + s1) * w.val[k];
           }
         }
       }

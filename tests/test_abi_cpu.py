@@ -95,6 +95,7 @@ CASES = [
     ("cfg4-face-2^3p3", ri.CONFIGS[4].with_mesh(2).with_p(3), 2, 0, 0),
     ("cfg3-vertex-2^3p3", ri.CONFIGS[3].with_mesh(2).with_p(3), 0, 0, 0),
     ("cfg5-icc-2^3p3", ri.CONFIGS[5].with_mesh(2).with_p(3), 0, 1, 0),
+    ("cfg5-icc-3^3p5", ri.CONFIGS[5].with_mesh(3).with_p(5), 0, 1, 0),   # levels wider than one 32-row piece
 ]
 
 
