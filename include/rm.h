@@ -96,6 +96,31 @@ typedef struct {
 
 void rm_default_options(rm_options *opt);
 
+/* Z-SLAB PARTITION (multi-GPU, H(grad) vertex stars only).  Rank g of G owns
+ * the cell layers [mesh.z_begin, mesh.z_end) (contiguous slabs, rank order = z order), the DoF
+ * planes z_begin*p .. z_end*p - 1 (the last rank also the top plane nz*p) and the vertex-star
+ * patches of the vertex layers z_begin .. z_end - 1 (+ nz on the last rank).  Its LOCAL problem
+ * is its slab plus one ghost cell layer below (rank > 0) and the shared plane above, so local
+ * vectors hold planes z_cell0*p .. (z_cell0 + nz_local)*p.  Per sweep the neighbours exchange,
+ * forward: u (and f) on the p planes below the slab and the shared plane above; reverse: the
+ * patch corrections on the p - 1 planes below the slab, ADDED by their owner.  All plane ranges
+ * below are LOCAL plane indices [first, last + 1); a plane is plane_len contiguous doubles.
+ * Pure host arithmetic (no device needed). */
+typedef struct {
+  int32_t z_cell0, nz_local, ghost_lo;   /* global layer of local cell 0; local cell layers; 0|1 */
+  int32_t v_lo, v_hi;                    /* owned vertex layers (local) = owned patches          */
+  int32_t own_lo, own_hi;                /* owned DoF planes                                      */
+  int32_t fwd_recv_lo[2], fwd_send_lo[2];   /* forward exchange with rank - 1 (u, f)            */
+  int32_t fwd_recv_hi[2], fwd_send_hi[2];   /* forward exchange with rank + 1                    */
+  int32_t rev_send_lo[2], rev_recv_hi[2];   /* reverse-add: corrections to rank - 1 / from + 1  */
+  uint32_t gamma_local;                  /* Gamma_D bits of the local problem (cut planes free)  */
+  int64_t plane_len;                     /* doubles per DoF plane: (nx p + 1)(ny p + 1)          */
+} rm_partition_info;
+rm_status rm_partition(const rm_mesh *mesh, int32_t p, rm_space space, uint32_t gamma_d, int32_t rank,
+                       int32_t nranks, rm_partition_info *info);
+/* 128-byte ncclUniqueId for options.nccl_id (rank 0 creates it, the caller broadcasts it). */
+rm_status rm_nccl_unique_id(void *id128);
+
 /* Builds the 1D FDM tables, the structured layout, all patch factors and uploads them.
  * alpha, beta: host arrays, n == 1 (constant) or one value per cell, C-order [z][y][x]. */
 rm_status rm_setup(rm_ctx **ctx, const rm_mesh *mesh, int32_t p, rm_space space,
@@ -114,6 +139,14 @@ rm_status rm_residual(rm_ctx *ctx, const double *f, const double *u, double *r);
 rm_status rm_relax(rm_ctx *ctx, const double *f, const double *u_in, double *u_out, double omega);
 /* z = P^{-1} r  (the additive Schwarz preconditioner = one sweep from zero with omega = 1). */
 rm_status rm_precondition(rm_ctx *ctx, const double *r, double *z);
+/* Multi-rank sweep in two stages, for callers that move the halos themselves (and the
+ * single-GPU partition tests): rm_relax_begin reads f and u_in on every local plane (the caller
+ * filled the forward halos) and writes the local patch correction c (all local planes, nonzero
+ * on the ghost planes too); the caller reverse-adds the rev_* planes of c between its ranks;
+ * rm_relax_end writes u_out = u_in + omega c.  With options.nccl_id set, rm_relax does all of
+ * this itself over NCCL on the context's stream. */
+rm_status rm_relax_begin(rm_ctx *ctx, const double *f, const double *u_in, double *c);
+rm_status rm_relax_end(rm_ctx *ctx, const double *u_in, const double *c, double *u_out, double omega);
 /* Same as rm_relax with HOST buffers: copies f, u_in to the device, sweeps, copies u_out back,
  * synchronises. */
 rm_status rm_relax_host(rm_ctx *ctx, const double *f, const double *u_in, double *u_out, double omega);

@@ -48,6 +48,22 @@ class rm_options(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32)]
 
 
+class rm_partition_info(ctypes.Structure):
+    _fields_ = [("z_cell0", ctypes.c_int32), ("nz_local", ctypes.c_int32), ("ghost_lo", ctypes.c_int32),
+                ("v_lo", ctypes.c_int32), ("v_hi", ctypes.c_int32), ("own_lo", ctypes.c_int32),
+                ("own_hi", ctypes.c_int32), ("fwd_recv_lo", ctypes.c_int32 * 2), ("fwd_send_lo", ctypes.c_int32 * 2),
+                ("fwd_recv_hi", ctypes.c_int32 * 2), ("fwd_send_hi", ctypes.c_int32 * 2),
+                ("rev_send_lo", ctypes.c_int32 * 2), ("rev_recv_hi", ctypes.c_int32 * 2),
+                ("gamma_local", ctypes.c_uint32), ("plane_len", ctypes.c_int64)]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = tuple(v) if hasattr(v, "__len__") else v
+        return d
+
+
 class rm_info(ctypes.Structure):
     _fields_ = [("n_local", ctypes.c_int64), ("n_free", ctypes.c_int64), ("n_patches", ctypes.c_int64),
                 ("n_patches_potential", ctypes.c_int64), ("n_factor_blocks", ctypes.c_int64),
@@ -73,6 +89,10 @@ def _load():
     lib.rm_relax.argtypes = [P, P, P, P, D]
     lib.rm_precondition.argtypes = [P, P, P]
     lib.rm_relax_host.argtypes = [P, P, P, P, D]
+    lib.rm_relax_begin.argtypes = [P, P, P, P]
+    lib.rm_relax_end.argtypes = [P, P, P, P, D]
+    lib.rm_partition.argtypes = [ctypes.POINTER(rm_mesh), I32, I32, U32, I32, I32, ctypes.POINTER(rm_partition_info)]
+    lib.rm_nccl_unique_id.argtypes = [P]
     lib.rm_pcg.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]
     lib.rm_timing_enable.argtypes = [P, I32]
     lib.rm_timing_read.argtypes = [P, ctypes.POINTER(D * RM_NPHASE), ctypes.POINTER(I64 * RM_NPHASE)]
@@ -80,7 +100,8 @@ def _load():
     lib.rm_destroy.restype = None
     lib.rm_last_error.restype = ctypes.c_char_p
     for f in ("rm_setup", "rm_layout", "rm_info_get", "rm_constrained_mask", "rm_apply", "rm_residual",
-              "rm_relax", "rm_precondition", "rm_relax_host", "rm_pcg", "rm_timing_enable", "rm_timing_read"):
+              "rm_relax", "rm_precondition", "rm_relax_host", "rm_pcg", "rm_timing_enable", "rm_timing_read",
+              "rm_relax_begin", "rm_relax_end", "rm_partition", "rm_nccl_unique_id"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -147,12 +168,30 @@ def _stream_ptr(stream):
     return int(stream)
 
 
+def rm_partition(nx, ny, nz, p, space, gamma_d, rank, nranks, z_begin, z_end) -> dict:
+    """Z-slab partition of rank `rank` owning cell layers [z_begin, z_end) (include/rm.h):
+    local mesh, owned planes / patches, halo plane ranges.  Host arithmetic only."""
+    mesh = rm_mesh(nx, ny, nz, None, z_begin, z_end)
+    info = rm_partition_info()
+    _check(_lib.rm_partition(ctypes.byref(mesh), p, space, gamma_d, rank, nranks, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def rm_nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it; broadcast it with torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.rm_nccl_unique_id(buf))
+    return buf.raw
+
+
 def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposition=RM_PAFW,
              factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-3, stream=None,
-             device=0) -> RmContext:
+             device=0, rank=0, nranks=1, z_begin=0, z_end=None, nccl_id=None) -> RmContext:
+    """coords / alpha / beta describe the GLOBAL mesh; with nranks > 1 the context holds the local
+    problem of the cell layers [z_begin, z_end) (rm_partition) and its vectors are local."""
     alpha = np.ascontiguousarray(np.atleast_1d(np.asarray(alpha, dtype=np.float64)).ravel())
     beta = np.ascontiguousarray(np.atleast_1d(np.asarray(beta, dtype=np.float64)).ravel())
-    mesh = rm_mesh(nx, ny, nz, None, 0, nz)
+    mesh = rm_mesh(nx, ny, nz, None, z_begin, nz if z_end is None else z_end)
     keep = None
     if coords is not None:
         keep = np.ascontiguousarray(np.asarray(coords, dtype=np.float64))
@@ -168,6 +207,14 @@ def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposit
     sp = _stream_ptr(stream)
     opt.stream = ctypes.c_void_p(sp)
     opt.device = device
+    opt.rank = rank
+    opt.nranks = nranks
+    idbuf = None
+    if nccl_id is not None:
+        if len(nccl_id) != 128:
+            raise ValueError("nccl_id must be 128 bytes")
+        idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        opt.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
     h = ctypes.c_void_p()
     _check(_lib.rm_setup(ctypes.byref(h), ctypes.byref(mesh), p, space,
                          alpha.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), alpha.size,
@@ -185,6 +232,16 @@ def rm_residual(ctx: RmContext, f, u, r):
 
 def rm_relax(ctx: RmContext, f, u_in, u_out, omega=1.0):
     _check(_lib.rm_relax(ctx.h, ctx._vec(f, "f"), ctx._vec(u_in, "u_in"), ctx._vec(u_out, "u_out"), float(omega)))
+
+
+def rm_relax_begin(ctx: RmContext, f, u_in, c):
+    """Multi-rank stage 1 (halos of f, u_in filled by the caller): c = local patch correction."""
+    _check(_lib.rm_relax_begin(ctx.h, ctx._vec(f, "f"), ctx._vec(u_in, "u_in"), ctx._vec(c, "c")))
+
+
+def rm_relax_end(ctx: RmContext, u_in, c, u_out, omega=1.0):
+    """Multi-rank stage 2 (c reverse-added by the caller): u_out = u_in + omega c."""
+    _check(_lib.rm_relax_end(ctx.h, ctx._vec(u_in, "u_in"), ctx._vec(c, "c"), ctx._vec(u_out, "u_out"), float(omega)))
 
 
 def rm_precondition(ctx: RmContext, r, z):

@@ -2,6 +2,8 @@
 #include "../../include/rm.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types and prototypes only: the library is dlopen'ed (rank > 1 only)
 
 #include <chrono>
 #include <cmath>
@@ -33,6 +35,86 @@ struct RmError : std::runtime_error {
     cudaError_t e_ = (x);                                                                      \
     if (e_ != cudaSuccess) throw RmError(RM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// ------------------------------------------------------------------ NCCL (loaded on demand)
+// The process may already hold torch's libnccl.so.2; dlopen returns that one.  No link-time
+// dependency: single-GPU use never touches NCCL.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) gstart = nullptr;
+  decltype(&ncclGroupEnd) gend = nullptr;
+  decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclGetErrorString) errstr = nullptr;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_id = reinterpret_cast<decltype(api.get_id)>(dlsym(h, "ncclGetUniqueId"));
+      api.init = reinterpret_cast<decltype(api.init)>(dlsym(h, "ncclCommInitRank"));
+      api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "ncclCommDestroy"));
+      api.send = reinterpret_cast<decltype(api.send)>(dlsym(h, "ncclSend"));
+      api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(h, "ncclRecv"));
+      api.gstart = reinterpret_cast<decltype(api.gstart)>(dlsym(h, "ncclGroupStart"));
+      api.gend = reinterpret_cast<decltype(api.gend)>(dlsym(h, "ncclGroupEnd"));
+      api.allreduce = reinterpret_cast<decltype(api.allreduce)>(dlsym(h, "ncclAllReduce"));
+      api.errstr = reinterpret_cast<decltype(api.errstr)>(dlsym(h, "ncclGetErrorString"));
+    }
+  }
+  if (!api.init || !api.send || !api.recv || !api.gstart || !api.gend || !api.allreduce || !api.get_id)
+    throw RmError(RM_ENCCL, "libnccl.so.2 not loadable");
+  return api;
+}
+#define NK(x)                                                                                       \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess)                                                                          \
+      throw RmError(RM_ENCCL, std::string(#x) + ": " + (nccl().errstr ? nccl().errstr(r_) : "error")); \
+  } while (0)
+
+// ------------------------------------------------------------------ z-slab partition (rm.h)
+void compute_partition(const rm_mesh& m, int p, int space, uint32_t gamma, int rank, int nranks,
+                       rm_partition_info& P) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw RmError(RM_EINVAL, "bad rank / nranks");
+  if (nranks > 1 && space != 0) throw RmError(RM_EINVAL, "multi-rank slabs: H(grad) only");
+  const int zb = m.z_begin, ze = m.z_end;
+  if (!(0 <= zb && zb < ze && ze <= m.nz)) throw RmError(RM_EINVAL, "bad z_begin / z_end");
+  if (nranks == 1 && (zb != 0 || ze != m.nz)) throw RmError(RM_EINVAL, "one rank must own all layers");
+  if (rank == 0 && zb != 0) throw RmError(RM_EINVAL, "rank 0 must start at layer 0");
+  if (rank == nranks - 1 && ze != m.nz) throw RmError(RM_EINVAL, "the last rank must end at layer nz");
+  std::memset(&P, 0, sizeof P);
+  const bool lo = rank > 0, hi = rank < nranks - 1;
+  P.ghost_lo = lo ? 1 : 0;
+  P.z_cell0 = zb - P.ghost_lo;
+  P.nz_local = ze - P.z_cell0;
+  const int top = P.nz_local * p;   // local index of the upper plane
+  P.v_lo = P.ghost_lo;
+  P.v_hi = hi ? P.nz_local : P.nz_local + 1;
+  P.own_lo = P.ghost_lo * p;
+  P.own_hi = hi ? top : top + 1;
+  if (lo) {
+    P.fwd_recv_lo[0] = 0; P.fwd_recv_lo[1] = p;          // ghost layer planes, owned by rank - 1
+    P.fwd_send_lo[0] = p; P.fwd_send_lo[1] = p + 1;      // my first plane = rank - 1's upper plane
+    P.rev_send_lo[0] = 1; P.rev_send_lo[1] = p;          // corrections on the ghost layer's interior
+  }
+  if (hi) {
+    P.fwd_recv_hi[0] = top; P.fwd_recv_hi[1] = top + 1;  // shared upper plane, owned by rank + 1
+    P.fwd_send_hi[0] = top - p; P.fwd_send_hi[1] = top;  // rank + 1's ghost layer
+    P.rev_recv_hi[0] = top - p + 1; P.rev_recv_hi[1] = top;
+  }
+  P.gamma_local = gamma & 0x0Fu;
+  if (!lo) P.gamma_local |= gamma & 0x10u;
+  if (!hi) P.gamma_local |= gamma & 0x20u;
+  P.plane_len = ((int64_t)m.nx * p + 1) * ((int64_t)m.ny * p + 1);
+}
 
 struct DevFamily {
   std::vector<void*> allocs;
@@ -308,6 +390,12 @@ struct rm_ctx {
   struct Ev { int phase; cudaEvent_t a, b; };
   std::vector<Ev> events;
   int64_t launches[RM_NPHASE] = {};
+  // z-slab partition (nranks > 1)
+  int rank = 0, nranks = 1;
+  rm_partition_info part{};
+  ncclComm_t comm = nullptr;
+  double *d_fh = nullptr, *d_uh = nullptr, *d_c = nullptr, *d_rtmp = nullptr;
+  int64_t nfree_global = 0;
 
   double* dalloc(size_t n) {
     void* d = nullptr;
@@ -316,6 +404,7 @@ struct rm_ctx {
     return static_cast<double*>(d);
   }
   ~rm_ctx() {
+    if (comm) { try { if (nccl().destroy) nccl().destroy(comm); } catch (...) {} }
     for (auto& e : events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : allocs) cudaFree(p);
     prim.release();
@@ -393,6 +482,31 @@ void rm_default_options(rm_options* o) {
 
 const char* rm_last_error(void) { return g_err.c_str(); }
 
+rm_status rm_partition(const rm_mesh* mesh, int32_t p, rm_space space, uint32_t gamma_d, int32_t rank, int32_t nranks,
+                       rm_partition_info* info) {
+  try {
+    if (!mesh || !info) throw RmError(RM_EINVAL, "null argument");
+    if (p < 1 || p > 15) throw RmError(RM_EINVAL, "p must be in 1..15");
+    compute_partition(*mesh, p, space, gamma_d, rank, nranks, *info);
+    return RM_OK;
+  } catch (const RmError& e) {
+    return fail(e);
+  }
+}
+
+rm_status rm_nccl_unique_id(void* id128) {
+  try {
+    if (!id128) throw RmError(RM_EINVAL, "null argument");
+    ncclUniqueId id;
+    NK(nccl().get_id(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof id);
+    return RM_OK;
+  } catch (const RmError& e) {
+    return fail(e);
+  }
+}
+
 rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space, const double* alpha,
                    int64_t n_alpha, const double* beta, int64_t n_beta, uint32_t gamma_d, const rm_options* opt) {
   auto t0 = std::chrono::steady_clock::now();
@@ -406,7 +520,6 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     if (mesh->nx < 1 || mesh->ny < 1 || mesh->nz < 1) throw RmError(RM_EINVAL, "mesh sizes must be >= 1");
     if (gamma_d > 0x3F) throw RmError(RM_EINVAL, "gamma_d has bits above bit 5");
     if (o.coarse != 0) throw RmError(RM_EINVAL, "coarse level not supported (reading G10)");
-    if (o.nranks > 1) throw RmError(RM_EINVAL, "multi-rank slabs not supported in this build");
     if (o.decomposition != RM_PAFW && o.decomposition != RM_PH) throw RmError(RM_EINVAL, "bad decomposition");
     if (o.factorization != RM_CHOL && o.factorization != RM_ICC_SC) throw RmError(RM_EINVAL, "bad factorization");
     const int64_t ncell = (int64_t)mesh->nx * mesh->ny * mesh->nz;
@@ -414,8 +527,44 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       throw RmError(RM_EINVAL, "alpha/beta must have 1 or ncells entries");
     for (int64_t i = 0; i < n_alpha; ++i) if (!(alpha[i] > 0)) throw RmError(RM_EINVAL, "alpha must be > 0");
     for (int64_t i = 0; i < n_beta; ++i) if (!(beta[i] >= 0)) throw RmError(RM_EINVAL, "beta must be >= 0");
+    // z-slab partition: the rest of the setup runs on the LOCAL mesh (slab + ghost layer below
+    // + shared plane above), with the patches of the owned vertex layers only
+    rm_partition_info part;
+    {
+      rm_mesh gm = *mesh;
+      if (o.nranks <= 1) { gm.z_begin = 0; gm.z_end = mesh->nz; }
+      compute_partition(gm, p, space, gamma_d, o.nranks > 1 ? o.rank : 0, std::max(o.nranks, 1), part);
+    }
+    const uint32_t gamma_global = gamma_d;
+    const int nz_global = mesh->nz;
+    rm_mesh lm = *mesh;
+    std::vector<double> lcoords;
+    if (o.nranks > 1) {
+      lm.nz = part.nz_local;
+      const size_t vplane = (size_t)(mesh->nx + 1) * (mesh->ny + 1) * 3;
+      if (mesh->coords) {
+        lm.coords = mesh->coords + (size_t)part.z_cell0 * vplane;
+      } else {   // the uniform unit-cube grid, sliced
+        lcoords.resize(vplane * (part.nz_local + 1));
+        for (int z = 0; z <= part.nz_local; ++z)
+          for (int y = 0; y <= mesh->ny; ++y)
+            for (int x = 0; x <= mesh->nx; ++x) {
+              double* X = &lcoords[((size_t)z * (mesh->ny + 1) + y) * (mesh->nx + 1) * 3 + (size_t)x * 3];
+              X[0] = (double)x / mesh->nx; X[1] = (double)y / mesh->ny; X[2] = (double)(part.z_cell0 + z) / nz_global;
+            }
+        lm.coords = lcoords.data();
+      }
+      const int64_t cplane = (int64_t)mesh->nx * mesh->ny;
+      if (n_alpha > 1) { alpha += part.z_cell0 * cplane; n_alpha = cplane * part.nz_local; }
+      if (n_beta > 1) { beta += part.z_cell0 * cplane; n_beta = cplane * part.nz_local; }
+      gamma_d = part.gamma_local;
+      mesh = &lm;
+    }
     CK(cudaSetDevice(o.device));
     std::unique_ptr<rm_ctx> c(new rm_ctx);
+    c->rank = o.nranks > 1 ? o.rank : 0;
+    c->nranks = std::max(o.nranks, 1);
+    c->part = part;
     c->k = space; c->p = p; c->n[0] = mesh->nx; c->n[1] = mesh->ny; c->n[2] = mesh->nz;
     c->gamma = gamma_d; c->decomposition = (space == 0) ? RM_PAFW : o.decomposition;
     c->st = static_cast<cudaStream_t>(o.stream);
@@ -511,6 +660,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.interior_only = o.patch_entities == RM_INTERIOR_ONLY;
     in.cartesian = cart;
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    in.zv_lo = part.v_lo; in.zv_hi = part.v_hi;   // owned vertex layers (all of them on one rank)
     {
       auto fam = rm::build_patch_family(in);
       upload_family(c->prim, *fam);
@@ -537,6 +687,21 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->d_t = c->dalloc(c->npot); c->d_s = c->dalloc(c->npot);
     }
     c->d_r = c->dalloc(c->ndof);
+    if (c->nranks > 1) {
+      // global free count; buffers of the multi-rank sweep; the communicator (if an id is given)
+      const uint32_t g = gamma_global;
+      const int64_t fx = (int64_t)c->n[0] * p + 1 - ((g >> 0) & 1) - ((g >> 1) & 1);
+      const int64_t fy = (int64_t)c->n[1] * p + 1 - ((g >> 2) & 1) - ((g >> 3) & 1);
+      const int64_t fz = (int64_t)nz_global * p + 1 - ((g >> 4) & 1) - ((g >> 5) & 1);
+      c->nfree = fx * fy * fz;
+      c->d_fh = c->dalloc(c->ndof); c->d_uh = c->dalloc(c->ndof); c->d_c = c->dalloc(c->ndof);
+      c->d_rtmp = c->dalloc((size_t)p * part.plane_len);
+      if (o.nccl_id) {
+        ncclUniqueId id;
+        std::memcpy(&id, o.nccl_id, sizeof id);
+        NK(nccl().init(&c->comm, c->nranks, id, c->rank));
+      }
+    }
     c->d_sc = c->dalloc(8);
     c->d_part = c->dalloc(1024);
     CK(cudaDeviceSynchronize());
@@ -674,6 +839,52 @@ void add_precond(rm_ctx* c, const double* r, double* u, double omega) {
   }
 }
 
+// ------------------------------------------------------------------ multi-rank sweep pieces
+// Forward halo: planes fwd_recv_* of v <- the owners' planes (NCCL send/recv on the stream).
+void halo_forward(rm_ctx* c, double* v) {
+  const rm_partition_info& P = c->part;
+  const NcclApi& N = nccl();
+  const size_t L = (size_t)P.plane_len;
+  NK(N.gstart());
+  if (c->rank > 0) {
+    NK(N.send(v + P.fwd_send_lo[0] * L, (P.fwd_send_lo[1] - P.fwd_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+    NK(N.recv(v + P.fwd_recv_lo[0] * L, (P.fwd_recv_lo[1] - P.fwd_recv_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+  }
+  if (c->rank < c->nranks - 1) {
+    NK(N.send(v + P.fwd_send_hi[0] * L, (P.fwd_send_hi[1] - P.fwd_send_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+    NK(N.recv(v + P.fwd_recv_hi[0] * L, (P.fwd_recv_hi[1] - P.fwd_recv_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+  }
+  NK(N.gend());
+}
+// Reverse-add: the corrections my patches put on rank - 1's planes go there and are added by it.
+void reverse_add(rm_ctx* c, double* cv) {
+  const rm_partition_info& P = c->part;
+  const NcclApi& N = nccl();
+  const size_t L = (size_t)P.plane_len;
+  const size_t nh = (size_t)(P.rev_recv_hi[1] - P.rev_recv_hi[0]) * L;
+  NK(N.gstart());
+  if (c->rank > 0)
+    NK(N.send(cv + P.rev_send_lo[0] * L, (P.rev_send_lo[1] - P.rev_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+  if (c->rank < c->nranks - 1 && nh > 0) NK(N.recv(c->d_rtmp, nh, ncclDouble, c->rank + 1, c->comm, c->st));
+  NK(N.gend());
+  if (c->rank < c->nranks - 1 && nh > 0)
+    CK(rm::launch_axpby((long long)nh, 1.0, c->d_rtmp, 1.0, cv + P.rev_recv_hi[0] * L, c->st));
+}
+// In-place sum over ranks of device scalars.
+void allreduce_sum(rm_ctx* c, double* x, size_t n) {
+  if (c->nranks > 1) NK(nccl().allreduce(x, x, n, ncclDouble, ncclSum, c->comm, c->st));
+}
+// Local patch correction cv = P_local^{-1} (f - A u): f, u with their forward halos filled.
+void local_correction(rm_ctx* c, const double* f, const double* u, double* cv) {
+  do_apply(c, u, f, c->d_r);
+  CK(cudaMemsetAsync(cv, 0, c->ndof * sizeof(double), c->st));
+  add_precond(c, c->d_r, cv, 1.0);
+}
+void need_comm(const rm_ctx* c) {
+  if (c->nranks > 1 && !c->comm)
+    throw RmError(RM_EINVAL, "multi-rank call needs options.nccl_id (or the rm_relax_begin / rm_relax_end stages)");
+}
+
 template <class F>
 rm_status guarded(rm_ctx* c, F&& f) {
   if (!c) { g_err = "null context"; return RM_EINVAL; }
@@ -693,36 +904,78 @@ rm_status guarded(rm_ctx* c, F&& f) {
 
 extern "C" {
 
+// u with its forward halo: the caller's vector itself on one rank (or without a communicator:
+// the caller filled the halo), else a copy with the halo exchanged
+const double* with_halo(rm_ctx* c, const double* u, double* buf) {
+  if (c->nranks == 1 || !c->comm) return u;
+  CK(cudaMemcpyAsync(buf, u, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  halo_forward(c, buf);
+  return buf;
+}
+
+// one sweep u_out = u_in + omega P^{-1} (f - A u_in) (z-slab: halos, local correction, reverse-add)
+void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
+  if (c->nranks > 1) {
+    need_comm(c);
+    const double* fh = with_halo(c, f, c->d_fh);
+    const double* uh = with_halo(c, u_in, c->d_uh);
+    local_correction(c, fh, uh, c->d_c);
+    reverse_add(c, c->d_c);
+    if (u_out != uh) CK(cudaMemcpyAsync(u_out, uh, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CK(rm::launch_axpby(c->ndof, omega, c->d_c, 1.0, u_out, c->st));
+    return;
+  }
+  do_apply(c, u_in, f, c->d_r);
+  if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  add_precond(c, c->d_r, u_out, omega);
+}
+
 rm_status rm_apply(rm_ctx* c, const double* u, double* v) {
   return guarded(c, [&] {
     if (!u || !v) throw RmError(RM_EINVAL, "null vector");
-    do_apply(c, u, nullptr, v);
+    do_apply(c, with_halo(c, u, c->d_uh), nullptr, v);
   });
 }
 
 rm_status rm_residual(rm_ctx* c, const double* f, const double* u, double* r) {
   return guarded(c, [&] {
     if (!f || !u || !r) throw RmError(RM_EINVAL, "null vector");
-    do_apply(c, u, f, r);
+    do_apply(c, with_halo(c, u, c->d_uh), f, r);
   });
 }
 
 rm_status rm_relax(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
   return guarded(c, [&] {
     if (!f || !u_in || !u_out) throw RmError(RM_EINVAL, "null vector");
-    do_apply(c, u_in, f, c->d_r);
+    relax_impl(c, f, u_in, u_out, omega);
+  });
+}
+
+rm_status rm_relax_begin(rm_ctx* c, const double* f, const double* u_in, double* cv) {
+  return guarded(c, [&] {
+    if (!f || !u_in || !cv) throw RmError(RM_EINVAL, "null vector");
+    local_correction(c, f, u_in, cv);
+  });
+}
+
+rm_status rm_relax_end(rm_ctx* c, const double* u_in, const double* cv, double* u_out, double omega) {
+  return guarded(c, [&] {
+    if (!u_in || !cv || !u_out) throw RmError(RM_EINVAL, "null vector");
     if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-    add_precond(c, c->d_r, u_out, omega);
+    CK(rm::launch_axpby(c->ndof, omega, cv, 1.0, u_out, c->st));
   });
 }
 
 rm_status rm_precondition(rm_ctx* c, const double* r, double* z) {
   return guarded(c, [&] {
     if (!r || !z) throw RmError(RM_EINVAL, "null vector");
-    // r with constrained entries read as zero: r_masked = r - 0*A0 ... use the residual kernel with u = 0
+    need_comm(c);
+    // r with constrained entries read as zero: the residual kernel with u = 0
+    const double* rh = with_halo(c, r, c->d_fh);
     CK(cudaMemsetAsync(z, 0, c->ndof * sizeof(double), c->st));
-    do_apply(c, z, r, c->d_r);   // d_r = r - A*0 = r, constrained entries zeroed
+    do_apply(c, z, rh, c->d_r);   // d_r = r - A*0 = r, constrained entries zeroed
     add_precond(c, c->d_r, z, 1.0);
+    if (c->nranks > 1) reverse_add(c, z);
   });
 }
 
@@ -733,8 +986,7 @@ rm_status rm_relax_host(rm_ctx* c, const double* f, const double* u_in, double* 
     const size_t B = c->ndof * sizeof(double);
     CK(cudaMemcpyAsync(c->d_hf, f, B, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_hu, u_in, B, cudaMemcpyHostToDevice, c->st));
-    do_apply(c, c->d_hu, c->d_hf, c->d_r);
-    add_precond(c, c->d_r, c->d_hu, omega);
+    relax_impl(c, c->d_hf, c->d_hu, c->d_hu, omega);
     CK(cudaMemcpyAsync(u_out, c->d_hu, B, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
   });
@@ -750,11 +1002,24 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
     double* rz = c->d_sc + 0;
     double* pq = c->d_sc + 1;
     double* rzn = c->d_sc + 2;
+    need_comm(c);
+    // multi-rank: dots over the owned planes (a contiguous range) + allreduce; halo of the
+    // search direction before each apply; reverse-add after each preconditioner application
+    const int64_t o0 = (int64_t)c->part.own_lo * c->part.plane_len;
+    const int64_t on = c->nranks > 1 ? (int64_t)(c->part.own_hi - c->part.own_lo) * c->part.plane_len : c->ndof;
+    auto dot = [&](const double* x, const double* y, double* out) {
+      CK(rm::launch_dot(on, x + (c->nranks > 1 ? o0 : 0), y + (c->nranks > 1 ? o0 : 0), c->d_part, out, c->st));
+      allreduce_sum(c, out, 1);
+    };
+    auto precond = [&](const double* rr, double* zz) {
+      CK(cudaMemsetAsync(zz, 0, B, c->st));
+      add_precond(c, rr, zz, 1.0);
+      if (c->nranks > 1) reverse_add(c, zz);
+    };
     CK(cudaMemsetAsync(u, 0, B, c->st));
-    do_apply(c, u, f, r);                         // r = f (masked)
-    CK(cudaMemsetAsync(c->d_z, 0, B, c->st));
-    add_precond(c, r, c->d_z, 1.0);
-    CK(rm::launch_dot(c->ndof, r, c->d_z, c->d_part, rz, c->st));
+    do_apply(c, u, with_halo(c, f, c->d_fh), r);   // r = f (masked)
+    precond(r, c->d_z);
+    dot(r, c->d_z, rz);
     double rz0 = 0.0;
     CK(cudaMemcpyAsync(&rz0, rz, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
@@ -765,12 +1030,12 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
       CK(cudaMemcpyAsync(c->d_pp, c->d_z, B, cudaMemcpyDeviceToDevice, c->st));
       bool done = false;
       for (it = 1; it <= maxit; ++it) {
+        if (c->nranks > 1) halo_forward(c, c->d_pp);
         do_apply(c, c->d_pp, nullptr, c->d_q);
-        CK(rm::launch_dot(c->ndof, c->d_pp, c->d_q, c->d_part, pq, c->st));
+        dot(c->d_pp, c->d_q, pq);
         CK(rm::launch_pcg_update(c->ndof, rz, pq, c->d_pp, c->d_q, u, r, c->st));
-        CK(cudaMemsetAsync(c->d_z, 0, B, c->st));
-        add_precond(c, r, c->d_z, 1.0);
-        CK(rm::launch_dot(c->ndof, r, c->d_z, c->d_part, rzn, c->st));
+        precond(r, c->d_z);
+        dot(r, c->d_z, rzn);
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, rzn, 8, cudaMemcpyDeviceToHost, c->st));
         CK(cudaStreamSynchronize(c->st));

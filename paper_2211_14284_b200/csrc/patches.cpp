@@ -1120,6 +1120,13 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   Builder B(in, fam.get());
   fam->sp = B.sp; fam->dim = in.dim; fam->gamma_d = in.gamma_d; fam->factorization = in.factorization;
   std::vector<Entity> ents = entities(B.sp, in.dim, in.interior_only != 0);
+  if (in.zv_lo > 0 || in.zv_hi <= B.sp.n[2]) {   // z-slab ownership: vertex stars of the owned layers
+    if (in.dim != 0) throw std::runtime_error("z-slab patch ownership: vertex stars only");
+    std::vector<Entity> kept;
+    for (const Entity& e : ents)
+      if (e.s[2].v >= in.zv_lo && e.s[2].v < in.zv_hi) kept.push_back(e);
+    ents.swap(kept);
+  }
   std::map<ClassKey, int> cls_of;
   std::vector<int> ecls(ents.size());
   std::vector<Entity> rep;

@@ -186,6 +186,7 @@ struct SetupInput {
   int interior_only;
   bool cartesian;                 // all cells axis-aligned
   const double* hx; const double* hy; const double* hz;   // per-direction cell sizes (cartesian)
+  int zv_lo = 0, zv_hi = 1 << 30;   // vertex stars kept: z vertex layers [zv_lo, zv_hi) (z-slab ownership)
 };
 
 // Builds the full patch family. Throws std::runtime_error with a message on failure.

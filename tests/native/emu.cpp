@@ -249,19 +249,43 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
 extern "C" {
 
 // z += P^{-1} r over one patch family on the uniform unit-cube grid (or the given coords).
+static int emu_precondition_impl(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
+                                 const double* beta, long long nb, const double* coords, int dim, int fact,
+                                 int interior_only, int zv_lo, int zv_hi, const double* hz, const double* r,
+                                 double* z, char* err, int errlen, long long* stats);
+
 int emu_precondition(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
                      const double* beta, long long nb, const double* coords, int dim, int fact, int interior_only,
                      const double* r, double* z, char* err, int errlen, long long* stats) {
+  return emu_precondition_impl(k, p, nx, ny, nz, gamma, alpha, na, beta, nb, coords, dim, fact, interior_only, 0,
+                               1 << 30, nullptr, r, z, err, errlen, stats);
+}
+
+// same, keeping only the vertex stars of the z vertex layers [zv_lo, zv_hi) (z-slab ownership);
+// hz: z cell sizes of an axis-aligned slab (coords == NULL), NULL = 1/nz
+int emu_precondition_zv(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
+                        const double* beta, long long nb, const double* coords, int dim, int fact, int zv_lo,
+                        int zv_hi, const double* hz, const double* r, double* z, char* err, int errlen) {
+  return emu_precondition_impl(k, p, nx, ny, nz, gamma, alpha, na, beta, nb, coords, dim, fact, 0, zv_lo, zv_hi, hz, r,
+                               z, err, errlen, nullptr);
+}
+
+static int emu_precondition_impl(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
+                                 const double* beta, long long nb, const double* coords, int dim, int fact,
+                                 int interior_only, int zv_lo, int zv_hi, const double* hz, const double* r,
+                                 double* z, char* err, int errlen, long long* stats) {
   try {
     std::vector<double> h[3];
     const int n[3] = {nx, ny, nz};
     for (int d = 0; d < 3; ++d) h[d].assign(n[d], 1.0 / n[d]);
+    if (hz) h[2].assign(hz, hz + nz);
     SetupInput in{};
     in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
     in.coords = coords; in.alpha = alpha; in.beta = beta; in.n_alpha = na; in.n_beta = nb;
     in.dim = dim; in.factorization = fact; in.interior_only = interior_only;
     in.cartesian = (coords == nullptr);
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    in.zv_lo = zv_lo; in.zv_hi = zv_hi;
     auto F = build_patch_family(in);
     emulate_family(*F, r, z);
     if (stats) {

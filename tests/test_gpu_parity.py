@@ -3,9 +3,12 @@ the same seeded inputs (rm_inputs).  Tolerance (BASELINE.json north_star): relat
 per apply and per sweep in fp64, PCG iteration counts within +-1.  The H(div) cases carry a
 conditioning-derived tolerance: two exact factorizations of the
 same patch differ by ~cond(A_II) eps, and cond(A_II) ~ 5e4 at these sizes."""
+import dataclasses
+
 import numpy as np
 import pytest
 
+import gpu_util as gu
 import rm_inputs as ri
 
 pytestmark = pytest.mark.gpu
@@ -172,3 +175,63 @@ def test_trilinear_apply_full_degree(dev, nx, p):
     ref = apply_matfree(sp_, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), np.where(m, 0.0, u))
     ref[m] = 0.0
     assert rel(v.cpu().numpy(), ref) < 1e-11
+
+
+# ------------------------------------------------------------------ z-slab partition on one GPU
+# Row a3: two contexts on the same device hold the local problems of rank 0 and
+# rank 1 of 2 (no communicator: the split-stage calls), the test moves the halo planes with plain
+# device copies following rm_partition's plan, and the owned planes of the result must equal the
+# single-context sweep.  (The NCCL path of rm_relax performs the same moves with ncclSend/Recv.)
+SLAB_CASES = [
+    ("q3-cart-dirichlet", dataclasses.replace(ri.CONFIGS[1].with_mesh(3), nz=4)),
+    ("q4-cart-neumann-z", dataclasses.replace(ri.CONFIGS[2].with_mesh(3).with_p(4), nz=5)),
+    ("q3-trilinear-iccsc", dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), nz=4)),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,w", SLAB_CASES, ids=[c[0] for c in SLAB_CASES])
+def test_slab_partition_two_contexts(dev, name, w):
+    import torch
+    import paper_2211_14284_b200 as rmb
+    G = 2
+    gctx = gu.setup_product(w)
+    n = gctx.n_local
+    mask = gctx.constrained_mask()
+    f = ri.uniform_vector(w.cfg, 0, n); f[mask] = 0
+    u = ri.uniform_vector(w.cfg, 3, n); u[mask] = 0
+    ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
+    ref = torch.empty_like(ut)
+    rmb.rm_relax(gctx, ft, ut, ref, 1.0)
+    bounds = [w.nz * g // G for g in range(G + 1)]
+    parts, ctxs, fl, ul = [], [], [], []
+    for g in range(G):
+        P = rmb.rm_partition(w.nx, w.ny, w.nz, w.p, 0, w.gamma_d, g, G, bounds[g], bounds[g + 1])
+        ctx = gu.setup_product(w, rank=g, nranks=G, z_begin=bounds[g], z_end=bounds[g + 1])
+        L, g0 = P["plane_len"], P["z_cell0"] * w.p * P["plane_len"]
+        assert ctx.n_local == (P["nz_local"] * w.p + 1) * L
+        own = slice(P["own_lo"] * L, P["own_hi"] * L)
+        a = torch.full((ctx.n_local,), float("nan"), dtype=torch.float64, device=dev)
+        b = a.clone()
+        a[own] = ft[g0:g0 + ctx.n_local][own]
+        b[own] = ut[g0:g0 + ctx.n_local][own]
+        parts.append(P); ctxs.append(ctx); fl.append(a); ul.append(b)
+    L = parts[0]["plane_len"]
+    sl = lambda r: slice(r[0] * L, r[1] * L)   # noqa: E731
+    for v in (fl, ul):   # forward halos (rank 0 <-> rank 1)
+        v[1][sl(parts[1]["fwd_recv_lo"])] = v[0][sl(parts[0]["fwd_send_hi"])]
+        v[0][sl(parts[0]["fwd_recv_hi"])] = v[1][sl(parts[1]["fwd_send_lo"])]
+    assert all(torch.isfinite(t).all() for t in fl + ul)
+    cs = [torch.empty_like(t) for t in ul]
+    for g in range(G):
+        rmb.rm_relax_begin(ctxs[g], fl[g], ul[g], cs[g])
+    cs[0][sl(parts[0]["rev_recv_hi"])] += cs[1][sl(parts[1]["rev_send_lo"])]   # reverse-add
+    for g in range(G):
+        uo = torch.empty_like(ul[g])
+        rmb.rm_relax_end(ctxs[g], ul[g], cs[g], uo, 1.0)
+        P = parts[g]
+        g0 = P["z_cell0"] * w.p * L
+        own = slice(P["own_lo"] * L, P["own_hi"] * L)
+        got = uo[own].cpu().numpy()
+        want = ref[g0:g0 + ctxs[g].n_local][own].cpu().numpy()
+        assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max()), (name, g)
