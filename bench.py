@@ -175,6 +175,8 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if world > 1:   # torchrun pins OMP_NUM_THREADS=1: give each rank's host setup its share of the cores
+        os.environ.setdefault("RM_SETUP_THREADS", str(max(1, (os.cpu_count() or 8) // world)))
     import torch
     import torch.distributed as dist
     import paper_2211_14284_b200 as rmb

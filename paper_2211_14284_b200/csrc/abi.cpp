@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <omp.h>
 #include <nccl.h>   // types and prototypes only: the library is dlopen'ed (rank > 1 only)
 
 #include <chrono>
@@ -512,6 +513,8 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
   auto t0 = std::chrono::steady_clock::now();
   try {
     if (!out || !mesh || !alpha || !beta) throw RmError(RM_EINVAL, "null argument");
+    // host setup threads (OpenMP); launchers that pin OMP_NUM_THREADS=1 per rank can override
+    if (const char* e = getenv("RM_SETUP_THREADS")) omp_set_num_threads(std::max(1, atoi(e)));
     *out = nullptr;
     rm_options o;
     if (opt) o = *opt; else rm_default_options(&o);
