@@ -259,6 +259,10 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     Lh.rpad = static_cast<double*>(a); Lh.cpad = static_cast<double*>(b);
   }
   Lh.npatch = (int)np;
+  // tile warps joining the ICC solve (measured slower: more ring walkers), opt-in experiment
+  Lh.icc_only = getenv("RM_ICC_ONLY") ? 1 : 0;
+  for (const auto& C : P.classes)
+    if (C.final_kind != rm::FINAL_ICC || !C.sc) Lh.icc_only = 0;
   Lh.cs.ncolors = P.ncolors;
   for (int c = 0; c <= P.ncolors; ++c) Lh.cs.start[c] = F.color_start[c];
   Lh.done = F.upload(std::vector<unsigned>(1, 0u));

@@ -129,6 +129,7 @@ struct PatchLaunch {
   const double* sc_c;
   const int* sc_nk;
   double* sc_fb;         // per-cell face line sums of the pre step [ncell][6][(p-1)^2]
+  int icc_only;          // every class ends in ICC (no dense tiles): the tile warps join the sparse warps
   int sc_p, sc_n[3];
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
                                                                const XferEntry* __restrict__ xfer,
                                                                const long long* __restrict__ xbeg, int nbox,
                                                                unsigned long long* __restrict__ prof, int dbg_q,
-                                                               double* __restrict__ dbg_out) {
+                                                               double* __restrict__ dbg_out, int icc_only) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* ringA = smraw + BAR_BYTES;
   unsigned char* ringB = ringA + capA;
@@ -371,11 +371,14 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   if (tid == 0) {
     for (int ch = 0; ch < 2; ++ch) {
       ChanSm c = chan_sm(smraw, ch);
-      for (int s = 0; s < NDESC; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], ch == 0 ? NC : NTW); }
+      for (int s = 0; s < NDESC; ++s) {
+        mbar_init(&c.full[s], 1);
+        mbar_init(&c.empty[s], ch == 0 ? (icc_only ? NC + NTW : NC) : NTW);
+      }
     }
     for (int b = 0; b < NBOX; ++b) {
       mbar_init(&vfull[b], 1); mbar_init(&gready[b], NC); mbar_init(&xready[b], NTW);
-      mbar_init(&vdone[b], NC); mbar_init(&vempty[b], 1);   // vempty unused (the store warp reloads)
+      mbar_init(&vdone[b], icc_only ? NC + NTW : NC); mbar_init(&vempty[b], 1);   // vempty unused
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -469,7 +472,9 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     return;
   }
   // ================================================================== tile warps
-  if (warp >= WT0) {
+  // (families whose classes all end in ICC (ICC-SC) have no tile work: the tile warps join the
+  // sparse warps instead, icc_only)
+  if (warp >= WT0 && !icc_only) {
     const int tw = warp - WT0;
     Consumer ct{chan_sm(smraw, 1), ringB, 0, 0, nullptr, nullptr};
     unsigned long long tt_wait = 0, tt0 = prof ? clock64() : 0;
@@ -532,8 +537,9 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   // ================================================================== sparse warps
   Consumer cn{chan_sm(smraw, 0), ringA, 0, 0, nullptr, nullptr};
   unsigned long long sp_box = 0, sp_x = 0, sp_fwd = 0, sp_bwd = 0, sp0 = prof ? clock64() : 0;
-  unsigned long long sp_icc_acq = 0, sp_icc_sync = 0;
   const bool pf = prof != nullptr && tid == 0;
+  const int ncw = icc_only ? NC + NTW : NC, nct = 32 * ncw;   // consumer warps / threads
+  auto csync_n = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory"); };
   auto forward = [&](int i) {
     const int q = (int)blockIdx.x + i * G;
     const DClass& C = classes[pclass[q]];
@@ -543,11 +549,11 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     mbar_wait(&vfull[b], (uint32_t)(i / nbox) & 1u);   // the window box of r has landed
     if (pf) { const unsigned long long tb = clock64(); sp_box += tb - ta; ta = tb; }
     if (dbg_out && dbg_q == 2) {   // debug dump of every loaded box (experiments only)
-      csync();
+      csync_n();
       double* d = dbg_out + (size_t)q * (box_total + 9);
       for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
       if (tid < 9) d[tid] = (double)porig[9 * q + tid];
-      csync();
+      csync_n();
     }
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
@@ -589,16 +595,16 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
         }
         cn.release(lane);
       }
-      csync();
+      csync_n();
       for (int pi = L.w_b; pi < L.w_e; ++pi) {
         const Piece_ pc = cn.acquire();
         sliced_piece(pc, v, L.w.nrows, warp, lane, [&](int rb, double acc) { v[rb] -= acc; });
         cn.release(lane);
       }
-      csync();
+      csync_n();
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&gready[b]);   // the tile warps may read v_F
+    if (lane == 0 && !icc_only) mbar_arrive(&gready[b]);   // the tile warps may read v_F
     if (pf) sp_fwd += clock64() - ta;
   };
   auto backward = [&](int i) {
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     const int b = i % nbox;
     double* v = box0 + b * boxd;
     unsigned long long ta = pf ? clock64() : 0;
-    mbar_wait(&xready[b], (uint32_t)(i / nbox) & 1u);   // tiles(i) done (or skipped)
+    if (!icc_only) mbar_wait(&xready[b], (uint32_t)(i / nbox) & 1u);   // tiles(i) done (or skipped)
     if (pf) { const unsigned long long tb = clock64(); sp_x += tb - ta; ta = tb; }
     if (C.final_kind != 0) {
       // ICC(0) on the final block: forward rows of L by levels (diag last, stored inverted),
@@ -619,14 +625,12 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
         for (int l = 0; l < nl; ++l) {
           const int pe = lp[l + 1];
           for (int pi = lp[l]; pi < pe; ++pi) {
-            const unsigned long long tq0 = pf ? clock64() : 0;
             const Piece_ pc = cn.acquire();
-            if (pf) sp_icc_acq += clock64() - tq0;
             // lane-interleaved piece (patches.cpp): <= 32 rows, one per lane; the level's pieces
             // are dealt round-robin to the sparse warps (every warp walks the ring cursor)
             const Hdr h = hdr(pc.pb);
             const int cnt = h.a1 - h.a0, Lm = h.e0;
-            if ((pi - lp[l]) % NC == warp && lane < cnt) {
+            if ((pi - lp[l]) % ncw == warp && lane < cnt) {
               const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
               const uint16_t* cols = rows + 32 + lane;
               const double* off = pc.val + 32 + lane;
@@ -651,9 +655,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
             }
             cn.release(lane);
           }
-          const unsigned long long tq1 = pf ? clock64() : 0;
-          csync();
-          if (pf) sp_icc_sync += clock64() - tq1;
+          csync_n();
         }
       }
     }
@@ -665,21 +667,21 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
         sliced_piece(pc, v, L.wt.nrows, warp, lane, [&](int rb, double acc) { v[rb] -= acc; });
         cn.release(lane);
       }
-      csync();
+      csync_n();
     }
     {   // zero the box entries outside the patch, hand the box to the store warp
       const Piece_ pc = cn.acquire();   // ZERO piece
       const Hdr h = hdr(pc.pb);
       const uint16_t* zl = reinterpret_cast<const uint16_t*>(pc.pb + 16);
-      for (int k = tid; k < h.a1 - h.a0; k += NT) v[zl[k]] = 0.0;
+      for (int k = tid; k < h.a1 - h.a0; k += nct) v[zl[k]] = 0.0;
       cn.release(lane);
     }
     if (dbg_out && dbg_q == 1) {   // debug dump of every finished box (experiments only, RM_DEBUG_Q)
-      csync();
+      csync_n();
       double* d = dbg_out + (size_t)q * (box_total + 9);
       for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
       if (tid < 9) d[tid] = (double)porig[9 * q + tid];
-      csync();
+      csync_n();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
     __syncwarp();
@@ -694,7 +696,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   if (pf) {
     unsigned long long* o = prof + 24 * blockIdx.x;
     o[7] = clock64() - sp0; o[8] = sp_box; o[9] = sp_x; o[10] = sp_fwd; o[11] = sp_bwd;
-    o[16] = sp_icc_acq; o[17] = sp_icc_sync;
+
   }
 }
 
@@ -959,7 +961,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
       L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
       (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof,
-      getenv("RM_DEBUG_Q") ? atoi(getenv("RM_DEBUG_Q")) : -1, dbg_buf(L.box_total));
+      getenv("RM_DEBUG_Q") ? atoi(getenv("RM_DEBUG_Q")) : -1, dbg_buf(L.box_total), L.icc_only);
   if (kt) kt->end(kt->arg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
@@ -972,8 +974,8 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     fprintf(stderr,
             "[rm prof kcyc] producer total %.0f idle %.0f | store total %.0f wait-done %.0f colour %.0f | tiles total %.0f "
             "wait-fwd %.0f | sparse total %.0f box-wait %.0f x-wait %.0f fwd %.0f bwd %.0f | prodA total %.0f room-wait %.0f "
-            "| prodB total %.0f room-wait %.0f | icc acquire-wait %.0f level-sync %.0f\n",
-            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15], a[16], a[17]);
+            "| prodB total %.0f room-wait %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15]);
   }
   if (L.sc_dinv && nint > 0 && !getenv("RM_DEBUG_SC_NOPOST")) {
     sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
