@@ -626,32 +626,36 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
           const int pe = lp[l + 1];
           for (int pi = lp[l]; pi < pe; ++pi) {
             const Piece_ pc = cn.acquire();
-            // lane-interleaved piece (patches.cpp): <= 32 rows, one per lane; the level's pieces
-            // are dealt round-robin to the sparse warps (every warp walks the ring cursor)
+            // multi-chunk ICC piece (patches.cpp): chunk c (<= 32 rows, lane-interleaved) is
+            // taken by consumer warp c; one header and one table entry per warp and piece
             const Hdr h = hdr(pc.pb);
-            const int cnt = h.a1 - h.a0, Lm = h.e0;
-            if ((pi - lp[l]) % ncw == warp && lane < cnt) {
-              const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + 16);
-              const uint16_t* cols = rows + 32 + lane;
-              const double* off = pc.val + 32 + lane;
-              const int a = rows[lane];
-              double s0 = v[a], s1 = 0.0;
-              int j = 0;
-              for (; j + 3 < Lm; j += 4) {   // step j of this row: conflict-free value / column loads
-                const int c0 = cols[32 * j], c1 = cols[32 * j + 32], c2 = cols[32 * j + 64], c3 = cols[32 * j + 96];
-                const double w0 = off[32 * j], w1 = off[32 * j + 32], w2 = off[32 * j + 64], w3 = off[32 * j + 96];
-                const double x0 = v[c0], x1 = v[c1], x2 = v[c2], x3 = v[c3];
-                s0 = fma(-w0, x0, s0);
-                s1 = fma(-w1, x1, s1);
-                s0 = fma(-w2, x2, s0);
-                s1 = fma(-w3, x3, s1);
+            if (warp < h.a1 - h.a0) {
+              const int4 ent = reinterpret_cast<const int4*>(pc.pb + 16)[warp];   // cnt, L, meta, values
+              const int cnt = ent.x, Lm = ent.y;
+              if (lane < cnt) {
+                const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + ent.z);
+                const uint16_t* cols = rows + 32 + lane;
+                const double* dgv = pc.val + ent.w;
+                const double* off = dgv + 32 + lane;
+                const int a = rows[lane];
+                double s0 = v[a], s1 = 0.0;
+                int j = 0;
+                for (; j + 3 < Lm; j += 4) {   // step j of this row: conflict-free value / column loads
+                  const int c0 = cols[32 * j], c1 = cols[32 * j + 32], c2 = cols[32 * j + 64], c3 = cols[32 * j + 96];
+                  const double w0 = off[32 * j], w1 = off[32 * j + 32], w2 = off[32 * j + 64], w3 = off[32 * j + 96];
+                  const double x0 = v[c0], x1 = v[c1], x2 = v[c2], x3 = v[c3];
+                  s0 = fma(-w0, x0, s0);
+                  s1 = fma(-w1, x1, s1);
+                  s0 = fma(-w2, x2, s0);
+                  s1 = fma(-w3, x3, s1);
+                }
+                for (; j < Lm; ++j) {
+                  const double x = v[cols[32 * j]];
+                  if (j & 1) s1 = fma(-off[32 * j], x, s1);
+                  else s0 = fma(-off[32 * j], x, s0);
+                }
+                v[a] = (s0 + s1) * dgv[lane];
               }
-              for (; j < Lm; ++j) {
-                const double x = v[cols[32 * j]];
-                if (j & 1) s1 = fma(-off[32 * j], x, s1);
-                else s0 = fma(-off[32 * j], x, s0);
-              }
-              v[a] = (s0 + s1) * pc.val[lane];
             }
             cn.release(lane);
           }

@@ -240,12 +240,21 @@ void build_meta(ClassProgram& C) {
         for (int z : C.zlist) put16(z);
         break;
       case PK_ICCF:
-      case PK_ICCB: {  // 32 uint16 row boxes, then the interleaved column boxes (pads: box 0)
+      case PK_ICCB: {  // chunk table {cnt, L, meta offset, value offset} x nchunks, then per chunk
+                       // 32 uint16 row boxes and the interleaved column boxes (pads: box 0)
         const bool f = p.kind == PK_ICCF;
         const std::vector<int>& row = f ? C.iccf_row : C.iccb_row;
         const std::vector<int>& col = f ? C.iccf_col : C.iccb_col;
-        for (int k = 0; k < 32; ++k) put16(k < p.a1 - p.a0 ? C.bidx[f0 + row[p.a0 + k]] : 0);
-        for (int k = 32; k < p.nd; ++k) put16(col[p.cofs + k] < 0 ? 0 : C.bidx[f0 + col[p.cofs + k]]);
+        const std::vector<IccChunk>& ch = f ? C.iccf_chunk : C.iccb_chunk;
+        const size_t tab = M.size();
+        M.resize(M.size() + 16 * (p.a1 - p.a0), 0);
+        for (int c = p.a0; c < p.a1; ++c) {
+          const IccChunk& k = ch[c];
+          const int32_t ent[4] = {k.cnt, k.L, (int)(M.size() - at), k.sofs - ch[p.a0].sofs};
+          std::memcpy(&M[tab + 16 * (c - p.a0)], ent, 16);
+          for (int q = 0; q < 32; ++q) put16(q < k.cnt ? C.bidx[f0 + row[k.r0 + q]] : 0);
+          for (int q = 32; q < 32 + 32 * k.L; ++q) put16(col[k.sofs + q] < 0 ? 0 : C.bidx[f0 + col[k.sofs + q]]);
+        }
         break;
       }
       default:
@@ -339,24 +348,27 @@ void build_stream(ClassProgram& C) {
       std::vector<int>& slot = pass == 0 ? C.iccf_src : C.iccb_src;   // per piece value slot -> canonical (-1: 0)
       std::vector<int>& colv = pass == 0 ? C.iccf_col : C.iccb_col;   // per piece value slot -> column (-1: pad)
       std::vector<int>& lpiece = pass == 0 ? C.iccf_lpiece : C.iccb_lpiece;
+      std::vector<IccChunk>& chunks = pass == 0 ? C.iccf_chunk : C.iccb_chunk;
       const std::vector<int>& lptr = pass == 0 ? C.icc_level_ptr : C.icct_level_ptr;
       const std::vector<int>& lrows = pass == 0 ? C.icc_level_rows : C.icct_level_rows;
       const std::vector<int>& rp = pass == 0 ? C.icc_rowptr : C.icct_rowptr;
       const std::vector<int>& cl = pass == 0 ? C.icc_col : C.icct_col;
-      rowv.clear(); slot.clear(); colv.clear(); lpiece.clear();
+      rowv.clear(); slot.clear(); colv.clear(); lpiece.clear(); chunks.clear();
       C.iccf_rp.clear(); C.iccb_rp.clear();
       const int nl = (int)lptr.size() - 1;
       for (int l = 0; l < nl; ++l) {
         lpiece.push_back((int)C.pieces.size());
         std::vector<int> lr(lrows.begin() + lptr[l], lrows.begin() + lptr[l + 1]);
         std::stable_sort(lr.begin(), lr.end(), [&](int x, int y) { return rp[x + 1] - rp[x] > rp[y + 1] - rp[y]; });
-        for (size_t c0 = 0; c0 < lr.size(); c0 += kIccRows) {
+        const int ch0 = (int)chunks.size();
+        for (size_t c0 = 0; c0 < lr.size(); c0 += kIccRows) {   // chunks of <= 32 rows
           const int cnt = (int)std::min<size_t>(kIccRows, lr.size() - c0);
           int Lmax = 0;
           for (int k = 0; k < cnt; ++k) Lmax = std::max(Lmax, rp[lr[c0 + k] + 1] - rp[lr[c0 + k]] - 1);
           const int nd = 32 + 32 * Lmax;
           if (nd > 4 * kPieceMax) throw std::runtime_error("ICC row too long for a piece");
-          const int a0 = (int)rowv.size(), sofs = (int)slot.size();
+          const int sofs = (int)slot.size();
+          chunks.push_back(IccChunk{(int)rowv.size(), cnt, Lmax, sofs});
           slot.resize(sofs + nd, -1);
           colv.resize(sofs + nd, -1);
           for (int k = 0; k < cnt; ++k) {
@@ -371,7 +383,18 @@ void build_stream(ClassProgram& C) {
               colv[sofs + 32 + 32 * j + k] = cl[t];
             }
           }
-          add_piece(C, s, Piece{pass == 0 ? PK_ICCF : PK_ICCB, l, a0, a0 + cnt, Lmax, 0, nd, sofs});
+        }
+        // pieces of <= kIccChunks consecutive chunks and <= 4 kPieceMax values (chunk c -> warp c)
+        for (int c = ch0; c < (int)chunks.size();) {
+          const int c0 = c;
+          int nd = 0;
+          while (c < (int)chunks.size() && c - c0 < kIccChunks) {
+            const int cd = 32 + 32 * chunks[c].L;
+            if (c > c0 && nd + cd > 4 * kPieceMax) break;
+            nd += cd;
+            ++c;
+          }
+          add_piece(C, s, Piece{pass == 0 ? PK_ICCF : PK_ICCB, l, c0, c, c - c0, 0, nd, chunks[c0].sofs});
         }
       }
       lpiece.push_back((int)C.pieces.size());

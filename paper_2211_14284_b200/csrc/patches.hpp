@@ -65,7 +65,9 @@ enum FinalKind { FINAL_DENSE_INV = 0, FINAL_ICC = 1 };
 // units form their own channel, consumed by the tile warps only)
 enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_FINAL = 6, PK_ZERO = 7 };
 constexpr int kPieceMax = 2048;      // doubles (16 KB) of values per piece
-constexpr int kIccRows = 32;      // rows per ICC piece: one row per lane of the warp that takes it
+constexpr int kIccRows = 32;      // rows per ICC chunk: one row per lane of the warp that takes it
+constexpr int kIccChunks = 8;     // chunks per ICC piece: chunk c is taken by sparse warp c
+struct IccChunk { int r0, cnt, L, sofs; };   // level-ordered rows [r0, r0+cnt), longest off-diag row, slot offset
 constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
 // Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
 // owns rows 4a..4a+3 and columns 8b..8b+7; step k (0..15) holds its elements (row 4a + k/4,
@@ -119,6 +121,7 @@ struct ClassProgram {
   // ICC in level order (stream layout): q = level-ordered row index; rp over values in stream order
   std::vector<int> iccf_row, iccf_rp, iccf_col, iccf_src, iccf_lpiece;   // forward (diag last)
   std::vector<int> iccb_row, iccb_rp, iccb_col, iccb_src, iccb_lpiece;   // backward (diag first)
+  std::vector<IccChunk> iccf_chunk, iccb_chunk;   // pieces hold chunk ranges [a0, a1)
   int64_t nvals_canon = 0;               // doubles per canonical (factorization-order) block
   int64_t nvals = 0;                     // doubles per patch value block (stream layout)
   // stream pieces and the piece ranges of each section

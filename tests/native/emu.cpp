@@ -188,20 +188,25 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
           for (int i = 0; i < m; ++i) v[fb[i]] = x[i];
         }
       } else {
-        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {   // lane-interleaved ICC pieces
+        for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {   // multi-chunk lane-interleaved ICC pieces
           PieceView w = view(pi);
-          const int cnt = w.a1 - w.a0, Lm = C.pieces[pi].e0;
-          const uint8_t* rows = w.pb + 16;
-          const uint8_t* cols = rows + 64;
-          for (int k = 0; k < cnt; ++k) {   // same arithmetic order as the kernel
-            const int a = rd<uint16_t>(rows, k);
-            double s0 = v[a], s1 = 0.0;
-            for (int j = 0; j < Lm; ++j) {
-              const double x = v[rd<uint16_t>(cols, 32 * j + k)], wv = w.val[32 + 32 * j + k];
-              if (j & 1) s1 = std::fma(-wv, x, s1);
-              else s0 = std::fma(-wv, x, s0);
+          const int nch = w.a1 - w.a0;
+          for (int c = 0; c < nch; ++c) {
+            const int cnt = rd<int32_t>(w.pb + 16, 4 * c), Lm = rd<int32_t>(w.pb + 16, 4 * c + 1);
+            const int mo = rd<int32_t>(w.pb + 16, 4 * c + 2), vo = rd<int32_t>(w.pb + 16, 4 * c + 3);
+            const uint8_t* rows = w.pb + mo;
+            const uint8_t* cols = rows + 64;
+            const double* val = w.val + vo;
+            for (int k = 0; k < cnt; ++k) {   // same arithmetic order as the kernel
+              const int a = rd<uint16_t>(rows, k);
+              double s0 = v[a], s1 = 0.0;
+              for (int j = 0; j < Lm; ++j) {
+                const double x = v[rd<uint16_t>(cols, 32 * j + k)], wv = val[32 + 32 * j + k];
+                if (j & 1) s1 = std::fma(-wv, x, s1);
+                else s0 = std::fma(-wv, x, s0);
+              }
+              v[a] = (s0 + s1) * val[k];
             }
-            v[a] = (s0 + s1) * w.val[k];
           }
         }
       }
