@@ -37,6 +37,10 @@ import numpy as np  # noqa: E402
 import rm_inputs as ri  # noqa: E402
 
 # bounded oracle samples (same p, space, coefficient law, BCs; smaller mesh) -- DESIGN.md
+# trilinear apply (apply_tri.cu, p = 15 tables padded to 16 x 24): per cell 2 x (196,608 + 442,368 +
+# 884,736) FMA in the z / y / x contractions + ~97 flops at each of the 24^3 points
+TRI_FLOPS_PER_CELL = 2 * 2 * (196608 + 442368 + 884736) + 97 * 24 ** 3
+FP64_PEAK_TFLOPS = 36.9   # measured on this pool's B200 (scripts/fp64_bench.cu; DMMA and DFMA alike)
 ORACLE_SAMPLE = {1: (4, 4, 4), 2: (3, 3, 3), 3: (2, 2, 2), 4: (2, 2, 2), 5: None}
 # cfg5 (p = 15, trilinear, ICC-SC): the oracle forms each patch's dense matrix (~24k DoFs) by
 # quadrature in numpy; even the smallest sample (2^3 cells, one interior vertex) does not finish
@@ -251,21 +255,39 @@ def main():
     nfree_all = info["n_free"] if slab else info["n_free"] * world   # slab: n_free is the global count
     value = nfree_all / (ms * 1e-3)
 
-    # roofline of the dominant kernel: the persistent patch kernel, timed alone (entry 4: CUDA
-    # events recorded by the library on its stream around each patch-kernel launch)
+    # roofline of the dominant kernel (the larger of the two timed alone by the library: entry 4 =
+    # the persistent patch kernel (HBM-bound), entry 5 = the apply kernel; for trilinear cells the
+    # apply is FP64-bound (DMMA + DFMA on one datapath), DESIGN.md §5 counts its flops)
     hbm, peak_kind = peaks()
     k_ms_sweep = phase_ms[4] / args.steps
     k_launch_sweep = max(launches[4] / args.steps, 1)
     prim_bytes = info["factor_bytes"] + 3 * 8 * n   # factor values + r window boxes + c reduce-add
     achieved = prim_bytes / (k_ms_sweep * 1e-3) / 1e9 if k_ms_sweep > 0 else 0.0
-    roof = {"kernel": "patch_stream_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
-            "bytes_per_launch": prim_bytes / k_launch_sweep,
-            "launch_ms_avg": k_ms_sweep / k_launch_sweep,
-            "share_of_step": k_ms_sweep / ms if ms > 0 else None,
-            "phase_ms_per_step": {"residual": phase_ms[0] / args.steps, "patch_stage": phase_ms[1] / args.steps,
-                                  "potential_stage": phase_ms[2] / args.steps, "other": phase_ms[3] / args.steps,
-                                  "patch_kernel": phase_ms[4] / args.steps, "apply_kernel": phase_ms[5] / args.steps}}
+    phases = {"residual": phase_ms[0] / args.steps, "patch_stage": phase_ms[1] / args.steps,
+              "potential_stage": phase_ms[2] / args.steps, "other": phase_ms[3] / args.steps,
+              "patch_kernel": phase_ms[4] / args.steps, "apply_kernel": phase_ms[5] / args.steps}
+    roof_patch = {"kernel": "patch_stream_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                  "frac": achieved / hbm, "traffic": ncu_traffic(args.config), "peak_kind": peak_kind,
+                  "bytes_per_launch": prim_bytes / k_launch_sweep, "launch_ms_avg": k_ms_sweep / k_launch_sweep,
+                  "share_of_step": k_ms_sweep / ms if ms > 0 else None, "phase_ms_per_step": phases}
+    roof = roof_patch
+    a_ms = phase_ms[5] / args.steps
+    if wg.perturb > 0 and a_ms > 0:
+        ncell_loc = wg.nx * wg.ny * (n // ((wg.nx * wg.p + 1) * (wg.ny * wg.p + 1)) // wg.p)
+        flops = ncell_loc * TRI_FLOPS_PER_CELL
+        tf = flops / (a_ms * 1e-3) / 1e12
+        roof_apply = {"kernel": "apply_tri_kernel", "bound": "fp64", "achieved": tf, "peak": FP64_PEAK_TFLOPS,
+                      "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "traffic": None,
+                      "peak_kind": "measured DMMA m8n8k4 f64 throughput (scripts/fp64_bench.cu)",
+                      "flops_per_launch": flops, "launch_ms_avg": a_ms,
+                      "share_of_step": a_ms / ms if ms > 0 else None, "phase_ms_per_step": phases}
+        if a_ms > k_ms_sweep:
+            roof, roof_patch = roof_apply, dict(roof_patch)
+            roof["secondary"] = {k: roof_patch[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac",
+                                                             "launch_ms_avg", "share_of_step")}
+        else:
+            roof["secondary"] = {k: roof_apply[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac",
+                                                             "launch_ms_avg", "share_of_step")}
 
     e2e = None
     if not args.no_e2e:
