@@ -188,14 +188,15 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
       q2[pl] = QQ[(pl * 2 + 1) * SZ_Q + lx * XS_Q + ly];
     }
 #pragma unroll 4
-    for (int z = 0; z < K1; ++z) {
-      double o = OUT[z * 256 + swu(lx, ly)];
+    for (int z = 0; z < K1; ++z) {   // two independent partial sums per z (short dependency chains)
+      double ts = 0.0, td = 0.0;
 #pragma unroll
       for (int pl = 0; pl < ZB; ++pl) {
         const int zq = b * ZB + pl;
-        o = fma(SG[zq * K1 + z], q1[pl], fma(DG[zq * K1 + z], q2[pl], o));
+        ts = fma(SG[zq * K1 + z], q1[pl], ts);
+        td = fma(DG[zq * K1 + z], q2[pl], td);
       }
-      OUT[z * 256 + swu(lx, ly)] = o;
+      OUT[z * 256 + swu(lx, ly)] += ts + td;
     }
   };
 
