@@ -120,6 +120,9 @@ rm_status rm_partition(const rm_mesh *mesh, int32_t p, rm_space space, uint32_t 
                        int32_t nranks, rm_partition_info *info);
 /* 128-byte ncclUniqueId for options.nccl_id (rank 0 creates it, the caller broadcasts it). */
 rm_status rm_nccl_unique_id(void *id128);
+/* Diagnostic: loads NCCL, builds a one-rank communicator on `device`, runs a grouped send/recv to
+ * itself and an allreduce on a stream and checks the data (RM_ENCCL on any failure). */
+rm_status rm_nccl_check(int32_t device);
 
 /* Builds the 1D FDM tables, the structured layout, all patch factors and uploads them.
  * alpha, beta: host arrays, n == 1 (constant) or one value per cell, C-order [z][y][x]. */

@@ -93,6 +93,7 @@ def _load():
     lib.rm_relax_end.argtypes = [P, P, P, P, D]
     lib.rm_partition.argtypes = [ctypes.POINTER(rm_mesh), I32, I32, U32, I32, I32, ctypes.POINTER(rm_partition_info)]
     lib.rm_nccl_unique_id.argtypes = [P]
+    lib.rm_nccl_check.argtypes = [I32]
     lib.rm_pcg.argtypes = [P, P, P, D, I32, ctypes.POINTER(I32), ctypes.POINTER(D)]
     lib.rm_timing_enable.argtypes = [P, I32]
     lib.rm_timing_read.argtypes = [P, ctypes.POINTER(D * RM_NPHASE), ctypes.POINTER(I64 * RM_NPHASE)]
@@ -101,7 +102,7 @@ def _load():
     lib.rm_last_error.restype = ctypes.c_char_p
     for f in ("rm_setup", "rm_layout", "rm_info_get", "rm_constrained_mask", "rm_apply", "rm_residual",
               "rm_relax", "rm_precondition", "rm_relax_host", "rm_pcg", "rm_timing_enable", "rm_timing_read",
-              "rm_relax_begin", "rm_relax_end", "rm_partition", "rm_nccl_unique_id"):
+              "rm_relax_begin", "rm_relax_end", "rm_partition", "rm_nccl_unique_id", "rm_nccl_check"):
         getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -175,6 +176,11 @@ def rm_partition(nx, ny, nz, p, space, gamma_d, rank, nranks, z_begin, z_end) ->
     info = rm_partition_info()
     _check(_lib.rm_partition(ctypes.byref(mesh), p, space, gamma_d, rank, nranks, ctypes.byref(info)))
     return info.as_dict()
+
+
+def rm_nccl_check(device=0):
+    """Diagnostic of the NCCL transport on one device (include/rm.h)."""
+    _check(_lib.rm_nccl_check(int(device)))
 
 
 def rm_nccl_unique_id() -> bytes:

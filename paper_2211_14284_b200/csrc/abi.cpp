@@ -499,6 +499,43 @@ rm_status rm_partition(const rm_mesh* mesh, int32_t p, rm_space space, uint32_t 
   }
 }
 
+rm_status rm_nccl_check(int32_t device) {
+  // one-rank communicator on `device`: grouped send/recv to self and an in-place allreduce on a
+  // stream, results checked on the host (the transport calls rm_relax uses with nranks > 1)
+  try {
+    CK(cudaSetDevice(device));
+    const NcclApi& N = nccl();
+    ncclUniqueId id;
+    NK(N.get_id(&id));
+    ncclComm_t comm = nullptr;
+    NK(N.init(&comm, 1, id, 0));
+    cudaStream_t st;
+    CK(cudaStreamCreate(&st));
+    const int n = 4096;
+    std::vector<double> h(n), back(n);
+    for (int i = 0; i < n; ++i) h[i] = 0.5 * i - 7.0;
+    double *a = nullptr, *b = nullptr;
+    CK(cudaMalloc(&a, n * sizeof(double)));
+    CK(cudaMalloc(&b, n * sizeof(double)));
+    CK(cudaMemcpy(a, h.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemset(b, 0, n * sizeof(double)));
+    NK(N.gstart());
+    NK(N.send(a, n, ncclDouble, 0, comm, st));
+    NK(N.recv(b, n, ncclDouble, 0, comm, st));
+    NK(N.gend());
+    NK(N.allreduce(b, b, n, ncclDouble, ncclSum, comm, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(back.data(), b, n * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(a); cudaFree(b); cudaStreamDestroy(st);
+    if (N.destroy) N.destroy(comm);
+    for (int i = 0; i < n; ++i)
+      if (back[i] != h[i]) throw RmError(RM_ENCCL, "NCCL self send/recv returned wrong data");
+    return RM_OK;
+  } catch (const RmError& e) {
+    return fail(e);
+  }
+}
+
 rm_status rm_nccl_unique_id(void* id128) {
   try {
     if (!id128) throw RmError(RM_EINVAL, "null argument");

@@ -235,3 +235,12 @@ def test_slab_partition_two_contexts(dev, name, w):
         got = uo[own].cpu().numpy()
         want = ref[g0:g0 + ctxs[g].n_local][own].cpu().numpy()
         assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max()), (name, g)
+
+
+@pytest.mark.gpu
+def test_nccl_transport_self_check(dev):
+    """The NCCL entry points rm_relax uses with nranks > 1 (dlopen, unique id, communicator,
+    grouped send/recv, allreduce on a stream), exercised on one device with a one-rank comm."""
+    import paper_2211_14284_b200 as rmb
+    rmb.rm_nccl_check(torch.cuda.current_device())
+    assert len(rmb.rm_nccl_unique_id()) == 128
