@@ -257,6 +257,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
       throw RmError(RM_ENOMEM, "cudaMalloc failed (padded r / c)");
     F.allocs.push_back(a); F.allocs.push_back(b);
     Lh.rpad = static_cast<double*>(a); Lh.cpad = static_cast<double*>(b);
+    // the pad column of rpad stays zero when the apply writes the residual there directly
+    CK(cudaMemset(Lh.rpad, 0, po2 * sizeof(double)));
   }
   Lh.npatch = (int)np;
   // tile warps joining the ICC solve (measured slower: more ring walkers), opt-in experiment
@@ -845,34 +847,39 @@ struct Phase {
   }
 };
 
-void do_apply(rm_ctx* c, const double* u, const double* f, double* out) {
+// out = f - A u (or A u); ldx > 0 (k = 0): out in the padded layout with x-stride ldx
+void do_apply(rm_ctx* c, const double* u, const double* f, double* out, long long ldx = 0) {
   Phase ph(c, 0);
   int nl = 0;
   KPhase kp{c, 5};
   const rm::KTimer kt = kp.timer();
   if (c->cartesian) {
+    c->op.ldx_out = ldx;
     CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl,
                                   &kt));
+    c->op.ldx_out = 0;
   } else {
+    c->tri.ldx_out = ldx;
     CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, f, out,
                                   f ? -1.0 : 1.0, c->d_cellbuf, c->st, &nl, &kt));
+    c->tri.ldx_out = 0;
   }
   c->launches[0] += nl;
 }
 
-int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega) {
+int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega, bool r_padded = false) {
   if (F.npatch == 0) return 0;
   KPhase kp{c, 4};
   const rm::KTimer kt = kp.timer();
-  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt));
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded));
   return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)
-void add_precond(rm_ctx* c, const double* r, double* u, double omega) {
+void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false) {
   {
     Phase ph(c, 1);
-    c->launches[1] += run_family(c, c->prim, r, u, omega);
+    c->launches[1] += run_family(c, c->prim, r, u, omega, r_padded);
   }
   if (c->pot.present) {
     Phase ph(c, 2);
@@ -967,6 +974,14 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
     reverse_add(c, c->d_c);
     if (u_out != uh) CK(cudaMemcpyAsync(u_out, uh, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(rm::launch_axpby(c->ndof, omega, c->d_c, 1.0, u_out, c->st));
+    return;
+  }
+  if (c->k == 0 && !c->pot.present && c->prim.npatch > 0) {
+    // the residual goes straight into the primary family's padded (TMA) layout: no pad pass
+    const rm::PatchLaunch& L = c->prim.launch;
+    do_apply(c, u_in, f, L.rpad, L.pad.lxp[0]);
+    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    add_precond(c, L.rpad, u_out, omega, true);
     return;
   }
   do_apply(c, u_in, f, c->d_r);

@@ -36,7 +36,8 @@ __global__ void apply_init_kernel(const __grid_constant__ OpParams op, const dou
   const long long idx[3] = {rr % Lx, (rr / Lx) % Ly, rr / (Lx * Ly)};
   bool con = false;
   for (int d = 0; d < 3; ++d) con |= cons_idx(op.fam[m][d], idx[d], (long long)op.n[d] * op.p, op.gamma_d, d);
-  out[g] = (con || !f) ? 0.0 : f[g];
+  const long long og = (op.ldx_out > 0 && op.ncomp == 1) ? (idx[2] * Ly + idx[1]) * op.ldx_out + idx[0] : g;
+  out[og] = (con || !f) ? 0.0 : f[g];
 }
 
 template <int WPB>
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
     cx = px + 2 * (int)(cw % ncx); cy = py + 2 * (int)((cw / ncx) % ncy); cz = pz + 2 * (int)(cw / ((long long)ncx * ncy));
   }
   const long long Lx = op.len[0][0], Ly = op.len[0][1];
+  const long long LDX = op.ldx_out > 0 ? op.ldx_out : Lx;   // output row stride (padded layout)
   const long long lastx = (long long)op.n[0] * P, lasty = (long long)op.n[1] * P, lastz = (long long)op.n[2] * P;
   if (valid) {
     for (int l = q; l < N3; l += N2) {
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
       for (int k = 0; k < N; ++k) {
         const long long iz = (long long)cz * P + k;
         if (cons_idx(FAMP, iz, lastz, op.gamma_d, 2)) continue;
-        out[(iz * Ly + iy) * Lx + ix] += sign * (y1[k] + sz * y2[k]);
+        out[(iz * Ly + iy) * LDX + ix] += sign * (y1[k] + sz * y2[k]);
       }
     }
   }

@@ -418,7 +418,8 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
       if (x == 0 || x == p || y == 0 || y == p || z == 0 || z == p) {
         ob[i] = v;
       } else {
-        const long long g = (((long long)cz * p + z) * tp.Ly + (long long)cy * p + y) * tp.Lx + (long long)cx * p + x;
+        const long long ldx = tp.ldx_out > 0 ? tp.ldx_out : tp.Lx;
+        const long long g = (((long long)cz * p + z) * tp.Ly + (long long)cy * p + y) * ldx + (long long)cx * p + x;
         out[g] = sign * v;
       }
     }
@@ -455,11 +456,12 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
       if (aa == 0 && cc > 0) { czv[nz] = cc - 1; azv[nz] = p; ++nz; }
       czv[nz] = cc; azv[nz] = aa; ++nz;
     }
-    const long long rbase = (long long)row * Lx;
+    const long long rbase = (long long)row * Lx;                                   // f (unpadded)
+    const long long obase = (long long)row * (tp.ldx_out > 0 ? tp.ldx_out : Lx);   // out (maybe padded)
     for (int gx = lane; gx < Lx; gx += 32) {
-      const long long g = rbase + gx;
+      const long long g = obase + gx;
       if (rcons || tri_cons(gx, tp.n[0] * p, tp.gamma_d, 0)) { out[g] = 0.0; continue; }
-      const double fv = f ? f[g] : 0.0;
+      const double fv = f ? f[rbase + gx] : 0.0;
       if (!rskel && gx % p != 0) { out[g] = fv + out[g]; continue; }   // cell interior
       int cxv[2], axv[2], nx = 0;
       int cc = gx / p; if (cc >= tp.n[0]) cc = tp.n[0] - 1;

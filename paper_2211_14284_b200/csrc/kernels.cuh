@@ -20,6 +20,7 @@ struct OpParams {
   int fam[3][3];                  // [comp][dir]
   long long len[3][3];            // [comp][dir] index lengths
   long long off[4];               // component offsets
+  long long ldx_out;              // k = 0: x-stride of the output (0 = len[0][0]; the padded TMA layout)
   unsigned gamma_d;
   OpTerm terms[RM_MAXTERMS];
   // k = 0: the two 1D matrices of the H(grad) operator, B-hat and A-hat = D-hat^T D-hat,
@@ -64,6 +65,7 @@ struct TriParams {
   int p, nq, n[3];
   long long Lx, Ly, Lz;
   unsigned gamma_d;
+  long long ldx_out;   // x-stride of the output (0 = Lx; the padded TMA layout)
 };
 // optional hooks around a launcher's main kernel (the ABI records CUDA events there for the
 // per-kernel timing phases of rm_timing_read)
@@ -150,8 +152,9 @@ struct PatchLaunch {
   unsigned long long* prof;   // RM_PROFILE=1 instrumentation counters (else null)
 };
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
+// r_padded: r is already in the padded layout L.rpad (the apply wrote it there): no pad pass
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt = nullptr);
+                               const KTimer* kt = nullptr, bool r_padded = false);
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;

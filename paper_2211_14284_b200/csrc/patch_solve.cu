@@ -915,12 +915,14 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
 }
 
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt) {
+                               const KTimer* kt, bool r_padded) {
   if (L.npatch <= 0) return cudaSuccess;
   const long long n = L.pad.off[L.pad.ncomp];
   cudaError_t e;
-  pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!r_padded) {
+    pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   ScGeom sg{};
   long long nface = 0, nint = 0;
   if (L.sc_dinv) {
