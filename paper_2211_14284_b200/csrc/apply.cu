@@ -24,6 +24,25 @@ __device__ __forceinline__ bool cons_idx(int fam, long long idx, long long last,
   return false;
 }
 
+// one component (k = 0): one row (y, z) per warp, grid-stride, 32-bit index math; out may be padded
+__global__ void apply_init_q_kernel(const __grid_constant__ OpParams op, const double* __restrict__ f,
+                                    double* __restrict__ out) {
+  const int Lx = (int)op.len[0][0], Ly = (int)op.len[0][1], Lz = (int)op.len[0][2];
+  const long long ldx = op.ldx_out > 0 ? op.ldx_out : Lx;
+  const int lane = threadIdx.x & 31;
+  const int nrow = Ly * Lz, wstride = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrow; row += wstride) {
+    const int y = row % Ly, z = row / Ly;
+    const bool rc = cons_idx(op.fam[0][1], y, (long long)op.n[1] * op.p, op.gamma_d, 1) ||
+                    cons_idx(op.fam[0][2], z, (long long)op.n[2] * op.p, op.gamma_d, 2);
+    const long long fb = (long long)row * Lx, ob = (long long)row * ldx;
+    for (int x = lane; x < Lx; x += 32) {
+      const bool con = rc || cons_idx(op.fam[0][0], x, (long long)op.n[0] * op.p, op.gamma_d, 0);
+      out[ob + x] = (con || !f) ? 0.0 : f[fb + x];
+    }
+  }
+}
+
 // out = f (or 0) with constrained entries zeroed
 __global__ void apply_init_kernel(const __grid_constant__ OpParams op, const double* __restrict__ f,
                                   double* __restrict__ out, long long ndof) {
@@ -306,7 +325,8 @@ cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, 
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt) {
-  apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
+  if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);
+  else apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
   int nl = 1;
   if (kt) kt->begin(kt->arg);
   struct End {
