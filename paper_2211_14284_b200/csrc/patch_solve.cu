@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   Consumer cn{chan_sm(smraw, 0), ringA, 0, 0, nullptr, nullptr};
   unsigned long long sp_box = 0, sp_x = 0, sp_fwd = 0, sp_bwd = 0, sp0 = prof ? clock64() : 0;
   const bool pf = prof != nullptr && tid == 0;
+  unsigned long long sp_acq = 0, sp_piv = 0, sp_w = 0, sp_sync = 0;
   const int ncw = icc_only ? NC + NTW : NC, nct = 32 * ncw;   // consumer warps / threads
   auto csync_n = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory"); };
   auto forward = [&](int i) {
@@ -561,7 +562,9 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       const int bs = L.blk.bs;
       // y^_E = L^{-T} L^{-1} v_E in place (pivot blocks <= 3x3, diagonal stored inverted)
       for (int pi = L.piv_b; pi < L.w_b; ++pi) {
+        unsigned long long tq = pf ? clock64() : 0;
         const Piece_ pc = cn.acquire();
+        if (pf) { const unsigned long long t2 = clock64(); sp_acq += t2 - tq; tq = t2; }
         const Hdr h = hdr(pc.pb);
         const uint16_t* mem = reinterpret_cast<const uint16_t*>(pc.pb + 16);
         const double* pv = pc.val;
@@ -594,14 +597,18 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
           v[m0] = y0 * l00;
         }
         cn.release(lane);
+        if (pf) sp_piv += clock64() - tq;
       }
-      csync_n();
+      { const unsigned long long tq = pf ? clock64() : 0; csync_n(); if (pf) sp_sync += clock64() - tq; }
       for (int pi = L.w_b; pi < L.w_e; ++pi) {
+        unsigned long long tq = pf ? clock64() : 0;
         const Piece_ pc = cn.acquire();
+        if (pf) { const unsigned long long t2 = clock64(); sp_acq += t2 - tq; tq = t2; }
         sliced_piece(pc, v, L.w.nrows, warp, lane, [&](int rb, double acc) { v[rb] -= acc; });
         cn.release(lane);
+        if (pf) sp_w += clock64() - tq;
       }
-      csync_n();
+      { const unsigned long long tq = pf ? clock64() : 0; csync_n(); if (pf) sp_sync += clock64() - tq; }
     }
     __syncwarp();
     if (lane == 0 && !icc_only) mbar_arrive(&gready[b]);   // the tile warps may read v_F
@@ -700,6 +707,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
   if (pf) {
     unsigned long long* o = prof + 24 * blockIdx.x;
     o[7] = clock64() - sp0; o[8] = sp_box; o[9] = sp_x; o[10] = sp_fwd; o[11] = sp_bwd;
+    o[16] = sp_acq; o[17] = sp_piv; o[18] = sp_w; o[19] = sp_sync;
 
   }
 }
@@ -980,8 +988,9 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     fprintf(stderr,
             "[rm prof kcyc] producer total %.0f idle %.0f | store total %.0f wait-done %.0f colour %.0f | tiles total %.0f "
             "wait-fwd %.0f | sparse total %.0f box-wait %.0f x-wait %.0f fwd %.0f bwd %.0f | prodA total %.0f room-wait %.0f "
-            "| prodB total %.0f room-wait %.0f\n",
-            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15]);
+            "| prodB total %.0f room-wait %.0f | fwd: acquire %.0f piv %.0f w %.0f sync %.0f\n",
+            a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15],
+            a[16], a[17], a[18], a[19]);
   }
   if (L.sc_dinv && nint > 0 && !getenv("RM_DEBUG_SC_NOPOST")) {
     sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
