@@ -877,7 +877,7 @@ cudaError_t encode_maps(PatchLaunch& L) {
 cudaError_t plan_patch_solve(PatchLaunch& L) {
   const size_t boxd = (size_t)((L.box_total + 15) & ~15);
   // three box buffers (patches i-1, i, i+1 in flight) when they fit, else two
-  L.nbox = NBOX;
+  L.nbox = getenv("RM_NBOX2") ? 2 : NBOX;   // experiments: two box buffers, more ring
   L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -910,7 +910,6 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if (occ < 1) return cudaErrorInvalidConfiguration;
   L.grid = std::max(1, std::min(L.npatch, occ * nsm));
   if (const char* g = getenv("RM_GRID")) L.grid = std::max(1, std::min(L.grid, atoi(g)));   // experiments
-  if (getenv("RM_NBOX2")) L.nbox = 2;
   if ((e = encode_maps(L)) != cudaSuccess) return e;
   if (getenv("RM_PROFILE") && !L.prof && (e = cudaMalloc(&L.prof, (size_t)24 * 8 * L.grid)) != cudaSuccess) return e;
   // descriptors live in global memory (64-byte aligned allocation), read by the TMA unit
