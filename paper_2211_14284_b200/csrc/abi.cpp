@@ -662,6 +662,11 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
       c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
+    } else if (space == 0 && getenv("RM_APPLY_CELLBUF")) {
+      // Cartesian H(grad), opt-in: one apply launch over all cells, interior DoFs stored directly,
+      // skeleton entries through the cell buffer and the gather (measured: apply 0.28 -> 0.19 ms at
+      // cfg2, but the gather costs what the colours and the init cost; the residual phase is equal)
+      c->d_cellbuf = c->dalloc((size_t)c->n[0] * c->n[1] * c->n[2] * (p + 1) * (p + 1) * (p + 1));
     }
     // ---- device operator
     c->op = make_op(c->sp, gamma_d);
@@ -856,7 +861,7 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out, long lon
   if (c->cartesian) {
     c->op.ldx_out = ldx;
     CK(rm::launch_apply_cartesian(c->op, c->d_alpha, c->d_beta, c->coef_const, c->d_hpow, u, f, out, c->ndof, c->st, &nl,
-                                  &kt));
+                                  &kt, c->d_cellbuf));
     c->op.ldx_out = 0;
   } else {
     c->tri.ldx_out = ldx;

@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
                                                        const double* __restrict__ beta, int coef_const,
                                                        const double* __restrict__ hpow,
                                                        const double* __restrict__ u, double* __restrict__ out,
-                                                       double sign, int px, int py, int pz) {
+                                                       double sign, int px, int py, int pz,
+                                                       double* __restrict__ cellbuf) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
   extern __shared__ double sm[];
@@ -218,12 +219,17 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
   const int cs = tid / N2, q = tid % N2;
   double* A = sm + cs * 2 * N3;
   double* Bf = A + N3;
-  const int ncx = (op.n[0] - px + 1) / 2, ncy = (op.n[1] - py + 1) / 2, ncz = (op.n[2] - pz + 1) / 2;
+  // colour mode: the cells of parity (px, py, pz), out += sign A_K u; cell-buffer mode (cellbuf):
+  // every cell, interior DoFs stored as sign A_K u, skeleton entries to cellbuf (summed by the gather)
+  const int ncx = cellbuf ? op.n[0] : (op.n[0] - px + 1) / 2, ncy = cellbuf ? op.n[1] : (op.n[1] - py + 1) / 2,
+            ncz = cellbuf ? op.n[2] : (op.n[2] - pz + 1) / 2;
+  const int cstep = cellbuf ? 1 : 2, ox = cellbuf ? 0 : px, oy = cellbuf ? 0 : py, oz = cellbuf ? 0 : pz;
   const long long cw = (long long)blockIdx.x * CPB + cs;
   const bool valid = cw < (long long)ncx * ncy * ncz;
   int cx = 0, cy = 0, cz = 0;
   if (valid) {
-    cx = px + 2 * (int)(cw % ncx); cy = py + 2 * (int)((cw / ncx) % ncy); cz = pz + 2 * (int)(cw / ((long long)ncx * ncy));
+    cx = ox + cstep * (int)(cw % ncx); cy = oy + cstep * (int)((cw / ncx) % ncy);
+    cz = oz + cstep * (int)(cw / ((long long)ncx * ncy));
   }
   const long long Lx = op.len[0][0], Ly = op.len[0][1];
   const long long LDX = op.ldx_out > 0 ? op.ldx_out : Lx;   // output row stride (padded layout)
@@ -281,6 +287,17 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
     apply_B<P>(op.Bh, x, y1);
     apply_A<P>(op.Ah, Qv, y2);
     const long long ix = (long long)cx * P + a, iy = (long long)cy * P + b;
+    if (cellbuf) {
+      double* cb = cellbuf + (long long)((cz * op.n[1] + cy) * op.n[0] + cx) * N3 + b * N + a;
+      const bool skel_ab = a == 0 || a == P || b == 0 || b == P;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double vv = y1[k] + sz * y2[k];
+        if (skel_ab || k == 0 || k == P) cb[k * N2] = vv;
+        else out[(((long long)cz * P + k) * Ly + iy) * LDX + ix] = sign * vv;
+      }
+      return;
+    }
     const bool conxy = cons_idx(FAMP, ix, lastx, op.gamma_d, 0) || cons_idx(FAMP, iy, lasty, op.gamma_d, 1);
     if (!conxy) {
 #pragma unroll
@@ -295,7 +312,8 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
 
 template <int P>
 static cudaError_t launch_q(const OpParams& op, const double* alpha, const double* beta, int coef_const,
-                            const double* hpow, const double* u, double* out, double sign, cudaStream_t st, int& nl) {
+                            const double* hpow, const double* u, double* out, double sign, cudaStream_t st, int& nl,
+                            double* cellbuf) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
   const size_t smem = (size_t)CPB * 2 * N3 * sizeof(double);
@@ -305,13 +323,21 @@ static cudaError_t launch_q(const OpParams& op, const double* alpha, const doubl
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  if (cellbuf) {   // one launch over every cell (the skeleton gather follows)
+    const long long ncell = (long long)op.n[0] * op.n[1] * op.n[2];
+    apply_q_kernel<P><<<(unsigned)((ncell + CPB - 1) / CPB), CPB * N2, smem, st>>>(op, alpha, beta, coef_const, hpow, u,
+                                                                                  out, sign, 0, 0, 0, cellbuf);
+    ++nl;
+    return cudaGetLastError();
+  }
   for (int pz = 0; pz < 2; ++pz)
     for (int py = 0; py < 2; ++py)
       for (int px = 0; px < 2; ++px) {
         const long long ncell = (long long)((op.n[0] - px + 1) / 2) * ((op.n[1] - py + 1) / 2) * ((op.n[2] - pz + 1) / 2);
         if (ncell <= 0) continue;
         const unsigned grid = (unsigned)((ncell + CPB - 1) / CPB);
-        apply_q_kernel<P><<<grid, CPB * N2, smem, st>>>(op, alpha, beta, coef_const, hpow, u, out, sign, px, py, pz);
+        apply_q_kernel<P><<<grid, CPB * N2, smem, st>>>(op, alpha, beta, coef_const, hpow, u, out, sign, px, py, pz,
+                                                        nullptr);
         ++nl;
       }
   return cudaGetLastError();
@@ -324,10 +350,15 @@ cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, 
 
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
-                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt) {
-  if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);
-  else apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
-  int nl = 1;
+                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt,
+                                   double* cellbuf) {
+  const bool cb = cellbuf && op.k == 0;   // cell-buffer mode: no init, no colours, a gather at the end
+  int nl = 0;
+  if (!cb) {
+    if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);
+    else apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
+    nl = 1;
+  }
   if (kt) kt->begin(kt->arg);
   struct End {
     const KTimer* kt;
@@ -337,21 +368,32 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
     const double sgn = f ? -1.0 : 1.0;
     cudaError_t e;
     switch (op.p) {
-      case 1: e = launch_q<1>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 2: e = launch_q<2>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 3: e = launch_q<3>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 4: e = launch_q<4>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 5: e = launch_q<5>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 6: e = launch_q<6>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 7: e = launch_q<7>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 8: e = launch_q<8>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 9: e = launch_q<9>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 10: e = launch_q<10>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 11: e = launch_q<11>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 12: e = launch_q<12>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 13: e = launch_q<13>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      case 14: e = launch_q<14>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
-      default: e = launch_q<15>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl); break;
+      case 1: e = launch_q<1>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 2: e = launch_q<2>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 3: e = launch_q<3>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 4: e = launch_q<4>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 5: e = launch_q<5>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 6: e = launch_q<6>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 7: e = launch_q<7>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 8: e = launch_q<8>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 9: e = launch_q<9>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 10: e = launch_q<10>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 11: e = launch_q<11>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 12: e = launch_q<12>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 13: e = launch_q<13>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      case 14: e = launch_q<14>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+      default: e = launch_q<15>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
+    }
+    if (e == cudaSuccess && cb) {   // the apply kernel is timed alone (as on the trilinear path)
+      if (kt) { kt->end(kt->arg); end_.kt = nullptr; }
+      TriParams tp{};
+      tp.p = op.p;
+      for (int d = 0; d < 3; ++d) tp.n[d] = op.n[d];
+      tp.Lx = op.len[0][0]; tp.Ly = op.len[0][1]; tp.Lz = op.len[0][2];
+      tp.gamma_d = op.gamma_d;
+      tp.ldx_out = op.ldx_out;
+      e = launch_skeleton_gather(tp, cellbuf, f, out, sgn, st);
+      ++nl;
     }
     if (nlaunch) *nlaunch = nl;
     return e;

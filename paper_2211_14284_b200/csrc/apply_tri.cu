@@ -511,6 +511,19 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
   return cudaGetLastError();
 }
 
+cudaError_t launch_skeleton_gather(const TriParams& tp, const double* cellbuf, const double* f, double* out, double sign,
+                                   cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
+  return cudaGetLastError();
+}
+
 size_t tri_cellbuf_doubles(const TriParams& tp) {
   return (size_t)tp.n[0] * tp.n[1] * tp.n[2] * (tp.p + 1) * (tp.p + 1) * (tp.p + 1);
 }

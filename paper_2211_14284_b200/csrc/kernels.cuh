@@ -87,7 +87,12 @@ cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, 
 // launchers (kernels.cu)
 cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                                    const double* hpow, const double* u, const double* f, double* out,
-                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt = nullptr);
+                                   long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt = nullptr,
+                                   double* cellbuf = nullptr);
+// out = f + sign * (sum of the cell-buffer skeleton entries | the stored interior values), constrained 0
+// (the gather of the cell-buffer applies, apply_tri.cu)
+cudaError_t launch_skeleton_gather(const TriParams& tp, const double* cellbuf, const double* f, double* out, double sign,
+                                   cudaStream_t st);
 // Padded component layout of the patch kernel's input r and correction c: x rows padded to an
 // even length so that TMA tensor maps (row strides multiple of 16 bytes) can address them.
 struct PadLayout {
