@@ -352,8 +352,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
                                                                uint32_t capB, int box_total,
                                                                const XferEntry* __restrict__ xfer,
                                                                const long long* __restrict__ xbeg, int nbox,
-                                                               unsigned long long* __restrict__ prof, int dbg_q,
-                                                               double* __restrict__ dbg_out, int icc_only) {
+                                                               unsigned long long* __restrict__ prof, int icc_only) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* ringA = smraw + BAR_BYTES;
   unsigned char* ringB = ringA + capA;
@@ -549,13 +548,6 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     unsigned long long ta = pf ? clock64() : 0;
     mbar_wait(&vfull[b], (uint32_t)(i / nbox) & 1u);   // the window box of r has landed
     if (pf) { const unsigned long long tb = clock64(); sp_box += tb - ta; ta = tb; }
-    if (dbg_out && dbg_q == 2) {   // debug dump of every loaded box (experiments only)
-      csync_n();
-      double* d = dbg_out + (size_t)q * (box_total + 9);
-      for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
-      if (tid < 9) d[tid] = (double)porig[9 * q + tid];
-      csync_n();
-    }
     const int nlev = C.nlev;
     for (int l = 0; l < nlev; ++l) {
       const DLevel& L = C.lev[l];
@@ -686,13 +678,6 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       const uint16_t* zl = reinterpret_cast<const uint16_t*>(pc.pb + 16);
       for (int k = tid; k < h.a1 - h.a0; k += nct) v[zl[k]] = 0.0;
       cn.release(lane);
-    }
-    if (dbg_out && dbg_q == 1) {   // debug dump of every finished box (experiments only, RM_DEBUG_Q)
-      csync_n();
-      double* d = dbg_out + (size_t)q * (box_total + 9);
-      for (int k = tid; k < box_total; k += NT) d[9 + k] = v[k];
-      if (tid < 9) d[tid] = (double)porig[9 * q + tid];
-      csync_n();
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
     __syncwarp();
@@ -832,19 +817,6 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   cp[gi] = dv * (nk[K] * rp[gi] - s);
 }
 
-double* dbg_buf(int n) {   // experiments: box dump buffer (RM_DEBUG_Q)
-  static double* b = nullptr;
-  if (!getenv("RM_DEBUG_Q")) return nullptr;
-  if (!b) { cudaMalloc(&b, (size_t)(1 << 22) * 8); cudaMemset(b, 0, (size_t)(1 << 22) * 8); }
-  (void)n;
-  return b;
-}
-extern "C" __attribute__((visibility("default"))) int rm_debug_box(double* host, int n) {
-  double* b = dbg_buf(n);
-  if (!b) return -1;
-  return cudaMemcpy(host, b, (size_t)n * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : -2;
-}
-
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                                   const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -956,10 +928,6 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
   }
-  if (getenv("RM_DEBUG_SC_PRE")) {   // debug: u += omega * r_sc (the pre step only)
-    unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.rpad, u, omega, n);
-    return cudaGetLastError();
-  }
   if ((e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
   BoxGeom bg;
@@ -974,7 +942,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
       L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
       (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof,
-      getenv("RM_DEBUG_Q") ? atoi(getenv("RM_DEBUG_Q")) : -1, dbg_buf(L.box_total), L.icc_only);
+      L.icc_only);
   if (kt) kt->end(kt->arg);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
@@ -991,7 +959,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
             a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10], a[11], a[12], a[13], a[14], a[15],
             a[16], a[17], a[18], a[19]);
   }
-  if (L.sc_dinv && nint > 0 && !getenv("RM_DEBUG_SC_NOPOST")) {
+  if (L.sc_dinv && nint > 0) {
     sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -224,16 +224,9 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
       // ---- scatter: zero the non-patch box entries, TMA reduce-add of the boxes
       PieceView zw = view((int)C.pieces.size() - 1);
       for (int k = 0; k < zw.a1 - zw.a0; ++k) v[rd<uint16_t>(zw.pb + 16, k)] = 0.0;
-      if (getenv("RM_DEBUG_EMU_PATCH")) {   // experiments: append every finished box (porig + box) to a file
-        FILE* fo = fopen(getenv("RM_DEBUG_EMU_PATCH"), "a");
-        for (int k2 = 0; k2 < 9; ++k2) fprintf(fo, "%d ", F.porig[t * 9 + k2]);
-        for (int b2 = 0; b2 < F.box_total; ++b2) fprintf(fo, "%.17g ", v[b2]);
-        fprintf(fo, "\n");
-        fclose(fo);
-      }
       box_walk([&](int b, int64_t g) { z[g] += v[b]; });
     }
-  if (sc && !getenv("RM_DEBUG_SC_NOPOST"))
+  if (sc)
     for (int cz = 0; cz < sp.n[2]; ++cz)
       for (int cy = 0; cy < sp.n[1]; ++cy)
         for (int cx = 0; cx < sp.n[0]; ++cx) {
