@@ -58,10 +58,11 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(cfg):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one patch-kernel launch (= one sweep's patch
-    phase) from the committed ncu --set full summary of the same workload, or None."""
-    path = os.path.join(ROOT, "profiles", f"r01_ncu_patch_solve_cfg{cfg}.txt")
+def ncu_traffic(cfg, kernel="patch_solve"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of the kernel (patch_solve: the
+    persistent patch kernel; apply_tri: the trilinear apply) from the committed ncu --set full
+    summary of the same workload, or None."""
+    path = os.path.join(ROOT, "profiles", f"r01_ncu_{kernel}_cfg{cfg}.txt")
     try:
         vals = {}
         for line in open(path):
@@ -277,7 +278,7 @@ def main():
         flops = ncell_loc * TRI_FLOPS_PER_CELL
         tf = flops / (a_ms * 1e-3) / 1e12
         roof_apply = {"kernel": "apply_tri_kernel", "bound": "fp64", "achieved": tf, "peak": FP64_PEAK_TFLOPS,
-                      "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "traffic": None,
+                      "unit": "TFLOP/s", "frac": tf / FP64_PEAK_TFLOPS, "traffic": ncu_traffic(args.config, "apply_tri"),
                       "peak_kind": "measured DMMA m8n8k4 f64 throughput (scripts/fp64_bench.cu)",
                       "flops_per_launch": flops, "launch_ms_avg": a_ms,
                       "share_of_step": a_ms / ms if ms > 0 else None, "phase_ms_per_step": phases}
