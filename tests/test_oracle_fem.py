@@ -204,3 +204,38 @@ def test_hcurl_hdiv_mass_stiffness_scaling():
         K2 = element_matrix(k, p, unit_cell((0.5, 0.5, 0.5)), 1.0, 0.0)
         np.testing.assert_allclose(M2, M1 * 0.5 ** mexp, atol=1e-13 * np.abs(M1).max() * 8)
         np.testing.assert_allclose(K2, K1 * 0.5 ** kexp, atol=1e-12 * np.abs(K1).max() * 8)
+
+
+def test_aux_operator_on_a_sheared_affine_cell_equals_the_equivalent_box():
+    """Pin of the auxiliary operator beyond axis-aligned cells (eq:sum-factorization_approx,
+    P:732-739): on an AFFINE cell x = b + J xi with a non-diagonal J the metric is constant, so
+    P_K = alpha |J| sum_m (J^-1 J^-T)_mm S_m + beta |J| M (only the metric's diagonal enters).  That
+    is exactly the TRUE operator of the axis-aligned box with half-sizes j_m = (J^-1 J^-T)_mm^(-1/2)
+    and coefficients (alpha, beta) |J| / prod(j), computed through the independent element_matrix
+    path (itself pinned by closed forms above).  Using J^T J instead of J^-1 J^-T, a transposed J or a
+    misplaced weight fails this."""
+    import numpy as np
+    from oracle.fem import aux_element_matrix, element_matrix
+    p, alpha, beta = 3, 1.7, 0.6
+    J = np.array([[0.30, 0.05, -0.02], [0.04, 0.25, 0.06], [-0.03, 0.02, 0.20]])
+    b = np.array([0.5, 0.4, 0.3])
+    Xc = np.zeros((2, 2, 2, 3))
+    for az in range(2):
+        for ay in range(2):
+            for ax in range(2):
+                Xc[az, ay, ax] = b + J @ np.array([2 * ax - 1, 2 * ay - 1, 2 * az - 1], dtype=float)
+    G = np.linalg.inv(J) @ np.linalg.inv(J).T
+    d = abs(np.linalg.det(J))
+    jm = 1.0 / np.sqrt(np.diag(G))
+    Xb = np.zeros((2, 2, 2, 3))
+    for az in range(2):
+        for ay in range(2):
+            for ax in range(2):
+                Xb[az, ay, ax] = np.array([2 * ax - 1, 2 * ay - 1, 2 * az - 1], dtype=float) * jm
+    s = d / np.prod(jm)
+    P = aux_element_matrix(p, Xc, alpha, beta)
+    A = element_matrix(0, p, Xb, alpha * s, beta * s)
+    assert np.abs(P - A).max() <= 1e-12 * np.abs(A).max()
+    # and the true operator of the sheared cell is NOT this (the off-diagonal metric matters)
+    At = element_matrix(0, p, Xc, alpha, beta)
+    assert np.abs(At - A).max() > 1e-3 * np.abs(A).max()
