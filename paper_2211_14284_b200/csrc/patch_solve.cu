@@ -50,6 +50,7 @@ namespace {
 constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // sparse warps
 constexpr int NT = NC * 32;
 constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps
+constexpr int kIccChunksDev = 4;   // = kIccChunks (patches.hpp): chunks per ICC piece
 constexpr int WT0 = NC, WPROD_A = NC + NTW, WPROD_B = NC + NTW + 1, WSTORE = NC + NTW + 2;
 constexpr int NTHR = 32 * (NC + NTW + 3);
 constexpr int NDESC = 16;                      // in-flight transfer units per channel
@@ -627,9 +628,12 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
             const Piece_ pc = cn.acquire();
             // multi-chunk ICC piece (patches.cpp): chunk c (<= 32 rows, lane-interleaved) is
             // taken by consumer warp c; one header and one table entry per warp and piece
+            // chunk c of the level's piece k is taken by warp c + kIccChunks (k % groups): several
+            // pieces in work at once (and in flight in the ring)
             const Hdr h = hdr(pc.pb);
-            if (warp < h.a1 - h.a0) {
-              const int4 ent = reinterpret_cast<const int4*>(pc.pb + 16)[warp];   // cnt, L, meta, values
+            const int ch = warp - kIccChunksDev * ((pi - lp[l]) % (NC / kIccChunksDev));
+            if (ch >= 0 && ch < h.a1 - h.a0) {
+              const int4 ent = reinterpret_cast<const int4*>(pc.pb + 16)[ch];   // cnt, L, meta, values
               const int cnt = ent.x, Lm = ent.y;
               if (lane < cnt) {
                 const uint16_t* rows = reinterpret_cast<const uint16_t*>(pc.pb + ent.z);

@@ -384,13 +384,13 @@ void build_stream(ClassProgram& C) {
             }
           }
         }
-        // pieces of <= kIccChunks consecutive chunks and <= 4 kPieceMax values (chunk c -> warp c)
+        // pieces of <= kIccChunks consecutive chunks and <= kIccPieceVals values (one chunk may exceed it)
         for (int c = ch0; c < (int)chunks.size();) {
           const int c0 = c;
           int nd = 0;
           while (c < (int)chunks.size() && c - c0 < kIccChunks) {
             const int cd = 32 + 32 * chunks[c].L;
-            if (c > c0 && nd + cd > 4 * kPieceMax) break;
+            if (c > c0 && nd + cd > kIccPieceVals) break;
             nd += cd;
             ++c;
           }

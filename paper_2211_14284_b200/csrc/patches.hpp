@@ -66,7 +66,11 @@ enum FinalKind { FINAL_DENSE_INV = 0, FINAL_ICC = 1 };
 enum PieceKind { PK_PIV = 0, PK_W = 1, PK_TILE = 2, PK_ICCF = 3, PK_ICCB = 4, PK_WT = 5, PK_FINAL = 6, PK_ZERO = 7 };
 constexpr int kPieceMax = 2048;      // doubles (16 KB) of values per piece
 constexpr int kIccRows = 32;      // rows per ICC chunk: one row per lane of the warp that takes it
-constexpr int kIccChunks = 8;     // chunks per ICC piece: chunk c is taken by sparse warp c
+// chunks per ICC piece: chunk c of the level's piece k -> warp c + kIccChunks (k % (8 / kIccChunks));
+// measured on cfg5 (chunks / value cap -> patch kernel): 8 / 8192 -> 1.34 ms, 4 / 4096 -> 1.27 ms,
+// 2 / 2048 -> 1.56 ms (ring prefetch depth vs. number of piece headers walked)
+constexpr int kIccChunks = 4;
+constexpr int kIccPieceVals = 4096;   // values per ICC piece (several pieces in flight in the ring)
 struct IccChunk { int r0, cnt, L, sofs; };   // level-ordered rows [r0, r0+cnt), longest off-diag row, slot offset
 constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
 // Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
