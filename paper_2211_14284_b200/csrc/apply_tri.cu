@@ -433,48 +433,59 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
 // row (gy, gz), grid-stride over rows; 32-bit index math.
 __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                   const double* __restrict__ f, double* __restrict__ out, double sign) {
+  // per-x table (once per block): the (<= 2) cells containing gx and the local indices, skeleton
+  // and constraint flags; per row the (<= 2 x 2) (cell-row, local) bases; every loop has constant
+  // bounds (registers, no local memory) and one table lookup replaces the per-DoF divisions
+  __shared__ int4 xtab[1024];   // (cell0, local0, cell1, local1); local1 < 0: one cell
+  __shared__ unsigned char xfl[1024];   // bit0: on a cell boundary, bit1: constrained
   const int Lx = (int)tp.Lx, Ly = (int)tp.Ly, Lz = (int)tp.Lz;
   const int p = tp.p, P1 = p + 1, n3 = P1 * P1 * P1;
+  for (int gx = threadIdx.x; gx < Lx; gx += blockDim.x) {
+    int cc = gx / p;
+    if (cc >= tp.n[0]) cc = tp.n[0] - 1;
+    const int aa = gx - cc * p;
+    xtab[gx] = (aa == 0 && cc > 0) ? make_int4(cc - 1, p, cc, 0) : make_int4(cc, aa, 0, -1);
+    xfl[gx] = (unsigned char)((aa == 0 || aa == p ? 1 : 0) | (tri_cons(gx, (long long)tp.n[0] * p, tp.gamma_d, 0) ? 2 : 0));
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int nrow = Ly * Lz;
-  const int wstride = gridDim.x * (blockDim.x >> 5);
+  const int nrow = Ly * Lz, wstride = gridDim.x * (blockDim.x >> 5);
+  const long long ldx = tp.ldx_out > 0 ? tp.ldx_out : Lx;
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrow; row += wstride) {
     const int gy = row % Ly, gz = row / Ly;
-    const bool rcons = tri_cons(gy, tp.n[1] * p, tp.gamma_d, 1) || tri_cons(gz, tp.n[2] * p, tp.gamma_d, 2);
-    const bool rskel = (gy % p == 0) || (gz % p == 0);
-    // cells and local indices along y and z of this row
-    int cyv[2], ayv[2], ny = 0, czv[2], azv[2], nz = 0;
+    const bool rcons = tri_cons(gy, (long long)tp.n[1] * p, tp.gamma_d, 1) || tri_cons(gz, (long long)tp.n[2] * p, tp.gamma_d, 2);
+    int cy0, ay0, cy1 = 0, ay1 = -1, cz0, az0, cz1 = 0, az1 = -1;
     {
       int cc = gy / p; if (cc >= tp.n[1]) cc = tp.n[1] - 1;
       const int aa = gy - cc * p;
-      if (aa == 0 && cc > 0) { cyv[ny] = cc - 1; ayv[ny] = p; ++ny; }
-      cyv[ny] = cc; ayv[ny] = aa; ++ny;
+      if (aa == 0 && cc > 0) { cy0 = cc - 1; ay0 = p; cy1 = cc; ay1 = 0; } else { cy0 = cc; ay0 = aa; }
     }
     {
       int cc = gz / p; if (cc >= tp.n[2]) cc = tp.n[2] - 1;
       const int aa = gz - cc * p;
-      if (aa == 0 && cc > 0) { czv[nz] = cc - 1; azv[nz] = p; ++nz; }
-      czv[nz] = cc; azv[nz] = aa; ++nz;
+      if (aa == 0 && cc > 0) { cz0 = cc - 1; az0 = p; cz1 = cc; az1 = 0; } else { cz0 = cc; az0 = aa; }
     }
-    const long long rbase = (long long)row * Lx;                                   // f (unpadded)
-    const long long obase = (long long)row * (tp.ldx_out > 0 ? tp.ldx_out : Lx);   // out (maybe padded)
+    const bool rskel = ay0 == 0 || ay0 == p || az0 == 0 || az0 == p;
+    // (cell-row base, local-row offset) of the (kz, ky) combinations; valid flags
+    const int rb00 = (cz0 * tp.n[1] + cy0) * tp.n[0], ro00 = (az0 * P1 + ay0) * P1;
+    const int rb01 = (cz0 * tp.n[1] + cy1) * tp.n[0], ro01 = (az0 * P1 + ay1) * P1;
+    const int rb10 = (cz1 * tp.n[1] + cy0) * tp.n[0], ro10 = (az1 * P1 + ay0) * P1;
+    const int rb11 = (cz1 * tp.n[1] + cy1) * tp.n[0], ro11 = (az1 * P1 + ay1) * P1;
+    const bool v01 = ay1 >= 0, v10 = az1 >= 0, v11 = v01 && v10;
+    const long long fbase = (long long)row * Lx, obase = (long long)row * ldx;
     for (int gx = lane; gx < Lx; gx += 32) {
       const long long g = obase + gx;
-      if (rcons || tri_cons(gx, tp.n[0] * p, tp.gamma_d, 0)) { out[g] = 0.0; continue; }
-      const double fv = f ? f[rbase + gx] : 0.0;
-      if (!rskel && gx % p != 0) { out[g] = fv + out[g]; continue; }   // cell interior
-      int cxv[2], axv[2], nx = 0;
-      int cc = gx / p; if (cc >= tp.n[0]) cc = tp.n[0] - 1;
-      const int aa = gx - cc * p;
-      if (aa == 0 && cc > 0) { cxv[nx] = cc - 1; axv[nx] = p; ++nx; }
-      cxv[nx] = cc; axv[nx] = aa; ++nx;
-      double s = 0.0;
-      for (int kz = 0; kz < nz; ++kz)
-        for (int ky = 0; ky < ny; ++ky)
-          for (int kx = 0; kx < nx; ++kx) {
-            const int cell = (czv[kz] * tp.n[1] + cyv[ky]) * tp.n[0] + cxv[kx];
-            s += cellbuf[(size_t)cell * n3 + (azv[kz] * P1 + ayv[ky]) * P1 + axv[kx]];
-          }
+      const int fl = xfl[gx];
+      if (rcons || (fl & 2)) { out[g] = 0.0; continue; }
+      const double fv = f ? f[fbase + gx] : 0.0;
+      if (!rskel && !(fl & 1)) { out[g] = fv + out[g]; continue; }   // cell interior (stored by the apply)
+      const int4 xe = xtab[gx];
+      auto at = [&](int rb, int ro, int c, int a) { return cellbuf[(size_t)(rb + c) * n3 + ro + a]; };
+      double s = at(rb00, ro00, xe.x, xe.y);
+      if (xe.w >= 0) s += at(rb00, ro00, xe.z, xe.w);
+      if (v01) { s += at(rb01, ro01, xe.x, xe.y); if (xe.w >= 0) s += at(rb01, ro01, xe.z, xe.w); }
+      if (v10) { s += at(rb10, ro10, xe.x, xe.y); if (xe.w >= 0) s += at(rb10, ro10, xe.z, xe.w); }
+      if (v11) { s += at(rb11, ro11, xe.x, xe.y); if (xe.w >= 0) s += at(rb11, ro11, xe.z, xe.w); }
       out[g] = fv + sign * s;
     }
   }
@@ -490,7 +501,7 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (tp.p + 1 > K1 || tp.nq > NQP) return cudaErrorInvalidValue;
+  if (tp.p + 1 > K1 || tp.nq > NQP || tp.Lx > 1024) return cudaErrorInvalidValue;
   const long long ncell = (long long)tp.n[0] * tp.n[1] * tp.n[2];
   const long long nd = tp.Lx * tp.Ly * tp.Lz;
   if (ncell <= 0) return cudaSuccess;
@@ -513,6 +524,7 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
 
 cudaError_t launch_skeleton_gather(const TriParams& tp, const double* cellbuf, const double* f, double* out, double sign,
                                    cudaStream_t st) {
+  if (tp.Lx > 1024) return cudaErrorInvalidValue;   // per-x table of the gather
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
