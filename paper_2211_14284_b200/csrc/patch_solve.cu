@@ -716,13 +716,20 @@ __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __
 
 __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* __restrict__ u,
                                   double omega, long long n) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
-  int m = 0;
-  while (m + 1 < P.ncomp && g >= P.off[m + 1]) ++m;
-  const long long rr = g - P.off[m];
-  const long long x = rr % P.len[m][0], yz = rr / P.len[m][0];
-  u[g] += omega * cp[P.poff[m] + yz * P.lxp[m] + x];
+  // one (y, z) row of one component per warp, grid-stride: no per-element 64-bit division
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * (blockDim.x >> 5);
+  int rows_before = 0;
+  for (int m = 0; m < P.ncomp; ++m) {
+    const int Lx = (int)P.len[m][0], nrow = (int)(P.len[m][1] * P.len[m][2]);
+    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) - rows_before; r < nrow; r += wstride) {
+      if (r < 0) continue;
+      const long long ub = P.off[m] + (long long)r * Lx, cb = P.poff[m] + (long long)r * P.lxp[m];
+      for (int x = lane; x < Lx; x += 32) u[ub + x] += omega * cp[cb + x];
+    }
+    rows_before += nrow;
+  }
+  (void)n;
 }
 
 // ---- static condensation of the cell interiors (ICC-SC families, k = 0), on the padded layout
@@ -802,13 +809,14 @@ __global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* _
 __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
                                const double* __restrict__ cc, const int* __restrict__ nk,
                                const double* __restrict__ rp, double* __restrict__ cp, long long nint) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nint) return;
+  // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
-  const long long K = t / ni;
-  const int I = (int)(t % ni);
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= ni) return;
+  const long long K = blockIdx.y;
   const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / (pm * pm) + 1;
   const int cx = (int)(K % G.n[0]), cy = (int)((K / G.n[0]) % G.n[1]), cz = (int)(K / ((long long)G.n[0] * G.n[1]));
+  (void)nint;
   const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
   const double dv = dinv[K * ni + I];
   double s = cc[(K * 6 + 0) * ni + I] * cp[sc_idx(G, x, y + j, z + k)];
@@ -964,10 +972,12 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
             a[16], a[17], a[18], a[19]);
   }
   if (L.sc_dinv && nint > 0) {
-    sc_post_kernel<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
+    const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
+    const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
+    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  unpad_axpy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
+  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
   return cudaGetLastError();
 }
 
