@@ -73,7 +73,7 @@ class rm_info(ctypes.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2211_14284_b200.build` "
+        raise ImportError(f"{LIB_PATH} not built: run `python paper_2211_14284_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     P, D, I32, I64, U32 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
