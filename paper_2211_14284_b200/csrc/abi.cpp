@@ -343,12 +343,21 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
       for (size_t q = (size_t)b; q < np; q += (size_t)G) qs.push_back(q);
       const int n = (int)qs.size();
       xb.push_back((long long)xl.size());
-      if (n > 0) push(qs[0], 0, P.classes[pc[qs[0]]].uf0);
-      for (int i = 0; i < n; ++i) {
-        if (i + 1 < n) push(qs[i + 1], 0, P.classes[pc[qs[i + 1]]].uf0);
-        const rm::ClassProgram& C = P.classes[pc[qs[i]]];
-        if (!fin_tiles(qs[i])) push(qs[i], C.uf0, C.uf1);
-        push(qs[i], C.uf1, (int)C.units.size());
+      if (Lh.nbox >= 2) {   // pipelined consumption order: fwd(0), then per i: fwd(i+1), [final(i)], bwd(i)
+        if (n > 0) push(qs[0], 0, P.classes[pc[qs[0]]].uf0);
+        for (int i = 0; i < n; ++i) {
+          if (i + 1 < n) push(qs[i + 1], 0, P.classes[pc[qs[i + 1]]].uf0);
+          const rm::ClassProgram& C = P.classes[pc[qs[i]]];
+          if (!fin_tiles(qs[i])) push(qs[i], C.uf0, C.uf1);
+          push(qs[i], C.uf1, (int)C.units.size());
+        }
+      } else {              // one box buffer: per i: fwd(i), [final(i)], bwd(i)
+        for (int i = 0; i < n; ++i) {
+          const rm::ClassProgram& C = P.classes[pc[qs[i]]];
+          push(qs[i], 0, C.uf0);
+          if (!fin_tiles(qs[i])) push(qs[i], C.uf0, C.uf1);
+          push(qs[i], C.uf1, (int)C.units.size());
+        }
       }
       xb.push_back((long long)xl.size());
       for (int i = 0; i < n; ++i)

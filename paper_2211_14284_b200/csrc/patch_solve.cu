@@ -688,10 +688,17 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
     if (lane == 0) mbar_arrive(&vdone[b]);
     if (pf) sp_bwd += clock64() - ta;
   };
-  if (n > 0) forward(0);
-  for (int i = 0; i < n; ++i) {
-    if (i + 1 < n) forward(i + 1);
-    backward(i);
+  if (nbox >= 2) {   // pipelined: forward(i+1) runs while the tiles of patch i are in flight
+    if (n > 0) forward(0);
+    for (int i = 0; i < n; ++i) {
+      if (i + 1 < n) forward(i + 1);
+      backward(i);
+    }
+  } else {           // one box buffer (very large windows): box i+1 arrives after patch i is reduced
+    for (int i = 0; i < n; ++i) {
+      forward(i);
+      backward(i);
+    }
   }
   if (pf) {
     unsigned long long* o = prof + 24 * blockIdx.x;
@@ -861,7 +868,7 @@ cudaError_t encode_maps(PatchLaunch& L) {
 cudaError_t plan_patch_solve(PatchLaunch& L) {
   const size_t boxd = (size_t)((L.box_total + 15) & ~15);
   // three box buffers (patches i-1, i, i+1 in flight) when they fit, else two
-  L.nbox = getenv("RM_NBOX2") ? 2 : NBOX;   // experiments: two box buffers, more ring
+  L.nbox = getenv("RM_NBOX1") ? 1 : (getenv("RM_NBOX2") ? 2 : NBOX);   // tests / experiments
   L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -873,8 +880,10 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   // one CTA per SM; the rings share what the boxes leave: about 1/3 sparse channel, 2/3 tile
   // channel, each holding at least two of its largest units (env RM_RING_A_KB overrides)
   const size_t ua = (size_t)((L.unit_bytes_max_a + 127) & ~127), ub = (size_t)((L.unit_bytes_max_b + 127) & ~127);
-  if ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub) {
-    L.nbox = 2;
+  // fewer box buffers when the windows are large (3 -> 2 -> 1; with one buffer the sparse warps
+  // run the patches strictly in sequence and the host issue list follows that order)
+  while ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub && L.nbox > 1) {
+    --L.nbox;
     L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
   }
   if ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub) return cudaErrorInvalidValue;
