@@ -244,3 +244,24 @@ def test_nccl_transport_self_check(dev):
     import paper_2211_14284_b200 as rmb
     rmb.rm_nccl_check(torch.cuda.current_device())
     assert len(rmb.rm_nccl_unique_id()) == 128
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_full_size_hcurl_hdiv_configs_sweep(dev, cfg):
+    """BASELINE configs 3 and 4 at full size (24^3, p = 6 / 8): the patch plans fit (cfg4's ~95 KB
+    window boxes run with one box buffer and the sequential schedule) and a sweep is finite and
+    non-trivial.  (Parity of these paths is tested on the small shapes above, also with
+    RM_NBOX1=1 forcing the one-buffer schedule.)"""
+    import paper_2211_14284_b200 as rmb
+    w = ri.CONFIGS[cfg]
+    ctx = gu.setup_product(w)
+    n = ctx.n_local
+    mask = ctx.constrained_mask()
+    f = ri.uniform_vector(w.cfg, 0, n); f[mask] = 0
+    ft = torch.tensor(f, device=dev)
+    u = torch.zeros_like(ft)
+    rmb.rm_relax(ctx, ft, u, u, 1.0)
+    uh = u.cpu().numpy()
+    assert np.isfinite(uh).all() and np.abs(uh).max() > 0
+    assert np.abs(uh[mask]).max() == 0.0
