@@ -393,7 +393,9 @@ struct rm_ctx {
   double* d_cellbuf = nullptr;                 // trilinear apply: per-cell local results
   rm::TriParams tri{};
   int coef_const = 0;
-  DevFamily prim, pot;
+  // patch families: one per star orientation for edge / face stars (tighter window boxes), one
+  // for vertex stars; prims[0] / pots[0] always exist (possibly empty)
+  std::vector<DevFamily> prims = std::vector<DevFamily>(1), pots = std::vector<DevFamily>(1);
   std::vector<double> Dh;   // p x (p+1)
   double *d_r = nullptr, *d_t = nullptr, *d_s = nullptr;
   double *d_z = nullptr, *d_pp = nullptr, *d_q = nullptr, *d_pr = nullptr;
@@ -423,8 +425,8 @@ struct rm_ctx {
     if (comm) { try { if (nccl().destroy) nccl().destroy(comm); } catch (...) {} }
     for (auto& e : events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : allocs) cudaFree(p);
-    prim.release();
-    pot.release();
+    for (auto& F : prims) F.release();
+    for (auto& F : pots) F.release();
   }
 };
 
@@ -722,8 +724,15 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
     in.zv_lo = part.v_lo; in.zv_hi = part.v_hi;   // owned vertex layers (all of them on one rank)
     {
-      auto fam = rm::build_patch_family(in);
-      upload_family(c->prim, *fam);
+      // edge / face stars: one family per orientation (window boxes ~2-4x smaller than the hull)
+      const int no = (in.dim == 1 || in.dim == 2) && !getenv("RM_ONE_FAMILY") ? 3 : 1;
+      c->prims.assign(no, DevFamily{});
+      for (int o = 0; o < no; ++o) {
+        rm::SetupInput io = in;
+        io.orient = no > 1 ? o : -1;
+        auto fam = rm::build_patch_family(io);
+        upload_family(c->prims[o], *fam);
+      }
     }
     if (c->decomposition == RM_PH && space >= 1) {
       // potential problem B = D^T A D (+ eps_s beta M^{k-1} for k = 2): the V^{k-1} operator with
@@ -735,8 +744,14 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       ip.k = space - 1; ip.alpha = ap.data(); ip.beta = bp.data(); ip.n_alpha = n_beta; ip.n_beta = n_beta;
       ip.dim = space - 1;
       ip.factorization = RM_CHOL;
-      auto fam = rm::build_patch_family(ip);
-      upload_family(c->pot, *fam);
+      const int no = (ip.dim == 1 || ip.dim == 2) && !getenv("RM_ONE_FAMILY") ? 3 : 1;
+      c->pots.assign(no, DevFamily{});
+      for (int o = 0; o < no; ++o) {
+        rm::SetupInput io = ip;
+        io.orient = no > 1 ? o : -1;
+        auto fam = rm::build_patch_family(io);
+        upload_family(c->pots[o], *fam);
+      }
       c->spot.init(space - 1, p, mesh->nx, mesh->ny, mesh->nz);
       c->npot = c->spot.ndof();
       const rm::Basis1D& b = rm::basis(p);
@@ -796,14 +811,21 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
   std::memset(info, 0, sizeof *info);
   info->n_local = c->ndof;
   info->n_free = c->nfree;
-  info->n_patches = c->prim.npatch;
-  info->n_patches_potential = c->pot.npatch;
-  info->n_factor_blocks = c->prim.nfactors + c->pot.nfactors;
-  info->factor_bytes = c->prim.sweep_value_bytes + c->pot.sweep_value_bytes;
+  for (const auto& F : c->prims) {
+    info->n_patches += F.npatch;
+    info->n_factor_blocks += F.nfactors;
+    info->factor_bytes += F.sweep_value_bytes;
+    info->n_classes += (int32_t)F.nclasses;
+  }
+  for (const auto& F : c->pots) {
+    info->n_patches_potential += F.npatch;
+    info->n_factor_blocks += F.nfactors;
+    info->factor_bytes += F.sweep_value_bytes;
+    info->n_classes += (int32_t)F.nclasses;
+  }
   info->sweep_bytes = info->factor_bytes + 3 * 8 * c->ndof;
-  info->n_colors = (int32_t)c->prim.color_start.size() - 1;
-  info->n_classes = (int32_t)(c->prim.nclasses + c->pot.nclasses);
-  info->icc_sigma_max = c->prim.sigma_max;
+  info->n_colors = (int32_t)c->prims[0].color_start.size() - 1;
+  info->icc_sigma_max = c->prims[0].sigma_max;
   info->setup_seconds = c->setup_seconds;
   return RM_OK;
 }
@@ -893,13 +915,14 @@ int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega
 void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false) {
   {
     Phase ph(c, 1);
-    c->launches[1] += run_family(c, c->prim, r, u, omega, r_padded);
+    for (auto& F : c->prims) c->launches[1] += run_family(c, F, r, u, omega, r_padded);
   }
-  if (c->pot.present) {
+  if (c->pots[0].present) {
     Phase ph(c, 2);
     CK(rm::launch_hiptmair_DT(c->k, c->p, c->n, c->gamma, c->Dh.data(), r, c->d_t, c->st));
     CK(cudaMemsetAsync(c->d_s, 0, c->npot * sizeof(double), c->st));
-    c->launches[2] += 2 + run_family(c, c->pot, c->d_t, c->d_s, 1.0);
+    c->launches[2] += 2;
+    for (auto& F : c->pots) c->launches[2] += run_family(c, F, c->d_t, c->d_s, 1.0);
     CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, u, omega, c->st));
   }
 }
@@ -990,9 +1013,9 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
     CK(rm::launch_axpby(c->ndof, omega, c->d_c, 1.0, u_out, c->st));
     return;
   }
-  if (c->k == 0 && !c->pot.present && c->prim.npatch > 0) {
+  if (c->k == 0 && !c->pots[0].present && c->prims.size() == 1 && c->prims[0].npatch > 0) {
     // the residual goes straight into the primary family's padded (TMA) layout: no pad pass
-    const rm::PatchLaunch& L = c->prim.launch;
+    const rm::PatchLaunch& L = c->prims[0].launch;
     do_apply(c, u_in, f, L.rpad, L.pad.lxp[0]);
     if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     add_precond(c, L.rpad, u_out, omega, true);

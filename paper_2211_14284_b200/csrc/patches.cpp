@@ -1143,6 +1143,16 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   Builder B(in, fam.get());
   fam->sp = B.sp; fam->dim = in.dim; fam->gamma_d = in.gamma_d; fam->factorization = in.factorization;
   std::vector<Entity> ents = entities(B.sp, in.dim, in.interior_only != 0);
+  if (in.orient >= 0 && (in.dim == 1 || in.dim == 2)) {   // one orientation: tighter window boxes
+    std::vector<Entity> kept;
+    for (const Entity& e : ents) {
+      int dir = -1;
+      for (int d = 0; d < 3; ++d)
+        if ((in.dim == 1 && e.s[d].kind == 1) || (in.dim == 2 && e.s[d].kind == 0)) dir = d;
+      if (dir == in.orient) kept.push_back(e);
+    }
+    ents.swap(kept);
+  }
   if (in.zv_lo > 0 || in.zv_hi <= B.sp.n[2]) {   // z-slab ownership: vertex stars of the owned layers
     if (in.dim != 0) throw std::runtime_error("z-slab patch ownership: vertex stars only");
     std::vector<Entity> kept;

@@ -194,6 +194,7 @@ struct SetupInput {
   bool cartesian;                 // all cells axis-aligned
   const double* hx; const double* hy; const double* hz;   // per-direction cell sizes (cartesian)
   int zv_lo = 0, zv_hi = 1 << 30;   // vertex stars kept: z vertex layers [zv_lo, zv_hi) (z-slab ownership)
+  int orient = -1;                  // edge / face stars: keep one orientation (edge direction / face normal), -1 = all
 };
 
 // Builds the full patch family. Throws std::runtime_error with a message on failure.
