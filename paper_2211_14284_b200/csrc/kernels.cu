@@ -56,15 +56,21 @@ __device__ __forceinline__ void decode(long long g, int ncomp, const long long* 
                                        int& m, long long* idx) {
   m = 0;
   while (m + 1 < ncomp && g >= off[m + 1]) ++m;
-  const long long rr = g - off[m];
-  idx[0] = rr % len[m][0];
-  idx[1] = (rr / len[m][0]) % len[m][1];
-  idx[2] = rr / (len[m][0] * len[m][1]);
+  // 32-bit index math (component sizes < 2^31): the 64-bit divisions dominated these kernels
+  const int rr = (int)(g - off[m]);
+  const int l0 = (int)len[m][0], l1 = (int)len[m][1];
+  const int q = rr / l0;
+  idx[0] = rr - q * l0;
+  idx[1] = q % l1;
+  idx[2] = q / l1;
 }
 
 // t = D^T r on the potential space (zero on constrained potential DoFs)
 __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const double* __restrict__ r,
                                    double* __restrict__ t, long long npot) {
+  __shared__ double Ds[RM_MAXP1 * RM_MAXP1];   // lane-varying indices: shared memory, not the param bank
+  for (int i = threadIdx.x; i < hp.p * (hp.p + 1); i += blockDim.x) Ds[i] = hp.D[i];
+  __syncthreads();
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= npot) return;
   int m;
@@ -87,7 +93,7 @@ __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const d
       long long j[3] = {idx[0], idx[1], idx[2]};
       for (int a = 0; a < p; ++a) {
         j[e] = (long long)cc[k] * p + a;
-        const double dv = hp.D[a * (p + 1) + aa[k]];
+        const double dv = Ds[a * (p + 1) + aa[k]];
         if (dv == 0.0) continue;
         s += dv * r[hp.off_pri[n] + (j[2] * hp.len_pri[n][1] + j[1]) * hp.len_pri[n][0] + j[0]];
       }
@@ -100,6 +106,9 @@ __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const d
 // u += omega * D s on the primal space (zero contribution on constrained primal DoFs)
 __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, const double* __restrict__ s,
                                       double* __restrict__ u, double omega, long long npri) {
+  __shared__ double Ds[RM_MAXP1 * RM_MAXP1];
+  for (int i = threadIdx.x; i < hp.p * (hp.p + 1); i += blockDim.x) Ds[i] = hp.D[i];
+  __syncthreads();
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= npri) return;
   int n;
@@ -119,7 +128,7 @@ __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, cons
     long long j[3] = {idx[0], idx[1], idx[2]};
     double sum = 0.0;
     for (int i = 0; i <= p; ++i) {
-      const double dv = hp.D[a * (p + 1) + i];
+      const double dv = Ds[a * (p + 1) + i];
       if (dv == 0.0) continue;
       j[e] = (long long)c * p + i;
       sum += dv * s[hp.off_pot[m] + (j[2] * hp.len_pot[m][1] + j[1]) * hp.len_pot[m][0] + j[0]];
