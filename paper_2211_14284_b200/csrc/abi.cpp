@@ -143,7 +143,8 @@ struct DevFamily {
   }
 };
 
-void upload_family(DevFamily& F, const rm::PatchFamily& P) {
+// share: a family of the same space whose padded r / c buffers this one uses (orientation families)
+void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* share = nullptr) {
   const int NW = rm::RM_PATCH_TILE_WARPS;
   std::vector<rm::DClass> hc(P.classes.size());
   int n_max = 0, piv_max = 0, mem_max = 0, aux_max = 0, unit_max = 0, unit_max_a = 0, unit_max_b = 0;
@@ -252,13 +253,17 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P) {
     }
     for (int m = pl.ncomp; m <= 3; ++m) { pl.off[m] = o; pl.poff[m] = po2; }
     Lh.npad = po2;
-    void *a = nullptr, *b = nullptr;
-    if (cudaMalloc(&a, po2 * sizeof(double)) != cudaSuccess || cudaMalloc(&b, po2 * sizeof(double)) != cudaSuccess)
-      throw RmError(RM_ENOMEM, "cudaMalloc failed (padded r / c)");
-    F.allocs.push_back(a); F.allocs.push_back(b);
-    Lh.rpad = static_cast<double*>(a); Lh.cpad = static_cast<double*>(b);
-    // the pad column of rpad stays zero when the apply writes the residual there directly
-    CK(cudaMemset(Lh.rpad, 0, po2 * sizeof(double)));
+    if (share && share->launch.npad == po2) {
+      Lh.rpad = share->launch.rpad; Lh.cpad = share->launch.cpad;
+    } else {
+      void *a = nullptr, *b = nullptr;
+      if (cudaMalloc(&a, po2 * sizeof(double)) != cudaSuccess || cudaMalloc(&b, po2 * sizeof(double)) != cudaSuccess)
+        throw RmError(RM_ENOMEM, "cudaMalloc failed (padded r / c)");
+      F.allocs.push_back(a); F.allocs.push_back(b);
+      Lh.rpad = static_cast<double*>(a); Lh.cpad = static_cast<double*>(b);
+      // the pad column of rpad stays zero when the apply writes the residual there directly
+      CK(cudaMemset(Lh.rpad, 0, po2 * sizeof(double)));
+    }
   }
   Lh.npatch = (int)np;
   // tile warps joining the ICC solve (measured slower: more ring walkers), opt-in experiment
@@ -731,7 +736,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
         rm::SetupInput io = in;
         io.orient = no > 1 ? o : -1;
         auto fam = rm::build_patch_family(io);
-        upload_family(c->prims[o], *fam);
+        upload_family(c->prims[o], *fam, o > 0 ? &c->prims[0] : nullptr);
       }
     }
     if (c->decomposition == RM_PH && space >= 1) {
@@ -750,7 +755,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
         rm::SetupInput io = ip;
         io.orient = no > 1 ? o : -1;
         auto fam = rm::build_patch_family(io);
-        upload_family(c->pots[o], *fam);
+        upload_family(c->pots[o], *fam, o > 0 ? &c->pots[0] : nullptr);
       }
       c->spot.init(space - 1, p, mesh->nx, mesh->ny, mesh->nz);
       c->npot = c->spot.ndof();
@@ -903,11 +908,14 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out, long lon
   c->launches[0] += nl;
 }
 
-int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega, bool r_padded = false) {
-  if (F.npatch == 0) return 0;
+// families of one space run back to back on shared padded buffers: the first pads r and zeroes c,
+// the last adds omega c to u
+int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega, bool r_padded = false,
+               bool zero_c = true, bool combine = true) {
+  if (!F.present) return 0;
   KPhase kp{c, 4};
   const rm::KTimer kt = kp.timer();
-  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded));
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded, zero_c, combine));
   return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
@@ -915,14 +923,18 @@ int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega
 void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false) {
   {
     Phase ph(c, 1);
-    for (auto& F : c->prims) c->launches[1] += run_family(c, F, r, u, omega, r_padded);
+    const int nf = (int)c->prims.size();
+    for (int o = 0; o < nf; ++o)
+      c->launches[1] += run_family(c, c->prims[o], r, u, omega, r_padded || o > 0, o == 0, o == nf - 1);
   }
   if (c->pots[0].present) {
     Phase ph(c, 2);
     CK(rm::launch_hiptmair_DT(c->k, c->p, c->n, c->gamma, c->Dh.data(), r, c->d_t, c->st));
     CK(cudaMemsetAsync(c->d_s, 0, c->npot * sizeof(double), c->st));
     c->launches[2] += 2;
-    for (auto& F : c->pots) c->launches[2] += run_family(c, F, c->d_t, c->d_s, 1.0);
+    const int np = (int)c->pots.size();
+    for (int o = 0; o < np; ++o)
+      c->launches[2] += run_family(c, c->pots[o], c->d_t, c->d_s, 1.0, o > 0, o == 0, o == np - 1);
     CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, u, omega, c->st));
   }
 }

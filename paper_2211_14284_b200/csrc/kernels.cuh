@@ -158,8 +158,11 @@ struct PatchLaunch {
 };
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
 // r_padded: r is already in the padded layout L.rpad (the apply wrote it there): no pad pass
+// zero_c / combine: zero the padded correction first / add omega * c to u at the end (families
+// sharing their padded buffers run back to back)
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt = nullptr, bool r_padded = false);
+                               const KTimer* kt = nullptr, bool r_padded = false, bool zero_c = true,
+                               bool combine = true);
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;

@@ -915,8 +915,14 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
 }
 
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt, bool r_padded) {
-  if (L.npatch <= 0) return cudaSuccess;
+                               const KTimer* kt, bool r_padded, bool zero_c, bool combine) {
+  if (L.npatch <= 0) {   // an empty family still does its part of a shared sequence
+    if (!L.cpad) return cudaSuccess;
+    if (!r_padded) pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
+    if (zero_c) cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st);
+    if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp]);
+    return cudaGetLastError();
+  }
   const long long n = L.pad.off[L.pad.ncomp];
   cudaError_t e;
   if (!r_padded) {
@@ -949,7 +955,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
   }
-  if ((e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
+  if (zero_c && (e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
   BoxGeom bg;
   bg.ncomp = L.nsub;
@@ -986,7 +992,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
+  if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
   return cudaGetLastError();
 }
 
