@@ -92,6 +92,15 @@ typedef struct {
   int32_t n_colors, n_classes;
   double icc_sigma_max;      /* largest ICC restart shift used (reading G7), 0 if none             */
   double setup_seconds;
+  int64_t factor_nnz;        /* SURVEY 8(d) algorithmic factor entries of one sweep: sum over the   */
+                             /* patches of nnz(L) of the exact Cholesky factor in the pinned order  */
+                             /* (reading G6), or of the ICC-SC mask (primary + potential)           */
+  int64_t factor_nnz_primary;   /* the same, primary (k-star) patches only                         */
+  int64_t factor_unique_bytes;  /* bytes of the distinct value blocks held in HBM (identical       */
+                                /* patches share one block)                                       */
+  int32_t comm_nranks;       /* ranks of the context's NCCL communicator (0 = none)                 */
+  int32_t coarse;            /* 1 if the p = 1 coarse level is set up (options.coarse)             */
+  int64_t coarse_ndof;       /* unconstrained DoFs of the coarse problem A_0 (0 without it)        */
 } rm_info;
 
 void rm_default_options(rm_options *opt);

@@ -5,7 +5,7 @@ There is no CPU fallback: importing this package fails loudly when the library i
 and every call checks that its vectors are fp64 CUDA tensors of the layout's length.
 
     ctx = rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposition=RM_PAFW,
-                   factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-6)
+                   factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-3)
     rm_apply(ctx, u, v); rm_residual(ctx, f, u, r); rm_relax(ctx, f, u_in, u_out, omega)
     rm_precondition(ctx, r, z); rm_relax_host(ctx, f_np, u_np, out_np, omega)
     iters, rel = rm_pcg(ctx, f, u, rtol, maxit)
@@ -68,7 +68,10 @@ class rm_info(ctypes.Structure):
     _fields_ = [("n_local", ctypes.c_int64), ("n_free", ctypes.c_int64), ("n_patches", ctypes.c_int64),
                 ("n_patches_potential", ctypes.c_int64), ("n_factor_blocks", ctypes.c_int64),
                 ("factor_bytes", ctypes.c_int64), ("sweep_bytes", ctypes.c_int64), ("n_colors", ctypes.c_int32),
-                ("n_classes", ctypes.c_int32), ("icc_sigma_max", ctypes.c_double), ("setup_seconds", ctypes.c_double)]
+                ("n_classes", ctypes.c_int32), ("icc_sigma_max", ctypes.c_double), ("setup_seconds", ctypes.c_double),
+                ("factor_nnz", ctypes.c_int64), ("factor_nnz_primary", ctypes.c_int64),
+                ("factor_unique_bytes", ctypes.c_int64), ("comm_nranks", ctypes.c_int32), ("coarse", ctypes.c_int32),
+                ("coarse_ndof", ctypes.c_int64)]
 
 
 def _load():

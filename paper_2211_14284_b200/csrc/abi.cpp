@@ -123,6 +123,8 @@ struct DevFamily {
   std::vector<int> color_start;
   int64_t npatch = 0, nfactors = 0, nclasses = 0;
   int64_t sweep_value_bytes = 0;   // sum over patches of value-block bytes
+  int64_t nnzL = 0, unique_bytes = 0;   // algorithmic factor entries (sum over patches), distinct block bytes
+  int ncolors = 0;
   double sigma_max = 0.0;
   bool present = false;
 
@@ -253,7 +255,10 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     }
     for (int m = pl.ncomp; m <= 3; ++m) { pl.off[m] = o; pl.poff[m] = po2; }
     Lh.npad = po2;
-    if (share && share->launch.npad == po2) {
+    if (share) {   // orientation families run back to back on ONE padded r / c pair (add_precond)
+      if (share->launch.npad != po2) throw RmError(RM_EINVAL, "orientation families: padded layouts differ");
+      if (!P.sc_nk.empty() || share->launch.sc_dinv)
+        throw RmError(RM_EINVAL, "static-condensation families modify rpad and cannot share it");
       Lh.rpad = share->launch.rpad; Lh.cpad = share->launch.cpad;
     } else {
       void *a = nullptr, *b = nullptr;
@@ -267,7 +272,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
   }
   Lh.npatch = (int)np;
   // tile warps joining the ICC solve (measured slower: more ring walkers), opt-in experiment
-  Lh.icc_only = getenv("RM_ICC_ONLY") ? 1 : 0;
+  Lh.icc_only = rm::exp_env("RM_ICC_ONLY") ? 1 : 0;
   for (const auto& C : P.classes)
     if (C.final_kind != rm::FINAL_ICC || !C.sc) Lh.icc_only = 0;
   Lh.cs.ncolors = P.ncolors;
@@ -376,6 +381,9 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
   F.nfactors = P.nfactors;
   F.nclasses = (int64_t)P.classes.size();
   F.sweep_value_bytes = bytes;
+  F.nnzL = P.nnzL_total;
+  F.unique_bytes = P.unique_value_bytes;
+  F.ncolors = P.ncolors;
   F.sigma_max = P.sigma_max;
   F.present = true;
 }
@@ -678,7 +686,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
       c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
-    } else if (space == 0 && getenv("RM_APPLY_CELLBUF")) {
+    } else if (space == 0 && rm::exp_env("RM_APPLY_CELLBUF")) {
       // Cartesian H(grad), opt-in: one apply launch over all cells, interior DoFs stored directly,
       // skeleton entries through the cell buffer and the gather (measured: apply 0.28 -> 0.19 ms at
       // cfg2, but the gather costs what the colours and the init cost; the residual phase is equal)
@@ -730,7 +738,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.zv_lo = part.v_lo; in.zv_hi = part.v_hi;   // owned vertex layers (all of them on one rank)
     {
       // edge / face stars: one family per orientation (window boxes ~2-4x smaller than the hull)
-      const int no = (in.dim == 1 || in.dim == 2) && !getenv("RM_ONE_FAMILY") ? 3 : 1;
+      const int no = (in.dim == 1 || in.dim == 2) && !rm::exp_env("RM_ONE_FAMILY") ? 3 : 1;
       c->prims.assign(no, DevFamily{});
       for (int o = 0; o < no; ++o) {
         rm::SetupInput io = in;
@@ -749,7 +757,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       ip.k = space - 1; ip.alpha = ap.data(); ip.beta = bp.data(); ip.n_alpha = n_beta; ip.n_beta = n_beta;
       ip.dim = space - 1;
       ip.factorization = RM_CHOL;
-      const int no = (ip.dim == 1 || ip.dim == 2) && !getenv("RM_ONE_FAMILY") ? 3 : 1;
+      const int no = (ip.dim == 1 || ip.dim == 2) && !rm::exp_env("RM_ONE_FAMILY") ? 3 : 1;
       c->pots.assign(no, DevFamily{});
       for (int o = 0; o < no; ++o) {
         rm::SetupInput io = ip;
@@ -829,8 +837,19 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
     info->n_classes += (int32_t)F.nclasses;
   }
   info->sweep_bytes = info->factor_bytes + 3 * 8 * c->ndof;
-  info->n_colors = (int32_t)c->prims[0].color_start.size() - 1;
-  info->icc_sigma_max = c->prims[0].sigma_max;
+  for (const auto& F : c->prims) {
+    info->n_colors += F.ncolors;
+    info->factor_nnz_primary += F.nnzL;
+    info->icc_sigma_max = std::max(info->icc_sigma_max, F.sigma_max);
+  }
+  info->factor_nnz = info->factor_nnz_primary;
+  for (const auto& F : c->prims) info->factor_unique_bytes += F.unique_bytes;
+  for (const auto& F : c->pots) {
+    info->factor_nnz += F.nnzL;
+    info->factor_unique_bytes += F.unique_bytes;
+    info->icc_sigma_max = std::max(info->icc_sigma_max, F.sigma_max);
+  }
+  info->comm_nranks = c->comm ? c->nranks : 0;
   info->setup_seconds = c->setup_seconds;
   return RM_OK;
 }
@@ -1000,10 +1019,6 @@ rm_status guarded(rm_ctx* c, F&& f) {
   }
 }
 
-}  // namespace
-
-extern "C" {
-
 // u with its forward halo: the caller's vector itself on one rank (or without a communicator:
 // the caller filled the halo), else a copy with the halo exchanged
 const double* with_halo(rm_ctx* c, const double* u, double* buf) {
@@ -1037,6 +1052,10 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
   if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   add_precond(c, c->d_r, u_out, omega);
 }
+
+}  // namespace
+
+extern "C" {
 
 rm_status rm_apply(rm_ctx* c, const double* u, double* v) {
   return guarded(c, [&] {

@@ -1,0 +1,18 @@
+#pragma once
+#include <cstdlib>
+
+namespace rm {
+
+// Experiment / instrumentation switches read from the environment (ring sizes, grid, profiling
+// counters, alternative kernels): compiled in only with -DRM_EXPERIMENTS, so the product build reads
+// none of them.  The two documented runtime knobs (rm.h) are RM_SETUP_THREADS and RM_NBOX1.
+inline const char* exp_env(const char* name) {
+#ifdef RM_EXPERIMENTS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+}  // namespace rm

@@ -1,10 +1,14 @@
 // Device-side data structures shared by the kernels and the host launcher (abi.cpp).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "exp_env.hpp"
+
 namespace rm {
+
 
 #define RM_MAXLEV 8
 #define RM_MAXTERMS 16

@@ -868,7 +868,7 @@ cudaError_t encode_maps(PatchLaunch& L) {
 cudaError_t plan_patch_solve(PatchLaunch& L) {
   const size_t boxd = (size_t)((L.box_total + 15) & ~15);
   // three box buffers (patches i-1, i, i+1 in flight) when they fit, else two
-  L.nbox = getenv("RM_NBOX1") ? 1 : (getenv("RM_NBOX2") ? 2 : NBOX);   // tests / experiments
+  L.nbox = getenv("RM_NBOX1") ? 1 : (exp_env("RM_NBOX2") ? 2 : NBOX);   // RM_NBOX1: documented test switch (rm.h)
   L.smem_fixed = BAR_BYTES + (L.nbox * boxd + (size_t)L.aux_max) * sizeof(double);
   int dev = 0, nsm = 0, optin = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -889,7 +889,7 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   if ((size_t)optin < L.smem_fixed + 2 * ua + 2 * ub) return cudaErrorInvalidValue;
   const size_t rings = (optin - L.smem_fixed) & ~(size_t)127;
   size_t capA = (rings / 3) & ~(size_t)127;
-  if (const char* s = getenv("RM_RING_A_KB")) capA = ((size_t)atoi(s) * 1024) & ~(size_t)127;
+  if (const char* s = exp_env("RM_RING_A_KB")) capA = ((size_t)atoi(s) * 1024) & ~(size_t)127;
   capA = std::min(std::max(capA, 2 * ua), rings - 2 * ub);
   if (ub == 0) capA = rings - 128;   // no dense tiles in this family: the sparse channel takes the rings
   capA = std::max(capA, (size_t)128);
@@ -902,13 +902,13 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
     return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   L.grid = std::max(1, std::min(L.npatch, occ * nsm));
-  if (const char* g = getenv("RM_GRID")) L.grid = std::max(1, std::min(L.grid, atoi(g)));   // experiments
+  if (const char* g = exp_env("RM_GRID")) L.grid = std::max(1, std::min(L.grid, atoi(g)));   // experiments
   if ((e = encode_maps(L)) != cudaSuccess) return e;
-  if (getenv("RM_PROFILE") && !L.prof && (e = cudaMalloc(&L.prof, (size_t)24 * 8 * L.grid)) != cudaSuccess) return e;
+  if (exp_env("RM_PROFILE") && !L.prof && (e = cudaMalloc(&L.prof, (size_t)24 * 8 * L.grid)) != cudaSuccess) return e;
   // descriptors live in global memory (64-byte aligned allocation), read by the TMA unit
   if (!L.tm_dev && (e = cudaMalloc(&L.tm_dev, sizeof(TMaps))) != cudaSuccess) return e;
   if ((e = cudaMemcpy(L.tm_dev, &L.tm, sizeof(TMaps), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
-  if (getenv("RM_VERBOSE"))
+  if (exp_env("RM_VERBOSE"))
     fprintf(stderr, "[rm] patch plan: npatch=%d box=%d x%d aux_max=%d fixed=%zu ringA=%zu ringB=%zu occ=%d grid=%d\n",
             L.npatch, L.box_total, L.nbox, L.aux_max, L.smem_fixed, capA, capB, occ, L.grid);
   return cudaSuccess;
@@ -966,11 +966,27 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     if (m < L.nsub) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
   }
   if (kt) kt->begin(kt->arg);
-  patch_stream_kernel<<<L.grid, NTHR, L.smem_fixed + L.ring_bytes + L.ring_b_bytes, st>>>(
-      L.tm_dev, L.classes, L.pclass, L.pvals, L.porig, L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes,
-      (uint32_t)L.ring_b_bytes, L.box_total, L.xfer, L.xbeg, L.nbox, L.prof,
-      L.icc_only);
+  // cooperative launch: the colour wait of the store warps spins on a counter advanced by other
+  // CTAs, so every CTA of the grid must be resident at once -- the runtime guarantees that (or
+  // fails the launch with cudaErrorCooperativeLaunchTooLarge) instead of a possible hang under
+  // MPS / green contexts / concurrent kernels holding SMs
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)L.grid);
+    cfg.blockDim = dim3(NTHR);
+    cfg.dynamicSmemBytes = L.smem_fixed + L.ring_bytes + L.ring_b_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, patch_stream_kernel, (const TMaps*)L.tm_dev, L.classes, L.pclass, L.pvals, L.porig,
+                           L.vals, L.npatch, L.cs, bg, L.done, (uint32_t)L.ring_bytes, (uint32_t)L.ring_b_bytes,
+                           L.box_total, L.xfer, L.xbeg, L.nbox, L.prof, L.icc_only);
+  }
   if (kt) kt->end(kt->arg);
+  if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;

@@ -1,4 +1,5 @@
 #include "patches.hpp"
+#include "exp_env.hpp"
 
 #include <algorithm>
 #include <array>
@@ -269,8 +270,8 @@ void build_meta(ClassProgram& C) {
   }
   // transfer units: consecutive pieces (metas and values both contiguous), split at the
   // dense-tile section (its own channel)
-  static const int unit_vals = getenv("RM_UNIT_VALS") ? atoi(getenv("RM_UNIT_VALS")) : kUnitVals;
-  static const int unit_vals_tile = getenv("RM_UNIT_VALS_TILE") ? atoi(getenv("RM_UNIT_VALS_TILE")) : kUnitValsTile;
+  static const int unit_vals = exp_env("RM_UNIT_VALS") ? atoi(exp_env("RM_UNIT_VALS")) : kUnitVals;
+  static const int unit_vals_tile = exp_env("RM_UNIT_VALS_TILE") ? atoi(exp_env("RM_UNIT_VALS_TILE")) : kUnitValsTile;
   C.units.clear();
   for (int i = 0; i < (int)C.pieces.size();) {
     Unit u{i, 0, C.pieces[i].mofs, 0, C.pieces[i].sofs, 0};
@@ -494,7 +495,7 @@ struct Builder {
   // ---------------------------------------------------------------- class program (symbolic)
   void build_class(const Entity& e, ClassProgram& C) {
     const int p = sp.p;
-    static const bool sc_off = getenv("RM_NO_SC") != nullptr;   // experiments: ICC-SC inside the patch kernel
+    static const bool sc_off = exp_env("RM_NO_SC") != nullptr;   // experiments: ICC-SC inside the patch kernel
     const bool sc = in.factorization == 1 && in.k == 0 && !sc_off;   // ICC-SC: condense cell interiors per cell
     std::vector<NatDof> dofs;
     int wlo_abs[3][3] = {{0}};
@@ -552,6 +553,41 @@ struct Builder {
         if (i >= 0 && j >= 0) adj[i].push_back(j);
       }
     for (auto& a : adj) { std::sort(a.begin(), a.end()); a.erase(std::unique(a.begin(), a.end()), a.end()); }
+    // algorithmic factor size: exact Cholesky -> nnz(L) in the pinned order by the
+    // elimination-tree row walk (every row of L = the etree paths from its A-row entries);
+    // ICC-SC -> the mask tril(pattern(P_v)) U tril(pattern(P_GI P_IG)) (interiors first)
+    {
+      int64_t nnz = 0;
+      if (in.factorization == 0) {
+        std::vector<int> parent(n, -1), flag(n, -1);
+        for (int i = 0; i < n; ++i) {
+          flag[i] = i;
+          ++nnz;
+          for (int j : adj[i]) {
+            if (j >= i) break;
+            for (int k = j; flag[k] != i; k = parent[k]) {
+              if (parent[k] == -1) parent[k] = i;
+              ++nnz;
+              flag[k] = i;
+            }
+          }
+        }
+      } else {
+        std::vector<char> interior(n, 0);
+        for (int i = 0; i < n; ++i) interior[i] = dofs[i].group == 0;
+        std::vector<int> mark(n, -1);
+        for (int i = 0; i < n; ++i) {
+          std::vector<int> row;
+          for (int j : adj[i]) if (j <= i) row.push_back(j);
+          if (!interior[i])
+            for (int k : adj[i])
+              if (interior[k])
+                for (int j : adj[k]) if (!interior[j] && j <= i) row.push_back(j);
+          for (int j : row) if (mark[j] != i) { mark[j] = i; ++nnz; }
+        }
+      }
+      C.nnzL = nnz;
+    }
 
     // ---- symbolic elimination
     // face orientation of group-1 DoFs (direction of the P index on a cell boundary), 3 otherwise
@@ -638,7 +674,7 @@ struct Builder {
         for (int t : pick) nnzW += deg[t];
         int64_t oldc = m * (m + 1) / 2;
         int64_t newc = nE + 2 * nnzW + (m - nE) * (m - nE + 1) / 2;
-        if (getenv("RM_DEBUG_LEVELS"))
+        if (exp_env("RM_DEBUG_LEVELS"))
           fprintf(stderr, "[levels] n=%d nG=%d m=%lld pick=%lld nnzW=%lld mindeg=%d maxdeg=%d old=%lld new=%lld\n", n, nG,
                   (long long)m, (long long)nE, (long long)nnzW, deg[ord.front()], deg[ord.back()], (long long)oldc,
                   (long long)newc);
@@ -1263,6 +1299,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
       frep.push_back(t);
       total += fam->classes[c].nvals;
     }
+    fam->nnzL_total += fam->classes[c].nnzL;
     fid[t] = it->second;
     fam->pvals[t] = foff[fid[t]];
   }
@@ -1285,6 +1322,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     build_meta(C);
   }
   fam->nfactors = (int64_t)foff.size();
+  fam->unique_value_bytes = total * (int64_t)sizeof(double);
   fam->values.assign(total, 0.0);
   std::string first_err;
   std::mutex emu;

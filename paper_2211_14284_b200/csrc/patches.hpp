@@ -126,6 +126,8 @@ struct ClassProgram {
   std::vector<int> iccf_row, iccf_rp, iccf_col, iccf_src, iccf_lpiece;   // forward (diag last)
   std::vector<int> iccb_row, iccb_rp, iccb_col, iccb_src, iccb_lpiece;   // backward (diag first)
   std::vector<IccChunk> iccf_chunk, iccb_chunk;   // pieces hold chunk ranges [a0, a1)
+  int64_t nnzL = 0;                      // SURVEY 8(d) algorithmic factor size: nnz of the exact Cholesky
+                                         // factor in the pinned order (G6), or of the ICC-SC mask
   int64_t nvals_canon = 0;               // doubles per canonical (factorization-order) block
   int64_t nvals = 0;                     // doubles per patch value block (stream layout)
   // stream pieces and the piece ranges of each section
@@ -178,6 +180,8 @@ struct PatchFamily {
   int box_total = 0;
   double sigma_max = 0.0;         // largest ICC restart shift used (reading G7)
   int64_t nfactors = 0;           // distinct value blocks
+  int64_t nnzL_total = 0;         // sum over patches of ClassProgram::nnzL (algorithmic factor entries)
+  int64_t unique_value_bytes = 0; // bytes of the distinct value blocks (what HBM holds)
   std::string err;
 };
 

@@ -365,6 +365,34 @@ long long emu_assemble(int k, int p, int nx, int ny, int nz, const double* alpha
   return cnt <= cap ? cnt : -cnt;
 }
 
+// SURVEY 8(d) algorithmic factor entries of a family (alpha = beta = 1, uniform grid):
+// out[0] = sum over patches of nnz(L), out[1] = patches, out[2] = largest class nnz(L)
+int emu_family_nnz(int k, int p, int nx, int ny, int nz, unsigned gamma, int dim, int fact, int interior_only,
+                   long long* out, char* err, int errlen) {
+  try {
+    std::vector<double> h[3];
+    const int n[3] = {nx, ny, nz};
+    for (int d = 0; d < 3; ++d) h[d].assign(n[d], 1.0 / n[d]);
+    const double one = 1.0;
+    SetupInput in{};
+    in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
+    in.coords = nullptr; in.alpha = &one; in.beta = &one; in.n_alpha = 1; in.n_beta = 1;
+    in.dim = dim; in.factorization = fact; in.interior_only = interior_only;
+    in.cartesian = true;
+    in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    auto F = build_patch_family(in);
+    out[0] = F->nnzL_total;
+    out[1] = (long long)F->pclass.size();
+    long long mx = 0;
+    for (auto& C : F->classes) mx = std::max<long long>(mx, C.nnzL);
+    out[2] = mx;
+    return 0;
+  } catch (const std::exception& e) {
+    snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}
+
 // 1D basis tables of the product (for cross-checks against the oracle's basis)
 int emu_basis(int p, double* S, double* lam, double* B, double* A, double* D, double* G) {
   const Basis1D& b = basis(p);

@@ -122,3 +122,25 @@ def test_product_patch_programs_match_oracle(emu, name, w, dim, fact, interior):
         zo[g] += S.solve(r[g])
     tol = 1e-11 if w.space != 2 else 1e-10   # H(div) face stars: cond(A_II) ~ 5e4 at this size
     assert np.linalg.norm(z - zo) / np.linalg.norm(zo) < tol
+
+
+# ------------------------------------------------------------ algorithmic factor size (rm_info)
+@pytest.mark.parametrize("name,k,p,n,gamma,dim,fact,interior,total,largest", [
+    # SURVEY 8(a) rows a5/a6 [V]: cfg1 sum of nnz(L) = 51,121; a full cfg2 vertex patch (Q7,
+    # (2p-1)^3 = 2197 DoFs) 70,183; a full cfg5 ICC-SC mask (Q15, 24,389 DoFs) 160,889
+    ("cfg1", 0, 3, 4, 63, 0, 0, 0, 51121, None),
+    ("cfg2-full-patch", 0, 7, 2, 0, 0, 0, 1, 70183, 70183),
+    ("cfg5-full-patch-iccsc", 0, 15, 2, 0, 0, 1, 1, 160889, 160889),
+])
+def test_algorithmic_factor_nnz_matches_survey(emu, name, k, p, n, gamma, dim, fact, interior, total, largest):
+    """The roofline's algorithmic bytes (bench.py) count nnz(L) of the exact Cholesky factor in
+    the pinned order (reading G6), or of the ICC-SC mask, per patch -- not the product's stored
+    format.  Checked against the counts SURVEY.md 8(a) verified independently."""
+    emu.emu_family_nnz.argtypes = [ctypes.c_int] * 5 + [ctypes.c_uint] + [ctypes.c_int] * 3 + [
+        ctypes.POINTER(ctypes.c_longlong), ctypes.c_char_p, ctypes.c_int]
+    out = (ctypes.c_longlong * 3)()
+    err = ctypes.create_string_buffer(256)
+    assert emu.emu_family_nnz(k, p, n, n, n, gamma, dim, fact, interior, out, err, 256) == 0, err.value
+    assert out[0] == total
+    if largest is not None:
+        assert out[2] == largest
