@@ -1,0 +1,367 @@
+"""Round-2 pins of the oracle parts VERDICT r1 listed as unpinned (CPU only).
+
+  * the k = 1, 2 operators ASSEMBLED BY QUADRATURE (oracle/fem.py reference_fields / pullbacks):
+    discrete complex K^1 D^0 = 0 and K^2 D^1 = 0 (curl grad = 0, div curl = 0; P:565-586,
+    eq:gradbasis..eq:divbasis) on Cartesian AND perturbed trilinear cells (the pullbacks F^k commute
+    with d), plus closed forms of M^1, M^2, K^1, K^2 on a box cell built from Kronecker
+    products of the 1D tables (eq:sum-factorization);
+  * the PH potential operator B (oracle/solver.py Problem.potential, eq:asm-hiptmair P:961-975):
+    for k = 1 it equals the H(grad) operator with (alpha', beta') = (beta, 0), for k = 2 the H(curl)
+    operator with (beta, eps_s beta) (remark P:916-927, reading G8); iteration counts of PH
+    stay flat from beta = 1 to beta = 1e-8 and blow up when the stage is dropped;
+  * G-bar (oracle/basis1d.py, reading G4): symmetric square root of B-hat_GG with the
+    closed form from B-hat_00, B-hat_0p;
+  * star windows (oracle/patches.py): the structured windows equal the DEFINITION
+    {free DoFs whose support lies in the star}, with support read off the cell -> DoF map;
+  * the ICC breakdown restart (reading G7) on a crafted matrix that breaks down.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import rm_inputs as ri
+from oracle.basis1d import fdm_basis
+from oracle.fem import (FAMILIES, P_FAM, Space, assemble, element_matrix, global_derivative, kron3,
+                        ref_derivative_pattern_or_values)
+from oracle.patches import ICCSCPatch, all_patches, entities, icc_masked, patch_dofs
+from oracle.solver import Problem
+
+
+def _grid(n, perturb, cfg=9):
+    w = ri.Workload(cfg, 0, 1, n, n, n, "one", 1.0, 0, perturb, "pafw", "chol")
+    return ri.vertex_coords(w)
+
+
+def _box(h):
+    X = np.zeros((2, 2, 2, 3))
+    for az in range(2):
+        for ay in range(2):
+            for ax in range(2):
+                X[az, ay, ax] = (ax * h[0], ay * h[1], az * h[2])
+    return X
+
+
+# ----------------------------------------------------------------- quadrature complex property
+@pytest.mark.parametrize("k,p,perturb", [(1, 2, 0.0), (1, 3, 0.15), (2, 2, 0.0), (2, 3, 0.15)])
+def test_quadrature_operators_annihilate_the_previous_derivative(k, p, perturb):
+    """K^k D^{k-1} = 0 with K^k = the d^k-part of A assembled BY QUADRATURE through the pullbacks
+    (alpha = 1, beta = 0) and D^{k-1} the tabulated exterior derivative: curl grad = 0 (k = 1) and
+    div curl = 0 (k = 2), to round-off, also on non-affine trilinear cells."""
+    n = 2
+    X = _grid(n, perturb)
+    K = assemble(Space(k, p, n, n, n), X, np.ones((n, n, n)), np.zeros((n, n, n)))
+    D = global_derivative(k - 1, p, n, n, n)
+    KD = (K @ D).toarray()
+    scale = abs(K).max() * abs(D).max()
+    assert np.abs(KD).max() < 1e-12 * scale
+    # and the test has teeth: K is not itself zero on the range of D's complement
+    assert np.abs(K.toarray()).max() > 1e-3
+
+
+def test_flipped_curl_component_breaks_the_complex(monkeypatch):
+    """Negative control: flipping the sign of ONE term of the reference curl (the d_z f term of
+    curl(f e_x), a plausible transcription slip of eq:curlbasis) makes K^1 D^0 = 0 fail.  (Flipping a
+    whole output component would not: it leaves C^T M C unchanged.)"""
+    import oracle.fem as fem
+    orig = fem.reference_fields
+
+    def flipped(k, p, nq, qz_slice=None):
+        val, der = orig(k, p, nq, qz_slice)
+        if k == 1:
+            der = der.copy()
+            nx_ = der.shape[2] // 3
+            der[:, 1, :nx_] *= -1.0
+        return val, der
+
+    monkeypatch.setattr(fem, "reference_fields", flipped)
+    fem._cartesian_parts.cache_clear()
+    try:
+        n, p = 2, 2
+        K = assemble(Space(1, p, n, n, n), _grid(n, 0.0), np.ones((n, n, n)), np.zeros((n, n, n)))
+        D = global_derivative(0, p, n, n, n)
+        assert np.abs((K @ D).toarray()).max() > 1e-3 * abs(K).max() * abs(D).max()
+    finally:
+        fem._cartesian_parts.cache_clear()
+
+
+def _blockdiag(blocks):
+    n = sum(b.shape[0] for b in blocks)
+    out = np.zeros((n, n))
+    o = 0
+    for b in blocks:
+        out[o:o + b.shape[0], o:o + b.shape[0]] = b
+        o += b.shape[0]
+    return out
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_box_cell_matrices_closed_form(k):
+    """On a box with sides (hx, hy, hz) (J = diag(h)/2) every pullback is a diagonal scaling, so
+    (eq:sum-factorization P:690-699) with B-hat the P-family mass and I the DP mass
+    (orthonormal DP basis):
+      M^0 = |J| B(x)B(x)B;          M^1_m = |J| (2/h_m)^2 (x)_d T_d;   M^2_m = |J|^-1 (h_m/2)^2 (x)_d T_d;
+      M^3 = |J|^-1 I;               K^k = D_k^T M^{k+1} D_k  (D_k the Kronecker-tabulated d-hat)
+    each assembled independently of the quadrature code (reference_fields / pullback_fields)."""
+    p = 3
+    h = (0.5, 0.8, 1.3)
+    X = _box(h)
+    f = fdm_basis(p)
+    detJ = h[0] * h[1] * h[2] / 8.0
+
+    def mass(kk):
+        blocks = []
+        for m, fam in enumerate(FAMILIES[kk]):
+            t = [f.B if fm == P_FAM else np.eye(p) for fm in fam]
+            if kk == 0:
+                s = detJ
+            elif kk == 1:
+                s = detJ * (2.0 / h[m]) ** 2
+            elif kk == 2:
+                s = (h[m] / 2.0) ** 2 / detJ
+            else:
+                s = 1.0 / detJ
+            blocks.append(s * kron3(t[2], t[1], t[0]))
+        return _blockdiag(blocks)
+
+    M = element_matrix(k, p, X, 0.0, 1.0)
+    K = element_matrix(k, p, X, 1.0, 0.0)
+    Dk = ref_derivative_pattern_or_values(k, p, values=True)
+    Mref = mass(k)
+    Kref = Dk.T @ mass(k + 1) @ Dk
+    assert np.abs(M - Mref).max() < 1e-13 * np.abs(Mref).max()
+    assert np.abs(K - Kref).max() < 1e-12 * np.abs(Kref).max()
+
+
+# ------------------------------------------------------------------------------ PH potential
+@pytest.mark.parametrize("k", [1, 2])
+def test_potential_operator_is_the_lower_form_operator(k):
+    """B = D^T A^k D (+ eps_s beta M^{k-1} for k = 2) equals the (k-1)-form operator with
+    coefficients (alpha', beta') = (beta, 0) for k = 1 and (beta, eps_s beta) for k = 2 (because
+    D^T K^k D = 0 and D^T M^k D = K^{k-1}), restricted to the free potential DoFs."""
+    w = ri.CONFIGS[2 + k].with_mesh(2).with_p(3)
+    beta = np.full((2, 2, 2), 0.37)
+    pb = Problem(k, 3, 2, 2, 2, ri.vertex_coords(w), np.full((2, 2, 2), 2.5), beta, w.gamma_d,
+                 decomposition="ph")
+    D, pcon, _ = pb.potential()
+    pspace = Space(k - 1, 3, 2, 2, 2)
+    Af = assemble(pb.space, pb.X, pb.alpha, pb.beta)
+    B = (D.T @ Af @ D).toarray()
+    if k == 2:
+        B = B + pb.potential_shift * assemble(pspace, pb.X, np.zeros_like(beta), beta).toarray()
+    ref = assemble(pspace, pb.X, beta, (pb.potential_shift if k == 2 else 0.0) * beta).toarray()
+    free = ~pcon
+    Bf, Rf = B[np.ix_(free, free)], ref[np.ix_(free, free)]
+    assert np.abs(Bf - Rf).max() < 1e-11 * np.abs(Rf).max()
+
+
+def _ph_iterations(k, p, n, beta, with_stage=True):
+    w = ri.CONFIGS[2 + k].with_mesh(n).with_p(p)
+    pb = Problem(k, p, n, n, n, ri.vertex_coords(w), np.ones((n, n, n)), np.full((n, n, n), beta), w.gamma_d,
+                 decomposition="ph")
+    if not with_stage:   # drop the potential stage: only the k-star patches remain
+        pb.decomposition = "ph-no-potential"   # Problem.precondition runs the stage only for "ph"
+    f = ri.uniform_vector(10 + k, 0, pb.space.ndof)
+    f[pb.constrained] = 0.0
+    _, it, rel = pb.pcg(f, maxit=400)
+    return it, rel
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_ph_iterations_robust_in_beta_and_stage_needed(k):
+    """PH relaxation is robust as beta -> 0 (P:1306-1313 report flat counts from beta = 1 to
+    1e-8); without the potential stage the near-kernel of d^k is unresolved and the count grows."""
+    it1, r1 = _ph_iterations(k, 2, 3, 1.0)
+    it8, r8 = _ph_iterations(k, 2, 3, 1e-8)
+    assert r1 <= 1e-8 and r8 <= 1e-8
+    assert it1 // 2 <= it8 <= it1 + 3, (it1, it8)   # no growth as beta -> 0 (one-level: no coarse term)
+    itn, _ = _ph_iterations(k, 2, 3, 1e-8, with_stage=False)
+    assert itn >= 2 * it8, (it8, itn)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_ph_iterations_scale_invariant(k):
+    """Counts depend only on alpha / beta: (alpha, beta) -> 1e3 (alpha, beta)."""
+    n, p = 2, 3
+    w = ri.CONFIGS[2 + k].with_mesh(n).with_p(p)
+    its = []
+    for c in (1.0, 1e3):
+        pb = Problem(k, p, n, n, n, ri.vertex_coords(w), np.full((n, n, n), c), np.full((n, n, n), 0.3 * c),
+                     w.gamma_d, decomposition="ph")
+        f = ri.uniform_vector(20 + k, 0, pb.space.ndof)
+        f[pb.constrained] = 0.0
+        its.append(pb.pcg(f)[1])
+    assert its[0] == its[1]
+
+
+# ---------------------------------------------------------------------------------- G-bar
+@pytest.mark.parametrize("p", [2, 3, 6, 7, 8, 15])
+def test_gbar_is_the_symmetric_square_root(p):
+    """Reading G4: G-bar_GG = B-hat_GG^{1/2}, the SYMMETRIC (Loewdin) root.  B-hat_GG =
+    [[d, o], [o, d]] with d = 2/(p(p+2)), o = (-1)^{p+1} 2/(p(p+1)(p+2)) (pinned in
+    test_oracle_basis), so G_GG = [[a, b], [b, a]] with a, b = (sqrt(d+o) +- sqrt(d-o))/2.  A
+    Cholesky-type orthonormalisation (triangular) also satisfies G^-T B G^-1 = I but fails here."""
+    f = fdm_basis(p)
+    d = 2.0 / (p * (p + 2))
+    o = (-1) ** (p + 1) * 2.0 / (p * (p + 1) * (p + 2))
+    a = (math.sqrt(d + o) + math.sqrt(d - o)) / 2
+    b = (math.sqrt(d + o) - math.sqrt(d - o)) / 2
+    G = f.G
+    GG = G[np.ix_([0, p], [0, p])]
+    np.testing.assert_allclose(GG, [[a, b], [b, a]], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(GG @ GG, f.B[np.ix_([0, p], [0, p])], rtol=1e-12, atol=1e-15)
+    inner = [i for i in range(p + 1) if i not in (0, p)]
+    np.testing.assert_array_equal(G[np.ix_(inner, inner)], np.eye(p - 1))
+    assert np.abs(G[np.ix_(inner, [0, p])]).max() == 0.0
+
+
+def test_gbar_closed_form_p2():
+    """p = 2: B-hat_GG = [[1/4, -1/12], [-1/12, 1/4]]: eigenvalues 1/6 on (1,1) and
+    1/3 on (1,-1), so G_GG = sqrt(1/6) P+ + sqrt(1/3) P-."""
+    G = fdm_basis(2).G
+    a = (math.sqrt(1 / 6) + math.sqrt(1 / 3)) / 2
+    b = (math.sqrt(1 / 6) - math.sqrt(1 / 3)) / 2
+    np.testing.assert_allclose(G[np.ix_([0, 2], [0, 2])], [[a, b], [b, a]], rtol=1e-14)
+
+
+# ----------------------------------------------------------------------------- star windows
+def _support_cells(space):
+    """support(g) = the cells K whose local basis contains g (read off cell_dofs, not windows)."""
+    sup = [set() for _ in range(space.ndof)]
+    for cz in range(space.nz):
+        for cy in range(space.ny):
+            for cx in range(space.nx):
+                for g in space.cell_dofs(cx, cy, cz):
+                    sup[int(g)].add((cx, cy, cz))
+    return sup
+
+
+def _star_cells(ent, n):
+    """Cells whose closure contains the entity (the star)."""
+    per = []
+    for d, (kind, v) in enumerate(ent):
+        per.append([v] if kind == "cell" else [c for c in (v - 1, v) if 0 <= c < n[d]])
+    return {(cx, cy, cz) for cz in per[2] for cy in per[1] for cx in per[0]}
+
+
+def _dof_entity(space, g):
+    """The entity whose interior carries DoF g: per direction a P-family index at a multiple of p
+    sits on the node index / p, any other index inside cell index // p (DP indices are always
+    cell-interior).  From the tensor-product structure of eq:hgrad-basis..eq:hdiv-basis."""
+    off = space.offsets()
+    m = int(np.searchsorted(off, g, side="right") - 1)
+    Lz, Ly, Lx = space.comp_shape(m)
+    r = g - off[m]
+    idx = (r % Lx, (r // Lx) % Ly, r // (Lx * Ly))
+    ent = []
+    for d in range(3):
+        i = int(idx[d])
+        if space.fams[m][d] == P_FAM and i % space.p == 0:
+            ent.append(("node", i // space.p))
+        else:
+            ent.append(("cell", i // space.p))
+    return tuple(ent)
+
+
+def _in_star(e, j):
+    """e lies in the star of j (the entities that contain j as a (recursive)
+    sub-entity, j included): per direction, a node of j must be a node of e or an endpoint of e's
+    cell; a cell direction of j must be the same cell of e."""
+    for (ke, ve), (kj, vj) in zip(e, j):
+        if kj == "node":
+            if not ((ke == "node" and ve == vj) or (ke == "cell" and ve in (vj - 1, vj))):
+                return False
+        elif not (ke == "cell" and ve == vj):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("k,dim", [(0, 0), (1, 1), (1, 0), (2, 2), (2, 1), (2, 0)])
+def test_windows_equal_the_star_definition(k, dim):
+    """V_h|_{star j} = {v : supp v in star j}: the star is OPEN (the patch of cells
+    "excluding the boundary of the patch"), so a basis function belongs iff its carrying
+    entity lies in the star.  Over every entity of a 3^3 mesh with mixed boundary conditions
+    (Dirichlet on x=0, y=1, z=0) the oracle's structured windows, after removing constrained DoFs,
+    must be exactly that set; and every member's support (read off the cell -> DoF map, not the
+    windows) lies in the star's cells."""
+    p, n = 3, 3
+    space = Space(k, p, n, n, n)
+    gamma = 0b011001
+    con = space.constrained_mask(gamma)
+    sup = _support_cells(space)
+    ent_of = [_dof_entity(space, g) for g in range(space.ndof)]
+    ents = entities(space, dim)
+    assert len(ents) > 0
+    for ent in ents:
+        star = _star_cells(ent, (n, n, n))
+        want = {g for g in range(space.ndof) if not con[g] and _in_star(ent_of[g], ent)}
+        got, _ = patch_dofs(space, ent, con)
+        assert set(int(x) for x in got) == want, ent
+        assert len(got) == len(want)
+        assert all(sup[g] <= star for g in want)
+
+
+# ------------------------------------------------------------------------- ICC restart (G7)
+def _breakdown_example():
+    """A symmetric positive definite matrix and a lower mask on which masked ICC breaks down,
+    found by a deterministic search using only oracle.patches.icc_masked."""
+    rng = np.random.default_rng(0)
+    for _ in range(20000):
+        n = 5
+        v = rng.integers(-3, 4, size=(n, n)).astype(float)
+        A = np.tril(v, -1)
+        A = A + A.T
+        A += np.eye(n) * (np.ceil(-np.linalg.eigvalsh(A).min()) + 1)
+        mask = np.tril(A != 0)
+        offs = [(i, j) for i in range(n) for j in range(i) if mask[i, j]]
+        if not offs:
+            continue
+        i, j = offs[rng.integers(len(offs))]
+        mask[i, j] = False
+        try:
+            icc_masked(sp.csr_matrix(A), sp.csr_matrix(mask.astype(float)))
+        except FloatingPointError:
+            return A, mask
+    raise AssertionError("no breakdown example found")
+
+
+def _icc_ok(A, mask):
+    try:
+        icc_masked(sp.csr_matrix(A), sp.csr_matrix(mask.astype(float)))
+        return True
+    except FloatingPointError:
+        return False
+
+
+def test_icc_breakdown_restart_reading_g7():
+    """Reading G7: on breakdown ICC restarts with P + sigma diag(P), sigma = 1e-10
+    doubling.  The crafted matrix A_t = A + t diag(A) sits just below the breakdown threshold t* of
+    a matrix that breaks down, so the restart runs and must stop at the FIRST sigma of the
+    sequence that succeeds; the factor then satisfies the masked definition (L L^T)_ij = a_ij + sigma
+    diag on the mask."""
+    A, mask = _breakdown_example()
+    D = np.diag(np.diag(A))
+    lo, hi = 0.0, 1.0
+    while _icc_ok(A + hi * D, mask) is False:
+        hi *= 2
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if _icc_ok(A + mid * D, mask):
+            hi = mid
+        else:
+            lo = mid
+    t = lo - 1e-7 * (1 + lo)        # below the threshold: breaks down, rescued by sigma ~ 1e-7
+    At = A + t * D
+    assert not _icc_ok(At, mask)
+    pat = sp.csr_matrix((mask | mask.T).astype(float))
+    P = ICCSCPatch(sp.csr_matrix(At), pat, np.zeros(len(A), dtype=bool))
+    sig = 1e-10
+    while not _icc_ok(At + sig * np.diag(np.diag(At)), mask):
+        sig *= 2
+    assert P.sigma == sig and 1e-9 < P.sigma < 1e-2
+    L = P.L.toarray()
+    As = At + P.sigma * np.diag(np.diag(At))
+    LLt = L @ L.T
+    assert np.abs((LLt - As)[mask]).max() < 1e-12 * np.abs(As).max()
+    assert np.all(L[~mask] == 0.0)
