@@ -540,7 +540,30 @@ def broken_G3(k, p):
     return G
 
 
-def aux_element_matrix(p, Xc, alpha, beta, nq=None):
+def _kron3_sparse(Tz, Ty, Tx):
+    """kron3 as a sparse matrix (same ordering, x fastest); for the high-p Kronecker factors."""
+    return sp.kron(sp.csr_matrix(Tz), sp.kron(sp.csr_matrix(Ty), sp.csr_matrix(Tx), format="csr"), format="csr")
+
+
+def broken_G3_sparse(k, p):
+    """broken_G3 as a sparse matrix (the same Kronecker products; dense would be 11,520^2 at p = 15)."""
+    f = fdm_basis(p)
+    blocks = []
+    for fam in FAMILIES[k]:
+        t = [f.G if fm == P_FAM else np.eye(p) for fm in fam]
+        blocks.append(_kron3_sparse(t[2], t[1], t[0]))
+    return sp.block_diag(blocks, format="csr")
+
+
+def grad_ref_sparse(p):
+    """The reference gradient d-hat^0 (V^0 -> V^1 local orders) as a sparse matrix: the same blocks
+    as ref_derivative_pattern_or_values(0, p, values=True), eq:gradbasis."""
+    f = fdm_basis(p)
+    IP = np.eye(p + 1)
+    return sp.vstack([_kron3_sparse(IP, IP, f.D), _kron3_sparse(IP, f.D, IP), _kron3_sparse(f.D, IP, IP)], format="csr")
+
+
+def aux_element_matrix(p, Xc, alpha, beta, nq=None, sparse=False):
     """P_K for k=0 (eq:sum-factorization_approx):
         diag(M-bar^0_beta)_a       = sum_q w_q beta detJ psi-bar_a^2
         diag(M-bar^1_alpha)_(m,a)  = sum_q w_q alpha detJ (J^{-1} J^{-T})_mm Psi-bar^(m)_a^2
@@ -565,32 +588,29 @@ def aux_element_matrix(p, Xc, alpha, beta, nq=None):
         tabs = [kron3(sb[sl], sb, r), kron3(sb[sl], r, sb), kron3(r[sl], sb, sb)]
         for m in range(3):
             diag1[m] += (w * alpha * JiJit[:, m, m]) @ (tabs[m] ** 2)
-    G0 = broken_G3(0, p)
-    G1 = broken_G3(1, p)
-    D = ref_derivative_pattern_or_values(0, p, values=True)
-    Db = G1 @ D
+    G0 = broken_G3_sparse(0, p)
+    Db = broken_G3_sparse(1, p) @ grad_ref_sparse(p)
     d1 = np.concatenate(diag1)
-    return G0.T @ (diag0[:, None] * G0) + Db.T @ (d1[:, None] * Db)
+    PK = G0.T @ sp.diags(diag0) @ G0 + Db.T @ sp.diags(d1) @ Db
+    return PK.tocsr() if sparse else PK.toarray()
 
 
 def aux_cell_pattern(p):
-    """Structural pattern of P_K: pattern(G)^T pattern(G) U pattern(G1 D)^T pattern(G1 D)."""
+    """Structural pattern of P_K: pattern(G)^T pattern(G) U pattern(G1 D)^T pattern(G1 D)
+    (0/1 Kronecker products, sparse)."""
     # G-bar_1D pattern is B-hat's pattern (identity + (0,p) corner)
     PB = pattern_B(p).astype(np.int64)
-    G0 = kron3(PB, PB, PB)
+    G0 = _kron3_sparse(PB, PB, PB)
     blocks = []
     for fam in FAMILIES[1]:
         t = [PB if fm == P_FAM else _I(p) for fm in fam]
-        blocks.append(kron3(t[2], t[1], t[0]))
-    n = sum(b.shape[0] for b in blocks)
-    G1 = np.zeros((n, n), dtype=np.int64)
-    o = 0
-    for b in blocks:
-        G1[o:o + b.shape[0], o:o + b.shape[0]] = b
-        o += b.shape[0]
-    D = ref_derivative_pattern_or_values(0, p, values=False).astype(np.int64)
+        blocks.append(_kron3_sparse(t[2], t[1], t[0]))
+    G1 = sp.block_diag(blocks, format="csr")
+    PD = pattern_D(p).astype(np.int64)
+    IP = _I(p + 1)
+    D = sp.vstack([_kron3_sparse(IP, IP, PD), _kron3_sparse(IP, PD, IP), _kron3_sparse(PD, IP, IP)], format="csr")
     Db = G1 @ D
-    return (G0.T @ G0 + Db.T @ Db) != 0
+    return ((G0.T @ G0 + Db.T @ Db) != 0).toarray()
 
 
 def assemble_aux(space: Space, X, alpha, beta):
@@ -602,10 +622,10 @@ def assemble_aux(space: Space, X, alpha, beta):
         for cy in range(space.ny):
             for cx in range(space.nx):
                 Xc = cell_vertices(X, cx, cy, cz)
-                PK = aux_element_matrix(space.p, Xc, alpha[cz, cy, cx], beta[cz, cy, cx])
+                PK = aux_element_matrix(space.p, Xc, alpha[cz, cy, cx], beta[cz, cy, cx], sparse=True)
                 g = space.cell_dofs(cx, cy, cz)
                 r, c = np.nonzero(pat)
-                rows.append(g[r]); cols.append(g[c]); vals.append(PK[r, c])
+                rows.append(g[r]); cols.append(g[c]); vals.append(np.asarray(PK[r, c]).ravel())
     n = space.ndof
     R, C, V = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
     P = sp.csr_matrix((V, (R, C)), shape=(n, n))

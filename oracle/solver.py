@@ -8,6 +8,8 @@
             B = D^T A D (k=1), B = D^T A D + eps_s beta M^{k-1} (k=2, remark P:916-927, reading G8)
       u_out = u + omega c                                   (reading G9)
   For the auxiliary-operator variant the patch matrices come from P instead of A.
+  With `coarse`, PCG's preconditioner is the hybrid V(1,1) cycle with the p = 1 coarse level
+  (oracle/coarse.py, reading G20).
   PCG: zero initial guess, stop at the first k with
       sqrt(r_k^T z_k) <= rtol sqrt(r_0^T z_0)  (natural P^{-1} norm), iters = k (reading G15).
 
@@ -43,6 +45,7 @@ class Problem:
     interior_only: bool = False
     matfree: bool = False            # apply A cell by cell (large p) instead of via CSR
     potential_shift: float = EPS_S   # eps_s of reading G8 (k = 2 PH)
+    coarse: bool = False             # p = 1 coarse level + hybrid V(1,1) in pcg / cycle (oracle.coarse)
     space: Space = field(init=False)
     constrained: np.ndarray = field(init=False)
     free: np.ndarray = field(init=False)
@@ -54,6 +57,7 @@ class Problem:
         self._A = None
         self._patches = None
         self._pot = None
+        self._coarse = None
 
     # ---------------------------------------------------------------- operator
     @property
@@ -143,6 +147,16 @@ class Problem:
             c += D @ s
         return np.where(self.free, c, 0.0)
 
+    def cycle(self, r):
+        """The PCG preconditioner: the one-level additive sweep, or with `coarse` the hybrid
+        V(1,1) cycle of oracle.coarse."""
+        if not self.coarse:
+            return self.precondition(r)
+        from .coarse import CoarseLevel, smoother_colours, vcycle
+        if self._coarse is None:
+            self._coarse = CoarseLevel(self)
+        return vcycle(self, self._coarse, r, 1.0 / smoother_colours(self.k, self.decomposition))
+
     def relax(self, f, u, omega=1.0):
         r = self.residual(f, u)
         return u + omega * self.precondition(r)
@@ -151,7 +165,7 @@ class Problem:
         f = np.where(self.free, f, 0.0)
         x = np.zeros_like(f)
         r = f.copy()
-        z = self.precondition(r)
+        z = self.cycle(r)
         rz = float(r @ z)
         rz0 = rz
         if rz0 == 0.0:
@@ -162,7 +176,7 @@ class Problem:
             a = rz / float(pdir @ q)
             x += a * pdir
             r -= a * q
-            z = self.precondition(r)
+            z = self.cycle(r)
             rz_new = float(r @ z)
             rel = math.sqrt(max(rz_new, 0.0) / rz0)
             if rel <= rtol:

@@ -481,6 +481,17 @@ rm::OpParams make_op(const rm::Space& sp, uint32_t gamma) {
     }
     op.rowptr[m][M.rows] = (short)nz;
   }
+  {   // B-hat and D-hat with their structural zeros exact (reading G18), for the line kernels
+    const rm::Basis1D& b = rm::basis(sp.p);
+    const int n = sp.p + 1;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const bool pat = (i == j) || ((i == 0 || i == sp.p) && (j == 0 || j == sp.p));
+        op.Bh[i * n + j] = pat ? b.B[i * n + j] : 0.0;
+      }
+    for (int i = 0; i < sp.p; ++i)
+      for (int j = 0; j < n; ++j) op.Dh[i * n + j] = (j == 0 || j == sp.p || j == i) ? b.D[i * n + j] : 0.0;
+  }
   if (sp.k == 0) {   // x-stiffness term: X = A-hat, Y = Z = B-hat
     for (int t = 0; t < op.nterms; ++t) {
       const rm::Term& T = co.terms[t];
@@ -686,6 +697,9 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
       c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
+    } else if (space >= 1) {
+      // Cartesian H(curl) / H(div): one apply launch over all cells + the skeleton gather
+      c->d_cellbuf = c->dalloc(rm::kform_cellbuf_doubles(space, p, c->n));
     } else if (space == 0 && rm::exp_env("RM_APPLY_CELLBUF")) {
       // Cartesian H(grad), opt-in: one apply launch over all cells, interior DoFs stored directly,
       // skeleton entries through the cell buffer and the gather (measured: apply 0.28 -> 0.19 ms at

@@ -352,6 +352,8 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt,
                                    double* cellbuf) {
+  if (op.k >= 1 && cellbuf)   // H(curl) / H(div): pointwise-stage kernels, one launch + gather
+    return launch_apply_kform(op, alpha, beta, coef_const, hpow, u, f, out, ndof, cellbuf, st, nlaunch, kt);
   const bool cb = cellbuf && op.k == 0;   // cell-buffer mode: no init, no colours, a gather at the end
   int nl = 0;
   if (!cb) {

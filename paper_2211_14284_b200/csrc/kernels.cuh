@@ -30,6 +30,8 @@ struct OpParams {
   // k = 0: the two 1D matrices of the H(grad) operator, B-hat and A-hat = D-hat^T D-hat,
   // (p+1)^2 row-major with structural zeros exact (used by the specialised apply_q kernel)
   double Bh[RM_MAXP1 * RM_MAXP1], Ah[RM_MAXP1 * RM_MAXP1];
+  // D-hat (p x (p+1), row-major, structural zeros exact): the H(curl) / H(div) kernels
+  double Dh[RM_MAXP1 * RM_MAXP1];
   short rowptr[RM_MAXMATS][RM_MAXP1 + 1];
   unsigned char col[RM_MAXMATS][RM_MAXMATNZ];
   double val[RM_MAXMATS][RM_MAXMATNZ];
@@ -85,6 +87,12 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
                                    const KTimer* kt = nullptr);
 // doubles of the per-cell result buffer the trilinear apply needs (apply_tri.cu)
 size_t tri_cellbuf_doubles(const TriParams& tp);
+// H(curl) / H(div) Cartesian apply (apply_kform.cu): one launch over all cells, interior entries
+// stored as f + sign A u, skeleton entries through `cellbuf` (kform_cellbuf_doubles) and a gather
+cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const double* beta, int coef_const,
+                               const double* hpow, const double* u, const double* f, double* out, long long ndof,
+                               double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt);
+size_t kform_cellbuf_doubles(int k, int p, const int* n);
 // out = f (or 0) with constrained entries zeroed (apply.cu)
 cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, long long ndof, cudaStream_t st);
 

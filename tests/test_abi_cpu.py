@@ -120,7 +120,11 @@ def test_product_patch_programs_match_oracle(emu, name, w, dim, fact, interior):
     zo = np.zeros(nd)
     for g, S in pb.patch_solvers():
         zo[g] += S.solve(r[g])
-    tol = 1e-11 if w.space != 2 else 1e-10   # H(div) face stars: cond(A_II) ~ 5e4 at this size
+    tol = 1e-11
+    if w.space == 2:   # H(div): 10x the oracle's own assembly noise (tests/golden/cfg4_conditioning.json)
+        import json
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", "cfg4_conditioning.json")))["cases"]
+        tol = max(1e-11, 10 * g[f"{w.nx}^3-p{w.p}"]["oracle_vs_closed_form_assembly_sweep_rel"])
     assert np.linalg.norm(z - zo) / np.linalg.norm(zo) < tol
 
 

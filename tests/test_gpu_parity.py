@@ -48,24 +48,47 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
+def check(name, err, tol):
+    from conftest import record_parity
+    record_parity(name, err, tol)
+    assert err < tol, (name, err, tol)
+
+
+def hdiv_tol(key):
+    """H(div) tolerance: 10x the difference between two equally exact ORACLE
+    assemblies of the same sweep (quadrature vs the box closed form), floored at the north-star
+    1e-11 -- scripts/cfg4_conditioning.py, tests/golden/cfg4_conditioning.json."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg4_conditioning.json")))["cases"][key]
+    return max(1e-11, 10 * g["oracle_vs_closed_form_assembly_sweep_rel"])
+
+
 CASES = [
     ("cfg1", ri.CONFIGS[1], 1e-11),
     ("cfg2-3^3", ri.CONFIGS[2].with_mesh(3), 1e-11),
     ("cfg2-2x3x4-p4", ri.CONFIGS[2].with_mesh(2, 3, 4).with_p(4), 1e-11),
     ("cfg3-2^3-p3", ri.CONFIGS[3].with_mesh(2).with_p(3), 1e-11),
     ("cfg3-2^3-p6", ri.CONFIGS[3].with_mesh(2), 1e-11),
-    ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), 1e-10),
-    ("cfg4-3^3-p4", ri.CONFIGS[4].with_mesh(3).with_p(4), 1e-10),
+    ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), hdiv_tol("2^3-p3")),
+    ("cfg4-3^3-p4", ri.CONFIGS[4].with_mesh(3).with_p(4), hdiv_tol("3^3-p4")),
+    ("cfg4-2^3-p8", ri.CONFIGS[4].with_mesh(2), hdiv_tol("2^3-p8")),   # cfg4's own degree
     # trilinear cells (perturbed vertices): true operator by quadrature, auxiliary-operator
     # patches with ICC on the static-condensation pattern (cfg5 shapes at reduced size)
     ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3), 1e-11),
     ("cfg5-2^3-p7", ri.CONFIGS[5].with_mesh(2).with_p(7), 1e-11),
+    ("cfg5-2^3-p15", ri.CONFIGS[5].with_mesh(2), 1e-11),             # cfg5's own degree (n_q = 24)
 ]
+# the one-box-buffer sequential schedule of the patch kernel (taken by full-size cfg4) forced
+NBOX1_CASES = [("nbox1-" + c[0], c[1], c[2]) for c in CASES if c[0] in ("cfg2-3^3", "cfg3-2^3-p3", "cfg4-2^3-p3",
+                                                                       "cfg5-3^3-p3", "cfg4-3^3-p4")]
 
 
-@pytest.mark.parametrize("name,w,tol", CASES, ids=[c[0] for c in CASES])
-def test_apply_and_sweep_parity(dev, name, w, tol):
+@pytest.mark.parametrize("name,w,tol", CASES + NBOX1_CASES, ids=[c[0] for c in CASES + NBOX1_CASES])
+def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
     import paper_2211_14284_b200 as rmb
+    if name.startswith("nbox1-"):
+        monkeypatch.setenv("RM_NBOX1", "1")   # read by the patch plan at setup (include/rm.h)
     ctx, pb = setup_pair(w)
     assert (ctx.constrained_mask() == pb.constrained).all()
     assert ctx.n_free == int(pb.free.sum())
@@ -73,13 +96,13 @@ def test_apply_and_sweep_parity(dev, name, w, tol):
     ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
     v = torch.empty_like(ut)
     rmb.rm_apply(ctx, ut, v)
-    assert rel(v.cpu().numpy(), pb.apply(u)) < 1e-11
+    check(name + " apply", rel(v.cpu().numpy(), pb.apply(u)), 1e-11)
     rmb.rm_residual(ctx, ft, ut, v)
-    assert rel(v.cpu().numpy(), pb.residual(f, u)) < 1e-11
+    check(name + " residual", rel(v.cpu().numpy(), pb.residual(f, u)), 1e-11)
     out = torch.empty_like(ut)
     for omega in (1.0, 0.7):
         rmb.rm_relax(ctx, ft, ut, out, omega)
-        assert rel(out.cpu().numpy(), pb.relax(f, u, omega)) < tol
+        check(f"{name} relax w={omega}", rel(out.cpu().numpy(), pb.relax(f, u, omega)), tol)
     # in-place (u_out aliases u_in) equals out-of-place
     u2 = ut.clone()
     rmb.rm_relax(ctx, ft, u2, u2, 0.7)
@@ -102,8 +125,8 @@ def test_pcg_iterations(dev, name, w):
     it, relres, ok = rmb.rm_pcg(ctx, torch.tensor(f, device=dev), x, 1e-8, 500)
     xo, ito, _ = pb.pcg(f)
     assert ok and relres <= 1e-8
-    assert abs(it - ito) <= 1
-    assert rel(x.cpu().numpy(), xo) < 1e-7
+    check(f"{name} pcg iters {it} vs oracle {ito}", abs(it - ito), 1.5)
+    check(f"{name} pcg solution", rel(x.cpu().numpy(), xo), 1e-7)
 
 
 def test_precondition_and_host_entry_points(dev):
@@ -113,10 +136,10 @@ def test_precondition_and_host_entry_points(dev):
     f, u = vecs(w, ctx)
     z = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
     rmb.rm_precondition(ctx, torch.tensor(f, device=dev), z)
-    assert rel(z.cpu().numpy(), pb.precondition(f)) < 1e-11
+    check("cfg1 precondition", rel(z.cpu().numpy(), pb.precondition(f)), 1e-11)
     out = np.empty_like(u)
     rmb.rm_relax_host(ctx, f, u, out, 1.0)
-    assert rel(out, pb.relax(f, u)) < 1e-11
+    check("cfg1 relax_host", rel(out, pb.relax(f, u)), 1e-11)
 
 
 def test_interior_only_single_patch_exact_solve(dev):
@@ -133,8 +156,9 @@ def test_interior_only_single_patch_exact_solve(dev):
 
 def test_cfg2_full_size_sampled(dev):
     """BASELINE configs[1] at full size in the bench's launch configuration: apply rows and sweep
-    outputs sampled at interior, face, edge and vertex DoFs, each recomputed by the oracle from
-    the cells / patches that carry it."""
+    outputs at 128 sampled DoFs -- 16 clusters of 8 (interior, face, edge and vertex DoFs around
+    seeded random vertices, so that neighbouring rows share their patches) -- each recomputed by
+    the oracle from the cells / patches that carry it."""
     import paper_2211_14284_b200 as rmb
     from oracle.fem import Space, cell_rows_apply
     from oracle.solver import sampled_relax
@@ -145,17 +169,31 @@ def test_cfg2_full_size_sampled(dev):
     f, u = vecs(w, ctx)
     ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
     L = w.nx * w.p + 1
-    idx = lambda x, y, z: (z * L + y) * L + x
-    rows = [idx(100, 101, 102), idx(105, 101, 102), idx(105, 105, 102), idx(105, 105, 105), idx(224, 3, 8), idx(1, 224, 224)]
+    idx = lambda x, y, z: (z * L + y) * L + x   # noqa: E731
+    g = np.random.default_rng(2024)
+    rows = []
+    for c in range(16):
+        # vertices anywhere, including the Dirichlet face x = 0 and the Neumann faces
+        vx, vy, vz = (int(t) for t in g.integers(0, w.nx + 1, size=3))
+        if c == 0:
+            vx, vy, vz = w.nx, w.ny, w.nz          # the far corner (Neumann on three sides)
+        base = np.array([vx, vy, vz]) * w.p
+        for off in ((0, 0, 0), (1, 0, 0), (1, 1, 0), (1, 1, 1), (-2, 0, 0), (-3, -1, 2), (0, 2, -1), (3, 3, 3)):
+            x, y, z = np.clip(base + np.array(off), 0, L - 1)
+            rows.append(idx(int(x), int(y), int(z)))
+    rows = sorted(set(rows))
+    um = np.where(ctx.constrained_mask(), 0.0, u)
     v = torch.empty_like(ut)
     rmb.rm_apply(ctx, ut, v)
-    vo = cell_rows_apply(sp, X, al, be, np.where(ctx.constrained_mask(), 0.0, u), rows)
-    np.testing.assert_allclose(v.cpu().numpy()[rows], vo, rtol=1e-12, atol=1e-12 * np.abs(vo).max())
+    vo = cell_rows_apply(sp, X, al, be, um, rows)
+    err = float(np.abs(v.cpu().numpy()[rows] - vo).max() / np.abs(vo).max())
+    check(f"cfg2 full size apply ({len(rows)} rows, max-abs rel)", err, 1e-11)
     out = torch.empty_like(ut)
     rmb.rm_relax(ctx, ft, ut, out, 1.0)
-    so = sampled_relax(sp, X, al, be, w.gamma_d, f, u, rows[:4])
-    got = out.cpu().numpy()[rows[:4]]
-    assert np.abs(got - so).max() < 1e-11 * np.abs(so).max()
+    so = sampled_relax(sp, X, al, be, w.gamma_d, f, u, rows)
+    got = out.cpu().numpy()[rows]
+    check(f"cfg2 full size relax ({len(rows)} rows, max-abs rel)", float(np.abs(got - so).max() / np.abs(so).max()),
+          1e-11)
 
 
 @pytest.mark.parametrize("nx,p", [(2, 15), (3, 5)])
@@ -174,7 +212,7 @@ def test_trilinear_apply_full_degree(dev, nx, p):
     sp_ = Space(0, w.p, w.nx, w.ny, w.nz)
     ref = apply_matfree(sp_, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), np.where(m, 0.0, u))
     ref[m] = 0.0
-    assert rel(v.cpu().numpy(), ref) < 1e-11
+    check(f"trilinear apply {nx}^3 p={p}", rel(v.cpu().numpy(), ref), 1e-11)
 
 
 # ------------------------------------------------------------------ z-slab partition on one GPU
