@@ -13,7 +13,9 @@
  *             [+ omega * D (sum_j R_j^T B_j^{-1} R_j) D^T r  for the PH decomposition, eq:asm-hiptmair]
  *             with star patches and exact Cholesky or, on non-Cartesian
  *             cells, the auxiliary operator (eq:sum-factorization_approx P:732-739) with ICC on the
- *             static-condensation pattern.  No p=1 coarse term (reading G10).
+ *             static-condensation pattern.  rm_relax has no coarse term (reading
+ *             G10); with options.coarse = 1 rm_precondition / rm_pcg use the hybrid V(1,1) cycle with
+ *             the p = 1 coarse level R_0^T A_0^{-1} R_0 of eq:asm-afw.
  *
  * VECTOR LAYOUT (reading G16): component-major; each component a C-order
  * [Z][Y][X] array (X fastest).  Per direction d a component uses a P family (n_d p + 1 entries,
@@ -76,7 +78,11 @@ typedef struct {
   int32_t factorization;     /* RM_CHOL | RM_ICC_SC                                                 */
   int32_t patch_entities;    /* RM_ALL_ENTITIES | RM_INTERIOR_ONLY                                  */
   double potential_shift;    /* eps_s for k = 2 PH (reading G8), default 1e-3                        */
-  int32_t coarse;            /* must be 0 (p = 1 coarse level not built, reading G10)              */
+  int32_t coarse;            /* 0: one-level additive Schwarz in rm_precondition / rm_pcg; 1: the    */
+                             /* p = 1 coarse level (A_0 rediscretised, R_0 the FDM embedding, direct */
+                             /* block-Cholesky solve) in a hybrid V(1,1) cycle with the patch sweep  */
+                             /* damped by 1/N_c (readings G10 / G20);        */
+                             /* single rank only. rm_relax is always the one-level sweep.           */
   void *stream;              /* cudaStream_t                                                        */
   const void *nccl_id;       /* 128-byte ncclUniqueId or NULL (single GPU)                          */
   int32_t rank, nranks, device;
@@ -149,7 +155,8 @@ rm_status rm_apply(rm_ctx *ctx, const double *u, double *v);                 /* 
 rm_status rm_residual(rm_ctx *ctx, const double *f, const double *u, double *r);   /* r = f - A u  */
 /* u_out = u_in + omega * P^{-1}(f - A u_in); u_out may alias u_in. */
 rm_status rm_relax(rm_ctx *ctx, const double *f, const double *u_in, double *u_out, double omega);
-/* z = P^{-1} r  (the additive Schwarz preconditioner = one sweep from zero with omega = 1). */
+/* z = M r: the additive Schwarz preconditioner (one sweep from zero with omega = 1), or with
+ * options.coarse = 1 the hybrid V(1,1) cycle with the p = 1 coarse level. */
 rm_status rm_precondition(rm_ctx *ctx, const double *r, double *z);
 /* Multi-rank sweep in two stages, for callers that move the halos themselves (and the
  * single-GPU partition tests): rm_relax_begin reads f and u_in on every local plane (the caller

@@ -195,7 +195,7 @@ def rm_nccl_unique_id() -> bytes:
 
 def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposition=RM_PAFW,
              factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-3, stream=None,
-             device=0, rank=0, nranks=1, z_begin=0, z_end=None, nccl_id=None) -> RmContext:
+             device=0, rank=0, nranks=1, z_begin=0, z_end=None, nccl_id=None, coarse=0) -> RmContext:
     """coords / alpha / beta describe the GLOBAL mesh; with nranks > 1 the context holds the local
     problem of the cell layers [z_begin, z_end) (rm_partition) and its vectors are local."""
     alpha = np.ascontiguousarray(np.atleast_1d(np.asarray(alpha, dtype=np.float64)).ravel())
@@ -213,6 +213,7 @@ def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposit
     opt.factorization = factorization
     opt.patch_entities = patch_entities
     opt.potential_shift = potential_shift
+    opt.coarse = int(coarse)
     sp = _stream_ptr(stream)
     opt.stream = ctypes.c_void_p(sp)
     opt.device = device

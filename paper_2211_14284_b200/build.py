@@ -18,8 +18,8 @@ LIB = os.path.join(HERE, "librm.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CXX_SRC = ["basis.cpp", "model.cpp", "patches.cpp", "abi.cpp"]
-CU_SRC = ["kernels.cu", "apply.cu", "apply_kform.cu", "apply_tri.cu", "patch_solve.cu"]
+CXX_SRC = ["basis.cpp", "model.cpp", "patches.cpp", "coarse.cpp", "abi.cpp"]
+CU_SRC = ["kernels.cu", "apply.cu", "apply_kform.cu", "apply_tri.cu", "patch_solve.cu", "coarse.cu"]
 
 
 def _headers():

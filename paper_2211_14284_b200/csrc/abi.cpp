@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "basis.hpp"
+#include "coarse.hpp"
 #include "kernels.cuh"
 #include "model.hpp"
 #include "patches.hpp"
@@ -427,6 +428,11 @@ struct rm_ctx {
   ncclComm_t comm = nullptr;
   double *d_fh = nullptr, *d_uh = nullptr, *d_c = nullptr, *d_rtmp = nullptr;
   int64_t nfree_global = 0;
+  // p = 1 coarse level + hybrid V(1,1) (options.coarse, reading G20)
+  std::unique_ptr<rm::CoarseFactor> coarse;
+  rm::CoarseLaunch cl{};
+  double *d_vz = nullptr, *d_vt = nullptr;   // cycle temporaries (fine size)
+  double smoother_omega = 1.0;
 
   double* dalloc(size_t n) {
     void* d = nullptr;
@@ -600,7 +606,8 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     if (space < 0 || space > 2) throw RmError(RM_EINVAL, "space must be 0, 1 or 2");
     if (mesh->nx < 1 || mesh->ny < 1 || mesh->nz < 1) throw RmError(RM_EINVAL, "mesh sizes must be >= 1");
     if (gamma_d > 0x3F) throw RmError(RM_EINVAL, "gamma_d has bits above bit 5");
-    if (o.coarse != 0) throw RmError(RM_EINVAL, "coarse level not supported (reading G10)");
+    if (o.coarse != 0 && o.coarse != 1) throw RmError(RM_EINVAL, "coarse must be 0 or 1");
+    if (o.coarse && o.nranks > 1) throw RmError(RM_EINVAL, "the coarse level is single-rank only");
     if (o.decomposition != RM_PAFW && o.decomposition != RM_PH) throw RmError(RM_EINVAL, "bad decomposition");
     if (o.factorization != RM_CHOL && o.factorization != RM_ICC_SC) throw RmError(RM_EINVAL, "bad factorization");
     const int64_t ncell = (int64_t)mesh->nx * mesh->ny * mesh->nz;
@@ -804,6 +811,48 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
         NK(nccl().init(&c->comm, c->nranks, id, c->rank));
       }
     }
+    if (o.coarse) {
+      // p = 1 coarse level: A_0 rediscretised, block-tridiagonal Cholesky, R_0 tables
+      rm::CoarseSetupInput ci{};
+      ci.k = space; ci.p = p; ci.n[0] = c->n[0]; ci.n[1] = c->n[1]; ci.n[2] = c->n[2];
+      ci.gamma_d = gamma_d; ci.coords = mesh->coords; ci.cartesian = cart;
+      ci.hx = h[0].data(); ci.hy = h[1].data(); ci.hz = h[2].data();
+      ci.alpha = alpha; ci.beta = beta; ci.n_alpha = n_alpha; ci.n_beta = n_beta;
+      c->coarse.reset(new rm::CoarseFactor);
+      rm::build_coarse(ci, *c->coarse);
+      const rm::CoarseFactor& F = *c->coarse;
+      rm::CoarseLaunch& L = c->cl;
+      L.p = p; L.ncomp = c->sp.ncomp;
+      for (int d = 0; d < 3; ++d) L.n[d] = c->n[d];
+      for (int m = 0; m < 3; ++m)
+        for (int d = 0; d < 3; ++d) {
+          L.fam[m][d] = c->sp.fam[m][d];
+          L.len[m][d] = m < c->sp.ncomp ? c->sp.len(m, d) : 0;
+          L.len1[m][d] = m < c->sp.ncomp ? F.sp1.len(m, d) : 0;
+        }
+      for (int m = 0; m <= 3; ++m) { L.off[m] = c->sp.offset(std::min(m, c->sp.ncomp)); L.off1[m] = F.sp1.offset(std::min(m, c->sp.ncomp)); }
+      L.ndof1 = F.ndof1;
+      L.nb = (int)F.bstart.size() - 1;
+      L.bstart = F.bstart.data();
+      L.o_linv = F.o_linv.data(); L.o_linvt = F.o_linvt.data(); L.o_lsub = F.o_lsub.data(); L.o_lsubt = F.o_lsubt.data();
+      auto up = [&](const void* h, size_t bytes) {
+        void* d = nullptr;
+        if (cudaMalloc(&d, std::max<size_t>(bytes, 8)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed (coarse level)");
+        c->allocs.push_back(d);
+        CK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+        return d;
+      };
+      L.perm = static_cast<const long long*>(up(F.perm.data(), F.perm.size() * sizeof(long long)));
+      L.cmask = static_cast<const unsigned char*>(up(F.cmask.data(), F.cmask.size()));
+      L.vals = static_cast<const double*>(up(F.vals.data(), F.vals.size() * sizeof(double)));
+      L.xc = c->dalloc(F.ndof1); L.b = c->dalloc(F.ndof1); L.y = c->dalloc(F.ndof1); L.t = c->dalloc(F.ndof1);
+      L.tA = c->dalloc(c->ndof); L.tB = c->dalloc(c->ndof);
+      for (int a = 0; a < 16; ++a) { L.e0[a] = F.e0[a]; L.e1[a] = F.e1[a]; }
+      c->d_vz = c->dalloc(c->ndof); c->d_vt = c->dalloc(c->ndof);
+      // reading G20: smoother damping 1 / N_c (N_c = patch colours of the level, potential included)
+      int nc = c->prims[0].ncolors + (c->pots[0].present ? c->pots[0].ncolors : 0);
+      c->smoother_omega = 1.0 / std::max(nc, 1);
+    }
     c->d_sc = c->dalloc(8);
     c->d_part = c->dalloc(1024);
     CK(cudaDeviceSynchronize());
@@ -864,6 +913,8 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
     info->icc_sigma_max = std::max(info->icc_sigma_max, F.sigma_max);
   }
   info->comm_nranks = c->comm ? c->nranks : 0;
+  info->coarse = c->coarse ? 1 : 0;
+  info->coarse_ndof = c->coarse ? c->coarse->nfree1 : 0;
   info->setup_seconds = c->setup_seconds;
   return RM_OK;
 }
@@ -970,6 +1021,27 @@ void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_pad
       c->launches[2] += run_family(c, c->pots[o], c->d_t, c->d_s, 1.0, o > 0, o == 0, o == np - 1);
     CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, u, omega, c->st));
   }
+}
+
+// z = M r: the PCG preconditioner.  One level: the additive sweep from zero.  With the coarse
+// level: the hybrid V(1,1) cycle (reading G20)
+//   z1 = w S r,  z2 = z1 + R_0^T A_0^{-1} R_0 (r - A z1),  z = z2 + w S (r - A z2)
+// (r zero on constrained DoFs; z overwritten)
+void apply_cycle(rm_ctx* c, const double* r, double* z) {
+  CK(cudaMemsetAsync(z, 0, c->ndof * sizeof(double), c->st));
+  if (!c->coarse) {
+    add_precond(c, r, z, 1.0);
+    return;
+  }
+  const double w = c->smoother_omega;
+  add_precond(c, r, z, w);
+  do_apply(c, z, r, c->d_vt);                         // r - A z1
+  {
+    Phase ph(c, 3);
+    CK(rm::launch_coarse_correct(c->cl, c->d_vt, z, c->st));
+  }
+  do_apply(c, z, r, c->d_vt);                         // r - A z2
+  add_precond(c, c->d_vt, z, w);
 }
 
 // ------------------------------------------------------------------ multi-rank sweep pieces
@@ -1115,7 +1187,7 @@ rm_status rm_precondition(rm_ctx* c, const double* r, double* z) {
     const double* rh = with_halo(c, r, c->d_fh);
     CK(cudaMemsetAsync(z, 0, c->ndof * sizeof(double), c->st));
     do_apply(c, z, rh, c->d_r);   // d_r = r - A*0 = r, constrained entries zeroed
-    add_precond(c, c->d_r, z, 1.0);
+    apply_cycle(c, c->d_r, z);
     if (c->nranks > 1) reverse_add(c, z);
   });
 }
@@ -1153,8 +1225,7 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
       allreduce_sum(c, out, 1);
     };
     auto precond = [&](const double* rr, double* zz) {
-      CK(cudaMemsetAsync(zz, 0, B, c->st));
-      add_precond(c, rr, zz, 1.0);
+      apply_cycle(c, rr, zz);
       if (c->nranks > 1) reverse_add(c, zz);
     };
     CK(cudaMemsetAsync(u, 0, B, c->st));

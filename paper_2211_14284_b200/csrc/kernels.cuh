@@ -93,6 +93,23 @@ cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const do
                                const double* hpow, const double* u, const double* f, double* out, long long ndof,
                                double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt);
 size_t kform_cellbuf_doubles(int k, int p, const int* n);
+// p = 1 coarse level (coarse.cu, host data from coarse.hpp): z += R_0^T A_0^{-1} R_0 r
+struct CoarseLaunch {
+  int p, ncomp, n[3], fam[3][3];
+  long long len[3][3], off[4];      // fine layout (x, y, z extents per component)
+  long long len1[3][3], off1[4];    // coarse layout
+  long long ndof1;
+  int nb;                           // z blocks of A_0
+  const int* bstart;                // HOST: nb + 1 block offsets (block order)
+  const long long *o_linv, *o_linvt, *o_lsub, *o_lsubt;   // HOST: offsets into vals
+  const long long* perm;            // device: block order -> coarse layout
+  const unsigned char* cmask;       // device: block order constrained flags
+  const double* vals;               // device: block factors
+  double *xc, *b, *y, *t;           // device: coarse vectors (ndof1)
+  double *tA, *tB;                  // device: transfer temporaries (fine size)
+  double e0[16], e1[16];            // 1D embedding, interior rows
+};
+cudaError_t launch_coarse_correct(const CoarseLaunch& L, const double* r, double* z, cudaStream_t st);
 // out = f (or 0) with constrained entries zeroed (apply.cu)
 cudaError_t launch_apply_init(const OpParams& op, const double* f, double* out, long long ndof, cudaStream_t st);
 

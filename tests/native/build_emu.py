@@ -9,7 +9,7 @@ LIB = os.path.join(HERE, "libemu.so")
 
 
 def build():
-    srcs = [os.path.join(HERE, "emu.cpp")] + [os.path.join(CSRC, f) for f in ("basis.cpp", "model.cpp", "patches.cpp")]
+    srcs = [os.path.join(HERE, "emu.cpp")] + [os.path.join(CSRC, f) for f in ("basis.cpp", "model.cpp", "patches.cpp", "coarse.cpp")]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".h"))]
     if os.path.exists(LIB) and all(os.path.getmtime(LIB) > os.path.getmtime(s) for s in deps):
         return LIB

@@ -15,6 +15,7 @@
 
 #include "model.hpp"
 #include "patches.hpp"
+#include "coarse.hpp"
 
 using namespace rm;
 
@@ -386,6 +387,103 @@ int emu_family_nnz(int k, int p, int nx, int ny, int nz, unsigned gamma, int dim
     long long mx = 0;
     for (auto& C : F->classes) mx = std::max<long long>(mx, C.nnzL);
     out[2] = mx;
+    return 0;
+  } catch (const std::exception& e) {
+    snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}
+
+// z = R_0^T A_0^{-1} R_0 r with the product's host coarse factor (coarse.cpp), re-enacting
+// launch_coarse_correct (coarse.cu) on the host: restriction by the 1D embedding tables, block
+// forward / backward substitution with the stored Linv / Lsub blocks, prolongation.
+int emu_coarse(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
+               const double* beta, long long nb_, const double* coords, const double* r, double* z, char* err,
+               int errlen) {
+  try {
+    std::vector<double> h[3];
+    const int n[3] = {nx, ny, nz};
+    for (int d = 0; d < 3; ++d) h[d].assign(n[d], 1.0 / n[d]);
+    CoarseSetupInput in{};
+    in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma; in.coords = coords;
+    in.cartesian = coords == nullptr; in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    in.alpha = alpha; in.beta = beta; in.n_alpha = na; in.n_beta = nb_;
+    CoarseFactor F;
+    build_coarse(in, F);
+    Space sp;
+    sp.init(k, p, nx, ny, nz);
+    const Space& s1 = F.sp1;
+    // 1D embedding E[i][c] of one direction
+    auto E = [&](int fam, int i, int c) -> double {
+      if (fam == FAM_D) return (i == c * p) ? 1.0 : 0.0;
+      const int cc = i / p, a = i - cc * p;
+      if (a == 0) return cc == c ? 1.0 : 0.0;
+      if (c == cc) return F.e0[a];
+      if (c == cc + 1) return F.e1[a];
+      return 0.0;
+    };
+    std::vector<double> xc(F.ndof1, 0.0);
+    for (int m = 0; m < sp.ncomp; ++m)
+      for (int64_t Z = 0; Z < s1.len(m, 2); ++Z)
+        for (int64_t Y = 0; Y < s1.len(m, 1); ++Y)
+          for (int64_t X = 0; X < s1.len(m, 0); ++X) {
+            double acc = 0.0;
+            for (int64_t iz = std::max<int64_t>(0, (Z - 1) * p); iz <= std::min<int64_t>(sp.len(m, 2) - 1, (Z + 1) * p); ++iz) {
+              const double ez = E(sp.fam[m][2], (int)iz, (int)Z);
+              if (ez == 0.0) continue;
+              for (int64_t iy = std::max<int64_t>(0, (Y - 1) * p); iy <= std::min<int64_t>(sp.len(m, 1) - 1, (Y + 1) * p); ++iy) {
+                const double ey = E(sp.fam[m][1], (int)iy, (int)Y);
+                if (ey == 0.0) continue;
+                for (int64_t ix = std::max<int64_t>(0, (X - 1) * p); ix <= std::min<int64_t>(sp.len(m, 0) - 1, (X + 1) * p); ++ix) {
+                  const double ex = E(sp.fam[m][0], (int)ix, (int)X);
+                  if (ex != 0.0) acc += ex * ey * ez * r[sp.gidx(m, iz, iy, ix)];
+                }
+              }
+            }
+            xc[s1.gidx(m, Z, Y, X)] = acc;
+          }
+    const int nb = (int)F.bstart.size() - 1;
+    std::vector<double> b(F.ndof1), y(F.ndof1), x(F.ndof1), t;
+    for (int64_t q = 0; q < F.ndof1; ++q) b[q] = F.cmask[q] ? 0.0 : xc[F.perm[q]];
+    auto gemv = [&](const double* M, const double* v, int rows, int cols, double* out, const double* add, double sg) {
+      for (int i = 0; i < rows; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < cols; ++j) s += M[(size_t)i * cols + j] * v[j];
+        out[i] = (add ? add[i] : 0.0) + sg * s;
+      }
+    };
+    for (int j = 0; j < nb; ++j) {
+      const int m = F.bstart[j + 1] - F.bstart[j];
+      std::vector<double> rhs(b.begin() + F.bstart[j], b.begin() + F.bstart[j + 1]);
+      if (j > 0) {
+        const int mp = F.bstart[j] - F.bstart[j - 1];
+        gemv(&F.vals[F.o_lsub[j - 1]], &y[F.bstart[j - 1]], m, mp, rhs.data(), rhs.data(), -1.0);
+      }
+      gemv(&F.vals[F.o_linv[j]], rhs.data(), m, m, &y[F.bstart[j]], nullptr, 1.0);
+    }
+    for (int j = nb - 1; j >= 0; --j) {
+      const int m = F.bstart[j + 1] - F.bstart[j];
+      std::vector<double> rhs(y.begin() + F.bstart[j], y.begin() + F.bstart[j + 1]);
+      if (j + 1 < nb) {
+        const int mn = F.bstart[j + 2] - F.bstart[j + 1];
+        gemv(&F.vals[F.o_lsubt[j]], &x[F.bstart[j + 1]], m, mn, rhs.data(), rhs.data(), -1.0);
+      }
+      gemv(&F.vals[F.o_linvt[j]], rhs.data(), m, m, &x[F.bstart[j]], nullptr, 1.0);
+    }
+    std::fill(xc.begin(), xc.end(), 0.0);
+    for (int64_t q = 0; q < F.ndof1; ++q) xc[F.perm[q]] = F.cmask[q] ? 0.0 : x[q];
+    for (int m = 0; m < sp.ncomp; ++m)
+      for (int64_t iz = 0; iz < sp.len(m, 2); ++iz)
+        for (int64_t iy = 0; iy < sp.len(m, 1); ++iy)
+          for (int64_t ix = 0; ix < sp.len(m, 0); ++ix) {
+            double acc = 0.0;
+            for (int64_t Z = iz / p; Z <= std::min<int64_t>(s1.len(m, 2) - 1, iz / p + 1); ++Z)
+              for (int64_t Y = iy / p; Y <= std::min<int64_t>(s1.len(m, 1) - 1, iy / p + 1); ++Y)
+                for (int64_t X = ix / p; X <= std::min<int64_t>(s1.len(m, 0) - 1, ix / p + 1); ++X)
+                  acc += E(sp.fam[m][0], (int)ix, (int)X) * E(sp.fam[m][1], (int)iy, (int)Y) * E(sp.fam[m][2], (int)iz, (int)Z) *
+                         xc[s1.gidx(m, Z, Y, X)];
+            z[sp.gidx(m, iz, iy, ix)] = acc;
+          }
     return 0;
   } catch (const std::exception& e) {
     snprintf(err, errlen, "%s", e.what());

@@ -148,3 +148,36 @@ def test_algorithmic_factor_nnz_matches_survey(emu, name, k, p, n, gamma, dim, f
     assert out[0] == total
     if largest is not None:
         assert out[2] == largest
+
+
+# ------------------------------------------------------------ p = 1 coarse level (host factor)
+@pytest.mark.parametrize("name,w", [
+    ("q3-dirichlet", ri.CONFIGS[1].with_mesh(3)),
+    ("q4-neumann-logalpha", ri.CONFIGS[2].with_mesh(3).with_p(4)),
+    ("nce3", ri.CONFIGS[3].with_mesh(2).with_p(3)),
+    ("ncf3", ri.CONFIGS[4].with_mesh(2).with_p(3)),
+    ("q3-trilinear", ri.CONFIGS[5].with_mesh(3).with_p(3)),
+])
+def test_product_coarse_level_matches_oracle(emu, name, w):
+    """The product's host coarse setup (A_0 assembly incl. the trilinear Q1 element matrix, the
+    block-tridiagonal Cholesky, the embedding tables) re-enacted by tests/native/emu.cpp equals the
+    oracle's R_0^T A_0^{-1} R_0 (oracle/coarse.py)."""
+    from oracle.coarse import CoarseLevel
+    from oracle.solver import Problem
+    pb = Problem(w.space, w.p, w.nx, w.ny, w.nz, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d,
+                 decomposition=w.decomposition, factorization=w.factorization)
+    r = ri.uniform_vector(w.cfg, 0, pb.space.ndof)
+    r[pb.constrained] = 0
+    al = np.ascontiguousarray(ri.cell_alpha(w).ravel())
+    be = np.ascontiguousarray(ri.cell_beta(w).ravel())
+    coords = None if w.perturb == 0 else np.ascontiguousarray(ri.vertex_coords(w).ravel())
+    D = ctypes.POINTER(ctypes.c_double)
+    emu.emu_coarse.argtypes = [ctypes.c_int] * 5 + [ctypes.c_uint, D, ctypes.c_longlong, D, ctypes.c_longlong, D, D, D,
+                                                    ctypes.c_char_p, ctypes.c_int]
+    z = np.zeros_like(r)
+    err = ctypes.create_string_buffer(256)
+    rc = emu.emu_coarse(w.space, w.p, w.nx, w.ny, w.nz, w.gamma_d, _dp(al), al.size, _dp(be), be.size,
+                        None if coords is None else _dp(coords), _dp(r), _dp(z), err, 256)
+    assert rc == 0, err.value
+    zo = CoarseLevel(pb).apply(r)
+    assert np.linalg.norm(z - zo) / np.linalg.norm(zo) < 1e-11

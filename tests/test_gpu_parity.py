@@ -303,3 +303,47 @@ def test_full_size_hcurl_hdiv_configs_sweep(dev, cfg):
     uh = u.cpu().numpy()
     assert np.isfinite(uh).all() and np.abs(uh).max() > 0
     assert np.abs(uh[mask]).max() == 0.0
+
+
+# ------------------------------------------------------------------ p = 1 coarse level (f1)
+COARSE_CASES = [
+    ("cfg1", ri.CONFIGS[1], 1e-11),
+    ("cfg2-3^3-p4", ri.CONFIGS[2].with_mesh(3).with_p(4), 1e-11),
+    ("cfg3-2^3-p3", ri.CONFIGS[3].with_mesh(2).with_p(3), 1e-11),
+    ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), hdiv_tol("2^3-p3")),
+    ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3), 1e-11),
+]
+
+
+@pytest.mark.parametrize("name,w,tol", COARSE_CASES, ids=[c[0] for c in COARSE_CASES])
+def test_coarse_cycle_and_pcg(dev, name, w, tol):
+    """rm_precondition with options.coarse = 1 is the hybrid V(1,1) cycle with the p = 1 coarse
+    level (reading G20): equal to the oracle's cycle; rm_pcg iteration
+    counts within +-1 of the oracle's."""
+    import paper_2211_14284_b200 as rmb
+    ctx = gu.setup_product(w, coarse=1)
+    pb = gu.setup_oracle(w, coarse=True)
+    info = ctx.info()
+    assert info["coarse"] == 1 and info["coarse_ndof"] > 0
+    f, _ = vecs(w, ctx)
+    z = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
+    rmb.rm_precondition(ctx, torch.tensor(f, device=dev), z)
+    check(f"{name} coarse V(1,1) cycle", rel(z.cpu().numpy(), pb.cycle(f)), tol)
+    x = torch.empty_like(z)
+    it, relres, ok = rmb.rm_pcg(ctx, torch.tensor(f, device=dev), x, 1e-8, 200)
+    _, ito, _ = pb.pcg(f)
+    assert ok and relres <= 1e-8
+    check(f"{name} coarse pcg iters {it} vs oracle {ito}", abs(it - ito), 1.5)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_coarse_p1_one_iteration(dev, cfg):
+    """p = 1: the coarse space is the whole space; PCG with the cycle converges in one iteration
+    (tab:hgrad-iter, p = 1, l = 0: "1/1", P:1343)."""
+    import paper_2211_14284_b200 as rmb
+    w = ri.CONFIGS[cfg].with_mesh(4).with_p(1)
+    ctx = gu.setup_product(w, coarse=1)
+    f, _ = vecs(w, ctx)
+    x = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
+    it, relres, ok = rmb.rm_pcg(ctx, torch.tensor(f, device=dev), x, 1e-8, 50)
+    assert ok and it == 1, (it, relres)
