@@ -120,6 +120,10 @@ void rm_default_options(rm_options *opt);
  * forward: u (and f) on the p planes below the slab and the shared plane above; reverse: the
  * patch corrections on the p - 1 planes below the slab, ADDED by their owner.  All plane ranges
  * below are LOCAL plane indices [first, last + 1); a plane is plane_len contiguous doubles.
+ * With a communicator (options.nccl_id) the library exchanges the forward halos IN PLACE: the
+ * non-owned planes of the input vectors of rm_apply / rm_residual / rm_relax / rm_precondition /
+ * rm_pcg are overwritten with the owners' values (their input content is ignored), and the
+ * non-owned planes of output vectors are unspecified on return (only owned planes are results).
  * Pure host arithmetic (no device needed). */
 typedef struct {
   int32_t z_cell0, nz_local, ghost_lo;   /* global layer of local cell 0; local cell layers; 0|1 */

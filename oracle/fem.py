@@ -258,8 +258,9 @@ def element_matrix(k, p, Xc, alpha, beta, nq=None):
         J = trilinear_geometry(Xc, xq, sl)
         pv, pd, detJ = pullback_fields(k, val, der, J)
         w = (wq[qz] * np.outer(wq, wq)).ravel() * detJ
-        Mq = np.einsum("q,qcn,qcm->nm", w * beta, pv, pv)
-        Kq = np.einsum("q,qcn,qcm->nm", w * alpha, pd, pd)
+        # sum_q w_q beta F psi_n(q) . F psi_m(q) (and the same for d): as matrix products (BLAS)
+        Mq = sum(pv[:, c, :].T @ ((w * beta)[:, None] * pv[:, c, :]) for c in range(pv.shape[1]))
+        Kq = sum(pd[:, c, :].T @ ((w * alpha)[:, None] * pd[:, c, :]) for c in range(pd.shape[1]))
         A = Mq + Kq if A is None else A + Mq + Kq
     return A
 
@@ -334,6 +335,7 @@ def mass_pattern(k, p):
     return out
 
 
+@lru_cache(maxsize=16)
 def cartesian_cell_pattern(k, p):
     """Structural pattern of A_K on Cartesian cells: pattern(M^k) U pattern(D^T M^{k+1} D)
     (eq:sum-factorization, P:690-699)."""
@@ -360,7 +362,7 @@ def is_axis_aligned(Xc, tol=1e-14):
     return True
 
 
-@lru_cache(maxsize=64)
+@lru_cache(maxsize=512)
 def _cartesian_parts(k, p, hx, hy, hz):
     """(M, K) cell matrices for alpha=beta=1 on an axis-aligned box with sides h, by
     quadrature, with structurally-zero entries set to exact zero."""
@@ -480,10 +482,12 @@ def cell_rows_apply(space: Space, X, alpha, beta, u, rows):
 
 
 # -------------------------------------------------------------------- global derivative D
-def global_derivative(k, p, nx, ny, nz) -> sp.csr_matrix:
-    """Tabulated d^k : V^k_h -> V^{k+1}_h on reference values: per direction the
-    1D global D-hat (row c p + a = sum_i D-hat[a, i] at column c p + i), Kronecker-combined
-    like eq:gradbasis/eq:curlbasis/eq:divbasis (standard curl sign)."""
+@lru_cache(maxsize=16)
+def derivative_blocks(k, p, nx, ny, nz):
+    """The blocks of the tabulated d^k : V^k_h -> V^{k+1}_h on reference values: per
+    direction the 1D global D-hat (row c p + a = sum_i D-hat[a, i] at column c p + i) or an
+    identity, Kronecker-combined like eq:gradbasis/eq:curlbasis/eq:divbasis (standard curl sign).
+    Returns [(row component, column component, sign, (Z, Y, X) 1D sparse factors)]."""
     f = fdm_basis(p)
     n = (nx, ny, nz)
 
@@ -500,26 +504,67 @@ def global_derivative(k, p, nx, ny, nz) -> sp.csr_matrix:
     def I(fam, d):
         return sp.identity(n[d] * p + 1 if fam == P_FAM else n[d] * p, format="csr")
 
-    def K3(z, y, x):
-        return sp.kron(z, sp.kron(y, x, format="csr"), format="csr")
-
     Dx, Dy, Dz = D1(0), D1(1), D1(2)
-    Pp = lambda d: I(P_FAM, d)
-    Dd = lambda d: I(D_FAM, d)
+    Pp = lambda d: I(P_FAM, d)   # noqa: E731
+    Dd = lambda d: I(D_FAM, d)   # noqa: E731
     if k == 0:
-        return sp.vstack([K3(Pp(2), Pp(1), Dx), K3(Pp(2), Dy, Pp(0)), K3(Dz, Pp(1), Pp(0))]).tocsr()
+        return [(0, 0, 1.0, (Pp(2), Pp(1), Dx)), (1, 0, 1.0, (Pp(2), Dy, Pp(0))), (2, 0, 1.0, (Dz, Pp(1), Pp(0)))]
     if k == 1:
-        # source comps: x (D,P,P), y (P,D,P), z (P,P,D)
-        ux_to_y = K3(Dz, Pp(1), Dd(0)); ux_to_z = K3(Pp(2), Dy, Dd(0))
-        uy_to_x = K3(Dz, Dd(1), Pp(0)); uy_to_z = K3(Pp(2), Dd(1), Dx)
-        uz_to_x = K3(Dd(2), Dy, Pp(0)); uz_to_y = K3(Dd(2), Pp(1), Dx)
-        row_x = [None, -uy_to_x, uz_to_x]
-        row_y = [ux_to_y, None, -uz_to_y]
-        row_z = [-ux_to_z, uy_to_z, None]
-        return sp.bmat([row_x, row_y, row_z], format="csr")
+        # source comps: x (D,P,P), y (P,D,P), z (P,P,D); curl x = d_y u_z - d_z u_y, ...
+        return [(0, 1, -1.0, (Dz, Dd(1), Pp(0))), (0, 2, 1.0, (Dd(2), Dy, Pp(0))),
+                (1, 0, 1.0, (Dz, Pp(1), Dd(0))), (1, 2, -1.0, (Dd(2), Pp(1), Dx)),
+                (2, 0, -1.0, (Pp(2), Dy, Dd(0))), (2, 1, 1.0, (Pp(2), Dd(1), Dx))]
     if k == 2:
-        return sp.hstack([K3(Dd(2), Dd(1), Dx), K3(Dd(2), Dy, Dd(0)), K3(Dz, Dd(1), Dd(0))]).tocsr()
+        return [(0, 0, 1.0, (Dd(2), Dd(1), Dx)), (0, 1, 1.0, (Dd(2), Dy, Dd(0))), (0, 2, 1.0, (Dz, Dd(1), Dd(0)))]
     raise ValueError(k)
+
+
+@lru_cache(maxsize=16)
+def _derivative_blocks_t(k, p, nx, ny, nz):
+    """derivative_blocks with every 1D factor transposed (column access)."""
+    return [(r, c, sg, tuple(M.T.tocsr() for M in f)) for r, c, sg, f in derivative_blocks(k, p, nx, ny, nz)]
+
+
+def _csr_row(M, i):
+    a, b = M.indptr[i], M.indptr[i + 1]
+    return list(zip(M.indices[a:b].tolist(), M.data[a:b].tolist()))
+
+
+def global_derivative(k, p, nx, ny, nz) -> sp.csr_matrix:
+    """d^k as one sparse matrix (rows V^{k+1}, columns V^k): the blocks of derivative_blocks."""
+    blocks = derivative_blocks(k, p, nx, ny, nz)
+    nr = 1 + max(b[0] for b in blocks)
+    nc = 1 + max(b[1] for b in blocks)
+    grid = [[None] * nc for _ in range(nr)]
+    for r, c, sg, (Z, Y, X) in blocks:
+        grid[r][c] = sg * sp.kron(Z, sp.kron(Y, X, format="csr"), format="csr")
+    return sp.bmat(grid, format="csr")
+
+
+def derivative_entries(k, p, nx, ny, nz, index, by="row"):
+    """Entries of one row (by="row") or one column (by="col") of global_derivative without forming
+    it: {other index: value}, from the same Kronecker blocks."""
+    blocks = derivative_blocks(k, p, nx, ny, nz) if by == "row" else _derivative_blocks_t(k, p, nx, ny, nz)
+    rsp, csp = Space(k + 1, p, nx, ny, nz), Space(k, p, nx, ny, nz)
+    own, oth = (rsp, csp) if by == "row" else (csp, rsp)
+    oo, ot = own.offsets(), oth.offsets()
+    m = int(np.searchsorted(oo, index, side="right") - 1)
+    Lz, Ly, Lx = own.comp_shape(m)
+    r = index - oo[m]
+    iz, iy, ix = r // (Lx * Ly), (r // Lx) % Ly, r % Lx
+    out = {}
+    for br, bc, sg, (Z, Y, X) in blocks:
+        if (br if by == "row" else bc) != m:
+            continue
+        mo = bc if by == "row" else br
+        Tz, Ty, Tx = oth.comp_shape(mo)
+        rz, ry, rx = (_csr_row(Z, iz), _csr_row(Y, iy), _csr_row(X, ix))
+        for cz, vz in rz:
+            for cy, vy in ry:
+                for cx, vx in rx:
+                    g = ot[mo] + (cz * Ty + cy) * Tx + cx
+                    out[g] = out.get(g, 0.0) + sg * vz * vy * vx
+    return out
 
 
 # ---------------------------------------------------------------- auxiliary operator (k=0)

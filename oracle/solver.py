@@ -223,3 +223,115 @@ def sampled_relax(space: Space, X, alpha, beta, gamma_d, f, u, rows, omega=1.0):
                         cache[key] = DenseCholeskyPatch(Ai).solve(r)
                     out[t] += omega * cache[key][where[0]]
     return out
+
+
+def sampled_relax_ph(space: Space, X, alpha, beta, gamma_d, f, u, rows, omega=1.0, potential_shift=EPS_S):
+    """u_out[rows] of one PH exact-Cholesky sweep (k = 1, 2; eq:asm-hiptmair without the coarse
+    term) computed only from the patches that reach those rows, each assembled from its own cells
+    (no global matrix; full-size sampled parity):
+        u_out[g] = u[g] + omega ( sum_{i contains g} (A_i^{-1} R_i r)[g] + sum_h D[g, h] s[h] ),
+        s[h] = sum_{j contains h} (B_j^{-1} R_j D^T r)[h],   r = f - A u,
+    with B_j the potential patch matrix, assembled as the (k-1)-form operator with coefficients
+    (beta, 0) (k = 1) or (beta, eps_s beta) (k = 2) -- equal to R_j D^T A D R_j^T (+ eps_s beta M)
+    (pinned in tests/test_oracle_pins.py::test_potential_operator_is_the_lower_form_operator)."""
+    from .fem import cell_rows_apply, derivative_entries, dof_coords, local_matrix
+    from .patches import entities, patch_dofs
+    k, p = space.k, space.p
+    n = (space.nx, space.ny, space.nz)
+    con = space.constrained_mask(gamma_d)
+    u = np.where(con, 0.0, u)
+    f = np.where(con, 0.0, f)
+    pspace = Space(k - 1, p, *n)
+    pcon = pspace.constrained_mask(gamma_d)
+    beta_p = potential_shift * beta if k == 2 else np.zeros_like(beta)
+    rcache = {}
+
+    def resid(gs):
+        need = [int(g) for g in gs if int(g) not in rcache and not con[int(g)]]
+        if need:
+            Au = cell_rows_apply(space, X, alpha, beta, u, need)
+            for g, v in zip(need, Au):
+                rcache[g] = f[g] - v
+        return np.array([0.0 if con[int(g)] else rcache[int(g)] for g in gs])
+
+    def near_entities(sp_, dim, g):
+        _, ix, iy, iz = dof_coords(sp_, int(g))
+        cand = []
+        for ent in _entities_near(sp_, dim, (ix, iy, iz)):
+            cand.append(ent)
+        return cand
+
+    pcache, scache = {}, {}
+
+    def prim_correction(g):
+        tot = 0.0
+        for ent in near_entities(space, k, g):
+            if ent not in pcache:
+                pcache[ent] = [patch_dofs(space, ent, con)[0], None]
+            gp, z = pcache[ent]
+            w = np.flatnonzero(gp == g)
+            if not len(w):
+                continue
+            if z is None:
+                Ai = local_matrix(space, X, alpha, beta, gp)
+                z = pcache[ent][1] = DenseCholeskyPatch(Ai).solve(resid(gp))
+            tot += z[w[0]]
+        return tot
+
+    def s_value(h):
+        tot = 0.0
+        for ent in near_entities(pspace, k - 1, h):
+            if ent not in scache:
+                scache[ent] = [patch_dofs(pspace, ent, pcon)[0], None]
+            gp, z = scache[ent]
+            w = np.flatnonzero(gp == h)
+            if not len(w):
+                continue
+            if z is None:
+                # t = (D^T r) on the patch: column entries of D
+                cols = [derivative_entries(k - 1, p, *n, int(hh), by="col") for hh in gp]
+                need = sorted({g2 for ce in cols for g2 in ce})
+                rmap = dict(zip(need, resid(need)))
+                t = np.array([sum(v * rmap[g2] for g2, v in ce.items()) for ce in cols])
+                Bj = local_matrix(pspace, X, beta, beta_p, gp)
+                z = scache[ent][1] = DenseCholeskyPatch(Bj).solve(t)
+            tot += z[w[0]]
+        return tot
+
+    out = u[np.asarray(rows)].copy()
+    for t_, g in enumerate(rows):
+        g = int(g)
+        if con[g]:
+            continue
+        c = prim_correction(g)
+        for h, dv in derivative_entries(k - 1, p, *n, g, by="row").items():
+            if not pcon[h]:
+                c += dv * s_value(h)
+        out[t_] += omega * c
+    return out
+
+
+def _entities_near(sp_, dim, idx):
+    """Entities of dimension dim whose star can contain a DoF at structured indices idx: node or
+    cell coordinates within one cell of the DoF in every direction."""
+    from .patches import entities
+    p = sp_.p
+    n = (sp_.nx, sp_.ny, sp_.nz)
+    lo = [max(0, i // p - 1) for i in idx]
+    hi = [min(n[d], idx[d] // p + 1) for d, i in enumerate(idx)]
+    out = []
+    for ent in _entities_cached(sp_, dim):
+        if all(lo[d] <= ent[d][1] <= hi[d] for d in range(3)):
+            out.append(ent)
+    return out
+
+
+_ENT_CACHE = {}
+
+
+def _entities_cached(sp_, dim):
+    from .patches import entities
+    key = (sp_, dim)
+    if key not in _ENT_CACHE:
+        _ENT_CACHE[key] = entities(sp_, dim)
+    return _ENT_CACHE[key]

@@ -426,7 +426,7 @@ struct rm_ctx {
   int rank = 0, nranks = 1;
   rm_partition_info part{};
   ncclComm_t comm = nullptr;
-  double *d_fh = nullptr, *d_uh = nullptr, *d_c = nullptr, *d_rtmp = nullptr;
+  double *d_c = nullptr, *d_rtmp = nullptr;
   int64_t nfree_global = 0;
   // p = 1 coarse level + hybrid V(1,1) (options.coarse, reading G20)
   std::unique_ptr<rm::CoarseFactor> coarse;
@@ -803,8 +803,9 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       const int64_t fy = (int64_t)c->n[1] * p + 1 - ((g >> 2) & 1) - ((g >> 3) & 1);
       const int64_t fz = (int64_t)nz_global * p + 1 - ((g >> 4) & 1) - ((g >> 5) & 1);
       c->nfree = fx * fy * fz;
-      c->d_fh = c->dalloc(c->ndof); c->d_uh = c->dalloc(c->ndof); c->d_c = c->dalloc(c->ndof);
-      c->d_rtmp = c->dalloc((size_t)p * part.plane_len);
+      c->d_c = c->dalloc(c->ndof);
+      // reverse-add receive buffer: p planes of the vector layout or of the padded (even-x) layout
+      c->d_rtmp = c->dalloc((size_t)p * ((int64_t)c->n[0] * p + 2) * ((int64_t)c->n[1] * p + 1));
       if (o.nccl_id) {
         ncclUniqueId id;
         std::memcpy(&id, o.nccl_id, sizeof id);
@@ -1045,27 +1046,32 @@ void apply_cycle(rm_ctx* c, const double* r, double* z) {
 }
 
 // ------------------------------------------------------------------ multi-rank sweep pieces
-// Forward halo: planes fwd_recv_* of v <- the owners' planes (NCCL send/recv on the stream).
-void halo_forward(rm_ctx* c, double* v) {
+// Forward halo: planes fwd_recv_* of each vector <- the owners' planes (NCCL send/recv in ONE
+// group on the stream, in place: the non-owned planes of the caller's input vectors are
+// overwritten, include/rm.h).  L = doubles per plane.
+void halo_forward(rm_ctx* c, double* const* vs, int nv, size_t L) {
   const rm_partition_info& P = c->part;
   const NcclApi& N = nccl();
-  const size_t L = (size_t)P.plane_len;
   NK(N.gstart());
-  if (c->rank > 0) {
-    NK(N.send(v + P.fwd_send_lo[0] * L, (P.fwd_send_lo[1] - P.fwd_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
-    NK(N.recv(v + P.fwd_recv_lo[0] * L, (P.fwd_recv_lo[1] - P.fwd_recv_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
-  }
-  if (c->rank < c->nranks - 1) {
-    NK(N.send(v + P.fwd_send_hi[0] * L, (P.fwd_send_hi[1] - P.fwd_send_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
-    NK(N.recv(v + P.fwd_recv_hi[0] * L, (P.fwd_recv_hi[1] - P.fwd_recv_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+  for (int i = 0; i < nv; ++i) {
+    double* v = vs[i];
+    if (c->rank > 0) {
+      NK(N.send(v + P.fwd_send_lo[0] * L, (P.fwd_send_lo[1] - P.fwd_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+      NK(N.recv(v + P.fwd_recv_lo[0] * L, (P.fwd_recv_lo[1] - P.fwd_recv_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+    }
+    if (c->rank < c->nranks - 1) {
+      NK(N.send(v + P.fwd_send_hi[0] * L, (P.fwd_send_hi[1] - P.fwd_send_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+      NK(N.recv(v + P.fwd_recv_hi[0] * L, (P.fwd_recv_hi[1] - P.fwd_recv_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+    }
   }
   NK(N.gend());
 }
-// Reverse-add: the corrections my patches put on rank - 1's planes go there and are added by it.
-void reverse_add(rm_ctx* c, double* cv) {
+void halo_forward(rm_ctx* c, double* v) { halo_forward(c, &v, 1, (size_t)c->part.plane_len); }
+// Reverse-add: the corrections my patches put on rank - 1's planes go there and are added by it
+// (L = doubles per plane: the vector layout, or the padded TMA layout of the patch kernel).
+void reverse_add(rm_ctx* c, double* cv, size_t L) {
   const rm_partition_info& P = c->part;
   const NcclApi& N = nccl();
-  const size_t L = (size_t)P.plane_len;
   const size_t nh = (size_t)(P.rev_recv_hi[1] - P.rev_recv_hi[0]) * L;
   NK(N.gstart());
   if (c->rank > 0)
@@ -1075,6 +1081,7 @@ void reverse_add(rm_ctx* c, double* cv) {
   if (c->rank < c->nranks - 1 && nh > 0)
     CK(rm::launch_axpby((long long)nh, 1.0, c->d_rtmp, 1.0, cv + P.rev_recv_hi[0] * L, c->st));
 }
+void reverse_add(rm_ctx* c, double* cv) { reverse_add(c, cv, (size_t)c->part.plane_len); }
 // In-place sum over ranks of device scalars.
 void allreduce_sum(rm_ctx* c, double* x, size_t n) {
   if (c->nranks > 1) NK(nccl().allreduce(x, x, n, ncclDouble, ncclSum, c->comm, c->st));
@@ -1105,28 +1112,47 @@ rm_status guarded(rm_ctx* c, F&& f) {
   }
 }
 
-// u with its forward halo: the caller's vector itself on one rank (or without a communicator:
-// the caller filled the halo), else a copy with the halo exchanged
-const double* with_halo(rm_ctx* c, const double* u, double* buf) {
+// the forward halo of an input vector, exchanged in place (multi-rank with a communicator; the
+// caller's non-owned planes are overwritten, include/rm.h); the vector itself otherwise
+const double* with_halo(rm_ctx* c, const double* u) {
   if (c->nranks == 1 || !c->comm) return u;
-  CK(cudaMemcpyAsync(buf, u, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-  halo_forward(c, buf);
-  return buf;
+  halo_forward(c, const_cast<double*>(u));
+  return u;
+}
+
+bool fused_k0(const rm_ctx* c) {
+  return c->k == 0 && !c->pots[0].present && c->prims.size() == 1 && c->prims[0].npatch > 0;
 }
 
 // one sweep u_out = u_in + omega P^{-1} (f - A u_in) (z-slab: halos, local correction, reverse-add)
 void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
   if (c->nranks > 1) {
     need_comm(c);
-    const double* fh = with_halo(c, f, c->d_fh);
-    const double* uh = with_halo(c, u_in, c->d_uh);
-    local_correction(c, fh, uh, c->d_c);
+    {
+      double* vs[2] = {const_cast<double*>(f), const_cast<double*>(u_in)};
+      halo_forward(c, vs, 2, (size_t)c->part.plane_len);   // f and u_in, in place, one NCCL group
+    }
+    if (fused_k0(c)) {
+      // as on one rank: the residual straight into the padded TMA layout, corrections accumulated
+      // in the padded c, reverse-added there (padded planes), then u_out = u_in + omega c
+      const rm::PatchLaunch& L = c->prims[0].launch;
+      do_apply(c, u_in, f, L.rpad, L.pad.lxp[0]);
+      {
+        Phase ph(c, 1);
+        c->launches[1] += run_family(c, c->prims[0], L.rpad, u_out, omega, true, true, false);
+      }
+      reverse_add(c, L.cpad, (size_t)(L.pad.lxp[0] * L.pad.len[0][1]));
+      if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+      CK(rm::launch_patch_combine(L, u_out, omega, c->st));
+      return;
+    }
+    local_correction(c, f, u_in, c->d_c);
     reverse_add(c, c->d_c);
-    if (u_out != uh) CK(cudaMemcpyAsync(u_out, uh, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(rm::launch_axpby(c->ndof, omega, c->d_c, 1.0, u_out, c->st));
     return;
   }
-  if (c->k == 0 && !c->pots[0].present && c->prims.size() == 1 && c->prims[0].npatch > 0) {
+  if (fused_k0(c)) {
     // the residual goes straight into the primary family's padded (TMA) layout: no pad pass
     const rm::PatchLaunch& L = c->prims[0].launch;
     do_apply(c, u_in, f, L.rpad, L.pad.lxp[0]);
@@ -1146,14 +1172,14 @@ extern "C" {
 rm_status rm_apply(rm_ctx* c, const double* u, double* v) {
   return guarded(c, [&] {
     if (!u || !v) throw RmError(RM_EINVAL, "null vector");
-    do_apply(c, with_halo(c, u, c->d_uh), nullptr, v);
+    do_apply(c, with_halo(c, u), nullptr, v);
   });
 }
 
 rm_status rm_residual(rm_ctx* c, const double* f, const double* u, double* r) {
   return guarded(c, [&] {
     if (!f || !u || !r) throw RmError(RM_EINVAL, "null vector");
-    do_apply(c, with_halo(c, u, c->d_uh), f, r);
+    do_apply(c, with_halo(c, u), f, r);
   });
 }
 
@@ -1184,7 +1210,7 @@ rm_status rm_precondition(rm_ctx* c, const double* r, double* z) {
     if (!r || !z) throw RmError(RM_EINVAL, "null vector");
     need_comm(c);
     // r with constrained entries read as zero: the residual kernel with u = 0
-    const double* rh = with_halo(c, r, c->d_fh);
+    const double* rh = with_halo(c, r);
     CK(cudaMemsetAsync(z, 0, c->ndof * sizeof(double), c->st));
     do_apply(c, z, rh, c->d_r);   // d_r = r - A*0 = r, constrained entries zeroed
     apply_cycle(c, c->d_r, z);
@@ -1229,7 +1255,7 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
       if (c->nranks > 1) reverse_add(c, zz);
     };
     CK(cudaMemsetAsync(u, 0, B, c->st));
-    do_apply(c, u, with_halo(c, f, c->d_fh), r);   // r = f (masked)
+    do_apply(c, u, with_halo(c, f), r);   // r = f (masked)
     precond(r, c->d_z);
     dot(r, c->d_z, rz);
     double rz0 = 0.0;

@@ -22,12 +22,6 @@ namespace {
 
 constexpr int KF_THREADS = 256;
 
-__device__ __forceinline__ bool kf_cons(long long idx, long long last, unsigned gamma_d, int d) {
-  if (idx == 0 && (gamma_d & (1u << (2 * d)))) return true;
-  if (idx == last && (gamma_d & (1u << (2 * d + 1)))) return true;
-  return false;
-}
-
 // (D-hat x)_a along a line with stride s (source: P + 1 entries)
 template <int P>
 __device__ __forceinline__ double dline(const double* __restrict__ sD, const double* x, int s, int a) {
@@ -68,6 +62,7 @@ __device__ __forceinline__ double bb(const double* __restrict__ sB, const double
 struct CellCtx {
   int cx, cy, cz;
   double al, be, hx, hy, hz;
+  unsigned clo, chi;   // bit d: the cell's low / high face in direction d lies on a Gamma_D plane
 };
 
 __device__ __forceinline__ CellCtx cell_ctx(const OpParams& op, const double* alpha, const double* beta, int coef_const,
@@ -81,38 +76,52 @@ __device__ __forceinline__ CellCtx cell_ctx(const OpParams& op, const double* al
   c.hx = hpow[4 * op.n[0] + c.cx];
   c.hy = hpow[7 * op.n[0] + 4 * op.n[1] + c.cy];
   c.hz = hpow[7 * (op.n[0] + op.n[1]) + 4 * op.n[2] + c.cz];
+  const int cc[3] = {c.cx, c.cy, c.cz};
+  c.clo = c.chi = 0;
+  for (int d = 0; d < 3; ++d) {
+    if (cc[d] == 0 && (op.gamma_d & (1u << (2 * d)))) c.clo |= 1u << d;
+    if (cc[d] == op.n[d] - 1 && (op.gamma_d & (1u << (2 * d + 1)))) c.chi |= 1u << d;
+  }
   return c;
 }
 
-// gathers one component of the cell window into shared memory (constrained entries read as 0)
-__device__ __forceinline__ void load_comp(const OpParams& op, int m, int lx, int ly, int lz, const CellCtx& c,
-                                          const double* __restrict__ u, double* dst) {
+// 64-bit global index of the cell window's origin in component m (32-bit offsets inside)
+__device__ __forceinline__ long long comp_base(const OpParams& op, int m, const CellCtx& c) {
   const int p = op.p;
-  const long long Lx = op.len[m][0], Ly = op.len[m][1];
-  const double* ub = u + op.off[m];
-  const int tot = lx * ly * lz;
-  for (int l = threadIdx.x; l < tot; l += blockDim.x) {
-    const int a = l % lx, b = (l / lx) % ly, cc = l / (lx * ly);
-    const int ix = c.cx * p + a, iy = c.cy * p + b, iz = c.cz * p + cc;
+  return op.off[m] + ((long long)(c.cz * p) * op.len[m][1] + c.cy * p) * op.len[m][0] + c.cx * p;
+}
+
+// gathers one component of the cell window (local dims LX, LY, LZ; P-family mask FP: bit d set
+// for a P direction) into shared memory, constrained entries read as 0
+template <int P, int LX, int LY, int LZ, int FP>
+__device__ __forceinline__ void load_comp(const OpParams& op, int m, const CellCtx& c, const double* __restrict__ u,
+                                          double* dst) {
+  const double* ub = u + comp_base(op, m, c);
+  const int Lx = (int)op.len[m][0], Lxy = (int)(op.len[m][0] * op.len[m][1]);
+  constexpr int TOT = LX * LY * LZ;
+  const unsigned lo = c.clo & FP, hi = c.chi & FP;
+  for (int l = threadIdx.x; l < TOT; l += KF_THREADS) {
+    const int a = l % LX, b = (l / LX) % LY, cc = l / (LX * LY);
     bool con = false;
-    if (op.fam[m][0] == 0) con |= kf_cons(ix, (long long)op.n[0] * p, op.gamma_d, 0);
-    if (op.fam[m][1] == 0) con |= kf_cons(iy, (long long)op.n[1] * p, op.gamma_d, 1);
-    if (op.fam[m][2] == 0) con |= kf_cons(iz, (long long)op.n[2] * p, op.gamma_d, 2);
-    dst[l] = con ? 0.0 : __ldg(ub + ((long long)iz * Ly + iy) * Lx + ix);
+    if (lo | hi) {
+      con = ((lo & 1) && a == 0) || ((hi & 1) && a == P) || ((lo & 2) && b == 0) || ((hi & 2) && b == P) ||
+            ((lo & 4) && cc == 0) || ((hi & 4) && cc == P);
+    }
+    dst[l] = con ? 0.0 : __ldg(ub + cc * Lxy + b * Lx + a);
   }
 }
 
 // stores one output entry: interior entries final (out = f + sign v), skeleton ones to the buffer
-__device__ __forceinline__ void store_entry(const OpParams& op, int m, int a, int b, int cc, bool skel, const CellCtx& c,
+// (a cell-interior entry is never constrained: Gamma_D planes are cell faces)
+__device__ __forceinline__ void store_entry(const OpParams& op, long long base, int m, int a, int b, int cc, bool skel,
                                             int cell, int nloc, int l, double v, const double* __restrict__ f,
                                             double* __restrict__ out, double* __restrict__ cellbuf, double sign) {
   if (skel) {
     cellbuf[(long long)cell * nloc + l] = v;
     return;
   }
-  const int p = op.p;
-  const long long g = op.off[m] + ((long long)(c.cz * p + cc) * op.len[m][1] + (c.cy * p + b)) * op.len[m][0] + c.cx * p + a;
-  out[g] = (f ? f[g] : 0.0) + sign * v;
+  const long long g = base + cc * (int)(op.len[m][0] * op.len[m][1]) + b * (int)op.len[m][0] + a;
+  out[g] = (f ? __ldg(f + g) : 0.0) + sign * v;
 }
 
 template <int P>
@@ -134,9 +143,9 @@ __global__ void __launch_bounds__(KF_THREADS) apply_nce_kernel(const __grid_cons
   const CellCtx c = cell_ctx(op, alpha, beta, coef_const, hpow, cell);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) sB[i] = op.Bh[i];
   for (int i = threadIdx.x; i < P * N; i += blockDim.x) sD[i] = op.Dh[i];
-  load_comp(op, 0, P, N, N, c, u, U);
-  load_comp(op, 1, N, P, N, c, u, U + NC);
-  load_comp(op, 2, N, N, P, c, u, U + 2 * NC);
+  load_comp<P, P, N, N, 6>(op, 0, c, u, U);
+  load_comp<P, N, P, N, 5>(op, 1, c, u, U + NC);
+  load_comp<P, N, N, P, 3>(op, 2, c, u, U + 2 * NC);
   __syncthreads();
   const double* Ux = U;
   const double* Uy = U + NC;
@@ -186,6 +195,7 @@ __global__ void __launch_bounds__(KF_THREADS) apply_nce_kernel(const __grid_cons
   const double* Wy = W2 + NF;
   const double* Wz = W2 + 2 * NF;
   constexpr int nloc = 3 * NC;
+  const long long base[3] = {comp_base(op, 0, c), comp_base(op, 1, c), comp_base(op, 2, c)};
   for (int l = threadIdx.x; l < 3 * NC; l += blockDim.x) {
     const int m = l / NC, r = l - m * NC;
     double v;
@@ -207,7 +217,7 @@ __global__ void __launch_bounds__(KF_THREADS) apply_nce_kernel(const __grid_cons
       v += dtline<P>(sD, Wx + (cc * P) * N + a, N, b) - dtline<P>(sD, Wy + (cc * N + b) * P, 1, a);
       skel = a == 0 || a == P || b == 0 || b == P;
     }
-    store_entry(op, m, a, b, cc, skel, c, cell, nloc, l, v, f, out, cellbuf, sign);
+    store_entry(op, base[m], m, a, b, cc, skel, cell, nloc, l, v, f, out, cellbuf, sign);
   }
 }
 
@@ -229,9 +239,9 @@ __global__ void __launch_bounds__(KF_THREADS) apply_ncf_kernel(const __grid_cons
   const CellCtx c = cell_ctx(op, alpha, beta, coef_const, hpow, cell);
   for (int i = threadIdx.x; i < N * N; i += blockDim.x) sB[i] = op.Bh[i];
   for (int i = threadIdx.x; i < P * N; i += blockDim.x) sD[i] = op.Dh[i];
-  load_comp(op, 0, N, P, P, c, u, U);
-  load_comp(op, 1, P, N, P, c, u, U + NF);
-  load_comp(op, 2, P, P, N, c, u, U + 2 * NF);
+  load_comp<P, N, P, P, 1>(op, 0, c, u, U);
+  load_comp<P, P, N, P, 2>(op, 1, c, u, U + NF);
+  load_comp<P, P, P, N, 4>(op, 2, c, u, U + 2 * NF);
   __syncthreads();
   const double* Ux = U;
   const double* Uy = U + NF;
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(KF_THREADS) apply_ncf_kernel(const __grid_cons
   __syncthreads();
   const double s2[3] = {2.0 * c.hx * c.hx / hv, 2.0 * c.hy * c.hy / hv, 2.0 * c.hz * c.hz / hv};
   constexpr int nloc = 3 * NF;
+  const long long base[3] = {comp_base(op, 0, c), comp_base(op, 1, c), comp_base(op, 2, c)};
   for (int l = threadIdx.x; l < 3 * NF; l += blockDim.x) {
     const int m = l / NF, r = l - m * NF;
     double v;
@@ -268,7 +279,7 @@ __global__ void __launch_bounds__(KF_THREADS) apply_ncf_kernel(const __grid_cons
       v = c.be * s2[2] * bline<P>(sB, Uz + r - cc * P * P, P * P, cc) + dtline<P>(sD, Dv + b * P + a, P * P, cc);
       skel = cc == 0 || cc == P;
     }
-    store_entry(op, m, a, b, cc, skel, c, cell, nloc, l, v, f, out, cellbuf, sign);
+    store_entry(op, base[m], m, a, b, cc, skel, cell, nloc, l, v, f, out, cellbuf, sign);
   }
 }
 
@@ -282,39 +293,45 @@ __global__ void kform_gather_kernel(const __grid_constant__ OpParams op, const d
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < ndof; g += (long long)gridDim.x * blockDim.x) {
     int m = 0;
     while (m + 1 < op.ncomp && g >= op.off[m + 1]) ++m;
-    const long long rr = g - op.off[m];
+    // 32-bit index math (component sizes < 2^31)
+    const int rr = (int)(g - op.off[m]);
     const int Lx = (int)op.len[m][0], Ly = (int)op.len[m][1];
-    const int idx[3] = {(int)(rr % Lx), (int)((rr / Lx) % Ly), (int)(rr / ((long long)Lx * Ly))};
-    int c0[3], a0[3], c1[3], a1[3], two[3], ls[3];
+    const int q = rr / Lx;
+    const int idx[3] = {rr - q * Lx, q % Ly, q / Ly};
+    int c0[3], a0[3], two[3], ls[3];
     bool skel = false, con = false;
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
       const bool P_ = op.fam[m][d] == 0;
       ls[d] = P_ ? p + 1 : p;
       int cc = idx[d] / p;
-      if (cc >= op.n[d]) cc = op.n[d] - 1;
       const int aa = idx[d] - cc * p;
-      c0[d] = cc; a0[d] = aa; two[d] = 0; c1[d] = cc; a1[d] = aa;
-      if (P_) {
-        if (aa == 0 || aa == p) skel = true;
-        if (aa == 0 && cc > 0) { c0[d] = cc - 1; a0[d] = p; two[d] = 1; c1[d] = cc; a1[d] = 0; }
-        con |= kf_cons(idx[d], (long long)op.n[d] * p, op.gamma_d, d);
+      two[d] = 0;
+      if (P_ && aa == 0) {
+        skel = true;
+        if (cc == 0) { c0[d] = 0; a0[d] = 0; }
+        else if (cc == op.n[d]) { c0[d] = cc - 1; a0[d] = p; }
+        else { c0[d] = cc - 1; a0[d] = p; two[d] = 1; }   // cells cc - 1 (local p) and cc (local 0)
+        con |= (cc == 0 && (op.gamma_d & (1u << (2 * d)))) || (cc == op.n[d] && (op.gamma_d & (2u << (2 * d))));
+      } else {
+        c0[d] = cc; a0[d] = aa;
       }
     }
-    if (!skel) continue;
+    if (!skel) continue;   // cell-interior entry: stored by the apply kernel
     if (con) { out[g] = 0.0; continue; }
     int lo = 0;
-    for (int q = 0; q < m; ++q) {
-      int s = 1;
-      for (int d = 0; d < 3; ++d) s *= (op.fam[q][d] == 0 ? p + 1 : p);
-      lo += s;
+    for (int t = 0; t < m; ++t) {
+      int sz = 1;
+      for (int d = 0; d < 3; ++d) sz *= (op.fam[t][d] == 0 ? p + 1 : p);
+      lo += sz;
     }
     double s = 0.0;
     for (int kz = 0; kz <= two[2]; ++kz)
       for (int ky = 0; ky <= two[1]; ++ky)
         for (int kx = 0; kx <= two[0]; ++kx) {
-          const int cx = kx ? c1[0] : c0[0], ax = kx ? a1[0] : a0[0];
-          const int cy = ky ? c1[1] : c0[1], ay = ky ? a1[1] : a0[1];
-          const int cz = kz ? c1[2] : c0[2], az = kz ? a1[2] : a0[2];
+          const int cx = c0[0] + kx, ax = kx ? 0 : a0[0];
+          const int cy = c0[1] + ky, ay = ky ? 0 : a0[1];
+          const int cz = c0[2] + kz, az = kz ? 0 : a0[2];
           const long long cell = ((long long)cz * op.n[1] + cy) * op.n[0] + cx;
           s += cellbuf[cell * nloc + lo + (az * ls[1] + ay) * ls[0] + ax];
         }

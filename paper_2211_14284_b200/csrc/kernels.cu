@@ -65,7 +65,9 @@ __device__ __forceinline__ void decode(long long g, int ncomp, const long long* 
   idx[2] = q / l1;
 }
 
-// t = D^T r on the potential space (zero on constrained potential DoFs)
+// t = D^T r on the potential space (zero on constrained potential DoFs).  D-hat's column
+// structure (eq:gradbasis: an interior column j has the single entry (j, j); columns 0 and p are
+// full) makes an interior index a one-term gather and a vertex index a p-term line sum.
 __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const double* __restrict__ r,
                                    double* __restrict__ t, long long npot) {
   __shared__ double Ds[RM_MAXP1 * RM_MAXP1];   // lane-varying indices: shared memory, not the param bank
@@ -76,7 +78,7 @@ __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const d
   int m;
   long long idx[3];
   decode(g, hp.ncomp_pot, hp.off_pot, hp.len_pot, m, idx);
-  const int p = hp.p;
+  const int p = hp.p, P1 = p + 1;
   for (int d = 0; d < 3; ++d)
     if (is_constrained_idx(hp.fam_pot[m][d], idx[d], (long long)hp.n[d] * p, hp.gamma_d, d)) { t[g] = 0.0; return; }
   const HipContrib* L = hp.kpot == 0 ? c_grad : c_curl;
@@ -85,25 +87,29 @@ __global__ void hiptmair_DT_kernel(const __grid_constant__ HipParams hp, const d
   for (int q = 0; q < nL; ++q) {
     if (L[q].m != m) continue;
     const int n = L[q].n, e = L[q].e;
-    // (D^T r)_I along e: I is a P index in direction e; cells containing I; r_n index c p + a (DP)
-    int cc[2], aa[2];
-    const int nc = cells_of(idx[e], FAM_P_, p, hp.n[e], cc, aa);
+    // (D^T r)_I along e: I is a P index in direction e; r_n has a DP index c p + a along e
+    const int lx = (int)hp.len_pri[n][0], ly = (int)hp.len_pri[n][1];
+    const int stride = e == 0 ? 1 : (e == 1 ? lx : lx * ly);
+    int j[3] = {(int)idx[0], (int)idx[1], (int)idx[2]};
+    const int I = j[e], c = I / p, aa = I - c * p;
+    j[e] = 0;
+    const double* rb = r + hp.off_pri[n] + ((long long)j[2] * ly + j[1]) * lx + j[0];
     double s = 0.0;
-    for (int k = 0; k < nc; ++k) {
-      long long j[3] = {idx[0], idx[1], idx[2]};
-      for (int a = 0; a < p; ++a) {
-        j[e] = (long long)cc[k] * p + a;
-        const double dv = Ds[a * (p + 1) + aa[k]];
-        if (dv == 0.0) continue;
-        s += dv * r[hp.off_pri[n] + (j[2] * hp.len_pri[n][1] + j[1]) * hp.len_pri[n][0] + j[0]];
-      }
+    if (aa != 0) {                 // interior column: the single entry (aa, aa)
+      s = Ds[aa * P1 + aa] * rb[(c * p + aa) * stride];
+    } else {                       // vertex column: cells c - 1 (as column p) and c (as column 0)
+      if (c >= 1)
+        for (int a = 0; a < p; ++a) s += Ds[a * P1 + p] * rb[((c - 1) * p + a) * stride];
+      if (c < hp.n[e])
+        for (int a = 0; a < p; ++a) s += Ds[a * P1] * rb[(c * p + a) * stride];
     }
     acc += L[q].sigma * s;
   }
   t[g] = acc;
 }
 
-// u += omega * D s on the primal space (zero contribution on constrained primal DoFs)
+// u += omega * D s on the primal space (zero contribution on constrained primal DoFs).  D-hat
+// row a has the entries (a, 0), (a, p) and, for a >= 1, (a, a): three gathers per term.
 __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, const double* __restrict__ s,
                                       double* __restrict__ u, double omega, long long npri) {
   __shared__ double Ds[RM_MAXP1 * RM_MAXP1];
@@ -114,7 +120,7 @@ __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, cons
   int n;
   long long idx[3];
   decode(g, hp.ncomp_pri, hp.off_pri, hp.len_pri, n, idx);
-  const int p = hp.p;
+  const int p = hp.p, P1 = p + 1;
   for (int d = 0; d < 3; ++d)
     if (is_constrained_idx(hp.fam_pri[n][d], idx[d], (long long)hp.n[d] * p, hp.gamma_d, d)) return;
   const HipContrib* L = hp.kpot == 0 ? c_grad : c_curl;
@@ -124,15 +130,14 @@ __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, cons
     if (L[q].n != n) continue;
     const int m = L[q].m, e = L[q].e;
     // (d_e s_m)_I : I is a DP index along e in cell c = I / p, a = I % p
-    const int c = (int)(idx[e] / p), a = (int)(idx[e] % p);
-    long long j[3] = {idx[0], idx[1], idx[2]};
-    double sum = 0.0;
-    for (int i = 0; i <= p; ++i) {
-      const double dv = Ds[a * (p + 1) + i];
-      if (dv == 0.0) continue;
-      j[e] = (long long)c * p + i;
-      sum += dv * s[hp.off_pot[m] + (j[2] * hp.len_pot[m][1] + j[1]) * hp.len_pot[m][0] + j[0]];
-    }
+    const int lx = (int)hp.len_pot[m][0], ly = (int)hp.len_pot[m][1];
+    const int stride = e == 0 ? 1 : (e == 1 ? lx : lx * ly);
+    int j[3] = {(int)idx[0], (int)idx[1], (int)idx[2]};
+    const int c = j[e] / p, a = j[e] - (j[e] / p) * p;
+    j[e] = c * p;
+    const double* sb = s + hp.off_pot[m] + ((long long)j[2] * ly + j[1]) * lx + j[0];
+    double sum = Ds[a * P1] * sb[0] + Ds[a * P1 + p] * sb[p * stride];
+    if (a >= 1) sum += Ds[a * P1 + a] * sb[a * stride];
     acc += L[q].sigma * sum;
   }
   u[g] += omega * acc;

@@ -192,6 +192,8 @@ struct PatchLaunch {
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
                                const KTimer* kt = nullptr, bool r_padded = false, bool zero_c = true,
                                bool combine = true);
+// u += omega * unpad(cpad) (the combine step of launch_patch_solve, on its own)
+cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st);
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;

@@ -914,6 +914,11 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   return cudaSuccess;
 }
 
+cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st) {
+  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp]);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
                                const KTimer* kt, bool r_padded, bool zero_c, bool combine) {
   if (L.npatch <= 0) {   // an empty family still does its part of a shared sequence

@@ -286,23 +286,30 @@ def test_nccl_transport_self_check(dev):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg", [3, 4])
-def test_full_size_hcurl_hdiv_configs_sweep(dev, cfg):
-    """BASELINE configs 3 and 4 at full size (24^3, p = 6 / 8): the patch plans fit (cfg4's ~95 KB
-    window boxes run with one box buffer and the sequential schedule) and a sweep is finite and
-    non-trivial.  (Parity of these paths is tested on the small shapes above, also with
-    RM_NBOX1=1 forcing the one-buffer schedule.)"""
+def test_full_size_hcurl_hdiv_sampled(dev, cfg):
+    """BASELINE configs 3 and 4 at full size (24^3, p = 6 / 8) in the bench's launch configuration
+    (cfg4's large windows take the one-box-buffer schedule): sweep outputs at sampled DoFs of every
+    component near an interior vertex, each recomputed by the oracle from the primary and potential
+    patches that reach it (oracle.solver.sampled_relax_ph, no global matrix)."""
     import paper_2211_14284_b200 as rmb
+    from oracle.fem import Space
+    from oracle.solver import sampled_relax_ph
     w = ri.CONFIGS[cfg]
     ctx = gu.setup_product(w)
-    n = ctx.n_local
-    mask = ctx.constrained_mask()
-    f = ri.uniform_vector(w.cfg, 0, n); f[mask] = 0
-    ft = torch.tensor(f, device=dev)
-    u = torch.zeros_like(ft)
-    rmb.rm_relax(ctx, ft, u, u, 1.0)
-    uh = u.cpu().numpy()
-    assert np.isfinite(uh).all() and np.abs(uh).max() > 0
-    assert np.abs(uh[mask]).max() == 0.0
+    sp_ = Space(w.space, w.p, w.nx, w.ny, w.nz)
+    f, u = vecs(w, ctx)
+    out = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
+    rmb.rm_relax(ctx, torch.tensor(f, device=dev), torch.tensor(u, device=dev), out, 1.0)
+    off = sp_.offsets()
+    rows = []
+    for m in range(3):
+        Lz, Ly, Lx = sp_.comp_shape(m)
+        x, y, z = 12 * w.p + 2, 11 * w.p + 1, 13 * w.p   # an interior vertex region (faces, edges, interiors)
+        rows += [off[m] + ((z + dz) * Ly + y + dy) * Lx + x + dx for dx, dy, dz in ((0, 0, 0), (-2, 1, 0))]
+    so = sampled_relax_ph(sp_, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d, f, u, rows, 1.0)
+    got = out.cpu().numpy()[rows]
+    tol = 1e-11 if cfg == 3 else hdiv_tol("2^3-p8")
+    check(f"cfg{cfg} full size relax ({len(rows)} rows, max-abs rel)", float(np.abs(got - so).max() / np.abs(so).max()), tol)
 
 
 # ------------------------------------------------------------------ p = 1 coarse level (f1)
