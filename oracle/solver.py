@@ -5,7 +5,8 @@
       r     = f - A u                                      (true A)
       c     = sum_i R_i^T A_i^{-1} R_i r                   (eq:asm-afw / first sum of eq:asm-hiptmair)
       PH:   c += D (sum_j R_j^T B_j^{-1} R_j) D^T r         (eq:asm-hiptmair)
-            B = D^T A D (k=1), B = D^T A D + eps_s beta M^{k-1} (k=2, remark P:916-927, reading G8)
+            B = the discretization of a^k(d phi, d psi) = the (k-1)-form operator with
+            (alpha', beta') = (beta, 0) (k=1) or (beta, eps_s beta) (k=2, remark P:916-927, G8)
       u_out = u + omega c                                   (reading G9)
   For the auxiliary-operator variant the patch matrices come from P instead of A.
   With `coarse`, PCG's preconditioner is the hybrid V(1,1) cycle with the p = 1 coarse level
@@ -119,11 +120,14 @@ class Problem:
         pspace = Space(kp, self.p, self.nx, self.ny, self.nz)
         pcon = pspace.constrained_mask(self.gamma_d)
         Pf = sp.diags((~pcon).astype(np.float64))
-        Af = assemble(self.space, self.X, self.alpha, self.beta)     # unconstrained A^k
-        B = D.T @ Af @ D
-        if self.k == 2:
-            M = assemble(pspace, self.X, np.zeros_like(self.alpha), self.beta)
-            B = B + self.potential_shift * M
+        # B "obtained as the discretization of a^k(d^{k-1} phi, d^{k-1} psi)": since
+        # d^k d^{k-1} = 0 this form is (d phi, beta d psi), i.e. the (k-1)-form operator with
+        # coefficients (alpha', beta') = (beta, 0), assembled directly by quadrature (+ the k = 2
+        # shift eps_s beta M^{k-1}, remark P:916-927, reading G8).  Forming D^T A D instead is equal
+        # in exact arithmetic but carries the round-off of D^T (alpha K^k) D ~ eps |K^k|, which grows
+        # like (alpha / beta) h^-2 (tests/test_oracle_pins.py pins the equality).
+        shift = self.potential_shift if self.k == 2 else 0.0
+        B = assemble(pspace, self.X, self.beta, shift * self.beta)
         B = (Pf @ B @ Pf).tocsr()
         pats = all_patches(pspace, kp, pcon, self.interior_only)
         sol = []

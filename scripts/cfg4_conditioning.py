@@ -72,7 +72,7 @@ def closed_form_parts(k, p, hx, hy, hz):
 
 def main():
     out = {}
-    for n, p in [(2, 3), (3, 4), (2, 8)]:
+    for n, p in [(2, 3), (3, 4), (5, 3), (2, 8)]:
         w = ri.CONFIGS[4].with_mesh(n).with_p(p)
         pb = Problem(w.space, w.p, n, n, n, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d,
                      decomposition="ph")

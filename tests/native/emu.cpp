@@ -294,6 +294,16 @@ static int emu_precondition_impl(int k, int p, int nx, int ny, int nz, unsigned 
       long long nlev = 0, mfin = 0, nv = 0;
       for (auto& C : F->classes) { nlev = std::max<long long>(nlev, C.lev.size()); mfin = std::max<long long>(mfin, C.m); nv = std::max<long long>(nv, C.nvals); }
       stats[3] = nlev; stats[4] = mfin; stats[5] = nv;
+      if (stats[6] == -1) {   // extended stats requested: window box, largest units (bytes) per channel
+        long long ua = 0, ub = 0;
+        for (auto& C : F->classes)
+          for (size_t u = 0; u < C.units.size(); ++u) {
+            const bool tile = (int)u >= C.tu0 && (int)u < C.tu1;
+            const long long by = C.units[u].mbytes + 8LL * C.units[u].nd;
+            if (tile) ub = std::max(ub, by); else ua = std::max(ua, by);
+          }
+        stats[6] = F->box_total; stats[7] = ua; stats[8] = ub;
+      }
     }
     return 0;
   } catch (const std::exception& e) {

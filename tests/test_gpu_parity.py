@@ -73,6 +73,9 @@ CASES = [
     ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), hdiv_tol("2^3-p3")),
     ("cfg4-3^3-p4", ri.CONFIGS[4].with_mesh(3).with_p(4), hdiv_tol("3^3-p4")),
     ("cfg4-2^3-p8", ri.CONFIGS[4].with_mesh(2), hdiv_tol("2^3-p8")),   # cfg4's own degree
+    # more patches than CTAs: the persistent kernel's cross-patch pipeline on edge / face families
+    ("cfg3-6^3-p3", ri.CONFIGS[3].with_mesh(6).with_p(3), 1e-11),
+    ("cfg4-5^3-p3", ri.CONFIGS[4].with_mesh(5).with_p(3), hdiv_tol("5^3-p3")),
     # trilinear cells (perturbed vertices): true operator by quadrature, auxiliary-operator
     # patches with ICC on the static-condensation pattern (cfg5 shapes at reduced size)
     ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3), 1e-11),
@@ -81,7 +84,8 @@ CASES = [
 ]
 # the one-box-buffer sequential schedule of the patch kernel (taken by full-size cfg4) forced
 NBOX1_CASES = [("nbox1-" + c[0], c[1], c[2]) for c in CASES if c[0] in ("cfg2-3^3", "cfg3-2^3-p3", "cfg4-2^3-p3",
-                                                                       "cfg5-3^3-p3", "cfg4-3^3-p4")]
+                                                                       "cfg5-3^3-p3", "cfg4-3^3-p4", "cfg3-6^3-p3",
+                                                                       "cfg4-5^3-p3")]
 
 
 @pytest.mark.parametrize("name,w,tol", CASES + NBOX1_CASES, ids=[c[0] for c in CASES + NBOX1_CASES])
