@@ -60,7 +60,10 @@ typedef enum {
   RM_ENCCL = -5       /* NCCL error (multi-GPU) */
 } rm_status;
 
-enum { RM_PAFW = 0, RM_PH = 1 };                       /* decomposition: vertex stars | k-stars + potential */
+/* decomposition: vertex stars | k-stars + potential | statically condensed vertex stars (SC-PAFW,
+ * eq:sc-pafw / eq:sc-asm-afw, H(grad) only: interface corrections from the vertex-star Schur
+ * complements S_v, cell interiors once, c_I = A_II^-1 (r_I - A_IG c_G)) */
+enum { RM_PAFW = 0, RM_PH = 1, RM_SC_PAFW = 2 };
 enum { RM_CHOL = 0, RM_ICC_SC = 1 };                   /* patch factorization */
 enum { RM_ALL_ENTITIES = 0, RM_INTERIOR_ONLY = 1 };    /* patch_entities (interior-only = test mode) */
 
@@ -75,7 +78,9 @@ typedef struct {
 
 typedef struct {
   int32_t decomposition;     /* RM_PAFW | RM_PH (k = 0: identical)                                 */
-  int32_t factorization;     /* RM_CHOL | RM_ICC_SC                                                 */
+  int32_t factorization;     /* RM_CHOL | RM_ICC_SC of the scalar (H(grad)) patch problems: the     */
+                             /* primary stars for k = 0, the PH potential vertex stars for k = 1     */
+                             /* (P:1158-1160); k-stars of k = 1, 2 are always exact  */
   int32_t patch_entities;    /* RM_ALL_ENTITIES | RM_INTERIOR_ONLY                                  */
   double potential_shift;    /* eps_s for k = 2 PH (reading G8), default 1e-3                        */
   int32_t coarse;            /* 0: one-level additive Schwarz in rm_precondition / rm_pcg; 1: the    */

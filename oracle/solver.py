@@ -25,7 +25,21 @@ import numpy as np
 import scipy.sparse as sp
 
 from .fem import Space, assemble, assemble_aux, apply_matfree, global_derivative
-from .patches import DenseCholeskyPatch, ICCSCPatch, all_patches
+from .patches import DenseCholeskyPatch, ICCSCPatch, all_patches, icc_masked
+
+
+class _TriangularPair:
+    """Solve with L L^T for a sparse lower triangular L (ICC factor)."""
+
+    def __init__(self, L):
+        import scipy.sparse.linalg as spla
+        self._spla = spla
+        self.L = L.tocsr()
+        self.LT = self.L.T.tocsr()
+
+    def solve(self, b):
+        y = self._spla.spsolve_triangular(self.L, b, lower=True)
+        return self._spla.spsolve_triangular(self.LT, y, lower=False)
 
 EPS_S = 1e-3   # reading G8 (DESIGN.md): eps_s = 1e-3 of the potential-space mass
 
@@ -41,7 +55,7 @@ class Problem:
     alpha: np.ndarray        # (nz, ny, nx)
     beta: np.ndarray
     gamma_d: int
-    decomposition: str = "pafw"      # "pafw" | "ph"
+    decomposition: str = "pafw"      # "pafw" | "ph" | "sc-pafw" (k = 0, eq:sc-asm-afw)
     factorization: str = "chol"      # "chol" | "icc_sc"
     interior_only: bool = False
     matfree: bool = False            # apply A cell by cell (large p) instead of via CSR
@@ -59,6 +73,7 @@ class Problem:
         self._patches = None
         self._pot = None
         self._coarse = None
+        self._sc = None
 
     # ---------------------------------------------------------------- operator
     @property
@@ -84,7 +99,7 @@ class Problem:
 
     # ---------------------------------------------------------------- patches
     def _patch_dim(self):
-        return 0 if self.decomposition == "pafw" else self.k
+        return self.k if self.decomposition == "ph" else 0
 
     def patch_solvers(self):
         if self._patches is not None:
@@ -92,13 +107,15 @@ class Problem:
         dim = self._patch_dim()
         pats = all_patches(self.space, dim, self.constrained, self.interior_only)
         out = []
-        if self.factorization == "chol":
+        # the factorization option applies to the scalar (H(grad)) patch problems: the primary
+        # patches for k = 0, the PH potential patches for k = 1; the k-star patches
+        # of k = 1, 2 are always factored exactly (their Cholesky has optimal fill)
+        if self.factorization == "chol" or self.k >= 1:
             A = self.A
             for ent, g, grp in pats:
                 Ai = A[g][:, g].toarray()
                 out.append((g, DenseCholeskyPatch(Ai)))
         elif self.factorization == "icc_sc":
-            assert self.k == 0
             Paux, Spat = assemble_aux(self.space, self.X, self.alpha, self.beta)
             for ent, g, grp in pats:
                 Ai = Paux[g][:, g].tocsr()
@@ -131,14 +148,85 @@ class Problem:
         B = (Pf @ B @ Pf).tocsr()
         pats = all_patches(pspace, kp, pcon, self.interior_only)
         sol = []
-        for ent, g, grp in pats:
-            sol.append((g, DenseCholeskyPatch(B[g][:, g].toarray())))
+        if self.factorization == "icc_sc" and kp == 0:
+            # "On the auxiliary scalar-valued problem posed on the vertex star, we employ the
+            # incomplete Cholesky factorization described above": ICC on the
+            # static-condensation pattern of the potential vertex-star matrices, with the
+            # structural pattern of the H(grad) operator (auxiliary pattern = Cartesian pattern)
+            _, Spat = assemble_aux(pspace, self.X, self.beta, shift * self.beta)
+            for ent, g, grp in pats:
+                sol.append((g, ICCSCPatch(B[g][:, g].tocsr(), Spat[g][:, g].tocsr(), grp == 0)))
+        else:
+            for ent, g, grp in pats:
+                sol.append((g, DenseCholeskyPatch(B[g][:, g].toarray())))
         self._pot = (D.tocsr(), pcon, sol)
         return self._pot
+
+    # ---------------------------------------------------------- statically condensed (SC-PAFW)
+    def sc_data(self):
+        """SC-PAFW (eq:sc-pafw, eq:schur, eq:sc-asm-afw; k = 0): the operator the patches are
+        built from (A on Cartesian cells, the auxiliary P with ICC-SC), its interior set I = the
+        cell-interior DoFs (A_II is diagonal for k = 0), and per vertex star the
+        interface DoFs with a factor of S_v = A_v,GG - A_v,GI A_v,II^{-1} A_v,IG -- exact dense
+        Cholesky, or ICC(0) on S_v's own structural pattern for SC-ICC (reading G19)."""
+        if self._sc is not None:
+            return self._sc
+        assert self.k == 0
+        if self.factorization == "icc_sc":
+            At, Spat = assemble_aux(self.space, self.X, self.alpha, self.beta)
+            Pf = sp.diags(self.free.astype(np.float64))
+            At = (Pf @ At @ Pf).tocsr()
+        else:
+            At, Spat = self.A, None
+        n = self.space.ndof
+        ids = np.arange(n)
+        Lz, Ly, Lx = self.space.comp_shape(0)
+        p = self.p
+        interior = (ids % Lx % p != 0) & ((ids // Lx) % Ly % p != 0) & (ids // (Lx * Ly) % p != 0)
+        I = np.flatnonzero(interior & self.free)
+        dI = At.diagonal()[I]
+        pats = all_patches(self.space, 0, self.constrained, self.interior_only)
+        out = []
+        for ent, g, grp in pats:
+            gI, gG = g[grp == 0], g[grp != 0]
+            if len(gG) == 0:
+                continue
+            AGG = At[gG][:, gG].toarray()
+            AGI = At[gG][:, gI].toarray()
+            Sv = AGG - AGI @ (AGI.T / At.diagonal()[gI][:, None])
+            if Spat is None:
+                out.append((gG, DenseCholeskyPatch(Sv)))
+            else:
+                pb_ = (Spat != 0).astype(np.int64).tocsr()
+                PGG, PGI = pb_[gG][:, gG], pb_[gG][:, gI]
+                mask = sp.tril(((PGG + PGI @ PGI.T) != 0).astype(np.int64), format="csr")
+                L = icc_masked(sp.csr_matrix(Sv), mask)
+                out.append((gG, _TriangularPair(L)))
+        self._sc = (At, I, dI, out)
+        return self._sc
+
+    def precondition_sc(self, r):
+        """c = R_I^T A_II^{-1} R_I r + R_G^T (sum_v R_v^T S_v^{-1} R_v) R_G r (eq:schur, eq:sc-asm-afw
+        without the coarse term), R_G = [-A_GI A_II^{-1}, I]."""
+        At, I, dI, pats = self.sc_data()
+        r = np.where(self.free, r, 0.0)
+        yI = r[I] / dI
+        rG = r.copy()
+        rG[I] = 0.0
+        rG -= At[:, I] @ yI
+        rG[I] = 0.0
+        cG = np.zeros_like(r)
+        for gG, S in pats:
+            cG[gG] += S.solve(rG[gG])
+        c = cG.copy()
+        c[I] = (r[I] - (At[I] @ cG)) / dI
+        return np.where(self.free, c, 0.0)
 
     # ---------------------------------------------------------------- sweep
     def precondition(self, r):
         """c = P^{-1} r (the additive Schwarz sum), r zero on constrained DoFs."""
+        if self.decomposition == "sc-pafw":
+            return self.precondition_sc(r)
         c = np.zeros_like(r)
         for g, S in self.patch_solvers():
             c[g] += S.solve(r[g])

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librm.so")
 
 RM_HGRAD, RM_HCURL, RM_HDIV = 0, 1, 2
-RM_PAFW, RM_PH = 0, 1
+RM_PAFW, RM_PH, RM_SC_PAFW = 0, 1, 2
 RM_CHOL, RM_ICC_SC = 0, 1
 RM_ALL_ENTITIES, RM_INTERIOR_ONLY = 0, 1
 RM_OK, RM_NOT_CONVERGED = 0, 1

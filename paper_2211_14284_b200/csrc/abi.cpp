@@ -240,6 +240,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     Lh.sc_nk = F.upload(P.sc_nk);
     Lh.sc_fb = F.upload(std::vector<double>(P.sc_nk.size() * 6 * (size_t)(P.sp.p - 1) * (P.sp.p - 1), 0.0));
     Lh.sc_p = P.sp.p;
+    Lh.sc_pre = P.sc_pre ? 1 : 0;
     for (int d = 0; d < 3; ++d) Lh.sc_n[d] = P.sp.n[d];
   }
   {
@@ -608,7 +609,12 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     if (gamma_d > 0x3F) throw RmError(RM_EINVAL, "gamma_d has bits above bit 5");
     if (o.coarse != 0 && o.coarse != 1) throw RmError(RM_EINVAL, "coarse must be 0 or 1");
     if (o.coarse && o.nranks > 1) throw RmError(RM_EINVAL, "the coarse level is single-rank only");
-    if (o.decomposition != RM_PAFW && o.decomposition != RM_PH) throw RmError(RM_EINVAL, "bad decomposition");
+    if (o.decomposition != RM_PAFW && o.decomposition != RM_PH && o.decomposition != RM_SC_PAFW)
+      throw RmError(RM_EINVAL, "bad decomposition");
+    if (o.decomposition == RM_SC_PAFW && space != 0)
+      throw RmError(RM_EINVAL, "SC-PAFW is built for H(grad) only (SC-PH for k = 1, 2 is not)");
+    if (o.decomposition == RM_SC_PAFW && o.nranks > 1)
+      throw RmError(RM_EINVAL, "SC-PAFW is single-rank only");
     if (o.factorization != RM_CHOL && o.factorization != RM_ICC_SC) throw RmError(RM_EINVAL, "bad factorization");
     const int64_t ncell = (int64_t)mesh->nx * mesh->ny * mesh->nz;
     if (!(n_alpha == 1 || n_alpha == ncell) || !(n_beta == 1 || n_beta == ncell))
@@ -654,7 +660,8 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     c->nranks = std::max(o.nranks, 1);
     c->part = part;
     c->k = space; c->p = p; c->n[0] = mesh->nx; c->n[1] = mesh->ny; c->n[2] = mesh->nz;
-    c->gamma = gamma_d; c->decomposition = (space == 0) ? RM_PAFW : o.decomposition;
+    c->gamma = gamma_d;
+    c->decomposition = (space == 0) ? (o.decomposition == RM_SC_PAFW ? RM_SC_PAFW : RM_PAFW) : o.decomposition;
     c->st = static_cast<cudaStream_t>(o.stream);
     c->device = o.device;
     c->sp.init(space, p, mesh->nx, mesh->ny, mesh->nz);
@@ -751,8 +758,12 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.k = space; in.p = p; in.n[0] = mesh->nx; in.n[1] = mesh->ny; in.n[2] = mesh->nz;
     in.gamma_d = gamma_d; in.coords = mesh->coords; in.alpha = alpha; in.beta = beta;
     in.n_alpha = n_alpha; in.n_beta = n_beta;
-    in.dim = (c->decomposition == RM_PAFW) ? 0 : space;
-    in.factorization = o.factorization;
+    in.dim = (c->decomposition == RM_PH) ? space : 0;
+    in.sc_decomposition = c->decomposition == RM_SC_PAFW;
+    // options.factorization applies to the scalar (H(grad)) patch problems: the primary patches
+    // for k = 0, the PH potential vertex stars for k = 1; k-star patches of k = 1, 2
+    // are factored exactly (optimal fill)
+    in.factorization = space == 0 ? o.factorization : RM_CHOL;
     in.interior_only = o.patch_entities == RM_INTERIOR_ONLY;
     in.cartesian = cart;
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
@@ -777,7 +788,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       rm::SetupInput ip = in;
       ip.k = space - 1; ip.alpha = ap.data(); ip.beta = bp.data(); ip.n_alpha = n_beta; ip.n_beta = n_beta;
       ip.dim = space - 1;
-      ip.factorization = RM_CHOL;
+      ip.factorization = (space == 1) ? o.factorization : RM_CHOL;
       const int no = (ip.dim == 1 || ip.dim == 2) && !rm::exp_env("RM_ONE_FAMILY") ? 3 : 1;
       c->pots.assign(no, DevFamily{});
       for (int o = 0; o < no; ++o) {

@@ -166,6 +166,8 @@ struct PatchLaunch {
   const int* sc_nk;
   double* sc_fb;         // per-cell face line sums of the pre step [ncell][6][(p-1)^2]
   int icc_only;          // every class ends in ICC (no dense tiles): the tile warps join the sparse warps
+  int sc_pre;            // run the static-condensation pre step (sc programs); SC-PAFW with the exact
+                         // program has only the post step
   int sc_p, sc_n[3];
   int n_max, piv_max, mem_max, aux_max;   // largest class: DoFs, pivot doubles, member u16, scratch doubles
   size_t smem_fixed;     // barriers + 2 boxes + aux (bytes)

@@ -936,7 +936,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   }
   ScGeom sg{};
   long long nface = 0, nint = 0;
-  if (L.sc_dinv) {
+  if (L.sc_dinv) {   // geometry for the pre / post steps
     sg.p = L.sc_p;
     for (int d = 0; d < 3; ++d) sg.n[d] = L.sc_n[d];
     sg.lxp = L.pad.lxp[0];
@@ -945,7 +945,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     nface = ((long long)(sg.n[0] + 1) * sg.n[1] * sg.n[2] + (long long)(sg.n[1] + 1) * sg.n[0] * sg.n[2] +
              (long long)(sg.n[2] + 1) * sg.n[0] * sg.n[1]) * pm * pm;
     nint = (long long)sg.n[0] * sg.n[1] * sg.n[2] * pm * pm * pm;
-    if (nface > 0) {
+    if (nface > 0 && L.sc_pre) {
       const int ncell = sg.n[0] * sg.n[1] * sg.n[2];
       const size_t smem = sizeof(double) * (size_t)(pm * pm * pm);
       static size_t smem_set = 0;

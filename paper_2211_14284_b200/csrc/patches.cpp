@@ -1319,6 +1319,11 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     for (int m = 0; m < fam->nsub; ++m)
       for (int b = fam->boff[m]; b < fam->boff[m] + fam->box[m][0] * fam->box[m][1] * fam->box[m][2]; ++b)
         if (!used[b]) C.zlist.push_back(b);
+    // SC-PAFW with the exact elimination program: the patch-local interior corrections are not
+    // scattered (the post step computes the cell interiors once from the interface corrections)
+    if (in.sc_decomposition && !C.sc)
+      for (int t2 = 0; t2 < C.n; ++t2)
+        if (C.group[t2] == 0 && C.bidx[t2] >= 0) C.zlist.push_back(C.bidx[t2]);
     build_meta(C);
   }
   fam->nfactors = (int64_t)foff.size();
@@ -1354,7 +1359,8 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     }
   }
   fam->sigma_max = smax;
-  if (fam_sc) {
+  fam->sc_pre = fam_sc;
+  if (fam_sc || in.sc_decomposition) {
     // per-cell static-condensation data from the same cell entries the patch matrices use
     const Space& sp = B.sp;
     const int p = sp.p, P1 = p + 1, pm = p - 1, ni = pm * pm * pm;
@@ -1425,6 +1431,8 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
       }
       for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0]) ++fam->sc_nk[((int64_t)cz * sp.n[1] + cy) * sp.n[0] + cx];
     }
+    // SC-PAFW: the cell interiors are solved once (eq:schur: R_I^T A_II^-1 R_I + R_G^T S^-1 R_G)
+    if (in.sc_decomposition) std::fill(fam->sc_nk.begin(), fam->sc_nk.end(), 1);
   }
   if (!first_err.empty()) throw std::runtime_error(first_err);
   return fam;

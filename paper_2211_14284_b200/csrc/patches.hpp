@@ -177,6 +177,7 @@ struct PatchFamily {
   // number of patches containing the cell
   std::vector<double> sc_dinv, sc_c;
   std::vector<int> sc_nk;
+  bool sc_pre = false;            // the static-condensation PRE step runs outside the patch kernel (sc programs)
   int box_total = 0;
   double sigma_max = 0.0;         // largest ICC restart shift used (reading G7)
   int64_t nfactors = 0;           // distinct value blocks
@@ -199,6 +200,8 @@ struct SetupInput {
   const double* hx; const double* hy; const double* hz;   // per-direction cell sizes (cartesian)
   int zv_lo = 0, zv_hi = 1 << 30;   // vertex stars kept: z vertex layers [zv_lo, zv_hi) (z-slab ownership)
   int orient = -1;                  // edge / face stars: keep one orientation (edge direction / face normal), -1 = all
+  bool sc_decomposition = false;    // SC-PAFW (eq:sc-asm-afw, k = 0): interface corrections from the patches, cell
+                                    // interiors once afterwards (c_I = A_II^-1 (r_I - A_IG c_G), n_K = 1)
 };
 
 // Builds the full patch family. Throws std::runtime_error with a message on failure.

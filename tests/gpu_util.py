@@ -9,7 +9,7 @@ def setup_product(w, **kw):
     coords = None if w.perturb == 0 else ri.vertex_coords(w)
     return rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(),
                         w.gamma_d, coords=coords,
-                        decomposition=kw.pop("decomposition", rmb.RM_PH if w.decomposition == "ph" else rmb.RM_PAFW),
+                        decomposition=kw.pop("decomposition", {"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW}.get(w.decomposition, rmb.RM_PAFW)),
                         factorization=kw.pop("factorization", rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL),
                         **kw)
 
@@ -22,3 +22,24 @@ def setup_oracle(w, **kw):
 
 def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def oracle_noise_floor(w, f, u):
+    """Relative L2 difference of the oracle's own sweep with the Cartesian cell matrices from
+    quadrature vs from the box closed form (identical in exact arithmetic; oracle only,
+    scripts/cfg4_conditioning.py): the round-off floor two exact implementations share."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import oracle.fem as fem
+    from cfg4_conditioning import closed_form_parts
+    a = setup_oracle(w).relax(f, u)
+    fem._cartesian_parts.cache_clear()
+    orig = fem._cartesian_parts
+    fem._cartesian_parts = closed_form_parts
+    try:
+        b = setup_oracle(w).relax(f, u)
+    finally:
+        fem._cartesian_parts = orig
+        fem._cartesian_parts.cache_clear()
+    return rel(b, a)

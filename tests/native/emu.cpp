@@ -73,7 +73,7 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
     return cell_dof(cx, cy, cz, a, b, c);
   };
   std::vector<double> rsc(r_in, r_in + sp.ndof()), cacc(sp.ndof(), 0.0);
-  if (sc)
+  if (sc && F.sc_pre)   // (SC-PAFW with the exact program: the patch elimination does the pre step)
     for (int cz = 0; cz < sp.n[2]; ++cz)
       for (int cy = 0; cy < sp.n[1]; ++cy)
         for (int cx = 0; cx < sp.n[0]; ++cx) {
@@ -281,7 +281,8 @@ static int emu_precondition_impl(int k, int p, int nx, int ny, int nz, unsigned 
     SetupInput in{};
     in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
     in.coords = coords; in.alpha = alpha; in.beta = beta; in.n_alpha = na; in.n_beta = nb;
-    in.dim = dim; in.factorization = fact; in.interior_only = interior_only;
+    in.dim = dim; in.factorization = fact; in.interior_only = interior_only & 1;
+    in.sc_decomposition = (interior_only & 2) != 0;   // bit 1: SC-PAFW
     in.cartesian = (coords == nullptr);
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
     in.zv_lo = zv_lo; in.zv_hi = zv_hi;
@@ -388,7 +389,8 @@ int emu_family_nnz(int k, int p, int nx, int ny, int nz, unsigned gamma, int dim
     SetupInput in{};
     in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
     in.coords = nullptr; in.alpha = &one; in.beta = &one; in.n_alpha = 1; in.n_beta = 1;
-    in.dim = dim; in.factorization = fact; in.interior_only = interior_only;
+    in.dim = dim; in.factorization = fact; in.interior_only = interior_only & 1;
+    in.sc_decomposition = (interior_only & 2) != 0;   // bit 1: SC-PAFW
     in.cartesian = true;
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
     auto F = build_patch_family(in);

@@ -181,3 +181,60 @@ def test_product_coarse_level_matches_oracle(emu, name, w):
     assert rc == 0, err.value
     zo = CoarseLevel(pb).apply(r)
     assert np.linalg.norm(z - zo) / np.linalg.norm(zo) < 1e-11
+
+
+@pytest.mark.parametrize("n,p", [(2, 3), (3, 4)])
+def test_product_icc_sc_potential_matches_oracle(emu, n, p):
+    """Row f3: ICC on the static-condensation pattern for the H(curl) PH potential vertex stars
+     -- the product's k = 0 ICC-SC family on Cartesian cells with the potential
+    coefficients (alpha', beta') = (beta, 0), re-enacted on the host, equals the oracle's potential
+    patch solves (oracle.solver.Problem.potential with factorization icc_sc)."""
+    from oracle.solver import Problem
+    w = ri.CONFIGS[3].with_mesh(n).with_p(p)
+    beta = np.full((n, n, n), 0.7)
+    pb = Problem(1, p, n, n, n, ri.vertex_coords(w), np.ones((n, n, n)), beta, w.gamma_d, decomposition="ph",
+                 factorization="icc_sc")
+    D, pcon, sol = pb.potential()
+    t = ri.uniform_vector(3, 5, D.shape[1])
+    t[pcon] = 0
+    so = np.zeros_like(t)
+    for g, S in sol:
+        so[g] += S.solve(t[g])
+    al = np.ascontiguousarray(beta.ravel())
+    be = np.zeros_like(al)
+    z = np.zeros_like(t)
+    err = ctypes.create_string_buffer(256)
+    st = (ctypes.c_longlong * 10)()
+    rc = emu.emu_precondition(0, p, n, n, n, w.gamma_d, _dp(al), al.size, _dp(be), be.size, None, 0, 1, 0, _dp(t),
+                              _dp(z), err, 256, st)
+    assert rc == 0, err.value
+    assert np.linalg.norm(z - so) / np.linalg.norm(so) < 1e-11
+
+
+@pytest.mark.parametrize("name,w", [
+    ("cfg1-sc-chol", ri.CONFIGS[1].with_mesh(3)),
+    ("cfg2-sc-chol-logalpha", ri.CONFIGS[2].with_mesh(3).with_p(4)),
+    ("cfg5-sc-icc", ri.CONFIGS[5].with_mesh(2).with_p(3)),
+    ("cfg5-sc-icc-3^3p5", ri.CONFIGS[5].with_mesh(3).with_p(5)),
+])
+def test_product_sc_pafw_matches_oracle(emu, name, w):
+    """Row f2 (k = 0): SC-PAFW (eq:sc-asm-afw) -- the product's family with the interior
+    corrections zeroed in the boxes (exact program) or n_K = 1 (ICC-SC program) and the post step
+    c_I = A_II^{-1}(r_I - A_IG c_G), re-enacted on the host, equals the oracle's definition."""
+    from oracle.solver import Problem
+    pb = Problem(w.space, w.p, w.nx, w.ny, w.nz, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d,
+                 decomposition="sc-pafw", factorization=w.factorization)
+    r = ri.uniform_vector(w.cfg, 0, pb.space.ndof)
+    r[pb.constrained] = 0
+    al = np.ascontiguousarray(ri.cell_alpha(w).ravel())
+    be = np.ascontiguousarray(ri.cell_beta(w).ravel())
+    coords = None if w.perturb == 0 else np.ascontiguousarray(ri.vertex_coords(w).ravel())
+    z = np.zeros_like(r)
+    err = ctypes.create_string_buffer(256)
+    st = (ctypes.c_longlong * 10)()
+    fact = 1 if w.factorization == "icc_sc" else 0
+    rc = emu.emu_precondition(0, w.p, w.nx, w.ny, w.nz, w.gamma_d, _dp(al), al.size, _dp(be), be.size,
+                              None if coords is None else _dp(coords), 0, fact, 2, _dp(r), _dp(z), err, 256, st)
+    assert rc == 0, err.value
+    zo = pb.precondition(r)
+    assert np.linalg.norm(z - zo) / np.linalg.norm(zo) < 1e-11

@@ -28,7 +28,7 @@ def setup_pair(w, **kw):
     from oracle.solver import Problem
     coords = None if w.perturb == 0 else ri.vertex_coords(w)
     ctx = rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(), w.gamma_d,
-                       coords=coords, decomposition=rmb.RM_PH if w.decomposition == "ph" else rmb.RM_PAFW,
+                       coords=coords, decomposition={"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW}.get(w.decomposition, rmb.RM_PAFW),
                        factorization=rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL,
                        patch_entities=kw.get("patch_entities", 0))
     pb = Problem(w.space, w.p, w.nx, w.ny, w.nz, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d,
@@ -81,6 +81,16 @@ CASES = [
     ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3), 1e-11),
     ("cfg5-2^3-p7", ri.CONFIGS[5].with_mesh(2).with_p(7), 1e-11),
     ("cfg5-2^3-p15", ri.CONFIGS[5].with_mesh(2), 1e-11),             # cfg5's own degree (n_q = 24)
+    # row f3: PAFW vertex stars for k = 1, 2, ICC-SC on the H(curl) potential
+    ("cfg3-pafw-2^3-p3", dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), decomposition="pafw"), 1e-11),
+    ("cfg4-pafw-2^3-p3", dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), decomposition="pafw"), None),
+    ("cfg3-iccsc-2^3-p3", dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), factorization="icc_sc"), 1e-11),
+    ("cfg3-iccsc-3^3-p4", dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(4), factorization="icc_sc"), 1e-11),
+    # row f2 (k = 0): statically condensed vertex stars SC-PAFW (eq:sc-asm-afw), exact and ICC
+    ("cfg1-sc", dataclasses.replace(ri.CONFIGS[1], decomposition="sc-pafw"), 1e-11),
+    ("cfg2-sc-3^3-p4", dataclasses.replace(ri.CONFIGS[2].with_mesh(3).with_p(4), decomposition="sc-pafw"), 1e-11),
+    ("cfg5-sc-3^3-p3", dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"), 1e-11),
+    ("cfg5-sc-2^3-p7", dataclasses.replace(ri.CONFIGS[5].with_mesh(2).with_p(7), decomposition="sc-pafw"), 1e-11),
 ]
 # the one-box-buffer sequential schedule of the patch kernel (taken by full-size cfg4) forced
 NBOX1_CASES = [("nbox1-" + c[0], c[1], c[2]) for c in CASES if c[0] in ("cfg2-3^3", "cfg3-2^3-p3", "cfg4-2^3-p3",
@@ -97,6 +107,8 @@ def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
     assert (ctx.constrained_mask() == pb.constrained).all()
     assert ctx.n_free == int(pb.free.sum())
     f, u = vecs(w, ctx)
+    if tol is None:   # H(div) PAFW: 10x the oracle's own assembly noise on this shape
+        tol = max(1e-11, 10 * gu.oracle_noise_floor(w, f, u))
     ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
     v = torch.empty_like(ut)
     rmb.rm_apply(ctx, ut, v)
@@ -120,7 +132,16 @@ def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
 @pytest.mark.parametrize("name,w", [("cfg1", ri.CONFIGS[1]), ("cfg2-2^3-p3", ri.CONFIGS[2].with_mesh(2).with_p(3)),
                                     ("cfg3-2^3-p3", ri.CONFIGS[3].with_mesh(2).with_p(3)),
                                     ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3)),
-                                    ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3))])
+                                    ("cfg5-3^3-p3", ri.CONFIGS[5].with_mesh(3).with_p(3)),
+                                    ("cfg3-pafw-2^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), decomposition="pafw")),
+                                    ("cfg4-pafw-2^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), decomposition="pafw")),
+                                    ("cfg3-iccsc-3^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(3), factorization="icc_sc")),
+                                    ("cfg1-sc", dataclasses.replace(ri.CONFIGS[1], decomposition="sc-pafw")),
+                                    ("cfg5-sc-3^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"))])
 def test_pcg_iterations(dev, name, w):
     import paper_2211_14284_b200 as rmb
     ctx, pb = setup_pair(w)
