@@ -162,6 +162,7 @@ def _ph_iterations(k, p, n, beta, with_stage=True):
                  decomposition="ph")
     if not with_stage:   # drop the potential stage: only the k-star patches remain
         pb.decomposition = "ph-no-potential"   # Problem.precondition runs the stage only for "ph"
+        pb._patch_dim = lambda: k              # ... but keep the k-star patches
     f = ri.uniform_vector(10 + k, 0, pb.space.ndof)
     f[pb.constrained] = 0.0
     _, it, rel = pb.pcg(f, maxit=400)
