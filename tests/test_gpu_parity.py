@@ -333,7 +333,14 @@ def test_full_size_hcurl_hdiv_sampled(dev, cfg):
         rows += [off[m] + ((z + dz) * Ly + y + dy) * Lx + x + dx for dx, dy, dz in ((0, 0, 0), (-2, 1, 0))]
     so = sampled_relax_ph(sp_, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d, f, u, rows, 1.0)
     got = out.cpu().numpy()[rows]
-    tol = 1e-11 if cfg == 3 else hdiv_tol("2^3-p8")
+    # tolerance: 10x the ORACLE's own noise floor at these rows (quadrature vs closed-form cell
+    # matrices, identical in exact arithmetic: scripts/fullsize_noise_floor.py), floored at 1e-11;
+    # at h = 1/24 the edge / face-star patch problems are ill-conditioned (stiffness / mass ~
+    # p^4 / h^2), DESIGN.md §7
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fullsize_noise_floor.json")))["cases"]
+    tol = max(1e-11, 10 * g[f"cfg{cfg}"]["oracle_vs_closed_form_assembly_maxabs_rel"])
     check(f"cfg{cfg} full size relax ({len(rows)} rows, max-abs rel)", float(np.abs(got - so).max() / np.abs(so).max()), tol)
 
 
