@@ -503,6 +503,26 @@ int emu_coarse(int k, int p, int nx, int ny, int nz, unsigned gamma, const doubl
   }
 }
 
+// values per piece kind (PIV, W, TILE, ICCF, ICCB, WT, FINAL, ZERO) of the largest class of a family
+// (diagnostic of the stream layout), plus its n, m, levels
+int emu_family_breakdown(int k, int p, int nx, int dim, int orient, long long* out) {
+  std::vector<double> h(nx, 1.0 / nx);
+  const double one = 1.0;
+  SetupInput in{};
+  in.k = k; in.p = p; in.n[0] = in.n[1] = in.n[2] = nx; in.gamma_d = 63;
+  in.coords = nullptr; in.alpha = &one; in.beta = &one; in.n_alpha = 1; in.n_beta = 1;
+  in.dim = dim; in.factorization = 0; in.interior_only = 1; in.cartesian = true;
+  in.hx = h.data(); in.hy = h.data(); in.hz = h.data(); in.orient = orient;
+  auto F = build_patch_family(in);
+  const ClassProgram* best = nullptr;
+  for (auto& C : F->classes) if (!best || C.nvals > best->nvals) best = &C;
+  for (int q = 0; q < 12; ++q) out[q] = 0;
+  if (!best) return 1;
+  for (auto& pc : best->pieces) out[pc.kind] += pc.nd;
+  out[8] = best->n; out[9] = best->m; out[10] = (long long)best->lev.size(); out[11] = best->nvals;
+  return 0;
+}
+
 // 1D basis tables of the product (for cross-checks against the oracle's basis)
 int emu_basis(int p, double* S, double* lam, double* B, double* A, double* D, double* G) {
   const Basis1D& b = basis(p);
