@@ -151,13 +151,13 @@ def oracle_sweep_rate(w, cfg):
 
 
 def measure(w, cfg, args, world, rank, local, torch, dist, rmb, with_e2e=True):
-    """Set up one workload (z-slabs over the ranks for H(grad), replicas otherwise), time
+    """Set up one workload (z-slabs over the ranks at N > 1), time
     args.steps sweeps after args.warmup, and return the bench-line fields of that workload."""
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
-    # N > 1, H(grad): weak-scaled z-slabs of ONE global mesh (nz * N layers), each rank the N = 1
-    # workload's cells plus halos, exchanged by the library over NCCL inside rm_relax (row a3).
-    slab = world > 1 and w.space == 0
+    # N > 1: weak-scaled z-slabs of ONE global mesh (nz * N layers), each rank the N = 1 workload's
+    # cells plus halos, exchanged by the library over NCCL inside rm_relax (row a3; every space)
+    slab = world > 1
     wg = dataclasses.replace(w, nz=w.nz * world) if slab else w
     t0 = time.perf_counter()
     coords = None if wg.perturb == 0 else ri.vertex_coords(wg)

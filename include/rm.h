@@ -116,10 +116,11 @@ typedef struct {
 
 void rm_default_options(rm_options *opt);
 
-/* Z-SLAB PARTITION (multi-GPU, H(grad) vertex stars only).  Rank g of G owns
+/* Z-SLAB PARTITION (multi-GPU; every space and decomposition except SC-PAFW).  Rank g of G owns
  * the cell layers [mesh.z_begin, mesh.z_end) (contiguous slabs, rank order = z order), the DoF
- * planes z_begin*p .. z_end*p - 1 (the last rank also the top plane nz*p) and the vertex-star
- * patches of the vertex layers z_begin .. z_end - 1 (+ nz on the last rank).  Its LOCAL problem
+ * planes z_begin*p .. z_end*p - 1 (the last rank also the top plane nz*p) and the star patches
+ * (primary and potential) whose entity's z anchor -- a vertex layer, or the cell layer of an
+ * entity spanning a cell in z -- lies in z_begin .. z_end - 1 (+ the vertex layer nz on the last rank).  Its LOCAL problem
  * is its slab plus one ghost cell layer below (rank > 0) and the shared plane above, so local
  * vectors hold planes z_cell0*p .. (z_cell0 + nz_local)*p.  Per sweep the neighbours exchange,
  * forward: u (and f) on the p planes below the slab and the shared plane above; reverse: the
@@ -139,6 +140,13 @@ typedef struct {
   int32_t rev_send_lo[2], rev_recv_hi[2];   /* reverse-add: corrections to rank - 1 / from + 1  */
   uint32_t gamma_local;                  /* Gamma_D bits of the local problem (cut planes free)  */
   int64_t plane_len;                     /* doubles per DoF plane: (nx p + 1)(ny p + 1)          */
+  /* H(curl) / H(div): the ranges above hold for the components with a P family in z (planes
+   * z_cell0*p .. (z_cell0 + nz_local)*p); components with a DP family in z have nz_local*p local
+   * planes (plane c*p + a inside cell layer c, no shared plane) and use these instead.  A
+   * component's plane has len_x * len_y doubles (rm_layout shape). */
+  int32_t dp_own_lo, dp_own_hi;
+  int32_t dp_fwd_recv_lo[2], dp_fwd_send_hi[2];   /* ghost cell layer <- rank - 1; my top layer -> rank + 1 */
+  int32_t dp_rev_send_lo[2], dp_rev_recv_hi[2];   /* corrections on the ghost layer -> rank - 1 (added)   */
 } rm_partition_info;
 rm_status rm_partition(const rm_mesh *mesh, int32_t p, rm_space space, uint32_t gamma_d, int32_t rank,
                        int32_t nranks, rm_partition_info *info);

@@ -54,7 +54,10 @@ class rm_partition_info(ctypes.Structure):
                 ("own_hi", ctypes.c_int32), ("fwd_recv_lo", ctypes.c_int32 * 2), ("fwd_send_lo", ctypes.c_int32 * 2),
                 ("fwd_recv_hi", ctypes.c_int32 * 2), ("fwd_send_hi", ctypes.c_int32 * 2),
                 ("rev_send_lo", ctypes.c_int32 * 2), ("rev_recv_hi", ctypes.c_int32 * 2),
-                ("gamma_local", ctypes.c_uint32), ("plane_len", ctypes.c_int64)]
+                ("gamma_local", ctypes.c_uint32), ("plane_len", ctypes.c_int64),
+                ("dp_own_lo", ctypes.c_int32), ("dp_own_hi", ctypes.c_int32),
+                ("dp_fwd_recv_lo", ctypes.c_int32 * 2), ("dp_fwd_send_hi", ctypes.c_int32 * 2),
+                ("dp_rev_send_lo", ctypes.c_int32 * 2), ("dp_rev_recv_hi", ctypes.c_int32 * 2)]
 
     def as_dict(self):
         d = {}

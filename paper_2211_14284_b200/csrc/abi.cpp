@@ -86,7 +86,7 @@ const NcclApi& nccl() {
 void compute_partition(const rm_mesh& m, int p, int space, uint32_t gamma, int rank, int nranks,
                        rm_partition_info& P) {
   if (nranks < 1 || rank < 0 || rank >= nranks) throw RmError(RM_EINVAL, "bad rank / nranks");
-  if (nranks > 1 && space != 0) throw RmError(RM_EINVAL, "multi-rank slabs: H(grad) only");
+  (void)space;
   const int zb = m.z_begin, ze = m.z_end;
   if (!(0 <= zb && zb < ze && ze <= m.nz)) throw RmError(RM_EINVAL, "bad z_begin / z_end");
   if (nranks == 1 && (zb != 0 || ze != m.nz)) throw RmError(RM_EINVAL, "one rank must own all layers");
@@ -111,6 +111,17 @@ void compute_partition(const rm_mesh& m, int p, int space, uint32_t gamma, int r
     P.fwd_recv_hi[0] = top; P.fwd_recv_hi[1] = top + 1;  // shared upper plane, owned by rank + 1
     P.fwd_send_hi[0] = top - p; P.fwd_send_hi[1] = top;  // rank + 1's ghost layer
     P.rev_recv_hi[0] = top - p + 1; P.rev_recv_hi[1] = top;
+  }
+  // DP-family components (z index c p + a inside cell layer c): no shared plane
+  P.dp_own_lo = P.ghost_lo * p;
+  P.dp_own_hi = P.nz_local * p;
+  if (lo) {
+    P.dp_fwd_recv_lo[0] = 0; P.dp_fwd_recv_lo[1] = p;   // the ghost cell layer, owned by rank - 1
+    P.dp_rev_send_lo[0] = 0; P.dp_rev_send_lo[1] = p;   // corrections on the ghost layer
+  }
+  if (hi) {
+    P.dp_fwd_send_hi[0] = top - p; P.dp_fwd_send_hi[1] = top;   // my top layer = rank + 1's ghost layer
+    P.dp_rev_recv_hi[0] = top - p; P.dp_rev_recv_hi[1] = top;
   }
   P.gamma_local = gamma & 0x0Fu;
   if (!lo) P.gamma_local |= gamma & 0x10u;
@@ -810,13 +821,18 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     if (c->nranks > 1) {
       // global free count; buffers of the multi-rank sweep; the communicator (if an id is given)
       const uint32_t g = gamma_global;
-      const int64_t fx = (int64_t)c->n[0] * p + 1 - ((g >> 0) & 1) - ((g >> 1) & 1);
-      const int64_t fy = (int64_t)c->n[1] * p + 1 - ((g >> 2) & 1) - ((g >> 3) & 1);
-      const int64_t fz = (int64_t)nz_global * p + 1 - ((g >> 4) & 1) - ((g >> 5) & 1);
-      c->nfree = fx * fy * fz;
+      const int ng[3] = {c->n[0], c->n[1], nz_global};
+      c->nfree = 0;
+      for (int m = 0; m < c->sp.ncomp; ++m) {   // per direction: P family n p + 1 minus Dirichlet ends, DP n p
+        int64_t fm = 1;
+        for (int d = 0; d < 3; ++d)
+          fm *= c->sp.fam[m][d] == rm::FAM_P ? (int64_t)ng[d] * p + 1 - ((g >> (2 * d)) & 1) - ((g >> (2 * d + 1)) & 1)
+                                             : (int64_t)ng[d] * p;
+        c->nfree += fm;
+      }
       c->d_c = c->dalloc(c->ndof);
       // reverse-add receive buffer: p planes of the vector layout or of the padded (even-x) layout
-      c->d_rtmp = c->dalloc((size_t)p * ((int64_t)c->n[0] * p + 2) * ((int64_t)c->n[1] * p + 1));
+      c->d_rtmp = c->dalloc((size_t)3 * p * ((int64_t)c->n[0] * p + 2) * ((int64_t)c->n[1] * p + 1));
       if (o.nccl_id) {
         ncclUniqueId id;
         std::memcpy(&id, o.nccl_id, sizeof id);
@@ -1057,42 +1073,75 @@ void apply_cycle(rm_ctx* c, const double* r, double* z) {
 }
 
 // ------------------------------------------------------------------ multi-rank sweep pieces
-// Forward halo: planes fwd_recv_* of each vector <- the owners' planes (NCCL send/recv in ONE
+// Per component: offset, doubles per z plane, and whether its z family is DP (H(curl) / H(div)
+// components; rm.h: the dp_* ranges)
+struct CompPlanes { long long off, L; bool dp; };
+std::vector<CompPlanes> comp_planes(const rm_ctx* c) {
+  std::vector<CompPlanes> v;
+  for (int m = 0; m < c->sp.ncomp; ++m)
+    v.push_back({(long long)c->sp.offset(m), (long long)(c->sp.len(m, 0) * c->sp.len(m, 1)), c->sp.fam[m][2] == rm::FAM_D});
+  return v;
+}
+
+// Forward halo: the non-owned planes of each vector <- the owners' planes (NCCL send/recv in ONE
 // group on the stream, in place: the non-owned planes of the caller's input vectors are
-// overwritten, include/rm.h).  L = doubles per plane.
-void halo_forward(rm_ctx* c, double* const* vs, int nv, size_t L) {
+// overwritten, include/rm.h), component by component.
+void halo_forward(rm_ctx* c, double* const* vs, int nv) {
   const rm_partition_info& P = c->part;
   const NcclApi& N = nccl();
+  const std::vector<CompPlanes> cp = comp_planes(c);
   NK(N.gstart());
-  for (int i = 0; i < nv; ++i) {
-    double* v = vs[i];
-    if (c->rank > 0) {
-      NK(N.send(v + P.fwd_send_lo[0] * L, (P.fwd_send_lo[1] - P.fwd_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
-      NK(N.recv(v + P.fwd_recv_lo[0] * L, (P.fwd_recv_lo[1] - P.fwd_recv_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+  for (int i = 0; i < nv; ++i)
+    for (const CompPlanes& q : cp) {
+      double* v = vs[i] + q.off;
+      const size_t L = (size_t)q.L;
+      const int* rlo = q.dp ? P.dp_fwd_recv_lo : P.fwd_recv_lo;
+      const int* slo = q.dp ? nullptr : P.fwd_send_lo;
+      const int* rhi = q.dp ? nullptr : P.fwd_recv_hi;
+      const int* shi = q.dp ? P.dp_fwd_send_hi : P.fwd_send_hi;
+      if (c->rank > 0) {
+        if (slo && slo[1] > slo[0]) NK(N.send(v + slo[0] * L, (slo[1] - slo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+        if (rlo[1] > rlo[0]) NK(N.recv(v + rlo[0] * L, (rlo[1] - rlo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
+      }
+      if (c->rank < c->nranks - 1) {
+        if (shi[1] > shi[0]) NK(N.send(v + shi[0] * L, (shi[1] - shi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+        if (rhi && rhi[1] > rhi[0]) NK(N.recv(v + rhi[0] * L, (rhi[1] - rhi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
+      }
     }
-    if (c->rank < c->nranks - 1) {
-      NK(N.send(v + P.fwd_send_hi[0] * L, (P.fwd_send_hi[1] - P.fwd_send_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
-      NK(N.recv(v + P.fwd_recv_hi[0] * L, (P.fwd_recv_hi[1] - P.fwd_recv_hi[0]) * L, ncclDouble, c->rank + 1, c->comm, c->st));
-    }
+  NK(N.gend());
+}
+void halo_forward(rm_ctx* c, double* v) { halo_forward(c, &v, 1); }
+// Reverse-add: the corrections my patches put on rank - 1's planes go there and are added by it,
+// component by component (Lpad > 0: one component in the patch kernel's padded layout, plane
+// length Lpad).
+void reverse_add(rm_ctx* c, double* cv, size_t Lpad = 0) {
+  const rm_partition_info& P = c->part;
+  const NcclApi& N = nccl();
+  std::vector<CompPlanes> cp = comp_planes(c);
+  if (Lpad) cp = {{0, (long long)Lpad, false}};
+  std::vector<size_t> roff(cp.size() + 1, 0);
+  for (size_t i = 0; i < cp.size(); ++i) {
+    const int* r = cp[i].dp ? P.dp_rev_recv_hi : P.rev_recv_hi;
+    roff[i + 1] = roff[i] + (size_t)(r[1] - r[0]) * cp[i].L;
+  }
+  NK(N.gstart());
+  for (size_t i = 0; i < cp.size(); ++i) {
+    const CompPlanes& q = cp[i];
+    const int* sl = q.dp ? P.dp_rev_send_lo : P.rev_send_lo;
+    if (c->rank > 0 && sl[1] > sl[0])
+      NK(N.send(cv + q.off + sl[0] * q.L, (sl[1] - sl[0]) * q.L, ncclDouble, c->rank - 1, c->comm, c->st));
+    if (c->rank < c->nranks - 1 && roff[i + 1] > roff[i])
+      NK(N.recv(c->d_rtmp + roff[i], roff[i + 1] - roff[i], ncclDouble, c->rank + 1, c->comm, c->st));
   }
   NK(N.gend());
+  if (c->rank < c->nranks - 1)
+    for (size_t i = 0; i < cp.size(); ++i) {
+      const int* r = cp[i].dp ? P.dp_rev_recv_hi : P.rev_recv_hi;
+      if (roff[i + 1] > roff[i])
+        CK(rm::launch_axpby((long long)(roff[i + 1] - roff[i]), 1.0, c->d_rtmp + roff[i], 1.0, cv + cp[i].off + r[0] * cp[i].L,
+                            c->st));
+    }
 }
-void halo_forward(rm_ctx* c, double* v) { halo_forward(c, &v, 1, (size_t)c->part.plane_len); }
-// Reverse-add: the corrections my patches put on rank - 1's planes go there and are added by it
-// (L = doubles per plane: the vector layout, or the padded TMA layout of the patch kernel).
-void reverse_add(rm_ctx* c, double* cv, size_t L) {
-  const rm_partition_info& P = c->part;
-  const NcclApi& N = nccl();
-  const size_t nh = (size_t)(P.rev_recv_hi[1] - P.rev_recv_hi[0]) * L;
-  NK(N.gstart());
-  if (c->rank > 0)
-    NK(N.send(cv + P.rev_send_lo[0] * L, (P.rev_send_lo[1] - P.rev_send_lo[0]) * L, ncclDouble, c->rank - 1, c->comm, c->st));
-  if (c->rank < c->nranks - 1 && nh > 0) NK(N.recv(c->d_rtmp, nh, ncclDouble, c->rank + 1, c->comm, c->st));
-  NK(N.gend());
-  if (c->rank < c->nranks - 1 && nh > 0)
-    CK(rm::launch_axpby((long long)nh, 1.0, c->d_rtmp, 1.0, cv + P.rev_recv_hi[0] * L, c->st));
-}
-void reverse_add(rm_ctx* c, double* cv) { reverse_add(c, cv, (size_t)c->part.plane_len); }
 // In-place sum over ranks of device scalars.
 void allreduce_sum(rm_ctx* c, double* x, size_t n) {
   if (c->nranks > 1) NK(nccl().allreduce(x, x, n, ncclDouble, ncclSum, c->comm, c->st));
@@ -1141,7 +1190,7 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
     need_comm(c);
     {
       double* vs[2] = {const_cast<double*>(f), const_cast<double*>(u_in)};
-      halo_forward(c, vs, 2, (size_t)c->part.plane_len);   // f and u_in, in place, one NCCL group
+      halo_forward(c, vs, 2);   // f and u_in, in place, one NCCL group
     }
     if (fused_k0(c)) {
       // as on one rank: the residual straight into the padded TMA layout, corrections accumulated
@@ -1255,10 +1304,20 @@ rm_status rm_pcg(rm_ctx* c, const double* f, double* u, double rtol, int32_t max
     need_comm(c);
     // multi-rank: dots over the owned planes (a contiguous range) + allreduce; halo of the
     // search direction before each apply; reverse-add after each preconditioner application
-    const int64_t o0 = (int64_t)c->part.own_lo * c->part.plane_len;
-    const int64_t on = c->nranks > 1 ? (int64_t)(c->part.own_hi - c->part.own_lo) * c->part.plane_len : c->ndof;
+    // multi-rank: owned planes of every component (a contiguous range per component)
+    const std::vector<CompPlanes> cpl = comp_planes(c);
     auto dot = [&](const double* x, const double* y, double* out) {
-      CK(rm::launch_dot(on, x + (c->nranks > 1 ? o0 : 0), y + (c->nranks > 1 ? o0 : 0), c->d_part, out, c->st));
+      if (c->nranks == 1) {
+        CK(rm::launch_dot(c->ndof, x, y, c->d_part, out, c->st));
+        return;
+      }
+      for (size_t m = 0; m < cpl.size(); ++m) {
+        const CompPlanes& q = cpl[m];
+        const int lo = q.dp ? c->part.dp_own_lo : c->part.own_lo, hi = q.dp ? c->part.dp_own_hi : c->part.own_hi;
+        const long long o = q.off + (long long)lo * q.L, nn = (long long)(hi - lo) * q.L;
+        CK(rm::launch_dot(nn, x + o, y + o, c->d_part, m == 0 ? out : c->d_sc + 4, c->st));
+        if (m > 0) CK(rm::launch_axpby(1, 1.0, c->d_sc + 4, 1.0, out, c->st));
+      }
       allreduce_sum(c, out, 1);
     };
     auto precond = [&](const double* rr, double* zz) {

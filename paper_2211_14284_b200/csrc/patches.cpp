@@ -1189,8 +1189,9 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     }
     ents.swap(kept);
   }
-  if (in.zv_lo > 0 || in.zv_hi <= B.sp.n[2]) {   // z-slab ownership: vertex stars of the owned layers
-    if (in.dim != 0) throw std::runtime_error("z-slab patch ownership: vertex stars only");
+  if (in.zv_lo > 0 || in.zv_hi <= B.sp.n[2]) {
+    // z-slab ownership: the stars whose entity's z anchor (a vertex layer, or a cell layer for
+    // entities spanning a cell in z) lies in the owned layers [zv_lo, zv_hi)
     std::vector<Entity> kept;
     for (const Entity& e : ents)
       if (e.s[2].v >= in.zv_lo && e.s[2].v < in.zv_hi) kept.push_back(e);

@@ -23,6 +23,7 @@ def setup(w, **kw):
     coords = None if w.perturb == 0 else ri.vertex_coords(w)
     return rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(), w.gamma_d,
                         coords=coords, factorization=rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL,
+                        decomposition=rmb.RM_PH if w.decomposition == "ph" else rmb.RM_PAFW,
                         device=torch.cuda.current_device(), **kw)
 
 
@@ -33,7 +34,9 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     cases = [dataclasses.replace(ri.CONFIGS[1].with_mesh(3), nz=2 * world),
              dataclasses.replace(ri.CONFIGS[2].with_mesh(3).with_p(4), nz=2 * world),
-             dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), nz=2 * world)]
+             dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), nz=2 * world),
+             dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), nz=2 * world),
+             dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), nz=2 * world)]
     bad = 0
     for w in cases:
         g = setup(w)
@@ -48,28 +51,38 @@ def main():
         ref_x = torch.empty_like(ut)
         it_ref, _, _ = rmb.rm_pcg(g, ft, ref_x, 1e-8, 300)
         zb, ze = w.nz * rank // world, w.nz * (rank + 1) // world
-        P = rmb.rm_partition(w.nx, w.ny, w.nz, w.p, 0, w.gamma_d, rank, world, zb, ze)
+        P = rmb.rm_partition(w.nx, w.ny, w.nz, w.p, w.space, w.gamma_d, rank, world, zb, ze)
         nid = [rmb.rm_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(nid, src=0)
         ctx = setup(w, rank=rank, nranks=world, z_begin=zb, z_end=ze, nccl_id=nid[0])
         assert ctx.info()["comm_nranks"] == world
-        L = P["plane_len"]
-        g0 = P["z_cell0"] * w.p * L
-        own = slice(P["own_lo"] * L, P["own_hi"] * L)
-        loc = lambda t: t[g0:g0 + ctx.n_local].clone()   # noqa: E731  (halo planes overwritten in place)
+        from oracle.fem import P_FAM, Space
+        gsp, lsp = Space(w.space, w.p, w.nx, w.ny, w.nz), Space(w.space, w.p, w.nx, w.ny, P["nz_local"])
+        comps = []
+        for m in range(len(lsp.fams)):
+            Lz, Ly, Lx = lsp.comp_shape(m)
+            dp = lsp.fams[m][2] != P_FAM
+            comps.append((gsp.offsets()[m] + P["z_cell0"] * w.p * Ly * Lx, lsp.offsets()[m], Lz * Ly * Lx, Ly * Lx,
+                          P["dp_own_lo" if dp else "own_lo"], P["dp_own_hi" if dp else "own_hi"]))
+
+        def loc(t):   # the local planes of a global vector (halo planes overwritten in place by the call)
+            return torch.cat([t[g0:g0 + ln] for g0, l0, ln, Lm, lo, hi in comps]).clone()
+
+        def owned(t):
+            return torch.cat([t[l0 + lo * Lm:l0 + hi * Lm] for g0, l0, ln, Lm, lo, hi in comps])
         out = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
         res = {}
         rmb.rm_relax(ctx, loc(ft), loc(ut), out, 0.8)
-        res["relax"] = (out[own], loc(ref_relax)[own])
+        res["relax"] = (owned(out), owned(loc(ref_relax)))
         out2 = torch.empty_like(out)
         rmb.rm_apply(ctx, loc(ut), out2)
-        res["apply"] = (out2[own], loc(ref_apply)[own])
+        res["apply"] = (owned(out2), owned(loc(ref_apply)))
         out3 = torch.empty_like(out)
         rmb.rm_precondition(ctx, loc(ft), out3)
-        res["precondition"] = (out3[own], loc(ref_z)[own])
+        res["precondition"] = (owned(out3), owned(loc(ref_z)))
         x = torch.empty_like(out)
         it, _, _ = rmb.rm_pcg(ctx, loc(ft), x, 1e-8, 300)
-        res["pcg"] = (x[own], loc(ref_x)[own])
+        res["pcg"] = (owned(x), owned(loc(ref_x)))
         for k, (a, b) in res.items():
             e = float((a - b).abs().max() / b.abs().max())
             tol = 1e-12 if k != "pcg" else 1e-7

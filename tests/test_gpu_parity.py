@@ -301,6 +301,83 @@ def test_slab_partition_two_contexts(dev, name, w):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name,w", [("nce3-ph", dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), nz=4)),
+                                    ("ncf3-ph", dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), nz=4))])
+def test_slab_partition_two_contexts_hcurl_hdiv(dev, name, w):
+    """H(curl) / H(div) z-slabs on one device: per-component halo planes (P family in z: the
+    ranges of rm_partition, DP family: its dp_* ranges) moved by device copies between two
+    contexts; owned planes equal the single-context sweep."""
+    import torch
+    import paper_2211_14284_b200 as rmb
+    from oracle.fem import P_FAM, Space
+    G = 2
+    gctx = gu.setup_product(w)
+    n = gctx.n_local
+    mask = gctx.constrained_mask()
+    f = ri.uniform_vector(w.cfg, 0, n); f[mask] = 0
+    u = ri.uniform_vector(w.cfg, 3, n); u[mask] = 0
+    ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
+    ref = torch.empty_like(ut)
+    rmb.rm_relax(gctx, ft, ut, ref, 1.0)
+    gsp = Space(w.space, w.p, w.nx, w.ny, w.nz)
+    bounds = [w.nz * g // G for g in range(G + 1)]
+    parts, ctxs, views = [], [], []
+    for g in range(G):
+        P = rmb.rm_partition(w.nx, w.ny, w.nz, w.p, w.space, w.gamma_d, g, G, bounds[g], bounds[g + 1])
+        ctx = gu.setup_product(w, rank=g, nranks=G, z_begin=bounds[g], z_end=bounds[g + 1])
+        lsp = Space(w.space, w.p, w.nx, w.ny, P["nz_local"])
+        assert ctx.n_local == lsp.ndof
+        v = []
+        go, lo = gsp.offsets(), lsp.offsets()
+        for m in range(3):
+            Lz, Ly, Lx = lsp.comp_shape(m)
+            Lm = Ly * Lx
+            v.append((go[m] + P["z_cell0"] * w.p * Lm, lo[m], Lz * Lm, Lm, lsp.fams[m][2] != P_FAM))
+        parts.append(P); ctxs.append(ctx); views.append(v)
+    key = lambda dp, k: ("dp_" if dp else "") + k   # noqa: E731
+    fl, ul = [], []
+    for g in range(G):
+        a = torch.full((ctxs[g].n_local,), float("nan"), dtype=torch.float64, device=dev)
+        b = a.clone()
+        for g0, l0, ln, Lm, dp in views[g]:
+            lo_, hi_ = parts[g][key(dp, "own_lo")], parts[g][key(dp, "own_hi")]
+            a[l0 + lo_ * Lm:l0 + hi_ * Lm] = ft[g0 + lo_ * Lm:g0 + hi_ * Lm]
+            b[l0 + lo_ * Lm:l0 + hi_ * Lm] = ut[g0 + lo_ * Lm:g0 + hi_ * Lm]
+        fl.append(a); ul.append(b)
+    P0, P1 = parts
+    for vecs in (fl, ul):   # forward halos, per component
+        for m in range(3):
+            _, l00, _, Lm, dp = views[0][m]
+            _, l10, _, _, _ = views[1][m]
+            if dp:
+                s0, r1 = P0["dp_fwd_send_hi"], P1["dp_fwd_recv_lo"]
+                vecs[1][l10 + r1[0] * Lm:l10 + r1[1] * Lm] = vecs[0][l00 + s0[0] * Lm:l00 + s0[1] * Lm]
+            else:
+                s0, r1 = P0["fwd_send_hi"], P1["fwd_recv_lo"]
+                vecs[1][l10 + r1[0] * Lm:l10 + r1[1] * Lm] = vecs[0][l00 + s0[0] * Lm:l00 + s0[1] * Lm]
+                s1, r0 = P1["fwd_send_lo"], P0["fwd_recv_hi"]
+                vecs[0][l00 + r0[0] * Lm:l00 + r0[1] * Lm] = vecs[1][l10 + s1[0] * Lm:l10 + s1[1] * Lm]
+    assert all(torch.isfinite(t).all() for t in fl + ul)
+    cs = [torch.empty_like(t) for t in ul]
+    for g in range(G):
+        rmb.rm_relax_begin(ctxs[g], fl[g], ul[g], cs[g])
+    for m in range(3):   # reverse-add
+        _, l00, _, Lm, dp = views[0][m]
+        _, l10, _, _, _ = views[1][m]
+        sl, rh = P1[key(dp, "rev_send_lo")], P0[key(dp, "rev_recv_hi")]
+        cs[0][l00 + rh[0] * Lm:l00 + rh[1] * Lm] += cs[1][l10 + sl[0] * Lm:l10 + sl[1] * Lm]
+    for g in range(G):
+        uo = torch.empty_like(ul[g])
+        rmb.rm_relax_end(ctxs[g], ul[g], cs[g], uo, 1.0)
+        for g0, l0, ln, Lm, dp in views[g]:
+            lo_, hi_ = parts[g][key(dp, "own_lo")], parts[g][key(dp, "own_hi")]
+            got = uo[l0 + lo_ * Lm:l0 + hi_ * Lm].cpu().numpy()
+            want = ref[g0 + lo_ * Lm:g0 + hi_ * Lm].cpu().numpy()
+            err = np.abs(got - want).max() / max(1.0, np.abs(want).max())
+            check(f"slab two-context {name} rank {g} comp", err, 1e-12)
+
+
+@pytest.mark.gpu
 def test_nccl_transport_self_check(dev):
     """The NCCL entry points rm_relax uses with nranks > 1 (dlopen, unique id, communicator,
     grouped send/recv, allreduce on a stream), exercised on one device with a one-rank comm."""

@@ -64,13 +64,33 @@ def test_partition_plan_consistency(nz, G, p, gamma):
     assert sorted(owned_layers) == list(range(nz + 1))
 
 
+@pytest.mark.parametrize("nz,G,p", [(4, 2, 3), (9, 3, 4), (6, 6, 2)])
+def test_partition_plan_consistency_dp_components(nz, G, p):
+    """H(curl) / H(div) components with a DP family in z (nz p planes, plane c p + a in cell layer
+    c, no shared plane): forward / reverse ranges of neighbours coincide plane by plane, owned
+    planes partition the global ones."""
+    parts = [rmb.rm_partition(3, 2, nz, p, 1, 63, g, G, *_splits(nz, G)[g]) for g in range(G)]
+    gplane = lambda P, j: P["z_cell0"] * p + j   # noqa: E731
+    owned = []
+    for g, P in enumerate(parts):
+        owned += [gplane(P, j) for j in range(P["dp_own_lo"], P["dp_own_hi"])]
+        if g + 1 < G:
+            Q = parts[g + 1]
+            up = [gplane(P, j) for j in range(*P["dp_fwd_send_hi"])]
+            assert up == [gplane(Q, j) for j in range(*Q["dp_fwd_recv_lo"])] and len(up) == p
+            rev = [gplane(Q, j) for j in range(*Q["dp_rev_send_lo"])]
+            assert rev == [gplane(P, j) for j in range(*P["dp_rev_recv_hi"])] and len(rev) == p
+            assert all(pl in range(gplane(P, P["dp_own_lo"]), gplane(P, P["dp_own_hi"])) for pl in up + rev)
+        else:
+            assert P["dp_fwd_send_hi"] == (0, 0) and P["dp_rev_recv_hi"] == (0, 0)
+    assert sorted(owned) == list(range(nz * p))
+
+
 def test_partition_rejects_bad_ranges():
     with pytest.raises(rmb.RmError):
         rmb.rm_partition(2, 2, 4, 3, 0, 63, 1, 2, 0, 2)   # rank 1 must not start at 0... it may not end before nz
     with pytest.raises(rmb.RmError):
         rmb.rm_partition(2, 2, 4, 3, 0, 63, 0, 2, 1, 2)   # rank 0 must start at layer 0
-    with pytest.raises(rmb.RmError):
-        rmb.rm_partition(2, 2, 4, 3, 1, 63, 0, 2, 0, 2)   # H(curl): not partitioned
 
 
 # ------------------------------------------------------------------ distributed sweep over gloo
@@ -172,3 +192,157 @@ def test_slab_sweep_gloo_world2(case):
         for rank in range(2):
             got, ref = np.load(os.path.join(d, f"r{rank}.npy"))
             assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()), (case, rank)
+
+
+# ------------------------------------------------------- H(curl) / H(div) slabs (PH) over gloo
+PH_CASES = {
+    "nce3-ph": dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), nz=4),
+    "ncf3-ph": dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), nz=4),
+    "nce3-ph-neumann-top": dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), nz=4, gamma_d=0x1F),
+}
+
+
+def comp_views(gsp, lsp, z_cell0, p):
+    """Per component: (global slice of the local planes, local slice, plane length, DP-in-z flag)."""
+    from oracle.fem import P_FAM
+    out = []
+    go, lo = gsp.offsets(), lsp.offsets()
+    for m in range(len(lsp.fams)):
+        Lz, Ly, Lx = lsp.comp_shape(m)
+        Lm = Ly * Lx
+        g0 = go[m] + z_cell0 * p * Lm
+        out.append((slice(g0, g0 + Lz * Lm), slice(lo[m], lo[m] + Lz * Lm), Lm, lsp.fams[m][2] != P_FAM))
+    return out
+
+
+def _rank_main_ph(rank, world, port, case, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    import build_emu
+    from oracle.fem import Space, global_derivative
+    from oracle.solver import EPS_S, Problem
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = PH_CASES[case]
+    k, p, nx, ny, nz = w.space, w.p, w.nx, w.ny, w.nz
+    X = ri.vertex_coords(w)
+    al, be = ri.cell_alpha(w), ri.cell_beta(w)
+    gp = Problem(k, p, nx, ny, nz, X, al, be, w.gamma_d, decomposition="ph")
+    n = gp.space.ndof
+    f = ri.uniform_vector(w.cfg, 0, n); f[gp.constrained] = 0
+    u = ri.uniform_vector(w.cfg, 3, n); u[gp.constrained] = 0
+    zb, ze = _splits(nz, world)[rank]
+    P = rmb.rm_partition(nx, ny, nz, p, k, w.gamma_d, rank, world, zb, ze)
+    z0, nzl = P["z_cell0"], P["nz_local"]
+    lsp = Space(k, p, nx, ny, nzl)
+    views = comp_views(gp.space, lsp, z0, p)
+    nloc = lsp.ndof
+    rng = lambda dp, key: P[("dp_" if dp else "") + key]   # noqa: E731
+    fl = np.full(nloc, np.nan); ul = np.full(nloc, np.nan)
+    for gs, ls, Lm, dp in views:
+        lo, hi = rng(dp, "own_lo"), rng(dp, "own_hi")
+        own = slice(ls.start + lo * Lm, ls.start + hi * Lm)
+        fl[own] = f[gs][lo * Lm:hi * Lm]
+        ul[own] = u[gs][lo * Lm:hi * Lm]
+
+    def xfer(send, recv, peer):
+        reqs, bufs = [], []
+        for s_ in send:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(s_)), peer))
+        for nr in recv:
+            b = torch.empty(nr, dtype=torch.float64)
+            bufs.append(b)
+            reqs.append(dist.irecv(b, peer))
+        for r_ in reqs:
+            r_.wait()
+        return [b.numpy() for b in bufs]
+
+    def planes(vec, ls, Lm, rg):
+        return vec[ls.start + rg[0] * Lm:ls.start + rg[1] * Lm]
+
+    for vec in (fl, ul):   # forward halos, per component
+        for peer, sk, rk in ((rank - 1, "fwd_send_lo", "fwd_recv_lo"), (rank + 1, "fwd_send_hi", "fwd_recv_hi")):
+            if not 0 <= peer < world:
+                continue
+            sends, recvs, where = [], [], []
+            for gs, ls, Lm, dp in views:
+                sr = (0, 0) if (dp and sk == "fwd_send_lo") else rng(dp, sk)
+                rr = (0, 0) if (dp and rk == "fwd_recv_hi") else rng(dp, rk)
+                if sr[1] > sr[0]:
+                    sends.append(planes(vec, ls, Lm, sr))
+                if rr[1] > rr[0]:
+                    recvs.append((rr[1] - rr[0]) * Lm)
+                    where.append((ls, Lm, rr))
+            got = xfer(sends, recvs, peer)
+            for (ls, Lm, rr), b in zip(where, got):
+                vec[ls.start + rr[0] * Lm:ls.start + rr[1] * Lm] = b
+    assert np.isfinite(fl).all() and np.isfinite(ul).all(), "forward halo left planes unfilled"
+    Xl = X[z0:z0 + nzl + 1]
+    lp = Problem(k, p, nx, ny, nzl, Xl, al[z0:z0 + nzl], be[z0:z0 + nzl], P["gamma_local"], decomposition="ph")
+    r = lp.residual(fl, ul)
+    emu = ctypes.CDLL(build_emu.build())
+    Dp = ctypes.POINTER(ctypes.c_double)
+    dptr = lambda a: a.ctypes.data_as(Dp)   # noqa: E731
+    hz = np.ascontiguousarray(np.diff(Xl[:, 0, 0, 2]))
+    err = ctypes.create_string_buffer(256)
+
+    def family(kk, alpha, beta, rhs):
+        out = np.zeros_like(rhs)
+        a_, b_ = np.ascontiguousarray(alpha.ravel()), np.ascontiguousarray(beta.ravel())
+        rc = emu.emu_precondition_zv(kk, p, nx, ny, nzl, ctypes.c_uint(P["gamma_local"]), dptr(a_),
+                                     ctypes.c_longlong(a_.size), dptr(b_), ctypes.c_longlong(b_.size), None, kk, 0,
+                                     P["v_lo"], P["v_hi"], dptr(hz), dptr(np.ascontiguousarray(rhs)), dptr(out), err, 256)
+        assert rc == 0, err.value
+        return out
+
+    alc, bec = al[z0:z0 + nzl], be[z0:z0 + nzl]
+    c = family(k, alc, bec, r)                                  # owned k-star patches
+    D = global_derivative(k - 1, p, nx, ny, nzl)
+    pcon = Space(k - 1, p, nx, ny, nzl).constrained_mask(P["gamma_local"])
+    t = D.T @ r
+    t[pcon] = 0.0
+    s_ = family(k - 1, bec, (EPS_S if k == 2 else 0.0) * bec, t)   # owned potential patches
+    c += np.where(lp.constrained, 0.0, D @ s_)
+    # reverse-add of the corrections on the neighbour's planes, per component
+    for peer, sk, rk in ((rank - 1, "rev_send_lo", None), (rank + 1, None, "rev_recv_hi")):
+        if not 0 <= peer < world:
+            continue
+        sends, recvs, where = [], [], []
+        for gs, ls, Lm, dp in views:
+            if sk:
+                sr = rng(dp, sk)
+                if sr[1] > sr[0]:
+                    sends.append(planes(c, ls, Lm, sr))
+            if rk:
+                rr = rng(dp, rk)
+                if rr[1] > rr[0]:
+                    recvs.append((rr[1] - rr[0]) * Lm)
+                    where.append((ls, Lm, rr))
+        got = xfer(sends, recvs, peer)
+        for (ls, Lm, rr), b in zip(where, got):
+            c[ls.start + rr[0] * Lm:ls.start + rr[1] * Lm] += b
+    uo = ul + c
+    ref = gp.relax(f, u)
+    got_own, ref_own = [], []
+    for gs, ls, Lm, dp in views:
+        lo, hi = rng(dp, "own_lo"), rng(dp, "own_hi")
+        got_own.append(uo[ls.start + lo * Lm:ls.start + hi * Lm])
+        ref_own.append(ref[gs][lo * Lm:hi * Lm])
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), np.stack([np.concatenate(got_own), np.concatenate(ref_own)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", list(PH_CASES))
+def test_slab_sweep_ph_gloo_world2(case):
+    """H(curl) / H(div) PH sweep over a world-2 gloo partition: per-component forward halos (P and
+    DP families in z), owned k-star and potential patches (the product's host code), the potential
+    stage on the local mesh, per-component reverse-add; the owned planes equal the single-domain
+    oracle sweep."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_rank_main_ph, args=(2, _free_port(), case, d), nprocs=2, join=True)
+        for rank in range(2):
+            got, ref = np.load(os.path.join(d, f"r{rank}.npy"))
+            assert np.abs(got - ref).max() <= 1e-11 * max(1.0, np.abs(ref).max()), (case, rank, np.abs(got - ref).max())
