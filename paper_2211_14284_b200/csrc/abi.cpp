@@ -247,7 +247,9 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
   for (int sb = 0; sb < 3; ++sb) Lh.sub_comp[sb] = P.sub_comp[sb];
   if (!P.sc_nk.empty()) {
     Lh.sc_dinv = F.upload(P.sc_dinv);
-    Lh.sc_c = F.upload(P.sc_c);
+    Lh.sc_c = P.sc_c.empty() ? nullptr : F.upload(P.sc_c);
+    Lh.sc_w = P.sc_w.empty() ? nullptr : F.upload(P.sc_w);
+    for (size_t i = 0; i < 16 && i < P.sc_kd.size(); ++i) { Lh.sc_kd[i] = P.sc_kd[i]; Lh.sc_k0[i] = P.sc_k0[i]; Lh.sc_kp[i] = P.sc_kp[i]; }
     Lh.sc_nk = F.upload(P.sc_nk);
     Lh.sc_fb = F.upload(std::vector<double>(P.sc_nk.size() * 6 * (size_t)(P.sp.p - 1) * (P.sp.p - 1), 0.0));
     Lh.sc_p = P.sp.p;

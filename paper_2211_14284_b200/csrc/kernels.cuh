@@ -162,7 +162,9 @@ struct PatchLaunch {
   // static condensation of the cell interiors (ICC-SC, k = 0): per cell inverse interior
   // diagonal [ncell][(p-1)^3], face couplings [ncell][6][(p-1)^3], patches per cell
   const double* sc_dinv;
-  const double* sc_c;
+  const double* sc_c;    // [ncell][6][(p-1)^3] couplings, or null with sc_w (compressed, trilinear)
+  const double* sc_w;    // [ncell][3][(p-1)^3] interior stiffness weights: coupling = (kd w) k0|kp
+  double sc_kd[16], sc_k0[16], sc_kp[16];
   const int* sc_nk;
   double* sc_fb;         // per-cell face line sums of the pre step [ncell][6][(p-1)^2]
   int icc_only;          // every class ends in ICC (no dense tiles): the tile warps join the sparse warps

@@ -177,7 +177,7 @@ CellEntries cartesian_cell_entries(const CellOperator& op, const Space& sp, doub
 }
 
 // ------------------------------------------------------------------ auxiliary operator k=0
-void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out) {
+void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out, double* w_int) {
   const Basis1D& b = basis(p);
   const int n = p + 1;
   const int nq = (3 * (p + 1) + 1) / 2;   // reading G1/G2
@@ -266,6 +266,17 @@ void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, C
   std::vector<double> d0 = contract(W0, sb, n, sb, n, sb, n);
   std::vector<double> d1[3] = {contract(W1[0], r, p, sb, n, sb, n), contract(W1[1], sb, n, r, p, sb, n),
                                contract(W1[2], sb, n, sb, n, r, p)};
+  if (w_int) {
+    const int pm = p - 1, ni = pm * pm * pm;
+    for (int k = 1; k < p; ++k)
+      for (int j = 1; j < p; ++j)
+        for (int i = 1; i < p; ++i) {
+          const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
+          w_int[0 * ni + I] = d1[0][((size_t)k * n + j) * p + i];   // x: (z P, y P, x DP)
+          w_int[1 * ni + I] = d1[1][((size_t)k * p + j) * n + i];   // y: (z P, y DP, x P)
+          w_int[2 * ni + I] = d1[2][((size_t)k * n + j) * n + i];   // z: (z DP, y P, x P)
+        }
+  }
   // sparse rows of G (n x n) and D-hat (p x n), structural pattern only
   std::vector<std::vector<std::pair<int, double>>> Gr(n), Dr(p);
   for (int i = 0; i < n; ++i)

@@ -76,6 +76,10 @@ CellEntries cartesian_cell_entries(const CellOperator& op, const Space& sp, doub
 
 // Auxiliary operator P_K for k = 0 on a trilinear cell (eq:sum-factorization_approx P:732-739):
 // returns entries on the structural pattern (row, col, val) with alpha, beta folded in.
-void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out);
+// w_int (optional, 3 (p-1)^3 doubles): the interior values of the three stiffness diagonals,
+// w_int[m][(k-1, j-1, i-1)] = diag(M-bar^1_alpha)_m at the DP index of direction m equal to the
+// interior index: every interior-to-face coupling of P_K is (D_ii w) D_i{0,p} (one term).
+void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out,
+                      double* w_int = nullptr);
 
 }  // namespace rm

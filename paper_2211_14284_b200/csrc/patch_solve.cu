@@ -742,7 +742,21 @@ __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const dou
 // ---- static condensation of the cell interiors (ICC-SC families, k = 0), on the padded layout
 // pre:  rp[f] -= sum over the 2 cells K at face DoF f, sum_i c_K(f, I) dinv_K(I) rp[I]   (one thread per face DoF)
 // post: cp[I] = n_K dinv_K(I) rp[I] - dinv_K(I) sum_faces c_K(f, I) cp[f]               (one thread per interior DoF)
-struct ScGeom { int p, n[3]; long long lxp, ly; };
+struct ScGeom {
+  int p, n[3];
+  long long lxp, ly;
+  int cmp;                          // couplings from the interior stiffness weights (sc_w)
+  double kd[16], k0[16], kp[16];    // D_ii, D_i0, D_ip
+};
+
+// coupling of interior DoF I (interior index iline along the face normal) to face f of its cell:
+// stored, or rebuilt as (D_ii w) D_i{0,p} -- bitwise the assembled value (patches.cpp checks it)
+__device__ __forceinline__ double sc_coup(const ScGeom& G, const double* __restrict__ cc, const double* __restrict__ cw,
+                                          long long K, int f, int I, int ni, int iline) {
+  if (!G.cmp) return cc[(K * 6 + f) * ni + I];
+  const double w = cw[(K * 3 + (f >> 1)) * ni + I];
+  return __dmul_rn(__dmul_rn(G.kd[iline], w), (f & 1) ? G.kp[iline] : G.k0[iline]);
+}
 
 __device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long long y, long long z) {
   return (z * G.ly + y) * G.lxp + x;
@@ -752,8 +766,8 @@ __device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long l
 // line sums e_f(j, k) = sum_i (P_GI)_{f, I(i, j, k)} y_I into the per-cell face buffer fb.
 // Every global array is read contiguously (couplings per (K, f) are stored I-contiguous).
 __global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
-                               const double* __restrict__ cc, const double* __restrict__ rp,
-                               double* __restrict__ fb) {
+                               const double* __restrict__ cc, const double* __restrict__ cw,
+                               const double* __restrict__ rp, double* __restrict__ fb) {
   extern __shared__ double scs[];
   const int p = G.p, pm = p - 1, ni = pm * pm * pm, nf = pm * pm;
   double* y = scs;          // [k][j][i]
@@ -769,11 +783,18 @@ __global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* _
   for (int q = threadIdx.x; q < 6 * nf; q += blockDim.x) {
     const int f = q / nf, pos = q - f * nf, dir = f >> 1;
     const int a = pos % pm, b = pos / pm;
-    const double* cf = cc + ((size_t)K * 6 + f) * ni;
     const int I0 = dir == 0 ? (b * pm + a) * pm : (dir == 1 ? b * pm * pm + a : b * pm + a);
     const int st = dir == 0 ? 1 : (dir == 1 ? pm : nf);
     double e = 0.0;
-    for (int l = 0; l < pm; ++l) e = fma(cf[I0 + l * st], y[I0 + l * st], e);
+    if (G.cmp) {   // the line runs along the face normal: interior index l + 1 of the 1D tables
+      const double* wf = cw + ((size_t)K * 3 + dir) * ni;
+      const double* kf = (f & 1) ? G.kp : G.k0;
+      for (int l = 0; l < pm; ++l)
+        e = fma(__dmul_rn(__dmul_rn(G.kd[l + 1], wf[I0 + l * st]), kf[l + 1]), y[I0 + l * st], e);
+    } else {
+      const double* cf = cc + ((size_t)K * 6 + f) * ni;
+      for (int l = 0; l < pm; ++l) e = fma(cf[I0 + l * st], y[I0 + l * st], e);
+    }
     fb[((size_t)K * 6 + f) * nf + pos] = e;
   }
 }
@@ -814,7 +835,7 @@ __global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* _
 }
 
 __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
-                               const double* __restrict__ cc, const int* __restrict__ nk,
+                               const double* __restrict__ cc, const double* __restrict__ cw, const int* __restrict__ nk,
                                const double* __restrict__ rp, double* __restrict__ cp, long long nint) {
   // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
@@ -826,12 +847,12 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   (void)nint;
   const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
   const double dv = dinv[K * ni + I];
-  double s = cc[(K * 6 + 0) * ni + I] * cp[sc_idx(G, x, y + j, z + k)];
-  s = fma(cc[(K * 6 + 1) * ni + I], cp[sc_idx(G, x + p, y + j, z + k)], s);
-  s = fma(cc[(K * 6 + 2) * ni + I], cp[sc_idx(G, x + i, y, z + k)], s);
-  s = fma(cc[(K * 6 + 3) * ni + I], cp[sc_idx(G, x + i, y + p, z + k)], s);
-  s = fma(cc[(K * 6 + 4) * ni + I], cp[sc_idx(G, x + i, y + j, z)], s);
-  s = fma(cc[(K * 6 + 5) * ni + I], cp[sc_idx(G, x + i, y + j, z + p)], s);
+  double s = sc_coup(G, cc, cw, K, 0, I, ni, i) * cp[sc_idx(G, x, y + j, z + k)];
+  s = fma(sc_coup(G, cc, cw, K, 1, I, ni, i), cp[sc_idx(G, x + p, y + j, z + k)], s);
+  s = fma(sc_coup(G, cc, cw, K, 2, I, ni, j), cp[sc_idx(G, x + i, y, z + k)], s);
+  s = fma(sc_coup(G, cc, cw, K, 3, I, ni, j), cp[sc_idx(G, x + i, y + p, z + k)], s);
+  s = fma(sc_coup(G, cc, cw, K, 4, I, ni, k), cp[sc_idx(G, x + i, y + j, z)], s);
+  s = fma(sc_coup(G, cc, cw, K, 5, I, ni, k), cp[sc_idx(G, x + i, y + j, z + p)], s);
   const long long gi = sc_idx(G, x + i, y + j, z + k);
   cp[gi] = dv * (nk[K] * rp[gi] - s);
 }
@@ -941,6 +962,8 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     for (int d = 0; d < 3; ++d) sg.n[d] = L.sc_n[d];
     sg.lxp = L.pad.lxp[0];
     sg.ly = L.pad.len[0][1];
+    sg.cmp = L.sc_w ? 1 : 0;
+    for (int a = 0; a < 16; ++a) { sg.kd[a] = L.sc_kd[a]; sg.k0[a] = L.sc_k0[a]; sg.kp[a] = L.sc_kp[a]; }
     const long long pm = L.sc_p - 1;
     nface = ((long long)(sg.n[0] + 1) * sg.n[1] * sg.n[2] + (long long)(sg.n[1] + 1) * sg.n[0] * sg.n[2] +
              (long long)(sg.n[2] + 1) * sg.n[0] * sg.n[1]) * pm * pm;
@@ -954,7 +977,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
           return e;
         smem_set = smem;
       }
-      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.rpad, L.sc_fb);
+      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       sc_face_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_fb, L.rpad, (int)nface);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1010,7 +1033,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
     const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
-    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_nk, L.rpad, L.cpad, nint);
+    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n);

@@ -1367,7 +1367,17 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     const int p = sp.p, P1 = p + 1, pm = p - 1, ni = pm * pm * pm;
     const int64_t ncell = (int64_t)sp.n[0] * sp.n[1] * sp.n[2];
     fam->sc_dinv.assign((size_t)ncell * ni, 0.0);
-    fam->sc_c.assign((size_t)ncell * 6 * ni, 0.0);
+    const bool cmp = !in.cartesian;   // trilinear auxiliary operator: compressed couplings
+    if (cmp) {
+      fam->sc_w.assign((size_t)ncell * 3 * ni, 0.0);
+      const Basis1D& b1 = basis(p);
+      fam->sc_kd.assign(P1, 0.0); fam->sc_k0.assign(P1, 0.0); fam->sc_kp.assign(P1, 0.0);
+      for (int i = 1; i < p; ++i) {
+        fam->sc_kd[i] = b1.D[i * P1 + i]; fam->sc_k0[i] = b1.D[i * P1]; fam->sc_kp[i] = b1.D[i * P1 + p];
+      }
+    } else {
+      fam->sc_c.assign((size_t)ncell * 6 * ni, 0.0);
+    }
     fam->sc_nk.assign(ncell, 0);
     std::string sc_err;
 #pragma omp parallel for schedule(dynamic, 8)
@@ -1386,7 +1396,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
               const int64_t vi = (((int64_t)(cz + az) * (sp.n[1] + 1) + (cy + ay)) * (sp.n[0] + 1) + (cx + ax)) * 3;
               for (int i = 0; i < 3; ++i) Xc[az * 4 + ay * 2 + ax][i] = in.coords[vi + i];
             }
-        aux_cell_entries(p, Xc, a, b, ce);
+        aux_cell_entries(p, Xc, a, b, ce, cmp ? &fam->sc_w[(size_t)K * 3 * ni] : nullptr);
         E = &ce;
       }
       std::vector<int> nc(ni, 0);
@@ -1409,7 +1419,17 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
           }
           continue;
         }
-        fam->sc_c[((size_t)K * 6 + face) * ni + I] += v;
+        if (cmp) {   // the compressed form must reproduce the assembled coupling exactly
+          const int iline = face < 2 ? ra : (face < 4 ? rb : rc);
+          const double w = fam->sc_w[((size_t)K * 3 + face / 2) * ni + I];
+          const double rec = (fam->sc_kd[iline] * w) * ((face & 1) ? fam->sc_kp[iline] : fam->sc_k0[iline]);
+          if (rec != v) {
+#pragma omp critical
+            sc_err = "static condensation: compressed coupling differs from the assembled one";
+          }
+        } else {
+          fam->sc_c[((size_t)K * 6 + face) * ni + I] += v;
+        }
         ++nc[I];
       }
       for (int I = 0; I < ni; ++I) {

@@ -177,6 +177,16 @@ struct PatchFamily {
   // number of patches containing the cell
   std::vector<double> sc_dinv, sc_c;
   std::vector<int> sc_nk;
+  // compressed couplings (trilinear auxiliary operator): per cell the three interior stiffness
+  // weights w[K][m][I] (sc_c empty); coupling to face 2m (+1) = (D_ii w) D_i0 (D_ip), i the
+  // interior index along m -- bitwise the assembled value (model.hpp aux_cell_entries)
+  std::vector<double> sc_w;
+  std::vector<double> sc_kd, sc_k0, sc_kp;   // D_ii, D_i0, D_ip (i = 0..p)
+  double sc_coupling(int64_t K, int f, int I, int ni, int iline) const {
+    if (sc_w.empty()) return sc_c[((size_t)K * 6 + f) * ni + I];
+    const double w = sc_w[((size_t)K * 3 + f / 2) * ni + I];
+    return (sc_kd[iline] * w) * ((f & 1) ? sc_kp[iline] : sc_k0[iline]);
+  }
   bool sc_pre = false;            // the static-condensation PRE step runs outside the patch kernel (sc programs)
   int box_total = 0;
   double sigma_max = 0.0;         // largest ICC restart shift used (reading G7)

@@ -83,7 +83,7 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
               for (int i = 1; i < p; ++i) {
                 const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
                 const double y = r_in[cell_dof(cx, cy, cz, i, j, k)] * F.sc_dinv[(size_t)K * ni + I];
-                for (int f = 0; f < 6; ++f) rsc[face_dof(cx, cy, cz, f, i, j, k)] -= F.sc_c[((size_t)K * 6 + f) * ni + I] * y;
+                for (int f = 0; f < 6; ++f) rsc[face_dof(cx, cy, cz, f, i, j, k)] -= F.sc_coupling(K, f, I, ni, f < 2 ? i : (f < 4 ? j : k)) * y;
               }
         }
   const double* r = rsc.data();
@@ -238,7 +238,7 @@ static void emulate_family(const PatchFamily& F, const double* r_in, double* z_o
                 const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
                 const double dinv = F.sc_dinv[(size_t)K * ni + I];
                 double s = 0.0;
-                for (int f = 0; f < 6; ++f) s += F.sc_c[((size_t)K * 6 + f) * ni + I] * cacc[face_dof(cx, cy, cz, f, i, j, k)];
+                for (int f = 0; f < 6; ++f) s += F.sc_coupling(K, f, I, ni, f < 2 ? i : (f < 4 ? j : k)) * cacc[face_dof(cx, cy, cz, f, i, j, k)];
                 cacc[cell_dof(cx, cy, cz, i, j, k)] = F.sc_nk[K] * r_in[cell_dof(cx, cy, cz, i, j, k)] * dinv - dinv * s;
               }
         }
@@ -340,7 +340,7 @@ int emu_sc_pre(int p, int nx, int ny, int nz, unsigned gamma, const double* alph
               const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
               const double y = r[cd(cx, cy, cz, i, j, k)] * F->sc_dinv[(size_t)K * ni + I];
               const int fa[6][3] = {{0, j, k}, {p, j, k}, {i, 0, k}, {i, p, k}, {i, j, 0}, {i, j, p}};
-              for (int f = 0; f < 6; ++f) rsc[cd(cx, cy, cz, fa[f][0], fa[f][1], fa[f][2])] -= F->sc_c[((size_t)K * 6 + f) * ni + I] * y;
+              for (int f = 0; f < 6; ++f) rsc[cd(cx, cy, cz, fa[f][0], fa[f][1], fa[f][2])] -= F->sc_coupling(K, f, I, ni, f < 2 ? i : (f < 4 ? j : k)) * y;
             }
       }
   return 0;
