@@ -722,16 +722,22 @@ __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __
 }
 
 __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* __restrict__ u,
-                                  double omega, long long n) {
-  // one (y, z) row of one component per warp, grid-stride: no per-element 64-bit division
+                                  double omega, long long n, int skip_p) {
+  // one (y, z) row of one component per warp, grid-stride: no per-element 64-bit division;
+  // skip_p > 0 (one component, static condensation with the post step writing u): the cell
+  // interiors are already done, only the skeleton entries (an index at a multiple of p) remain
   const int lane = threadIdx.x & 31;
   const int wstride = gridDim.x * (blockDim.x >> 5);
   int rows_before = 0;
   for (int m = 0; m < P.ncomp; ++m) {
-    const int Lx = (int)P.len[m][0], nrow = (int)(P.len[m][1] * P.len[m][2]);
+    const int Lx = (int)P.len[m][0], Ly = (int)P.len[m][1], nrow = (int)(P.len[m][1] * P.len[m][2]);
     for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) - rows_before; r < nrow; r += wstride) {
       if (r < 0) continue;
       const long long ub = P.off[m] + (long long)r * Lx, cb = P.poff[m] + (long long)r * P.lxp[m];
+      if (skip_p > 0 && (r % Ly) % skip_p != 0 && (r / Ly) % skip_p != 0) {   // interior row: x skeleton only
+        for (int x = lane * skip_p; x < Lx; x += 32 * skip_p) u[ub + x] += omega * cp[cb + x];
+        continue;
+      }
       for (int x = lane; x < Lx; x += 32) u[ub + x] += omega * cp[cb + x];
     }
     rows_before += nrow;
@@ -836,7 +842,8 @@ __global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* _
 
 __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
                                const double* __restrict__ cc, const double* __restrict__ cw, const int* __restrict__ nk,
-                               const double* __restrict__ rp, double* __restrict__ cp, long long nint) {
+                               const double* __restrict__ rp, double* __restrict__ cp, long long nint,
+                               double* __restrict__ u, double omega, long long lx) {
   // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
@@ -854,7 +861,9 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   s = fma(sc_coup(G, cc, cw, K, 4, I, ni, k), cp[sc_idx(G, x + i, y + j, z)], s);
   s = fma(sc_coup(G, cc, cw, K, 5, I, ni, k), cp[sc_idx(G, x + i, y + j, z + p)], s);
   const long long gi = sc_idx(G, x + i, y + j, z + k);
-  cp[gi] = dv * (nk[K] * rp[gi] - s);
+  const double c = dv * (nk[K] * rp[gi] - s);
+  if (u) u[((z + k) * G.ly + y + j) * lx + x + i] += omega * c;   // fused combine (one rank): u directly
+  else cp[gi] = c;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -936,7 +945,7 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
 }
 
 cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st) {
-  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp]);
+  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0);
   return cudaGetLastError();
 }
 
@@ -946,7 +955,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     if (!L.cpad) return cudaSuccess;
     if (!r_padded) pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
     if (zero_c) cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st);
-    if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp]);
+    if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0);
     return cudaGetLastError();
   }
   const long long n = L.pad.off[L.pad.ncomp];
@@ -1033,10 +1042,18 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
     const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
-    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint);
+    // with the combine in this launch the post step adds omega c_I to u itself and the combine
+    // skips the cell interiors (one fewer pass over them); otherwise c_I goes to cpad (multi-rank:
+    // the ghost layer's interiors are reverse-added before the combine)
+    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint, combine ? u : nullptr,
+                                       omega, L.pad.len[0][0]);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (combine) {
+      unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, L.sc_p);
+      return cudaGetLastError();
+    }
   }
-  if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n);
+  if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, 0);
   return cudaGetLastError();
 }
 
