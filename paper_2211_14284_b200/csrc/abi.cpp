@@ -714,6 +714,48 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       tabs.insert(tabs.end(), dsv.begin(), dsv.end());
       tabs.insert(tabs.end(), xq.begin(), xq.end());
       tabs.insert(tabs.end(), wq.begin(), wq.end());
+      // even / odd tables of the x contractions (TriParams): needs mirror point pairs (nq even)
+      // and definite parity of every interior FDM basis function at the quadrature points
+      c->tri.eo = 0;
+      if (nq % 2 == 0) {
+        const int P1 = p + 1, ne = nq / 2;
+        std::vector<int> ev, od;
+        bool ok = true;
+        for (int j = 1; j < p && ok; ++j) {
+          double se = 0, so = 0, mx = 0;
+          for (int q = 0; q < nq; ++q) {
+            const double a = sv[q * P1 + j], b = sv[(nq - 1 - q) * P1 + j];
+            se = std::max(se, std::fabs(a - b)); so = std::max(so, std::fabs(a + b)); mx = std::max(mx, std::fabs(a));
+          }
+          if (se <= 1e-12 * mx) ev.push_back(j);
+          else if (so <= 1e-12 * mx) od.push_back(j);
+          else ok = false;
+        }
+        if (ok && ev.size() <= 7 && od.size() <= 7) {
+          for (int k = 0; k < 16; ++k) c->tri.xsig[k] = -1;
+          c->tri.xsig[0] = 0; c->tri.xsig[8] = p;   // E_0 / O_0 (the vertex pair, butterflied)
+          for (size_t i = 0; i < ev.size(); ++i) c->tri.xsig[1 + i] = ev[i];
+          for (size_t i = 0; i < od.size(); ++i) c->tri.xsig[9 + i] = od[i];
+          std::vector<double> T(4 * 12 * 8, 0.0);   // S_E, S_O, D_E, D_O [r][e]
+          for (int r = 0; r < ne; ++r)
+            for (int e = 0; e < 8; ++e) {
+              const int je = c->tri.xsig[e], jo = c->tri.xsig[8 + e];
+              double sE = 0, sO = 0, dE = 0, dO = 0;
+              if (e == 0) {
+                sE = sv[r * P1] + sv[r * P1 + p]; dE = dsv[r * P1] + dsv[r * P1 + p];
+                sO = sv[r * P1] - sv[r * P1 + p]; dO = dsv[r * P1] - dsv[r * P1 + p];
+              } else {
+                if (je >= 0) { sE = sv[r * P1 + je]; dE = dsv[r * P1 + je]; }
+                if (jo >= 0) { sO = sv[r * P1 + jo]; dO = dsv[r * P1 + jo]; }
+              }
+              T[0 * 96 + r * 8 + e] = sE; T[1 * 96 + r * 8 + e] = sO;
+              T[2 * 96 + r * 8 + e] = dE; T[3 * 96 + r * 8 + e] = dO;
+            }
+          tabs.insert(tabs.end(), T.begin(), T.end());
+          c->tri.eo = 1;
+          c->tri.ne = ne;
+        }
+      }
       c->d_tabs = c->dalloc(tabs.size());
       CK(cudaMemcpy(c->d_tabs, tabs.data(), tabs.size() * 8, cudaMemcpyHostToDevice));
       const size_t nv = (size_t)(c->n[0] + 1) * (c->n[1] + 1) * (c->n[2] + 1) * 3;

@@ -43,7 +43,11 @@ constexpr int XS_Q = 18, SZ_Q = K1 * XS_Q; // Q1/Q2 plane [x][y] (fragment store
 constexpr int O_SG = 0, O_DG = O_SG + NQP * K1, O_XQ = O_DG + NQP * K1, O_WQ = O_XQ + NQP, O_GC = O_WQ + NQP,
               O_FA = O_GC + 24, O_FT = O_FA + 2 * 3 * 4 * 32, O_U = O_FT + 2 * 6 * 2 * 32, O_OUT = O_U + 4096,
               O_AZ = O_OUT + 4096, O_WR = O_AZ + ZB * 2 * 256, O_P = O_WR + TRI_WARPS * WR_SIZE,
-              O_VX = O_P + ZB * 3 * SZ_P, O_END = O_VX + 28;
+              O_VX = O_P + ZB * 3 * SZ_P, O_FX = O_VX + 28, O_FB = O_FX + 2 * 2 * 2 * 2 * 32,
+              O_END = O_FB + 2 * 2 * 3 * 32;
+// even / odd x path (TriParams::eo): forward-x B fragments [S/D][E/O][n tile][k][lane] of the 12 x 8
+// tables, backward-x B fragments [S/D][E/O][k][lane]; pointwise output rows [8 combos][8][XE]
+constexpr int XE = 12;
 constexpr size_t TRI_SMEM = sizeof(double) * O_END;
 static_assert(ZB * 2 * SZ_Q <= TRI_WARPS * WR_SIZE, "Q aliases the warp regions");
 static_assert(TRI_SMEM <= 232448, "shared memory");
@@ -81,6 +85,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 }  // namespace
 
+template <bool EO>
 __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_constant__ TriParams tp,
                                                                     const double* __restrict__ tabs,
                                                                     const double* __restrict__ X,
@@ -154,6 +159,23 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
   }
   auto fa = [&](int f, int m, int k) { return FA[((f * 3 + m) * 4 + k) * 32 + lane]; };
   auto ft = [&](int f, int k, int n) { return FT[((f * 6 + k) * 2 + n) * 32 + lane]; };
+  double* FX = sm + O_FX;
+  double* FB = sm + O_FB;
+  if (EO) {
+    const double* T4 = tabs + 2 * NQ * P1 + 2 * NQ;   // S_E, S_O, D_E, D_O [r][e], 12 x 8 each
+    for (int i = t; i < 2 * 2 * 2 * 2 * 32; i += TRI_THREADS) {   // forward x: B[e = 4k + l%4][r = 8nt + l/4]
+      const int f = i >> 8, eo = (i >> 7) & 1, nt = (i >> 6) & 1, k = (i >> 5) & 1, l = i & 31;
+      const int r = 8 * nt + (l >> 2), e = 4 * k + (l & 3);
+      FX[i] = r < tp.ne ? T4[(2 * f + eo) * 96 + r * 8 + e] : 0.0;
+    }
+    for (int i = t; i < 2 * 2 * 3 * 32; i += TRI_THREADS) {       // backward x: B[r = 4k + l%4][e = l/4]
+      const int f = i / 192, eo = (i / 96) & 1, k = (i >> 5) % 3, l = i & 31;
+      const int r = 4 * k + (l & 3), e = l >> 2;
+      FB[i] = r < tp.ne ? T4[(2 * f + eo) * 96 + r * 8 + e] : 0.0;
+    }
+  }
+  auto fx = [&](int f, int eo, int nt, int k) { return FX[(((f * 2 + eo) * 2 + nt) * 2 + k) * 32 + lane]; };
+  auto fb = [&](int f, int eo, int k) { return FB[((f * 2 + eo) * 3 + k) * 32 + lane]; };
   const int ly = t & 15, lx = t >> 4;   // per-thread line (x, y), y fastest (threads < 256)
   const bool zline = t < K1 * K1;
   const int nb = (NQ + ZB - 1) / ZB;
@@ -204,6 +226,32 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
   for (long long cell = blockIdx.x; cell < ncell; cell += gridDim.x) {
   cp_async_wait_all();
   __syncthreads();   // U, VX of this cell landed; OUT zeroed
+  if (EO) {   // x coefficients to the even / odd basis: u'_E0 = (u_0 + u_p)/2, u'_O0 = (u_0 - u_p)/2, permuted
+    if (t < 256) {
+      const int z = t >> 4, y = t & 15;
+      double r[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x) r[x] = U[z * 256 + swu(x, y)];
+      double rp = 0.0;   // r[p] without a dynamically indexed (local-memory) register array
+#pragma unroll
+      for (int x = 0; x < 16; ++x) rp = (x == p) ? r[x] : rp;
+#pragma unroll
+      for (int pos = 0; pos < 16; ++pos) {
+        const int j = tp.xsig[pos];
+        double v = 0.0;
+        if (pos == 0) {
+          v = 0.5 * (r[0] + rp);
+        } else if (pos == 8) {
+          v = 0.5 * (r[0] - rp);
+        } else {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) v = (x == j) ? r[x] : v;
+        }
+        U[z * 256 + swu(pos, y)] = v;
+      }
+    }
+    __syncthreads();
+  }
   if (t < 24) {
     // x(xi, eta, zeta) = sum_a X_a prod_d (1 + s_ad xi_d) / 2 = sum_m GC[m] mono_m,
     // monomials m: 1, xi, eta, zeta, xi eta, xi zeta, eta zeta, xi eta zeta
@@ -251,6 +299,130 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
       }
     }
     __syncwarp();
+    if constexpr (EO) {
+    // ----- even / odd x (TriParams::eo): per product the even part P_E = T_E a_E and the odd part
+    // P_O = T_O a_O (K = 8, N = 12 point pairs); left / right points: values P_E +- P_O,
+    // x-derivatives +-P_E + P_O (E' odd, O' even)
+    double vE[4][2][2] = {}, vO[4][2][2] = {};   // [u, d_xi, d_eta, d_zeta][n tile][e]
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {   // even coefficients: k steps 0, 1; odd: k steps 2, 3
+      const double* ae = WRg + l4 * XS_AS + ((4 * kk + lm) ^ h_as(l4));
+      const double* ao = WRg + l4 * XS_AS + ((4 * (kk + 2) + lm) ^ h_as(l4));
+      const double eS = ae[0], eD = ae[SZ_ASF], eB = ae[2 * SZ_ASF];
+      const double oS = ao[0], oD = ao[SZ_ASF], oB = ao[2 * SZ_ASF];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const double bSe = fx(0, 0, nt, kk), bDe = fx(1, 0, nt, kk), bSo = fx(0, 1, nt, kk), bDo = fx(1, 1, nt, kk);
+        dmma(vE[0][nt], eS, bSe);
+        dmma(vE[1][nt], eS, bDe);
+        dmma(vE[2][nt], eD, bSe);
+        dmma(vE[3][nt], eB, bSe);
+        dmma(vO[0][nt], oS, bSo);
+        dmma(vO[1][nt], oS, bDo);
+        dmma(vO[2][nt], oD, bSo);
+        dmma(vO[3][nt], oB, bSo);
+      }
+    }
+    __syncwarp();   // AS rows consumed: the region now takes the pointwise combinations
+    {   // pointwise at (zq, yq, x_r) and (zq, yq, -x_r); stores T+-, HX+-, HY+-, HZ+- [combo][row][r]
+      const int yq = 8 * wmt + l4;
+      const double ze = XQ[zq], et = XQ[yq];
+      const double wzy = WQ[zq] * WQ[yq];
+      double Jx[3], Jya[3], Jyb[3], Jza[3], Jzb[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double g1 = GC[3 + i], g2 = GC[6 + i], g3 = GC[9 + i], g4 = GC[12 + i], g5 = GC[15 + i], g6 = GC[18 + i],
+                     g7 = GC[21 + i];
+        Jx[i] = fma(fma(g7, ze, g4), et, fma(g5, ze, g1));
+        Jya[i] = fma(g6, ze, g2);
+        Jyb[i] = fma(g7, ze, g4);
+        Jza[i] = fma(g6, et, g3);
+        Jzb[i] = fma(g7, et, g5);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * nt + 2 * lm + e;
+          if (r >= XE) continue;
+          double out8[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // T+, T-, HX+, HX-, HY+, HY-, HZ+, HZ-
+          if (r < tp.ne) {
+            double tvs[2], hxs[2], hys[2], hzs[2];
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {   // 0: left point r, 1: its mirror NQ - 1 - r
+              const int xq = side ? NQ - 1 - r : r;
+              const double sg = side ? -1.0 : 1.0;
+              const double cu = fma(sg, vO[0][nt][e], vE[0][nt][e]);
+              const double g0 = fma(sg, vE[1][nt][e], vO[1][nt][e]);
+              const double g1 = fma(sg, vO[2][nt][e], vE[2][nt][e]);
+              const double g2 = fma(sg, vO[3][nt][e], vE[3][nt][e]);
+              const double xi = XQ[xq];
+              double J[3][3];
+#pragma unroll
+              for (int i = 0; i < 3; ++i) {
+                J[i][0] = Jx[i];
+                J[i][1] = fma(Jyb[i], xi, Jya[i]);
+                J[i][2] = fma(Jzb[i], xi, Jza[i]);
+              }
+              const double a00 = J[1][1] * J[2][2] - J[1][2] * J[2][1], a01 = J[0][2] * J[2][1] - J[0][1] * J[2][2],
+                           a02 = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+              const double a10 = J[1][2] * J[2][0] - J[1][0] * J[2][2], a11 = J[0][0] * J[2][2] - J[0][2] * J[2][0],
+                           a12 = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+              const double a20 = J[1][0] * J[2][1] - J[1][1] * J[2][0], a21 = J[0][1] * J[2][0] - J[0][0] * J[2][1],
+                           a22 = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+              const double det = J[0][0] * a00 + J[0][1] * a10 + J[0][2] * a20;
+              const double wgt = wzy * WQ[xq];
+              const double ad = fabs(det);
+              const double kk = al * wgt * __drcp_rn(ad);
+              const double v0 = a00 * g0 + a10 * g1 + a20 * g2, v1 = a01 * g0 + a11 * g1 + a21 * g2,
+                           v2 = a02 * g0 + a12 * g1 + a22 * g2;
+              hxs[side] = kk * (a00 * v0 + a01 * v1 + a02 * v2);
+              hys[side] = kk * (a10 * v0 + a11 * v1 + a12 * v2);
+              hzs[side] = kk * (a20 * v0 + a21 * v1 + a22 * v2);
+              tvs[side] = be * wgt * ad * cu;
+            }
+            out8[0] = tvs[0] + tvs[1]; out8[1] = tvs[0] - tvs[1];
+            out8[2] = hxs[0] + hxs[1]; out8[3] = hxs[0] - hxs[1];
+            out8[4] = hys[0] + hys[1]; out8[5] = hys[0] - hys[1];
+            out8[6] = hzs[0] + hzs[1]; out8[7] = hzs[0] - hzs[1];
+          }
+#pragma unroll
+          for (int cmb = 0; cmb < 8; ++cmb) WRg[(cmb * 8 + l4) * XE + r] = out8[cmb];
+        }
+    }
+    __syncwarp();
+    {   // backward x: even outputs from (T+, HX-, HY+, HZ+), odd outputs from (T-, HX+, HY-, HZ-), 24 DMMA
+      double pE[4][2] = {}, pO[4][2] = {};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double* a = WRg + l4 * XE + 4 * k + lm;
+        const double Tp = a[0], Tm = a[8 * XE], Xp = a[16 * XE], Xm = a[24 * XE], Yp = a[32 * XE], Ym = a[40 * XE],
+                     Zp = a[48 * XE], Zm = a[56 * XE];
+        const double sE = fb(0, 0, k), dE = fb(1, 0, k), sO = fb(0, 1, k), dO = fb(1, 1, k);
+        dmma(pE[0], Tp, sE);
+        dmma(pE[1], Xm, dE);
+        dmma(pE[2], Yp, sE);
+        dmma(pE[3], Zp, sE);
+        dmma(pO[0], Tm, sO);
+        dmma(pO[1], Xp, dO);
+        dmma(pO[2], Ym, sO);
+        dmma(pO[3], Zm, sO);
+      }
+      const int yq = 8 * wmt + l4;
+      double* P = PP + (wpl * 3) * SZ_P;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int xe = 2 * lm + e, xo = 8 + 2 * lm + e;   // even / odd positions
+        const int oe = xe * XS_P + (yq ^ h_p(xe)), oo = xo * XS_P + (yq ^ h_p(xo));
+        P[oe] = pE[0][e] + pE[1][e];
+        P[SZ_P + oe] = pE[2][e];
+        P[2 * SZ_P + oe] = pE[3][e];
+        P[oo] = pO[0][e] + pO[1][e];
+        P[SZ_P + oo] = pO[2][e];
+        P[2 * SZ_P + oo] = pO[3][e];
+      }
+    }
+    } else {
     // forward x: u_q and hat-gradient at the 8 x 24 points of the rows, 48 DMMA
     double cu[3][2] = {}, c0[3][2] = {}, c1[3][2] = {}, c2[3][2] = {};
 #pragma unroll
@@ -352,6 +524,7 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
           P[2 * SZ_P + o] = p3[nt][e];
         }
     }
+    }
     __syncthreads();
     // ===== backward y: warps 0-7 two Q1 jobs (2 terms), warps 8-11 four Q2 jobs; Q stored [x][y]
     if (w < 8) {
@@ -411,10 +584,31 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
               cz = (int)(cell / ((long long)tp.n[0] * tp.n[1]));
     const int n3 = P1 * P1 * P1;
     double* ob = cellbuf + cell * n3;
+    int xpos[16];   // even / odd position of each x index (EO); x = 0, p from the (E_0, O_0) pair
+    if (EO) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) xpos[q] = 0;
+#pragma unroll
+      for (int pos = 1; pos < 16; ++pos)
+        if (pos != 8 && tp.xsig[pos] >= 0) xpos[tp.xsig[pos]] = pos;
+    }
     for (int i = t; i < n3; i += TRI_THREADS) {
       const int z = i / (P1 * P1), y = (i / P1) % P1, x = i % P1;
-      const double v = OUT[z * 256 + swu(x, y)];
-      OUT[z * 256 + swu(x, y)] = 0.0;
+      double v;
+      if (EO) {   // back from the even / odd basis: v_0 = (v'_E0 + v'_O0)/2, v_p = (v'_E0 - v'_O0)/2
+        if (x == 0 || x == p) {
+          const double e0 = OUT[z * 256 + swu(0, y)], o0 = OUT[z * 256 + swu(8, y)];
+          v = 0.5 * (x == 0 ? e0 + o0 : e0 - o0);
+        } else {
+          int q = 0;
+#pragma unroll
+          for (int xx = 0; xx < 16; ++xx) q = (xx == x) ? xpos[xx] : q;
+          v = OUT[z * 256 + swu(q, y)];
+        }
+      } else {
+        v = OUT[z * 256 + swu(x, y)];
+        OUT[z * 256 + swu(x, y)] = 0.0;
+      }
       if (x == 0 || x == p || y == 0 || y == p || z == 0 || z == p) {
         ob[i] = v;
       } else {
@@ -422,6 +616,10 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
         const long long g = (((long long)cz * p + z) * tp.Ly + (long long)cy * p + y) * ldx + (long long)cx * p + x;
         out[g] = sign * v;
       }
+    }
+    if (EO) {   // the pair (E_0, O_0) is read by two threads: zero OUT after everyone has read it
+      __syncthreads();
+      for (int i = t; i < 4096; i += TRI_THREADS) OUT[i] = 0.0;
     }
   }
   }
@@ -497,7 +695,9 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
                                    double sign, double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(apply_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(apply_tri_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(apply_tri_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TRI_SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -514,7 +714,10 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
   }
   const unsigned grid = (unsigned)std::min<long long>(ncell, nsm);   // persistent: one CTA per SM
   if (kt) kt->begin(kt->arg);
-  apply_tri_kernel<<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, f, out, sign, cellbuf);
+  if (tp.eo)
+    apply_tri_kernel<true><<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, f, out, sign, cellbuf);
+  else
+    apply_tri_kernel<false><<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, f, out, sign, cellbuf);
   if (kt) kt->end(kt->arg);
   tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
   (void)nd;

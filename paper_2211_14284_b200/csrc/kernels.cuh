@@ -72,6 +72,13 @@ struct TriParams {
   long long Lx, Ly, Lz;
   unsigned gamma_d;
   long long ldx_out;   // x-stride of the output (0 = Lx; the padded TMA layout)
+  // even / odd split of the x contractions (nq even): the FDM basis functions have definite
+  // parity (E_0 = s_0 + s_p, O_0 = s_0 - s_p, interior s_j even or odd) and the GLL points come in
+  // mirror pairs, so each 24 x 16 contraction splits into two 12 x 8 ones.  xsig[pos] = the
+  // original x index at even/odd position pos (0: E_0, 8: O_0, -1: padding); the tables follow the
+  // standard ones in `tabs` (S_E, S_O, D_E, D_O at the left points, 12 x 8 each, zero padded)
+  int eo, ne;          // even/odd path on; number of point pairs
+  int xsig[16];
 };
 // optional hooks around a launcher's main kernel (the ABI records CUDA events there for the
 // per-kernel timing phases of rm_timing_read)

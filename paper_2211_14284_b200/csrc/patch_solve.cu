@@ -755,14 +755,6 @@ struct ScGeom {
   double kd[16], k0[16], kp[16];    // D_ii, D_i0, D_ip
 };
 
-// coupling of interior DoF I (interior index iline along the face normal) to face f of its cell:
-// stored, or rebuilt as (D_ii w) D_i{0,p} -- bitwise the assembled value (patches.cpp checks it)
-__device__ __forceinline__ double sc_coup(const ScGeom& G, const double* __restrict__ cc, const double* __restrict__ cw,
-                                          long long K, int f, int I, int ni, int iline) {
-  if (!G.cmp) return cc[(K * 6 + f) * ni + I];
-  const double w = cw[(K * 3 + (f >> 1)) * ni + I];
-  return __dmul_rn(__dmul_rn(G.kd[iline], w), (f & 1) ? G.kp[iline] : G.k0[iline]);
-}
 
 __device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long long y, long long z) {
   return (z * G.ly + y) * G.lxp + x;
@@ -845,6 +837,10 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
                                const double* __restrict__ rp, double* __restrict__ cp, long long nint,
                                double* __restrict__ u, double omega, long long lx) {
   // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
+  __shared__ double kt[3][16];   // D_ii, D_i0, D_ip: lane-varying indices (shared, not the param bank)
+  if (threadIdx.x < 48) kt[threadIdx.x >> 4][threadIdx.x & 15] =
+      (threadIdx.x < 16 ? G.kd : (threadIdx.x < 32 ? G.k0 : G.kp))[threadIdx.x & 15];
+  __syncthreads();
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= ni) return;
@@ -854,12 +850,23 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   (void)nint;
   const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
   const double dv = dinv[K * ni + I];
-  double s = sc_coup(G, cc, cw, K, 0, I, ni, i) * cp[sc_idx(G, x, y + j, z + k)];
-  s = fma(sc_coup(G, cc, cw, K, 1, I, ni, i), cp[sc_idx(G, x + p, y + j, z + k)], s);
-  s = fma(sc_coup(G, cc, cw, K, 2, I, ni, j), cp[sc_idx(G, x + i, y, z + k)], s);
-  s = fma(sc_coup(G, cc, cw, K, 3, I, ni, j), cp[sc_idx(G, x + i, y + p, z + k)], s);
-  s = fma(sc_coup(G, cc, cw, K, 4, I, ni, k), cp[sc_idx(G, x + i, y + j, z)], s);
-  s = fma(sc_coup(G, cc, cw, K, 5, I, ni, k), cp[sc_idx(G, x + i, y + j, z + p)], s);
+  double c0, c1, c2, c3, c4, c5;
+  if (G.cmp) {   // couplings (D_ii w) D_i{0,p} rebuilt from the three interior stiffness weights
+    const double wx = cw[(K * 3 + 0) * ni + I], wy = cw[(K * 3 + 1) * ni + I], wz = cw[(K * 3 + 2) * ni + I];
+    const double ax = __dmul_rn(kt[0][i], wx), ay = __dmul_rn(kt[0][j], wy), az = __dmul_rn(kt[0][k], wz);
+    c0 = __dmul_rn(ax, kt[1][i]); c1 = __dmul_rn(ax, kt[2][i]);
+    c2 = __dmul_rn(ay, kt[1][j]); c3 = __dmul_rn(ay, kt[2][j]);
+    c4 = __dmul_rn(az, kt[1][k]); c5 = __dmul_rn(az, kt[2][k]);
+  } else {
+    c0 = cc[(K * 6 + 0) * ni + I]; c1 = cc[(K * 6 + 1) * ni + I]; c2 = cc[(K * 6 + 2) * ni + I];
+    c3 = cc[(K * 6 + 3) * ni + I]; c4 = cc[(K * 6 + 4) * ni + I]; c5 = cc[(K * 6 + 5) * ni + I];
+  }
+  double s = c0 * cp[sc_idx(G, x, y + j, z + k)];
+  s = fma(c1, cp[sc_idx(G, x + p, y + j, z + k)], s);
+  s = fma(c2, cp[sc_idx(G, x + i, y, z + k)], s);
+  s = fma(c3, cp[sc_idx(G, x + i, y + p, z + k)], s);
+  s = fma(c4, cp[sc_idx(G, x + i, y + j, z)], s);
+  s = fma(c5, cp[sc_idx(G, x + i, y + j, z + p)], s);
   const long long gi = sc_idx(G, x + i, y + j, z + k);
   const double c = dv * (nk[K] * rp[gi] - s);
   if (u) u[((z + k) * G.ly + y + j) * lx + x + i] += omega * c;   // fused combine (one rank): u directly
