@@ -174,6 +174,13 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
       FB[i] = r < tp.ne ? T4[(2 * f + eo) * 96 + r * 8 + e] : 0.0;
     }
   }
+  __shared__ int XPOS[16];   // EO: even / odd position of each interior x index
+  if (EO && t < 16) {
+    int q = 0;
+    for (int pos = 1; pos < 16; ++pos)
+      if (pos != 8 && tp.xsig[pos] == t) q = pos;
+    XPOS[t] = q;
+  }
   auto fx = [&](int f, int eo, int nt, int k) { return FX[(((f * 2 + eo) * 2 + nt) * 2 + k) * 32 + lane]; };
   auto fb = [&](int f, int eo, int k) { return FB[((f * 2 + eo) * 3 + k) * 32 + lane]; };
   const int ly = t & 15, lx = t >> 4;   // per-thread line (x, y), y fastest (threads < 256)
@@ -227,28 +234,19 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
   cp_async_wait_all();
   __syncthreads();   // U, VX of this cell landed; OUT zeroed
   if (EO) {   // x coefficients to the even / odd basis: u'_E0 = (u_0 + u_p)/2, u'_O0 = (u_0 - u_p)/2, permuted
-    if (t < 256) {
+    if (t < 256) {   // this thread's (z, y) row: read every source first (smem addressing), then write
       const int z = t >> 4, y = t & 15;
-      double r[16];
-#pragma unroll
-      for (int x = 0; x < 16; ++x) r[x] = U[z * 256 + swu(x, y)];
-      double rp = 0.0;   // r[p] without a dynamically indexed (local-memory) register array
-#pragma unroll
-      for (int x = 0; x < 16; ++x) rp = (x == p) ? r[x] : rp;
+      double v[16];
 #pragma unroll
       for (int pos = 0; pos < 16; ++pos) {
         const int j = tp.xsig[pos];
-        double v = 0.0;
-        if (pos == 0) {
-          v = 0.5 * (r[0] + rp);
-        } else if (pos == 8) {
-          v = 0.5 * (r[0] - rp);
-        } else {
-#pragma unroll
-          for (int x = 0; x < 16; ++x) v = (x == j) ? r[x] : v;
-        }
-        U[z * 256 + swu(pos, y)] = v;
+        v[pos] = j >= 0 ? U[z * 256 + swu(j, y)] : 0.0;
       }
+      const double u0 = v[0], up = v[8];   // xsig[0] = 0, xsig[8] = p
+      v[0] = 0.5 * (u0 + up);
+      v[8] = 0.5 * (u0 - up);
+#pragma unroll
+      for (int pos = 0; pos < 16; ++pos) U[z * 256 + swu(pos, y)] = v[pos];
     }
     __syncthreads();
   }
@@ -339,12 +337,33 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
         Jza[i] = fma(g6, et, g3);
         Jzb[i] = fma(g7, et, g5);
       }
+      // 12 point pairs x 8 rows per warp = 3 slots per lane: the fragment layout gives lanes
+      // lm < 2 four valid slots (n tile 1 holds r = 8..11) and lanes lm >= 2 two, so the slot
+      // (n tile 1, e = 1) of lane lm is handed to lane lm + 2 (shuffle) and every lane runs three
+      double hv[8];
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int q = 0; q < 4; ++q) {
+        hv[q] = __shfl_xor_sync(0xffffffffu, vE[q][1][1], 2);
+        hv[4 + q] = __shfl_xor_sync(0xffffffffu, vO[q][1][1], 2);
+      }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * nt + 2 * lm + e;
-          if (r >= XE) continue;
+      for (int sl = 0; sl < 3; ++sl) {
+        double ve[4], vo[4];
+        int r;
+        if (sl < 2) {
+          r = 2 * lm + sl;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { ve[q] = vE[q][0][sl]; vo[q] = vO[q][0][sl]; }
+        } else if (lm < 2) {
+          r = 8 + 2 * lm;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { ve[q] = vE[q][1][0]; vo[q] = vO[q][1][0]; }
+        } else {
+          r = 8 + 2 * (lm - 2) + 1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { ve[q] = hv[q]; vo[q] = hv[4 + q]; }
+        }
+        {
           double out8[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // T+, T-, HX+, HX-, HY+, HY-, HZ+, HZ-
           if (r < tp.ne) {
             double tvs[2], hxs[2], hys[2], hzs[2];
@@ -352,10 +371,10 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
             for (int side = 0; side < 2; ++side) {   // 0: left point r, 1: its mirror NQ - 1 - r
               const int xq = side ? NQ - 1 - r : r;
               const double sg = side ? -1.0 : 1.0;
-              const double cu = fma(sg, vO[0][nt][e], vE[0][nt][e]);
-              const double g0 = fma(sg, vE[1][nt][e], vO[1][nt][e]);
-              const double g1 = fma(sg, vO[2][nt][e], vE[2][nt][e]);
-              const double g2 = fma(sg, vO[3][nt][e], vE[3][nt][e]);
+              const double cu = fma(sg, vo[0], ve[0]);
+              const double g0 = fma(sg, ve[1], vo[1]);
+              const double g1 = fma(sg, vo[2], ve[2]);
+              const double g2 = fma(sg, vo[3], ve[3]);
               const double xi = XQ[xq];
               double J[3][3];
 #pragma unroll
@@ -389,6 +408,7 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
 #pragma unroll
           for (int cmb = 0; cmb < 8; ++cmb) WRg[(cmb * 8 + l4) * XE + r] = out8[cmb];
         }
+      }
     }
     __syncwarp();
     {   // backward x: even outputs from (T+, HX-, HY+, HZ+), odd outputs from (T-, HX+, HY-, HZ-), 24 DMMA
@@ -584,14 +604,7 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
               cz = (int)(cell / ((long long)tp.n[0] * tp.n[1]));
     const int n3 = P1 * P1 * P1;
     double* ob = cellbuf + cell * n3;
-    int xpos[16];   // even / odd position of each x index (EO); x = 0, p from the (E_0, O_0) pair
-    if (EO) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) xpos[q] = 0;
-#pragma unroll
-      for (int pos = 1; pos < 16; ++pos)
-        if (pos != 8 && tp.xsig[pos] >= 0) xpos[tp.xsig[pos]] = pos;
-    }
+
     for (int i = t; i < n3; i += TRI_THREADS) {
       const int z = i / (P1 * P1), y = (i / P1) % P1, x = i % P1;
       double v;
@@ -600,10 +613,7 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
           const double e0 = OUT[z * 256 + swu(0, y)], o0 = OUT[z * 256 + swu(8, y)];
           v = 0.5 * (x == 0 ? e0 + o0 : e0 - o0);
         } else {
-          int q = 0;
-#pragma unroll
-          for (int xx = 0; xx < 16; ++xx) q = (xx == x) ? xpos[xx] : q;
-          v = OUT[z * 256 + swu(q, y)];
+          v = OUT[z * 256 + swu(XPOS[x], y)];
         }
       } else {
         v = OUT[z * 256 + swu(x, y)];
