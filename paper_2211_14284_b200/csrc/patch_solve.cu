@@ -1049,16 +1049,12 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
     const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
-    // with the combine in this launch the post step adds omega c_I to u itself and the combine
-    // skips the cell interiors (one fewer pass over them); otherwise c_I goes to cpad (multi-rank:
-    // the ghost layer's interiors are reverse-added before the combine)
-    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint, combine ? u : nullptr,
-                                       omega, L.pad.len[0][0]);
+    // c_I to cpad; the combine below adds omega c to u for every DoF (measured: adding omega c_I
+    // to u inside the post step and skipping the interiors in the combine is slower -- the post
+    // step's scattered read-modify-write of u costs more than the combine's streaming pass)
+    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint, nullptr, omega,
+                                       L.pad.len[0][0]);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (combine) {
-      unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, L.sc_p);
-      return cudaGetLastError();
-    }
   }
   if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, 0);
   return cudaGetLastError();
