@@ -766,14 +766,12 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
       c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
-    } else if (space >= 1) {
-      // Cartesian H(curl) / H(div): one apply launch over all cells + the skeleton gather
+    } else if (space >= 1 || rm::exp_env("RM_APPLY_PW")) {
+      // Cartesian H(curl) / H(div): pointwise-stage apply, one launch over all cells + the skeleton
+      // gather (apply_kform.cu).  H(grad) keeps the colour kernel of apply.cu: the k = 0 pointwise
+      // kernel (experiment RM_APPLY_PW) measured residual 0.48 ms at cfg2 (apply 0.26 + gather 0.20)
+      // against 0.34 ms for the colours (profiles/r02_bench_cfg2_k.json)
       c->d_cellbuf = c->dalloc(rm::kform_cellbuf_doubles(space, p, c->n));
-    } else if (space == 0 && rm::exp_env("RM_APPLY_CELLBUF")) {
-      // Cartesian H(grad), opt-in: one apply launch over all cells, interior DoFs stored directly,
-      // skeleton entries through the cell buffer and the gather (measured: apply 0.28 -> 0.19 ms at
-      // cfg2, but the gather costs what the colours and the init cost; the residual phase is equal)
-      c->d_cellbuf = c->dalloc((size_t)c->n[0] * c->n[1] * c->n[2] * (p + 1) * (p + 1) * (p + 1));
     }
     // ---- device operator
     c->op = make_op(c->sp, gamma_d);

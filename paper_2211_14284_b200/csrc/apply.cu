@@ -352,15 +352,11 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt,
                                    double* cellbuf) {
-  if (op.k >= 1 && cellbuf)   // H(curl) / H(div): pointwise-stage kernels, one launch + gather
+  if (cellbuf)   // pointwise-stage kernels (apply_kform.cu), one launch + skeleton gather, every k
     return launch_apply_kform(op, alpha, beta, coef_const, hpow, u, f, out, ndof, cellbuf, st, nlaunch, kt);
-  const bool cb = cellbuf && op.k == 0;   // cell-buffer mode: no init, no colours, a gather at the end
-  int nl = 0;
-  if (!cb) {
-    if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);
-    else apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
-    nl = 1;
-  }
+  int nl = 1;
+  if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);
+  else apply_init_kernel<<<(unsigned)((ndof + 255) / 256), 256, 0, st>>>(op, f, out, ndof);
   if (kt) kt->begin(kt->arg);
   struct End {
     const KTimer* kt;
@@ -370,32 +366,21 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
     const double sgn = f ? -1.0 : 1.0;
     cudaError_t e;
     switch (op.p) {
-      case 1: e = launch_q<1>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 2: e = launch_q<2>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 3: e = launch_q<3>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 4: e = launch_q<4>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 5: e = launch_q<5>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 6: e = launch_q<6>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 7: e = launch_q<7>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 8: e = launch_q<8>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 9: e = launch_q<9>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 10: e = launch_q<10>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 11: e = launch_q<11>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 12: e = launch_q<12>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 13: e = launch_q<13>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      case 14: e = launch_q<14>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-      default: e = launch_q<15>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cb ? cellbuf : nullptr); break;
-    }
-    if (e == cudaSuccess && cb) {   // the apply kernel is timed alone (as on the trilinear path)
-      if (kt) { kt->end(kt->arg); end_.kt = nullptr; }
-      TriParams tp{};
-      tp.p = op.p;
-      for (int d = 0; d < 3; ++d) tp.n[d] = op.n[d];
-      tp.Lx = op.len[0][0]; tp.Ly = op.len[0][1]; tp.Lz = op.len[0][2];
-      tp.gamma_d = op.gamma_d;
-      tp.ldx_out = op.ldx_out;
-      e = launch_skeleton_gather(tp, cellbuf, f, out, sgn, st);
-      ++nl;
+      case 1: e = launch_q<1>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 2: e = launch_q<2>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 3: e = launch_q<3>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 4: e = launch_q<4>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 5: e = launch_q<5>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 6: e = launch_q<6>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 7: e = launch_q<7>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 8: e = launch_q<8>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 9: e = launch_q<9>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 10: e = launch_q<10>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 11: e = launch_q<11>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 12: e = launch_q<12>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 13: e = launch_q<13>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      case 14: e = launch_q<14>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
+      default: e = launch_q<15>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, nullptr); break;
     }
     if (nlaunch) *nlaunch = nl;
     return e;

@@ -283,12 +283,84 @@ __global__ void __launch_bounds__(KF_THREADS) apply_ncf_kernel(const __grid_cons
   }
 }
 
+// (A-hat x)_i along a line with stride s: interior rows (0, i, p), vertex rows full (eq:fdmbasis)
+template <int P>
+__device__ __forceinline__ double aline(const double* __restrict__ sA, const double* x, int s, int i) {
+  constexpr int N = P + 1;
+  if (i >= 1 && i < P) return sA[i * N] * x[0] + sA[i * N + i] * x[i * s] + sA[i * N + P] * x[P * s];
+  double v = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) v += sA[i * N + j] * x[j * s];
+  return v;
+}
+
+// H(grad), Cartesian (k = 0): A_K u = beta s_M (B B B) u + alpha sum_d s_d (A-hat along d, B-hat
+// across), in three pointwise stages on the cell window (x: B u, A u; y: B (Bu), A (Bu), B (Au)
+// combined into Q = beta s_M B B u + alpha (s_x B A u + s_y A B u); z: v = B_z Q + alpha s_z A_z (B B u)).
+// One CTA per cell, ONE launch over all cells; interior entries final (out = f + sign v, padded
+// x-stride ldx), skeleton entries to the cell buffer, summed by kform_gather_kernel.
+template <int P>
+__global__ void __launch_bounds__(KF_THREADS) apply_q_pw_kernel(const __grid_constant__ OpParams op,
+                                                                 const double* __restrict__ alpha,
+                                                                 const double* __restrict__ beta, int coef_const,
+                                                                 const double* __restrict__ hpow,
+                                                                 const double* __restrict__ u,
+                                                                 const double* __restrict__ f, double* __restrict__ out,
+                                                                 long long ldx, double* __restrict__ cellbuf,
+                                                                 double sign) {
+  constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  extern __shared__ double sm[];
+  double* sB = sm;
+  double* sA = sB + N2;
+  double* U = sA + N2;
+  double* X1 = U + N3;
+  double* X2 = X1 + N3;
+  double* Y1 = X2 + N3;
+  double* Q = U;   // U is dead after the x stage
+  const int cell = blockIdx.x;
+  const CellCtx c = cell_ctx(op, alpha, beta, coef_const, hpow, cell);
+  for (int i = threadIdx.x; i < N2; i += blockDim.x) { sB[i] = op.Bh[i]; sA[i] = op.Ah[i]; }
+  load_comp<P, N, N, N, 7>(op, 0, c, u, U);
+  __syncthreads();
+  for (int l = threadIdx.x; l < N3; l += KF_THREADS) {
+    const int a = l % N;
+    X1[l] = bline<P>(sB, U + l - a, 1, a);
+    X2[l] = aline<P>(sA, U + l - a, 1, a);
+  }
+  __syncthreads();
+  const double hv = c.hx * c.hy * c.hz;
+  const double sM = c.be * hv * 0.125, sx = c.al * c.hy * c.hz / (2.0 * c.hx), sy = c.al * c.hx * c.hz / (2.0 * c.hy),
+               sz = c.al * c.hx * c.hy / (2.0 * c.hz);
+  for (int l = threadIdx.x; l < N3; l += KF_THREADS) {
+    const int b = (l / N) % N;
+    const double* x1 = X1 + l - b * N;
+    const double y1 = bline<P>(sB, x1, N, b);
+    const double y2 = aline<P>(sA, x1, N, b);
+    const double y3 = bline<P>(sB, X2 + l - b * N, N, b);
+    Y1[l] = y1;
+    Q[l] = sM * y1 + sx * y3 + sy * y2;
+  }
+  __syncthreads();
+  const long long Lx = op.len[0][0], Ly = op.len[0][1];
+  const long long ox = (long long)c.cx * P, oy = (long long)c.cy * P, oz = (long long)c.cz * P;
+  for (int l = threadIdx.x; l < N3; l += KF_THREADS) {
+    const int a = l % N, b = (l / N) % N, cc = l / N2;
+    const double v = bline<P>(sB, Q + l - cc * N2, N2, cc) + sz * aline<P>(sA, Y1 + l - cc * N2, N2, cc);
+    if (a == 0 || a == P || b == 0 || b == P || cc == 0 || cc == P) {
+      cellbuf[(long long)cell * N3 + l] = v;
+    } else {   // interior of the cell: never constrained
+      const long long row = (oz + cc) * Ly + oy + b;
+      out[row * ldx + ox + a] = (f ? __ldg(f + row * Lx + ox + a) : 0.0) + sign * v;
+    }
+  }
+}
+
 // out[g] = f[g] + sign * sum over the <= 4 cells carrying skeleton DoF g of their buffered
 // contributions (cells in z, y, x order); constrained entries 0; cell-interior entries were
 // stored by the apply kernel and are left alone.  One thread per DoF.
 __global__ void kform_gather_kernel(const __grid_constant__ OpParams op, const double* __restrict__ cellbuf,
                                     const double* __restrict__ f, double* __restrict__ out, double sign,
-                                    long long ndof, int nloc) {
+                                    long long ndof, int nloc, long long ldx) {
   const int p = op.p;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < ndof; g += (long long)gridDim.x * blockDim.x) {
     int m = 0;
@@ -318,7 +390,9 @@ __global__ void kform_gather_kernel(const __grid_constant__ OpParams op, const d
       }
     }
     if (!skel) continue;   // cell-interior entry: stored by the apply kernel
-    if (con) { out[g] = 0.0; continue; }
+    // output index: the vector layout, or (one component) a padded x-stride ldx
+    const long long go = ldx > 0 ? ((long long)idx[2] * Ly + idx[1]) * ldx + idx[0] : g;
+    if (con) { out[go] = 0.0; continue; }
     int lo = 0;
     for (int t = 0; t < m; ++t) {
       int sz = 1;
@@ -335,7 +409,7 @@ __global__ void kform_gather_kernel(const __grid_constant__ OpParams op, const d
           const long long cell = ((long long)cz * op.n[1] + cy) * op.n[0] + cx;
           s += cellbuf[cell * nloc + lo + (az * ls[1] + ay) * ls[0] + ax];
         }
-    out[g] = (f ? f[g] : 0.0) + sign * s;
+    out[go] = (f ? f[g] : 0.0) + sign * s;
   }
 }
 
@@ -345,7 +419,17 @@ cudaError_t launch_kform_p(const OpParams& op, const double* alpha, const double
                            double sign, cudaStream_t st) {
   constexpr int N = P + 1;
   const int ncell = op.n[0] * op.n[1] * op.n[2];
-  if (op.k == 1) {
+  if (op.k == 0) {
+    const size_t smem = sizeof(double) * (size_t)(2 * N * N + 4 * N * N * N);
+    static bool set = false;
+    if (!set && smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(apply_q_pw_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    set = true;
+    const long long ldx = op.ldx_out > 0 ? op.ldx_out : op.len[0][0];
+    apply_q_pw_kernel<P><<<ncell, KF_THREADS, smem, st>>>(op, alpha, beta, coef_const, hpow, u, f, out, ldx, cellbuf, sign);
+  } else if (op.k == 1) {
     const size_t smem = sizeof(double) * (size_t)(N * N + P * N + 3 * P * N * N + 6 * N * P * P);
     static bool set = false;
     if (!set && smem > 48 * 1024) {
@@ -370,7 +454,8 @@ cudaError_t launch_kform_p(const OpParams& op, const double* alpha, const double
 }  // namespace
 
 size_t kform_cellbuf_doubles(int k, int p, const int* n) {
-  const size_t nloc = (k == 1) ? 3 * (size_t)p * (p + 1) * (p + 1) : 3 * (size_t)(p + 1) * p * p;
+  const size_t nloc = k == 0 ? (size_t)(p + 1) * (p + 1) * (p + 1)
+                             : (k == 1 ? 3 * (size_t)p * (p + 1) * (p + 1) : 3 * (size_t)(p + 1) * p * p);
   return nloc * (size_t)n[0] * n[1] * n[2];
 }
 
@@ -378,7 +463,7 @@ cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const do
                                const double* hpow, const double* u, const double* f, double* out, long long ndof,
                                double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt) {
   const double sign = f ? -1.0 : 1.0;
-  if (op.k != 1 && op.k != 2) return cudaErrorInvalidValue;
+  if (op.k < 0 || op.k > 2) return cudaErrorInvalidValue;
   if (kt) kt->begin(kt->arg);
   cudaError_t e;
   switch (op.p) {
@@ -391,8 +476,8 @@ cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const do
   if (kt) kt->end(kt->arg);
   if (e != cudaSuccess) return e;
   const int p = op.p;
-  const int nloc = (op.k == 1) ? 3 * p * (p + 1) * (p + 1) : 3 * (p + 1) * p * p;
-  kform_gather_kernel<<<148 * 16, 256, 0, st>>>(op, cellbuf, f, out, sign, ndof, nloc);
+  const int nloc = op.k == 0 ? (p + 1) * (p + 1) * (p + 1) : (op.k == 1 ? 3 * p * (p + 1) * (p + 1) : 3 * (p + 1) * p * p);
+  kform_gather_kernel<<<148 * 16, 256, 0, st>>>(op, cellbuf, f, out, sign, ndof, nloc, op.k == 0 ? op.ldx_out : 0);
   if (nlaunch) *nlaunch = 2;
   return cudaGetLastError();
 }
