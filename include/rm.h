@@ -112,6 +112,8 @@ typedef struct {
   int32_t comm_nranks;       /* ranks of the context's NCCL communicator (0 = none)                 */
   int32_t coarse;            /* 1 if the p = 1 coarse level is set up (options.coarse)             */
   int64_t coarse_ndof;       /* unconstrained DoFs of the coarse problem A_0 (0 without it)        */
+  int32_t batched_families;  /* patch families solved by the class-batched kernel (RM_PATCH_STREAM) */
+  int32_t batch_width;       /* patches per CTA of the widest batched family (0 if none)           */
 } rm_info;
 
 void rm_default_options(rm_options *opt);
@@ -157,7 +159,13 @@ rm_status rm_nccl_unique_id(void *id128);
 rm_status rm_nccl_check(int32_t device);
 
 /* Builds the 1D FDM tables, the structured layout, all patch factors and uploads them.
- * alpha, beta: host arrays, n == 1 (constant) or one value per cell, C-order [z][y][x]. */
+ * alpha, beta: host arrays, n == 1 (constant) or one value per cell, C-order [z][y][x].
+ * Environment read at setup (the only runtime knobs of the product build):
+ *   RM_SETUP_THREADS=n  host threads of the setup (default: all cores);
+ *   RM_NBOX1=1          the persistent patch kernel keeps one window box in flight (test switch);
+ *   RM_PATCH_STREAM=1   families whose patches share few factor blocks (uniform Cartesian meshes)
+ *                       use the persistent stream kernel instead of the class-batched kernel
+ *                       (test switch: both paths are parity-tested). */
 rm_status rm_setup(rm_ctx **ctx, const rm_mesh *mesh, int32_t p, rm_space space,
                    const double *alpha, int64_t n_alpha, const double *beta, int64_t n_beta,
                    uint32_t gamma_d, const rm_options *opt);

@@ -74,7 +74,8 @@ class rm_info(ctypes.Structure):
                 ("n_classes", ctypes.c_int32), ("icc_sigma_max", ctypes.c_double), ("setup_seconds", ctypes.c_double),
                 ("factor_nnz", ctypes.c_int64), ("factor_nnz_primary", ctypes.c_int64),
                 ("factor_unique_bytes", ctypes.c_int64), ("comm_nranks", ctypes.c_int32), ("coarse", ctypes.c_int32),
-                ("coarse_ndof", ctypes.c_int64)]
+                ("coarse_ndof", ctypes.c_int64), ("batched_families", ctypes.c_int32),
+                ("batch_width", ctypes.c_int32)]
 
 
 def _load():

@@ -49,6 +49,8 @@ def build(verbose: bool = False) -> str:
     headers = _headers()
     objs = []
     inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include"]
+    if os.environ.get("RM_BUILD_EXPERIMENTS"):   # instrumentation build (exp_env.hpp); rebuild from clean
+        inc += ["-DRM_EXPERIMENTS"]
     for s in CXX_SRC:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")

@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -157,6 +158,102 @@ struct DevFamily {
   }
 };
 
+// Class-batched mode (patch_solve.cu, patch_batch_kernel): families whose patches share few value
+// blocks (on average >= 4 patches per block), with exact programs (dense final block or none) and
+// no static condensation.  Batches = runs of <= B patches of one (class, value block) inside one
+// colour; B = the largest of 8, 4, 2 whose working set fits in shared memory.  RM_PATCH_STREAM=1
+// (documented test knob, rm.h) keeps the persistent stream kernel.
+// pc / pv / pvn: per patch in colour-sorted order: class, host stream-block offset, device offset.
+void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>& pc, const std::vector<long long>& pv,
+                  const std::vector<long long>& pvn, size_t nblocks) {
+  rm::PatchLaunch& Lh = F.launch;
+  Lh.batch = 0;
+  const size_t np = pc.size();
+  if (np == 0 || std::getenv("RM_PATCH_STREAM") || !P.sc_nk.empty() || nblocks * 4 > np) return;
+  int mr_max = 0, np_max = 0;
+  for (const auto& C : P.classes) {
+    if (C.n > 0 && (C.final_kind != rm::FINAL_DENSE_INV || C.sc)) return;
+    mr_max = std::max(mr_max, (C.m + 31) & ~31);
+    np_max = std::max(np_max, (int)C.pieces.size());
+  }
+  if (np_max > rm::kBatchMaxPieces) return;
+  int B = 0;
+  size_t smem = 0;
+  for (int b : {8, 4, 2})
+    if ((smem = rm::patch_batch_smem(P.box_total, mr_max, b)) > 0) { B = b; break; }
+  if (B == 0) return;
+  std::vector<int> bp;
+  std::vector<int> bc;
+  std::vector<long long> bb, bf;
+  std::vector<double> fin;
+  std::unordered_map<long long, long long> fin_of;   // host block offset -> offset in fin
+  auto full_inverse = [&](int cls, long long hofs) -> long long {
+    const rm::ClassProgram& C = P.classes[cls];
+    if (C.m == 0) return 0;
+    auto it = fin_of.find(hofs);
+    if (it != fin_of.end()) return it->second;
+    const int m = C.m, mr = (m + 31) & ~31;
+    const long long at = (long long)fin.size();
+    fin.resize(fin.size() + (size_t)mr * mr, 0.0);
+    double* S = fin.data() + at;
+    const double* blk = P.values.data() + hofs;
+    for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {   // half-stored lane-block tiles -> full matrix
+      const rm::Piece& pcs = C.pieces[pi];
+      if (pcs.kind != rm::PK_TILE) continue;
+      const int I = pcs.a0, J = pcs.a1;
+      for (int r = 0; r < 32; ++r)
+        for (int c = 0; c < 32; ++c) {
+          const int gr = 32 * I + r, gc = 32 * J + c;
+          if (gr >= m || gc >= m) continue;
+          double x;
+          if (I != J) x = blk[pcs.sofs + rm::tile_pos_full(r, c)];
+          else if (c < r) x = blk[pcs.sofs + rm::tile_pos_diag(r, c)];
+          else if (c == r) x = 2.0 * blk[pcs.sofs + rm::tile_pos_diag(r, c)];
+          else continue;
+          S[(size_t)gr * mr + gc] = x;
+          S[(size_t)gc * mr + gr] = x;
+        }
+    }
+    fin_of.emplace(hofs, at);
+    return at;
+  };
+  for (int c = 0; c < P.ncolors; ++c) {
+    Lh.bstart[c] = (int)bc.size();
+    // runs of one (class, block) in first-appearance order inside the colour
+    std::vector<std::pair<long long, int>> keys;
+    std::unordered_map<long long, std::vector<int>> runs;
+    for (int i = F.color_start[c]; i < F.color_start[c + 1]; ++i) {
+      const long long key = pvn[i] * 4096 + pc[i];
+      auto it = runs.find(key);
+      if (it == runs.end()) { keys.emplace_back(key, i); it = runs.emplace(key, std::vector<int>()).first; }
+      it->second.push_back(i);
+    }
+    for (const auto& k : keys) {
+      const std::vector<int>& r = runs[k.first];
+      const int i0 = k.second;
+      const long long fo = full_inverse(pc[i0], pv[i0]);
+      for (size_t s = 0; s < r.size(); s += B) {
+        for (int b = 0; b < B; ++b) bp.push_back(s + b < r.size() ? r[s + b] : -1);
+        bc.push_back(pc[i0]);
+        bb.push_back(pvn[i0]);
+        bf.push_back(fo);
+      }
+    }
+  }
+  Lh.bstart[P.ncolors] = (int)bc.size();
+  Lh.bpatch = F.upload(bp);
+  Lh.bclass = F.upload(bc);
+  Lh.bblock = F.upload(bb);
+  Lh.bfin = F.upload(bf);
+  Lh.fin = fin.empty() ? nullptr : F.upload(fin);
+  Lh.mr_max = mr_max;
+  Lh.bsmem = smem;
+  Lh.batch = B;
+  if (rm::exp_env("RM_VERBOSE"))
+    fprintf(stderr, "[rm] batched patch solve: %zu patches, %zu blocks, B=%d, %zu batches, smem=%zu\n", np, nblocks, B,
+            bc.size(), smem);
+}
+
 // share: a family of the same space whose padded r / c buffers this one uses (orientation families)
 void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* share = nullptr) {
   const int NW = rm::RM_PATCH_TILE_WARPS;
@@ -192,6 +289,12 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     }
     d.units = F.upload(us);
     d.meta = F.upload(C.meta);
+    {
+      std::vector<int2> pt(C.pieces.size());
+      for (size_t i = 0; i < pt.size(); ++i) pt[i] = make_int2(C.pieces[i].mofs, C.pieces[i].sofs);
+      d.ptab = F.upload(pt);
+      d.npieces = (int)pt.size();
+    }
     d.nunits = (int)us.size();
     d.ngs = C.ngs;
     d.tile_p0 = C.tile_p0; d.tile_p1 = C.tile_p1;
@@ -343,6 +446,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     flush();
     Lh.pvals = F.upload(pvn);
     Lh.vals = dvals;
+    plan_batches(F, P, pc, pv, pvn, remap.size());
     // per-CTA producer issue lists in consumption order (patch_solve.cu): sparse channel
     // fwd(0), then per i: fwd(i+1), final(i) unless dense tiles, bwd(i); tile channel tiles(i)
     std::vector<unsigned char*> dmeta(P.classes.size());
@@ -985,6 +1089,12 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
   info->comm_nranks = c->comm ? c->nranks : 0;
   info->coarse = c->coarse ? 1 : 0;
   info->coarse_ndof = c->coarse ? c->coarse->nfree1 : 0;
+  for (const auto* fams : {&c->prims, &c->pots})
+    for (const auto& F : *fams)
+      if (F.launch.batch) {
+        ++info->batched_families;
+        info->batch_width = std::max(info->batch_width, F.launch.batch);
+      }
   info->setup_seconds = c->setup_seconds;
   return RM_OK;
 }

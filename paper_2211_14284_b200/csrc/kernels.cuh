@@ -61,6 +61,8 @@ struct DClass {
   int nunits, ngs, tile_p0, tile_p1, iccf_nlev, iccb_nlev;
   int uf0, uf1, fin_tiles, pad2;  // final segment units [uf0, uf1); fin_tiles: on the tile channel
   const int *iccf_lp, *iccb_lp;  // per ICC level: first piece (size nlev + 1)
+  const int2* ptab;              // per piece {meta offset, value offset} (class-batched kernel)
+  int npieces, pad3;
 };
 constexpr int RM_MAXCOLORS = 12;
 struct ColorStarts { int ncolors; int start[RM_MAXCOLORS + 1]; };
@@ -195,7 +197,23 @@ struct PatchLaunch {
   const long long* xbeg;         // [2 * grid + 2]: CTA b's sparse list = [xbeg[2b], xbeg[2b+1]),
                                  //                tile list = [xbeg[2b+1], xbeg[2b+2])
   unsigned long long* prof;   // RM_PROFILE=1 instrumentation counters (else null)
+  // Class-batched mode (families whose patches share few value blocks -- uniform Cartesian meshes,
+  // cfg1/3/4): each CTA solves `batch` patches of ONE value block at once (the block is read once
+  // for all of them, every elimination step has `batch` independent right-hand sides), one launch
+  // per colour (patch_batch_kernel).  batch = 0: the persistent stream kernel.
+  int batch;
+  const int* bpatch;          // [nbatch][batch] patch index (colour-sorted order), -1 = empty slot
+  const int* bclass;          // per batch: class
+  const long long* bblock;    // per batch: value-block offset in vals
+  const long long* bfin;      // per batch: offset of the block's full final-block inverse in fin
+  const double* fin;          // full symmetric final-block inverses, mr x mr row-major (mr = m rounded to 32)
+  int bstart[RM_MAXCOLORS + 1];   // first batch of each colour
+  int mr_max;
+  size_t bsmem;               // dynamic shared memory of the batched kernel (bytes)
 };
+// shared memory of the class-batched kernel for B right-hand sides (0 if it does not fit)
+constexpr int kBatchMaxPieces = 1024;   // piece table of a class, staged in shared memory
+size_t patch_batch_smem(int box_total, int mr_max, int B);
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
 // r_padded: r is already in the padded layout L.rpad (the apply wrote it there): no pad pass
 // zero_c / combine: zero the padded correction first / add omega * c to u at the end (families

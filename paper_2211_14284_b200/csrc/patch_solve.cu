@@ -710,6 +710,255 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
 
 namespace {
 
+// ===================================================================== class-batched patch solve
+// Families whose patches share few value blocks (uniform Cartesian meshes: cfg1, cfg3, cfg4 have
+// 27 to 54 distinct blocks for 10^4 .. 10^5 patches) keep their blocks in L2, and the stream kernel
+// above is then latency-bound: one right-hand side per elimination level, the same block re-read
+// per patch (cfg4 potential family, RM_PROFILE: ~36 us per patch and SM, producers waiting for
+// ring room 75% of the time).  Here one CTA takes B patches of ONE value block and runs the same
+// elimination program -- the class's stream pieces, read straight from global memory / L2 -- on
+// all B at once: every value and index is loaded once per B patches, and every lane carries B
+// independent FMA chains.  The B window boxes are interleaved in shared memory (box entry e of
+// patch b at X[e B + b]); gather and scatter are plain coalesced loads and fp64 atomic adds of
+// the NONZERO box entries: within a colour the patches are disjoint and the box entries outside a
+// patch are zeroed first (ZERO piece), so every c entry receives at most one nonzero addend per
+// launch -- deterministic.  One launch per colour (the stream kernel's colour order).  The dense
+// final block is applied with the full symmetric inverse (row-major mr x mr, host-expanded from the
+// half-stored tiles): one coalesced column read per row, B vectors per read.
+constexpr int BT = 512;   // threads per batched CTA
+constexpr int BW = BT / 32;
+
+struct BatchArgs {
+  const DClass* classes;
+  const double* vals;
+  const double* fin;
+  const int* bpatch;
+  const int* bclass;
+  const long long* bblock;
+  const long long* bfin;
+  const int* porig;
+  const TMaps* tm;                              // the family's r / c tensor maps (one per sub-box)
+  int nsub, boxd, gofs, pofs, tofs;             // sub-boxes; box stride; G / partials / piece-table offsets (doubles)
+  int boff[3];
+  unsigned box_bytes;                           // bytes of one patch's window box (all sub-boxes)
+};
+
+// one sliced-ELL piece (W or WT) on the B boxes (stride boxd): slice s owned by warp s % BW.  The
+// values and indices come from global memory (L2): steps of U entries per lane with every load
+// of a step issued before its first use (predicated tail; the slice length is warp-uniform)
+template <int B>
+__device__ __forceinline__ void batch_sliced(const unsigned char* pb, const double* __restrict__ val, int nrows,
+                                             int warp, int lane, double* __restrict__ X, int boxd) {
+  constexpr int U = 8;
+  const Hdr h = hdr(pb);
+  const int nsl = h.a1 - h.a0;
+  const uint32_t* si = reinterpret_cast<const uint32_t*>(pb + 16);
+  const uint16_t* rows = reinterpret_cast<const uint16_t*>(si + nsl);
+  const uint16_t* cols = rows + 32 * nsl;
+  for (int ls = (warp - h.a0 % BW + BW) % BW; ls < nsl; ls += BW) {
+    const uint32_t info = si[ls];
+    const int st = 32 * (int)(info & 0xFFFFu) + lane, cnt = (int)(info >> 16);
+    const int rb = rows[ls * 32 + lane];
+    double acc[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = 0.0;
+    for (int kk = 0; kk < cnt; kk += U) {
+      double w[U];
+      int c[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const bool on = kk + j < cnt;
+        const int e = st + (kk + j) * 32;
+        w[j] = on ? __ldg(val + e) : 0.0;
+        c[j] = on ? (int)cols[e] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = fma(w[j], X[b * boxd + c[j]], acc[b]);
+    }
+    if ((h.a0 + ls) * 32 + lane < nrows) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) X[b * boxd + rb] -= acc[b];
+    }
+  }
+}
+
+template <int B>
+__global__ void __launch_bounds__(BT, 1) patch_batch_kernel(const __grid_constant__ BatchArgs a, int batch0) {
+  extern __shared__ __align__(128) double smb[];
+  __shared__ int sq[B];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bt = batch0 + (int)blockIdx.x;
+  const int boxd = a.boxd;
+  double* X = smb;   // box of slot b at X + b * boxd (the TMA box layout)
+  if (tid < B) sq[tid] = a.bpatch[(long long)bt * B + tid];
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // ---- gather: the window boxes of r by TMA tensor copies (out-of-domain entries zero-filled)
+  if (tid == 0) {
+    int nv = 0;
+    for (int b = 0; b < B; ++b) nv += sq[b] >= 0;
+    mbar_arrive_expect_tx(&bar, (uint32_t)nv * a.box_bytes);
+    for (int b = 0; b < B; ++b) {
+      if (sq[b] < 0) continue;
+      const int* o = a.porig + 9LL * sq[b];
+      for (int sb = 0; sb < a.nsub; ++sb)
+        tma_load_3d(X + b * boxd + a.boff[sb], &a.tm->r[sb], o[3 * sb], o[3 * sb + 1], o[3 * sb + 2], &bar);
+    }
+  }
+  const DClass& C = a.classes[a.bclass[bt]];
+  // the class program's piece table {meta offset, value offset} in shared memory
+  int2* ptab = reinterpret_cast<int2*>(smb + a.tofs);
+  for (int i = tid; i < C.npieces; i += BT) ptab[i] = C.ptab[i];
+  const unsigned char* const meta = C.meta;
+  const double* const vblk = a.vals + a.bblock[bt];
+  __syncthreads();
+  mbar_wait(&bar, 0u);
+  const int nlev = C.nlev;
+  for (int l = 0; l < nlev; ++l) {   // forward
+    const DLevel& L = C.lev[l];
+    const int bs = L.blk.bs;
+    for (int pi = L.piv_b; pi < L.w_b; ++pi) {   // y^_E = L^{-T} L^{-1} v_E (pivot blocks <= 3x3)
+      const int2 pt = ptab[pi];
+      const unsigned char* mc = meta + pt.x;
+      const Hdr h = hdr(mc);
+      const uint16_t* mem = reinterpret_cast<const uint16_t*>(mc + 16);
+      const double* pv = vblk + pt.y;
+      const int cnt = h.a1 - h.a0;
+      for (int t = tid; t < cnt * B; t += BT) {
+        const int li = t / B, b = t - li * B;
+        double* Xb = X + b * boxd;
+        const int m0 = mem[li];
+        if (bs == 1) {
+          const double d = __ldg(pv + li);
+          Xb[m0] *= d * d;
+          continue;
+        }
+        const int m1 = mem[cnt + li];
+        const int m2 = (bs > 2) ? mem[2 * cnt + li] : 0xFFFF;
+        const double l00 = __ldg(pv + li), l10 = __ldg(pv + cnt + li), l11 = __ldg(pv + 2 * cnt + li);
+        double y0 = Xb[m0] * l00, y1 = 0.0, y2 = 0.0;
+        if (m1 != 0xFFFF) y1 = (Xb[m1] - l10 * y0) * l11;
+        if (m2 != 0xFFFF) {
+          const double l20 = __ldg(pv + 3 * cnt + li), l21 = __ldg(pv + 4 * cnt + li), l22 = __ldg(pv + 5 * cnt + li);
+          y2 = (Xb[m2] - l20 * y0 - l21 * y1) * l22;
+          y2 *= l22;
+          Xb[m2] = y2;
+          if (m1 != 0xFFFF) y1 -= l21 * y2;
+          y0 -= l20 * y2;
+        }
+        if (m1 != 0xFFFF) {
+          y1 *= l11;
+          Xb[m1] = y1;
+          y0 -= l10 * y1;
+        }
+        Xb[m0] = y0 * l00;
+      }
+    }
+    __syncthreads();
+    for (int pi = L.w_b; pi < L.w_e; ++pi) {   // v_R -= P_RE y^_E
+      const int2 pt = ptab[pi];
+      batch_sliced<B>(meta + pt.x, vblk + pt.y, L.w.nrows, warp, lane, X, boxd);
+    }
+    __syncthreads();
+  }
+  const int m = C.m;
+  if (m > 0) {   // x_F = S_F^{-1} v_F with the full inverse
+    const uint16_t* fbs = reinterpret_cast<const uint16_t*>(meta + ptab[C.tile_p0].x + 16);   // FINAL piece: final-block boxes
+    const int mr = (m + 31) & ~31;
+    double* G = smb + a.gofs;
+    double* PT = smb + a.pofs;
+    for (int t = tid; t < m * B; t += BT) {
+      const int j = t / B, b = t - j * B;
+      G[t] = X[b * boxd + fbs[j]];
+    }
+    __syncthreads();
+    const double* S = a.fin + a.bfin[bt];
+    const int ns = mr < BT ? BT / mr : 1;   // column segments per row (partials summed below)
+    const int seg = (m + ns - 1) / ns;
+    for (int t = tid; t < ns * mr; t += BT) {
+      const int hs = t / mr, r = t - hs * mr;
+      double acc[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[b] = 0.0;
+      if (r < m) {
+        const int c0 = hs * seg, c1 = min(m, c0 + seg);
+        const double* Sr = S + r;
+        for (int c = c0; c < c1; c += 8) {   // 8 column loads in flight, predicated tail
+          double s[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) s[j] = c + j < c1 ? __ldg(Sr + (long long)(c + j) * mr) : 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double2* g2 = reinterpret_cast<const double2*>(G + min(c + j, c1 - 1) * B);
+#pragma unroll
+            for (int b = 0; b < B / 2; ++b) {
+              const double2 gv = g2[b];
+              acc[2 * b] = fma(s[j], gv.x, acc[2 * b]);
+              acc[2 * b + 1] = fma(s[j], gv.y, acc[2 * b + 1]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) PT[t * B + b] = acc[b];
+    }
+    __syncthreads();
+    for (int t = tid; t < m * B; t += BT) {
+      const int r = t / B, b = t - r * B;
+      double s = 0.0;
+      for (int hs = 0; hs < ns; ++hs) s += PT[(hs * mr + r) * B + b];
+      X[b * boxd + fbs[r]] = s;
+    }
+    __syncthreads();
+  }
+  for (int l = nlev - 1; l >= 0; --l) {   // backward: x_E = y^_E - (P_EE^{-1} P_ER) x_R
+    const DLevel& L = C.lev[l];
+    for (int pi = L.wt_b; pi < L.wt_e; ++pi) {
+      const int2 pt = ptab[pi];
+      batch_sliced<B>(meta + pt.x, vblk + pt.y, L.wt.nrows, warp, lane, X, boxd);
+    }
+    __syncthreads();
+  }
+  {   // ZERO piece (the last): box entries that are not DoFs of the patch
+    const unsigned char* mc = meta + ptab[C.npieces - 1].x;
+    const Hdr h = hdr(mc);
+    const uint16_t* zl = reinterpret_cast<const uint16_t*>(mc + 16);
+    const int cnt = h.a1 - h.a0;
+    for (int t = tid; t < cnt * B; t += BT) {
+      const int k = t / B, b = t - k * B;
+      X[b * boxd + zl[k]] = 0.0;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
+  __syncthreads();
+  // ---- scatter: TMA tensor reduce-add of every box into c (fp64 add per element; within a
+  // colour the patches are disjoint and the entries outside a patch are zero, so every c entry
+  // receives at most one nonzero addend per launch: deterministic)
+  if (tid == 0) {
+    for (int b = 0; b < B; ++b) {
+      if (sq[b] < 0) continue;
+      const int* o = a.porig + 9LL * sq[b];
+      for (int sb = 0; sb < a.nsub; ++sb)
+        tma_reduce_add_3d(&a.tm->c[sb], o[3 * sb], o[3 * sb + 1], o[3 * sb + 2], X + b * boxd + a.boff[sb]);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // complete before the next colour's launch
+  }
+}
+
+template <int B>
+size_t batch_smem_t(int box_total, int mr_max) {
+  const size_t boxd = (size_t)((box_total + 15) & ~15);
+  const size_t mr = (size_t)((mr_max + 31) & ~31);
+  return sizeof(double) * (B * (boxd + mr + std::max<size_t>(BT, mr)) + kBatchMaxPieces);   // + piece table (int2)
+}
+
 __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ r, double* __restrict__ rp,
                            long long npad) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -951,6 +1200,61 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   return cudaSuccess;
 }
 
+size_t patch_batch_smem(int box_total, int mr_max, int B) {
+  size_t s = 0;
+  switch (B) {
+    case 2: s = batch_smem_t<2>(box_total, mr_max); break;
+    case 4: s = batch_smem_t<4>(box_total, mr_max); break;
+    case 8: s = batch_smem_t<8>(box_total, mr_max); break;
+    default: return 0;
+  }
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  if (s + 1024 > (size_t)optin) return 0;   // + the static shared arrays
+  // the attribute is per instantiation, shared by every family: always the full opt-in size
+  const int lim = optin - 1024;
+  cudaError_t e = cudaSuccess;
+  switch (B) {
+    case 2: e = cudaFuncSetAttribute(patch_batch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
+    case 4: e = cudaFuncSetAttribute(patch_batch_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
+    default: e = cudaFuncSetAttribute(patch_batch_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
+  }
+  return e == cudaSuccess ? s : 0;
+}
+
+namespace {
+
+cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
+  BatchArgs a{};
+  a.classes = L.classes; a.vals = L.vals; a.fin = L.fin;
+  a.bpatch = L.bpatch; a.bclass = L.bclass; a.bblock = L.bblock; a.bfin = L.bfin;
+  a.porig = L.porig; a.tm = L.tm_dev;
+  a.nsub = L.nsub;
+  a.boxd = (L.box_total + 15) & ~15;
+  const int mr = (L.mr_max + 31) & ~31;
+  a.gofs = a.boxd * L.batch;
+  a.pofs = a.gofs + mr * L.batch;
+  a.tofs = a.pofs + std::max(BT, mr) * L.batch;
+  a.box_bytes = 0;
+  for (int sb = 0; sb < 3; ++sb) {
+    a.boff[sb] = L.boff[sb];
+    if (sb < L.nsub) a.box_bytes += 8u * (unsigned)(L.box[sb][0] * L.box[sb][1] * L.box[sb][2]);
+  }
+  for (int c = 0; c < L.cs.ncolors; ++c) {
+    const int nb = L.bstart[c + 1] - L.bstart[c];
+    if (nb <= 0) continue;
+    switch (L.batch) {
+      case 2: patch_batch_kernel<2><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
+      case 4: patch_batch_kernel<4><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
+      default: patch_batch_kernel<8><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
 cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st) {
   unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0);
   return cudaGetLastError();
@@ -1010,6 +1314,9 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     if (m < L.nsub) bg.bytes += 8 * L.box[m][0] * L.box[m][1] * L.box[m][2];
   }
   if (kt) kt->begin(kt->arg);
+  if (L.batch) {
+    e = launch_batched(L, st);
+  } else
   // cooperative launch: the colour wait of the store warps spins on a counter advanced by other
   // CTAs, so every CTA of the grid must be resident at once -- the runtime guarantees that (or
   // fails the launch with cudaErrorCooperativeLaunchTooLarge) instead of a possible hang under
@@ -1032,7 +1339,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   if (kt) kt->end(kt->arg);
   if (e != cudaSuccess) return e;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (L.prof) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
+  if (L.prof && !L.batch) {   // RM_PROFILE=1: per-CTA clock64 counters averaged over CTAs (instrumentation only)
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     std::vector<unsigned long long> h((size_t)24 * L.grid);
     if ((e = cudaMemcpy(h.data(), L.prof, h.size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess) return e;

@@ -97,13 +97,26 @@ NBOX1_CASES = [("nbox1-" + c[0], c[1], c[2]) for c in CASES if c[0] in ("cfg2-3^
                                                                        "cfg5-3^3-p3", "cfg4-3^3-p4", "cfg3-6^3-p3",
                                                                        "cfg4-5^3-p3")]
 
+# uniform Cartesian meshes run the class-batched patch kernel by default (few distinct factor
+# blocks); the persistent stream kernel on the same shapes (RM_PATCH_STREAM=1)
+STREAM_CASES = [("stream-" + c[0], c[1], c[2]) for c in CASES
+                if c[0] in ("cfg1", "cfg3-2^3-p6", "cfg4-2^3-p8", "cfg3-6^3-p3", "cfg4-5^3-p3", "cfg3-pafw-2^3-p3",
+                            "cfg4-pafw-2^3-p3")]
+ALL_CASES = CASES + NBOX1_CASES + STREAM_CASES
 
-@pytest.mark.parametrize("name,w,tol", CASES + NBOX1_CASES, ids=[c[0] for c in CASES + NBOX1_CASES])
+
+@pytest.mark.parametrize("name,w,tol", ALL_CASES, ids=[c[0] for c in ALL_CASES])
 def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
     import paper_2211_14284_b200 as rmb
+    if name.startswith(("nbox1-", "stream-")):
+        monkeypatch.setenv("RM_PATCH_STREAM", "1")   # read at setup (include/rm.h)
     if name.startswith("nbox1-"):
         monkeypatch.setenv("RM_NBOX1", "1")   # read by the patch plan at setup (include/rm.h)
     ctx, pb = setup_pair(w)
+    info = ctx.info()
+    if name.startswith(("nbox1-", "stream-")):
+        assert info["batched_families"] == 0
+    name = f"{name} [B={info['batch_width']}]" if info["batched_families"] else name
     assert (ctx.constrained_mask() == pb.constrained).all()
     assert ctx.n_free == int(pb.free.sum())
     f, u = vecs(w, ctx)
