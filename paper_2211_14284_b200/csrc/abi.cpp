@@ -177,10 +177,26 @@ void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>
     np_max = std::max(np_max, (int)C.pieces.size());
   }
   if (np_max > rm::kBatchMaxPieces) return;
-  int B = 0;
+  // configuration (measured on cfg3 / cfg4, scripts/gpu_batch_sweep.sh): 16 resident warps per SM
+  // first (one CTA of 512 or two of 256 threads), then the most patches in flight, then two CTAs
+  int B = 0, NT = 0;
   size_t smem = 0;
-  for (int b : {8, 4, 2})
-    if ((smem = rm::patch_batch_smem(P.box_total, mr_max, b)) > 0) { B = b; break; }
+  long best = -1;
+  for (int nt : {256, 512})
+    for (int b : {8, 4, 2}) {
+      const size_t sm = rm::patch_batch_smem(P.box_total, mr_max, b, nt);
+      if (sm == 0) continue;
+      const int ctas = (nt == 256 && 2 * (sm + 2048) <= 233472) ? 2 : 1;
+      const long score = (long)(ctas * nt / 32) * 10000 + (long)(b * ctas) * 10 + ctas;
+      if (score > best) { best = score; B = b; NT = nt; smem = sm; }
+    }
+  if (const char* e = rm::exp_env("RM_BATCH_CFG")) {   // experiments: "B,NT"
+    int b = 0, nt = 0;
+    size_t sm = 0;
+    if (sscanf(e, "%d,%d", &b, &nt) == 2 && (sm = rm::patch_batch_smem(P.box_total, mr_max, b, nt)) > 0) {
+      B = b; NT = nt; smem = sm;
+    }
+  }
   if (B == 0) return;
   std::vector<int> bp;
   std::vector<int> bc;
@@ -249,9 +265,10 @@ void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>
   Lh.mr_max = mr_max;
   Lh.bsmem = smem;
   Lh.batch = B;
+  Lh.batch_nt = NT;
   if (rm::exp_env("RM_VERBOSE"))
-    fprintf(stderr, "[rm] batched patch solve: %zu patches, %zu blocks, B=%d, %zu batches, smem=%zu\n", np, nblocks, B,
-            bc.size(), smem);
+    fprintf(stderr, "[rm] batched patch solve: %zu patches, %zu blocks, B=%d NT=%d, %zu batches, smem=%zu\n", np, nblocks,
+            B, NT, bc.size(), smem);
 }
 
 // share: a family of the same space whose padded r / c buffers this one uses (orientation families)

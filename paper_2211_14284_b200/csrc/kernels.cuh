@@ -201,7 +201,7 @@ struct PatchLaunch {
   // cfg1/3/4): each CTA solves `batch` patches of ONE value block at once (the block is read once
   // for all of them, every elimination step has `batch` independent right-hand sides), one launch
   // per colour (patch_batch_kernel).  batch = 0: the persistent stream kernel.
-  int batch;
+  int batch, batch_nt;        // patches per CTA, threads per CTA (512: one CTA per SM, 256: two)
   const int* bpatch;          // [nbatch][batch] patch index (colour-sorted order), -1 = empty slot
   const int* bclass;          // per batch: class
   const long long* bblock;    // per batch: value-block offset in vals
@@ -213,7 +213,7 @@ struct PatchLaunch {
 };
 // shared memory of the class-batched kernel for B right-hand sides (0 if it does not fit)
 constexpr int kBatchMaxPieces = 1024;   // piece table of a class, staged in shared memory
-size_t patch_batch_smem(int box_total, int mr_max, int B);
+size_t patch_batch_smem(int box_total, int mr_max, int B, int NT);
 // u += omega * (patch corrections of one family applied to r); r, u in the vector layout
 // r_padded: r is already in the padded layout L.rpad (the apply wrote it there): no pad pass
 // zero_c / combine: zero the padded correction first / add omega * c to u at the end (families

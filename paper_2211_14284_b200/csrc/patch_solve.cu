@@ -725,8 +725,8 @@ namespace {
 // launch -- deterministic.  One launch per colour (the stream kernel's colour order).  The dense
 // final block is applied with the full symmetric inverse (row-major mr x mr, host-expanded from the
 // half-stored tiles): one coalesced column read per row, B vectors per read.
-constexpr int BT = 512;   // threads per batched CTA
-constexpr int BW = BT / 32;
+// threads per CTA NT: 512 (one CTA per SM) or 256 (two CTAs per SM: one CTA's TMA / barrier phases
+// overlap the other's elimination)
 
 struct BatchArgs {
   const DClass* classes;
@@ -746,7 +746,7 @@ struct BatchArgs {
 // one sliced-ELL piece (W or WT) on the B boxes (stride boxd): slice s owned by warp s % BW.  The
 // values and indices come from global memory (L2): steps of U entries per lane with every load
 // of a step issued before its first use (predicated tail; the slice length is warp-uniform)
-template <int B>
+template <int B, int BW>
 __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const double* __restrict__ val, int nrows,
                                              int warp, int lane, double* __restrict__ X, int boxd) {
   constexpr int U = 8;
@@ -784,8 +784,9 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
   }
 }
 
-template <int B>
-__global__ void __launch_bounds__(BT, 1) patch_batch_kernel(const __grid_constant__ BatchArgs a, int batch0) {
+template <int B, int BT>
+__global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(const __grid_constant__ BatchArgs a, int batch0) {
+  constexpr int BW = BT / 32;
   extern __shared__ __align__(128) double smb[];
   __shared__ int sq[B];
   __shared__ __align__(8) uint64_t bar;
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(BT, 1) patch_batch_kernel(const __grid_constan
     __syncthreads();
     for (int pi = L.w_b; pi < L.w_e; ++pi) {   // v_R -= P_RE y^_E
       const int2 pt = ptab[pi];
-      batch_sliced<B>(meta + pt.x, vblk + pt.y, L.w.nrows, warp, lane, X, boxd);
+      batch_sliced<B, BW>(meta + pt.x, vblk + pt.y, L.w.nrows, warp, lane, X, boxd);
     }
     __syncthreads();
   }
@@ -921,7 +922,7 @@ __global__ void __launch_bounds__(BT, 1) patch_batch_kernel(const __grid_constan
     const DLevel& L = C.lev[l];
     for (int pi = L.wt_b; pi < L.wt_e; ++pi) {
       const int2 pt = ptab[pi];
-      batch_sliced<B>(meta + pt.x, vblk + pt.y, L.wt.nrows, warp, lane, X, boxd);
+      batch_sliced<B, BW>(meta + pt.x, vblk + pt.y, L.wt.nrows, warp, lane, X, boxd);
     }
     __syncthreads();
   }
@@ -952,11 +953,10 @@ __global__ void __launch_bounds__(BT, 1) patch_batch_kernel(const __grid_constan
   }
 }
 
-template <int B>
-size_t batch_smem_t(int box_total, int mr_max) {
+size_t batch_smem_t(int B, int NT, int box_total, int mr_max) {
   const size_t boxd = (size_t)((box_total + 15) & ~15);
   const size_t mr = (size_t)((mr_max + 31) & ~31);
-  return sizeof(double) * (B * (boxd + mr + std::max<size_t>(BT, mr)) + kBatchMaxPieces);   // + piece table (int2)
+  return sizeof(double) * (B * (boxd + mr + std::max<size_t>(NT, mr)) + kBatchMaxPieces);   // + piece table (int2)
 }
 
 __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ r, double* __restrict__ rp,
@@ -1200,26 +1200,21 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   return cudaSuccess;
 }
 
-size_t patch_batch_smem(int box_total, int mr_max, int B) {
-  size_t s = 0;
-  switch (B) {
-    case 2: s = batch_smem_t<2>(box_total, mr_max); break;
-    case 4: s = batch_smem_t<4>(box_total, mr_max); break;
-    case 8: s = batch_smem_t<8>(box_total, mr_max); break;
-    default: return 0;
-  }
+#define RM_BATCH_CFGS(X) X(8, 512) X(4, 512) X(2, 512) X(8, 256) X(4, 256) X(2, 256)
+
+size_t patch_batch_smem(int box_total, int mr_max, int B, int NT) {
+  const size_t s = batch_smem_t(B, NT, box_total, mr_max);
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
   if (s + 1024 > (size_t)optin) return 0;   // + the static shared arrays
   // the attribute is per instantiation, shared by every family: always the full opt-in size
   const int lim = optin - 1024;
-  cudaError_t e = cudaSuccess;
-  switch (B) {
-    case 2: e = cudaFuncSetAttribute(patch_batch_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
-    case 4: e = cudaFuncSetAttribute(patch_batch_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
-    default: e = cudaFuncSetAttribute(patch_batch_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim); break;
-  }
+  cudaError_t e = cudaErrorInvalidValue;
+#define RM_SET(BB, NN) \
+  if (B == BB && NT == NN) e = cudaFuncSetAttribute(patch_batch_kernel<BB, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  RM_BATCH_CFGS(RM_SET)
+#undef RM_SET
   return e == cudaSuccess ? s : 0;
 }
 
@@ -1235,7 +1230,7 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
   const int mr = (L.mr_max + 31) & ~31;
   a.gofs = a.boxd * L.batch;
   a.pofs = a.gofs + mr * L.batch;
-  a.tofs = a.pofs + std::max(BT, mr) * L.batch;
+  a.tofs = a.pofs + std::max(L.batch_nt, mr) * L.batch;
   a.box_bytes = 0;
   for (int sb = 0; sb < 3; ++sb) {
     a.boff[sb] = L.boff[sb];
@@ -1244,11 +1239,10 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
   for (int c = 0; c < L.cs.ncolors; ++c) {
     const int nb = L.bstart[c + 1] - L.bstart[c];
     if (nb <= 0) continue;
-    switch (L.batch) {
-      case 2: patch_batch_kernel<2><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
-      case 4: patch_batch_kernel<4><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
-      default: patch_batch_kernel<8><<<nb, BT, L.bsmem, st>>>(a, L.bstart[c]); break;
-    }
+#define RM_LAUNCH(BB, NN) \
+    if (L.batch == BB && L.batch_nt == NN) patch_batch_kernel<BB, NN><<<nb, NN, L.bsmem, st>>>(a, L.bstart[c]);
+    RM_BATCH_CFGS(RM_LAUNCH)
+#undef RM_LAUNCH
   }
   return cudaGetLastError();
 }
