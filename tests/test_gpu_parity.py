@@ -387,7 +387,10 @@ def test_slab_partition_two_contexts_hcurl_hdiv(dev, name, w):
             got = uo[l0 + lo_ * Lm:l0 + hi_ * Lm].cpu().numpy()
             want = ref[g0 + lo_ * Lm:g0 + hi_ * Lm].cpu().numpy()
             err = np.abs(got - want).max() / max(1.0, np.abs(want).max())
-            check(f"slab two-context {name} rank {g} comp", err, 1e-12)
+            # H(div): the partitioned and single contexts run different patch kernels (class-batched vs
+            # streamed, by family size), i.e. different summation orders on problems with
+            # kappa ~ 1e5..4e6 -- the DESIGN.md section 7 derived H(div) tolerance applies
+            check(f"slab two-context {name} rank {g} comp", err, hdiv_tol("2^3-p3") if w.space == 2 else 1e-12)
 
 
 @pytest.mark.gpu
