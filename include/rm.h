@@ -91,7 +91,14 @@ typedef struct {
   void *stream;              /* cudaStream_t                                                        */
   const void *nccl_id;       /* 128-byte ncclUniqueId or NULL (single GPU)                          */
   int32_t rank, nranks, device;
+  int32_t setup;             /* RM_SETUP_DEVICE (default): the numeric setup -- cell matrices (incl.  */
+                             /* the trilinear auxiliary operator), patch assembly, block elimination,*/
+                             /* dense Cholesky / ICC-SC with the G7 restart, stream packing -- runs  */
+                             /* on the GPU; RM_SETUP_HOST: the same factorization   */
+                             /* on the host (OpenMP).  The symbolic setup is host C++ in both.       */
 } rm_options;
+
+enum { RM_SETUP_HOST = 0, RM_SETUP_DEVICE = 1 };
 
 typedef struct {
   int64_t n_local;           /* DoFs in the local vectors (constrained included)                   */
@@ -114,6 +121,7 @@ typedef struct {
   int64_t coarse_ndof;       /* unconstrained DoFs of the coarse problem A_0 (0 without it)        */
   int32_t batched_families;  /* patch families solved by the class-batched kernel (RM_PATCH_STREAM) */
   int32_t batch_width;       /* patches per CTA of the widest batched family (0 if none)           */
+  int32_t setup_on_device;   /* 1 if the numeric setup ran on the GPU (options.setup)              */
 } rm_info;
 
 void rm_default_options(rm_options *opt);

@@ -24,6 +24,7 @@ RM_HGRAD, RM_HCURL, RM_HDIV = 0, 1, 2
 RM_PAFW, RM_PH, RM_SC_PAFW = 0, 1, 2
 RM_CHOL, RM_ICC_SC = 0, 1
 RM_ALL_ENTITIES, RM_INTERIOR_ONLY = 0, 1
+RM_SETUP_HOST, RM_SETUP_DEVICE = 0, 1
 RM_OK, RM_NOT_CONVERGED = 0, 1
 RM_NPHASE = 8   # entries of rm_timing_read (include/rm.h)
 STATUS = {0: "RM_OK", 1: "RM_NOT_CONVERGED", -1: "RM_EINVAL", -2: "RM_ENOMEM", -3: "RM_ENUMERIC",
@@ -45,7 +46,8 @@ class rm_options(ctypes.Structure):
     _fields_ = [("decomposition", ctypes.c_int32), ("factorization", ctypes.c_int32),
                 ("patch_entities", ctypes.c_int32), ("potential_shift", ctypes.c_double),
                 ("coarse", ctypes.c_int32), ("stream", ctypes.c_void_p), ("nccl_id", ctypes.c_void_p),
-                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("setup", ctypes.c_int32)]
 
 
 class rm_partition_info(ctypes.Structure):
@@ -75,7 +77,7 @@ class rm_info(ctypes.Structure):
                 ("factor_nnz", ctypes.c_int64), ("factor_nnz_primary", ctypes.c_int64),
                 ("factor_unique_bytes", ctypes.c_int64), ("comm_nranks", ctypes.c_int32), ("coarse", ctypes.c_int32),
                 ("coarse_ndof", ctypes.c_int64), ("batched_families", ctypes.c_int32),
-                ("batch_width", ctypes.c_int32)]
+                ("batch_width", ctypes.c_int32), ("setup_on_device", ctypes.c_int32)]
 
 
 def _load():
@@ -199,9 +201,11 @@ def rm_nccl_unique_id() -> bytes:
 
 def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposition=RM_PAFW,
              factorization=RM_CHOL, patch_entities=RM_ALL_ENTITIES, potential_shift=1e-3, stream=None,
-             device=0, rank=0, nranks=1, z_begin=0, z_end=None, nccl_id=None, coarse=0) -> RmContext:
+             device=0, rank=0, nranks=1, z_begin=0, z_end=None, nccl_id=None, coarse=0,
+             setup=None) -> RmContext:
     """coords / alpha / beta describe the GLOBAL mesh; with nranks > 1 the context holds the local
-    problem of the cell layers [z_begin, z_end) (rm_partition) and its vectors are local."""
+    problem of the cell layers [z_begin, z_end) (rm_partition) and its vectors are local.
+    setup: RM_SETUP_DEVICE (default: numeric setup on the GPU) or RM_SETUP_HOST."""
     alpha = np.ascontiguousarray(np.atleast_1d(np.asarray(alpha, dtype=np.float64)).ravel())
     beta = np.ascontiguousarray(np.atleast_1d(np.asarray(beta, dtype=np.float64)).ravel())
     mesh = rm_mesh(nx, ny, nz, None, z_begin, nz if z_end is None else z_end)
@@ -218,6 +222,8 @@ def rm_setup(nx, ny, nz, p, space, alpha, beta, gamma_d, coords=None, decomposit
     opt.patch_entities = patch_entities
     opt.potential_shift = potential_shift
     opt.coarse = int(coarse)
+    if setup is not None:
+        opt.setup = int(setup)
     sp = _stream_ptr(stream)
     opt.stream = ctypes.c_void_p(sp)
     opt.device = device

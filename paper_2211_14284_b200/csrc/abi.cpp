@@ -6,6 +6,7 @@
 #include <omp.h>
 #include <nccl.h>   // types and prototypes only: the library is dlopen'ed (rank > 1 only)
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -20,6 +21,7 @@
 
 #include "basis.hpp"
 #include "coarse.hpp"
+#include "dsetup.hpp"
 #include "kernels.cuh"
 #include "model.hpp"
 #include "patches.hpp"
@@ -150,6 +152,13 @@ struct DevFamily {
     CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
     return static_cast<T*>(d);
   }
+  template <class T>
+  T* alloc(size_t n) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed");
+    allocs.push_back(d);
+    return static_cast<T*>(d);
+  }
   void release() {
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
@@ -165,7 +174,7 @@ struct DevFamily {
 // (documented test knob, rm.h) keeps the persistent stream kernel.
 // pc / pv / pvn: per patch in colour-sorted order: class, host stream-block offset, device offset.
 void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>& pc, const std::vector<long long>& pv,
-                  const std::vector<long long>& pvn, size_t nblocks) {
+                  const std::vector<long long>& pvn, size_t nblocks, const double* hvals) {
   rm::PatchLaunch& Lh = F.launch;
   Lh.batch = 0;
   const size_t np = pc.size();
@@ -212,7 +221,7 @@ void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>
     const long long at = (long long)fin.size();
     fin.resize(fin.size() + (size_t)mr * mr, 0.0);
     double* S = fin.data() + at;
-    const double* blk = P.values.data() + hofs;
+    const double* blk = hvals + hofs;
     for (int pi = C.tile_p0; pi < C.tile_p1; ++pi) {   // half-stored lane-block tiles -> full matrix
       const rm::Piece& pcs = C.pieces[pi];
       if (pcs.kind != rm::PK_TILE) continue;
@@ -366,9 +375,16 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
   Lh.nsub = P.nsub;
   for (int sb = 0; sb < 3; ++sb) Lh.sub_comp[sb] = P.sub_comp[sb];
   if (!P.sc_nk.empty()) {
-    Lh.sc_dinv = F.upload(P.sc_dinv);
-    Lh.sc_c = P.sc_c.empty() ? nullptr : F.upload(P.sc_c);
-    Lh.sc_w = P.sc_w.empty() ? nullptr : F.upload(P.sc_w);
+    if (P.deferred) {   // filled by the device numeric setup below
+      const size_t ni = (size_t)(P.sp.p - 1) * (P.sp.p - 1) * (P.sp.p - 1), nc = P.sc_nk.size();
+      Lh.sc_dinv = F.alloc<double>(nc * ni);
+      Lh.sc_c = P.cartesian ? F.alloc<double>(nc * 6 * ni) : nullptr;
+      Lh.sc_w = P.cartesian ? nullptr : F.alloc<double>(nc * 3 * ni);
+    } else {
+      Lh.sc_dinv = F.upload(P.sc_dinv);
+      Lh.sc_c = P.sc_c.empty() ? nullptr : F.upload(P.sc_c);
+      Lh.sc_w = P.sc_w.empty() ? nullptr : F.upload(P.sc_w);
+    }
     for (size_t i = 0; i < 16 && i < P.sc_kd.size(); ++i) { Lh.sc_kd[i] = P.sc_kd[i]; Lh.sc_k0[i] = P.sc_k0[i]; Lh.sc_kp[i] = P.sc_kp[i]; }
     Lh.sc_nk = F.upload(P.sc_nk);
     Lh.sc_fb = F.upload(std::vector<double>(P.sc_nk.size() * 6 * (size_t)(P.sp.p - 1) * (P.sp.p - 1), 0.0));
@@ -432,11 +448,13 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     remap.reserve(2 * P.nfactors + 16);
     std::vector<long long> pvn(np);
     void* dv = nullptr;
-    if (!P.values.empty()) {
-      if (cudaMalloc(&dv, P.values.size() * sizeof(double)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed (patch factors)");
+    const int64_t nvalues = P.deferred ? P.nvalues : (int64_t)P.values.size();
+    if (nvalues > 0) {
+      if (cudaMalloc(&dv, nvalues * sizeof(double)) != cudaSuccess) throw RmError(RM_ENOMEM, "cudaMalloc failed (patch factors)");
       F.allocs.push_back(dv);
     }
     double* dvals = static_cast<double*>(dv);
+    std::vector<std::pair<long long, long long>> blocks_nv;   // distinct blocks: host offset, doubles
     std::vector<double> stage;
     const size_t chunk = (size_t)32 << 20;   // doubles per staging flush (256 MB)
     long long cur = 0, flushed = 0;
@@ -454,7 +472,8 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
         if (it == remap.end()) {
           const long long nv = P.classes[pc[q]].nvals;
           it = remap.emplace(pv[q], cur).first;
-          stage.insert(stage.end(), P.values.begin() + pv[q], P.values.begin() + pv[q] + nv);
+          blocks_nv.push_back({pv[q], nv});
+          if (!P.deferred) stage.insert(stage.end(), P.values.begin() + pv[q], P.values.begin() + pv[q] + nv);
           cur += nv;
           if (stage.size() >= chunk) flush();
         }
@@ -463,7 +482,33 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
     flush();
     Lh.pvals = F.upload(pvn);
     Lh.vals = dvals;
-    plan_batches(F, P, pc, pv, pvn, remap.size());
+    std::vector<double> hcopy;   // host copy of device-computed blocks at host offsets (batch planning)
+    const double* hvals = P.values.data();
+    if (P.deferred) {
+      // device-resident numeric setup: every distinct block computed on the GPU at its device offset
+      std::vector<long long> fdst(P.foff.size(), 0);
+      for (size_t f = 0; f < P.foff.size(); ++f) {
+        auto it = remap.find(P.foff[f]);
+        fdst[f] = it == remap.end() ? 0 : it->second;
+      }
+      double sg = 0.0;
+      try {
+        rm::device_numeric_setup(P, fdst, dvals, const_cast<double*>(Lh.sc_dinv), const_cast<double*>(Lh.sc_c), const_cast<double*>(Lh.sc_w),
+                                 nullptr, &sg);
+      } catch (const rm::NumericError& e) {
+        throw RmError(RM_ENUMERIC, e.what());
+      } catch (const std::runtime_error& e) {
+        throw RmError(RM_ECUDA, e.what());
+      }
+      F.sigma_max = sg;
+      if (remap.size() * 4 <= np) {   // few shared blocks: the class-batched plan reads them on the host
+        hcopy.assign(P.nvalues, 0.0);
+        for (const auto& b : blocks_nv)
+          CK(cudaMemcpy(hcopy.data() + b.first, dvals + remap[b.first], b.second * sizeof(double), cudaMemcpyDeviceToHost));
+        hvals = hcopy.data();
+      }
+    }
+    plan_batches(F, P, pc, pv, pvn, remap.size(), hvals);
     // per-CTA producer issue lists in consumption order (patch_solve.cu): sparse channel
     // fwd(0), then per i: fwd(i+1), final(i) unless dense tiles, bwd(i); tile channel tiles(i)
     std::vector<unsigned char*> dmeta(P.classes.size());
@@ -520,7 +565,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
   F.nnzL = P.nnzL_total;
   F.unique_bytes = P.unique_value_bytes;
   F.ncolors = P.ncolors;
-  F.sigma_max = P.sigma_max;
+  if (!P.deferred) F.sigma_max = P.sigma_max;
   F.present = true;
 }
 
@@ -531,6 +576,7 @@ struct rm_ctx {
   uint32_t gamma = 0;
   int decomposition = RM_PAFW;
   bool cartesian = true;
+  bool setup_device = false;   // numeric setup ran on the GPU (options.setup)
   rm::Space sp, spot;
   int64_t ndof = 0, npot = 0, nfree = 0;
   cudaStream_t st = nullptr;
@@ -661,6 +707,7 @@ void rm_default_options(rm_options* o) {
   o->patch_entities = RM_ALL_ENTITIES;
   o->potential_shift = 1e-3;   // reading G8: roundoff of the sweep grows like eps/eps_s
   o->nranks = 1;
+  o->setup = RM_SETUP_DEVICE;
 }
 
 const char* rm_last_error(void) { return g_err.c_str(); }
@@ -942,6 +989,8 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.cartesian = cart;
     in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
     in.zv_lo = part.v_lo; in.zv_hi = part.v_hi;   // owned vertex layers (all of them on one rank)
+    in.defer_numeric = o.setup == RM_SETUP_DEVICE;   // numeric factorization on the GPU (dsetup.cu)
+    c->setup_device = in.defer_numeric;
     {
       // edge / face stars: one family per orientation (window boxes ~2-4x smaller than the hull)
       const int no = (in.dim == 1 || in.dim == 2) && !rm::exp_env("RM_ONE_FAMILY") ? 3 : 1;
@@ -1113,6 +1162,7 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
         info->batch_width = std::max(info->batch_width, F.launch.batch);
       }
   info->setup_seconds = c->setup_seconds;
+  info->setup_on_device = c->setup_device ? 1 : 0;
   return RM_OK;
 }
 

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <tuple>
 
@@ -177,15 +179,24 @@ CellEntries cartesian_cell_entries(const CellOperator& op, const Space& sp, doub
 }
 
 // ------------------------------------------------------------------ auxiliary operator k=0
-void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out, double* w_int) {
+// P_K = G0^T diag0 G0 + sum_m (G1 D)_m^T diag1_m (G1 D)_m (eq:sum-factorization_approx P:732-739):
+// every entry is a fixed linear combination of the four sum-factorised diagonals, so the
+// geometry enters only through aux_cell_diagonals and the entry map is built once per p.
+namespace {
+std::mutex aux_mu;
+std::map<int, std::unique_ptr<AuxTables>> aux_cache;
+
+AuxTables* make_aux_tables(int p) {
+  auto T = std::make_unique<AuxTables>();
   const Basis1D& b = basis(p);
   const int n = p + 1;
-  const int nq = (3 * (p + 1) + 1) / 2;   // reading G1/G2
-  std::vector<double> xq, wq;
-  gll_rule(nq, xq, wq);
+  T->p = p;
+  T->nq = (3 * (p + 1) + 1) / 2;   // reading G1/G2
+  const int nq = T->nq;
+  gll_rule(nq, T->xq, T->wq);
   std::vector<double> s, ds, r;
-  b.tab_s(xq, s, ds);
-  b.tab_r(xq, r);
+  b.tab_s(T->xq, s, ds);
+  b.tab_r(T->xq, r);
   // broken P basis s-bar = s G^{-1}: only columns 0, p change (2x2 inverse of G_GG)
   const double g00 = b.G[0], g0p = b.G[p], gp0 = b.G[p * n], gpp = b.G[p * n + p];
   const double det = g00 * gpp - g0p * gp0;
@@ -196,6 +207,73 @@ void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, C
     sb[q * n + 0] = s0 * i00 + sp_ * ip0;
     sb[q * n + p] = s0 * i0p + sp_ * ipp;
   }
+  T->sb2.resize(sb.size());
+  for (size_t i = 0; i < sb.size(); ++i) T->sb2[i] = sb[i] * sb[i];
+  T->r2.resize(r.size());
+  for (size_t i = 0; i < r.size(); ++i) T->r2[i] = r[i] * r[i];
+  T->off[0] = 0;
+  T->off[1] = n * n * n;
+  T->off[2] = T->off[1] + n * n * p;
+  T->off[3] = T->off[2] + n * n * p;
+  T->ndiag = T->off[3] + n * n * p;
+  // sparse rows of G (n x n) and D-hat (p x n), structural pattern only
+  std::vector<std::vector<std::pair<int, double>>> Gr(n), Dr(p);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      bool pat = (i == j) || ((i == 0 || i == p) && (j == 0 || j == p));
+      if (pat) Gr[i].push_back({j, b.G[i * n + j]});
+    }
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < n; ++j)
+      if (j == 0 || j == p || j == i) Dr[i].push_back({j, b.D[i * n + j]});
+  struct Tm { int g; double a, c; };
+  std::map<std::pair<int, int>, std::vector<Tm>> acc;
+  auto idx3 = [&](int l, int j, int i) { return (l * n + j) * n + i; };
+  // G0^T diag0 G0 : broken dof (l,j,i) row of G0 = G[l,:] x G[j,:] x G[i,:]
+  for (int l = 0; l < n; ++l)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const int g = idx3(l, j, i);
+        std::vector<std::pair<int, double>> rowv;
+        for (auto& zl : Gr[l]) for (auto& yj : Gr[j]) for (auto& xi : Gr[i])
+          rowv.push_back({idx3(zl.first, yj.first, xi.first), zl.second * yj.second * xi.second});
+        for (auto& a : rowv) for (auto& c : rowv) acc[{a.first, c.first}].push_back({g, a.second, c.second});
+      }
+  // (G1 D)^T diag1 (G1 D): comp x row = G[l,:] x G[j,:] x D[i,:], etc.
+  for (int m = 0; m < 3; ++m) {
+    const int nx_ = (m == 0) ? p : n, ny_ = (m == 1) ? p : n, nz_ = (m == 2) ? p : n;
+    for (int l = 0; l < nz_; ++l)
+      for (int j = 0; j < ny_; ++j)
+        for (int i = 0; i < nx_; ++i) {
+          const int g = T->off[1 + m] + (l * ny_ + j) * nx_ + i;
+          const auto& Rz = (m == 2) ? Dr[l] : Gr[l];
+          const auto& Ry = (m == 1) ? Dr[j] : Gr[j];
+          const auto& Rx = (m == 0) ? Dr[i] : Gr[i];
+          std::vector<std::pair<int, double>> rowv;
+          for (auto& zl : Rz) for (auto& yj : Ry) for (auto& xi : Rx)
+            rowv.push_back({idx3(zl.first, yj.first, xi.first), zl.second * yj.second * xi.second});
+          for (auto& a : rowv) for (auto& c : rowv) acc[{a.first, c.first}].push_back({g, a.second, c.second});
+        }
+  }
+  T->tptr.push_back(0);
+  for (auto& kv : acc) {
+    T->row.push_back(kv.first.first); T->col.push_back(kv.first.second);
+    for (const Tm& t : kv.second) { T->tg.push_back(t.g); T->ta.push_back(t.a); T->tc.push_back(t.c); }
+    T->tptr.push_back((int)T->tg.size());
+  }
+  return T.release();
+}
+}  // namespace
+
+const AuxTables& aux_tables(int p) {
+  std::lock_guard<std::mutex> lk(aux_mu);
+  auto it = aux_cache.find(p);
+  if (it == aux_cache.end()) it = aux_cache.emplace(p, std::unique_ptr<AuxTables>(make_aux_tables(p))).first;
+  return *it->second;
+}
+
+void aux_cell_diagonals(const AuxTables& T, const double Xc[8][3], double alpha, double beta, double* diag) {
+  const int p = T.p, n = p + 1, nq = T.nq;
   // geometry at the nq^3 points: W0 = w detJ beta, W1[m] = w detJ alpha (J^{-1}J^{-T})_mm
   const size_t NQ = (size_t)nq * nq * nq;
   std::vector<double> W0(NQ), W1[3];
@@ -203,7 +281,7 @@ void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, C
   for (int qz = 0; qz < nq; ++qz)
     for (int qy = 0; qy < nq; ++qy)
       for (int qx = 0; qx < nq; ++qx) {
-        const double t[3] = {xq[qx], xq[qy], xq[qz]};
+        const double t[3] = {T.xq[qx], T.xq[qy], T.xq[qz]};
         double phi[3][2], dphi[3][2];
         for (int d = 0; d < 3; ++d) { phi[d][0] = 0.5 * (1 - t[d]); phi[d][1] = 0.5 * (1 + t[d]); dphi[d][0] = -0.5; dphi[d][1] = 0.5; }
         double J[3][3] = {{0}};
@@ -229,7 +307,7 @@ void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, C
         Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / dJ;
         Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / dJ;
         const size_t q = ((size_t)qz * nq + qy) * nq + qx;
-        const double w = wq[qx] * wq[qy] * wq[qz] * dJ;
+        const double w = T.wq[qx] * T.wq[qy] * T.wq[qz] * dJ;
         W0[q] = w * beta;
         for (int m = 0; m < 3; ++m) {
           double jj = Ji[m][0] * Ji[m][0] + Ji[m][1] * Ji[m][1] + Ji[m][2] * Ji[m][2];   // (J^{-1}J^{-T})_mm
@@ -238,88 +316,67 @@ void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, C
       }
   // sum-factorised diagonals: diag[l,j,i] = sum_q Tz^2[qz,l] Ty^2[qy,j] Tx^2[qx,i] W[q]
   auto contract = [&](const std::vector<double>& W, const std::vector<double>& Tx, int nx_,
-                      const std::vector<double>& Ty, int ny_, const std::vector<double>& Tz, int nz_) {
-    std::vector<double> a((size_t)nq * nq * nx_, 0.0), bb((size_t)nq * ny_ * nx_, 0.0), c((size_t)nz_ * ny_ * nx_, 0.0);
+                      const std::vector<double>& Ty, int ny_, const std::vector<double>& Tz, int nz_, double* c) {
+    std::vector<double> a((size_t)nq * nq * nx_, 0.0), bb((size_t)nq * ny_ * nx_, 0.0);
     for (int qz = 0; qz < nq; ++qz)
       for (int qy = 0; qy < nq; ++qy)
         for (int i = 0; i < nx_; ++i) {
           double acc = 0;
-          for (int qx = 0; qx < nq; ++qx) { double t = Tx[qx * nx_ + i]; acc += t * t * W[((size_t)qz * nq + qy) * nq + qx]; }
+          for (int qx = 0; qx < nq; ++qx) acc += Tx[qx * nx_ + i] * W[((size_t)qz * nq + qy) * nq + qx];
           a[((size_t)qz * nq + qy) * nx_ + i] = acc;
         }
     for (int qz = 0; qz < nq; ++qz)
       for (int j = 0; j < ny_; ++j)
         for (int i = 0; i < nx_; ++i) {
           double acc = 0;
-          for (int qy = 0; qy < nq; ++qy) { double t = Ty[qy * ny_ + j]; acc += t * t * a[((size_t)qz * nq + qy) * nx_ + i]; }
+          for (int qy = 0; qy < nq; ++qy) acc += Ty[qy * ny_ + j] * a[((size_t)qz * nq + qy) * nx_ + i];
           bb[((size_t)qz * ny_ + j) * nx_ + i] = acc;
         }
     for (int l = 0; l < nz_; ++l)
       for (int j = 0; j < ny_; ++j)
         for (int i = 0; i < nx_; ++i) {
           double acc = 0;
-          for (int qz = 0; qz < nq; ++qz) { double t = Tz[qz * nz_ + l]; acc += t * t * bb[((size_t)qz * ny_ + j) * nx_ + i]; }
+          for (int qz = 0; qz < nq; ++qz) acc += Tz[qz * nz_ + l] * bb[((size_t)qz * ny_ + j) * nx_ + i];
           c[((size_t)l * ny_ + j) * nx_ + i] = acc;
         }
-    return c;
   };
-  std::vector<double> d0 = contract(W0, sb, n, sb, n, sb, n);
-  std::vector<double> d1[3] = {contract(W1[0], r, p, sb, n, sb, n), contract(W1[1], sb, n, r, p, sb, n),
-                               contract(W1[2], sb, n, sb, n, r, p)};
-  if (w_int) {
-    const int pm = p - 1, ni = pm * pm * pm;
-    for (int k = 1; k < p; ++k)
-      for (int j = 1; j < p; ++j)
-        for (int i = 1; i < p; ++i) {
-          const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
-          w_int[0 * ni + I] = d1[0][((size_t)k * n + j) * p + i];   // x: (z P, y P, x DP)
-          w_int[1 * ni + I] = d1[1][((size_t)k * p + j) * n + i];   // y: (z P, y DP, x P)
-          w_int[2 * ni + I] = d1[2][((size_t)k * n + j) * n + i];   // z: (z DP, y P, x P)
-        }
+  contract(W0, T.sb2, n, T.sb2, n, T.sb2, n, diag + T.off[0]);
+  contract(W1[0], T.r2, p, T.sb2, n, T.sb2, n, diag + T.off[1]);
+  contract(W1[1], T.sb2, n, T.r2, p, T.sb2, n, diag + T.off[2]);
+  contract(W1[2], T.sb2, n, T.sb2, n, T.r2, p, diag + T.off[3]);
+}
+
+void aux_entries_from_diagonals(const AuxTables& T, const double* diag, double* vals) {
+  const int ne = (int)T.row.size();
+  for (int t = 0; t < ne; ++t) {
+    double acc = 0.0;
+    for (int k = T.tptr[t]; k < T.tptr[t + 1]; ++k) acc += T.ta[k] * diag[T.tg[k]] * T.tc[k];
+    vals[t] = acc;
   }
-  // sparse rows of G (n x n) and D-hat (p x n), structural pattern only
-  std::vector<std::vector<std::pair<int, double>>> Gr(n), Dr(p);
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) {
-      bool pat = (i == j) || ((i == 0 || i == p) && (j == 0 || j == p));
-      if (pat) Gr[i].push_back({j, b.G[i * n + j]});
-    }
-  for (int i = 0; i < p; ++i)
-    for (int j = 0; j < n; ++j)
-      if (j == 0 || j == p || j == i) Dr[i].push_back({j, b.D[i * n + j]});
-  std::map<std::pair<int, int>, double> acc;
-  auto idx3 = [&](int l, int j, int i) { return (l * n + j) * n + i; };
-  // G0^T diag0 G0 : broken dof (l,j,i) row of G0 = G[l,:] x G[j,:] x G[i,:]
-  for (int l = 0; l < n; ++l)
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i < n; ++i) {
-        double dv = d0[idx3(l, j, i)];
-        std::vector<std::pair<int, double>> rowv;
-        for (auto& zl : Gr[l]) for (auto& yj : Gr[j]) for (auto& xi : Gr[i])
-          rowv.push_back({idx3(zl.first, yj.first, xi.first), zl.second * yj.second * xi.second});
-        for (auto& a : rowv) for (auto& c : rowv) acc[{a.first, c.first}] += a.second * dv * c.second;
+}
+
+void aux_interior_weights(const AuxTables& T, const double* diag, double* w_int) {
+  const int p = T.p, n = p + 1, pm = p - 1, ni = pm * pm * pm;
+  const double* d1[3] = {diag + T.off[1], diag + T.off[2], diag + T.off[3]};
+  for (int k = 1; k < p; ++k)
+    for (int j = 1; j < p; ++j)
+      for (int i = 1; i < p; ++i) {
+        const int I = ((k - 1) * pm + (j - 1)) * pm + (i - 1);
+        w_int[0 * ni + I] = d1[0][((size_t)k * n + j) * p + i];   // x: (z P, y P, x DP)
+        w_int[1 * ni + I] = d1[1][((size_t)k * p + j) * n + i];   // y: (z P, y DP, x P)
+        w_int[2 * ni + I] = d1[2][((size_t)k * n + j) * n + i];   // z: (z DP, y P, x P)
       }
-  // (G1 D)^T diag1 (G1 D): comp x row = G[l,:] x G[j,:] x D[i,:], etc.
-  for (int m = 0; m < 3; ++m) {
-    const int nx_ = (m == 0) ? p : n, ny_ = (m == 1) ? p : n, nz_ = (m == 2) ? p : n;
-    for (int l = 0; l < nz_; ++l)
-      for (int j = 0; j < ny_; ++j)
-        for (int i = 0; i < nx_; ++i) {
-          double dv = d1[m][((size_t)l * ny_ + j) * nx_ + i];
-          const auto& Rz = (m == 2) ? Dr[l] : Gr[l];
-          const auto& Ry = (m == 1) ? Dr[j] : Gr[j];
-          const auto& Rx = (m == 0) ? Dr[i] : Gr[i];
-          std::vector<std::pair<int, double>> rowv;
-          for (auto& zl : Rz) for (auto& yj : Ry) for (auto& xi : Rx)
-            rowv.push_back({idx3(zl.first, yj.first, xi.first), zl.second * yj.second * xi.second});
-          for (auto& a : rowv) for (auto& c : rowv) acc[{a.first, c.first}] += a.second * dv * c.second;
-        }
-  }
-  out.row.clear(); out.col.clear(); out.kval.clear(); out.mval.clear();
-  for (auto& kv : acc) {
-    out.row.push_back(kv.first.first); out.col.push_back(kv.first.second);
-    out.kval.push_back(kv.second); out.mval.push_back(0.0);
-  }
+}
+
+void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out, double* w_int) {
+  const AuxTables& T = aux_tables(p);
+  std::vector<double> diag(T.ndiag);
+  aux_cell_diagonals(T, Xc, alpha, beta, diag.data());
+  if (w_int) aux_interior_weights(T, diag.data(), w_int);
+  out.row = T.row; out.col = T.col;
+  out.kval.resize(T.row.size());
+  aux_entries_from_diagonals(T, diag.data(), out.kval.data());
+  out.mval.assign(T.row.size(), 0.0);
 }
 
 }  // namespace rm

@@ -82,4 +82,21 @@ CellEntries cartesian_cell_entries(const CellOperator& op, const Space& sp, doub
 void aux_cell_entries(int p, const double Xc[8][3], double alpha, double beta, CellEntries& out,
                       double* w_int = nullptr);
 
+// The same operator split into its geometry-dependent and geometry-independent parts (cached per
+// p): four sum-factorised diagonals per cell (d0: (l,j,i) n^3; d1_x: n*n*p, d1_y: n*p*n,
+// d1_z: p*n*n, concatenated at off[0..3]) and the entry map: entry t (in (row, col) order) =
+// sum over its terms k of (ta[k] * diag[tg[k]]) * tc[k].  aux_cell_entries = diagonals + map.
+struct AuxTables {
+  int p = 0, nq = 0;
+  std::vector<double> xq, wq;      // GLL rule, nq points (reading G1/G2)
+  std::vector<double> sb2, r2;     // squared broken P basis (nq x n) and DP basis (nq x p)
+  int off[4] = {0, 0, 0, 0}, ndiag = 0;
+  std::vector<int> row, col, tptr, tg;
+  std::vector<double> ta, tc;
+};
+const AuxTables& aux_tables(int p);
+void aux_cell_diagonals(const AuxTables& T, const double Xc[8][3], double alpha, double beta, double* diag);
+void aux_entries_from_diagonals(const AuxTables& T, const double* diag, double* vals);
+void aux_interior_weights(const AuxTables& T, const double* diag, double* w_int);
+
 }  // namespace rm

@@ -1174,6 +1174,174 @@ struct Builder {
   }
 };
 
+// ------------------------------------------------------------------ device numeric program
+// (patches.hpp NumProg; executed by dsetup.cu).  Mirrors factor_patch value by value.
+void build_numeric_program(const ClassProgram& C, const std::vector<int>& cell_rows,
+                           const std::vector<int>& cell_cols, NumProg& o) {
+  o = NumProg();
+  const int n = C.n;
+  o.n = n;
+  o.nnzP = (int)C.pcol.size();
+  o.final_kind = C.final_kind;
+  o.ncanon = C.nvals_canon;
+  o.nvals = C.nvals;
+  o.vofs_final = C.vofs_final;
+  if (n == 0) return;
+  const Level& L0 = C.lev[0];
+  const int nI = L0.e1, nG = n - nI;
+  o.nI = nI; o.nG = nG; o.m = C.m;
+  auto csr = [&](int i, int j) -> int {
+    const int* b0 = &C.pcol[C.prow[i]];
+    const int* b1 = &C.pcol[C.prow[i + 1]];
+    const int* it = std::lower_bound(b0, b1, j);
+    return (it != b1 && *it == j) ? (int)(it - C.pcol.data()) : -1;
+  };
+  // canonical index of element (row r, column col) of a sliced block
+  auto sliced_at = [&](const Sliced& S, int r, int col) -> int {
+    const int rr = r - S.r0, sl = rr / 32, l = rr % 32;
+    const auto& rc = S.rowcols[rr];
+    const int kk = (int)(std::lower_bound(rc.begin(), rc.end(), col) - rc.begin());
+    if (kk >= (int)rc.size() || rc[kk] != col) throw std::runtime_error("numeric program: sliced entry missing");
+    return (int)(S.vofs + S.slice_off[sl] + (int64_t)kk * 32 + l);
+  };
+  // assembly terms in factor_patch's order: slot, then cell entry
+  const int ne = (int)cell_rows.size();
+  std::vector<std::vector<int>> terms(o.nnzP);
+  for (size_t slot = 0; slot < C.slot_map.size(); ++slot) {
+    const std::vector<int>& mp = C.slot_map[slot];
+    for (int t = 0; t < ne; ++t) {
+      const int i = mp[cell_rows[t]], j = mp[cell_cols[t]];
+      if (i < 0 || j < 0) continue;
+      const int e = csr(i, j);
+      if (e < 0) throw std::runtime_error("numeric program: cell entry outside the patch pattern");
+      terms[e].push_back((int)slot * ne + t);
+    }
+  }
+  o.asm_ptr.assign(o.nnzP + 1, 0);
+  for (int e = 0; e < o.nnzP; ++e) {
+    o.asm_ptr[e + 1] = o.asm_ptr[e] + (int)terms[e].size();
+    o.asm_src.insert(o.asm_src.end(), terms[e].begin(), terms[e].end());
+  }
+  o.pdiag.resize(n);
+  for (int i = 0; i < n; ++i) o.pdiag[i] = csr(i, i);
+  // level 0: blocks, neighbour records (r, P(r, b_j), canon W^(b_j, r)), W = P_RE copies
+  o.nb0 = (int)L0.blocks.size();
+  o.bs0 = L0.blk.bs;
+  o.blk0_vofs = L0.blk.vofs;
+  std::vector<std::vector<int>> nbs(o.nb0);
+  for (int bi = 0; bi < o.nb0; ++bi) {
+    const auto& b = L0.blocks[bi];
+    const int bs = (int)b.size();
+    int rec[12];
+    std::fill(rec, rec + 12, -1);
+    rec[0] = bs;
+    for (int j = 0; j < bs; ++j) rec[1 + j] = b[j];
+    for (int i = 0, k = 0; i < 3; ++i)
+      for (int j = 0; j <= i; ++j, ++k) rec[4 + k] = (i < bs && j < bs) ? csr(b[i], b[j]) : -1;
+    std::vector<int> nb;
+    for (int q : b)
+      for (int t = C.prow[q]; t < C.prow[q + 1]; ++t) if (C.pcol[t] >= nI) nb.push_back(C.pcol[t]);
+    std::sort(nb.begin(), nb.end()); nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+    rec[10] = (int)(o.nbr.size() / 7);
+    for (int r : nb) {
+      o.nbr.push_back(r - nI);
+      for (int j = 0; j < 3; ++j) o.nbr.push_back(j < bs ? csr(r, b[j]) : -1);
+      for (int j = 0; j < 3; ++j) o.nbr.push_back(j < bs ? sliced_at(L0.wt, b[j], r) : -1);
+    }
+    rec[11] = (int)(o.nbr.size() / 7);
+    o.b0.insert(o.b0.end(), rec, rec + 12);
+    nbs[bi] = nb;
+  }
+  for (int rr = 0; rr < L0.w.nrows; ++rr)
+    for (int q : L0.w.rowcols[rr]) {
+      const int r = L0.w.r0 + rr;
+      o.w0.push_back(sliced_at(L0.w, r, q));
+      o.w0.push_back(csr(r, q));
+    }
+  // S targets (lower): P_GG entries and the level-0 contributions M_a . M_c, in block order
+  const bool icc = C.final_kind == FINAL_ICC;
+  if (icc && C.m != nG) throw std::runtime_error("numeric program: ICC final block is not the whole interface");
+  std::map<std::pair<int, int>, int> tid;
+  std::vector<int> tcsr;
+  std::vector<std::vector<int>> tsrc;
+  auto target = [&](int a, int c) -> int {
+    auto it = tid.find({a, c});
+    if (it != tid.end()) return it->second;
+    const int id = (int)tcsr.size();
+    tid.emplace(std::make_pair(a, c), id);
+    tcsr.push_back(csr(nI + a, nI + c));
+    tsrc.emplace_back();
+    return id;
+  };
+  for (int r = nI; r < n; ++r)
+    for (int t = C.prow[r]; t < C.prow[r + 1]; ++t)
+      if (C.pcol[t] >= nI && C.pcol[t] <= r) target(r - nI, C.pcol[t] - nI);
+  for (int bi = 0; bi < o.nb0; ++bi) {
+    const int r0 = o.b0[12 * bi + 10];
+    const auto& nb = nbs[bi];
+    for (size_t i = 0; i < nb.size(); ++i)
+      for (size_t c = 0; c <= i; ++c) {
+        const int id = target(nb[i] - nI, nb[c] - nI);
+        tsrc[id].push_back(r0 + (int)i);
+        tsrc[id].push_back(r0 + (int)c);
+      }
+  }
+  std::vector<int> icc_at;
+  if (icc) {   // ICC entry of (row a, column c) in the final pattern
+    o.icc_rowptr = C.icc_rowptr; o.icc_col = C.icc_col;
+    o.icc_lptr = C.icc_level_ptr; o.icc_lrows = C.icc_level_rows;
+    o.icct_src = C.icct_src;
+  }
+  o.st_ptr.push_back(0);
+  for (auto& kv : tid) {
+    const int a = kv.first.first, c = kv.first.second, id = kv.second;
+    int idx;
+    if (icc) {
+      const int* b0 = &C.icc_col[C.icc_rowptr[a]];
+      const int* b1 = &C.icc_col[C.icc_rowptr[a + 1]];
+      const int* it = std::lower_bound(b0, b1, c);
+      if (it == b1 || *it != c) throw std::runtime_error("numeric program: Schur entry outside the ICC pattern");
+      idx = (int)(it - C.icc_col.data());
+    } else {
+      idx = a * nG + c;
+    }
+    o.st_idx.push_back(idx);
+    o.st_csr.push_back(tcsr[id]);
+    o.st_src.insert(o.st_src.end(), tsrc[id].begin(), tsrc[id].end());
+    o.st_ptr.push_back((int)o.st_src.size() / 2);
+  }
+  // exact levels >= 1 read off the dense Cholesky factor of S (position order)
+  if (!icc)
+    for (size_t l = 1; l < C.lev.size(); ++l) {
+      const Level& L = C.lev[l];
+      for (int i = 0; i < L.blk.nblk; ++i) {
+        const int q = L.blocks[i][0] - nI;
+        o.rec.insert(o.rec.end(), {(int)(L.blk.vofs + i), 0, q, q});
+      }
+      for (int rr = 0; rr < L.w.nrows; ++rr)
+        for (int q : L.w.rowcols[rr]) {
+          const int r = L.w.r0 + rr;
+          o.rec.insert(o.rec.end(), {sliced_at(L.w, r, q), 1, r - nI, q - nI});
+        }
+      for (int qq = 0; qq < L.wt.nrows; ++qq)
+        for (int r : L.wt.rowcols[qq]) {
+          const int q = L.wt.r0 + qq;
+          o.rec.insert(o.rec.end(), {sliced_at(L.wt, q, r), 2, r - nI, q - nI});
+        }
+    }
+  // canonical -> stream map: pack canon[c] = 2c + 1 (odd integers; halved entries are not integers)
+  std::vector<double> canon(C.nvals_canon), out(C.nvals);
+  for (int64_t c = 0; c < C.nvals_canon; ++c) canon[c] = 2.0 * (double)c + 1.0;
+  pack_stream(C, canon.data(), out.data());
+  o.smap.resize(C.nvals);
+  for (int64_t k = 0; k < C.nvals; ++k) {
+    const double x = out[k];
+    if (x == 0.0) o.smap[k] = -1;
+    else if (x == std::floor(x)) o.smap[k] = (int)((x - 1.0) / 2.0);
+    else o.smap[k] = -2 - (int)(x - 0.5);
+  }
+}
+
 std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   auto fam = std::make_unique<PatchFamily>();
   Builder B(in, fam.get());
@@ -1334,8 +1502,55 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   std::mutex emu;
   double smax = 0.0;
   const int64_t nf = (int64_t)foff.size();
+  fam->nvalues = total;
+  if (in.defer_numeric) {   // device-resident numeric setup: record the inputs, factor nothing here
+    fam->deferred = true;
+    fam->values.clear();
+    fam->values.shrink_to_fit();
+    fam->fclass.resize(nf);
+    fam->foff = foff;
+    fam->fcells.assign((size_t)nf * kMaxSlots, -1);
+    for (int64_t f = 0; f < nf; ++f) {
+      const size_t t = frep[f];
+      const Entity& e = ents[keep[t]];
+      fam->fclass[f] = fam->pclass[t];
+      std::vector<int> cr[3];
+      for (int d = 0; d < 3; ++d) {
+        const DirSpec& ds = e.s[d];
+        if (ds.kind == 1) cr[d] = {ds.v};
+        else { if (ds.v - 1 >= 0) cr[d].push_back(ds.v - 1); if (ds.v < B.sp.n[d]) cr[d].push_back(ds.v); }
+      }
+      int slot = 0;
+      for (int cz : cr[2]) for (int cy : cr[1]) for (int cx : cr[0])
+        fam->fcells[(size_t)f * kMaxSlots + slot++] = (cz * B.sp.n[1] + cy) * B.sp.n[0] + cx;
+    }
+    fam->cell_rows = B.cell_rows; fam->cell_cols = B.cell_cols;
+    fam->cartesian = in.cartesian;
+    const int64_t ncell = (int64_t)B.sp.n[0] * B.sp.n[1] * B.sp.n[2];
+    fam->cell_alpha.resize(ncell); fam->cell_beta.resize(ncell);
+    std::map<std::tuple<double, double, double>, int> sets;
+    if (in.cartesian) fam->cell_set.resize(ncell);
+    for (int64_t K = 0; K < ncell; ++K) {
+      const int cx = (int)(K % B.sp.n[0]), cy = (int)((K / B.sp.n[0]) % B.sp.n[1]), cz = (int)(K / ((int64_t)B.sp.n[0] * B.sp.n[1]));
+      fam->cell_alpha[K] = B.coef(in.alpha, in.n_alpha, cx, cy, cz);
+      fam->cell_beta[K] = B.coef(in.beta, in.n_beta, cx, cy, cz);
+      if (in.cartesian) {
+        auto key = std::make_tuple(in.hx[cx], in.hy[cy], in.hz[cz]);
+        auto it = sets.find(key);
+        if (it == sets.end()) {
+          it = sets.emplace(key, (int)sets.size()).first;
+          const CellEntries& E = B.cart_entries(in.hx[cx], in.hy[cy], in.hz[cz]);
+          if (E.row != B.cell_rows || E.col != B.cell_cols) throw std::runtime_error("cell pattern depends on the cell size");
+          fam->cset_k.insert(fam->cset_k.end(), E.kval.begin(), E.kval.end());
+          fam->cset_m.insert(fam->cset_m.end(), E.mval.begin(), E.mval.end());
+        }
+        fam->cell_set[K] = it->second;
+      }
+    }
+    if (!in.cartesian) fam->coords.assign(in.coords, in.coords + (B.sp.n[0] + 1) * (B.sp.n[1] + 1) * (B.sp.n[2] + 1) * 3);
+  }
 #pragma omp parallel for schedule(dynamic, 4) reduction(max : smax)
-  for (int64_t f = 0; f < nf; ++f) {
+  for (int64_t f = 0; f < (in.defer_numeric ? 0 : nf); ++f) {
     size_t t = frep[f];
     const Entity& e = ents[keep[t]];
     const ClassProgram& C = fam->classes[fam->pclass[t]];
@@ -1380,8 +1595,11 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
     }
     fam->sc_nk.assign(ncell, 0);
     std::string sc_err;
+    if (in.defer_numeric) {   // sc_dinv / sc_c / sc_w are computed on the device (sizes kept)
+      fam->sc_dinv.clear(); fam->sc_c.clear(); fam->sc_w.clear();
+    }
 #pragma omp parallel for schedule(dynamic, 8)
-    for (int64_t K = 0; K < ncell; ++K) {
+    for (int64_t K = 0; K < (in.defer_numeric ? 0 : ncell); ++K) {
       const int cx = (int)(K % sp.n[0]), cy = (int)((K / sp.n[0]) % sp.n[1]), cz = (int)(K / ((int64_t)sp.n[0] * sp.n[1]));
       const double a = B.coef(in.alpha, in.n_alpha, cx, cy, cz), b = B.coef(in.beta, in.n_beta, cx, cy, cz);
       CellEntries ce;

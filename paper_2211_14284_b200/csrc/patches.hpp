@@ -194,7 +194,47 @@ struct PatchFamily {
   int64_t nnzL_total = 0;         // sum over patches of ClassProgram::nnzL (algorithmic factor entries)
   int64_t unique_value_bytes = 0; // bytes of the distinct value blocks (what HBM holds)
   std::string err;
+  // ---- device-resident numeric setup (SetupInput::defer_numeric): the host
+  // builds the symbolic programs only; values / sc_dinv / sc_c / sc_w are left empty and computed
+  // on the GPU (dsetup.cu) from these inputs
+  bool deferred = false;
+  int64_t nvalues = 0;                    // doubles of all distinct value blocks (host offsets)
+  std::vector<int> fclass;                // per distinct block: class of its representative patch
+  std::vector<int64_t> foff;              // per distinct block: host value offset
+  std::vector<int> fcells;                // per distinct block: kMaxSlots star cells in slot order (-1 unused)
+  std::vector<int> cell_rows, cell_cols;  // cell-matrix pattern (entry order of CellEntries)
+  bool cartesian = true;
+  std::vector<double> cset_k, cset_m;     // Cartesian: per distinct (hx, hy, hz) the K / M entries
+  std::vector<int> cell_set;              // Cartesian: per cell its entry set
+  std::vector<double> cell_alpha, cell_beta;   // per cell
+  std::vector<double> coords;             // trilinear: (nz+1)(ny+1)(nx+1)*3 vertex coordinates
 };
+
+constexpr int kMaxSlots = 8;   // star cells per patch (vertex stars)
+
+// Device numeric program of one class (host arrays; dsetup.cu uploads them).  Every value of the
+// class's canonical block is produced by the same block elimination as the host factorization
+// (factor_patch): assembly of P on the class pattern, level-0 pivot blocks, the interface Schur
+// complement S, then either a dense Cholesky S = L L^T in position order (levels >= 1 read off L:
+// pivots 1/L_qq, W = L_rq L_qq, W^ = L_rq / L_qq; the final block's inverse from L_FF) or ICC(0) on
+// the final pattern; finally the canonical -> stream permutation (stream_map).
+struct NumProg {
+  int n = 0, nI = 0, nG = 0, m = 0, nnzP = 0, final_kind = 0;
+  int nb0 = 0, bs0 = 1;                   // level-0 blocks and their padded size
+  int64_t blk0_vofs = 0, vofs_final = 0, ncanon = 0, nvals = 0;
+  std::vector<int> asm_ptr, asm_src;      // per P entry: terms slot * ne + t (host summation order)
+  std::vector<int> pdiag;                 // per position: CSR index of the diagonal
+  std::vector<int> b0;                    // per block 12 ints: bs, mem[3], lcsr[6] (lower, row-major), nb0, nb1
+  std::vector<int> nbr;                   // per neighbour record 7 ints: r - nI, csr P(r, b_j) [3], canon W^ (b_j, r) [3]
+  std::vector<int> w0;                    // pairs: canon index, CSR index (level-0 W = P_RE)
+  std::vector<int> st_idx, st_csr, st_ptr, st_src;   // S targets: index (dense a*nG+c | ICC entry), P entry, pairs of records
+  std::vector<int> rec;                   // exact levels >= 1: (canon, op, a, b), op 0 = 1/L_bb, 1 = L_ab L_bb, 2 = L_ab / L_bb
+  std::vector<int> icc_rowptr, icc_col, icc_lptr, icc_lrows, icct_src;
+  std::vector<int> smap;                  // per stream slot: canon c (>= 0), -1 zero, -2 - c (0.5 * canon c)
+};
+// cell_rows / cell_cols: the cell-matrix pattern; ne = its size
+void build_numeric_program(const ClassProgram& C, const std::vector<int>& cell_rows,
+                           const std::vector<int>& cell_cols, NumProg& out);
 
 struct SetupInput {
   int k, p, n[3];
@@ -210,6 +250,7 @@ struct SetupInput {
   const double* hx; const double* hy; const double* hz;   // per-direction cell sizes (cartesian)
   int zv_lo = 0, zv_hi = 1 << 30;   // vertex stars kept: z vertex layers [zv_lo, zv_hi) (z-slab ownership)
   int orient = -1;                  // edge / face stars: keep one orientation (edge direction / face normal), -1 = all
+  bool defer_numeric = false;       // device-resident numeric setup (PatchFamily::deferred)
   bool sc_decomposition = false;    // SC-PAFW (eq:sc-asm-afw, k = 0): interface corrections from the patches, cell
                                     // interiors once afterwards (c_I = A_II^-1 (r_I - A_IG c_G), n_K = 1)
 };

@@ -523,6 +523,215 @@ int emu_family_breakdown(int k, int p, int nx, int dim, int orient, long long* o
   return 0;
 }
 
+// Host re-enactment of the DEVICE numeric setup program (patches.hpp NumProg, executed by
+// dsetup.cu factor_kernel): evaluates every value block from the program's assembly lists,
+// level-0 records, Schur targets, a dense Cholesky of S, the level recipes, the final inverse /
+// ICC(0) and the stream map, and compares with the host factorization (factor_patch) of the same
+// family.  Returns the largest |difference| / max|value| over all blocks in *rel (-1 on error).
+static void numprog_eval(const NumProg& g, const PatchFamily& F, int f, const std::vector<double>& cent_all,
+                         int ne, double* out) {
+  const int* cells = F.fcells.data() + (size_t)f * kMaxSlots;
+  std::vector<double> Pv(g.nnzP), C(g.ncanon, 0.0), M(3 * (g.nbr.size() / 7), 0.0);
+  for (int e = 0; e < g.nnzP; ++e) {
+    double v = 0.0;
+    for (int k = g.asm_ptr[e]; k < g.asm_ptr[e + 1]; ++k) {
+      const int src = g.asm_src[k], sl = src / ne, t = src % ne, cell = cells[sl];
+      if (F.cartesian) {
+        const size_t so = (size_t)F.cell_set[cell] * ne + t;
+        v += F.cell_alpha[cell] * F.cset_k[so] + F.cell_beta[cell] * F.cset_m[so];
+      } else {
+        v += cent_all[(size_t)cell * ne + t];
+      }
+    }
+    Pv[e] = v;
+  }
+  auto pv = [&](int x) { return x < 0 ? 0.0 : Pv[x]; };
+  for (int bi = 0; bi < g.nb0; ++bi) {
+    const int* rc = &g.b0[12 * bi];
+    const int bs = rc[0];
+    double Lm[3][3] = {{0}};
+    for (int j = 0; j < bs; ++j) {
+      double d = pv(rc[4 + j * (j + 1) / 2 + j]);
+      for (int k = 0; k < j; ++k) d -= Lm[j][k] * Lm[j][k];
+      if (!(d > 0)) throw std::runtime_error("numprog: level-0 breakdown");
+      Lm[j][j] = std::sqrt(d);
+      for (int i = j + 1; i < bs; ++i) {
+        double s = pv(rc[4 + i * (i + 1) / 2 + j]);
+        for (int k = 0; k < j; ++k) s -= Lm[i][k] * Lm[j][k];
+        Lm[i][j] = s / Lm[j][j];
+      }
+    }
+    for (int r = 0, slot = 0; r < g.bs0; ++r)
+      for (int c = 0; c <= r; ++c, ++slot) {
+        double v = r < bs ? Lm[r][c] : 0.0;
+        if (r == c) v = r < bs ? 1.0 / v : 0.0;
+        C[g.blk0_vofs + (int64_t)slot * g.nb0 + bi] = v;
+      }
+    for (int k = rc[10]; k < rc[11]; ++k) {
+      const int* nr = &g.nbr[7 * k];
+      double y[3] = {0, 0, 0}, z[3] = {0, 0, 0};
+      for (int j = 0; j < bs; ++j) {
+        double s = pv(nr[1 + j]);
+        for (int kk = 0; kk < j; ++kk) s -= Lm[j][kk] * y[kk];
+        y[j] = s / Lm[j][j];
+      }
+      for (int j = 0; j < 3; ++j) M[3 * k + j] = y[j];
+      for (int j = bs - 1; j >= 0; --j) {
+        double s = y[j];
+        for (int kk = j + 1; kk < bs; ++kk) s -= Lm[kk][j] * z[kk];
+        z[j] = s / Lm[j][j];
+        C[nr[4 + j]] = z[j];
+      }
+    }
+  }
+  for (size_t i = 0; i < g.w0.size() / 2; ++i) C[g.w0[2 * i]] = pv(g.w0[2 * i + 1]);
+  const bool icc = g.final_kind == FINAL_ICC;
+  const int nG = g.nG;
+  std::vector<double> S(icc ? (g.icc_rowptr.empty() ? 0 : g.icc_rowptr.back()) : (size_t)nG * nG, 0.0);
+  for (size_t q = 0; q < g.st_idx.size(); ++q) {
+    double v = pv(g.st_csr[q]);
+    for (int k = g.st_ptr[q]; k < g.st_ptr[q + 1]; ++k) {
+      const double* a = &M[3 * g.st_src[2 * k]];
+      const double* c = &M[3 * g.st_src[2 * k + 1]];
+      v -= a[0] * c[0] + a[1] * c[1] + a[2] * c[2];
+    }
+    S[g.st_idx[q]] = v;
+  }
+  if (!icc) {
+    for (int j = 0; j < nG; ++j) {   // dense Cholesky, lower, row-major
+      double d = S[(size_t)j * nG + j];
+      for (int k = 0; k < j; ++k) d -= S[(size_t)j * nG + k] * S[(size_t)j * nG + k];
+      if (!(d > 0)) throw std::runtime_error("numprog: interface breakdown");
+      d = std::sqrt(d);
+      S[(size_t)j * nG + j] = d;
+      for (int i = j + 1; i < nG; ++i) {
+        double s = S[(size_t)i * nG + j];
+        for (int k = 0; k < j; ++k) s -= S[(size_t)i * nG + k] * S[(size_t)j * nG + k];
+        S[(size_t)i * nG + j] = s / d;
+      }
+    }
+    for (size_t i = 0; i < g.rec.size() / 4; ++i) {
+      const int* r = &g.rec[4 * i];
+      const double lab = S[(size_t)r[2] * nG + r[3]], lbb = S[(size_t)r[3] * nG + r[3]];
+      C[r[0]] = r[1] == 0 ? 1.0 / lbb : (r[1] == 1 ? lab * lbb : lab / lbb);
+    }
+    const int m = g.m, g0 = nG - m;
+    if (m > 0) {
+      std::vector<double> Y((size_t)m * m, 0.0), Fi((size_t)m * m, 0.0);
+      auto L = [&](int i, int j) { return S[(size_t)(g0 + i) * nG + g0 + j]; };
+      for (int c = 0; c < m; ++c)
+        for (int i = c; i < m; ++i) {
+          double s = (i == c) ? 1.0 : 0.0;
+          for (int k = c; k < i; ++k) s -= L(i, k) * Y[(size_t)k * m + c];
+          Y[(size_t)i * m + c] = s / L(i, i);
+        }
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j <= i; ++j) {
+          double s = 0.0;
+          for (int k = i; k < m; ++k) s += Y[(size_t)k * m + i] * Y[(size_t)k * m + j];
+          Fi[(size_t)i * m + j] = Fi[(size_t)j * m + i] = s;
+        }
+      const int T = (m + 31) / 32;
+      for (int I = 0; I < T; ++I)
+        for (int J = 0; J <= I; ++J)
+          for (int r = 0; r < 32; ++r)
+            for (int c = 0; c < 32; ++c) {
+              const int i = 32 * I + r, j = 32 * J + c;
+              C[g.vofs_final + (int64_t)(I * (I + 1) / 2 + J) * 1024 + r * 32 + ((c + r) & 31)] =
+                  (i < m && j < m) ? Fi[(size_t)i * m + j] : 0.0;
+            }
+    }
+  } else {
+    const int nnz = (int)S.size();
+    for (size_t lv = 0; lv + 1 < g.icc_lptr.size(); ++lv)
+      for (int q = g.icc_lptr[lv]; q < g.icc_lptr[lv + 1]; ++q) {
+        const int ra = g.icc_lrows[q], a0 = g.icc_rowptr[ra], a1 = g.icc_rowptr[ra + 1];
+        for (int t = a0; t < a1; ++t) {
+          const int b = g.icc_col[t];
+          double s = S[t];
+          int ia = a0, ib = g.icc_rowptr[b];
+          const int eb = g.icc_rowptr[b + 1] - 1;
+          while (ia < t && ib < eb) {
+            const int ca = g.icc_col[ia], cb = g.icc_col[ib];
+            if (ca == cb) { s -= S[ia] * S[ib]; ++ia; ++ib; }
+            else if (ca < cb) ++ia; else ++ib;
+          }
+          if (b == ra) {
+            if (!(s > 0)) throw std::runtime_error("numprog: icc breakdown");
+            S[t] = std::sqrt(s);
+          } else {
+            S[t] = s / S[g.icc_rowptr[b + 1] - 1];
+          }
+        }
+      }
+    double* o = C.data() + g.vofs_final;
+    for (int ra = 0; ra < g.m; ++ra)
+      for (int t = g.icc_rowptr[ra]; t < g.icc_rowptr[ra + 1]; ++t) o[t] = (t == g.icc_rowptr[ra + 1] - 1) ? 1.0 / S[t] : S[t];
+    for (int t = 0; t < nnz; ++t) o[nnz + t] = o[g.icct_src[t]];
+  }
+  for (int64_t k = 0; k < g.nvals; ++k) {
+    const int c = g.smap[k];
+    out[k] = c >= 0 ? C[c] : (c == -1 ? 0.0 : 0.5 * C[-2 - c]);
+  }
+}
+
+int emu_numeric_program_check(int k, int p, int nx, int ny, int nz, unsigned gamma, const double* alpha, long long na,
+                              const double* beta, long long nb, const double* coords, int dim, int fact, double* rel,
+                              char* err, int errlen) {
+  try {
+    std::vector<double> h[3];
+    const int n[3] = {nx, ny, nz};
+    for (int d = 0; d < 3; ++d) h[d].assign(n[d], 1.0 / n[d]);
+    SetupInput in{};
+    in.k = k; in.p = p; in.n[0] = nx; in.n[1] = ny; in.n[2] = nz; in.gamma_d = gamma;
+    in.coords = coords; in.alpha = alpha; in.beta = beta; in.n_alpha = na; in.n_beta = nb;
+    in.dim = dim; in.factorization = fact; in.cartesian = (coords == nullptr);
+    in.hx = h[0].data(); in.hy = h[1].data(); in.hz = h[2].data();
+    auto Fh = build_patch_family(in);
+    in.defer_numeric = true;
+    auto Fd = build_patch_family(in);
+    if (Fd->foff.size() != (size_t)Fh->nfactors) throw std::runtime_error("block count differs");
+    const int ne = (int)Fd->cell_rows.size();
+    std::vector<double> cent;
+    if (!Fd->cartesian) {   // per-cell entries through the AuxTables split (what the device computes)
+      const AuxTables& T = aux_tables(p);
+      const int64_t ncell = (int64_t)nx * ny * nz;
+      cent.resize((size_t)ncell * ne);
+      std::vector<double> dg(T.ndiag);
+      for (int64_t K = 0; K < ncell; ++K) {
+        const int cx = (int)(K % nx), cy = (int)((K / nx) % ny), cz = (int)(K / ((int64_t)nx * ny));
+        double Xc[8][3];
+        for (int v = 0; v < 8; ++v)
+          for (int i = 0; i < 3; ++i)
+            Xc[v][i] = coords[(((int64_t)(cz + (v >> 2)) * (ny + 1) + (cy + ((v >> 1) & 1))) * (nx + 1) + (cx + (v & 1))) * 3 + i];
+        aux_cell_diagonals(T, Xc, Fd->cell_alpha[K], Fd->cell_beta[K], dg.data());
+        aux_entries_from_diagonals(T, dg.data(), &cent[(size_t)K * ne]);
+      }
+    }
+    std::vector<NumProg> progs(Fd->classes.size());
+    std::vector<char> built(Fd->classes.size(), 0);
+    double md = 0.0, mv = 0.0;
+    for (size_t f = 0; f < Fd->foff.size(); ++f) {
+      const int c = Fd->fclass[f];
+      if (!built[c]) { build_numeric_program(Fd->classes[c], Fd->cell_rows, Fd->cell_cols, progs[c]); built[c] = 1; }
+      const NumProg& g = progs[c];
+      std::vector<double> out(g.nvals);
+      numprog_eval(g, *Fd, (int)f, cent, ne, out.data());
+      const double* ref = Fh->values.data() + Fd->foff[f];
+      for (int64_t q = 0; q < g.nvals; ++q) {
+        md = std::max(md, std::fabs(out[q] - ref[q]));
+        mv = std::max(mv, std::fabs(ref[q]));
+      }
+    }
+    *rel = mv > 0 ? md / mv : md;
+    return 0;
+  } catch (const std::exception& e) {
+    snprintf(err, errlen, "%s", e.what());
+    *rel = -1;
+    return 1;
+  }
+}
+
 // 1D basis tables of the product (for cross-checks against the oracle's basis)
 int emu_basis(int p, double* S, double* lam, double* B, double* A, double* D, double* G) {
   const Basis1D& b = basis(p);

@@ -479,3 +479,34 @@ def test_coarse_p1_one_iteration(dev, cfg):
     x = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
     it, relres, ok = rmb.rm_pcg(ctx, torch.tensor(f, device=dev), x, 1e-8, 50)
     assert ok and it == 1, (it, relres)
+
+
+# ------------------------------------------------------------------ device-resident setup (f4)
+DSETUP_CASES = [("cfg1", ri.CONFIGS[1], 1e-13), ("cfg2-3^3-p7", ri.CONFIGS[2].with_mesh(3), 1e-13),
+                ("cfg3-2^3-p6", ri.CONFIGS[3].with_mesh(2), 1e-12), ("cfg4-2^3-p3", ri.CONFIGS[4].with_mesh(2).with_p(3), 1e-11),
+                ("cfg5-2^3-p15", ri.CONFIGS[5].with_mesh(2), 1e-13), ("cfg5-3^3-p5", ri.CONFIGS[5].with_mesh(3).with_p(5), 1e-13),
+                ("cfg3-pafw-2^3-p3", dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), decomposition="pafw"), 1e-12),
+                ("cfg3-iccsc-3^3-p3", dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(3), factorization="icc_sc"), 1e-12),
+                ("cfg5-sc-3^3-p3", dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"), 1e-13)]
+
+
+@pytest.mark.parametrize("name,w,tol", DSETUP_CASES, ids=[c[0] for c in DSETUP_CASES])
+def test_device_setup_matches_host_setup_and_oracle(dev, name, w, tol):
+    """the numeric setup on the GPU (dsetup.cu) -- cell matrices incl. the trilinear
+    auxiliary operator, patch assembly, block elimination, dense Cholesky / ICC-SC, static-
+    condensation cell data, stream packing -- gives the sweep of the host setup to rounding (the
+    interface elimination runs as one dense Cholesky; differences ~ kappa * eps) and the oracle's
+    sweep within the north-star tolerance."""
+    import paper_2211_14284_b200 as rmb
+    cd = gu.setup_product(w, setup=rmb.RM_SETUP_DEVICE)
+    ch = gu.setup_product(w, setup=rmb.RM_SETUP_HOST)
+    assert cd.info()["setup_on_device"] == 1 and ch.info()["setup_on_device"] == 0
+    f, u = vecs(w, cd)
+    ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
+    od, oh = torch.empty_like(ut), torch.empty_like(ut)
+    rmb.rm_relax(cd, ft, ut, od, 1.0)
+    rmb.rm_relax(ch, ft, ut, oh, 1.0)
+    check(f"dsetup {name} device vs host setup", rel(od.cpu().numpy(), oh.cpu().numpy()), tol)
+    pb = gu.setup_oracle(w)
+    otol = hdiv_tol("2^3-p3") if w.space == 2 else 1e-11
+    check(f"dsetup {name} device setup vs oracle", rel(od.cpu().numpy(), pb.relax(f, u)), otol)
