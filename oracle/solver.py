@@ -8,6 +8,9 @@
             B = the discretization of a^k(d phi, d psi) = the (k-1)-form operator with
             (alpha', beta') = (beta, 0) (k=1) or (beta, eps_s beta) (k=2, remark P:916-927, G8)
       u_out = u + omega c                                   (reading G9)
+  SC-PAFW / SC-PH (eq:sc-asm-afw / eq:sc-asm-hiptmair, eq:schur): c = R_I^T A_II^{-1} R_I r +
+      R_G^T S^{-1}_{PAFW|PH} R_G r with patches on interface DoFs only (precondition_sc,
+      precondition_sc_ph).
   For the auxiliary-operator variant the patch matrices come from P instead of A.
   With `coarse`, PCG's preconditioner is the hybrid V(1,1) cycle with the p = 1 coarse level
   (oracle/coarse.py, reading G20).
@@ -24,7 +27,7 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
-from .fem import Space, assemble, assemble_aux, apply_matfree, global_derivative
+from .fem import P_FAM, Space, assemble, assemble_aux, apply_matfree, global_derivative
 from .patches import DenseCholeskyPatch, ICCSCPatch, all_patches, icc_masked
 
 
@@ -55,7 +58,7 @@ class Problem:
     alpha: np.ndarray        # (nz, ny, nx)
     beta: np.ndarray
     gamma_d: int
-    decomposition: str = "pafw"      # "pafw" | "ph" | "sc-pafw" (k = 0, eq:sc-asm-afw)
+    decomposition: str = "pafw"      # "pafw" | "ph" | "sc-pafw" (k = 0, eq:sc-asm-afw) | "sc-ph" (k >= 1, eq:sc-asm-hiptmair)
     factorization: str = "chol"      # "chol" | "icc_sc"
     interior_only: bool = False
     matfree: bool = False            # apply A cell by cell (large p) instead of via CSR
@@ -74,6 +77,7 @@ class Problem:
         self._pot = None
         self._coarse = None
         self._sc = None
+        self._scph = None
 
     # ---------------------------------------------------------------- operator
     @property
@@ -99,7 +103,7 @@ class Problem:
 
     # ---------------------------------------------------------------- patches
     def _patch_dim(self):
-        return self.k if self.decomposition == "ph" else 0
+        return self.k if self.decomposition in ("ph", "sc-ph") else 0
 
     def patch_solvers(self):
         if self._patches is not None:
@@ -131,7 +135,7 @@ class Problem:
         patch solvers on the stars of (k-1)-entities."""
         if self._pot is not None:
             return self._pot
-        assert self.decomposition == "ph" and self.k >= 1
+        assert self.decomposition in ("ph", "sc-ph") and self.k >= 1
         kp = self.k - 1
         D = global_derivative(kp, self.p, self.nx, self.ny, self.nz)
         pspace = Space(kp, self.p, self.nx, self.ny, self.nz)
@@ -146,6 +150,7 @@ class Problem:
         shift = self.potential_shift if self.k == 2 else 0.0
         B = assemble(pspace, self.X, self.beta, shift * self.beta)
         B = (Pf @ B @ Pf).tocsr()
+        self._pot_B = B
         pats = all_patches(pspace, kp, pcon, self.interior_only)
         sol = []
         if self.factorization == "icc_sc" and kp == 0:
@@ -222,11 +227,78 @@ class Problem:
         c[I] = (r[I] - (At[I] @ cG)) / dI
         return np.where(self.free, c, 0.0)
 
+    # ------------------------------------------------------------ statically condensed (SC-PH)
+    def sc_ph_data(self):
+        """SC-PH (eq:sc-ph, eq:schur, eq:sc-asm-hiptmair; k = 1, 2, exact factors): the interior set I
+        (cell-interior DoFs) and interface G of V^k with A_II^{-1} (block diagonal, blocks
+        <= 3x3, remark P:1061-1066) and S = A_GG - A_GI A_II^{-1} A_IG (eq:LDU); per k-star the
+        interface DoFs and a Cholesky factor of S_i = R~_i S R~_i^T; D~ = D_GG, the derivative
+        tabulated between the interface DoFs of V^{k-1} and V^k; and per (k-1)-star a factor of
+        B~_j = R~_j S_B R~_j^T, S_B the interface Schur complement of the potential matrix B (the
+        discretization of a^k(d phi, d psi) = PH's B)."""
+        if self._scph is not None:
+            return self._scph
+        import scipy.sparse.linalg as spla
+        assert self.k >= 1 and self.factorization == "chol", "SC-PH: k = 1, 2 with exact factors"
+        A = self.A
+        I = np.flatnonzero(self.free & interior_mask(self.space))
+        G = np.flatnonzero(self.free & ~interior_mask(self.space))
+        AIIinv = spla.inv(A[I][:, I].tocsc()).tocsr()
+        S = (A[G][:, G] - A[G][:, I] @ AIIinv @ A[I][:, G]).tocsr()
+        gpos = np.full(self.space.ndof, -1)
+        gpos[G] = np.arange(len(G))
+        prim = []
+        for ent, g, grp in all_patches(self.space, self.k, self.constrained, self.interior_only):
+            loc = gpos[g[grp != 0]]
+            if len(loc):
+                prim.append((loc, DenseCholeskyPatch(S[loc][:, loc].toarray())))
+        D, pcon, _ = self.potential()
+        B = self._pot_B
+        pspace = Space(self.k - 1, self.p, self.nx, self.ny, self.nz)
+        Ib = np.flatnonzero(~pcon & interior_mask(pspace))
+        Gb = np.flatnonzero(~pcon & ~interior_mask(pspace))
+        BIIinv = spla.inv(B[Ib][:, Ib].tocsc()).tocsr()
+        SB = (B[Gb][:, Gb] - B[Gb][:, Ib] @ BIIinv @ B[Ib][:, Gb]).tocsr()
+        bpos = np.full(pspace.ndof, -1)
+        bpos[Gb] = np.arange(len(Gb))
+        pot = []
+        for ent, g, grp in all_patches(pspace, self.k - 1, pcon, self.interior_only):
+            loc = bpos[g[grp != 0]]
+            if len(loc):
+                pot.append((loc, DenseCholeskyPatch(SB[loc][:, loc].toarray())))
+        Dt = D[G][:, Gb].tocsr()
+        self._scph = (A, I, G, AIIinv, S, prim, Dt, pot)
+        return self._scph
+
+    def precondition_sc_ph(self, r, potential_stage=True):
+        """c = R_I^T A_II^{-1} R_I r + R_G^T S_PH^{-1} R_G r (eq:schur, eq:sc-asm-hiptmair without the
+        coarse term), S_PH^{-1} = sum_i R~_i^T S_i^{-1} R~_i + D~ (sum_j R~_j^T B~_j^{-1} R~_j) D~^T,
+        R_G = [-A_GI A_II^{-1}, I]."""
+        A, I, G, AIIinv, S, prim, Dt, pot = self.sc_ph_data()
+        r = np.where(self.free, r, 0.0)
+        yI = AIIinv @ r[I]
+        rG = r[G] - A[G][:, I] @ yI
+        cG = np.zeros(len(G))
+        for loc, P_ in prim:
+            cG[loc] += P_.solve(rG[loc])
+        if potential_stage:
+            t = Dt.T @ rG
+            s_ = np.zeros(Dt.shape[1])
+            for loc, P_ in pot:
+                s_[loc] += P_.solve(t[loc])
+            cG += Dt @ s_
+        c = np.zeros_like(r)
+        c[G] = cG
+        c[I] = yI - AIIinv @ (A[I][:, G] @ cG)
+        return np.where(self.free, c, 0.0)
+
     # ---------------------------------------------------------------- sweep
     def precondition(self, r):
         """c = P^{-1} r (the additive Schwarz sum), r zero on constrained DoFs."""
         if self.decomposition == "sc-pafw":
             return self.precondition_sc(r)
+        if self.decomposition == "sc-ph":
+            return self.precondition_sc_ph(r)
         c = np.zeros_like(r)
         for g, S in self.patch_solvers():
             c[g] += S.solve(r[g])
@@ -276,6 +348,23 @@ class Problem:
             pdir = z + (rz_new / rz) * pdir
             rz = rz_new
         return x, maxit, rel
+
+
+def interior_mask(space: Space) -> np.ndarray:
+    """Cell-interior DoFs of a space (I = E^d): every P-family index off the cell
+    boundaries (index % p != 0); DP-family indices are interior to their cell."""
+    p = space.p
+    out = np.zeros(space.ndof, dtype=bool)
+    off = space.offsets()
+    for m, fam in enumerate(space.fams):
+        Lz, Ly, Lx = space.comp_shape(m)
+        iz, iy, ix = np.meshgrid(np.arange(Lz), np.arange(Ly), np.arange(Lx), indexing="ij")
+        ok = np.ones((Lz, Ly, Lx), dtype=bool)
+        for idx, f in zip((ix, iy, iz), fam):
+            if f == P_FAM:
+                ok &= idx % p != 0
+        out[off[m]:off[m + 1]] = ok.ravel()
+    return out
 
 
 def sampled_relax(space: Space, X, alpha, beta, gamma_d, f, u, rows, omega=1.0):
