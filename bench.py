@@ -289,7 +289,11 @@ def measure(w, cfg, args, world, rank, local, torch, dist, rmb, with_e2e=True):
                               else f"replicas x{world}") if world > 1 else "single",
               "l2": "inputs larger than L2 (patch factors %.1f GB streamed per sweep, %.2f GB distinct)"
                     % (8 * info["factor_nnz"] / 1e9, info["factor_unique_bytes"] / 1e9),
-              "setup_s": setup_s, "patches": info["n_patches"] + info["n_patches_potential"],
+              "setup_s": setup_s,
+              "setup": {"numeric_on_device": bool(info["setup_on_device"]),
+                        "host_patch_families_s": info["setup_host_family_seconds"],
+                        "device_numeric_s": info["setup_device_numeric_seconds"]},
+              "patches": info["n_patches"] + info["n_patches_potential"],
               "factor_blocks": info["n_factor_blocks"]}
     res = {"value": value, "ms_per_step": ms, "config": config, "roofline": roof, "e2e": e2e, "clocks": clocks,
            "gpu_launches": int(sum(launches[:4]))}

@@ -63,7 +63,12 @@ typedef enum {
 /* decomposition: vertex stars | k-stars + potential | statically condensed vertex stars (SC-PAFW,
  * eq:sc-pafw / eq:sc-asm-afw, H(grad) only: interface corrections from the vertex-star Schur
  * complements S_v, cell interiors once, c_I = A_II^-1 (r_I - A_IG c_G)) */
-enum { RM_PAFW = 0, RM_PH = 1, RM_SC_PAFW = 2 };
+enum { RM_PAFW = 0, RM_PH = 1, RM_SC_PAFW = 2, RM_SC_PH = 3 };
+/* RM_SC_PH (eq:sc-ph / eq:sc-asm-hiptmair, k = 1, 2, Cartesian cells, exact factors, single rank,
+ * one level): c = R_I^T A_II^-1 R_I r + R_G^T S_PH^-1 R_G r with S_PH^-1 = sum over k-stars of
+ * S_i^-1 on their interface DoFs + D~ (sum over (k-1)-stars of B~_j^-1) D~^T, D~ = D_GG; the star
+ * solves are the PH patch programs run on interface-only input with their interior corrections
+ * dropped (eq:LDU), A_II^-1 by the <= 3x3 cell-interior blocks (remark P:1061-1066). */
 enum { RM_CHOL = 0, RM_ICC_SC = 1 };                   /* patch factorization */
 enum { RM_ALL_ENTITIES = 0, RM_INTERIOR_ONLY = 1 };    /* patch_entities (interior-only = test mode) */
 
@@ -122,6 +127,9 @@ typedef struct {
   int32_t batched_families;  /* patch families solved by the class-batched kernel (RM_PATCH_STREAM) */
   int32_t batch_width;       /* patches per CTA of the widest batched family (0 if none)           */
   int32_t setup_on_device;   /* 1 if the numeric setup ran on the GPU (options.setup)              */
+  double setup_host_family_seconds;     /* host patch-family builds (symbolic programs; with        */
+                                        /* RM_SETUP_HOST also the numeric factorization)            */
+  double setup_device_numeric_seconds;  /* GPU numeric setup (RM_SETUP_DEVICE), incl. its uploads  */
 } rm_info;
 
 void rm_default_options(rm_options *opt);

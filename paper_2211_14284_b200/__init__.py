@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librm.so")
 
 RM_HGRAD, RM_HCURL, RM_HDIV = 0, 1, 2
-RM_PAFW, RM_PH, RM_SC_PAFW = 0, 1, 2
+RM_PAFW, RM_PH, RM_SC_PAFW, RM_SC_PH = 0, 1, 2, 3
 RM_CHOL, RM_ICC_SC = 0, 1
 RM_ALL_ENTITIES, RM_INTERIOR_ONLY = 0, 1
 RM_SETUP_HOST, RM_SETUP_DEVICE = 0, 1
@@ -77,7 +77,8 @@ class rm_info(ctypes.Structure):
                 ("factor_nnz", ctypes.c_int64), ("factor_nnz_primary", ctypes.c_int64),
                 ("factor_unique_bytes", ctypes.c_int64), ("comm_nranks", ctypes.c_int32), ("coarse", ctypes.c_int32),
                 ("coarse_ndof", ctypes.c_int64), ("batched_families", ctypes.c_int32),
-                ("batch_width", ctypes.c_int32), ("setup_on_device", ctypes.c_int32)]
+                ("batch_width", ctypes.c_int32), ("setup_on_device", ctypes.c_int32),
+                ("setup_host_family_seconds", ctypes.c_double), ("setup_device_numeric_seconds", ctypes.c_double)]
 
 
 def _load():

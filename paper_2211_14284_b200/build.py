@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CXX_SRC = ["basis.cpp", "model.cpp", "patches.cpp", "coarse.cpp", "abi.cpp"]
-CU_SRC = ["kernels.cu", "apply.cu", "apply_kform.cu", "apply_tri.cu", "patch_solve.cu", "coarse.cu", "dsetup.cu"]
+CU_SRC = ["kernels.cu", "apply.cu", "apply_kform.cu", "apply_tri.cu", "patch_solve.cu", "coarse.cu", "dsetup.cu", "sc_ph.cu"]
 
 
 def _headers():

@@ -12,7 +12,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -141,6 +144,7 @@ struct DevFamily {
   int64_t nnzL = 0, unique_bytes = 0;   // algorithmic factor entries (sum over patches), distinct block bytes
   int ncolors = 0;
   double sigma_max = 0.0;
+  double numeric_s = 0.0;          // seconds of the numeric setup (device or host) of this family
   bool present = false;
 
   template <class T>
@@ -492,6 +496,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
         fdst[f] = it == remap.end() ? 0 : it->second;
       }
       double sg = 0.0;
+      const auto t0 = std::chrono::steady_clock::now();
       try {
         rm::device_numeric_setup(P, fdst, dvals, const_cast<double*>(Lh.sc_dinv), const_cast<double*>(Lh.sc_c), const_cast<double*>(Lh.sc_w),
                                  nullptr, &sg);
@@ -501,6 +506,7 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
         throw RmError(RM_ECUDA, e.what());
       }
       F.sigma_max = sg;
+      F.numeric_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       if (remap.size() * 4 <= np) {   // few shared blocks: the class-batched plan reads them on the host
         hcopy.assign(P.nvalues, 0.0);
         for (const auto& b : blocks_nv)
@@ -577,6 +583,7 @@ struct rm_ctx {
   int decomposition = RM_PAFW;
   bool cartesian = true;
   bool setup_device = false;   // numeric setup ran on the GPU (options.setup)
+  double setup_family_s = 0.0;  // host build_patch_family (symbolic; + numeric with RM_SETUP_HOST)
   rm::Space sp, spot;
   int64_t ndof = 0, npot = 0, nfree = 0;
   cudaStream_t st = nullptr;
@@ -613,6 +620,12 @@ struct rm_ctx {
   std::unique_ptr<rm::CoarseFactor> coarse;
   rm::CoarseLaunch cl{};
   double *d_vz = nullptr, *d_vt = nullptr;   // cycle temporaries (fine size)
+  // SC-PH (sc_ph.cu): layout, cell-interior blocks, temporaries y = A_II^-1 r_I, w, R_G r, c_G, z
+  rm::ScPhParams scph{};
+  int* d_scph_set = nullptr;
+  int* d_scph_mem = nullptr;
+  double *d_scph_K = nullptr, *d_scph_M = nullptr;
+  double *d_sy = nullptr, *d_sw = nullptr, *d_srg = nullptr, *d_scg = nullptr, *d_sz = nullptr;
   double smoother_omega = 1.0;
 
   double* dalloc(size_t n) {
@@ -697,6 +710,99 @@ void check_cuda_status() { CK(cudaGetLastError()); }
 rm_status fail(const RmError& e) { g_err = e.what(); return e.st; }
 
 }  // namespace
+
+// SC-PH cell-interior blocks (remark P:1061-1066: <= 3x3 on Cartesian cells): from the cell
+// operator's entries, per distinct cell size (hx, hy, hz); members as cell-local codes
+void setup_scph(rm_ctx* c, const std::vector<double>* h) {
+  const rm::Space& sp = c->sp;
+  const int p = c->p;
+  rm::ScPhParams& P = c->scph;
+  std::memset(&P, 0, sizeof P);
+  P.p = p; P.ncomp = sp.ncomp;
+  for (int d = 0; d < 3; ++d) P.n[d] = c->n[d];
+  for (int m = 0; m < sp.ncomp; ++m) {
+    for (int d = 0; d < 3; ++d) { P.fam[m][d] = sp.fam[m][d] == rm::FAM_P ? 0 : 1; P.len[m][d] = sp.len(m, d); }
+    P.off[m] = sp.offset(m);
+  }
+  for (int m = sp.ncomp; m <= 3; ++m) P.off[m] = sp.ndof();
+  // cell-local DoFs (component-major, z, y, x), interior flags and codes
+  std::vector<int> code, interior;
+  for (int m = 0; m < sp.ncomp; ++m)
+    for (int cc = 0; cc < sp.lsize(m, 2); ++cc)
+      for (int b = 0; b < sp.lsize(m, 1); ++b)
+        for (int a = 0; a < sp.lsize(m, 0); ++a) {
+          const int idx[3] = {a, b, cc};
+          bool in = true;
+          for (int d = 0; d < 3; ++d)
+            if (sp.fam[m][d] == rm::FAM_P && (idx[d] == 0 || idx[d] == p)) in = false;
+          code.push_back(m << 24 | cc << 16 | b << 8 | a);
+          interior.push_back(in);
+        }
+  const rm::CellOperator op = rm::build_cell_operator(c->k, p);
+  std::map<std::tuple<double, double, double>, int> sets;
+  std::vector<int> cset((size_t)c->n[0] * c->n[1] * c->n[2]);
+  std::vector<rm::CellEntries> ents;
+  for (size_t K = 0; K < cset.size(); ++K) {
+    const int cx = (int)(K % c->n[0]), cy = (int)((K / c->n[0]) % c->n[1]), cz = (int)(K / ((size_t)c->n[0] * c->n[1]));
+    auto key = std::make_tuple(h[0][cx], h[1][cy], h[2][cz]);
+    auto it = sets.find(key);
+    if (it == sets.end()) {
+      it = sets.emplace(key, (int)ents.size()).first;
+      ents.push_back(rm::cartesian_cell_entries(op, sp, h[0][cx], h[1][cy], h[2][cz]));
+    }
+    cset[K] = it->second;
+  }
+  // blocks = connected components of the interior-interior pattern (the same for every set)
+  const int nl = (int)code.size();
+  std::vector<int> parent(nl);
+  for (int i = 0; i < nl; ++i) parent[i] = i;
+  std::function<int(int)> root = [&](int i) { return parent[i] == i ? i : parent[i] = root(parent[i]); };
+  const rm::CellEntries& E0 = ents[0];
+  for (size_t t = 0; t < E0.row.size(); ++t)
+    if (interior[E0.row[t]] && interior[E0.col[t]]) parent[root(E0.row[t])] = root(E0.col[t]);
+  std::map<int, std::vector<int>> comps;
+  for (int i = 0; i < nl; ++i) if (interior[i]) comps[root(i)].push_back(i);
+  std::vector<int> mem;
+  std::vector<std::vector<int>> blocks;
+  for (auto& kv : comps) {
+    if (kv.second.size() > 3) throw RmError(RM_EINVAL, "SC-PH: cell-interior block larger than 3x3");
+    blocks.push_back(kv.second);
+    for (int j = 0; j < 3; ++j) mem.push_back(j < (int)kv.second.size() ? code[kv.second[j]] : -1);
+  }
+  P.nblk = (int)blocks.size();
+  std::vector<double> bk((size_t)ents.size() * P.nblk * 6, 0.0), bm(bk.size(), 0.0);
+  for (size_t s = 0; s < ents.size(); ++s) {
+    std::map<std::pair<int, int>, std::pair<double, double>> at;
+    for (size_t t = 0; t < ents[s].row.size(); ++t) at[{ents[s].row[t], ents[s].col[t]}] = {ents[s].kval[t], ents[s].mval[t]};
+    for (int b = 0; b < P.nblk; ++b)
+      for (int i = 0, q = 0; i < 3; ++i)
+        for (int j = 0; j <= i; ++j, ++q) {
+          if (i >= (int)blocks[b].size() || j >= (int)blocks[b].size()) continue;
+          auto it = at.find({blocks[b][i], blocks[b][j]});
+          if (it == at.end()) continue;
+          bk[(s * P.nblk + b) * 6 + q] = it->second.first;
+          bm[(s * P.nblk + b) * 6 + q] = it->second.second;
+        }
+  }
+  auto upi = [&](const std::vector<int>& v) {
+    int* d = nullptr;
+    CK(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(int)));
+    c->allocs.push_back(d);
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return d;
+  };
+  auto upd = [&](const std::vector<double>& v) {
+    double* d = c->dalloc(std::max<size_t>(v.size(), 1));
+    if (!v.empty()) CK(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return d;
+  };
+  c->d_scph_set = upi(cset);
+  c->d_scph_mem = upi(mem);
+  c->d_scph_K = upd(bk);
+  c->d_scph_M = upd(bm);
+  c->d_sy = c->dalloc(c->ndof); c->d_sw = c->dalloc(c->ndof); c->d_srg = c->dalloc(c->ndof);
+  c->d_scg = c->dalloc(c->ndof); c->d_sz = c->dalloc(c->ndof);
+}
 
 extern "C" {
 
@@ -790,10 +896,13 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     if (gamma_d > 0x3F) throw RmError(RM_EINVAL, "gamma_d has bits above bit 5");
     if (o.coarse != 0 && o.coarse != 1) throw RmError(RM_EINVAL, "coarse must be 0 or 1");
     if (o.coarse && o.nranks > 1) throw RmError(RM_EINVAL, "the coarse level is single-rank only");
-    if (o.decomposition != RM_PAFW && o.decomposition != RM_PH && o.decomposition != RM_SC_PAFW)
+    if (o.decomposition != RM_PAFW && o.decomposition != RM_PH && o.decomposition != RM_SC_PAFW &&
+        o.decomposition != RM_SC_PH)
       throw RmError(RM_EINVAL, "bad decomposition");
     if (o.decomposition == RM_SC_PAFW && space != 0)
-      throw RmError(RM_EINVAL, "SC-PAFW is built for H(grad) only (SC-PH for k = 1, 2 is not)");
+      throw RmError(RM_EINVAL, "SC-PAFW is the H(grad) decomposition (k = 1, 2: SC-PH)");
+    if (o.decomposition == RM_SC_PH && (space == 0 || o.nranks > 1 || o.coarse))
+      throw RmError(RM_EINVAL, "SC-PH: k = 1, 2, single rank, one level");
     if (o.decomposition == RM_SC_PAFW && o.nranks > 1)
       throw RmError(RM_EINVAL, "SC-PAFW is single-rank only");
     if (o.factorization != RM_CHOL && o.factorization != RM_ICC_SC) throw RmError(RM_EINVAL, "bad factorization");
@@ -979,8 +1088,10 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
     in.k = space; in.p = p; in.n[0] = mesh->nx; in.n[1] = mesh->ny; in.n[2] = mesh->nz;
     in.gamma_d = gamma_d; in.coords = mesh->coords; in.alpha = alpha; in.beta = beta;
     in.n_alpha = n_alpha; in.n_beta = n_beta;
-    in.dim = (c->decomposition == RM_PH) ? space : 0;
+    const bool scph = c->decomposition == RM_SC_PH;
+    in.dim = (c->decomposition == RM_PH || scph) ? space : 0;
     in.sc_decomposition = c->decomposition == RM_SC_PAFW;
+    in.interface_only = scph;   // SC-PH: interface corrections S_i^{-1} only (eq:LDU)
     // options.factorization applies to the scalar (H(grad)) patch problems: the primary patches
     // for k = 0, the PH potential vertex stars for k = 1; k-star patches of k = 1, 2
     // are factored exactly (optimal fill)
@@ -998,11 +1109,13 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       for (int o = 0; o < no; ++o) {
         rm::SetupInput io = in;
         io.orient = no > 1 ? o : -1;
+        const auto tb = std::chrono::steady_clock::now();
         auto fam = rm::build_patch_family(io);
+        c->setup_family_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
         upload_family(c->prims[o], *fam, o > 0 ? &c->prims[0] : nullptr);
       }
     }
-    if (c->decomposition == RM_PH && space >= 1) {
+    if ((c->decomposition == RM_PH || scph) && space >= 1) {
       // potential problem B = D^T A D (+ eps_s beta M^{k-1} for k = 2): the V^{k-1} operator with
       // (alpha', beta') = (beta, 0) for k = 1 and (beta, eps_s beta) for k = 2 (reading G8)
       std::vector<double> ap(beta, beta + n_beta), bp(n_beta);
@@ -1011,13 +1124,16 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       rm::SetupInput ip = in;
       ip.k = space - 1; ip.alpha = ap.data(); ip.beta = bp.data(); ip.n_alpha = n_beta; ip.n_beta = n_beta;
       ip.dim = space - 1;
-      ip.factorization = (space == 1) ? o.factorization : RM_CHOL;
+      ip.factorization = (space == 1 && !scph) ? o.factorization : RM_CHOL;
+      ip.interface_only = scph;   // SC-PH: B~_j^{-1} on interface-only input, interface part kept
       const int no = (ip.dim == 1 || ip.dim == 2) && !rm::exp_env("RM_ONE_FAMILY") ? 3 : 1;
       c->pots.assign(no, DevFamily{});
       for (int o = 0; o < no; ++o) {
         rm::SetupInput io = ip;
         io.orient = no > 1 ? o : -1;
+        const auto tb = std::chrono::steady_clock::now();
         auto fam = rm::build_patch_family(io);
+        c->setup_family_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
         upload_family(c->pots[o], *fam, o > 0 ? &c->pots[0] : nullptr);
       }
       c->spot.init(space - 1, p, mesh->nx, mesh->ny, mesh->nz);
@@ -1029,6 +1145,7 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
           if (j == 0 || j == p || j == i) c->Dh[i * (p + 1) + j] = b.D[i * (p + 1) + j];
       c->d_t = c->dalloc(c->npot); c->d_s = c->dalloc(c->npot);
     }
+    if (scph) setup_scph(c.get(), h);
     c->d_r = c->dalloc(c->ndof);
     if (c->nranks > 1) {
       // global free count; buffers of the multi-rank sweep; the communicator (if an id is given)
@@ -1163,6 +1280,9 @@ rm_status rm_info_get(const rm_ctx* c, rm_info* info) {
       }
   info->setup_seconds = c->setup_seconds;
   info->setup_on_device = c->setup_device ? 1 : 0;
+  info->setup_host_family_seconds = c->setup_family_s;
+  for (const auto* fams : {&c->prims, &c->pots})
+    for (const auto& F : *fams) info->setup_device_numeric_seconds += F.numeric_s;
   return RM_OK;
 }
 
@@ -1252,6 +1372,48 @@ int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)
 void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false) {
+  if (c->decomposition == RM_SC_PH) {
+    // c = R_I^T A_II^{-1} R_I r + R_G^T S_PH^{-1} R_G r (eq:schur, eq:sc-asm-hiptmair)
+    const rm::ScPhParams& P = c->scph;
+    const double* al = c->d_alpha;
+    const double* be = c->d_beta;
+    const int cc = c->coef_const;
+    {
+      Phase ph(c, 1);
+      CK(rm::launch_scph_interior_solve(P, al, be, cc, c->d_scph_set, c->d_scph_mem, c->d_scph_K, c->d_scph_M, r,
+                                        c->d_sy, c->st));                       // y = A_II^-1 r_I
+    }
+    do_apply(c, c->d_sy, nullptr, c->d_sw);                                     // w = A y
+    {
+      Phase ph(c, 1);
+      CK(rm::launch_scph_vec(P, 0, r, c->d_sw, nullptr, c->d_srg, 0.0, c->st));  // R_G r = (r - A y)_G
+      CK(cudaMemsetAsync(c->d_scg, 0, c->ndof * sizeof(double), c->st));
+      const int nf = (int)c->prims.size();
+      for (int o = 0; o < nf; ++o)                                              // c_G = sum_i R~_i^T S_i^-1 R~_i R_G r
+        c->launches[1] += run_family(c, c->prims[o], c->d_srg, c->d_scg, 1.0, o > 0, o == 0, o == nf - 1);
+      c->launches[1] += 3;
+    }
+    {
+      Phase ph(c, 2);                                                           // + D~ (sum_j B~_j^-1) D~^T R_G r
+      CK(rm::launch_hiptmair_DT(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_srg, c->d_t, c->st));
+      CK(cudaMemsetAsync(c->d_s, 0, c->npot * sizeof(double), c->st));
+      const int np = (int)c->pots.size();
+      for (int o = 0; o < np; ++o)
+        c->launches[2] += run_family(c, c->pots[o], c->d_t, c->d_s, 1.0, o > 0, o == 0, o == np - 1);
+      CK(rm::launch_hiptmair_D_add(c->k, c->p, c->n, c->gamma, c->Dh.data(), c->d_s, c->d_scg, 1.0, c->st));
+      CK(rm::launch_scph_vec(P, 1, nullptr, nullptr, nullptr, c->d_scg, 0.0, c->st));   // D~ = D_GG
+      c->launches[2] += 3;
+    }
+    do_apply(c, c->d_scg, nullptr, c->d_sw);                                    // w = A c_G
+    {
+      Phase ph(c, 1);
+      CK(rm::launch_scph_interior_solve(P, al, be, cc, c->d_scph_set, c->d_scph_mem, c->d_scph_K, c->d_scph_M,
+                                        c->d_sw, c->d_sz, c->st));              // z = A_II^-1 (A c_G)_I
+      CK(rm::launch_scph_vec(P, 2, c->d_sy, c->d_sz, c->d_scg, u, omega, c->st));   // u += omega (y_I - z_I ; c_G)
+      c->launches[1] += 4;
+    }
+    return;
+  }
   {
     Phase ph(c, 1);
     const int nf = (int)c->prims.size();

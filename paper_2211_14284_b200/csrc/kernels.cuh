@@ -231,6 +231,19 @@ cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, con
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                   const double* s, double* u, double omega, cudaStream_t st);
+// SC-PH (sc_ph.cu): layout of V^k, and the cell-interior blocks (<= 3x3) of the Cartesian cell
+// operator: members as codes comp << 24 | c << 16 | b << 8 | a (cell-local x, y, z indices), per
+// cell-size set the lower K and M entries (6 per block, row-major lower)
+struct ScPhParams {
+  int p, ncomp, n[3], nblk;
+  int fam[3][3];                  // [comp][dir], 0 = P family
+  long long len[3][3], off[4];
+};
+cudaError_t launch_scph_interior_solve(const ScPhParams& P, const double* alpha, const double* beta, int coef_const,
+                                       const int* cell_set, const int* bmem, const double* bK, const double* bM,
+                                       const double* x, double* y, cudaStream_t st);
+cudaError_t launch_scph_vec(const ScPhParams& P, int mode, const double* a, const double* b, const double* c,
+                            double* out, double omega, cudaStream_t st);
 // y = a*x + b*y ; dot products with deterministic two-stage reduction
 cudaError_t launch_axpby(long long n, double a, const double* x, double b, double* y, cudaStream_t st);
 cudaError_t launch_dot(long long n, const double* x, const double* y, double* partial, double* out, cudaStream_t st);

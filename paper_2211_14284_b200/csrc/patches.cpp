@@ -1490,7 +1490,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
         if (!used[b]) C.zlist.push_back(b);
     // SC-PAFW with the exact elimination program: the patch-local interior corrections are not
     // scattered (the post step computes the cell interiors once from the interface corrections)
-    if (in.sc_decomposition && !C.sc)
+    if ((in.sc_decomposition || in.interface_only) && !C.sc)
       for (int t2 = 0; t2 < C.n; ++t2)
         if (C.group[t2] == 0 && C.bidx[t2] >= 0) C.zlist.push_back(C.bidx[t2]);
     build_meta(C);

@@ -251,6 +251,8 @@ struct SetupInput {
   int zv_lo = 0, zv_hi = 1 << 30;   // vertex stars kept: z vertex layers [zv_lo, zv_hi) (z-slab ownership)
   int orient = -1;                  // edge / face stars: keep one orientation (edge direction / face normal), -1 = all
   bool defer_numeric = false;       // device-resident numeric setup (PatchFamily::deferred)
+  bool interface_only = false;      // SC-PH: the patches' interior corrections are dropped (their interface
+                                    // part is the interface Schur complement solve, eq:LDU)
   bool sc_decomposition = false;    // SC-PAFW (eq:sc-asm-afw, k = 0): interface corrections from the patches, cell
                                     // interiors once afterwards (c_I = A_II^-1 (r_I - A_IG c_G), n_K = 1)
 };

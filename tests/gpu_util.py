@@ -9,7 +9,7 @@ def setup_product(w, **kw):
     coords = None if w.perturb == 0 else ri.vertex_coords(w)
     return rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(),
                         w.gamma_d, coords=coords,
-                        decomposition=kw.pop("decomposition", {"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW}.get(w.decomposition, rmb.RM_PAFW)),
+                        decomposition=kw.pop("decomposition", {"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW, "sc-ph": rmb.RM_SC_PH}.get(w.decomposition, rmb.RM_PAFW)),
                         factorization=kw.pop("factorization", rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL),
                         **kw)
 

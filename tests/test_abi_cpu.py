@@ -54,6 +54,8 @@ def test_setup_errors_without_gpu_are_reported_not_raised():
         rmb.rm_setup(2, 2, 2, 0, 0, [1.0], [1.0], 63)          # p = 0 is invalid
     with pytest.raises(rmb.RmError):
         rmb.rm_setup(2, 2, 2, 3, 0, [1.0, 2.0], [1.0], 63)     # alpha size neither 1 nor ncells
+    with pytest.raises(rmb.RmError):
+        rmb.rm_setup(2, 2, 2, 3, 0, [1.0], [1.0], 63, decomposition=rmb.RM_SC_PH)   # SC-PH is k = 1, 2
 
 
 # ------------------------------------------------------------------ host re-enactment vs oracle

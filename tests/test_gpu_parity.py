@@ -28,7 +28,7 @@ def setup_pair(w, **kw):
     from oracle.solver import Problem
     coords = None if w.perturb == 0 else ri.vertex_coords(w)
     ctx = rmb.rm_setup(w.nx, w.ny, w.nz, w.p, w.space, ri.cell_alpha(w).ravel(), ri.cell_beta(w).ravel(), w.gamma_d,
-                       coords=coords, decomposition={"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW}.get(w.decomposition, rmb.RM_PAFW),
+                       coords=coords, decomposition={"ph": rmb.RM_PH, "sc-pafw": rmb.RM_SC_PAFW, "sc-ph": rmb.RM_SC_PH}.get(w.decomposition, rmb.RM_PAFW),
                        factorization=rmb.RM_ICC_SC if w.factorization == "icc_sc" else rmb.RM_CHOL,
                        patch_entities=kw.get("patch_entities", 0))
     pb = Problem(w.space, w.p, w.nx, w.ny, w.nz, ri.vertex_coords(w), ri.cell_alpha(w), ri.cell_beta(w), w.gamma_d,
@@ -91,6 +91,15 @@ CASES = [
     ("cfg2-sc-3^3-p4", dataclasses.replace(ri.CONFIGS[2].with_mesh(3).with_p(4), decomposition="sc-pafw"), 1e-11),
     ("cfg5-sc-3^3-p3", dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"), 1e-11),
     ("cfg5-sc-2^3-p7", dataclasses.replace(ri.CONFIGS[5].with_mesh(2).with_p(7), decomposition="sc-pafw"), 1e-11),
+    # row f2 (k = 1, 2): SC-PH (eq:sc-asm-hiptmair), interface-only star solves + interiors once.
+    # The explicit condensation (S = A_GG - A_GI A_II^-1 A_IG, c_I = y_I - A_II^-1 A_IG c_G) cancels:
+    # the oracle's own two exact assemblies differ by 1.5e-11 (3^3, p = 4) and 3.2e-11 (2^3, p = 6),
+    # so these cases take the derived tolerance (None: 10x the oracle noise floor)
+    ("cfg3-scph-2^3-p3", dataclasses.replace(ri.CONFIGS[3].with_mesh(2).with_p(3), decomposition="sc-ph"), 1e-11),
+    ("cfg3-scph-3^3-p4", dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(4), decomposition="sc-ph"), None),
+    ("cfg3-scph-2^3-p6", dataclasses.replace(ri.CONFIGS[3].with_mesh(2), decomposition="sc-ph"), None),
+    ("cfg4-scph-2^3-p3", dataclasses.replace(ri.CONFIGS[4].with_mesh(2).with_p(3), decomposition="sc-ph"), None),
+    ("cfg4-scph-3^3-p3", dataclasses.replace(ri.CONFIGS[4].with_mesh(3).with_p(3), decomposition="sc-ph"), None),
 ]
 # the one-box-buffer sequential schedule of the patch kernel (taken by full-size cfg4) forced
 NBOX1_CASES = [("nbox1-" + c[0], c[1], c[2]) for c in CASES if c[0] in ("cfg2-3^3", "cfg3-2^3-p3", "cfg4-2^3-p3",
@@ -120,7 +129,7 @@ def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
     assert (ctx.constrained_mask() == pb.constrained).all()
     assert ctx.n_free == int(pb.free.sum())
     f, u = vecs(w, ctx)
-    if tol is None:   # H(div) PAFW: 10x the oracle's own assembly noise on this shape
+    if tol is None:   # H(div) PAFW, SC-PH: 10x the oracle's own assembly noise on this shape
         tol = max(1e-11, 10 * gu.oracle_noise_floor(w, f, u))
     ft, ut = torch.tensor(f, device=dev), torch.tensor(u, device=dev)
     v = torch.empty_like(ut)
@@ -153,6 +162,10 @@ def test_apply_and_sweep_parity(dev, name, w, tol, monkeypatch):
                                     ("cfg3-iccsc-3^3-p3",
                                      dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(3), factorization="icc_sc")),
                                     ("cfg1-sc", dataclasses.replace(ri.CONFIGS[1], decomposition="sc-pafw")),
+                                    ("cfg3-scph-3^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[3].with_mesh(3).with_p(3), decomposition="sc-ph")),
+                                    ("cfg4-scph-3^3-p3",
+                                     dataclasses.replace(ri.CONFIGS[4].with_mesh(3).with_p(3), decomposition="sc-ph")),
                                     ("cfg5-sc-3^3-p3",
                                      dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"))])
 def test_pcg_iterations(dev, name, w):
