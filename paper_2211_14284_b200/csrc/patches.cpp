@@ -1497,7 +1497,7 @@ std::unique_ptr<PatchFamily> build_patch_family(const SetupInput& in) {
   }
   fam->nfactors = (int64_t)foff.size();
   fam->unique_value_bytes = total * (int64_t)sizeof(double);
-  fam->values.assign(total, 0.0);
+  if (!in.defer_numeric) fam->values.assign(total, 0.0);   // deferred: the blocks live on the device only
   std::string first_err;
   std::mutex emu;
   double smax = 0.0;
