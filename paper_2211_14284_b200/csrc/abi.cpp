@@ -1362,11 +1362,11 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out, long lon
 // families of one space run back to back on shared padded buffers: the first pads r and zeroes c,
 // the last adds omega c to u
 int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega, bool r_padded = false,
-               bool zero_c = true, bool combine = true) {
+               bool zero_c = true, bool combine = true, bool sc_pre_done = false) {
   if (!F.present) return 0;
   KPhase kp{c, 4};
   const rm::KTimer kt = kp.timer();
-  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded, zero_c, combine));
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded, zero_c, combine, sc_pre_done));
   return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
@@ -1565,6 +1565,28 @@ bool fused_k0(const rm_ctx* c) {
   return c->k == 0 && !c->pots[0].present && c->prims.size() == 1 && c->prims[0].npatch > 0;
 }
 
+// trilinear ICC-SC family on one rank: the SC pre step joins the residual (apply -> condensation
+// of the cell interiors -> skeleton gather minus the line sums)
+bool sc_fused(const rm_ctx* c) {
+  return fused_k0(c) && !c->cartesian && c->nranks == 1 && c->prims[0].launch.sc_dinv && c->prims[0].launch.sc_pre;
+}
+
+void residual_sc_fused(rm_ctx* c, const double* u, const double* f, const rm::PatchLaunch& L) {
+  Phase ph(c, 0);
+  int nl = 0;
+  KPhase kp{c, 5};
+  const rm::KTimer kt = kp.timer();
+  c->tri.ldx_out = L.pad.lxp[0];
+  c->tri.skip_gather = 1;
+  CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, f, L.rpad, -1.0,
+                                c->d_cellbuf, c->st, &nl, &kt));
+  c->tri.skip_gather = 0;
+  CK(rm::launch_sc_pre_fused(L, f, c->tri.Lx, c->st));
+  CK(rm::launch_skeleton_gather_sc(c->tri, c->d_cellbuf, f, L.rpad, -1.0, L.sc_fb, c->st));
+  c->tri.ldx_out = 0;
+  c->launches[0] += nl + 2;
+}
+
 // one sweep u_out = u_in + omega P^{-1} (f - A u_in) (z-slab: halos, local correction, reverse-add)
 void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, double omega) {
   if (c->nranks > 1) {
@@ -1591,6 +1613,14 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
     reverse_add(c, c->d_c);
     if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(rm::launch_axpby(c->ndof, omega, c->d_c, 1.0, u_out, c->st));
+    return;
+  }
+  if (sc_fused(c)) {
+    const rm::PatchLaunch& L = c->prims[0].launch;
+    residual_sc_fused(c, u_in, f, L);
+    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    Phase ph(c, 1);
+    c->launches[1] += run_family(c, c->prims[0], L.rpad, u_out, omega, true, true, true, true);
     return;
   }
   if (fused_k0(c)) {

@@ -700,6 +700,109 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
   (void)Lz;
 }
 
+// Static-condensation variant of the gather (ICC-SC families on one rank; the SC pre step ran
+// between the apply and this kernel and already completed the cell-interior residuals in place):
+// only SKELETON DoFs are written, out[g] = f[g] + sign * (sum of the <= 8 cell contributions)
+// and, for face-interior DoFs, minus the condensation line sums e of the (<= 2) cells sharing the
+// face (lower cell first) -- the same operations, in the same order, as the gather followed by
+// sc_face_kernel.  Rows with y and z off the cell boundaries only visit the x-boundary DoFs.
+__global__ void tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
+                                     const double* __restrict__ f, double* __restrict__ out, double sign,
+                                     const double* __restrict__ fb) {
+  __shared__ int4 xtab[1024];
+  __shared__ unsigned char xfl[1024];
+  const int Lx = (int)tp.Lx, Ly = (int)tp.Ly;
+  const int p = tp.p, P1 = p + 1, n3 = P1 * P1 * P1, pm = p - 1, nf = pm * pm;
+  for (int gx = threadIdx.x; gx < Lx; gx += blockDim.x) {
+    int cc = gx / p;
+    if (cc >= tp.n[0]) cc = tp.n[0] - 1;
+    const int aa = gx - cc * p;
+    xtab[gx] = (aa == 0 && cc > 0) ? make_int4(cc - 1, p, cc, 0) : make_int4(cc, aa, 0, -1);
+    xfl[gx] = (unsigned char)((aa == 0 || aa == p ? 1 : 0) | (tri_cons(gx, (long long)tp.n[0] * p, tp.gamma_d, 0) ? 2 : 0));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nrow = Ly * (int)tp.Lz, wstride = gridDim.x * (blockDim.x >> 5);
+  const long long ldx = tp.ldx_out > 0 ? tp.ldx_out : Lx;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < nrow; row += wstride) {
+    const int gy = row % Ly, gz = row / Ly;
+    const bool rcons = tri_cons(gy, (long long)tp.n[1] * p, tp.gamma_d, 1) || tri_cons(gz, (long long)tp.n[2] * p, tp.gamma_d, 2);
+    int cy0, ay0, cy1 = 0, ay1 = -1, cz0, az0, cz1 = 0, az1 = -1;
+    {
+      int cc = gy / p; if (cc >= tp.n[1]) cc = tp.n[1] - 1;
+      const int aa = gy - cc * p;
+      if (aa == 0 && cc > 0) { cy0 = cc - 1; ay0 = p; cy1 = cc; ay1 = 0; } else { cy0 = cc; ay0 = aa; }
+    }
+    {
+      int cc = gz / p; if (cc >= tp.n[2]) cc = tp.n[2] - 1;
+      const int aa = gz - cc * p;
+      if (aa == 0 && cc > 0) { cz0 = cc - 1; az0 = p; cz1 = cc; az1 = 0; } else { cz0 = cc; az0 = aa; }
+    }
+    const bool by = gy % p == 0, bz = gz % p == 0;
+    const bool rskel = by || bz;
+    const int rb00 = (cz0 * tp.n[1] + cy0) * tp.n[0], ro00 = (az0 * P1 + ay0) * P1;
+    const int rb01 = (cz0 * tp.n[1] + cy1) * tp.n[0], ro01 = (az0 * P1 + ay1) * P1;
+    const int rb10 = (cz1 * tp.n[1] + cy0) * tp.n[0], ro10 = (az1 * P1 + ay0) * P1;
+    const int rb11 = (cz1 * tp.n[1] + cy1) * tp.n[0], ro11 = (az1 * P1 + ay1) * P1;
+    const bool v01 = ay1 >= 0, v10 = az1 >= 0, v11 = v01 && v10;
+    const long long fbase = (long long)row * Lx, obase = (long long)row * ldx;
+    // skeleton rows: every x; other rows: the x-boundary DoFs (cell index t = gx / p)
+    const int nx_ = rskel ? Lx : tp.n[0] + 1;
+    for (int t = lane; t < nx_; t += 32) {
+      const int gx = rskel ? t : t * p;
+      const long long g = obase + gx;
+      const int fl = xfl[gx];
+      if (rcons || (fl & 2)) { out[g] = 0.0; continue; }
+      if (!(fl & 1) && !rskel) continue;   // cell interior (completed by the SC pre step)
+      const double fv = f ? f[fbase + gx] : 0.0;
+      const int4 xe = xtab[gx];
+      auto at = [&](int rb, int ro, int c, int a) { return cellbuf[(size_t)(rb + c) * n3 + ro + a]; };
+      double s = at(rb00, ro00, xe.x, xe.y);
+      if (xe.w >= 0) s += at(rb00, ro00, xe.z, xe.w);
+      if (v01) { s += at(rb01, ro01, xe.x, xe.y); if (xe.w >= 0) s += at(rb01, ro01, xe.z, xe.w); }
+      if (v10) { s += at(rb10, ro10, xe.x, xe.y); if (xe.w >= 0) s += at(rb10, ro10, xe.z, xe.w); }
+      if (v11) { s += at(rb11, ro11, xe.x, xe.y); if (xe.w >= 0) s += at(rb11, ro11, xe.z, xe.w); }
+      double r = fv + sign * s;
+      const bool bx = (fl & 1) != 0;
+      if ((int)bx + (int)by + (int)bz == 1) {   // face-interior DoF: the condensation line sums
+        const int dir = bx ? 0 : (by ? 1 : 2);
+        const int gg[3] = {gx, gy, gz};
+        const int d1 = dir == 0 ? 1 : 0, d2 = dir == 2 ? 1 : 2;
+        const int a = gg[d1] % p - 1, b = gg[d2] % p - 1, P = gg[dir] / p;
+        int cell[3];
+        cell[d1] = gg[d1] / p; cell[d2] = gg[d2] / p;
+        double e = 0.0;
+        if (P > 0) {
+          cell[dir] = P - 1;
+          const int K = (cell[2] * tp.n[1] + cell[1]) * tp.n[0] + cell[0];
+          e += fb[((size_t)K * 6 + 2 * dir + 1) * nf + b * pm + a];
+        }
+        if (P < tp.n[dir]) {
+          cell[dir] = P;
+          const int K = (cell[2] * tp.n[1] + cell[1]) * tp.n[0] + cell[0];
+          e += fb[((size_t)K * 6 + 2 * dir) * nf + b * pm + a];
+        }
+        r -= e;
+      }
+      out[g] = r;
+    }
+  }
+}
+
+cudaError_t launch_skeleton_gather_sc(const TriParams& tp, const double* cellbuf, const double* f, double* out,
+                                      double sign, const double* fb, cudaStream_t st) {
+  if (tp.Lx > 1024 || tp.p < 2) return cudaErrorInvalidValue;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  tri_gather_sc_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign, fb);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, const double* X, const double* alpha,
                                    const double* beta, int coef_const, const double* u, const double* f, double* out,
                                    double sign, double* cellbuf, cudaStream_t st, int* nlaunch, const KTimer* kt) {
@@ -729,7 +832,7 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
   else
     apply_tri_kernel<false><<<grid, TRI_THREADS, TRI_SMEM, st>>>(tp, tabs, X, alpha, beta, coef_const, u, f, out, sign, cellbuf);
   if (kt) kt->end(kt->arg);
-  tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
+  if (!tp.skip_gather) tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
   (void)nd;
   if (nlaunch) *nlaunch += 2;
   return cudaGetLastError();

@@ -81,6 +81,7 @@ struct TriParams {
   // standard ones in `tabs` (S_E, S_O, D_E, D_O at the left points, 12 x 8 each, zero padded)
   int eo, ne;          // even/odd path on; number of point pairs
   int xsig[16];
+  int skip_gather;     // launch_apply_trilinear stops after the apply (the SC-fused residual path)
 };
 // optional hooks around a launcher's main kernel (the ABI records CUDA events there for the
 // per-kernel timing phases of rm_timing_read)
@@ -96,6 +97,10 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
                                    const KTimer* kt = nullptr);
 // doubles of the per-cell result buffer the trilinear apply needs (apply_tri.cu)
 size_t tri_cellbuf_doubles(const TriParams& tp);
+// skeleton gather of the SC-fused residual (ICC-SC, one rank): skeleton DoFs only, minus the
+// condensation line sums fb of the face-interior DoFs (apply_tri.cu tri_gather_sc_kernel)
+cudaError_t launch_skeleton_gather_sc(const TriParams& tp, const double* cellbuf, const double* f, double* out,
+                                      double sign, const double* fb, cudaStream_t st);
 // H(curl) / H(div) Cartesian apply (apply_kform.cu): one launch over all cells, interior entries
 // stored as f + sign A u, skeleton entries through `cellbuf` (kform_cellbuf_doubles) and a gather
 cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const double* beta, int coef_const,
@@ -220,7 +225,11 @@ size_t patch_batch_smem(int box_total, int mr_max, int B, int NT);
 // sharing their padded buffers run back to back)
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
                                const KTimer* kt = nullptr, bool r_padded = false, bool zero_c = true,
-                               bool combine = true);
+                               bool combine = true, bool sc_pre_done = false);
+// ICC-SC pre step, part 1, on the residual of the SC-fused path: the cell-interior entries of rpad
+// hold sign * (A u)_I (trilinear apply with skip_gather); r_I = f_I + rpad_I is completed in place
+// and the condensation line sums go to L.sc_fb (f: the vector layout, x-stride lx)
+cudaError_t launch_sc_pre_fused(const PatchLaunch& L, const double* f, long long lx, cudaStream_t st);
 // u += omega * unpad(cpad) (the combine step of launch_patch_solve, on its own)
 cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st);
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)

@@ -1014,7 +1014,8 @@ __device__ __forceinline__ long long sc_idx(const ScGeom& G, long long x, long l
 // Every global array is read contiguously (couplings per (K, f) are stored I-contiguous).
 __global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
                                const double* __restrict__ cc, const double* __restrict__ cw,
-                               const double* __restrict__ rp, double* __restrict__ fb) {
+                               double* __restrict__ rp, double* __restrict__ fb, const double* __restrict__ f,
+                               long long lxf) {
   extern __shared__ double scs[];
   const int p = G.p, pm = p - 1, ni = pm * pm * pm, nf = pm * pm;
   double* y = scs;          // [k][j][i]
@@ -1023,7 +1024,14 @@ __global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* _
   const double* dk = dinv + (size_t)K * ni;
   for (int I = threadIdx.x; I < ni; I += blockDim.x) {
     const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / nf + 1;
-    y[I] = dk[I] * rp[sc_idx(G, (long long)cx * p + i, (long long)cy * p + j, (long long)cz * p + k)];
+    const long long gx = (long long)cx * p + i, gy = (long long)cy * p + j, gz = (long long)cz * p + k;
+    const long long g = sc_idx(G, gx, gy, gz);
+    double r = rp[g];
+    if (f) {   // SC-fused residual: rp holds sign * (A u)_I; complete r_I = f_I + rp_I in place
+      r = f[(gz * G.ly + gy) * lxf + gx] + r;
+      rp[g] = r;
+    }
+    y[I] = dk[I] * r;
   }
   __syncthreads();
   // one thread per (face, line): the line through face position (a, b) along the face normal
@@ -1254,8 +1262,32 @@ cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, 
   return cudaGetLastError();
 }
 
+cudaError_t launch_sc_pre_fused(const PatchLaunch& L, const double* f, long long lx, cudaStream_t st) {
+  if (!L.sc_dinv || !L.sc_pre) return cudaErrorInvalidValue;
+  ScGeom sg{};
+  sg.p = L.sc_p;
+  for (int d = 0; d < 3; ++d) sg.n[d] = L.sc_n[d];
+  sg.lxp = L.pad.lxp[0];
+  sg.ly = L.pad.len[0][1];
+  sg.cmp = L.sc_w ? 1 : 0;
+  for (int a = 0; a < 16; ++a) { sg.kd[a] = L.sc_kd[a]; sg.k0[a] = L.sc_k0[a]; sg.kp[a] = L.sc_kp[a]; }
+  const int pm = L.sc_p - 1;
+  const int ncell = sg.n[0] * sg.n[1] * sg.n[2];
+  if (ncell == 0 || pm <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t)(pm * pm * pm);
+  static size_t smem_set = 0;
+  cudaError_t e;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    if ((e = cudaFuncSetAttribute(sc_cell_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return e;
+    smem_set = smem;
+  }
+  sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, f, lx);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt, bool r_padded, bool zero_c, bool combine) {
+                               const KTimer* kt, bool r_padded, bool zero_c, bool combine, bool sc_pre_done) {
   if (L.npatch <= 0) {   // an empty family still does its part of a shared sequence
     if (!L.cpad) return cudaSuccess;
     if (!r_padded) pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
@@ -1282,7 +1314,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     nface = ((long long)(sg.n[0] + 1) * sg.n[1] * sg.n[2] + (long long)(sg.n[1] + 1) * sg.n[0] * sg.n[2] +
              (long long)(sg.n[2] + 1) * sg.n[0] * sg.n[1]) * pm * pm;
     nint = (long long)sg.n[0] * sg.n[1] * sg.n[2] * pm * pm * pm;
-    if (nface > 0 && L.sc_pre) {
+    if (nface > 0 && L.sc_pre && !sc_pre_done) {
       const int ncell = sg.n[0] * sg.n[1] * sg.n[2];
       const size_t smem = sizeof(double) * (size_t)(pm * pm * pm);
       static size_t smem_set = 0;
@@ -1291,7 +1323,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
           return e;
         smem_set = smem;
       }
-      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb);
+      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, nullptr, 0);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       sc_face_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_fb, L.rpad, (int)nface);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
