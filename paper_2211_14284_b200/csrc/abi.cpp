@@ -1043,11 +1043,11 @@ rm_status rm_setup(rm_ctx** out, const rm_mesh* mesh, int32_t p, rm_space space,
       c->tri.Lx = c->sp.len(0, 0); c->tri.Ly = c->sp.len(0, 1); c->tri.Lz = c->sp.len(0, 2);
       c->tri.gamma_d = gamma_d;
       c->d_cellbuf = c->dalloc(rm::tri_cellbuf_doubles(c->tri));
-    } else if (space >= 1 || rm::exp_env("RM_APPLY_PW")) {
-      // Cartesian H(curl) / H(div): pointwise-stage apply, one launch over all cells + the skeleton
-      // gather (apply_kform.cu).  H(grad) keeps the colour kernel of apply.cu: the k = 0 pointwise
-      // kernel (experiment RM_APPLY_PW) measured residual 0.48 ms at cfg2 (apply 0.26 + gather 0.20)
-      // against 0.34 ms for the colours (profiles/r02_bench_cfg2_k.json)
+    } else {
+      // Cartesian: one apply launch over all cells + the skeleton gather.  H(curl) / H(div): the
+      // pointwise-stage kernels (apply_kform.cu); H(grad): the line-stage kernel of apply.cu
+      // (interior entries final) + the skeleton-only gather (round 2; the 8-colour launches
+      // measured 0.34 ms at cfg2, the k = 0 pointwise kernel, experiment RM_APPLY_PW, 0.48 ms)
       c->d_cellbuf = c->dalloc(rm::kform_cellbuf_doubles(space, p, c->n));
     }
     // ---- device operator

@@ -211,14 +211,17 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
                                                        const double* __restrict__ hpow,
                                                        const double* __restrict__ u, double* __restrict__ out,
                                                        double sign, int px, int py, int pz,
-                                                       double* __restrict__ cellbuf) {
+                                                       double* __restrict__ cellbuf, const double* __restrict__ f) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
+  // cell window in shared memory with x lines padded to N + 1 doubles: the x stage (thread per
+  // x line) and the y stage read conflict-free (unpadded, stride-N lines were 16-way conflicts)
+  constexpr int NP = N + 1, NW = N2 * NP;
   constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
   const int cs = tid / N2, q = tid % N2;
-  double* A = sm + cs * 2 * N3;
-  double* Bf = A + N3;
+  double* A = sm + cs * 2 * NW;
+  double* Bf = A + NW;
   // colour mode: the cells of parity (px, py, pz), out += sign A_K u; cell-buffer mode (cellbuf):
   // every cell, interior DoFs stored as sign A_K u, skeleton entries to cellbuf (summed by the gather)
   const int ncx = cellbuf ? op.n[0] : (op.n[0] - px + 1) / 2, ncy = cellbuf ? op.n[1] : (op.n[1] - py + 1) / 2,
@@ -240,14 +243,14 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
       const long long ix = (long long)cx * P + a, iy = (long long)cy * P + b, iz = (long long)cz * P + c;
       const bool con = cons_idx(FAMP, ix, lastx, op.gamma_d, 0) || cons_idx(FAMP, iy, lasty, op.gamma_d, 1) ||
                        cons_idx(FAMP, iz, lastz, op.gamma_d, 2);
-      A[l] = con ? 0.0 : __ldg(u + (iz * Ly + iy) * Lx + ix);
+      A[(c * N + b) * NP + a] = con ? 0.0 : __ldg(u + (iz * Ly + iy) * Lx + ix);
     }
   }
   __syncthreads();
   double x[N], y1[N], y2[N];
   // x-stage: thread q = (b, c)
   if (valid) {
-    const int base = q * N;
+    const int base = q * NP;
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = A[base + i];
     apply_B<P>(op.Bh, x, y1);
@@ -268,14 +271,14 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
     const int a = q % N, c = q / N;
     double bx[N], Pv[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) { bx[j] = Bf[c * N2 + j * N + a]; x[j] = A[c * N2 + j * N + a]; }
+    for (int j = 0; j < N; ++j) { bx[j] = Bf[(c * N + j) * NP + a]; x[j] = A[(c * N + j) * NP + a]; }
     apply_B<P>(op.Bh, x, y1);    // B_y ax
     apply_A<P>(op.Ah, bx, y2);   // A_y bx
     apply_B<P>(op.Bh, bx, x);    // Q = B_y bx
 #pragma unroll
     for (int j = 0; j < N; ++j) Pv[j] = sM * x[j] + sx * y1[j] + sy * y2[j];
 #pragma unroll
-    for (int j = 0; j < N; ++j) { A[c * N2 + j * N + a] = Pv[j]; Bf[c * N2 + j * N + a] = x[j]; }
+    for (int j = 0; j < N; ++j) { A[(c * N + j) * NP + a] = Pv[j]; Bf[(c * N + j) * NP + a] = x[j]; }
   }
   __syncthreads();
   // z-stage: thread q = (a, b): lines [.][b][a]
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
     const int a = q % N, b = q / N;
     double Qv[N];
 #pragma unroll
-    for (int k = 0; k < N; ++k) { x[k] = A[k * N2 + b * N + a]; Qv[k] = Bf[k * N2 + b * N + a]; }
+    for (int k = 0; k < N; ++k) { x[k] = A[(k * N + b) * NP + a]; Qv[k] = Bf[(k * N + b) * NP + a]; }
     apply_B<P>(op.Bh, x, y1);
     apply_A<P>(op.Ah, Qv, y2);
     const long long ix = (long long)cx * P + a, iy = (long long)cy * P + b;
@@ -294,7 +297,10 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
       for (int k = 0; k < N; ++k) {
         const double vv = y1[k] + sz * y2[k];
         if (skel_ab || k == 0 || k == P) cb[k * N2] = vv;
-        else out[(((long long)cz * P + k) * Ly + iy) * LDX + ix] = sign * vv;
+        else {   // cell interior (owned by this cell alone): final, out = f + sign A_K u
+          const long long row = (long long)cz * P + k;
+          out[(row * Ly + iy) * LDX + ix] = (f ? __ldg(f + (row * Ly + iy) * Lx + ix) : 0.0) + sign * vv;
+        }
       }
       return;
     }
@@ -313,10 +319,10 @@ __global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ Op
 template <int P>
 static cudaError_t launch_q(const OpParams& op, const double* alpha, const double* beta, int coef_const,
                             const double* hpow, const double* u, double* out, double sign, cudaStream_t st, int& nl,
-                            double* cellbuf) {
+                            double* cellbuf, const double* f = nullptr) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
   constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
-  const size_t smem = (size_t)CPB * 2 * N3 * sizeof(double);
+  const size_t smem = (size_t)CPB * 2 * N2 * (N + 1) * sizeof(double);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(apply_q_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -326,7 +332,7 @@ static cudaError_t launch_q(const OpParams& op, const double* alpha, const doubl
   if (cellbuf) {   // one launch over every cell (the skeleton gather follows)
     const long long ncell = (long long)op.n[0] * op.n[1] * op.n[2];
     apply_q_kernel<P><<<(unsigned)((ncell + CPB - 1) / CPB), CPB * N2, smem, st>>>(op, alpha, beta, coef_const, hpow, u,
-                                                                                  out, sign, 0, 0, 0, cellbuf);
+                                                                                  out, sign, 0, 0, 0, cellbuf, f);
     ++nl;
     return cudaGetLastError();
   }
@@ -337,7 +343,7 @@ static cudaError_t launch_q(const OpParams& op, const double* alpha, const doubl
         if (ncell <= 0) continue;
         const unsigned grid = (unsigned)((ncell + CPB - 1) / CPB);
         apply_q_kernel<P><<<grid, CPB * N2, smem, st>>>(op, alpha, beta, coef_const, hpow, u, out, sign, px, py, pz,
-                                                        nullptr);
+                                                        nullptr, nullptr);
         ++nl;
       }
   return cudaGetLastError();
@@ -352,7 +358,33 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt,
                                    double* cellbuf) {
-  if (cellbuf)   // pointwise-stage kernels (apply_kform.cu), one launch + skeleton gather, every k
+  if (cellbuf && op.k == 0 && op.ncomp == 1 && op.len[0][0] <= 1024 && !exp_env("RM_APPLY_PW")) {
+    // H(grad): ONE launch of the line-stage kernel over every cell (cell-interior DoFs final,
+    // out = f + sign A_K u; skeleton entries to the cell buffer), then the skeleton-only gather
+    const double sgn = f ? -1.0 : 1.0;
+    int nl = 0;
+    cudaError_t e;
+    if (kt) kt->begin(kt->arg);
+    switch (op.p) {
+#define RM_QC(PP) case PP: e = launch_q<PP>(op, alpha, beta, coef_const, hpow, u, out, sgn, st, nl, cellbuf, f); break;
+      RM_QC(1) RM_QC(2) RM_QC(3) RM_QC(4) RM_QC(5) RM_QC(6) RM_QC(7) RM_QC(8)
+      RM_QC(9) RM_QC(10) RM_QC(11) RM_QC(12) RM_QC(13) RM_QC(14) RM_QC(15)
+#undef RM_QC
+      default: e = cudaErrorInvalidValue;
+    }
+    if (kt) kt->end(kt->arg);
+    if (e != cudaSuccess) return e;
+    TriParams tp{};
+    tp.p = op.p;
+    for (int d = 0; d < 3; ++d) tp.n[d] = op.n[d];
+    tp.Lx = op.len[0][0]; tp.Ly = op.len[0][1]; tp.Lz = op.len[0][2];
+    tp.gamma_d = op.gamma_d;
+    tp.ldx_out = op.ldx_out;
+    e = launch_skeleton_gather_sc(tp, cellbuf, f, out, sgn, nullptr, st);
+    if (nlaunch) *nlaunch = nl + 1;
+    return e;
+  }
+  if (cellbuf && (op.k != 0 || exp_env("RM_APPLY_PW")))   // pointwise-stage kernels (apply_kform.cu) + gather, k = 1, 2
     return launch_apply_kform(op, alpha, beta, coef_const, hpow, u, f, out, ndof, cellbuf, st, nlaunch, kt);
   int nl = 1;
   if (op.ncomp == 1) apply_init_q_kernel<<<148 * 8, 256, 0, st>>>(op, f, out);

@@ -700,12 +700,12 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
   (void)Lz;
 }
 
-// Static-condensation variant of the gather (ICC-SC families on one rank; the SC pre step ran
-// between the apply and this kernel and already completed the cell-interior residuals in place):
-// only SKELETON DoFs are written, out[g] = f[g] + sign * (sum of the <= 8 cell contributions)
+// Skeleton-only gather: the cell-interior entries are final already (the Cartesian H(grad) apply
+// writes f + sign A_K u there; on the SC-fused path (ICC-SC, one rank) the SC pre step completed
+// them in place between the apply and this kernel); only SKELETON DoFs are written, out[g] = f[g] + sign * (sum of the <= 8 cell contributions)
 // and, for face-interior DoFs, minus the condensation line sums e of the (<= 2) cells sharing the
-// face (lower cell first) -- the same operations, in the same order, as the gather followed by
-// sc_face_kernel.  Rows with y and z off the cell boundaries only visit the x-boundary DoFs.
+// face (lower cell first; fb != null) -- the same operations, in the same order, as the gather
+// followed by sc_face_kernel.  Rows with y and z off the cell boundaries only visit the x-boundary DoFs.
 __global__ void tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                      const double* __restrict__ f, double* __restrict__ out, double sign,
                                      const double* __restrict__ fb) {
@@ -764,7 +764,7 @@ __global__ void tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const
       if (v11) { s += at(rb11, ro11, xe.x, xe.y); if (xe.w >= 0) s += at(rb11, ro11, xe.z, xe.w); }
       double r = fv + sign * s;
       const bool bx = (fl & 1) != 0;
-      if ((int)bx + (int)by + (int)bz == 1) {   // face-interior DoF: the condensation line sums
+      if (fb && (int)bx + (int)by + (int)bz == 1) {   // face-interior DoF: the condensation line sums
         const int dir = bx ? 0 : (by ? 1 : 2);
         const int gg[3] = {gx, gy, gz};
         const int d1 = dir == 0 ? 1 : 0, d2 = dir == 2 ? 1 : 2;
@@ -791,7 +791,7 @@ __global__ void tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const
 
 cudaError_t launch_skeleton_gather_sc(const TriParams& tp, const double* cellbuf, const double* f, double* out,
                                       double sign, const double* fb, cudaStream_t st) {
-  if (tp.Lx > 1024 || tp.p < 2) return cudaErrorInvalidValue;
+  if (tp.Lx > 1024 || (fb && tp.p < 2)) return cudaErrorInvalidValue;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
