@@ -325,6 +325,11 @@ void upload_family(DevFamily& F, const rm::PatchFamily& P, const DevFamily* shar
       d.ptab = F.upload(pt);
       d.npieces = (int)pt.size();
     }
+    if (!C.frange.empty()) {
+      std::vector<int2> fr(C.frange.size() / 2);
+      for (size_t i = 0; i < fr.size(); ++i) fr[i] = make_int2(C.frange[2 * i], C.frange[2 * i + 1]);
+      d.frange = F.upload(fr);
+    }
     d.nunits = (int)us.size();
     d.ngs = C.ngs;
     d.tile_p0 = C.tile_p0; d.tile_p1 = C.tile_p1;

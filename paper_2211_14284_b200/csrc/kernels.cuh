@@ -63,6 +63,7 @@ struct DClass {
   const int *iccf_lp, *iccb_lp;  // per ICC level: first piece (size nlev + 1)
   const int2* ptab;              // per piece {meta offset, value offset} (class-batched kernel)
   int npieces, pad3;
+  const int2* frange;            // per final row: [lo, hi) of its independent block (null: the whole block)
 };
 constexpr int RM_MAXCOLORS = 12;
 struct ColorStarts { int ncolors; int start[RM_MAXCOLORS + 1]; };

@@ -888,7 +888,14 @@ __global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(const __grid_
 #pragma unroll
       for (int b = 0; b < B; ++b) acc[b] = 0.0;
       if (r < m) {
-        const int c0 = hs * seg, c1 = min(m, c0 + seg);
+        // columns of row r's independent block only (the inverse is block diagonal in the final
+        // order, patches.cpp frange): the edge-star final blocks split into ~p blocks
+        int c0 = hs * seg, c1 = min(m, c0 + seg);
+        if (C.frange) {
+          const int2 fr = C.frange[r];
+          c0 = max(c0, fr.x);
+          c1 = min(c1, fr.y);
+        }
         const double* Sr = S + r;
         for (int c = c0; c < c1; c += 8) {   // 8 column loads in flight, predicated tail
           double s[8];

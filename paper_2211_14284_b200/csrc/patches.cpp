@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <numeric>
@@ -695,6 +696,38 @@ struct Builder {
     for (auto& L : Elev) for (int t : L) order.push_back(G[t]);
     std::vector<int> finalset;
     for (int t = 0; t < nG; ++t) if (alive[t]) finalset.push_back(t);
+    // exact programs: the final Schur block decouples into independent blocks (edge stars: ~p
+    // blocks); order them contiguously (natural order inside each) so that its
+    // inverse is block diagonal in position order and every final row records its block's range
+    std::vector<int> fcomp_start;   // per final index: first index of its block; block end below
+    if (in.factorization == 0 && !finalset.empty()) {
+      const int nf = (int)finalset.size();
+      std::vector<int> par(nf);
+      for (int i = 0; i < nf; ++i) par[i] = i;
+      std::function<int(int)> root = [&](int i) { return par[i] == i ? i : par[i] = root(par[i]); };
+      for (int i = 0; i < nf; ++i)
+        for (int j = 0; j < i; ++j)
+          if (Sb[(size_t)finalset[i] * nG + finalset[j]] || Sb[(size_t)finalset[j] * nG + finalset[i]]) par[root(i)] = root(j);
+      std::vector<int> first(nf, -1), ord;
+      for (int i = 0; i < nf; ++i) if (first[root(i)] < 0) first[root(i)] = i;
+      std::vector<std::pair<int, int>> key(nf);
+      for (int i = 0; i < nf; ++i) key[i] = {first[root(i)], i};
+      std::sort(key.begin(), key.end());
+      std::vector<int> fs2(nf);
+      fcomp_start.assign(nf, 0);
+      for (int i = 0; i < nf; ++i) fs2[i] = finalset[key[i].second];
+      for (int i = 0; i < nf; ++i) fcomp_start[i] = (i > 0 && key[i].first == key[i - 1].first) ? fcomp_start[i - 1] : i;
+      finalset.swap(fs2);
+      C.frange.assign(2 * (size_t)nf, 0);
+      for (int i = 0; i < nf; ++i) {
+        int e = i;
+        while (e < nf && fcomp_start[e] == fcomp_start[i]) ++e;
+        C.frange[2 * i] = fcomp_start[i];
+        C.frange[2 * i + 1] = e;
+      }
+    } else {
+      C.frange.clear();
+    }
     for (int t : finalset) order.push_back(G[t]);
     std::vector<int> pos(n);
     for (int q = 0; q < n; ++q) pos[order[q]] = q;

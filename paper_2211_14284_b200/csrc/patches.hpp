@@ -152,6 +152,8 @@ struct ClassProgram {
   std::vector<int> pcoord, bidx, zlist;
   // structural pattern of the patch matrix (CSR over positions)
   std::vector<int> prow, pcol;
+  // exact programs: per final row, the [lo, hi) range (final indices) of its independent block
+  std::vector<int> frange;
 };
 
 struct PatchFamily {
