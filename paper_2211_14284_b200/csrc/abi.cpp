@@ -1367,16 +1367,26 @@ void do_apply(rm_ctx* c, const double* u, const double* f, double* out, long lon
 // families of one space run back to back on shared padded buffers: the first pads r and zeroes c,
 // the last adds omega c to u
 int run_family(rm_ctx* c, DevFamily& F, const double* r, double* u, double omega, bool r_padded = false,
-               bool zero_c = true, bool combine = true, bool sc_pre_done = false) {
-  if (!F.present) return 0;
+               bool zero_c = true, bool combine = true, bool sc_pre_done = false, const double* u_in = nullptr) {
+  if (!F.present) {
+    if (combine && u_in && u_in != u) CK(cudaMemcpyAsync(u, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    return 0;
+  }
   KPhase kp{c, 4};
   const rm::KTimer kt = kp.timer();
-  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded, zero_c, combine, sc_pre_done));
+  CK(rm::launch_patch_solve(F.launch, r, u, omega, c->st, &kt, r_padded, zero_c, combine, sc_pre_done,
+                            u_in != u ? u_in : nullptr));
   return 3;   // pad(r), persistent patch kernel, u += omega * unpad(c)
 }
 
 // u += omega * P^{-1} r  (r zero on constrained DoFs)
-void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false) {
+// u_in (optional, != u): the primary combine writes u = u_in + omega c (no u_out = u_in copy)
+void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_padded = false,
+                 const double* u_in = nullptr) {
+  if (u_in && u_in != u && (c->decomposition == RM_SC_PH || c->prims.empty())) {
+    CK(cudaMemcpyAsync(u, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    u_in = nullptr;
+  }
   if (c->decomposition == RM_SC_PH) {
     // c = R_I^T A_II^{-1} R_I r + R_G^T S_PH^{-1} R_G r (eq:schur, eq:sc-asm-hiptmair)
     const rm::ScPhParams& P = c->scph;
@@ -1423,7 +1433,8 @@ void add_precond(rm_ctx* c, const double* r, double* u, double omega, bool r_pad
     Phase ph(c, 1);
     const int nf = (int)c->prims.size();
     for (int o = 0; o < nf; ++o)
-      c->launches[1] += run_family(c, c->prims[o], r, u, omega, r_padded || o > 0, o == 0, o == nf - 1);
+      c->launches[1] += run_family(c, c->prims[o], r, u, omega, r_padded || o > 0, o == 0, o == nf - 1, false,
+                                   o == nf - 1 ? u_in : nullptr);
   }
   if (c->pots[0].present) {
     Phase ph(c, 2);
@@ -1623,22 +1634,19 @@ void relax_impl(rm_ctx* c, const double* f, const double* u_in, double* u_out, d
   if (sc_fused(c)) {
     const rm::PatchLaunch& L = c->prims[0].launch;
     residual_sc_fused(c, u_in, f, L);
-    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     Phase ph(c, 1);
-    c->launches[1] += run_family(c, c->prims[0], L.rpad, u_out, omega, true, true, true, true);
+    c->launches[1] += run_family(c, c->prims[0], L.rpad, u_out, omega, true, true, true, true, u_in);
     return;
   }
   if (fused_k0(c)) {
     // the residual goes straight into the primary family's padded (TMA) layout: no pad pass
     const rm::PatchLaunch& L = c->prims[0].launch;
     do_apply(c, u_in, f, L.rpad, L.pad.lxp[0]);
-    if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-    add_precond(c, L.rpad, u_out, omega, true);
+    add_precond(c, L.rpad, u_out, omega, true, u_in);
     return;
   }
   do_apply(c, u_in, f, c->d_r);
-  if (u_out != u_in) CK(cudaMemcpyAsync(u_out, u_in, c->ndof * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-  add_precond(c, c->d_r, u_out, omega);
+  add_precond(c, c->d_r, u_out, omega, false, u_in);
 }
 
 }  // namespace

@@ -226,7 +226,8 @@ size_t patch_batch_smem(int box_total, int mr_max, int B, int NT);
 // sharing their padded buffers run back to back)
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
                                const KTimer* kt = nullptr, bool r_padded = false, bool zero_c = true,
-                               bool combine = true, bool sc_pre_done = false);
+                               bool combine = true, bool sc_pre_done = false, const double* u_in = nullptr);
+// (u_in: the combine writes u = u_in + omega c instead of u += omega c)
 // ICC-SC pre step, part 1, on the residual of the SC-fused path: the cell-interior entries of rpad
 // hold sign * (A u)_I (trilinear apply with skip_gather); r_I = f_I + rpad_I is completed in place
 // and the condensation line sums go to L.sc_fb (f: the vector layout, x-stride lx)

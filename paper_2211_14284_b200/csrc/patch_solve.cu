@@ -977,8 +977,9 @@ __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __
   rp[g] = (x < P.len[m][0]) ? r[P.off[m] + yz * P.len[m][0] + x] : 0.0;
 }
 
-__global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* __restrict__ u,
-                                  double omega, long long n, int skip_p) {
+__global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* u,
+                                  double omega, long long n, int skip_p, const double* uin) {
+  // u = (uin ? uin : u) + omega * unpad(cp): out of place the sweep needs no u_out = u_in copy
   // one (y, z) row of one component per warp, grid-stride: no per-element 64-bit division;
   // skip_p > 0 (one component, static condensation with the post step writing u): the cell
   // interiors are already done, only the skeleton entries (an index at a multiple of p) remain
@@ -991,10 +992,10 @@ __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const dou
       if (r < 0) continue;
       const long long ub = P.off[m] + (long long)r * Lx, cb = P.poff[m] + (long long)r * P.lxp[m];
       if (skip_p > 0 && (r % Ly) % skip_p != 0 && (r / Ly) % skip_p != 0) {   // interior row: x skeleton only
-        for (int x = lane * skip_p; x < Lx; x += 32 * skip_p) u[ub + x] += omega * cp[cb + x];
+        for (int x = lane * skip_p; x < Lx; x += 32 * skip_p) u[ub + x] = (uin ? uin[ub + x] : u[ub + x]) + omega * cp[cb + x];
         continue;
       }
-      for (int x = lane; x < Lx; x += 32) u[ub + x] += omega * cp[cb + x];
+      for (int x = lane; x < Lx; x += 32) u[ub + x] = (uin ? uin[ub + x] : u[ub + x]) + omega * cp[cb + x];
     }
     rows_before += nrow;
   }
@@ -1265,7 +1266,7 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, cudaStream_t st) {
-  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0);
+  unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0, nullptr);
   return cudaGetLastError();
 }
 
@@ -1294,12 +1295,13 @@ cudaError_t launch_sc_pre_fused(const PatchLaunch& L, const double* f, long long
 }
 
 cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u, double omega, cudaStream_t st,
-                               const KTimer* kt, bool r_padded, bool zero_c, bool combine, bool sc_pre_done) {
+                               const KTimer* kt, bool r_padded, bool zero_c, bool combine, bool sc_pre_done,
+                               const double* u_in) {
   if (L.npatch <= 0) {   // an empty family still does its part of a shared sequence
     if (!L.cpad) return cudaSuccess;
     if (!r_padded) pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
     if (zero_c) cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st);
-    if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0);
+    if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0, u_in);
     return cudaGetLastError();
   }
   const long long n = L.pad.off[L.pad.ncomp];
@@ -1396,7 +1398,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
                                        L.pad.len[0][0]);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, 0);
+  if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, 0, u_in);
   return cudaGetLastError();
 }
 
