@@ -228,7 +228,8 @@ def measure(w, cfg, args, world, rank, local, torch, dist, rmb, with_e2e=True):
     k_launch = max(launches[4] / args.steps, 1)
     prim_bytes = 8 * info["factor_nnz"] + 3 * 8 * n
     achieved = prim_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
-    roof_patch = {"kernel": "patch_stream_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+    pk_name = "patch_batch_kernel" if info.get("batched_families", 0) else "patch_stream_kernel"
+    roof_patch = {"kernel": pk_name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                   "frac": achieved / hbm, "traffic": ncu_traffic(cfg), "peak_kind": peak_kind,
                   "bytes_per_launch": prim_bytes / k_launch, "launches_per_step": k_launch,
                   "launch_ms_avg": k_ms / k_launch, "share_of_step": k_ms / ms if ms > 0 else None,
@@ -248,7 +249,7 @@ def measure(w, cfg, args, world, rank, local, torch, dist, rmb, with_e2e=True):
     else:
         ab = 3 * 8 * n
         gbs = ab / (a_ms * 1e-3) / 1e9 if a_ms > 0 else 0.0
-        roof_apply = {"kernel": "apply_q_kernel" if w.space == 0 else "apply_cells_kernel", "bound": "hbm",
+        roof_apply = {"kernel": ("apply_q_kernel", "apply_nce_kernel", "apply_ncf_kernel")[w.space], "bound": "hbm",
                       "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "traffic": None,
                       "peak_kind": peak_kind, "bytes_per_launch": ab / a_launch, "launches_per_step": a_launch,
                       "launch_ms_avg": a_ms / a_launch, "share_of_step": a_ms / ms if ms > 0 else None,

@@ -12,7 +12,7 @@
 // One CTA per cell: the cell's u in shared memory, then 3 (k = 1) / 2 (k = 2) pointwise stages
 // with one barrier each -- O(p^3) per cell, no line loops.  Output: one launch over all cells
 // (no colours); entries interior to the cell (in every P direction) are final and stored
-// directly as f - A u; skeleton entries go to the per-cell buffer and kform_gather_kernel sums
+// directly as f - A u; skeleton entries go to the per-cell buffer and kform_gather_rows_kernel sums
 // the <= 4 cell contributions of each in a fixed order (bitwise deterministic).
 #include "kernels.cuh"
 
@@ -298,7 +298,7 @@ __device__ __forceinline__ double aline(const double* __restrict__ sA, const dou
 // across), in three pointwise stages on the cell window (x: B u, A u; y: B (Bu), A (Bu), B (Au)
 // combined into Q = beta s_M B B u + alpha (s_x B A u + s_y A B u); z: v = B_z Q + alpha s_z A_z (B B u)).
 // One CTA per cell, ONE launch over all cells; interior entries final (out = f + sign v, padded
-// x-stride ldx), skeleton entries to the cell buffer, summed by kform_gather_kernel.
+// x-stride ldx), skeleton entries to the cell buffer, summed by kform_gather_rows_kernel.
 template <int P>
 __global__ void __launch_bounds__(KF_THREADS) apply_q_pw_kernel(const __grid_constant__ OpParams op,
                                                                  const double* __restrict__ alpha,
@@ -357,59 +357,72 @@ __global__ void __launch_bounds__(KF_THREADS) apply_q_pw_kernel(const __grid_con
 
 // out[g] = f[g] + sign * sum over the <= 4 cells carrying skeleton DoF g of their buffered
 // contributions (cells in z, y, x order); constrained entries 0; cell-interior entries were
-// stored by the apply kernel and are left alone.  One thread per DoF.
-__global__ void kform_gather_kernel(const __grid_constant__ OpParams op, const double* __restrict__ cellbuf,
-                                    const double* __restrict__ f, double* __restrict__ out, double sign,
-                                    long long ndof, int nloc, long long ldx) {
-  const int p = op.p;
-  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < ndof; g += (long long)gridDim.x * blockDim.x) {
-    int m = 0;
-    while (m + 1 < op.ncomp && g >= op.off[m + 1]) ++m;
-    // 32-bit index math (component sizes < 2^31)
-    const int rr = (int)(g - op.off[m]);
-    const int Lx = (int)op.len[m][0], Ly = (int)op.len[m][1];
-    const int q = rr / Lx;
-    const int idx[3] = {rr - q * Lx, q % Ly, q / Ly};
-    int c0[3], a0[3], two[3], ls[3];
-    bool skel = false, con = false;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const bool P_ = op.fam[m][d] == 0;
-      ls[d] = P_ ? p + 1 : p;
-      int cc = idx[d] / p;
-      const int aa = idx[d] - cc * p;
-      two[d] = 0;
-      if (P_ && aa == 0) {
-        skel = true;
-        if (cc == 0) { c0[d] = 0; a0[d] = 0; }
-        else if (cc == op.n[d]) { c0[d] = cc - 1; a0[d] = p; }
-        else { c0[d] = cc - 1; a0[d] = p; two[d] = 1; }   // cells cc - 1 (local p) and cc (local 0)
-        con |= (cc == 0 && (op.gamma_d & (1u << (2 * d)))) || (cc == op.n[d] && (op.gamma_d & (2u << (2 * d))));
-      } else {
-        c0[d] = cc; a0[d] = aa;
+// stored by the apply kernel and are left alone.
+// The same sums, row by row: one (y, z) row of one component per warp, SKELETON entries only
+// (the apply kernels store the cell-interior entries final, out = f + sign A_K u).  A row whose y
+// and z indices are both cell-interior visits only its x-boundary entries (x in the P family) or
+// nothing (x in the DP family); the per-DoF divisions and the interior passes of the one-thread-
+// per-DoF gather are gone.  Same addends in the same order (cells in z, y, x order): bitwise equal.
+__device__ __forceinline__ void kf_dir(int idx, bool P_, int p, int n, unsigned gam, int d, int& c0, int& a0, int& two,
+                                       bool& skel, bool& con) {
+  const int cc = idx / p, aa = idx - cc * p;
+  two = 0;
+  skel = false;
+  con = false;
+  if (P_ && aa == 0) {
+    skel = true;
+    if (cc == 0) { c0 = 0; a0 = 0; }
+    else if (cc == n) { c0 = cc - 1; a0 = p; }
+    else { c0 = cc - 1; a0 = p; two = 1; }
+    con = (cc == 0 && (gam & (1u << (2 * d)))) || (cc == n && (gam & (2u << (2 * d))));
+  } else {
+    c0 = cc; a0 = aa;
+  }
+}
+
+__global__ void kform_gather_rows_kernel(const __grid_constant__ OpParams op, const double* __restrict__ cellbuf,
+                                         const double* __restrict__ f, double* __restrict__ out, double sign, int nloc,
+                                         long long ldx) {
+  const int p = op.p, lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * (blockDim.x >> 5);
+  int rows_before = 0, lo = 0;
+  for (int m = 0; m < op.ncomp; ++m) {
+    const int Lx = (int)op.len[m][0], Ly = (int)op.len[m][1], Lz = (int)op.len[m][2], nrow = Ly * Lz;
+    const bool Px = op.fam[m][0] == 0, Py = op.fam[m][1] == 0, Pz = op.fam[m][2] == 0;
+    const int ls0 = Px ? p + 1 : p, ls1 = Py ? p + 1 : p, ls2 = Pz ? p + 1 : p;
+    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) - rows_before; r < nrow; r += wstride) {
+      if (r < 0) continue;
+      const int iy = r % Ly, iz = r / Ly;
+      int cy0, ay0, twy, cz0, az0, twz;
+      bool sy, sz, cy, cz;
+      kf_dir(iy, Py, p, op.n[1], op.gamma_d, 1, cy0, ay0, twy, sy, cy);
+      kf_dir(iz, Pz, p, op.n[2], op.gamma_d, 2, cz0, az0, twz, sz, cz);
+      const bool rskel = sy || sz, rcons = cy || cz;
+      if (!rskel && !Px) continue;   // no skeleton entry in this row
+      const int cnt = rskel ? Lx : op.n[0] + 1;
+      const long long fb = op.off[m] + (long long)r * Lx;
+      const long long ob = ldx > 0 ? (long long)r * ldx : fb;
+      for (int t = lane; t < cnt; t += 32) {
+        const int ix = rskel ? t : t * p;
+        int cx0, ax0, twx;
+        bool sx, cxn;
+        kf_dir(ix, Px, p, op.n[0], op.gamma_d, 0, cx0, ax0, twx, sx, cxn);
+        if (rcons || cxn) { out[ob + ix] = 0.0; continue; }
+        double s = 0.0;
+        for (int kz = 0; kz <= twz; ++kz)
+          for (int ky = 0; ky <= twy; ++ky)
+            for (int kx = 0; kx <= twx; ++kx) {
+              const int cx = cx0 + kx, ax = kx ? 0 : ax0;
+              const int cyy = cy0 + ky, ay = ky ? 0 : ay0;
+              const int czz = cz0 + kz, az = kz ? 0 : az0;
+              const long long cell = ((long long)czz * op.n[1] + cyy) * op.n[0] + cx;
+              s += cellbuf[cell * nloc + lo + (az * ls1 + ay) * ls0 + ax];
+            }
+        out[ob + ix] = (f ? f[fb + ix] : 0.0) + sign * s;
       }
     }
-    if (!skel) continue;   // cell-interior entry: stored by the apply kernel
-    // output index: the vector layout, or (one component) a padded x-stride ldx
-    const long long go = ldx > 0 ? ((long long)idx[2] * Ly + idx[1]) * ldx + idx[0] : g;
-    if (con) { out[go] = 0.0; continue; }
-    int lo = 0;
-    for (int t = 0; t < m; ++t) {
-      int sz = 1;
-      for (int d = 0; d < 3; ++d) sz *= (op.fam[t][d] == 0 ? p + 1 : p);
-      lo += sz;
-    }
-    double s = 0.0;
-    for (int kz = 0; kz <= two[2]; ++kz)
-      for (int ky = 0; ky <= two[1]; ++ky)
-        for (int kx = 0; kx <= two[0]; ++kx) {
-          const int cx = c0[0] + kx, ax = kx ? 0 : a0[0];
-          const int cy = c0[1] + ky, ay = ky ? 0 : a0[1];
-          const int cz = c0[2] + kz, az = kz ? 0 : a0[2];
-          const long long cell = ((long long)cz * op.n[1] + cy) * op.n[0] + cx;
-          s += cellbuf[cell * nloc + lo + (az * ls[1] + ay) * ls[0] + ax];
-        }
-    out[go] = (f ? f[g] : 0.0) + sign * s;
+    rows_before += nrow;
+    lo += ls0 * ls1 * ls2;
   }
 }
 
@@ -477,7 +490,8 @@ cudaError_t launch_apply_kform(const OpParams& op, const double* alpha, const do
   if (e != cudaSuccess) return e;
   const int p = op.p;
   const int nloc = op.k == 0 ? (p + 1) * (p + 1) * (p + 1) : (op.k == 1 ? 3 * p * (p + 1) * (p + 1) : 3 * (p + 1) * p * p);
-  kform_gather_kernel<<<148 * 16, 256, 0, st>>>(op, cellbuf, f, out, sign, ndof, nloc, op.k == 0 ? op.ldx_out : 0);
+  kform_gather_rows_kernel<<<148 * 16, 256, 0, st>>>(op, cellbuf, f, out, sign, nloc, op.k == 0 ? op.ldx_out : 0);
+  (void)ndof;
   if (nlaunch) *nlaunch = 2;
   return cudaGetLastError();
 }
