@@ -205,7 +205,7 @@ __device__ __forceinline__ void apply_A(const double* __restrict__ Ah, const dou
 }
 
 template <int P>
-__global__ void __launch_bounds__(256) apply_q_kernel(const __grid_constant__ OpParams op,
+__global__ void __launch_bounds__(256, 5) apply_q_kernel(const __grid_constant__ OpParams op,
                                                        const double* __restrict__ alpha,
                                                        const double* __restrict__ beta, int coef_const,
                                                        const double* __restrict__ hpow,

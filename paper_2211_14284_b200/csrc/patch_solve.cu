@@ -1100,7 +1100,7 @@ __global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* _
 __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
                                const double* __restrict__ cc, const double* __restrict__ cw, const int* __restrict__ nk,
                                const double* __restrict__ rp, double* __restrict__ cp, long long nint,
-                               double* __restrict__ u, double omega, long long lx) {
+                               double* u, double omega, long long lx, const double* uin) {
   // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
   __shared__ double kt[3][16];   // D_ii, D_i0, D_ip: lane-varying indices (shared, not the param bank)
   if (threadIdx.x < 48) kt[threadIdx.x >> 4][threadIdx.x & 15] =
@@ -1134,7 +1134,10 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   s = fma(c5, cp[sc_idx(G, x + i, y + j, z + p)], s);
   const long long gi = sc_idx(G, x + i, y + j, z + k);
   const double c = dv * (nk[K] * rp[gi] - s);
-  if (u) u[((z + k) * G.ly + y + j) * lx + x + i] += omega * c;   // fused combine (one rank): u directly
+  if (u) {   // fused combine: u = (uin ? uin : u) + omega c_I directly (the combine skips the interiors)
+    const long long gu = ((z + k) * G.ly + y + j) * lx + x + i;
+    u[gu] = (uin ? uin[gu] : u[gu]) + omega * c;
+  }
   else cp[gi] = c;
 }
 
@@ -1391,12 +1394,17 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
     const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
-    // c_I to cpad; the combine below adds omega c to u for every DoF (measured: adding omega c_I
-    // to u inside the post step and skipping the interiors in the combine is slower -- the post
-    // step's scattered read-modify-write of u costs more than the combine's streaming pass)
-    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint, nullptr, omega,
-                                       L.pad.len[0][0]);
+    // c_I to cpad; the combine below writes u for every DoF (measured twice: writing u_out = u_in +
+    // omega c_I from the post step and a skeleton-only combine is slower -- cfg5 patch stage 1.562
+    // -> 1.587 ms in round 2 -- the post step's scattered u traffic costs more than the streaming pass)
+    const bool fuse = combine && L.pad.ncomp == 1 && exp_env("RM_POST_FUSED") != nullptr;
+    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint,
+                                       fuse ? u : nullptr, omega, L.pad.len[0][0], u_in);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (fuse) {
+      unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, L.sc_p, u_in);
+      return cudaGetLastError();
+    }
   }
   if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, n, 0, u_in);
   return cudaGetLastError();
