@@ -706,7 +706,7 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
 // and, for face-interior DoFs, minus the condensation line sums e of the (<= 2) cells sharing the
 // face (lower cell first; fb != null) -- the same operations, in the same order, as the gather
 // followed by sc_face_kernel.  Rows with y and z off the cell boundaries only visit the x-boundary DoFs.
-__global__ void tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
+__global__ void __launch_bounds__(256, 6) tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                      const double* __restrict__ f, double* __restrict__ out, double sign,
                                      const double* __restrict__ fb) {
   __shared__ int4 xtab[1024];

@@ -1042,23 +1042,34 @@ __global__ void sc_cell_kernel(const __grid_constant__ ScGeom G, const double* _
     y[I] = dk[I] * r;
   }
   __syncthreads();
-  // one thread per (face, line): the line through face position (a, b) along the face normal
-  for (int q = threadIdx.x; q < 6 * nf; q += blockDim.x) {
-    const int f = q / nf, pos = q - f * nf, dir = f >> 1;
+  // one thread per (direction, line): the line through face position (a, b) along the face
+  // normal serves both faces of that direction (the - face with D_i0, the + face with D_ip): one
+  // pass over the weights and y, two sums (each in the order of the one-face loop: bitwise equal)
+  for (int q = threadIdx.x; q < 3 * nf; q += blockDim.x) {
+    const int dir = q / nf, pos = q - dir * nf;
     const int a = pos % pm, b = pos / pm;
     const int I0 = dir == 0 ? (b * pm + a) * pm : (dir == 1 ? b * pm * pm + a : b * pm + a);
     const int st = dir == 0 ? 1 : (dir == 1 ? pm : nf);
-    double e = 0.0;
+    double e0 = 0.0, e1 = 0.0;
     if (G.cmp) {   // the line runs along the face normal: interior index l + 1 of the 1D tables
       const double* wf = cw + ((size_t)K * 3 + dir) * ni;
-      const double* kf = (f & 1) ? G.kp : G.k0;
-      for (int l = 0; l < pm; ++l)
-        e = fma(__dmul_rn(__dmul_rn(G.kd[l + 1], wf[I0 + l * st]), kf[l + 1]), y[I0 + l * st], e);
+#pragma unroll 7
+      for (int l = 0; l < pm; ++l) {
+        const double kw = __dmul_rn(G.kd[l + 1], wf[I0 + l * st]), yv = y[I0 + l * st];
+        e0 = fma(__dmul_rn(kw, G.k0[l + 1]), yv, e0);
+        e1 = fma(__dmul_rn(kw, G.kp[l + 1]), yv, e1);
+      }
     } else {
-      const double* cf = cc + ((size_t)K * 6 + f) * ni;
-      for (int l = 0; l < pm; ++l) e = fma(cf[I0 + l * st], y[I0 + l * st], e);
+      const double* cf0 = cc + ((size_t)K * 6 + 2 * dir) * ni;
+      const double* cf1 = cf0 + ni;
+      for (int l = 0; l < pm; ++l) {
+        const double yv = y[I0 + l * st];
+        e0 = fma(cf0[I0 + l * st], yv, e0);
+        e1 = fma(cf1[I0 + l * st], yv, e1);
+      }
     }
-    fb[((size_t)K * 6 + f) * nf + pos] = e;
+    fb[((size_t)K * 6 + 2 * dir) * nf + pos] = e0;
+    fb[((size_t)K * 6 + 2 * dir + 1) * nf + pos] = e1;
   }
 }
 
