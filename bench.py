@@ -296,8 +296,19 @@ def measure(w, cfg, args, world, rank, local, torch, dist, rmb, with_e2e=True):
                         "device_numeric_s": info["setup_device_numeric_seconds"]},
               "patches": info["n_patches"] + info["n_patches_potential"],
               "factor_blocks": info["n_factor_blocks"]}
-    res = {"value": value, "ms_per_step": ms, "config": config, "roofline": roof, "e2e": e2e, "clocks": clocks,
-           "gpu_launches": int(sum(launches[:4]))}
+    # the whole sweep against its roofline, T_roof = sum over phases of
+    # max(bytes / BW, flops / F64) with algorithmic bytes (u, f in, u_out out; one read of every
+    # factor entry) and flops (trilinear apply: TRI_FLOPS_PER_CELL per cell; solves 4 per factor
+    # entry; the Cartesian sum-factorised apply's O(p) flops per DoF are below its byte term)
+    ncell_all = wg.nx * wg.ny * wg.nz
+    t_apply = max(3 * 8 * n / (hbm * 1e9), (ncell_all * TRI_FLOPS_PER_CELL if wg.perturb > 0 else 0) / (FP64_PEAK_TFLOPS * 1e12))
+    t_solve = max(8 * info["factor_nnz"] / (hbm * 1e9), 4 * info["factor_nnz"] / (FP64_PEAK_TFLOPS * 1e12))
+    t_roof_ms = (t_apply + t_solve) * 1e3
+    sweep_roof = {"t_roof_ms": t_roof_ms, "t_ms": ms, "frac": t_roof_ms / ms if ms > 0 else None,
+                  "terms_ms": {"apply": t_apply * 1e3, "patch_solves": t_solve * 1e3},
+                  "bw_GBs": hbm, "f64_TFs": FP64_PEAK_TFLOPS, "basis": "SURVEY 8(d) T_roof / T_measured"}
+    res = {"value": value, "ms_per_step": ms, "config": config, "roofline": roof, "sweep_roofline": sweep_roof,
+           "e2e": e2e, "clocks": clocks, "gpu_launches": int(sum(launches[:4]))}
     ctx.close()
     torch.cuda.empty_cache()
     return res
@@ -364,7 +375,7 @@ def main():
         ws = ri.CONFIGS[args.secondary]
         r2 = measure(ws, args.secondary, args, world, rank, local, torch, dist, rmb, with_e2e=not args.no_e2e)
         sec = {"value": r2["value"], "unit": "DoFs/s", "ms_per_step": r2["ms_per_step"], "config": r2["config"],
-               "roofline": r2["roofline"], "e2e": r2["e2e"], "clocks": r2["clocks"],
+               "roofline": r2["roofline"], "sweep_roofline": r2["sweep_roofline"], "e2e": r2["e2e"], "clocks": r2["clocks"],
                "gpu_launches": r2["gpu_launches"]}
 
     cpu = None
@@ -380,8 +391,8 @@ def main():
         line = {"metric": metric, "value": res["value"], "unit": "DoFs/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (rm_inputs seeded recipe)",
-                "config": res["config"], "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": res["e2e"],
-                "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
+                "config": res["config"], "roofline": res["roofline"], "sweep_roofline": res["sweep_roofline"],
+                "cpu_baseline": cpu, "e2e": res["e2e"], "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
         if sec is not None:
             line["secondary"] = sec
         print(json.dumps(line), flush=True)
