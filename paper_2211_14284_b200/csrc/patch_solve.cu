@@ -1120,9 +1120,10 @@ __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* _
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
   const int I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I >= ni) return;
-  const long long K = blockIdx.y;
+  const int K32 = (int)blockIdx.y;   // 32-bit decode (the 64-bit divisions were most of the instructions)
+  const long long K = K32;
   const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / (pm * pm) + 1;
-  const int cx = (int)(K % G.n[0]), cy = (int)((K / G.n[0]) % G.n[1]), cz = (int)(K / ((long long)G.n[0] * G.n[1]));
+  const int cx = K32 % G.n[0], cy = (K32 / G.n[0]) % G.n[1], cz = K32 / (G.n[0] * G.n[1]);
   (void)nint;
   const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
   const double dv = dinv[K * ni + I];
