@@ -358,7 +358,7 @@ cudaError_t launch_apply_cartesian(const OpParams& op, const double* alpha, cons
                                    const double* hpow, const double* u, const double* f, double* out,
                                    long long ndof, cudaStream_t st, int* nlaunch, const KTimer* kt,
                                    double* cellbuf) {
-  if (cellbuf && op.k == 0 && op.ncomp == 1 && op.len[0][0] <= 1024 && !exp_env("RM_APPLY_PW")) {
+  if (cellbuf && op.k == 0 && op.ncomp == 1 && !exp_env("RM_APPLY_PW")) {
     // H(grad): ONE launch of the line-stage kernel over every cell (cell-interior DoFs final,
     // out = f + sign A_K u; skeleton entries to the cell buffer), then the skeleton-only gather
     const double sgn = f ? -1.0 : 1.0;

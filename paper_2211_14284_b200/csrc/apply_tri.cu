@@ -639,21 +639,34 @@ __global__ void __launch_bounds__(TRI_THREADS, 1) apply_tri_kernel(const __grid_
 // on a cell face, edge or vertex: sign * the sum over the cells containing g of their local
 // result, cells ascending in z, y, x: deterministic); constrained entries 0.  One warp per grid
 // row (gy, gz), grid-stride over rows; 32-bit index math.
+// x decode of the gathers: the (<= 2) cells containing gx and the local indices, and the flags
+// (bit0: on a cell boundary, bit1: constrained); tabulated in shared memory for gx < 1024 and
+// computed on the fly beyond (meshes with more than 1024 x entries)
+constexpr int kXTab = 1024;
+__device__ __forceinline__ void tri_xdec(const TriParams& tp, int gx, int4& xe, int& fl) {
+  const int p = tp.p;
+  int cc = gx / p;
+  if (cc >= tp.n[0]) cc = tp.n[0] - 1;
+  const int aa = gx - cc * p;
+  xe = (aa == 0 && cc > 0) ? make_int4(cc - 1, p, cc, 0) : make_int4(cc, aa, 0, -1);
+  fl = (aa == 0 || aa == p ? 1 : 0) | (tri_cons(gx, (long long)tp.n[0] * p, tp.gamma_d, 0) ? 2 : 0);
+}
+
 __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                   const double* __restrict__ f, double* __restrict__ out, double sign) {
   // per-x table (once per block): the (<= 2) cells containing gx and the local indices, skeleton
   // and constraint flags; per row the (<= 2 x 2) (cell-row, local) bases; every loop has constant
   // bounds (registers, no local memory) and one table lookup replaces the per-DoF divisions
-  __shared__ int4 xtab[1024];   // (cell0, local0, cell1, local1); local1 < 0: one cell
-  __shared__ unsigned char xfl[1024];   // bit0: on a cell boundary, bit1: constrained
+  __shared__ int4 xtab[kXTab];   // (cell0, local0, cell1, local1); local1 < 0: one cell
+  __shared__ unsigned char xfl[kXTab];   // bit0: on a cell boundary, bit1: constrained
   const int Lx = (int)tp.Lx, Ly = (int)tp.Ly, Lz = (int)tp.Lz;
   const int p = tp.p, P1 = p + 1, n3 = P1 * P1 * P1;
-  for (int gx = threadIdx.x; gx < Lx; gx += blockDim.x) {
-    int cc = gx / p;
-    if (cc >= tp.n[0]) cc = tp.n[0] - 1;
-    const int aa = gx - cc * p;
-    xtab[gx] = (aa == 0 && cc > 0) ? make_int4(cc - 1, p, cc, 0) : make_int4(cc, aa, 0, -1);
-    xfl[gx] = (unsigned char)((aa == 0 || aa == p ? 1 : 0) | (tri_cons(gx, (long long)tp.n[0] * p, tp.gamma_d, 0) ? 2 : 0));
+  for (int gx = threadIdx.x; gx < Lx && gx < kXTab; gx += blockDim.x) {
+    int4 xe;
+    int fl;
+    tri_xdec(tp, gx, xe, fl);
+    xtab[gx] = xe;
+    xfl[gx] = (unsigned char)fl;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -683,11 +696,12 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
     const long long fbase = (long long)row * Lx, obase = (long long)row * ldx;
     for (int gx = lane; gx < Lx; gx += 32) {
       const long long g = obase + gx;
-      const int fl = xfl[gx];
+      int4 xe;
+      int fl;
+      if (gx < kXTab) { xe = xtab[gx]; fl = xfl[gx]; } else tri_xdec(tp, gx, xe, fl);
       if (rcons || (fl & 2)) { out[g] = 0.0; continue; }
       const double fv = f ? f[fbase + gx] : 0.0;
       if (!rskel && !(fl & 1)) { out[g] = fv + out[g]; continue; }   // cell interior (stored by the apply)
-      const int4 xe = xtab[gx];
       auto at = [&](int rb, int ro, int c, int a) { return cellbuf[(size_t)(rb + c) * n3 + ro + a]; };
       double s = at(rb00, ro00, xe.x, xe.y);
       if (xe.w >= 0) s += at(rb00, ro00, xe.z, xe.w);
@@ -709,16 +723,16 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
 __global__ void __launch_bounds__(256, 6) tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                      const double* __restrict__ f, double* __restrict__ out, double sign,
                                      const double* __restrict__ fb) {
-  __shared__ int4 xtab[1024];
-  __shared__ unsigned char xfl[1024];
+  __shared__ int4 xtab[kXTab];
+  __shared__ unsigned char xfl[kXTab];
   const int Lx = (int)tp.Lx, Ly = (int)tp.Ly;
   const int p = tp.p, P1 = p + 1, n3 = P1 * P1 * P1, pm = p - 1, nf = pm * pm;
-  for (int gx = threadIdx.x; gx < Lx; gx += blockDim.x) {
-    int cc = gx / p;
-    if (cc >= tp.n[0]) cc = tp.n[0] - 1;
-    const int aa = gx - cc * p;
-    xtab[gx] = (aa == 0 && cc > 0) ? make_int4(cc - 1, p, cc, 0) : make_int4(cc, aa, 0, -1);
-    xfl[gx] = (unsigned char)((aa == 0 || aa == p ? 1 : 0) | (tri_cons(gx, (long long)tp.n[0] * p, tp.gamma_d, 0) ? 2 : 0));
+  for (int gx = threadIdx.x; gx < Lx && gx < kXTab; gx += blockDim.x) {
+    int4 xe;
+    int fl;
+    tri_xdec(tp, gx, xe, fl);
+    xtab[gx] = xe;
+    xfl[gx] = (unsigned char)fl;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -751,11 +765,12 @@ __global__ void __launch_bounds__(256, 6) tri_gather_sc_kernel(const __grid_cons
     for (int t = lane; t < nx_; t += 32) {
       const int gx = rskel ? t : t * p;
       const long long g = obase + gx;
-      const int fl = xfl[gx];
+      int4 xe;
+      int fl;
+      if (gx < kXTab) { xe = xtab[gx]; fl = xfl[gx]; } else tri_xdec(tp, gx, xe, fl);
       if (rcons || (fl & 2)) { out[g] = 0.0; continue; }
       if (!(fl & 1) && !rskel) continue;   // cell interior (completed by the SC pre step)
       const double fv = f ? f[fbase + gx] : 0.0;
-      const int4 xe = xtab[gx];
       auto at = [&](int rb, int ro, int c, int a) { return cellbuf[(size_t)(rb + c) * n3 + ro + a]; };
       double s = at(rb00, ro00, xe.x, xe.y);
       if (xe.w >= 0) s += at(rb00, ro00, xe.z, xe.w);
@@ -791,7 +806,7 @@ __global__ void __launch_bounds__(256, 6) tri_gather_sc_kernel(const __grid_cons
 
 cudaError_t launch_skeleton_gather_sc(const TriParams& tp, const double* cellbuf, const double* f, double* out,
                                       double sign, const double* fb, cudaStream_t st) {
-  if (tp.Lx > 1024 || (fb && tp.p < 2)) return cudaErrorInvalidValue;
+  if (fb && tp.p < 2) return cudaErrorInvalidValue;
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -814,7 +829,7 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (tp.p + 1 > K1 || tp.nq > NQP || tp.Lx > 1024) return cudaErrorInvalidValue;
+  if (tp.p + 1 > K1 || tp.nq > NQP) return cudaErrorInvalidValue;
   const long long ncell = (long long)tp.n[0] * tp.n[1] * tp.n[2];
   const long long nd = tp.Lx * tp.Ly * tp.Lz;
   if (ncell <= 0) return cudaSuccess;
@@ -840,7 +855,6 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
 
 cudaError_t launch_skeleton_gather(const TriParams& tp, const double* cellbuf, const double* f, double* out, double sign,
                                    cudaStream_t st) {
-  if (tp.Lx > 1024) return cudaErrorInvalidValue;   // per-x table of the gather
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;

@@ -91,6 +91,9 @@ CASES = [
     ("cfg2-sc-3^3-p4", dataclasses.replace(ri.CONFIGS[2].with_mesh(3).with_p(4), decomposition="sc-pafw"), 1e-11),
     ("cfg5-sc-3^3-p3", dataclasses.replace(ri.CONFIGS[5].with_mesh(3).with_p(3), decomposition="sc-pafw"), 1e-11),
     ("cfg5-sc-2^3-p7", dataclasses.replace(ri.CONFIGS[5].with_mesh(2).with_p(7), decomposition="sc-pafw"), 1e-11),
+    # more than 1024 x entries (Lx = 342 * 3 + 1): the gathers' per-x tables end, x decoded on the fly
+    ("cfg2-long-x", ri.CONFIGS[2].with_mesh(342, 1, 1).with_p(3), 1e-11),
+    ("cfg5-long-x", ri.CONFIGS[5].with_mesh(342, 2, 2).with_p(3), 1e-11),
     # row f2 (k = 1, 2): SC-PH (eq:sc-asm-hiptmair), interface-only star solves + interiors once.
     # The explicit condensation (S = A_GG - A_GI A_II^-1 A_IG, c_I = y_I - A_II^-1 A_IG c_G) cancels:
     # the oracle's own two exact assemblies differ by 1.5e-11 (3^3, p = 4) and 3.2e-11 (2^3, p = 6),
