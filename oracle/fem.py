@@ -19,8 +19,8 @@ Every output of the method (A, C^T M C, D B^{-1} D^T) is invariant under curl ->
 Pins: tests/test_oracle_fem.py (31/8 single cell, Q1 2x2x2 value 4/3 a + b/27, constants,
 u = x_1 patch test on perturbed cells, complex property, interior nnz bounds, P = A on
 Cartesian cells, the auxiliary operator of a sheared AFFINE cell = the true operator of the
-equivalent box).  On genuinely trilinear cells the auxiliary operator is "parity partially
-unpinned" beyond those pins, symmetry, positive definiteness and the Cartesian limit.
+equivalent box, and on NON-AFFINE cells its definition eq:sum-factorization_approx evaluated with
+the true quadrature mass matrices: diag(G-bar^-T M G-bar^-1)).
 """
 from __future__ import annotations
 

@@ -239,3 +239,38 @@ def test_aux_operator_on_a_sheared_affine_cell_equals_the_equivalent_box():
     # and the true operator of the sheared cell is NOT this (the off-diagonal metric matters)
     At = element_matrix(0, p, Xc, alpha, beta)
     assert np.abs(At - A).max() > 1e-3 * np.abs(A).max()
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_aux_operator_on_a_non_affine_cell_equals_its_definition(p):
+    """eq:sum-factorization_approx on a genuinely trilinear (non-affine) cell, from the
+    definition with the TRUE weighted mass matrices: diag(M-bar) = diag(G-bar^-T M G-bar^-1) with
+    M^0_beta and M^1_alpha assembled by quadrature (element_matrix; their pullbacks are pinned by
+    the discrete complex on trilinear cells and the box closed forms), then
+    P_K = G0^T diag(M-bar^0) G0 + (G1 D)^T diag(M-bar^1) (G1 D).  aux_element_matrix computes the
+    diagonals by sum factorisation with squared broken-basis tables and (J^-1 J^-T)_mm: a wrong
+    metric entry, table or square fails here (the off-diagonal metric terms of M^1 drop out of
+    its broken-basis diagonal)."""
+    from oracle.fem import broken_G3, ref_derivative_pattern_or_values
+    rng = np.random.default_rng(7 + p)
+    Xc = np.zeros((2, 2, 2, 3))                                  # [az][ay][ax][xyz]
+    for az in range(2):
+        for ay in range(2):
+            for ax in range(2):
+                Xc[az, ay, ax] = 0.5 * np.array([ax, ay, az], dtype=float)
+    Xc += rng.uniform(-0.08, 0.08, Xc.shape)                     # every vertex moved: non-affine
+    alpha, beta = 1.7, 0.6
+    M0 = element_matrix(0, p, Xc, 0.0, beta)                     # (psi, beta psi)_K
+    M1 = element_matrix(1, p, Xc, 0.0, alpha)                    # (F Psi, alpha F Psi)_K, covariant pullback
+    G0, G1 = broken_G3(0, p), broken_G3(1, p)
+    d0 = np.diag(np.linalg.solve(G0.T, np.linalg.solve(G0.T, M0.T).T))   # diag(G0^-T M0 G0^-1)
+    d1 = np.diag(np.linalg.solve(G1.T, np.linalg.solve(G1.T, M1.T).T))
+    D = ref_derivative_pattern_or_values(0, p, values=True)
+    D = D.toarray() if hasattr(D, "toarray") else np.asarray(D)
+    Db = G1 @ D
+    P_def = G0.T @ np.diag(d0) @ G0 + Db.T @ np.diag(d1) @ Db
+    P = aux_element_matrix(p, Xc, alpha, beta)
+    assert np.abs(P - P_def).max() < 1e-12 * np.abs(P_def).max()
+    # and it is not the true operator (the cell is not Cartesian): P differs from A off its pattern
+    A = element_matrix(0, p, Xc, alpha, beta)
+    assert np.abs(A - P).max() > 1e-3 * np.abs(A).max()
