@@ -639,7 +639,13 @@ struct rm_ctx {
     allocs.push_back(d);
     return static_cast<double*>(d);
   }
+  // rm_relax_host on the SC-fused path: f is copied on a second stream while the apply runs
+  cudaStream_t st_copy = nullptr;
+  cudaEvent_t ev_u = nullptr, ev_f = nullptr;
   ~rm_ctx() {
+    if (ev_u) cudaEventDestroy(ev_u);
+    if (ev_f) cudaEventDestroy(ev_f);
+    if (st_copy) cudaStreamDestroy(st_copy);
     if (comm) { try { if (nccl().destroy) nccl().destroy(comm); } catch (...) {} }
     for (auto& e : events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
     for (void* p : allocs) cudaFree(p);
@@ -1587,7 +1593,9 @@ bool sc_fused(const rm_ctx* c) {
   return fused_k0(c) && !c->cartesian && c->nranks == 1 && c->prims[0].launch.sc_dinv && c->prims[0].launch.sc_pre;
 }
 
-void residual_sc_fused(rm_ctx* c, const double* u, const double* f, const rm::PatchLaunch& L) {
+// f_ready (optional): f arrives on another stream; the apply (u only) runs before the wait
+void residual_sc_fused(rm_ctx* c, const double* u, const double* f, const rm::PatchLaunch& L,
+                       cudaEvent_t f_ready = nullptr) {
   Phase ph(c, 0);
   int nl = 0;
   KPhase kp{c, 5};
@@ -1597,6 +1605,7 @@ void residual_sc_fused(rm_ctx* c, const double* u, const double* f, const rm::Pa
   CK(rm::launch_apply_trilinear(c->tri, c->d_tabs, c->d_X, c->d_alpha, c->d_beta, c->coef_const, u, f, L.rpad, -1.0,
                                 c->d_cellbuf, c->st, &nl, &kt));
   c->tri.skip_gather = 0;
+  if (f_ready) CK(cudaStreamWaitEvent(c->st, f_ready, 0));
   CK(rm::launch_sc_pre_fused(L, f, c->tri.Lx, c->st));
   CK(rm::launch_skeleton_gather_sc(c->tri, c->d_cellbuf, f, L.rpad, -1.0, L.sc_fb, c->st));
   c->tri.ldx_out = 0;
@@ -1707,6 +1716,27 @@ rm_status rm_relax_host(rm_ctx* c, const double* f, const double* u_in, double* 
     if (!f || !u_in || !u_out) throw RmError(RM_EINVAL, "null vector");
     if (!c->d_hf) { c->d_hf = c->dalloc(c->ndof); c->d_hu = c->dalloc(c->ndof); }
     const size_t B = c->ndof * sizeof(double);
+    if (sc_fused(c)) {
+      // the trilinear apply needs u only: copy u first, then f on a second stream while the
+      // apply runs (f is first read by the SC pre step); same kernels and results as relax_impl
+      if (!c->st_copy) {
+        CK(cudaStreamCreateWithFlags(&c->st_copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_u, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
+      }
+      CK(cudaMemcpyAsync(c->d_hu, u_in, B, cudaMemcpyHostToDevice, c->st));
+      CK(cudaEventRecord(c->ev_u, c->st));
+      CK(cudaStreamWaitEvent(c->st_copy, c->ev_u, 0));   // u's copy first (one H2D engine at a time)
+      CK(cudaMemcpyAsync(c->d_hf, f, B, cudaMemcpyHostToDevice, c->st_copy));
+      CK(cudaEventRecord(c->ev_f, c->st_copy));
+      const rm::PatchLaunch& L = c->prims[0].launch;
+      residual_sc_fused(c, c->d_hu, c->d_hf, L, c->ev_f);
+      Phase ph(c, 1);
+      c->launches[1] += run_family(c, c->prims[0], L.rpad, c->d_hu, omega, true, true, true, true, nullptr);
+      CK(cudaMemcpyAsync(u_out, c->d_hu, B, cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      return;
+    }
     CK(cudaMemcpyAsync(c->d_hf, f, B, cudaMemcpyHostToDevice, c->st));
     CK(cudaMemcpyAsync(c->d_hu, u_in, B, cudaMemcpyHostToDevice, c->st));
     relax_impl(c, c->d_hf, c->d_hu, c->d_hu, omega);

@@ -196,6 +196,22 @@ def test_precondition_and_host_entry_points(dev):
     check("cfg1 relax_host", rel(out, pb.relax(f, u)), 1e-11)
 
 
+def test_relax_host_overlapped_copy_trilinear(dev):
+    """rm_relax_host on the SC-fused path (trilinear ICC-SC, one rank) copies f on a second stream
+    while the apply runs: bitwise the device-buffer sweep, and the oracle's sweep within 1e-11."""
+    import paper_2211_14284_b200 as rmb
+    w = ri.CONFIGS[5].with_mesh(3).with_p(5)
+    ctx, pb = setup_pair(w)
+    f, u = vecs(w, ctx)
+    out = np.empty_like(u)
+    for _ in range(2):   # second call: reused staging buffers, stream and events
+        rmb.rm_relax_host(ctx, f, u, out, 0.7)
+    dv = torch.empty(ctx.n_local, dtype=torch.float64, device=dev)
+    rmb.rm_relax(ctx, torch.tensor(f, device=dev), torch.tensor(u, device=dev), dv, 0.7)
+    assert np.array_equal(out, dv.cpu().numpy())
+    check("cfg5-3^3-p5 relax_host (overlapped copies)", rel(out, pb.relax(f, u, 0.7)), 1e-11)
+
+
 def test_interior_only_single_patch_exact_solve(dev):
     import paper_2211_14284_b200 as rmb
     w = ri.CONFIGS[1].with_mesh(2)
