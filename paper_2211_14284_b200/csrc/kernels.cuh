@@ -237,7 +237,7 @@ cudaError_t launch_patch_combine(const PatchLaunch& L, double* u, double omega, 
 // shared-memory plan, grid size and tensor maps (rpad / cpad must be allocated)
 cudaError_t plan_patch_solve(PatchLaunch& L);
 constexpr int RM_PATCH_CONSUMER_WARPS = 8;
-constexpr int RM_PATCH_TILE_WARPS = 4;   // consumer warps sharing the dense tiles
+constexpr int RM_PATCH_TILE_WARPS = 4;   // consumer warps sharing the dense tiles (5 measured: cfg2 patch kernel 3.665 vs 3.658 ms)
 cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
                                const double* r, double* t, cudaStream_t st);
 cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, const double* Dh,
