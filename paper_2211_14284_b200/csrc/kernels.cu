@@ -143,6 +143,134 @@ __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, cons
   u[g] += omega * acc;
 }
 
+// Row-per-warp forms of the two kernels above (one (y, z) row of one component per warp, lanes
+// along x; no per-DoF index decode).  D^T: for the terms along x (e = 0) the warp stages the
+// source row of r_n in shared memory once, so the vertex columns' p-term sums read shared memory
+// instead of diverging global loops.  Same addends in the same order: bitwise equal.
+constexpr int HIP_ROWS_WARPS = 8;
+constexpr int HIP_ROW_MAX = 640;    // 2 staged rows of <= 320 doubles per warp; longer rows read global memory
+__global__ void __launch_bounds__(32 * HIP_ROWS_WARPS) hiptmair_DT_rows_kernel(const __grid_constant__ HipParams hp,
+                                                                               const double* __restrict__ r,
+                                                                               double* __restrict__ t) {
+  __shared__ double Ds[RM_MAXP1 * RM_MAXP1];
+  __shared__ double rowbuf[HIP_ROWS_WARPS][2][HIP_ROW_MAX / 2];
+  for (int i = threadIdx.x; i < hp.p * (hp.p + 1); i += blockDim.x) Ds[i] = hp.D[i];
+  __syncthreads();
+  const int p = hp.p, P1 = p + 1, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const HipContrib* L = hp.kpot == 0 ? c_grad : c_curl;
+  const int nL = hp.kpot == 0 ? 3 : 6;
+  int rows_before = 0;
+  for (int m = 0; m < hp.ncomp_pot; ++m) {
+    const int Lx = (int)hp.len_pot[m][0], Ly = (int)hp.len_pot[m][1], nrow = Ly * (int)hp.len_pot[m][2];
+    for (int row = blockIdx.x * HIP_ROWS_WARPS + w - rows_before; row < nrow; row += gridDim.x * HIP_ROWS_WARPS) {
+      if (row < 0) continue;
+      const int iy = row % Ly, iz = row / Ly;
+      const bool rcon = is_constrained_idx(hp.fam_pot[m][1], iy, (long long)hp.n[1] * p, hp.gamma_d, 1) ||
+                        is_constrained_idx(hp.fam_pot[m][2], iz, (long long)hp.n[2] * p, hp.gamma_d, 2);
+      double* trow = t + hp.off_pot[m] + (long long)row * Lx;
+      if (rcon) {
+        for (int x = lane; x < Lx; x += 32) trow[x] = 0.0;
+        continue;
+      }
+      // stage the x-direction source rows (terms with e = 0; at most two per component)
+      int ns = 0;
+      const double* xsrc[2] = {nullptr, nullptr};
+      for (int q = 0; q < nL; ++q) {
+        if (L[q].m != m || L[q].e != 0) continue;
+        const int n = L[q].n;
+        const int lx = (int)hp.len_pri[n][0], ly = (int)hp.len_pri[n][1];
+        const double* rb = r + hp.off_pri[n] + ((long long)iz * ly + iy) * lx;
+        if (lx <= HIP_ROW_MAX / 2 && ns < 2) {
+          for (int x = lane; x < lx; x += 32) rowbuf[w][ns][x] = rb[x];
+          xsrc[ns] = rowbuf[w][ns];
+        } else {
+          xsrc[ns] = rb;
+        }
+        ++ns;
+      }
+      __syncwarp();
+      for (int x = lane; x < Lx; x += 32) {
+        if (is_constrained_idx(hp.fam_pot[m][0], x, (long long)hp.n[0] * p, hp.gamma_d, 0)) { trow[x] = 0.0; continue; }
+        double acc = 0.0;
+        int si = 0;
+        for (int q = 0; q < nL; ++q) {
+          if (L[q].m != m) continue;
+          const int n = L[q].n, e = L[q].e;
+          const int lx = (int)hp.len_pri[n][0], ly = (int)hp.len_pri[n][1];
+          const int j[3] = {x, iy, iz};
+          const int I = j[e], c = I / p, aa = I - c * p;
+          const double* rb;
+          int stride;
+          if (e == 0) {
+            rb = xsrc[si++];
+            stride = 1;
+          } else {
+            int jj[3] = {x, iy, iz};
+            jj[e] = 0;
+            rb = r + hp.off_pri[n] + ((long long)jj[2] * ly + jj[1]) * lx + jj[0];
+            stride = e == 1 ? lx : lx * ly;
+          }
+          double s = 0.0;
+          if (aa != 0) {
+            s = Ds[aa * P1 + aa] * rb[(c * p + aa) * stride];
+          } else {
+            if (c >= 1)
+              for (int a = 0; a < p; ++a) s += Ds[a * P1 + p] * rb[((c - 1) * p + a) * stride];
+            if (c < hp.n[e])
+              for (int a = 0; a < p; ++a) s += Ds[a * P1] * rb[(c * p + a) * stride];
+          }
+          acc += L[q].sigma * s;
+        }
+        trow[x] = acc;
+      }
+      __syncwarp();
+    }
+    rows_before += nrow;
+  }
+}
+
+__global__ void __launch_bounds__(32 * HIP_ROWS_WARPS) hiptmair_D_add_rows_kernel(const __grid_constant__ HipParams hp,
+                                                                                  const double* __restrict__ s,
+                                                                                  double* __restrict__ u, double omega) {
+  __shared__ double Ds[RM_MAXP1 * RM_MAXP1];
+  for (int i = threadIdx.x; i < hp.p * (hp.p + 1); i += blockDim.x) Ds[i] = hp.D[i];
+  __syncthreads();
+  const int p = hp.p, P1 = p + 1, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const HipContrib* L = hp.kpot == 0 ? c_grad : c_curl;
+  const int nL = hp.kpot == 0 ? 3 : 6;
+  int rows_before = 0;
+  for (int n = 0; n < hp.ncomp_pri; ++n) {
+    const int Lx = (int)hp.len_pri[n][0], Ly = (int)hp.len_pri[n][1], nrow = Ly * (int)hp.len_pri[n][2];
+    for (int row = blockIdx.x * HIP_ROWS_WARPS + w - rows_before; row < nrow; row += gridDim.x * HIP_ROWS_WARPS) {
+      if (row < 0) continue;
+      const int iy = row % Ly, iz = row / Ly;
+      if (is_constrained_idx(hp.fam_pri[n][1], iy, (long long)hp.n[1] * p, hp.gamma_d, 1) ||
+          is_constrained_idx(hp.fam_pri[n][2], iz, (long long)hp.n[2] * p, hp.gamma_d, 2))
+        continue;
+      double* urow = u + hp.off_pri[n] + (long long)row * Lx;
+      for (int x = lane; x < Lx; x += 32) {
+        if (is_constrained_idx(hp.fam_pri[n][0], x, (long long)hp.n[0] * p, hp.gamma_d, 0)) continue;
+        double acc = 0.0;
+        for (int q = 0; q < nL; ++q) {
+          if (L[q].n != n) continue;
+          const int m = L[q].m, e = L[q].e;
+          const int lx = (int)hp.len_pot[m][0], ly = (int)hp.len_pot[m][1];
+          const int stride = e == 0 ? 1 : (e == 1 ? lx : lx * ly);
+          int j[3] = {x, iy, iz};
+          const int c = j[e] / p, a = j[e] - c * p;
+          j[e] = c * p;
+          const double* sb = s + hp.off_pot[m] + ((long long)j[2] * ly + j[1]) * lx + j[0];
+          double sum = Ds[a * P1] * sb[0] + Ds[a * P1 + p] * sb[p * stride];
+          if (a >= 1) sum += Ds[a * P1 + a] * sb[a * stride];
+          acc += L[q].sigma * sum;
+        }
+        urow[x] += omega * acc;
+      }
+    }
+    rows_before += nrow;
+  }
+}
+
 static HipParams make_hip(int k, int p, const int* n, unsigned gamma_d, const double* Dh) {
   static const int FAMS[4][3][3] = {
       {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}},
@@ -179,7 +307,8 @@ cudaError_t launch_hiptmair_DT(int k, int p, const int* n, unsigned gamma_d, con
                                double* t, cudaStream_t st) {
   HipParams hp = make_hip(k, p, n, gamma_d, Dh);
   const long long N = hp.off_pot[hp.ncomp_pot];
-  hiptmair_DT_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(hp, r, t, N);
+  if (exp_env("RM_HIP_PERDOF")) hiptmair_DT_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(hp, r, t, N);
+  else hiptmair_DT_rows_kernel<<<148 * 8, 32 * HIP_ROWS_WARPS, 0, st>>>(hp, r, t);
   return cudaGetLastError();
 }
 
@@ -187,7 +316,8 @@ cudaError_t launch_hiptmair_D_add(int k, int p, const int* n, unsigned gamma_d, 
                                   double* u, double omega, cudaStream_t st) {
   HipParams hp = make_hip(k, p, n, gamma_d, Dh);
   const long long N = hp.off_pri[hp.ncomp_pri];
-  hiptmair_D_add_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(hp, s, u, omega, N);
+  if (exp_env("RM_HIP_PERDOF")) hiptmair_D_add_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(hp, s, u, omega, N);
+  else hiptmair_D_add_rows_kernel<<<148 * 8, 32 * HIP_ROWS_WARPS, 0, st>>>(hp, s, u, omega);
   return cudaGetLastError();
 }
 
