@@ -966,15 +966,24 @@ size_t batch_smem_t(int B, int NT, int box_total, int mr_max) {
   return sizeof(double) * (B * (boxd + mr + std::max<size_t>(NT, mr)) + kBatchMaxPieces);   // + piece table (int2)
 }
 
+// rp = pad(r): one (y, z) row of one component per warp, grid-stride (the per-element 64-bit
+// divisions of a thread-per-entry pad dominated it); the pad column is written as zero
 __global__ void pad_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ r, double* __restrict__ rp,
                            long long npad) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= npad) return;
-  int m = 0;
-  while (m + 1 < P.ncomp && g >= P.poff[m + 1]) ++m;
-  const long long rr = g - P.poff[m];
-  const long long x = rr % P.lxp[m], yz = rr / P.lxp[m];
-  rp[g] = (x < P.len[m][0]) ? r[P.off[m] + yz * P.len[m][0] + x] : 0.0;
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * (blockDim.x >> 5);
+  int rows_before = 0;
+  for (int m = 0; m < P.ncomp; ++m) {
+    const int Lx = (int)P.len[m][0], Lxp = (int)P.lxp[m], nrow = (int)(P.len[m][1] * P.len[m][2]);
+    for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5) - rows_before; row < nrow; row += wstride) {
+      if (row < 0) continue;
+      const double* src = r + P.off[m] + (long long)row * Lx;
+      double* dst = rp + P.poff[m] + (long long)row * Lxp;
+      for (int x = lane; x < Lxp; x += 32) dst[x] = x < Lx ? src[x] : 0.0;
+    }
+    rows_before += nrow;
+  }
+  (void)npad;
 }
 
 __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const double* __restrict__ cp, double* u,
@@ -1314,7 +1323,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
                                const double* u_in) {
   if (L.npatch <= 0) {   // an empty family still does its part of a shared sequence
     if (!L.cpad) return cudaSuccess;
-    if (!r_padded) pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
+    if (!r_padded) pad_kernel<<<148 * 8, 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
     if (zero_c) cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st);
     if (combine) unpad_axpy_kernel<<<148 * 8, 256, 0, st>>>(L.pad, L.cpad, u, omega, L.pad.off[L.pad.ncomp], 0, u_in);
     return cudaGetLastError();
@@ -1322,7 +1331,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   const long long n = L.pad.off[L.pad.ncomp];
   cudaError_t e;
   if (!r_padded) {
-    pad_kernel<<<(unsigned)((L.npad + 255) / 256), 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
+    pad_kernel<<<148 * 8, 256, 0, st>>>(L.pad, r, L.rpad, L.npad);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   ScGeom sg{};
