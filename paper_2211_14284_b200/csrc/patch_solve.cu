@@ -749,7 +749,7 @@ struct BatchArgs {
 template <int B, int BW>
 __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const double* __restrict__ val, int nrows,
                                              int warp, int lane, double* __restrict__ X, int boxd) {
-  constexpr int U = 8;
+  constexpr int U = 4;   // entries per lane and step (measured at cfg4: U = 2 10.2 ms, 4 9.35 ms, 8 9.82 ms, 16 10.4 ms)
   const Hdr h = hdr(pb);
   const int nsl = h.a1 - h.a0;
   const uint32_t* si = reinterpret_cast<const uint32_t*>(pb + 16);
