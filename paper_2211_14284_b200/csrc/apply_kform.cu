@@ -20,7 +20,7 @@ namespace rm {
 
 namespace {
 
-constexpr int KF_THREADS = 256;
+constexpr int KF_THREADS = 128;   // measured per apply: 64 -> 0.36 / 0.42 ms, 128 -> 0.26 / 0.26 ms, 256 -> 0.29 / 0.28 ms (cfg3 / cfg4)
 
 // (D-hat x)_a along a line with stride s (source: P + 1 entries)
 template <int P>
