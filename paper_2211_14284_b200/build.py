@@ -51,6 +51,8 @@ def build(verbose: bool = False) -> str:
     inc = ["-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include"]
     if os.environ.get("RM_BUILD_EXPERIMENTS"):   # instrumentation build (exp_env.hpp); rebuild from clean
         inc += ["-DRM_EXPERIMENTS"]
+    if os.environ.get("RM_BUILD_DEFS"):   # tuning sweeps: extra -D definitions (rebuild from clean)
+        inc += os.environ["RM_BUILD_DEFS"].split()
     for s in CXX_SRC:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s + ".o")

@@ -204,8 +204,14 @@ __device__ __forceinline__ void apply_A(const double* __restrict__ Ah, const dou
   y[P] = sP;
 }
 
+#ifndef RM_Q_THREADS   // CTA size of the k = 0 apply (tuning knob: -DRM_Q_THREADS, -DRM_Q_MINB)
+#define RM_Q_THREADS 256
+#endif
+#ifndef RM_Q_MINB
+#define RM_Q_MINB 5
+#endif
 template <int P>
-__global__ void __launch_bounds__(256, 5) apply_q_kernel(const __grid_constant__ OpParams op,
+__global__ void __launch_bounds__(RM_Q_THREADS, RM_Q_MINB) apply_q_kernel(const __grid_constant__ OpParams op,
                                                        const double* __restrict__ alpha,
                                                        const double* __restrict__ beta, int coef_const,
                                                        const double* __restrict__ hpow,
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(256, 5) apply_q_kernel(const __grid_constant__
   // cell window in shared memory with x lines padded to N + 1 doubles: the x stage (thread per
   // x line) and the y stage read conflict-free (unpadded, stride-N lines were 16-way conflicts)
   constexpr int NP = N + 1, NW = N2 * NP;
-  constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
+  constexpr int CPB = (RM_Q_THREADS / N2) > 0 ? (RM_Q_THREADS / N2) : 1;
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
   const int cs = tid / N2, q = tid % N2;
@@ -321,7 +327,7 @@ static cudaError_t launch_q(const OpParams& op, const double* alpha, const doubl
                             const double* hpow, const double* u, double* out, double sign, cudaStream_t st, int& nl,
                             double* cellbuf, const double* f = nullptr) {
   constexpr int N = P + 1, N2 = N * N, N3 = N2 * N;
-  constexpr int CPB = (256 / N2) > 0 ? (256 / N2) : 1;
+  constexpr int CPB = (RM_Q_THREADS / N2) > 0 ? (RM_Q_THREADS / N2) : 1;
   const size_t smem = (size_t)CPB * 2 * N2 * (N + 1) * sizeof(double);
   static bool configured = false;
   if (!configured) {

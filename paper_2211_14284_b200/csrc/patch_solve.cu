@@ -1012,6 +1012,12 @@ __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const dou
 }
 
 // ---- static condensation of the cell interiors (ICC-SC families, k = 0), on the padded layout
+#ifndef RM_SCC_THREADS   // CTA sizes of the SC pre / post steps (tuning knobs)
+#define RM_SCC_THREADS 256
+#endif
+#ifndef RM_SCP_THREADS
+#define RM_SCP_THREADS 256
+#endif
 // pre:  rp[f] -= sum over the 2 cells K at face DoF f, sum_i c_K(f, I) dinv_K(I) rp[I]   (one thread per face DoF)
 // post: cp[I] = n_K dinv_K(I) rp[I] - dinv_K(I) sum_faces c_K(f, I) cp[f]               (one thread per interior DoF)
 struct ScGeom {
@@ -1314,7 +1320,7 @@ cudaError_t launch_sc_pre_fused(const PatchLaunch& L, const double* f, long long
       return e;
     smem_set = smem;
   }
-  sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, f, lx);
+  sc_cell_kernel<<<(unsigned)ncell, RM_SCC_THREADS, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, f, lx);
   return cudaGetLastError();
 }
 
@@ -1356,7 +1362,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
           return e;
         smem_set = smem;
       }
-      sc_cell_kernel<<<(unsigned)ncell, 256, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, nullptr, 0);
+      sc_cell_kernel<<<(unsigned)ncell, RM_SCC_THREADS, smem, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.rpad, L.sc_fb, nullptr, 0);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       sc_face_kernel<<<(unsigned)((nface + 255) / 256), 256, 0, st>>>(sg, L.sc_fb, L.rpad, (int)nface);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1414,12 +1420,12 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   }
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
-    const dim3 gp((unsigned)((ni + 255) / 256), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
+    const dim3 gp((unsigned)((ni + RM_SCP_THREADS - 1) / RM_SCP_THREADS), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
     // c_I to cpad; the combine below writes u for every DoF (measured twice: writing u_out = u_in +
     // omega c_I from the post step and a skeleton-only combine is slower -- cfg5 patch stage 1.562
     // -> 1.587 ms in round 2 -- the post step's scattered u traffic costs more than the streaming pass)
     const bool fuse = combine && L.pad.ncomp == 1 && exp_env("RM_POST_FUSED") != nullptr;
-    sc_post_kernel<<<gp, 256, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint,
+    sc_post_kernel<<<gp, RM_SCP_THREADS, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint,
                                        fuse ? u : nullptr, omega, L.pad.len[0][0], u_in);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (fuse) {
