@@ -50,7 +50,10 @@ namespace {
 constexpr int NC = RM_PATCH_CONSUMER_WARPS;   // sparse warps
 constexpr int NT = NC * 32;
 constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps
-constexpr int kIccChunksDev = 4;   // = kIccChunks (patches.hpp): chunks per ICC piece
+#ifndef RM_ICC_CHUNKS
+#define RM_ICC_CHUNKS 4
+#endif
+constexpr int kIccChunksDev = RM_ICC_CHUNKS;   // = kIccChunks (patches.hpp): chunks per ICC piece
 constexpr int WT0 = NC, WPROD_A = NC + NTW, WPROD_B = NC + NTW + 1, WSTORE = NC + NTW + 2;
 constexpr int NTHR = 32 * (NC + NTW + 3);
 constexpr int NDESC = 16;                      // in-flight transfer units per channel

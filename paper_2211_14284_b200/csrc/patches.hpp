@@ -69,8 +69,14 @@ constexpr int kIccRows = 32;      // rows per ICC chunk: one row per lane of the
 // chunks per ICC piece: chunk c of the level's piece k -> warp c + kIccChunks (k % (8 / kIccChunks));
 // measured on cfg5 (chunks / value cap -> patch kernel): 8 / 8192 -> 1.34 ms, 4 / 4096 -> 1.27 ms,
 // 2 / 2048 -> 1.56 ms (ring prefetch depth vs. number of piece headers walked)
-constexpr int kIccChunks = 4;
-constexpr int kIccPieceVals = 4096;   // values per ICC piece (several pieces in flight in the ring)
+#ifndef RM_ICC_CHUNKS            // tuning knobs (-D): chunks per ICC piece, values per ICC piece
+#define RM_ICC_CHUNKS 4
+#endif
+#ifndef RM_ICC_PIECE_VALS
+#define RM_ICC_PIECE_VALS 8192   // measured (cfg5 patch kernel): 2048 1.75, 3072 1.42, 4096 1.28, 6144 1.32, 8192 1.266, 12288 1.266, 16384 1.269 ms
+#endif
+constexpr int kIccChunks = RM_ICC_CHUNKS;
+constexpr int kIccPieceVals = RM_ICC_PIECE_VALS;   // values per ICC piece (several pieces in flight in the ring)
 struct IccChunk { int r0, cnt, L, sofs; };   // level-ordered rows [r0, r0+cnt), longest off-diag row, slot offset
 constexpr int kGatherMax = 2048;     // positions per GATHER/SCATTER piece
 // Dense tiles (32x32 blocks of the final block's inverse) in LANE-BLOCK order: lane l = 4a + b
