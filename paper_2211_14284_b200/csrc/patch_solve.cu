@@ -56,7 +56,10 @@ constexpr int NTW = RM_PATCH_TILE_WARPS;       // tile warps
 constexpr int kIccChunksDev = RM_ICC_CHUNKS;   // = kIccChunks (patches.hpp): chunks per ICC piece
 constexpr int WT0 = NC, WPROD_A = NC + NTW, WPROD_B = NC + NTW + 1, WSTORE = NC + NTW + 2;
 constexpr int NTHR = 32 * (NC + NTW + 3);
-constexpr int NDESC = 16;                      // in-flight transfer units per channel
+#ifndef RM_NDESC
+#define RM_NDESC 16
+#endif
+constexpr int NDESC = RM_NDESC;                // in-flight transfer units per channel
 constexpr int NBOX = 3;                        // window-box buffers (patches i-1, i, i+1)
 // shared-memory header: per channel full/empty mbarriers and slot tables (offset, pieces, meta),
 // then the box barriers vfull (TMA box landed), gready (forward done), xready (tiles done),

@@ -107,8 +107,14 @@ struct Piece {
 
 // Transfer unit: consecutive pieces moved by one mbarrier round trip (<= kUnitVals doubles of
 // values and <= kUnitMeta bytes of metadata; the ring holds [metas][values] of the unit).
-constexpr int kUnitVals = 2048;       // sparse-channel units (16 KB of values)
-constexpr int kUnitValsTile = 4096;   // tile-channel units (32 KB)
+#ifndef RM_UNIT_VALS               // tuning knobs (-D): values per transfer unit of each channel
+#define RM_UNIT_VALS 2048
+#endif
+#ifndef RM_UNIT_VALS_TILE
+#define RM_UNIT_VALS_TILE 4096
+#endif
+constexpr int kUnitVals = RM_UNIT_VALS;             // sparse-channel units (16 KB of values)
+constexpr int kUnitValsTile = RM_UNIT_VALS_TILE;    // tile-channel units (32 KB)
 constexpr int kUnitMeta = 16384;
 struct Unit { int p0, np, mofs, mbytes, sofs, nd; };
 
