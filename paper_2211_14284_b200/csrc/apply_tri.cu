@@ -720,7 +720,10 @@ __global__ void tri_gather_kernel(const __grid_constant__ TriParams tp, const do
 // and, for face-interior DoFs, minus the condensation line sums e of the (<= 2) cells sharing the
 // face (lower cell first; fb != null) -- the same operations, in the same order, as the gather
 // followed by sc_face_kernel.  Rows with y and z off the cell boundaries only visit the x-boundary DoFs.
-__global__ void __launch_bounds__(256, 6) tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
+// resident CTAs per SM: measured best with the line sums (cfg5: 8 vs 6 -> -15 us) and without them
+// (cfg2: 4 vs 6 -> -4 us; 8 -> +12 us)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) tri_gather_sc_kernel(const __grid_constant__ TriParams tp, const double* __restrict__ cellbuf,
                                      const double* __restrict__ f, double* __restrict__ out, double sign,
                                      const double* __restrict__ fb) {
   __shared__ int4 xtab[kXTab];
@@ -814,7 +817,8 @@ cudaError_t launch_skeleton_gather_sc(const TriParams& tp, const double* cellbuf
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  tri_gather_sc_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign, fb);
+  if (fb) tri_gather_sc_kernel<8><<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign, fb);
+  else tri_gather_sc_kernel<4><<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign, fb);
   return cudaGetLastError();
 }
 

@@ -147,7 +147,10 @@ __global__ void hiptmair_D_add_kernel(const __grid_constant__ HipParams hp, cons
 // along x; no per-DoF index decode).  D^T: for the terms along x (e = 0) the warp stages the
 // source row of r_n in shared memory once, so the vertex columns' p-term sums read shared memory
 // instead of diverging global loops.  Same addends in the same order: bitwise equal.
-constexpr int HIP_ROWS_WARPS = 8;
+#ifndef RM_HIP_WARPS   // tuning knob (-D): warps per CTA of the Hiptmair row kernels (4: cfg4 potential +0.17 ms)
+#define RM_HIP_WARPS 8
+#endif
+constexpr int HIP_ROWS_WARPS = RM_HIP_WARPS;
 constexpr int HIP_ROW_MAX = 640;    // 2 staged rows of <= 320 doubles per warp; longer rows read global memory
 __global__ void __launch_bounds__(32 * HIP_ROWS_WARPS) hiptmair_DT_rows_kernel(const __grid_constant__ HipParams hp,
                                                                                const double* __restrict__ r,

@@ -1021,8 +1021,8 @@ __global__ void unpad_axpy_kernel(const __grid_constant__ PadLayout P, const dou
 #ifndef RM_SCC_THREADS   // CTA sizes of the SC pre / post steps (tuning knobs)
 #define RM_SCC_THREADS 256
 #endif
-#ifndef RM_SCP_THREADS
-#define RM_SCP_THREADS 256
+#ifndef RM_SCP_THREADS   // measured: 128 / 256 / 512 -> cfg5 patch stage 1.560 / 1.572 / 1.652 ms
+#define RM_SCP_THREADS 128
 #endif
 // pre:  rp[f] -= sum over the 2 cells K at face DoF f, sum_i c_K(f, I) dinv_K(I) rp[I]   (one thread per face DoF)
 // post: cp[I] = n_K dinv_K(I) rp[I] - dinv_K(I) sum_faces c_K(f, I) cp[f]               (one thread per interior DoF)
