@@ -1609,7 +1609,7 @@ void residual_sc_fused(rm_ctx* c, const double* u, const double* f, const rm::Pa
   CK(rm::launch_sc_pre_fused(L, f, c->tri.Lx, c->st));
   CK(rm::launch_skeleton_gather_sc(c->tri, c->d_cellbuf, f, L.rpad, -1.0, L.sc_fb, c->st));
   c->tri.ldx_out = 0;
-  c->launches[0] += nl + 2;
+  c->launches[0] += nl + 2;   // the apply (skip_gather: 1), sc_cell, the skeleton gather
 }
 
 // one sweep u_out = u_in + omega P^{-1} (f - A u_in) (z-slab: halos, local correction, reverse-add)

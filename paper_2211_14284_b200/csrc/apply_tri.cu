@@ -853,7 +853,7 @@ cudaError_t launch_apply_trilinear(const TriParams& tp, const double* tabs, cons
   if (kt) kt->end(kt->arg);
   if (!tp.skip_gather) tri_gather_kernel<<<(unsigned)(nsm * 8), 256, 0, st>>>(tp, cellbuf, f, out, sign);
   (void)nd;
-  if (nlaunch) *nlaunch += 2;
+  if (nlaunch) *nlaunch += tp.skip_gather ? 1 : 2;
   return cudaGetLastError();
 }
 

@@ -1129,49 +1129,67 @@ __global__ void sc_face_kernel(const __grid_constant__ ScGeom G, const double* _
   rp[sc_idx(G, g[0], g[1], g[2])] -= e;
 }
 
+#ifndef RM_SCP_DOFS   // interior DoFs per thread of the SC post step (all loads issued before the stores);
+#define RM_SCP_DOFS 2   // measured 1 / 2 / 4: cfg5 patch stage 1.544 / 1.500 / 1.519 ms (pass AJ)
+#endif
+template <int D>
 __global__ void sc_post_kernel(const __grid_constant__ ScGeom G, const double* __restrict__ dinv,
                                const double* __restrict__ cc, const double* __restrict__ cw, const int* __restrict__ nk,
                                const double* __restrict__ rp, double* __restrict__ cp, long long nint,
                                double* u, double omega, long long lx, const double* uin) {
-  // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math
+  // one cell per blockIdx.y row of blocks, interior DoFs across x-blocks: 32-bit index math;
+  // D DoFs per thread (I, I + blockDim, ...): every load of the D DoFs precedes the first store
+  // (cp is read and written), the same operations per DoF as D = 1 (bitwise equal)
   __shared__ double kt[3][16];   // D_ii, D_i0, D_ip: lane-varying indices (shared, not the param bank)
   if (threadIdx.x < 48) kt[threadIdx.x >> 4][threadIdx.x & 15] =
       (threadIdx.x < 16 ? G.kd : (threadIdx.x < 32 ? G.k0 : G.kp))[threadIdx.x & 15];
   __syncthreads();
   const int p = G.p, pm = p - 1, ni = pm * pm * pm;
-  const int I = blockIdx.x * blockDim.x + threadIdx.x;
-  if (I >= ni) return;
   const int K32 = (int)blockIdx.y;   // 32-bit decode (the 64-bit divisions were most of the instructions)
   const long long K = K32;
-  const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / (pm * pm) + 1;
   const int cx = K32 % G.n[0], cy = (K32 / G.n[0]) % G.n[1], cz = K32 / (G.n[0] * G.n[1]);
   (void)nint;
   const long long x = (long long)cx * p, y = (long long)cy * p, z = (long long)cz * p;
-  const double dv = dinv[K * ni + I];
-  double c0, c1, c2, c3, c4, c5;
-  if (G.cmp) {   // couplings (D_ii w) D_i{0,p} rebuilt from the three interior stiffness weights
-    const double wx = cw[(K * 3 + 0) * ni + I], wy = cw[(K * 3 + 1) * ni + I], wz = cw[(K * 3 + 2) * ni + I];
-    const double ax = __dmul_rn(kt[0][i], wx), ay = __dmul_rn(kt[0][j], wy), az = __dmul_rn(kt[0][k], wz);
-    c0 = __dmul_rn(ax, kt[1][i]); c1 = __dmul_rn(ax, kt[2][i]);
-    c2 = __dmul_rn(ay, kt[1][j]); c3 = __dmul_rn(ay, kt[2][j]);
-    c4 = __dmul_rn(az, kt[1][k]); c5 = __dmul_rn(az, kt[2][k]);
-  } else {
-    c0 = cc[(K * 6 + 0) * ni + I]; c1 = cc[(K * 6 + 1) * ni + I]; c2 = cc[(K * 6 + 2) * ni + I];
-    c3 = cc[(K * 6 + 3) * ni + I]; c4 = cc[(K * 6 + 4) * ni + I]; c5 = cc[(K * 6 + 5) * ni + I];
+  const double nkK = (double)nk[K];
+  double cres[D];
+  long long gout[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    const int I = (blockIdx.x * D + d) * blockDim.x + threadIdx.x;
+    gout[d] = -1;
+    if (I >= ni) continue;
+    const int i = I % pm + 1, j = (I / pm) % pm + 1, k = I / (pm * pm) + 1;
+    const double dv = dinv[K * ni + I];
+    double c0, c1, c2, c3, c4, c5;
+    if (G.cmp) {   // couplings (D_ii w) D_i{0,p} rebuilt from the three interior stiffness weights
+      const double wx = cw[(K * 3 + 0) * ni + I], wy = cw[(K * 3 + 1) * ni + I], wz = cw[(K * 3 + 2) * ni + I];
+      const double ax = __dmul_rn(kt[0][i], wx), ay = __dmul_rn(kt[0][j], wy), az = __dmul_rn(kt[0][k], wz);
+      c0 = __dmul_rn(ax, kt[1][i]); c1 = __dmul_rn(ax, kt[2][i]);
+      c2 = __dmul_rn(ay, kt[1][j]); c3 = __dmul_rn(ay, kt[2][j]);
+      c4 = __dmul_rn(az, kt[1][k]); c5 = __dmul_rn(az, kt[2][k]);
+    } else {
+      c0 = cc[(K * 6 + 0) * ni + I]; c1 = cc[(K * 6 + 1) * ni + I]; c2 = cc[(K * 6 + 2) * ni + I];
+      c3 = cc[(K * 6 + 3) * ni + I]; c4 = cc[(K * 6 + 4) * ni + I]; c5 = cc[(K * 6 + 5) * ni + I];
+    }
+    double s = c0 * cp[sc_idx(G, x, y + j, z + k)];
+    s = fma(c1, cp[sc_idx(G, x + p, y + j, z + k)], s);
+    s = fma(c2, cp[sc_idx(G, x + i, y, z + k)], s);
+    s = fma(c3, cp[sc_idx(G, x + i, y + p, z + k)], s);
+    s = fma(c4, cp[sc_idx(G, x + i, y + j, z)], s);
+    s = fma(c5, cp[sc_idx(G, x + i, y + j, z + p)], s);
+    const long long gi = sc_idx(G, x + i, y + j, z + k);
+    cres[d] = dv * (nkK * rp[gi] - s);
+    gout[d] = u ? ((z + k) * G.ly + y + j) * lx + x + i : gi;
   }
-  double s = c0 * cp[sc_idx(G, x, y + j, z + k)];
-  s = fma(c1, cp[sc_idx(G, x + p, y + j, z + k)], s);
-  s = fma(c2, cp[sc_idx(G, x + i, y, z + k)], s);
-  s = fma(c3, cp[sc_idx(G, x + i, y + p, z + k)], s);
-  s = fma(c4, cp[sc_idx(G, x + i, y + j, z)], s);
-  s = fma(c5, cp[sc_idx(G, x + i, y + j, z + p)], s);
-  const long long gi = sc_idx(G, x + i, y + j, z + k);
-  const double c = dv * (nk[K] * rp[gi] - s);
-  if (u) {   // fused combine: u = (uin ? uin : u) + omega c_I directly (the combine skips the interiors)
-    const long long gu = ((z + k) * G.ly + y + j) * lx + x + i;
-    u[gu] = (uin ? uin[gu] : u[gu]) + omega * c;
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    if (gout[d] < 0) continue;
+    if (u) {   // fused combine: u = (uin ? uin : u) + omega c_I directly (the combine skips the interiors)
+      const long long gu = gout[d];
+      u[gu] = (uin ? uin[gu] : u[gu]) + omega * cres[d];
+    }
+    else cp[gout[d]] = cres[d];
   }
-  else cp[gi] = c;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -1426,12 +1444,13 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   }
   if (L.sc_dinv && nint > 0) {
     const int ni = (L.sc_p - 1) * (L.sc_p - 1) * (L.sc_p - 1);
-    const dim3 gp((unsigned)((ni + RM_SCP_THREADS - 1) / RM_SCP_THREADS), (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
+    const dim3 gp((unsigned)((ni + RM_SCP_THREADS * RM_SCP_DOFS - 1) / (RM_SCP_THREADS * RM_SCP_DOFS)),
+                  (unsigned)(sg.n[0] * sg.n[1] * sg.n[2]));
     // c_I to cpad; the combine below writes u for every DoF (measured twice: writing u_out = u_in +
     // omega c_I from the post step and a skeleton-only combine is slower -- cfg5 patch stage 1.562
     // -> 1.587 ms in round 2 -- the post step's scattered u traffic costs more than the streaming pass)
     const bool fuse = combine && L.pad.ncomp == 1 && exp_env("RM_POST_FUSED") != nullptr;
-    sc_post_kernel<<<gp, RM_SCP_THREADS, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint,
+    sc_post_kernel<RM_SCP_DOFS><<<gp, RM_SCP_THREADS, 0, st>>>(sg, L.sc_dinv, L.sc_c, L.sc_w, L.sc_nk, L.rpad, L.cpad, nint,
                                        fuse ? u : nullptr, omega, L.pad.len[0][0], u_in);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (fuse) {
