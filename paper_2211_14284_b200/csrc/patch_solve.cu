@@ -92,6 +92,36 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(b))
                : "memory");
 }
+// L2 eviction priorities (tuning knobs): the factor values are read once per sweep, the window
+// boxes of r (and the reduce-added c boxes) are re-read by the patches of the other colours
+#ifndef RM_L2_VALS   // 1: factor value stream with L2::evict_first (measured, pass AK: cfg5 patch kernel
+#define RM_L2_VALS 1  // 1.273 -> 1.253 ms; cfg2 unchanged 3.647 / 3.644; the box / reduce hints add nothing)
+#endif
+#ifndef RM_L2_BOX    // 1: window-box loads of r with L2::evict_last
+#define RM_L2_BOX 0
+#endif
+#ifndef RM_L2_RED    // 1: reduce-adds into c with L2::evict_last
+#define RM_L2_RED 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+  uint64_t pol;
+  if (last) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_vals(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+#if RM_L2_VALS
+  bulk_g2s_hint(dst, src, bytes, b, l2_policy(false));
+#else
+  bulk_g2s(dst, src, bytes, b);
+#endif
+}
 // named barriers: 1 = sparse warps, 2 = tile warps
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
@@ -111,6 +141,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
           smem_u32(dst)),
       "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_load_box(void* dst, const CUtensorMap* tm, int x, int y, int z, uint64_t* bar) {
+#if RM_L2_BOX
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(l2_policy(true))
+      : "memory");
+#else
+  tma_load_3d(dst, tm, x, y, z, bar);
+#endif
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* tm, int x, int y, int z, const void* src);
+__device__ __forceinline__ void tma_reduce_box(const CUtensorMap* tm, int x, int y, int z, const void* src) {
+#if RM_L2_RED
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(tm),
+               "r"(x), "r"(y), "r"(z), "r"(smem_u32(src)), "l"(l2_policy(true))
+               : "memory");
+#else
+  tma_reduce_add_3d(tm, x, y, z, src);
+#endif
 }
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* tm, int x, int y, int z, const void* src) {
   asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
@@ -341,7 +392,7 @@ struct ProdChan {
     vs_of[sl] = vs;
     mbar_arrive_expect_tx(&c.full[sl], mb + vb);
     bulk_g2s(ring + vs % cap, meta, mb, &c.full[sl]);
-    if (vb) bulk_g2s(ring + vs % cap + mb, vals, vb, &c.full[sl]);
+    if (vb) bulk_vals(ring + vs % cap + mb, vals, vb, &c.full[sl]);
     ++j;
   }
 };
@@ -425,7 +476,7 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       const double* src = reinterpret_cast<const double*>(((unsigned long long)(unsigned)lo.w << 32) | (unsigned)lo.z);
       mbar_arrive_expect_tx(&c.full[sl], tot);
       bulk_g2s(ring + vs % cap, meta, mb, &c.full[sl]);
-      if (vb) bulk_g2s(ring + vs % cap + mb, src, vb, &c.full[sl]);
+      if (vb) bulk_vals(ring + vs % cap + mb, src, vb, &c.full[sl]);
       ++j;
     }
     if (prof) { unsigned long long* o = prof + 24 * blockIdx.x + 12 + 2 * ch; o[0] = clock64() - t0; o[1] = t_wait; }
@@ -440,9 +491,9 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       const int* o = porig + 9 * q;
       double* vb = box0 + b * boxd;
       mbar_arrive_expect_tx(&vfull[b], (uint32_t)bg.bytes);
-      tma_load_3d(vb + bg.boff[0], &tmg->r[0], o[0], o[1], o[2], &vfull[b]);
-      if (bg.ncomp > 1) tma_load_3d(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
-      if (bg.ncomp > 2) tma_load_3d(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
+      tma_load_box(vb + bg.boff[0], &tmg->r[0], o[0], o[1], o[2], &vfull[b]);
+      if (bg.ncomp > 1) tma_load_box(vb + bg.boff[1], &tmg->r[1], o[3], o[4], o[5], &vfull[b]);
+      if (bg.ncomp > 2) tma_load_box(vb + bg.boff[2], &tmg->r[2], o[6], o[7], o[8], &vfull[b]);
     };
     for (int i = 0; i < n && i < nbox; ++i) load_box(i);
     unsigned long long st_done = 0, st_col = 0, st0 = prof ? clock64() : 0;
@@ -460,9 +511,9 @@ __global__ void __launch_bounds__(NTHR, 1) patch_stream_kernel(const TMaps* __re
       if (prof) st_col += clock64() - ta;
       const int* o = porig + 9 * q;
       const double* vb = box0 + b * boxd;
-      tma_reduce_add_3d(&tmg->c[0], o[0], o[1], o[2], vb + bg.boff[0]);
-      if (bg.ncomp > 1) tma_reduce_add_3d(&tmg->c[1], o[3], o[4], o[5], vb + bg.boff[1]);
-      if (bg.ncomp > 2) tma_reduce_add_3d(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
+      tma_reduce_box(&tmg->c[0], o[0], o[1], o[2], vb + bg.boff[0]);
+      if (bg.ncomp > 1) tma_reduce_box(&tmg->c[1], o[3], o[4], o[5], vb + bg.boff[1]);
+      if (bg.ncomp > 2) tma_reduce_box(&tmg->c[2], o[6], o[7], o[8], vb + bg.boff[2]);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if (i + nbox < n) load_box(i + nbox);   // the buffer has been read: reload it
