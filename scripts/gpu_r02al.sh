@@ -1,0 +1,21 @@
+#!/bin/bash
+# round-2 pass AL (final state after SC post 2 DoFs / thread and the evict_first value stream):
+# full GPU suite, default bench, cfg3/cfg4 bench, reference arm, launch lists, ncu --set full of the top kernels, smoke
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest_rc=$?" >> gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log > gpurun_out/bench.json
+timeout 900 python bench.py --config 3 --secondary 4 --no-cpu-baseline > gpurun_out/bench34.log 2>&1; tail -1 gpurun_out/bench34.log > gpurun_out/bench34.json
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log > gpurun_out/bench_ref.json
+for c in 5 2 3 4; do
+  CMD="python bench.py --config $c --secondary 0 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg$c.csv $CMD > /dev/null 2>&1
+  python scripts/launch_summary.py gpurun_out/launches_cfg$c.csv > gpurun_out/launches_cfg$c.txt 2>&1
+done
+C5="python bench.py --config 5 --secondary 0 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+C2="python bench.py --config 2 --secondary 0 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:patch_stream -s 2 -c 1 -o gpurun_out/prof_patch_cfg5 $C5 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:apply_tri -s 2 -c 1 -o gpurun_out/prof_apply_tri_cfg5 $C5 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sc_cell|sc_post|tri_gather_sc|unpad" -s 4 -c 4 -o gpurun_out/prof_sc_cfg5 $C5 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:patch_stream -s 2 -c 1 -o gpurun_out/prof_patch_cfg2 $C2 > /dev/null 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke_rc=$?" >> gpurun_out/smoke.log
+echo done
