@@ -812,6 +812,75 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
   const uint32_t* si = reinterpret_cast<const uint32_t*>(pb + 16);
   const uint16_t* rows = reinterpret_cast<const uint16_t*>(si + nsl);
   const uint16_t* cols = rows + 32 * nsl;
+#ifndef RM_BATCH_NOPIPE
+  // the warp's (slice, step) pairs form ONE stream with a one-step look-ahead: the values and
+  // columns of the next step -- of this slice or of the warp's next one, whose header word was
+  // fetched a slice earlier -- are requested before the FMAs of the current step, so the L2
+  // latency of a step overlaps the arithmetic of the step before it instead of following it
+  // (same addends in the same order: bitwise the unpipelined sums)
+  int ls = (warp - h.a0 % BW + BW) % BW;
+  if (ls >= nsl) return;
+  uint32_t info = si[ls];
+  uint32_t info_n = ls + BW < nsl ? si[ls + BW] : 0u;
+  int rb = rows[ls * 32 + lane];
+  int kk = 0;
+  double w[U];
+  int c[U];
+  {
+    const int st = 32 * (int)(info & 0xFFFFu) + lane, cnt = (int)(info >> 16);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const bool on = j < cnt;
+      const int e = st + j * 32;
+      w[j] = on ? __ldg(val + e) : 0.0;
+      c[j] = on ? (int)cols[e] : 0;
+    }
+  }
+  double acc[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) acc[b] = 0.0;
+  for (;;) {
+    const int cnt = (int)(info >> 16);
+    const bool last = kk + U >= cnt;   // the slice's last step
+    const int ls2 = last ? ls + BW : ls, kk2 = last ? 0 : kk + U;
+    const uint32_t info2 = last ? info_n : info;
+    const bool more = ls2 < nsl;
+    double w2[U];
+    int c2[U];
+    {
+      const int st2 = 32 * (int)(info2 & 0xFFFFu) + lane, cnt2 = more ? (int)(info2 >> 16) : 0;
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const bool on = kk2 + j < cnt2;
+        const int e = st2 + (kk2 + j) * 32;
+        w2[j] = on ? __ldg(val + e) : 0.0;
+        c2[j] = on ? (int)cols[e] : 0;
+      }
+    }
+    int rb2 = rb;
+    uint32_t info_n2 = info_n;
+    if (last && more) {
+      rb2 = rows[ls2 * 32 + lane];
+      info_n2 = ls2 + BW < nsl ? si[ls2 + BW] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[b] = fma(w[j], X[b * boxd + c[j]], acc[b]);
+    if (last) {
+      if ((h.a0 + ls) * 32 + lane < nrows) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) X[b * boxd + rb] -= acc[b];
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[b] = 0.0;
+    }
+    if (!more) break;
+    ls = ls2; kk = kk2; info = info2; info_n = info_n2; rb = rb2;
+#pragma unroll
+    for (int j = 0; j < U; ++j) { w[j] = w2[j]; c[j] = c2[j]; }
+  }
+#else   // the unpipelined loop (tuning reference: -DRM_BATCH_NOPIPE)
   for (int ls = (warp - h.a0 % BW + BW) % BW; ls < nsl; ls += BW) {
     const uint32_t info = si[ls];
     const int st = 32 * (int)(info & 0xFFFFu) + lane, cnt = (int)(info >> 16);
@@ -839,6 +908,7 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
       for (int b = 0; b < B; ++b) X[b * boxd + rb] -= acc[b];
     }
   }
+#endif
 }
 
 template <int B, int BT>
