@@ -806,22 +806,98 @@ struct BatchArgs {
 template <int B, int BW>
 __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const double* __restrict__ val, int nrows,
                                              int warp, int lane, double* __restrict__ X, int boxd) {
-  constexpr int U = 4;   // entries per lane and step (measured at cfg4: U = 2 10.2 ms, 4 9.35 ms, 8 9.82 ms, 16 10.4 ms)
+#ifndef RM_BATCH_U
+#define RM_BATCH_U 4
+#endif
+  constexpr int U = RM_BATCH_U;   // entries per lane and step (measured at cfg4: U = 2 10.2 ms, 4 9.35 ms, 8 9.82 ms, 16 10.4 ms)
   const Hdr h = hdr(pb);
   const int nsl = h.a1 - h.a0;
   const uint32_t* si = reinterpret_cast<const uint32_t*>(pb + 16);
   const uint16_t* rows = reinterpret_cast<const uint16_t*>(si + nsl);
   const uint16_t* cols = rows + 32 * nsl;
-#ifndef RM_BATCH_NOPIPE
+#ifndef RM_BATCH_SLICES
+#define RM_BATCH_SLICES 1   // slices a warp works on at once when B <= 2 (B = 4: 2; 1: the look-ahead loop).
+                            // Measured (pass AP, cfg4): 1: 8.82 ms, 2: 10.0 ms, 4: 12.5 ms -- the look-ahead wins
+#endif
+#if RM_BATCH_SLICES > 1 && !defined(RM_BATCH_NOPIPE)
+  // ncu (pass AO, cfg4 NCE8 edge-star potential family): a level has ~3.5 slices per warp of
+  // ~1.4 steps each, every step one L2 round trip (header word -> values / columns), and the
+  // FMAs of a step are far shorter than the trip -- long-scoreboard stalls dominate.  The warp
+  // therefore takes S slices at once: S header words in one trip, the first steps of all S in
+  // the next, further steps (the longest slice counts) again S at a time.  Each row still sums
+  // its entries in order: bitwise the one-slice sums.
+  constexpr int S = B <= 2 ? RM_BATCH_SLICES : (B <= 4 ? (RM_BATCH_SLICES > 2 ? 2 : RM_BATCH_SLICES) : 1);
+  for (int l0 = (warp - h.a0 % BW + BW) % BW; l0 < nsl; l0 += S * BW) {
+    int st[S], cnt[S], rb[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const int ls = l0 + q * BW;
+      const uint32_t info = ls < nsl ? si[ls] : 0u;
+      st[q] = 32 * (int)(info & 0xFFFFu) + lane;
+      cnt[q] = (int)(info >> 16);
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const int ls = l0 + q * BW;
+      rb[q] = ls < nsl && (h.a0 + ls) * 32 + lane < nrows ? (int)rows[ls * 32 + lane] : -1;
+    }
+    double acc[S][B];
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[q][b] = 0.0;
+    int cmax = 0;
+#pragma unroll
+    for (int q = 0; q < S; ++q) cmax = max(cmax, cnt[q]);
+    for (int kk = 0; kk < cmax; kk += U) {
+      double w[S][U];
+      int c[S][U];
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const bool on = kk + j < cnt[q];
+          const int e = st[q] + (kk + j) * 32;
+          w[q][j] = on ? __ldg(val + e) : 0.0;
+          c[q][j] = on ? (int)cols[e] : 0;
+        }
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        if (kk < cnt[q]) {
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+#pragma unroll
+            for (int b = 0; b < B; ++b) acc[q][b] = fma(w[q][j], X[b * boxd + c[q][j]], acc[q][b]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (rb[q] >= 0) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) X[b * boxd + rb[q]] -= acc[q][b];
+      }
+  }
+#elif !defined(RM_BATCH_NOPIPE)
   // the warp's (slice, step) pairs form ONE stream with a one-step look-ahead: the values and
   // columns of the next step -- of this slice or of the warp's next one, whose header word was
   // fetched a slice earlier -- are requested before the FMAs of the current step, so the L2
   // latency of a step overlaps the arithmetic of the step before it instead of following it
   // (same addends in the same order: bitwise the unpipelined sums)
+#ifdef RM_BATCH_SERP
+  // serpentine slice -> warp map (round r of BW slices: warp i takes slice i in even rounds,
+  // BW - 1 - i in odd ones): the slices of a sorted sliced-ELL piece shorten with their index,
+  // and plain round-robin gives warp 0 the longest slice of every round
+  auto at = [&](int r) { return r * BW + ((r & 1) ? BW - 1 - warp : warp) - h.a0; };
+  auto nxt = [&](int l) { return at((h.a0 + l) / BW + 1); };
+  int ls = at(h.a0 / BW);
+  if (ls < 0) ls = at(h.a0 / BW + 1);
+#else
+  auto nxt = [&](int l) { return l + BW; };
   int ls = (warp - h.a0 % BW + BW) % BW;
+#endif
   if (ls >= nsl) return;
   uint32_t info = si[ls];
-  uint32_t info_n = ls + BW < nsl ? si[ls + BW] : 0u;
+  uint32_t info_n = nxt(ls) < nsl ? si[nxt(ls)] : 0u;
   int rb = rows[ls * 32 + lane];
   int kk = 0;
   double w[U];
@@ -842,7 +918,7 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
   for (;;) {
     const int cnt = (int)(info >> 16);
     const bool last = kk + U >= cnt;   // the slice's last step
-    const int ls2 = last ? ls + BW : ls, kk2 = last ? 0 : kk + U;
+    const int ls2 = last ? nxt(ls) : ls, kk2 = last ? 0 : kk + U;
     const uint32_t info2 = last ? info_n : info;
     const bool more = ls2 < nsl;
     double w2[U];
@@ -861,7 +937,7 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
     uint32_t info_n2 = info_n;
     if (last && more) {
       rb2 = rows[ls2 * 32 + lane];
-      info_n2 = ls2 + BW < nsl ? si[ls2 + BW] : 0u;
+      info_n2 = nxt(ls2) < nsl ? si[nxt(ls2)] : 0u;
     }
 #pragma unroll
     for (int j = 0; j < U; ++j)
@@ -958,34 +1034,62 @@ __global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(const __grid_
       const uint16_t* mem = reinterpret_cast<const uint16_t*>(mc + 16);
       const double* pv = vblk + pt.y;
       const int cnt = h.a1 - h.a0;
-      for (int t = tid; t < cnt * B; t += BT) {
-        const int li = t / B, b = t - li * B;
-        double* Xb = X + b * boxd;
-        const int m0 = mem[li];
-        if (bs == 1) {
-          const double d = __ldg(pv + li);
-          Xb[m0] *= d * d;
-          continue;
+      // PU iterations at a time, every index and factor load of all PU issued before the first
+      // dependent shared-memory access (pass AO: ~3 iterations per thread and level, each one
+      // L2 round trip when taken one after the other)
+      constexpr int PU = 3;
+      for (int t0 = tid; t0 < cnt * B; t0 += PU * BT) {
+        int m0[PU], m1[PU], m2[PU];
+        double f0[PU], f1[PU], f2[PU], f3[PU], f4[PU], f5[PU];
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          const int t = t0 + u * BT;
+          const bool on = t < cnt * B;
+          const int li = on ? t / B : 0;
+          m0[u] = on ? (int)mem[li] : -1;
+          f0[u] = __ldg(pv + li);
+          m1[u] = m2[u] = 0xFFFF;
+          f1[u] = f2[u] = f3[u] = f4[u] = f5[u] = 0.0;
+          if (bs > 1) {
+            m1[u] = mem[cnt + li];
+            f1[u] = __ldg(pv + cnt + li);
+            f2[u] = __ldg(pv + 2 * cnt + li);
+            if (bs > 2) {
+              m2[u] = mem[2 * cnt + li];
+              f3[u] = __ldg(pv + 3 * cnt + li);
+              f4[u] = __ldg(pv + 4 * cnt + li);
+              f5[u] = __ldg(pv + 5 * cnt + li);
+            }
+          }
         }
-        const int m1 = mem[cnt + li];
-        const int m2 = (bs > 2) ? mem[2 * cnt + li] : 0xFFFF;
-        const double l00 = __ldg(pv + li), l10 = __ldg(pv + cnt + li), l11 = __ldg(pv + 2 * cnt + li);
-        double y0 = Xb[m0] * l00, y1 = 0.0, y2 = 0.0;
-        if (m1 != 0xFFFF) y1 = (Xb[m1] - l10 * y0) * l11;
-        if (m2 != 0xFFFF) {
-          const double l20 = __ldg(pv + 3 * cnt + li), l21 = __ldg(pv + 4 * cnt + li), l22 = __ldg(pv + 5 * cnt + li);
-          y2 = (Xb[m2] - l20 * y0 - l21 * y1) * l22;
-          y2 *= l22;
-          Xb[m2] = y2;
-          if (m1 != 0xFFFF) y1 -= l21 * y2;
-          y0 -= l20 * y2;
+#pragma unroll
+        for (int u = 0; u < PU; ++u) {
+          if (m0[u] < 0) continue;
+          const int t = t0 + u * BT;
+          double* Xb = X + (t % B) * boxd;
+          if (bs == 1) {
+            const double d = f0[u];
+            Xb[m0[u]] *= d * d;
+            continue;
+          }
+          const double l00 = f0[u], l10 = f1[u], l11 = f2[u];
+          double y0 = Xb[m0[u]] * l00, y1 = 0.0, y2 = 0.0;
+          if (m1[u] != 0xFFFF) y1 = (Xb[m1[u]] - l10 * y0) * l11;
+          if (m2[u] != 0xFFFF) {
+            const double l20 = f3[u], l21 = f4[u], l22 = f5[u];
+            y2 = (Xb[m2[u]] - l20 * y0 - l21 * y1) * l22;
+            y2 *= l22;
+            Xb[m2[u]] = y2;
+            if (m1[u] != 0xFFFF) y1 -= l21 * y2;
+            y0 -= l20 * y2;
+          }
+          if (m1[u] != 0xFFFF) {
+            y1 *= l11;
+            Xb[m1[u]] = y1;
+            y0 -= l10 * y1;
+          }
+          Xb[m0[u]] = y0 * l00;
         }
-        if (m1 != 0xFFFF) {
-          y1 *= l11;
-          Xb[m1] = y1;
-          y0 -= l10 * y1;
-        }
-        Xb[m0] = y0 * l00;
       }
     }
     __syncthreads();
@@ -1065,9 +1169,17 @@ __global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(const __grid_
     const Hdr h = hdr(mc);
     const uint16_t* zl = reinterpret_cast<const uint16_t*>(mc + 16);
     const int cnt = h.a1 - h.a0;
-    for (int t = tid; t < cnt * B; t += BT) {
-      const int k = t / B, b = t - k * B;
-      X[b * boxd + zl[k]] = 0.0;
+    constexpr int ZU = 4;   // index loads in flight per thread
+    for (int t0 = tid; t0 < cnt * B; t0 += ZU * BT) {
+      int z[ZU];
+#pragma unroll
+      for (int u = 0; u < ZU; ++u) {
+        const int t = t0 + u * BT;
+        z[u] = t < cnt * B ? (t % B) * boxd + (int)zl[t / B] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < ZU; ++u)
+        if (z[u] >= 0) X[z[u]] = 0.0;
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> TMA reads
