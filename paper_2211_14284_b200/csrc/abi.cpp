@@ -199,7 +199,11 @@ void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>
     for (int b : {8, 4, 2}) {
       const size_t sm = rm::patch_batch_smem(P.box_total, mr_max, b, nt);
       if (sm == 0) continue;
+#ifdef RM_BATCH_512X2   // tuning build: the 512-thread kernels are capped at 64 registers (two CTAs per SM)
+      const int ctas = (2 * (sm + 2048) <= 233472) ? 2 : 1;
+#else
       const int ctas = (nt == 256 && 2 * (sm + 2048) <= 233472) ? 2 : 1;
+#endif
       const long score = (long)(ctas * nt / 32) * 10000 + (long)(b * ctas) * 10 + ctas;
       if (score > best) { best = score; B = b; NT = nt; smem = sm; }
     }

@@ -988,7 +988,12 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
 }
 
 template <int B, int BT>
-__global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(const __grid_constant__ BatchArgs a, int batch0) {
+#ifdef RM_BATCH_512X2   // tuning: two 512-thread CTAs per SM (32 warps, 64 registers per thread)
+__global__ void __launch_bounds__(BT, 2) patch_batch_kernel(
+#else
+__global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(
+#endif
+    const __grid_constant__ BatchArgs a, int batch0) {
   constexpr int BW = BT / 32;
   extern __shared__ __align__(128) double smb[];
   __shared__ int sq[B];
