@@ -987,11 +987,13 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
 #endif
 }
 
-template <int B, int BT>
+// MINB: resident CTAs per SM the register allocation allows (512 threads: 1; 256 threads: 2, or 3
+// for the families whose working set leaves room for a third CTA -- 24 warps per SM at <= 85 registers)
+template <int B, int BT, int MINB>
 #ifdef RM_BATCH_512X2   // tuning: two 512-thread CTAs per SM (32 warps, 64 registers per thread)
-__global__ void __launch_bounds__(BT, 2) patch_batch_kernel(
+__global__ void __launch_bounds__(BT, MINB < 2 ? 2 : MINB) patch_batch_kernel(
 #else
-__global__ void __launch_bounds__(BT, 512 / BT) patch_batch_kernel(
+__global__ void __launch_bounds__(BT, MINB) patch_batch_kernel(
 #endif
     const __grid_constant__ BatchArgs a, int batch0) {
   constexpr int BW = BT / 32;
@@ -1508,7 +1510,16 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
   return cudaSuccess;
 }
 
-#define RM_BATCH_CFGS(X) X(8, 512) X(4, 512) X(2, 512) X(8, 256) X(4, 256) X(2, 256)
+#ifndef RM_BATCH_CTA3
+#define RM_BATCH_CTA3 1   // 1: a third 256-thread CTA per SM where shared memory allows (0: tuning reference)
+#endif
+#define RM_BATCH_CFGS(X) X(8, 512, 1) X(4, 512, 1) X(2, 512, 1) X(8, 256, 2) X(4, 256, 2) X(2, 256, 2) X(4, 256, 3) X(2, 256, 3)
+
+// resident 256-thread CTAs per SM by shared memory (the chooser in abi.cpp counts two the same way)
+static int batch_minb(int B, int NT, size_t smem) {
+  if (NT != 256) return 1;
+  return RM_BATCH_CTA3 && B <= 4 && 3 * (smem + 2048) <= 233472 ? 3 : 2;   // B = 8 needs > 85 registers
+}
 
 size_t patch_batch_smem(int box_total, int mr_max, int B, int NT) {
   const size_t s = batch_smem_t(B, NT, box_total, mr_max);
@@ -1519,8 +1530,9 @@ size_t patch_batch_smem(int box_total, int mr_max, int B, int NT) {
   // the attribute is per instantiation, shared by every family: always the full opt-in size
   const int lim = optin - 1024;
   cudaError_t e = cudaErrorInvalidValue;
-#define RM_SET(BB, NN) \
-  if (B == BB && NT == NN) e = cudaFuncSetAttribute(patch_batch_kernel<BB, NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+#define RM_SET(BB, NN, MM) \
+  if (B == BB && NT == NN && (e == cudaSuccess || e == cudaErrorInvalidValue)) \
+    e = cudaFuncSetAttribute(patch_batch_kernel<BB, NN, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   RM_BATCH_CFGS(RM_SET)
 #undef RM_SET
   return e == cudaSuccess ? s : 0;
@@ -1544,13 +1556,19 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
     a.boff[sb] = L.boff[sb];
     if (sb < L.nsub) a.box_bytes += 8u * (unsigned)(L.box[sb][0] * L.box[sb][1] * L.box[sb][2]);
   }
+  const int minb = batch_minb(L.batch, L.batch_nt, L.bsmem);
   for (int c = 0; c < L.cs.ncolors; ++c) {
     const int nb = L.bstart[c + 1] - L.bstart[c];
     if (nb <= 0) continue;
-#define RM_LAUNCH(BB, NN) \
-    if (L.batch == BB && L.batch_nt == NN) patch_batch_kernel<BB, NN><<<nb, NN, L.bsmem, st>>>(a, L.bstart[c]);
+    bool launched = false;
+#define RM_LAUNCH(BB, NN, MM) \
+    if (L.batch == BB && L.batch_nt == NN && minb == MM) { \
+      patch_batch_kernel<BB, NN, MM><<<nb, NN, L.bsmem, st>>>(a, L.bstart[c]); \
+      launched = true; \
+    }
     RM_BATCH_CFGS(RM_LAUNCH)
 #undef RM_LAUNCH
+    if (!launched) return cudaErrorInvalidConfiguration;   // no instantiation for (B, threads, CTAs per SM)
   }
   return cudaGetLastError();
 }
