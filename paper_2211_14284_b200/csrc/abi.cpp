@@ -195,14 +195,29 @@ void plan_batches(DevFamily& F, const rm::PatchFamily& P, const std::vector<int>
   int B = 0, NT = 0;
   size_t smem = 0;
   long best = -1;
-  for (int nt : {256, 512})
+  for (int nt : {256, 384, 512})
     for (int b : {8, 4, 2}) {
+      if (nt == 384 && b == 8) continue;   // no instantiation (B = 8 needs > 85 registers)
+#ifndef RM_BATCH_384
+      if (nt == 384) continue;
+#endif
       const size_t sm = rm::patch_batch_smem(P.box_total, mr_max, b, nt);
       if (sm == 0) continue;
 #ifdef RM_BATCH_512X2   // tuning build: the 512-thread kernels are capped at 64 registers (two CTAs per SM)
       const int ctas = (2 * (sm + 2048) <= 233472) ? 2 : 1;
 #else
-      const int ctas = (nt == 256 && 2 * (sm + 2048) <= 233472) ? 2 : 1;
+      // resident CTAs per SM (patch_solve.cu batch_minb): 256 threads: 3 (B <= 4) or 2 by shared
+      // memory; 384 threads: 2 (24 warps where three 256-thread CTAs do not fit); 512: 1
+      int ctas = 1;
+#ifdef RM_BATCH_384
+      if (nt == 256) ctas = (b <= 4 && 3 * (sm + 2048) <= 233472) ? 3 : (2 * (sm + 2048) <= 233472 ? 2 : 1);
+#else
+      if (nt == 256) ctas = 2 * (sm + 2048) <= 233472 ? 2 : 1;   // (a third CTA, where it fits, does not change the choice)
+#endif
+      if (nt == 384) {
+        if (2 * (sm + 2048) > 233472) continue;
+        ctas = 2;
+      }
 #endif
       const long score = (long)(ctas * nt / 32) * 10000 + (long)(b * ctas) * 10 + ctas;
       if (score > best) { best = score; B = b; NT = nt; smem = sm; }

@@ -1513,10 +1513,12 @@ cudaError_t plan_patch_solve(PatchLaunch& L) {
 #ifndef RM_BATCH_CTA3
 #define RM_BATCH_CTA3 1   // 1: a third 256-thread CTA per SM where shared memory allows (0: tuning reference)
 #endif
-#define RM_BATCH_CFGS(X) X(8, 512, 1) X(4, 512, 1) X(2, 512, 1) X(8, 256, 2) X(4, 256, 2) X(2, 256, 2) X(4, 256, 3) X(2, 256, 3)
+#define RM_BATCH_CFGS(X) \
+  X(8, 512, 1) X(4, 512, 1) X(2, 512, 1) X(8, 256, 2) X(4, 256, 2) X(2, 256, 2) X(4, 256, 3) X(2, 256, 3) X(4, 384, 2) X(2, 384, 2)
 
 // resident 256-thread CTAs per SM by shared memory (the chooser in abi.cpp counts two the same way)
 static int batch_minb(int B, int NT, size_t smem) {
+  if (NT == 384) return 2;   // two 384-thread CTAs: 24 warps where three 256-thread CTAs do not fit
   if (NT != 256) return 1;
   return RM_BATCH_CTA3 && B <= 4 && 3 * (smem + 2048) <= 233472 ? 3 : 2;   // B = 8 needs > 85 registers
 }
