@@ -987,6 +987,9 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
 #endif
 }
 
+#ifndef RM_BATCH_PDL
+#define RM_BATCH_PDL 1   // colours c >= 1 of a family as programmatic dependent launches (0: plain stream order)
+#endif
 // MINB: resident CTAs per SM the register allocation allows (512 threads: 1; 256 threads: 2, or 3
 // for the families whose working set leaves room for a third CTA -- 24 warps per SM at <= 85 registers)
 template <int B, int BT, int MINB>
@@ -1004,6 +1007,11 @@ __global__ void __launch_bounds__(BT, MINB) patch_batch_kernel(
   const int bt = batch0 + (int)blockIdx.x;
   const int boxd = a.boxd;
   double* X = smb;   // box of slot b at X + b * boxd (the TMA box layout)
+#if RM_BATCH_PDL
+  // let the next colour's CTAs take the SM slots this launch's last wave leaves idle (they block
+  // at their reduce-add until this grid is complete)
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   if (tid < B) sq[tid] = a.bpatch[(long long)bt * B + tid];
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -1195,6 +1203,12 @@ __global__ void __launch_bounds__(BT, MINB) patch_batch_kernel(
   // colour the patches are disjoint and the entries outside a patch are zero, so every c entry
   // receives at most one nonzero addend per launch: deterministic)
   if (tid == 0) {
+#if RM_BATCH_PDL
+    // the previous colour's launch (programmatic dependent launch, launch_batched) must be complete
+    // and its reduce-adds visible before this colour adds into c: same order of addends as with
+    // plain stream order.  Everything above reads only r and the class data, final before colour 0
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
     for (int b = 0; b < B; ++b) {
       if (sq[b] < 0) continue;
       const int* o = a.porig + 9LL * sq[b];
@@ -1559,18 +1573,33 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
     if (sb < L.nsub) a.box_bytes += 8u * (unsigned)(L.box[sb][0] * L.box[sb][1] * L.box[sb][2]);
   }
   const int minb = batch_minb(L.batch, L.batch_nt, L.bsmem);
+  // colour 0 in plain stream order (r and c of the kernels before it complete and visible); colours
+  // c >= 1 as programmatic dependent launches: their CTAs start while the previous colour's last
+  // wave runs and wait (griddepcontrol.wait) before their reduce-adds
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.dynamicSmemBytes = L.bsmem;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  bool chained = false;
   for (int c = 0; c < L.cs.ncolors; ++c) {
     const int nb = L.bstart[c + 1] - L.bstart[c];
     if (nb <= 0) continue;
     bool launched = false;
 #define RM_LAUNCH(BB, NN, MM) \
     if (L.batch == BB && L.batch_nt == NN && minb == MM) { \
-      patch_batch_kernel<BB, NN, MM><<<nb, NN, L.bsmem, st>>>(a, L.bstart[c]); \
+      cfg.gridDim = dim3(nb); cfg.blockDim = dim3(NN); \
+      cfg.numAttrs = (RM_BATCH_PDL && chained) ? 1 : 0; \
+      const cudaError_t le = cudaLaunchKernelEx(&cfg, patch_batch_kernel<BB, NN, MM>, a, L.bstart[c]); \
+      if (le != cudaSuccess) return le; \
       launched = true; \
     }
     RM_BATCH_CFGS(RM_LAUNCH)
 #undef RM_LAUNCH
     if (!launched) return cudaErrorInvalidConfiguration;   // no instantiation for (B, threads, CTAs per SM)
+    chained = true;
   }
   return cudaGetLastError();
 }
