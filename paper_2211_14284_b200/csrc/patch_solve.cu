@@ -987,6 +987,10 @@ __device__ __forceinline__ void batch_sliced(const unsigned char* pb, const doub
 #endif
 }
 
+#ifndef RM_BATCH_CHAINF
+#define RM_BATCH_CHAINF 0   // 1: the colour chain continues across the orientation families of a space (measured without
+                            // timing events, pass BA: cfg3 3.066 vs 3.033 ms, cfg4 8.364 vs 8.395 ms -- no gain, left off)
+#endif
 #ifndef RM_BATCH_PDL
 #define RM_BATCH_PDL 1   // colours c >= 1 of a family as programmatic dependent launches (0: plain stream order)
 #endif
@@ -1556,7 +1560,7 @@ size_t patch_batch_smem(int box_total, int mr_max, int B, int NT) {
 
 namespace {
 
-cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
+cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st, bool chain_first) {
   BatchArgs a{};
   a.classes = L.classes; a.vals = L.vals; a.fin = L.fin;
   a.bpatch = L.bpatch; a.bclass = L.bclass; a.bblock = L.bblock; a.bfin = L.bfin;
@@ -1583,7 +1587,9 @@ cudaError_t launch_batched(const PatchLaunch& L, cudaStream_t st) {
   cfg.dynamicSmemBytes = L.bsmem;
   cfg.stream = st;
   cfg.attrs = pdl;
-  bool chained = false;
+  // chain_first: this family follows another batched family of the same padded r / c pair with
+  // nothing but timing events in between (orientation families): its colour 0 joins that chain
+  bool chained = chain_first;
   for (int c = 0; c < L.cs.ncolors; ++c) {
     const int nb = L.bstart[c + 1] - L.bstart[c];
     if (nb <= 0) continue;
@@ -1680,7 +1686,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
     }
   }
   if (zero_c && (e = cudaMemsetAsync(L.cpad, 0, (size_t)L.npad * sizeof(double), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+  if (!L.batch && (e = cudaMemsetAsync(L.done, 0, sizeof(unsigned), st)) != cudaSuccess) return e;   // the stream kernel's colour counter
   BoxGeom bg;
   bg.ncomp = L.nsub;
   bg.bytes = 0;
@@ -1691,7 +1697,7 @@ cudaError_t launch_patch_solve(const PatchLaunch& L, const double* r, double* u,
   }
   if (kt) kt->begin(kt->arg);
   if (L.batch) {
-    e = launch_batched(L, st);
+    e = launch_batched(L, st, RM_BATCH_CHAINF && r_padded && !zero_c);
   } else
   // cooperative launch: the colour wait of the store warps spins on a counter advanced by other
   // CTAs, so every CTA of the grid must be resident at once -- the runtime guarantees that (or
